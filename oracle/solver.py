@@ -1,0 +1,228 @@
+"""Oracle time step (test infrastructure only — see oracle/__init__.py).
+
+One backward-Euler step as the argmin of the barrier-augmented incremental potential with AL
+kinematic constraints (P:L89-97 Eq. IP, P:L127-131 Eq. unified_ipc_variational
+Eq. unified_ipc_AL, P:L370 velocity update).  The paper gives no minimiser; the machinery follows
+SURVEY §8(c)-14..17 (readings R14-R17 in DESIGN.md):
+
+  x̃ = xⁿ + Δt ẋⁿ;  λ = 0, ρ = ρ₀;  q = qⁿ (feasible start)
+  repeat AL rounds:
+    repeat Newton:
+      𝒜 = active set at q;  g, H = assemble (PSD-projected);  p = −H⁻¹g (exact sparse solve)
+      if ‖p‖_emb,∞ ≤ τ_N·L_env: inner converged
+      C′ = swept candidates over [q, q+p];  α = min(1, ACCD over C′)
+      halve α until no det F ≤ 0 and E(q+αp) ≤ E(q) + c·α·gᵀp  (α < 1e-10 → NEWTON_STALL)
+      q ← q + αp
+    r = max constraint residual on embedded vertices;  r ≤ τ_AL·L_env → done
+    if r > ½ r_prev: ρ ← 2ρ;   λ ← λ − ρ·(S q − s)
+  ẋⁿ⁺¹ = (xⁿ⁺¹ − xⁿ)/Δt,  ẏⁿ⁺¹ = (yⁿ⁺¹ − yⁿ)/Δt
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from . import contact as C
+from . import energy as En
+from .mesh import Model, all_positions, embed, env_scale
+
+ENV_OK, NEWTON_STALL, AL_INFEASIBLE, CAPACITY, NONFINITE, BAD_STATE, DISABLED = range(7)
+
+
+@dataclasses.dataclass
+class State:
+    x: np.ndarray     # (V,3)
+    v: np.ndarray     # (V,3)
+    y: np.ndarray     # (NA,12)
+    ydot: np.ndarray  # (NA,12)
+
+
+@dataclasses.dataclass
+class StepStats:
+    status: int = ENV_OK
+    newton_iters: int = 0
+    ls_backtracks: int = 0
+    al_rounds: int = 0
+    pcg_iters: int = 0
+    alpha_min: float = 1.0
+    n_active: int = 0
+    energy: float = 0.0
+    constraint_residual: float = 0.0
+    min_dist: float = np.inf
+
+
+def embedded_inf_norm(model: Model, p, y_like=None):
+    """‖p‖_emb,∞: max |p_i| over soft DoFs and max component of J_v p_b over the vertices of every
+    non-static affine body (reading R14)."""
+    V = model.V
+    m = float(np.abs(p[:3 * V]).max()) if V else 0.0
+    for bi, xb in enumerate(model.body_xbar):
+        s = model.dof_slot[bi]
+        if s < 0:
+            continue
+        pb = p[3 * V + 12 * s:3 * V + 12 * s + 12]
+        m = max(m, float(np.abs(embed(pb, xb)).max()))
+    return m
+
+
+def constraint_residual(model: Model, ctx: En.Context, x, y):
+    """max over ∂⁻G vertices of ‖x_v − s_v‖ and over kinematic bodies' vertices of
+    ‖(t−t_s) + (A−A_s) x̄_v‖ (reading R13)."""
+    r = 0.0
+    if len(model.att_vert):
+        r = float(np.sqrt(((x[model.att_vert] - ctx.s_att) ** 2).sum(1)).max())
+    for k, b in enumerate(model.kin_bodies):
+        d = y[b] - ctx.s_kin[k]
+        r = max(r, float(np.sqrt((embed(d, model.body_xbar[b]) ** 2).sum(1)).max()))
+    return r
+
+
+def any_inverted(model: Model, x):
+    if len(model.tets) == 0:
+        return False
+    X = x[model.tets]
+    Ds = np.stack([X[:, 1] - X[:, 0], X[:, 2] - X[:, 0], X[:, 3] - X[:, 0]], 2)
+    F = Ds @ model.Dm_inv
+    return bool((np.linalg.det(F) <= 0).any())
+
+
+def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
+    """Block-Jacobi PCG for H p = −g from p₀ = 0 (3×3 per soft vertex, 12×12 per body); stop
+    at rᵀz ≤ η² r₀ᵀz₀ or max_iter (reading R15; P:L325 names PCG)."""
+    n = len(g)
+    V = model.V
+    blocks = [(3 * v, 3) for v in range(V)] + [(3 * V + 12 * s, 12) for s in range(model.n_dof_bodies)]
+    Hd = H.toarray() if n <= 4000 else None
+    inv = []
+    for o, k in blocks:
+        B = Hd[o:o + k, o:o + k] if Hd is not None else H[o:o + k, o:o + k].toarray()
+        inv.append(np.linalg.inv(B))
+
+    def prec(r):
+        z = np.zeros_like(r)
+        for (o, k), Bi in zip(blocks, inv):
+            z[o:o + k] = Bi @ r[o:o + k]
+        return z
+
+    p = np.zeros(n)
+    r = -g.copy()
+    z = prec(r)
+    d = z.copy()
+    rz = r @ z
+    rz0 = rz
+    it = 0
+    while it < max_iter and rz > eta * eta * rz0:
+        q = H @ d
+        a = rz / (d @ q)
+        p += a * d
+        r -= a * q
+        z = prec(r)
+        rz_new = r @ z
+        d = z + (rz_new / rz) * d
+        rz = rz_new
+        it += 1
+    return p, it
+
+
+def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, trace=None):
+    """Advance one env by one time step; returns (new State, StepStats)."""
+    cfg = model.scene.config
+    dt = cfg.dt
+    stats = StepStats()
+    L = env_scale(model, st.x, st.y) if L_env is None else L_env
+    ctx = En.make_context(model, st.x, st.v, st.y, st.ydot, y_kin_target, dt)
+    x, y = st.x.copy(), st.y.copy()
+    r_prev = np.inf
+    done = False
+    for al_round in range(cfg.max_al_rounds):
+        stats.al_rounds = al_round + 1
+        converged = False
+        while stats.newton_iters < cfg.max_newton:
+            P = all_positions(model, x, y)
+            pairs = C.active_pairs(model, P)
+            g, H = En.assemble(model, ctx, x, y, pairs)
+            if solver == "direct":
+                p = spla.spsolve(sp.csc_matrix(H), -g)
+            else:
+                p, it = block_jacobi_pcg(model, H, g, cfg.pcg_eta, cfg.max_pcg)
+                stats.pcg_iters += it
+            stats.newton_iters += 1
+            if not np.all(np.isfinite(p)):
+                stats.status = NONFINITE
+                break
+            if embedded_inf_norm(model, p) <= cfg.newton_tol_rel * L:
+                converged = True
+                break
+            dx, dy = En.unpack(model, p, np.zeros_like(y))
+            Pd = _disp_positions(model, dx, dy)
+            cand = C.candidate_pairs(model, P, P + Pd)
+            alpha = C.accd_bound(model, P, Pd, cand)
+            E0 = En.total_energy(model, ctx, x, y, pairs)
+            gp = float(g @ p)
+            while True:
+                xt, yt = x + alpha * dx, y + alpha * dy
+                ok = not any_inverted(model, xt)
+                if ok:
+                    Pt = all_positions(model, xt, yt)
+                    E1 = En.total_energy(model, ctx, xt, yt, C.active_pairs(model, Pt, cand))
+                    if E1 <= E0 + cfg.armijo_c * alpha * gp:
+                        break
+                alpha *= 0.5
+                stats.ls_backtracks += 1
+                if alpha < 1e-10:
+                    break
+            if alpha < 1e-10:
+                stats.status = NEWTON_STALL
+                break
+            stats.alpha_min = min(stats.alpha_min, alpha)
+            if trace is not None:
+                trace.append(dict(alpha=alpha, E0=E0, E1=E1, p_inf=embedded_inf_norm(model, p)))
+            x, y = xt, yt
+        if stats.status != ENV_OK:
+            break
+        if not converged:
+            stats.status = NEWTON_STALL
+            break
+        res = constraint_residual(model, ctx, x, y)
+        stats.constraint_residual = res
+        if trace is not None:
+            trace.append(dict(al_round=al_round, residual=res, rho=ctx.rho, newton=stats.newton_iters))
+        if res <= cfg.al_tol_rel * L:
+            done = True
+            break
+        if res > 0.5 * r_prev:
+            ctx.rho *= 2.0
+        r_prev = res
+        if len(model.att_vert):
+            ctx.lam_att = ctx.lam_att - ctx.rho * (x[model.att_vert] - ctx.s_att)
+        for k, b in enumerate(model.kin_bodies):
+            ctx.lam_kin[k] = ctx.lam_kin[k] - ctx.rho * (y[b] - ctx.s_kin[k])
+    if stats.status == ENV_OK and not done:
+        stats.status = AL_INFEASIBLE
+    if stats.status != ENV_OK:
+        return dataclasses.replace(st), stats          # rollback to xⁿ
+    P = all_positions(model, x, y)
+    pairs = C.active_pairs(model, P)
+    stats.n_active = len(pairs)
+    stats.energy = En.total_energy(model, ctx, x, y, pairs)
+    new = State(x=x, v=(x - st.x) / dt, y=y, ydot=(y - st.y) / dt)
+    for bi in range(len(model.body_xbar)):
+        if model.dof_slot[bi] < 0:
+            new.ydot[bi] = 0.0
+            new.y[bi] = st.y[bi]
+    return new, stats
+
+
+def _disp_positions(model: Model, dx, dy):
+    """Vertex displacements of a DoF step: soft dx, affine J_v p_b (static bodies 0)."""
+    Pd = np.zeros((model.NVall, 3))
+    Pd[:model.V] = dx
+    o = model.V
+    for bi, xb in enumerate(model.body_xbar):
+        if model.dof_slot[bi] >= 0:
+            Pd[o:o + len(xb)] = embed(dy[bi], xb)
+        o += len(xb)
+    return Pd

@@ -1,0 +1,417 @@
+"""Seeded synthetic scene generator (shared INPUT module — holds none of the method's arithmetic).
+
+This module only builds geometry and per-env scripted inputs: tet lattices, watertight box-union
+surfaces, rest poses, initial states and kinematic targets.  It is imported by both the oracle
+(``oracle/``) and the CUDA path's harness; it never computes energies, derivatives, masses,
+distances, surfaces-for-contact or any other step of the method.  Mesh preparation (volumes,
+D_m^-1, lumped masses, surface extraction, areas, reduced mass) is done independently by each side.
+
+Workloads follow SURVEY.md §8(d) (the configs of BASELINE.json):
+  C1   1 env: ~500-tet gel pad pressed 1 mm by one kinematic ABD cube, 10 steps at dt=1e-2
+  C1b  free ABD cube dropped on the pad (variant used for parity)
+  C1c  soft cube resting on a static plate (statics variant)
+  C2   peg insertion, dual low-res pads (8x6x3 lattice), 1024 envs
+  C3   as C2 with high-res pads (19x16x5 lattice), 4096 envs
+Per-env randomness uses numpy's Philox keyed by (250412908 + cfg index, global env id), so an
+env's inputs never depend on how envs are sharded across GPUs.
+
+Units are SI (m, kg, s).  Affine states y are 12-vectors (t[3], A[3x3] row-major): a body vertex
+with rest position xbar (body frame) sits at t + A xbar (P:L110-116 embedding phi).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import List, Optional
+
+import numpy as np
+
+DYNAMIC, KINEMATIC, STATIC = 0, 1, 2
+CFG_INDEX = {"C1": 1, "C1b": 11, "C1c": 12, "C2": 2, "C3": 3}
+SEED_BASE = 250412908
+
+
+@dataclasses.dataclass
+class SoftPad:
+    """A tetrahedral gel pad G_i. rest_pos is in the pad (sensor) frame."""
+    rest_pos: np.ndarray            # (nv,3) f64
+    tets: np.ndarray                # (nt,4) i32
+    youngs: float = 1.0e5
+    poisson: float = 0.40
+    density: float = 1.0e3
+    mount_body: int = -1            # index into Scene.affine, -1 = free soft body
+    mount_T: np.ndarray = dataclasses.field(default_factory=lambda: np.r_[np.zeros(3), np.eye(3).ravel()])
+    attached: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.int32))   # ∂⁻G
+    coated: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.int32))     # ∂⁺G
+    marker_tri: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros((0, 3), np.int32))
+    marker_bary: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros((0, 3)))
+
+
+@dataclasses.dataclass
+class AffineBody:
+    """An ABD body: closed outward-oriented triangle surface in its body frame."""
+    rest_pos: np.ndarray            # (nv,3) f64, body frame
+    tris: np.ndarray                # (nt,3) i32, outward
+    kind: int = DYNAMIC
+    density: float = 1.0e3
+    kappa_s: float = 1.0e8
+
+
+@dataclasses.dataclass
+class Config:
+    """Solver constants (proposals; the paper gives none)."""
+    dt: float = 0.02
+    dhat: float = 1.0e-4
+    kappa: float = 1.0e8
+    newton_tol_rel: float = 1.0e-7
+    al_tol_rel: float = 1.0e-6
+    pcg_eta: float = 1.0e-4
+    armijo_c: float = 1.0e-4
+    accd_s: float = 0.1
+    al_rho0: float = 1.0e8
+    max_newton: int = 200
+    max_al_rounds: int = 8
+    max_pcg: int = 2000
+    max_accd_iters: int = 10000
+    ee_mollifier: int = 1
+    cand_capacity_per_env: int = 16384
+    active_capacity_per_env: int = 4096
+
+
+@dataclasses.dataclass
+class Scene:
+    name: str
+    soft: List[SoftPad]
+    affine: List[AffineBody]
+    gravity: np.ndarray
+    config: Config
+    n_steps: int
+    collide: Optional[np.ndarray] = None
+
+    @property
+    def n_soft_verts(self) -> int:
+        return int(sum(p.rest_pos.shape[0] for p in self.soft))
+
+    @property
+    def kinematic_bodies(self) -> List[int]:
+        return [i for i, b in enumerate(self.affine) if b.kind == KINEMATIC]
+
+
+# ----------------------------------------------------------------------------------------------
+# geometry builders (topology + coordinates only)
+# ----------------------------------------------------------------------------------------------
+
+def lattice_tets(nx: int, ny: int, nz: int, size):
+    """Node lattice nx*ny*nz spanning [0,sx]x[0,sy]x[0,sz], each hex split into 5 tets with the
+    alternating (parity) split so neighbouring hexes share face diagonals.  Node id = i + nx*(j + ny*k).
+    Tets are returned with the index order of the split; orientation is NOT normalised here."""
+    sx, sy, sz = size
+    xs, ys, zs = np.linspace(0, sx, nx), np.linspace(0, sy, ny), np.linspace(0, sz, nz)
+    X = np.stack(np.meshgrid(xs, ys, zs, indexing="ij"), -1)          # (nx,ny,nz,3)
+    pos = X.transpose(2, 1, 0, 3).reshape(-1, 3).copy()                # id = i + nx*(j + ny*k)
+    nid = lambda i, j, k: i + nx * (j + ny * k)
+    even = [(1, 2, 4, 7), (0, 1, 2, 4), (3, 1, 2, 7), (5, 1, 4, 7), (6, 2, 4, 7)]
+    odd = [(0, 3, 5, 6), (1, 0, 3, 5), (2, 0, 3, 6), (4, 0, 5, 6), (7, 3, 5, 6)]
+    tets = []
+    for k in range(nz - 1):
+        for j in range(ny - 1):
+            for i in range(nx - 1):
+                c = [nid(i + (b & 1), j + ((b >> 1) & 1), k + ((b >> 2) & 1)) for b in range(8)]
+                for t in (even if (i + j + k) % 2 == 0 else odd):
+                    tets.append([c[t[0]], c[t[1]], c[t[2]], c[t[3]]])
+    return pos, np.asarray(tets, np.int32)
+
+
+def _axis_lines(breaks, spacing):
+    """Grid lines covering the sorted break points with segments no longer than `spacing`."""
+    out = [breaks[0]]
+    for a, b in zip(breaks[:-1], breaks[1:]):
+        n = max(1, int(math.ceil((b - a) / spacing - 1e-9)))
+        out += list(a + (b - a) * np.arange(1, n + 1) / n)
+    return np.asarray(out)
+
+
+def cell_union_surface(xl, yl, zl, solid):
+    """Watertight outward-oriented triangle surface of a union of cells of a rectilinear grid.
+    solid[i,j,k] marks cell [xl[i],xl[i+1]]x[yl[j],yl[j+1]]x[zl[k],zl[k+1]].  Every face between
+    a solid and an empty cell becomes a quad split into two triangles; vertices are grid nodes."""
+    nx, ny, nz = solid.shape
+    S = np.zeros((nx + 2, ny + 2, nz + 2), bool)
+    S[1:-1, 1:-1, 1:-1] = solid
+    vid = {}
+    verts, tris = [], []
+
+    def v(i, j, k):
+        key = (i, j, k)
+        if key not in vid:
+            vid[key] = len(verts)
+            verts.append((xl[i], yl[j], zl[k]))
+        return vid[key]
+
+    for ax in range(3):
+        for i in range(nx + 1 if ax == 0 else nx):
+            for j in range(ny + 1 if ax == 1 else ny):
+                for k in range(nz + 1 if ax == 2 else nz):
+                    lo = [i, j, k]
+                    # cells on either side of the face at grid index lo along axis ax
+                    c_lo = list(lo); c_lo[ax] -= 1
+                    s_lo = S[c_lo[0] + 1, c_lo[1] + 1, c_lo[2] + 1]
+                    s_hi = S[lo[0] + 1, lo[1] + 1, lo[2] + 1]
+                    if s_lo == s_hi:
+                        continue
+                    u, w = [(1, 2), (2, 0), (0, 1)][ax]
+                    p = []
+                    for du, dw in ((0, 0), (1, 0), (1, 1), (0, 1)):
+                        q = list(lo); q[u] += du; q[w] += dw
+                        p.append(v(*q))
+                    # (u,w,ax) is right-handed, so quad p0..p3 has normal +ax; flip if solid is on +ax side
+                    if s_lo:       # solid below -> outward normal +ax
+                        tris += [(p[0], p[1], p[2]), (p[0], p[2], p[3])]
+                    else:
+                        tris += [(p[0], p[2], p[1]), (p[0], p[3], p[2])]
+    return np.asarray(verts, np.float64), np.asarray(tris, np.int32)
+
+
+def box_surface(size, spacing=None, center=True):
+    sx, sy, sz = size
+    sp = spacing if spacing is not None else max(size) * 2
+    xl, yl, zl = (_axis_lines([0.0, s], sp) for s in size)
+    V, T = cell_union_surface(xl, yl, zl, np.ones((len(xl) - 1, len(yl) - 1, len(zl) - 1), bool))
+    if center:
+        V = V - np.array([sx, sy, sz]) / 2
+    return V, T
+
+
+def rot_z(theta):
+    c, s = math.cos(theta), math.sin(theta)
+    return np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
+
+
+def rot_y(theta):
+    c, s = math.cos(theta), math.sin(theta)
+    return np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
+
+
+def pose(t, R=None):
+    R = np.eye(3) if R is None else np.asarray(R, np.float64)
+    return np.r_[np.asarray(t, np.float64), R.ravel()]
+
+
+def compose(y_parent, T_child):
+    """Compose two 12-vector affine poses: x -> tp + Ap (tc + Ac x)."""
+    tp, Ap = y_parent[:3], y_parent[3:].reshape(3, 3)
+    tc, Ac = T_child[:3], T_child[3:].reshape(3, 3)
+    return np.r_[tp + Ap @ tc, (Ap @ Ac).ravel()]
+
+
+def apply_pose(y, X):
+    return X @ y[3:].reshape(3, 3).T + y[:3]
+
+
+def _pad_regions(nx, ny, nz):
+    """Bottom face (k=0) is the attached region ∂⁻G, top face (k=nz-1) the coated region ∂⁺G."""
+    ids = np.arange(nx * ny * nz).reshape(nz, ny, nx)
+    return ids[0].ravel().astype(np.int32), ids[-1].ravel().astype(np.int32)
+
+
+def _markers(nx, ny, nz, every=2):
+    """Markers at the centroids-ish of top-face triangles on a regular sub-grid of ∂⁺G: each marker
+    is a (tri of 3 top vertices, barycentric weights) with Σα=1, α∈[0,1]."""
+    ids = np.arange(nx * ny * nz).reshape(nz, ny, nx)[-1]
+    tri, bary = [], []
+    for j in range(0, ny - 1, every):
+        for i in range(0, nx - 1, every):
+            tri.append([ids[j, i], ids[j, i + 1], ids[j + 1, i]])
+            bary.append([0.5, 0.25, 0.25])
+    return np.asarray(tri, np.int32), np.asarray(bary, np.float64)
+
+
+def make_pad(nx, ny, nz, size, mount_body, mount_T, **mat):
+    pos, tets = lattice_tets(nx, ny, nz, size)
+    pos = pos - np.array([size[0] / 2, size[1] / 2, 0.0])      # pad frame: bottom face centred at 0
+    att, coat = _pad_regions(nx, ny, nz)
+    mt, mb = _markers(nx, ny, nz)
+    return SoftPad(rest_pos=pos, tets=tets, mount_body=mount_body, mount_T=np.asarray(mount_T, np.float64),
+                   attached=att, coated=coat, marker_tri=mt, marker_bary=mb, **mat)
+
+
+# ----------------------------------------------------------------------------------------------
+# configs
+# ----------------------------------------------------------------------------------------------
+
+MM = 1e-3
+
+
+def scene_C1(variant="C1"):
+    """C1: one 8x8x3 pad (21x21x4 mm) with its bottom attached to a static base;
+    a kinematic 10 mm cube (8 v / 12 t) 0.2 mm above, yawed 7°, offset (0.37,-0.21) mm, whose
+    target descends 0.12 mm/step for 10 steps (nominal press 1.0 mm).  dt = 0.01 s.
+    C1b: the cube is dynamic and dropped from 1 mm.  C1c: a soft 5-tet-lattice cube on a static plate."""
+    cfg = Config(dt=0.01)
+    base_V, base_T = box_surface((30 * MM, 30 * MM, 5 * MM))
+    base = AffineBody(base_V, base_T, kind=STATIC)
+    if variant == "C1c":
+        cube_pos, cube_tets = lattice_tets(4, 4, 4, (8 * MM, 8 * MM, 8 * MM))
+        cube_pos = cube_pos - np.array([4 * MM, 4 * MM, 0.0])
+        soft = SoftPad(rest_pos=cube_pos, tets=cube_tets, mount_body=-1,
+                       mount_T=pose([0.3 * MM, -0.2 * MM, 2.5 * MM + 0.05 * MM]))
+        return Scene("C1c", [soft], [base], np.array([0, 0, -9.81]), cfg, n_steps=10)
+    pad = make_pad(8, 8, 3, (21 * MM, 21 * MM, 4 * MM), mount_body=0, mount_T=pose([0, 0, 2.5 * MM]))
+    cube_V, cube_T = box_surface((10 * MM, 10 * MM, 10 * MM))
+    kind = DYNAMIC if variant == "C1b" else KINEMATIC
+    cube = AffineBody(cube_V, cube_T, kind=kind)
+    return Scene(variant, [pad], [base, cube], np.array([0, 0, -9.81]), cfg, n_steps=10)
+
+
+def scene_C2(high_res=False):
+    """C2/C3: two pads on two kinematic finger boxes (25x22x6 mm) squeezing a
+    dynamic 12x12x60 mm square peg (~3 mm tessellation) that rests on the floor of a static blind
+    hole (40x40x20 mm block, 12.6 mm square hole 15 mm deep, 0.3 mm clearance).  dt = 0.02 s."""
+    cfg = Config(dt=0.02)
+    # static block with the hole; top face at z=0
+    hw = 6.3 * MM
+    xl = _axis_lines([-20 * MM, -hw, hw, 20 * MM], 3.5 * MM)
+    yl = _axis_lines([-20 * MM, -hw, hw, 20 * MM], 3.5 * MM)
+    zl = _axis_lines([-20 * MM, -15 * MM, 0.0], 5.0 * MM)
+    solid = np.ones((len(xl) - 1, len(yl) - 1, len(zl) - 1), bool)
+    xc, yc, zc = (xl[:-1] + xl[1:]) / 2, (yl[:-1] + yl[1:]) / 2, (zl[:-1] + zl[1:]) / 2
+    solid &= ~((np.abs(xc)[:, None, None] < hw) & (np.abs(yc)[None, :, None] < hw) & (zc[None, None, :] > -15 * MM))
+    hole_V, hole_T = cell_union_surface(xl, yl, zl, solid)
+    hole = AffineBody(hole_V, hole_T, kind=STATIC)
+    peg_V, peg_T = box_surface((12 * MM, 12 * MM, 60 * MM), spacing=3 * MM)
+    peg = AffineBody(peg_V, peg_T, kind=DYNAMIC)
+    fV, fT = box_surface((6 * MM, 22 * MM, 25 * MM))
+    finger_l = AffineBody(fV, fT, kind=KINEMATIC)
+    finger_r = AffineBody(fV.copy(), fT.copy(), kind=KINEMATIC)
+    if high_res:
+        lat, size = (19, 16, 5), (21 * MM, 17.5 * MM, 4 * MM)
+    else:
+        lat, size = (8, 6, 3), (21 * MM, 15 * MM, 4 * MM)
+    # pad frame: z = thickness (bottom attached to finger inner face), x along world z, y along world y.
+    # finger frame: centred box, inner face at +x (left finger) / -x (right finger).
+    # left finger's inner face is at local x=+3 mm; pad frame maps pad-z -> +x, pad-x -> world z.
+    R_l = np.array([[0.0, 0.0, 1.0], [0.0, 1.0, 0.0], [-1.0, 0.0, 0.0]])   # pad (x,y,z) -> finger (-z.. ) frame
+    R_r = np.array([[0.0, 0.0, -1.0], [0.0, 1.0, 0.0], [1.0, 0.0, 0.0]])
+    pad_l = make_pad(*lat, size, mount_body=2, mount_T=pose([3 * MM, 0, 0], R_l))
+    pad_r = make_pad(*lat, size, mount_body=3, mount_T=pose([-3 * MM, 0, 0], R_r))
+    name = "C3" if high_res else "C2"
+    return Scene(name, [pad_l, pad_r], [hole, peg, finger_l, finger_r], np.array([0, 0, -9.81]), cfg,
+                 n_steps=200)
+
+
+def make_scene(name: str) -> Scene:
+    if name in ("C1", "C1b", "C1c"):
+        return scene_C1(name)
+    if name == "C2":
+        return scene_C2(False)
+    if name == "C3":
+        return scene_C2(True)
+    raise ValueError(f"unknown scene {name}")
+
+
+# ----------------------------------------------------------------------------------------------
+# per-env seeded inputs
+# ----------------------------------------------------------------------------------------------
+
+def env_rng(name: str, env_id: int) -> np.random.Generator:
+    key = (SEED_BASE + CFG_INDEX[name]) * (1 << 32) + int(env_id)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+@dataclasses.dataclass
+class EnvInputs:
+    x0: np.ndarray        # (E, V, 3) initial soft vertex world positions
+    y0: np.ndarray        # (E, NA, 12) initial affine states (all bodies, static included)
+    ykin: np.ndarray      # (S, E, NK, 12) per-step kinematic targets s^y
+
+
+def _soft_world(scene: Scene, y0: np.ndarray, jitter: Optional[np.random.Generator] = None):
+    xs = []
+    for pad in scene.soft:
+        if pad.mount_body >= 0:
+            yp = compose(y0[pad.mount_body], pad.mount_T)
+        else:
+            yp = pad.mount_T
+        xs.append(apply_pose(yp, pad.rest_pos))
+    return np.concatenate(xs, 0)
+
+
+def _c1_env(scene, env_id, n_steps):
+    rng = env_rng(scene.name, env_id)
+    if env_id == 0:
+        yaw, off, gap, rate = 7.0, (0.37 * MM, -0.21 * MM), 0.2 * MM, 0.12 * MM
+    else:
+        yaw = rng.uniform(3.0, 11.0)
+        off = tuple(rng.uniform(-1.0, 1.0, 2) * MM)
+        gap = rng.uniform(0.15, 0.25) * MM
+        rate = rng.uniform(0.08, 0.14) * MM
+    pad_top = 2.5 * MM + 4 * MM
+    y_base = pose([0, 0, 0])
+    if scene.name == "C1c":
+        y0 = np.stack([y_base])
+        return y0, np.zeros((n_steps, 0, 12))
+    if scene.name == "C1b":
+        gap = 1.0 * MM
+    cube_y = pose([off[0], off[1], pad_top + gap + 5 * MM], rot_z(math.radians(yaw)))
+    y0 = np.stack([y_base, cube_y])
+    if scene.name == "C1b":
+        return y0, np.zeros((n_steps, 0, 12))
+    tk = []
+    for s in range(n_steps):
+        yt = cube_y.copy()
+        yt[2] -= rate * (s + 1)
+        tk.append(yt[None])
+    return y0, np.stack(tk)
+
+
+def _c2_env(scene, env_id, n_steps):
+    rng = env_rng(scene.name, env_id)
+    dx, dy = rng.uniform(-0.1, 0.1, 2) * MM
+    yaw0 = math.radians(rng.uniform(-0.5, 0.5))
+    tau_d = rng.uniform(0.5, 1.5) * MM
+    A_x = rng.uniform(0.5, 1.5) * MM
+    A_th = math.radians(rng.uniform(1.0, 2.0))
+    # static hole at origin (top face z=0); peg (centre frame) resting 0.08 mm above the floor
+    y_hole = pose([0, 0, 0])
+    y_peg = pose([dx, dy, -15 * MM + 0.08 * MM + 30 * MM], rot_z(yaw0))
+    grip_z = 32 * MM
+    pad_th = 4 * MM
+    gap0 = 0.2 * MM
+    # finger centre x so that the pad surface is gap0 away from the peg face (|x| = 6 mm)
+    fx = 6 * MM + gap0 + pad_th + 3 * MM
+    y_fl = pose([-fx + dx, dy, grip_z])
+    y_fr = pose([fx + dx, dy, grip_z])
+    y0 = np.stack([y_hole, y_peg, y_fl, y_fr])
+    close = 40
+    tk = []
+    for k in range(n_steps):
+        if k < close:
+            sq = (gap0 + tau_d) * (k + 1) / close
+            ox, th = 0.0, 0.0
+        else:
+            sq = gap0 + tau_d
+            ox = A_x * math.sin(2 * math.pi * 2 * (k + 1 - close) / 160.0)
+            th = A_th * math.sin(2 * math.pi * (k + 1 - close) / 160.0)
+        R = rot_z(th)
+        c = np.array([dx + ox, dy, grip_z])
+        yl = pose(c + R @ np.array([-fx + sq, 0, 0]), R)
+        yr = pose(c + R @ np.array([fx - sq, 0, 0]), R)
+        tk.append(np.stack([yl, yr]))
+    return y0, np.stack(tk)
+
+
+def env_inputs(scene: Scene, env_ids, n_steps: Optional[int] = None) -> EnvInputs:
+    """Initial states (zero velocities) and per-step kinematic targets for the given global
+    env ids.  Deterministic per env id."""
+    n_steps = scene.n_steps if n_steps is None else n_steps
+    ys, tks, xs = [], [], []
+    for e in env_ids:
+        if scene.name.startswith("C1"):
+            y0, tk = _c1_env(scene, int(e), n_steps)
+        else:
+            y0, tk = _c2_env(scene, int(e), n_steps)
+        ys.append(y0)
+        tks.append(tk)
+        xs.append(_soft_world(scene, y0))
+    ykin = np.stack(tks, 1) if len(tks) else np.zeros((n_steps, 0, 0, 12))
+    return EnvInputs(x0=np.stack(xs), y0=np.stack(ys), ykin=ykin)

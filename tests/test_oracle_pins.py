@@ -1,0 +1,533 @@
+"""Pins for the CPU oracle: each test ties an oracle function to something other than itself —
+values the paper fixes (tests/golden/closed_forms.json), closed forms, invariants, special cases
+that reduce to a textbook result, and brute force on tiny inputs."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2504_12908_b200 import scenes as S
+from oracle import contact as C
+from oracle import distance as D
+from oracle import energy as En
+from oracle import mesh as M
+from oracle import readout as R
+from oracle import solver as SO
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "closed_forms.json")))
+T = torch.as_tensor
+
+
+def unit_tet():
+    return np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float), np.array([[0, 1, 2, 3]])
+
+
+# ------------------------------------------------------------------------------------ mesh
+
+def test_unit_simplex_volume_and_mass():
+    X, tets = unit_tet()
+    Dinv, vol = M.tet_rest(X, tets)
+    assert vol[0] == pytest.approx(1 / 6, rel=1e-15)
+    g = GOLD["lumped_mass_unit_simplex"]
+    m = M.lumped_mass(4, tets, vol, g["density"])
+    assert np.allclose(m, g["mass_per_vertex"], rtol=1e-14)
+
+
+def test_orientation_fix_and_degenerate_reject():
+    X, tets = unit_tet()
+    flipped = tets[:, [0, 2, 1, 3]]
+    assert np.array_equal(M.orient_tets(X, flipped)[0][[0, 3]], [0, 3])
+    assert M.tet_rest(X, M.orient_tets(X, flipped))[1][0] > 0
+    Xd = X.copy()
+    Xd[3] = [0.5, 0.5, 0.0]
+    with pytest.raises(ValueError):
+        M.orient_tets(Xd, tets)
+
+
+def test_single_tet_surface_outward():
+    X, tets = unit_tet()
+    F = M.boundary_faces(tets)
+    assert len(F) == 4
+    c = X.mean(0)
+    for f in F:
+        n = np.cross(X[f[1]] - X[f[0]], X[f[2]] - X[f[0]])
+        assert np.dot(n, X[f].mean(0) - c) > 0
+
+
+def test_lattice_surface_area_and_mass():
+    pos, tets = S.lattice_tets(3, 3, 3, (1.0, 1.0, 1.0))
+    tets = M.orient_tets(pos, tets)
+    F = M.boundary_faces(tets)
+    assert M.tri_area(pos, F).sum() == pytest.approx(6.0, rel=1e-13)
+    Dinv, vol = M.tet_rest(pos, tets)
+    assert vol.sum() == pytest.approx(1.0, rel=1e-13)
+    m = M.lumped_mass(len(pos), tets, vol, 7.0)
+    assert m.sum() == pytest.approx(7.0, rel=1e-12)
+    # divergence-theorem volume of the extracted surface == Σ V_e (S:L52 property)
+    v = np.einsum("ij,ij->i", pos[F[:, 0]], np.cross(pos[F[:, 1]], pos[F[:, 2]])).sum() / 6
+    assert v == pytest.approx(1.0, rel=1e-12)
+
+
+@pytest.mark.parametrize("offset", [(0, 0, 0), (0.3, -0.7, 1.1)])
+def test_reduced_mass_box_closed_form(offset):
+    a, b, c, rho = 0.3, 0.5, 0.7, 900.0
+    V, Tr = S.box_surface((a, b, c), spacing=0.2)
+    V = V + np.array(offset)
+    vol, m, s1, My = M.body_moments(V, Tr, rho)
+    mm = rho * a * b * c
+    o = np.array(offset)
+    S2 = mm * (np.outer(o, o) + np.diag([a * a, b * b, c * c]) / 12)
+    assert vol == pytest.approx(a * b * c, rel=1e-12)
+    assert np.allclose(s1, mm * o, rtol=1e-12, atol=1e-15)
+    # M^y = I₃⊗[[m, s1ᵀ],[s1, S2]] in (t, A row-major) ordering (P:L113-116 JᵀMJ)
+    for i in range(3):
+        assert My[i, i] == pytest.approx(mm, rel=1e-12)
+        for j in range(3):
+            assert My[i, 3 + 3 * i + j] == pytest.approx(mm * o[j], rel=1e-12, abs=1e-15)
+            for k in range(3):
+                assert My[3 + 3 * i + j, 3 + 3 * i + k] == pytest.approx(S2[j, k], rel=1e-11, abs=1e-15)
+    assert np.allclose(My, My.T)
+    assert np.linalg.eigvalsh(My).min() > 0
+
+
+def test_reduced_mass_L_shape_equals_sum_of_boxes():
+    """Union of two boxes: moments add (linearity of ∫ over disjoint cells)."""
+    xl, yl, zl = np.array([0, 1, 2.0]), np.array([0, 1.0]), np.array([0, 1, 2.0])
+    solid = np.zeros((2, 1, 2), bool)
+    solid[0, 0, 0] = solid[1, 0, 0] = solid[0, 0, 1] = True
+    V, Tr = S.cell_union_surface(xl, yl, zl, solid)
+    vol, m, s1, My = M.body_moments(V, Tr, 1.0)
+    tot = np.zeros((12, 12))
+    for c in ([0.5, 0.5, 0.5], [1.5, 0.5, 0.5], [0.5, 0.5, 1.5]):
+        Vb, Tb = S.box_surface((1, 1, 1))
+        tot += M.body_moments(Vb + np.array(c), Tb, 1.0)[3]
+    assert vol == pytest.approx(3.0, rel=1e-12)
+    assert np.allclose(My, tot, rtol=1e-12, atol=1e-14)
+
+
+def test_reduced_kinetic_energy_equals_full_space():
+    """½ẏᵀM^yẏ = ½∫ρ‖J ẏ‖² (P:L113 chain of equalities), checked by Monte-Carlo-free exact
+    sampling: for a box the full-space integral of ‖v(x)‖² with v = ṫ + Ȧx is a quadratic
+    polynomial integrated exactly by the box closed form."""
+    a, b, c, rho = 0.2, 0.3, 0.4, 1000.0
+    V, Tr = S.box_surface((a, b, c), spacing=0.1)
+    My = M.body_moments(V, Tr, rho)[3]
+    rng = np.random.default_rng(0)
+    yd = rng.normal(size=12)
+    td, Ad = yd[:3], yd[3:].reshape(3, 3)
+    m = rho * a * b * c
+    S2 = m * np.diag([a * a, b * b, c * c]) / 12
+    full = 0.5 * (m * td @ td + np.trace(Ad @ S2 @ Ad.T))
+    assert 0.5 * yd @ My @ yd == pytest.approx(full, rel=1e-11)
+
+
+def test_rest_areas_partition_surface():
+    sc = S.make_scene("C1")
+    mod = M.prepare(sc)
+    total = M.tri_area(mod.vert_xbar, mod.tris).sum()
+    assert mod.A_v.sum() == pytest.approx(total, rel=1e-12)
+    assert mod.A_e.sum() == pytest.approx(total, rel=1e-12)
+
+
+def test_affine_jacobian_matches_fd_of_embedding():
+    rng = np.random.default_rng(1)
+    xb = rng.normal(size=3)
+    y = rng.normal(size=12)
+    J = M.affine_jacobian(xb)
+    h = 1e-6
+    for k in range(12):
+        e = np.zeros(12)
+        e[k] = h
+        fd = (M.embed(y + e, xb[None])[0] - M.embed(y - e, xb[None])[0]) / (2 * h)
+        assert np.allclose(fd, J[:, k], atol=1e-8)
+    assert np.allclose(M.embed(np.r_[0, 0, 0, np.eye(3).ravel()], xb[None])[0], xb)
+
+
+# ------------------------------------------------------------------------------------ energies
+
+def test_barrier_closed_forms():
+    g = GOLD["barrier"]
+    dh = g["dhat"]
+    d = T(np.array([dh, 0.5 * dh]), dtype=torch.float64).requires_grad_(True)
+    b = En.barrier(d, dh)
+    (gb,) = torch.autograd.grad(b.sum(), d, create_graph=True)
+    (hb,) = torch.autograd.grad(gb.sum(), d)
+    assert float(b[0]) == 0.0 and float(gb[0]) == 0.0 and float(hb[0]) == 0.0
+    assert float(b[1]) / dh ** 2 == pytest.approx(g["b_at_half_over_dhat2"], rel=1e-14)
+    assert float(gb[1]) / dh == pytest.approx(g["db_at_half_over_dhat"], rel=1e-14)
+    assert float(hb[1]) == pytest.approx(g["d2b_at_half"], rel=1e-13)
+    # support: zero beyond d̂, monotone decreasing inside
+    dd = T(np.linspace(0.05, 2.0, 60) * dh)
+    bb = En.barrier(dd, dh).numpy()
+    assert np.all(bb[dd.numpy() >= dh] == 0)
+    inside = bb[dd.numpy() < dh]
+    assert np.all(np.diff(inside) < 0)
+
+
+def test_neo_hookean_rest_and_rotation_invariance():
+    mu, lam = M.lame(1e5, 0.4)
+    F = torch.eye(3, dtype=torch.float64, requires_grad=True)
+    psi = En.neo_hookean_psi(F, mu, lam)
+    (P,) = torch.autograd.grad(psi, F)
+    assert abs(float(psi)) < 1e-12 and float(P.abs().max()) < 1e-9
+    rng = np.random.default_rng(2)
+    Q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+    Q *= np.sign(np.linalg.det(Q))
+    Fr = rng.normal(size=(3, 3)) * 0.1 + np.eye(3)
+    a = float(En.neo_hookean_psi(T(Fr), mu, lam))
+    b = float(En.neo_hookean_psi(T(Q @ Fr), mu, lam))
+    assert abs(a - b) < 1e-12 * max(1.0, abs(a))
+    assert abs(float(En.neo_hookean_psi(T(Q), mu, lam))) < 1e-9
+
+
+def test_neo_hookean_uniaxial_closed_form_and_rest_spectrum():
+    mu, lam = 3.0, 5.0
+    for s in (0.7, 1.0, 1.3):
+        Fs = np.diag([s, 1.0, 1.0])
+        closed = mu / 2 * (s * s - 1) - mu * math.log(s) + lam / 2 * math.log(s) ** 2
+        assert float(En.neo_hookean_psi(T(Fs), mu, lam)) == pytest.approx(closed, rel=1e-13, abs=1e-14)
+    H = torch.func.hessian(En.neo_hookean_psi)(torch.eye(3, dtype=torch.float64), mu, lam).reshape(9, 9).numpy()
+    w = np.sort(np.linalg.eigvalsh(H))
+    m = GOLD["neo_hookean_rest_spectrum"]["multiplicities"]
+    assert np.allclose(w[:m["zero"]], 0, atol=1e-12)
+    assert np.allclose(w[3:8], 2 * mu, rtol=1e-12)
+    assert w[8] == pytest.approx(2 * mu + 3 * lam, rel=1e-12)
+
+
+def test_ortho_energy_closed_forms():
+    kap, vol = 1e8, 2e-6
+    assert float(En.ortho_energy(torch.eye(3, dtype=torch.float64), kap, vol)) == 0.0
+    R = S.rot_z(math.radians(30)) @ S.rot_y(0.3)
+    assert abs(float(En.ortho_energy(T(R), kap, vol))) < 1e-12 * kap * vol
+    e = 1e-3
+    A = np.diag([1 + e, 1, 1])
+    assert float(En.ortho_energy(T(A), kap, vol)) == pytest.approx(kap * vol * (2 * e + e * e) ** 2, rel=1e-12)
+
+
+def test_mollifier_continuity():
+    eps = 2.0
+    c = T(np.array([eps * (1 - 1e-9), eps]), dtype=torch.float64).requires_grad_(True)
+    m = En.ee_mollifier(c, eps)
+    (dm,) = torch.autograd.grad(m.sum(), c)
+    assert float(m[0]) == pytest.approx(1.0, abs=1e-12) and float(m[1]) == 1.0
+    assert abs(float(dm[0])) < 1e-8 and float(dm[1]) == 0.0
+    assert float(En.ee_mollifier(T(0.0), eps)) == 0.0
+
+
+# ------------------------------------------------------------------------------------ distances
+
+def _random_tri(rng):
+    while True:
+        t = rng.normal(size=(3, 3))
+        if np.linalg.norm(np.cross(t[1] - t[0], t[2] - t[0])) > 0.3:
+            return t
+
+
+def _seg_dist2_dense(p, a, b, n=20001):
+    s = np.linspace(0, 1, n)[:, None]
+    return (((a + s * (b - a)) - p) ** 2).sum(1).min()
+
+
+def test_pt_centroid_normal_distance():
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        t = _random_tri(rng)
+        n = np.cross(t[1] - t[0], t[2] - t[0])
+        n /= np.linalg.norm(n)
+        h = rng.uniform(0.01, 1)
+        typ, d2 = D.pt_type(t.mean(0) + h * n, t[0], t[1], t[2])
+        assert int(typ) == D.PT_T and math.sqrt(d2) == pytest.approx(h, rel=1e-12)
+
+
+def test_pt_distance_vs_dense_sampling():
+    """Brute force: min over a dense barycentric grid of the closed triangle."""
+    rng = np.random.default_rng(4)
+    nn = 400
+    u, v = np.meshgrid(np.linspace(0, 1, nn), np.linspace(0, 1, nn))
+    keep = (u + v) <= 1
+    u, v = u[keep], v[keep]
+    for _ in range(30):
+        t = _random_tri(rng)
+        p = rng.normal(size=3) * 1.5
+        pts = t[0] + u[:, None] * (t[1] - t[0]) + v[:, None] * (t[2] - t[0])
+        bf = ((pts - p) ** 2).sum(1).min()
+        typ, d2 = D.pt_type(p, t[0], t[1], t[2])
+        # the grid min is an upper bound within grid resolution of the exact min
+        assert d2 <= bf + 1e-12
+        assert math.sqrt(bf) - math.sqrt(d2) < 5e-3
+        # classified sub-distance equals the exact closest-point distance on its sub-primitive
+        if typ == D.PT_T:
+            pass
+        elif typ <= D.PT_E2:
+            i = typ - D.PT_E0
+            assert d2 == pytest.approx(_seg_dist2_dense(p, t[i], t[(i + 1) % 3]), rel=1e-6, abs=1e-12)
+        else:
+            assert d2 == pytest.approx(((p - t[typ - D.PT_V0]) ** 2).sum(), rel=1e-14)
+
+
+def test_ee_closed_forms_and_grid():
+    h = 0.37
+    typ, d2 = D.ee_type([0, 0, 0], [1, 0, 0], [0.5, -0.5, h], [0.5, 0.5, h])
+    assert int(typ) == D.EE_LL and math.sqrt(d2) == pytest.approx(h, rel=1e-13)
+    typ, d2 = D.ee_type([0, 0, 0], [1, 0, 0], [0, h, 0], [1, h, 0])       # parallel
+    assert math.sqrt(d2) == pytest.approx(h, rel=1e-13)
+    rng = np.random.default_rng(5)
+    s = np.linspace(0, 1, 200)
+    for _ in range(30):
+        a0, a1, b0, b1 = rng.normal(size=(4, 3))
+        P = a0 + s[:, None, None] * (a1 - a0)
+        Q = b0 + s[None, :, None] * (b1 - b0)
+        bf = ((P - Q) ** 2).sum(-1).min()
+        typ, d2 = D.ee_type(a0, a1, b0, b1)
+        assert d2 <= bf + 1e-12
+        assert math.sqrt(bf) - math.sqrt(d2) < 2e-2
+        typ2, d2s = D.ee_type(b0, b1, a0, a1)                          # symmetry under swap
+        assert d2s == pytest.approx(d2, rel=1e-9, abs=1e-14)
+
+
+def test_distance_rigid_invariance():
+    rng = np.random.default_rng(6)
+    R = S.rot_z(0.7) @ S.rot_y(-0.4)
+    t = rng.normal(size=3) * 10
+    for _ in range(20):
+        X = rng.normal(size=(4, 3))
+        Y = X @ R.T + t
+        assert D.pt_type(*X)[1] == pytest.approx(D.pt_type(*Y)[1], rel=1e-9, abs=1e-12)
+        assert D.ee_type(*X)[1] == pytest.approx(D.ee_type(*Y)[1], rel=1e-9, abs=1e-12)
+
+
+# ------------------------------------------------------------------------------------ gradients
+
+def _perturbed_state(name, seed, amp=2e-5):
+    sc = S.make_scene(name)
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=1)
+    rng = np.random.default_rng(seed)
+    x = ei.x0[0] + rng.normal(size=ei.x0[0].shape) * amp
+    y = ei.y0[0].copy()
+    for b in range(len(y)):
+        if mod.dof_slot[b] >= 0:
+            y[b] += rng.normal(size=12) * amp * np.r_[np.ones(3), np.ones(9) * 0.01]
+    v = rng.normal(size=x.shape) * 1e-3
+    yd = rng.normal(size=y.shape) * 1e-3
+    ctx = En.make_context(mod, ei.x0[0], v, ei.y0[0], yd, ei.ykin[0, 0], sc.config.dt)
+    ctx.lam_att = rng.normal(size=ctx.lam_att.shape) * 1e-6
+    ctx.lam_kin = rng.normal(size=ctx.lam_kin.shape) * 1e-6
+    return sc, mod, ctx, x, y
+
+
+def _press_state():
+    """C1 with the cube pushed into the barrier zone (active PT and EE pairs)."""
+    sc, mod, ctx, x, y = _perturbed_state("C1", 7)
+    y[1, 2] -= 0.2e-3 - 0.04e-3          # cube bottom 40 µm above the pad top
+    return sc, mod, ctx, x, y
+
+
+def test_total_gradient_and_hvp_vs_finite_differences():
+    """Unprojected gradient/HVP against central differences of the energy."""
+    sc, mod, ctx, x, y = _press_state()
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    assert len(pairs) > 0 and (pairs.kind == 1).any() and (pairs.kind == 0).any()
+    g, H = En.assemble(mod, ctx, x, y, pairs, project=False)
+    q0 = En.pack(mod, x, y)
+    rng = np.random.default_rng(8)
+    v = rng.normal(size=q0.shape)
+    h = 1e-9
+
+    def E(q):
+        xx, yy = En.unpack(mod, q, y)
+        return En.total_energy(mod, ctx, xx, yy, pairs)
+    fd = (E(q0 + h * v) - E(q0 - h * v)) / (2 * h)
+    assert fd == pytest.approx(g @ v, rel=2e-5)
+
+    def G(q):
+        xx, yy = En.unpack(mod, q, y)
+        return En.assemble(mod, ctx, xx, yy, pairs, project=False)[0]
+    fdh = (G(q0 + h * v) - G(q0 - h * v)) / (2 * h)
+    hv = H @ v
+    assert np.abs(fdh - hv).max() <= 1e-4 * np.abs(hv).max()
+
+
+def test_projected_hessian_is_psd_and_exact_at_rest():
+    sc, mod, ctx, x, y = _press_state()
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    g, H = En.assemble(mod, ctx, x, y, pairs, project=True)
+    Hd = H.toarray()
+    assert np.allclose(Hd, Hd.T, atol=1e-12 * np.abs(Hd).max())
+    assert np.linalg.eigvalsh(Hd).min() > 0
+    # at the rest state no element clamp occurs: projected == unprojected (elastic part)
+    sc2 = S.make_scene("C1")
+    m2 = M.prepare(sc2)
+    ei = S.env_inputs(sc2, [0], 1)
+    ctx2 = En.make_context(m2, ei.x0[0], 0 * ei.x0[0], ei.y0[0], 0 * ei.y0[0], ei.ykin[0, 0], sc2.config.dt)
+    e = En.Pairs(*(np.zeros(0, np.int64),) * 4, np.zeros(0))
+    Hp = En.assemble(m2, ctx2, ei.x0[0], ei.y0[0], e, True)[1]
+    Hu = En.assemble(m2, ctx2, ei.x0[0], ei.y0[0], e, False)[1]
+    assert abs(Hp - Hu).max() <= 1e-12 * abs(Hu).max()
+
+
+def test_affine_gravity_is_jacobian_pullback():
+    """Affine gravity gradient equals Jᵀ of the full-space gradient −m g."""
+    a, rho = 0.1, 1000.0
+    V, Tr = S.box_surface((a, a, a), spacing=0.05)
+    V = V + np.array([0.02, -0.01, 0.03])
+    vol, m, s1, My = M.body_moments(V, Tr, rho)
+    g = T([0.0, 0.0, -9.81])
+    y = T(np.r_[0.1, 0.2, 0.3, (np.eye(3) + 0.01).ravel()]).requires_grad_(True)
+    E = -(g * (m * y[:3] + y[3:].reshape(3, 3) @ T(s1))).sum()
+    (gy,) = torch.autograd.grad(E, y)
+    # ∫ρ J(x̄)ᵀ(−g) dV = [−m g ; −g ⊗ s1]
+    expect = np.r_[-m * g.numpy(), np.outer(-g.numpy(), s1).ravel()]
+    assert np.allclose(gy.numpy(), expect, rtol=1e-12, atol=1e-15)
+
+
+# ------------------------------------------------------------------------------------ contact / CCD
+
+def test_active_set_equals_naive_all_pairs():
+    sc, mod, ctx, x, y = _press_state()
+    P = M.all_positions(mod, x, y)
+    act = C.active_pairs(mod, P)
+    dhat2 = sc.config.dhat ** 2
+    naive = []
+    for v in mod.surf_verts:
+        for t in range(len(mod.tris)):
+            if mod.allowed[mod.vert_body[v], mod.tri_body[t]]:
+                tt = mod.tris[t]
+                if D.pt_type(P[v], P[tt[0]], P[tt[1]], P[tt[2]])[1] < dhat2:
+                    naive.append((0, v, t))
+    E = mod.edges
+    for a in range(len(E)):
+        for b in range(a + 1, len(E)):
+            if mod.allowed[mod.edge_body[a], mod.edge_body[b]]:
+                if D.ee_type(P[E[a, 0]], P[E[a, 1]], P[E[b, 0]], P[E[b, 1]])[1] < dhat2:
+                    naive.append((1, a, b))
+    assert np.array_equal(act.keys(), np.asarray(naive).reshape(-1, 3))
+
+
+def test_far_cubes_empty_and_filter_rules():
+    sc = S.make_scene("C1")
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], 1)
+    P = M.all_positions(mod, ei.x0[0], ei.y0[0])      # cube 0.2 mm > d̂ above the pad
+    assert len(C.active_pairs(mod, P)) == 0
+    # the pad touches its mount (base) at distance 0 but that body pair is excluded
+    assert not mod.allowed[0, 1] and mod.allowed[0, 2] and not mod.allowed[1, 2]
+
+
+def test_accd_closed_forms():
+    g = GOLD["accd_normal_approach"]
+    tri = np.array([[-1, -1, 0], [2, -1, 0], [-1, 2, 0.0]])
+    X = np.vstack([[0, 0, g["d0"]], tri])
+    Pd = np.zeros((4, 3))
+    Pd[0, 2] = -g["speed"]
+    assert C.accd(0, X, Pd) == pytest.approx(g["alpha"], rel=1e-12)
+    assert C.accd(0, X, np.zeros((4, 3))) == 1.0
+    assert C.accd(0, X, np.tile([0.3, 0.2, 0.1], (4, 1))) == 1.0      # common translation
+
+
+def test_accd_conservative_audit():
+    """100 random trials: returned α ≤ exact TOI (dense bisection) and distance > 0 after the move
+    (S:L138)."""
+    rng = np.random.default_rng(9)
+    for trial in range(100):
+        kind = trial % 2
+        X = rng.normal(size=(4, 3))
+        Pd = rng.normal(size=(4, 3)) * 2.0
+        t = C.accd(kind, X, Pd)
+        ts = np.linspace(0, 1, 4001)
+        d2 = np.array([C._pair_d2(kind, X + s * Pd) for s in ts])
+        hit = np.nonzero(d2 < 1e-14)[0]
+        toi = ts[hit[0]] if len(hit) else 1.0
+        assert t <= toi + 1e-9
+        assert C._pair_d2(kind, X + min(t, 1.0) * Pd) > 0
+
+
+# ------------------------------------------------------------------------------------ solver
+
+def _free_body_scene(gravity=(0, 0, -9.81)):
+    V, Tr = S.box_surface((0.01, 0.01, 0.01))
+    body = S.AffineBody(V, Tr, kind=S.DYNAMIC)
+    sc = S.Scene("C1", [], [body], np.array(gravity, float), S.Config(dt=0.01), n_steps=1)
+    return sc, M.prepare(sc)
+
+
+def test_free_fall_one_newton_step_exact():
+    sc, mod = _free_body_scene()
+    y0 = np.array([[0.1, 0.2, 0.3, *S.rot_z(0.4).ravel()]])
+    yd0 = np.array([[0.5, -0.2, 0.1, *np.zeros(9)]])
+    st = SO.State(np.zeros((0, 3)), np.zeros((0, 3)), y0, yd0)
+    new, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=0.02)
+    dt = sc.config.dt
+    expect = y0[0, :3] + dt * yd0[0, :3] + dt * dt * sc.gravity
+    assert stats.status == SO.ENV_OK and stats.newton_iters == 2    # one step + convergence check
+    assert np.allclose(new.y[0, :3], expect, rtol=0, atol=1e-15)
+    assert np.allclose(new.y[0, 3:], y0[0, 3:], atol=1e-15)
+
+
+def test_fixed_point_without_forces():
+    sc, mod = _free_body_scene(gravity=(0, 0, 0))
+    y0 = np.array([[0.1, 0.2, 0.3, *np.eye(3).ravel()]])
+    st = SO.State(np.zeros((0, 3)), np.zeros((0, 3)), y0, np.zeros_like(y0))
+    new, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=0.02)
+    assert np.array_equal(new.y, y0) and stats.newton_iters == 1
+
+
+def test_descent_direction_and_pcg_agrees_with_direct():
+    sc, mod, ctx, x, y = _press_state()
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    g, H = En.assemble(mod, ctx, x, y, pairs)
+    import scipy.sparse.linalg as spla
+    p = spla.spsolve(H.tocsc(), -g)
+    assert g @ p < 0
+    pp, it = SO.block_jacobi_pcg(mod, H, g, 1e-8, 5000)
+    assert it > 1
+    assert np.abs(pp - p).max() <= 1e-5 * np.abs(p).max()
+    assert g @ pp < 0
+
+
+def test_al_fixed_vertex_single_tet():
+    """A tet with one vertex constrained to a moved target converges within ≤5 AL rounds
+    (S:L387)."""
+    X, tets = unit_tet()
+    X = X * 0.01
+    base_V, base_T = S.box_surface((0.05, 0.05, 0.01))
+    base = S.AffineBody(base_V, base_T, kind=S.KINEMATIC)
+    pad = S.SoftPad(rest_pos=X, tets=tets, mount_body=0, mount_T=S.pose([0, 0, 0.1]),
+                    attached=np.array([0], np.int32))
+    sc = S.Scene("C1", [pad], [base], np.array([0, 0, -9.81]), S.Config(dt=0.01), n_steps=1)
+    mod = M.prepare(sc)
+    y0 = np.array([S.pose([0, 0, 0])])
+    x0 = X + np.array([0, 0, 0.1])
+    st = SO.State(x0, np.zeros_like(x0), y0, np.zeros_like(y0))
+    target = S.pose([0.001, -0.0005, 0.0002])
+    new, stats = SO.step(mod, st, target[None], L_env=0.1)
+    assert stats.status == SO.ENV_OK and stats.al_rounds <= 5
+    assert np.linalg.norm(new.x[0] - (np.array([0.001, -0.0005, 0.1002]))) <= sc.config.al_tol_rel * 0.1
+
+
+# ------------------------------------------------------------------------------------ readout
+
+def test_readout_rigid_motion_and_bary():
+    sc = S.make_scene("C1")
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], 1)
+    x, y = ei.x0[0].copy(), ei.y0[0].copy()
+    # undeformed → zero displacement and flow
+    coated, mpos, mflow = R.gel_deformation(mod, x, y)[0]
+    assert np.abs(coated).max() < 1e-15 and np.abs(mflow).max() < 1e-15
+    # rigid motion of the base (mount) together with the pad → zero flow
+    Rz = S.rot_z(0.3)
+    y2 = y.copy()
+    y2[0] = S.pose([0.01, 0.02, -0.03], Rz)
+    x2 = x @ Rz.T + np.array([0.01, 0.02, -0.03])
+    coated, mpos, mflow = R.gel_deformation(mod, x2, y2)[0]
+    assert np.abs(coated).max() < 1e-15 and np.abs(mflow).max() < 1e-15
+    # barycentric weights (1,0,0) → exactly that vertex
+    pad = sc.soft[0]
+    pad.marker_bary = np.array([[1.0, 0.0, 0.0]])
+    pad.marker_tri = pad.marker_tri[:1]
+    c, mp, mf = R.gel_deformation(mod, x2, y2)[0]
+    assert np.array_equal(mp[0], x2[pad.marker_tri[0, 0]])
