@@ -1,0 +1,196 @@
+/*
+ * taccel.h — C ABI of the B200-native batched IPC + ABD Newton step (Taccel, arXiv 2504.12908).
+ *
+ * Implemented by libtaccel_cuda.so (paper_2504_12908_b200/csrc/, sm_100a, fp64, no CPU fallback).
+ * The calls follow the paper's problem statement:
+ *   load robots/objects/sensors ........ tac_batch_create
+ *   initialise states, zero velocities .. tac_set_state
+ *   apply kinematic targets s^y, s^x ..... tac_set_targets
+ *   time-step by argmin E_IPC^AL ........ tac_step                (P:L127-131 Eq. unified_ipc_variational,
+ *                                                                   P:L137 Eq. unified_ipc_AL)
+ *   read positions / gel deformation .... tac_get_state, tac_get_gel_deformation
+ *
+ * Conventions (all calls):
+ *   - SI units (m, kg, s); all floating point is IEEE binary64; indices int32; arrays row-major.
+ *   - An affine state y is 12 doubles: t[3] then A[3][3] row-major; a body vertex with body-frame
+ *     rest position xbar sits at t + A·xbar (embedding φ).
+ *   - Buffers passed to set/get calls may be HOST or DEVICE memory (the library copies with
+ *     cudaMemcpyDefault on `stream`); tac_debug_* take HOST buffers.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Functions return tac_status; on failure tac_last_error() returns a thread-local message that
+ *     stays valid until the next call on that thread.  No C++ exception crosses the ABI.
+ *   - Per-env failures never abort other envs: tac_step returns TAC_E_ENV_FAILED and sets
+ *     that env's tac_env_status; the env is rolled back to its state at the start of the step and
+ *     stays DISABLED until the next tac_set_state for it.
+ *
+ * Ownership: descriptor arrays are borrowed only during tac_batch_create (copied to the device).
+ * The workspace is caller-owned device memory (e.g. a torch uint8 tensor) of at least
+ * tac_workspace_size() bytes that must outlive the batch handle; the handle itself is heap memory
+ * owned by the caller and released with tac_batch_destroy.  State/target buffers are borrowed per
+ * call.
+ *
+ * Homogeneous batch: all envs of a batch share one template (topology, rest shapes, materials);
+ * envs differ only through state (x, ẋ, y, ẏ — static bodies' poses are per-env through y) and
+ * kinematic targets.
+ *
+ * Canonical contact primitives (used by tac_debug_active_pairs; the CPU oracle uses the same rule):
+ *   global vertex ids: soft vertices (pads in order), then each affine body's vertices;
+ *   triangles: per body in body order (pads first) — a pad's surface is the set of tet faces used
+ *   by exactly one tet, oriented outward; each triangle is stored rotated so its smallest vertex
+ *   id comes first, and a body's triangles are sorted by their sorted vertex triple;
+ *   edges: per body, the unique (min,max) vertex pairs of its triangles, sorted.
+ *   A PT pair is (kind=0, a=vertex id, b=triangle id); an EE pair is (kind=1, a=edge, b=edge, a<b).
+ */
+#ifndef TACCEL_H
+#define TACCEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TAC_OK = 0,
+  TAC_E_INVALID = 1,     /* bad argument (null pointer, out-of-range env range, bad config) */
+  TAC_E_VALIDATION = 2,  /* degenerate tet (|V| < 1e-15 m^3) or triangle (area < 1e-12 m^2) */
+  TAC_E_ENV_FAILED = 3,  /* tac_step: at least one env failed; see per-env status              */
+  TAC_E_CAPACITY = 4,    /* a fixed-capacity table is too small for the template              */
+  TAC_E_WORKSPACE = 5,   /* workspace too small or misaligned (needs 256-byte alignment)     */
+  TAC_E_CUDA = 6         /* CUDA runtime error (message has the CUDA error string)           */
+} tac_status;
+
+typedef enum {
+  TAC_ENV_OK = 0,
+  TAC_ENV_NEWTON_STALL = 1,   /* line search α < 1e-10 or Newton iteration cap reached          */
+  TAC_ENV_AL_INFEASIBLE = 2,  /* AL residual above tolerance after max_al_rounds                */
+  TAC_ENV_CAPACITY = 3,       /* candidate/active pair capacity exceeded                        */
+  TAC_ENV_NONFINITE = 4,      /* NaN/Inf in the Newton system                                   */
+  TAC_ENV_BAD_STATE = 5,      /* tac_set_state: inverted tet (det F <= 0) or a contact distance <= 0 */
+  TAC_ENV_DISABLED = 6        /* failed earlier; waits for tac_set_state                         */
+} tac_env_status;
+
+typedef enum { TAC_BODY_DYNAMIC = 0, TAC_BODY_KINEMATIC = 1, TAC_BODY_STATIC = 2 } tac_body_kind;
+
+/* A tetrahedral gel pad G_i.  rest_pos is in the pad (sensor) frame.  mount_T maps
+ * pad frame → mount-body frame (^{l_j}_{G_i}T): x_link = t + R·x_pad.  Attached vertices (∂⁻G) are
+ * driven by the AL to the mount body's target; coated vertices (∂⁺G) are read out. */
+typedef struct {
+  int32_t n_verts, n_tets;
+  const double* rest_pos;        /* [n_verts][3]                                  */
+  const int32_t* tets;           /* [n_tets][4], any orientation (fixed internally) */
+  double youngs, poisson, density;
+  int32_t mount_body;            /* affine body index, or -1 (free soft body: mount_T = world pose) */
+  double mount_T[12];            /* t[3], R[3][3] row-major                       */
+  int32_t n_attached; const int32_t* attached;     /* ∂⁻G vertex ids            */
+  int32_t n_coated;   const int32_t* coated;       /* ∂⁺G vertex ids            */
+  int32_t n_markers;  const int32_t* marker_tri;   /* [n_markers][3] vertex ids */
+  const double* marker_bary;                       /* [n_markers][3], Σα = 1    */
+} tac_soft_desc;
+
+/* An ABD body: closed, outward-oriented triangle surface in its body frame. */
+typedef struct {
+  int32_t n_verts, n_tris;
+  const double* rest_pos;        /* [n_verts][3] */
+  const int32_t* tris;           /* [n_tris][3]  */
+  int32_t kind;                  /* tac_body_kind */
+  double density, kappa_s;       /* kg/m^3; orthogonality stiffness κ_s (Pa) */
+} tac_affine_desc;
+
+typedef struct {
+  int32_t n_soft, n_affine;
+  const tac_soft_desc* soft;
+  const tac_affine_desc* affine;
+  const uint8_t* collide;        /* [(n_soft+n_affine)^2] extra body-pair mask (1 = may collide), or NULL */
+  double gravity[3];
+} tac_scene_desc;
+
+/* Solver constants (proposals; the paper fixes none — DESIGN.md §3). */
+typedef struct {
+  double dt, dhat, kappa;        /* Δt (s), barrier range d̂ (m), contact stiffness κ   */
+  double newton_tol_rel;         /* converged iff ‖p‖_emb,∞ ≤ newton_tol_rel · L_env            */
+  double al_tol_rel;             /* AL residual tolerance relative to L_env                     */
+  double pcg_eta;                /* PCG stops at rᵀz ≤ η² r₀ᵀz₀                                 */
+  double armijo_c, accd_s, al_rho0;
+  int32_t max_newton, max_al_rounds, max_pcg, max_accd_iters, ee_mollifier;
+  int32_t cand_capacity_per_env, active_capacity_per_env;
+} tac_config;
+
+typedef struct {
+  int32_t status;                /* tac_env_status of the last step */
+  int32_t newton_iters, pcg_iters, ls_backtracks, n_active, al_rounds, n_candidates;
+  double alpha_min, energy, constraint_residual;
+} tac_env_stats;
+
+struct tac_batch;
+typedef struct tac_batch tac_batch;
+
+/* Bytes of device workspace a batch of n_envs needs. */
+tac_status tac_workspace_size(const tac_scene_desc* scene, int32_t n_envs, const tac_config* cfg, size_t* bytes);
+
+/* Validate and pre-process the template (orientation, D_m⁻¹, lumped masses, surfaces, rest areas,
+ * M^y, sparsity pattern and gather maps), carve `workspace` and upload.  Synchronises `stream`. */
+tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_envs, const tac_config* cfg, int32_t device,
+                            void* workspace, size_t ws_bytes, void* stream, tac_batch** out);
+tac_status tac_batch_destroy(tac_batch* b);
+
+/* Template sizes: [0]=soft verts V, [1]=tets, [2]=affine bodies NA, [3]=kinematic NK,
+ * [4]=coated verts total, [5]=markers total, [6]=DoFs per env n, [7]=all contact vertices,
+ * [8]=surface triangles, [9]=surface edges. */
+tac_status tac_batch_dims(const tac_batch* b, int32_t dims[10]);
+
+/* Set the state of envs [env0, env0+n): x [n][V][3], xdot [n][V][3] (NULL → 0), y [n][NA][12],
+ * ydot [n][NA][12] (NULL → 0).  Resets per-env status and derives L_env (bounding-box diagonal of
+ * all vertices).  Validates every env (det F > 0 for all tets, all contact distances > 0); envs
+ * failing get TAC_ENV_BAD_STATE in env_status[n] (host or device, may be NULL). Host-blocking. */
+tac_status tac_set_state(tac_batch* b, int32_t env0, int32_t n, const double* x, const double* xdot,
+                         const double* y, const double* ydot, uint8_t* env_status, void* stream);
+
+/* Kinematic targets s^y for the next step, y_kin [n][NK][12] in kinematic-body order; the
+ * attached-vertex targets s^x follow from the mount links. */
+tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, const double* y_kin, void* stream);
+
+/* Advance every enabled env by n_steps time steps.  Host-blocking.  env_status [E] (may be NULL). */
+tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_status, void* stream);
+
+tac_status tac_get_state(tac_batch* b, int32_t env0, int32_t n, double* x, double* xdot, double* y,
+                         double* ydot, void* stream);
+
+/* Gel deformation in the pad (sensor) frame from the mount link's CURRENT pose:
+ * coated_disp [n][Σcoated][3], marker_pos [n][Σmarkers][3] (world), marker_flow [n][Σmarkers][3]
+ * (sensor frame).  Any pointer may be NULL. */
+tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_t n, double* coated_disp,
+                                   double* marker_pos, double* marker_flow, void* stream);
+
+tac_status tac_get_stats(tac_batch* b, tac_env_stats* out /* [E] host */, void* stream);
+
+const char* tac_last_error(void);
+
+/* ---- parity hooks (exported, test-only; host buffers) ---------------------------------------
+ * tac_debug_eval: at (x [V][3], y [NA][12]) of env `env`, with x̃/ỹ from the env's last set_state
+ * and kinematic targets from the last set_targets, and AL multipliers lam_att [NC][3],
+ * lam_kin [NK][12] (NULL → 0) and penalty rho (≤ 0 → al_rho0): the six energy terms
+ * e_terms[6] = {inertia, elastic, ortho, gravity, barrier, AL}, the gradient grad [n] over
+ * q = [x; y of non-static bodies] and hv = H·v_in [n] with H the PSD-projected Hessian (any
+ * output may be NULL).  The active set is recomputed at (x, y) through the spatial hash. */
+tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x, const double* y, const double* lam_att,
+                          const double* lam_kin, double rho, const double* v_in, double* e_terms, double* grad,
+                          double* hv, void* stream);
+/* Active pairs at (x, y): rows (kind, a, b) in canonical order. */
+tac_status tac_debug_active_pairs(tac_batch* b, int32_t env, const double* x, const double* y, int32_t* pairs,
+                                  int32_t cap, int32_t* count, void* stream);
+/* Candidate pairs (swept boxes over [q, q + p], p [n] or NULL for static) in canonical order. */
+tac_status tac_debug_candidates(tac_batch* b, int32_t env, const double* x, const double* y, const double* p,
+                                int32_t* pairs, int32_t cap, int32_t* count, void* stream);
+/* α_max = min(1, min ACCD over the swept candidates) along p [n]. */
+tac_status tac_debug_accd(tac_batch* b, int32_t env, const double* x, const double* y, const double* p,
+                          double* alpha, void* stream);
+/* Block-Jacobi PCG solve of H p = −g at (x, y) (AL as in tac_debug_eval): p [n], iterations. */
+tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, const double* y, double* p,
+                         int32_t* iters, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TACCEL_H */

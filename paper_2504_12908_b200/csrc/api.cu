@@ -1,0 +1,887 @@
+// api.cu — host side of libtaccel_cuda.so: the C ABI of include/taccel.h.
+// Template preparation (orientation, D_m⁻¹, lumped masses, canonical surfaces, rest areas, M^y by
+// closed-form tet moments, BSR pattern + gather lists), workspace carving, and the host-driven
+// Newton loop (one 4-byte device→host flag per Newton iteration is the only crossing).
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/taccel.h"
+#include "impl.cuh"
+#include "launch.h"
+
+using namespace tac;
+
+static thread_local std::string g_err;
+static tac_status fail(tac_status s, const std::string& msg) { g_err = msg; return s; }
+#define CUDA_TRY(x)                                                                         \
+  do {                                                                                      \
+    cudaError_t _e = (x);                                                                   \
+    if (_e != cudaSuccess) return fail(TAC_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+extern "C" const char* tac_last_error(void) { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------------------------
+// host template
+// ---------------------------------------------------------------------------------------------
+struct HostT {
+  int V = 0, T = 0, NA = 0, ND = 0, NVall = 0, NSV = 0, NT = 0, NE = 0, NEs = 0, NC = 0, NK = 0, NB = 0, n = 0;
+  int npads = 0, NCOAT = 0, NMARK = 0;
+  double cell = 0;
+  std::vector<int> tets;            // T*4
+  std::vector<double> Dmi, vol, mu, lam, mass, Xrest;
+  std::vector<int> sedge, vadj_ptr, vadj, vdiag_ptr, vdiag, eblk_ptr, eblk;
+  std::vector<int> body_kind, dof_slot, dof_body;
+  std::vector<double> My, bmass, bs1, bvol, bkappa;
+  std::vector<int> vert_body, vert_aff;
+  std::vector<double> vert_xbar;
+  std::vector<int> sverts, tris, tri_body, edges, edge_body;
+  std::vector<double> A_v, A_e, elen2;
+  std::vector<unsigned char> allowed;
+  std::vector<int> att_vert, att_body, att_of_vert, kin_body, kin_of_body, affv_list, kin_vlist;
+  std::vector<double> att_local;
+  std::vector<int> coat_vert, coat_pad, mark_tri, mark_pad, pad_mount;
+  std::vector<double> mark_bary, pad_T;
+};
+
+static std::array<double, 3> sub3(const double* a, const double* b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
+static std::array<double, 3> cross3(std::array<double, 3> a, std::array<double, 3> b) {
+  return {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+}
+static double dot3(std::array<double, 3> a, std::array<double, 3> b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+static std::array<int, 3> canon_tri(int a, int b, int c) {
+  if (a <= b && a <= c) return {a, b, c};
+  if (b <= a && b <= c) return {b, c, a};
+  return {c, a, b};
+}
+static std::array<int, 3> sorted3(std::array<int, 3> t) { std::sort(t.begin(), t.end()); return t; }
+
+static void sort_canonical(std::vector<std::array<int, 3>>& tris) {
+  std::stable_sort(tris.begin(), tris.end(), [](const std::array<int, 3>& x, const std::array<int, 3>& y) {
+    return sorted3(x) < sorted3(y);
+  });
+}
+static std::vector<std::array<int, 2>> tri_edges(const std::vector<std::array<int, 3>>& tris) {
+  std::vector<std::array<int, 2>> e;
+  for (auto& t : tris)
+    for (int i = 0; i < 3; ++i) {
+      int a = t[i], b = t[(i + 1) % 3];
+      e.push_back({std::min(a, b), std::max(a, b)});
+    }
+  std::sort(e.begin(), e.end());
+  e.erase(std::unique(e.begin(), e.end()), e.end());
+  return e;
+}
+
+// closed-form moments of the solid bounded by an outward triangle surface: for each signed tet
+// (0, a, b, c): V = a·(b×c)/6, ∫x = V(a+b+c)/4, ∫xxᵀ = V/20 (Σ v vᵀ + s sᵀ), s = a+b+c
+static void body_moments(const double* X, const std::vector<std::array<int, 3>>& tris, double rho, double* vol,
+                         double* mass, double* s1, double* My) {
+  double V = 0, S1[3] = {0, 0, 0}, S2[9] = {0};
+  for (auto& t : tris) {
+    const double *a = X + 3 * t[0], *b = X + 3 * t[1], *c = X + 3 * t[2];
+    double v = (a[0] * (b[1] * c[2] - b[2] * c[1]) - a[1] * (b[0] * c[2] - b[2] * c[0]) + a[2] * (b[0] * c[1] - b[1] * c[0])) / 6.0;
+    V += v;
+    double s[3];
+    for (int i = 0; i < 3; ++i) { s[i] = a[i] + b[i] + c[i]; S1[i] += v * s[i] / 4.0; }
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) S2[3 * i + j] += v / 20.0 * (a[i] * a[j] + b[i] * b[j] + c[i] * c[j] + s[i] * s[j]);
+  }
+  *vol = V;
+  *mass = rho * V;
+  for (int i = 0; i < 3; ++i) s1[i] = rho * S1[i];
+  // M^y = ∫ρ JᵀJ with y = (t, A row-major): tt = m I, t_i–A_ij = s1_j, A_ij–A_ik = S2_jk
+  for (int i = 0; i < 144; ++i) My[i] = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    My[12 * i + i] = rho * V;
+    for (int j = 0; j < 3; ++j) {
+      My[12 * i + 3 + 3 * i + j] = rho * S1[j];
+      My[12 * (3 + 3 * i + j) + i] = rho * S1[j];
+      for (int k = 0; k < 3; ++k) My[12 * (3 + 3 * i + j) + 3 + 3 * i + k] = rho * S2[3 * j + k];
+    }
+  }
+}
+
+static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg, HostT& H) {
+  if (!sc || !cfg) return fail(TAC_E_INVALID, "null scene or config");
+  const int ns = sc->n_soft, na = sc->n_affine;
+  H.NA = na;
+  H.npads = ns;
+  H.NB = ns + na;
+  // ---- soft ----
+  std::vector<std::vector<std::array<int, 3>>> soft_tris(ns);
+  int off = 0;
+  for (int p = 0; p < ns; ++p) {
+    const tac_soft_desc& S = sc->soft[p];
+    if (S.n_verts <= 0 || S.n_tets <= 0 || !S.rest_pos || !S.tets) return fail(TAC_E_INVALID, "empty soft body");
+    if (S.mount_body >= na) return fail(TAC_E_INVALID, "mount_body out of range");
+    double mu = S.youngs / (2.0 * (1.0 + S.poisson));
+    double lam = S.youngs * S.poisson / ((1.0 + S.poisson) * (1.0 - 2.0 * S.poisson));
+    std::vector<double> m(S.n_verts, 0.0);
+    std::map<std::array<int, 3>, std::pair<int, std::array<int, 3>>> faces;
+    for (int t = 0; t < S.n_tets; ++t) {
+      int v[4];
+      for (int k = 0; k < 4; ++k) {
+        v[k] = S.tets[4 * t + k];
+        if (v[k] < 0 || v[k] >= S.n_verts) return fail(TAC_E_INVALID, "tet index out of range");
+      }
+      const double* X = S.rest_pos;
+      auto d1 = sub3(X + 3 * v[1], X + 3 * v[0]), d2 = sub3(X + 3 * v[2], X + 3 * v[0]), d3 = sub3(X + 3 * v[3], X + 3 * v[0]);
+      double det = dot3(d1, cross3(d2, d3));
+      if (std::fabs(det / 6.0) < 1e-15)
+        return fail(TAC_E_VALIDATION, "degenerate tet " + std::to_string(t) + " of soft body " + std::to_string(p));
+      if (det < 0) std::swap(v[1], v[2]);
+      d1 = sub3(X + 3 * v[1], X + 3 * v[0]); d2 = sub3(X + 3 * v[2], X + 3 * v[0]); d3 = sub3(X + 3 * v[3], X + 3 * v[0]);
+      double Dm[9] = {d1[0], d2[0], d3[0], d1[1], d2[1], d3[1], d1[2], d2[2], d3[2]};
+      double Di[9];
+      inv33(Dm, Di);
+      double vol = det33(Dm) / 6.0;
+      for (int k = 0; k < 4; ++k) { H.tets.push_back(off + v[k]); m[v[k]] += S.density * vol / 4.0; }
+      for (int i = 0; i < 9; ++i) H.Dmi.push_back(Di[i]);
+      H.vol.push_back(vol);
+      H.mu.push_back(mu);
+      H.lam.push_back(lam);
+      const int fl[4][3] = {{v[0], v[2], v[1]}, {v[0], v[1], v[3]}, {v[0], v[3], v[2]}, {v[1], v[2], v[3]}};
+      for (auto& f : fl) {
+        auto key = sorted3({f[0], f[1], f[2]});
+        auto it = faces.find(key);
+        if (it == faces.end()) faces[key] = {1, canon_tri(f[0] + off, f[1] + off, f[2] + off)};
+        else it->second.first += 1;
+      }
+    }
+    for (auto& kv : faces)
+      if (kv.second.first == 1) soft_tris[p].push_back(kv.second.second);
+    sort_canonical(soft_tris[p]);
+    for (int i = 0; i < S.n_verts; ++i) {
+      H.mass.push_back(m[i]);
+      for (int c = 0; c < 3; ++c) H.Xrest.push_back(S.rest_pos[3 * i + c]);
+    }
+    off += S.n_verts;
+  }
+  H.V = off;
+  H.T = (int)H.vol.size();
+  if (H.V > 8000) return fail(TAC_E_CAPACITY, "more than 8000 soft vertices per env");
+  // ---- affine ----
+  int nd = 0;
+  for (int b = 0; b < na; ++b) {
+    const tac_affine_desc& A = sc->affine[b];
+    if (A.n_verts <= 0 || A.n_tris <= 0 || !A.rest_pos || !A.tris) return fail(TAC_E_INVALID, "empty affine body");
+    H.body_kind.push_back(A.kind);
+    H.dof_slot.push_back(A.kind == TAC_BODY_STATIC ? -1 : nd);
+    if (A.kind != TAC_BODY_STATIC) { H.dof_body.push_back(b); ++nd; }
+    H.bkappa.push_back(A.kappa_s);
+  }
+  H.ND = nd;
+  H.n = 3 * H.V + 12 * nd;
+  // ---- global contact primitives ----
+  H.NVall = H.V;
+  for (int b = 0; b < na; ++b) H.NVall += sc->affine[b].n_verts;
+  H.vert_body.assign(H.NVall, 0);
+  H.vert_aff.assign(H.NVall, -1);
+  H.vert_xbar.assign(3 * (size_t)H.NVall, 0.0);
+  {
+    int o = 0;
+    for (int p = 0; p < ns; ++p)
+      for (int i = 0; i < sc->soft[p].n_verts; ++i, ++o) {
+        H.vert_body[o] = p;
+        for (int c = 0; c < 3; ++c) H.vert_xbar[3 * o + c] = sc->soft[p].rest_pos[3 * i + c];
+      }
+  }
+  std::vector<std::array<int, 3>> all_tris;
+  std::vector<std::array<int, 2>> all_edges;
+  for (int p = 0; p < ns; ++p) {
+    for (auto& t : soft_tris[p]) { all_tris.push_back(t); H.tri_body.push_back(p); }
+    for (auto& e : tri_edges(soft_tris[p])) { all_edges.push_back(e); H.edge_body.push_back(p); }
+  }
+  H.My.assign(144 * (size_t)na, 0.0);
+  H.bmass.assign(na, 0.0);
+  H.bs1.assign(3 * na, 0.0);
+  H.bvol.assign(na, 0.0);
+  int o = H.V;
+  for (int b = 0; b < na; ++b) {
+    const tac_affine_desc& A = sc->affine[b];
+    std::vector<std::array<int, 3>> tl, tg;
+    for (int t = 0; t < A.n_tris; ++t) {
+      int a0 = A.tris[3 * t], a1 = A.tris[3 * t + 1], a2 = A.tris[3 * t + 2];
+      if (a0 < 0 || a1 < 0 || a2 < 0 || a0 >= A.n_verts || a1 >= A.n_verts || a2 >= A.n_verts)
+        return fail(TAC_E_INVALID, "triangle index out of range");
+      auto n = cross3(sub3(A.rest_pos + 3 * a1, A.rest_pos + 3 * a0), sub3(A.rest_pos + 3 * a2, A.rest_pos + 3 * a0));
+      if (0.5 * std::sqrt(dot3(n, n)) < 1e-12)
+        return fail(TAC_E_VALIDATION, "degenerate triangle " + std::to_string(t) + " of affine body " + std::to_string(b));
+      tl.push_back({a0, a1, a2});
+      tg.push_back(canon_tri(a0 + o, a1 + o, a2 + o));
+    }
+    body_moments(A.rest_pos, tl, A.density, &H.bvol[b], &H.bmass[b], &H.bs1[3 * b], &H.My[144 * (size_t)b]);
+    if (!(H.bvol[b] > 0)) return fail(TAC_E_VALIDATION, "affine body " + std::to_string(b) + " has non-positive volume");
+    for (int i = 0; i < A.n_verts; ++i) {
+      H.vert_body[o + i] = ns + b;
+      H.vert_aff[o + i] = b;
+      for (int c = 0; c < 3; ++c) H.vert_xbar[3 * (o + i) + c] = A.rest_pos[3 * i + c];
+    }
+    sort_canonical(tg);
+    for (auto& t : tg) { all_tris.push_back(t); H.tri_body.push_back(ns + b); }
+    for (auto& e : tri_edges(tg)) { all_edges.push_back(e); H.edge_body.push_back(ns + b); }
+    o += A.n_verts;
+  }
+  H.NT = (int)all_tris.size();
+  H.NE = (int)all_edges.size();
+  for (auto& t : all_tris) for (int k = 0; k < 3; ++k) H.tris.push_back(t[k]);
+  for (auto& e : all_edges) for (int k = 0; k < 2; ++k) H.edges.push_back(e[k]);
+  {
+    std::vector<char> is_s(H.NVall, 0);
+    for (int v : H.tris) is_s[v] = 1;
+    for (int v = 0; v < H.NVall; ++v) if (is_s[v]) H.sverts.push_back(v);
+    H.NSV = (int)H.sverts.size();
+  }
+  // rest areas A_v, A_e (1/3 of incident rest triangle areas) and rest edge lengths
+  H.A_v.assign(H.NVall, 0.0);
+  H.A_e.assign(H.NE, 0.0);
+  {
+    std::map<std::array<int, 2>, int> eid;
+    for (int i = 0; i < H.NE; ++i) eid[all_edges[i]] = i;
+    for (auto& t : all_tris) {
+      const double* X = H.vert_xbar.data();
+      auto n = cross3(sub3(X + 3 * t[1], X + 3 * t[0]), sub3(X + 3 * t[2], X + 3 * t[0]));
+      double a = 0.5 * std::sqrt(dot3(n, n));
+      if (a < 1e-12) return fail(TAC_E_VALIDATION, "degenerate surface triangle");
+      for (int k = 0; k < 3; ++k) {
+        H.A_v[t[k]] += a / 3.0;
+        int u = t[k], w = t[(k + 1) % 3];
+        H.A_e[eid[{std::min(u, w), std::max(u, w)}]] += a / 3.0;
+      }
+    }
+    std::vector<double> len;
+    for (auto& e : all_edges) {
+      auto d = sub3(&H.vert_xbar[3 * e[1]], &H.vert_xbar[3 * e[0]]);
+      H.elen2.push_back(dot3(d, d));
+      len.push_back(std::sqrt(dot3(d, d)));
+    }
+    std::sort(len.begin(), len.end());
+    double med = len.empty() ? 1.0 : len[len.size() / 2];
+    H.cell = std::max(2.0 * cfg->dhat, med);
+  }
+  // body-pair mask (reading R8)
+  H.allowed.assign((size_t)H.NB * H.NB, 0);
+  for (int a = 0; a < H.NB; ++a)
+    for (int b = 0; b < H.NB; ++b) {
+      bool ok = a != b;
+      for (int r = 0; r < 2 && ok; ++r) {
+        int s = r ? b : a, t = r ? a : b;
+        if (s < ns && sc->soft[s].mount_body >= 0 && ns + sc->soft[s].mount_body == t) ok = false;
+      }
+      int ka = a < ns ? 0 : sc->affine[a - ns].kind, kb = b < ns ? 0 : sc->affine[b - ns].kind;
+      if (ka != 0 && kb != 0) ok = false;
+      if (sc->collide && !sc->collide[(size_t)a * H.NB + b]) ok = false;
+      H.allowed[(size_t)a * H.NB + b] = ok ? 1 : 0;
+    }
+  // soft BSR pattern: undirected tet edges, vertex adjacency, element→block gather lists
+  {
+    std::vector<std::array<int, 2>> se;
+    for (int t = 0; t < H.T; ++t)
+      for (int a = 0; a < 4; ++a)
+        for (int b = a + 1; b < 4; ++b) {
+          int u = H.tets[4 * t + a], w = H.tets[4 * t + b];
+          se.push_back({std::min(u, w), std::max(u, w)});
+        }
+    std::sort(se.begin(), se.end());
+    se.erase(std::unique(se.begin(), se.end()), se.end());
+    H.NEs = (int)se.size();
+    std::map<std::array<int, 2>, int> sid;
+    for (int i = 0; i < H.NEs; ++i) { sid[se[i]] = i; H.sedge.push_back(se[i][0]); H.sedge.push_back(se[i][1]); }
+    std::vector<std::vector<int>> vadj(H.V), vdiag(H.V), eblk(H.NEs);
+    for (int i = 0; i < H.NEs; ++i) { vadj[se[i][0]].push_back(2 * i); vadj[se[i][1]].push_back(2 * i + 1); }
+    for (int t = 0; t < H.T; ++t)
+      for (int a = 0; a < 4; ++a) {
+        vdiag[H.tets[4 * t + a]].push_back(4 * t + a);
+        for (int b = 0; b < 4; ++b) {
+          int u = H.tets[4 * t + a], w = H.tets[4 * t + b];
+          if (u < w) eblk[sid[{u, w}]].push_back(16 * t + 4 * a + b);
+        }
+      }
+    auto flat = [](std::vector<std::vector<int>>& L, std::vector<int>& ptr, std::vector<int>& ent) {
+      ptr.assign(1, 0);
+      for (auto& l : L) { ent.insert(ent.end(), l.begin(), l.end()); ptr.push_back((int)ent.size()); }
+    };
+    flat(vadj, H.vadj_ptr, H.vadj);
+    flat(vdiag, H.vdiag_ptr, H.vdiag);
+    flat(eblk, H.eblk_ptr, H.eblk);
+  }
+  // constraints: ∂⁻G vertices and kinematic bodies
+  H.att_of_vert.assign(H.V, -1);
+  {
+    int off2 = 0;
+    for (int p = 0; p < ns; ++p) {
+      const tac_soft_desc& S = sc->soft[p];
+      if (S.mount_body >= 0)
+        for (int i = 0; i < S.n_attached; ++i) {
+          int v = S.attached[i];
+          if (v < 0 || v >= S.n_verts) return fail(TAC_E_INVALID, "attached vertex out of range");
+          const double* X = S.rest_pos + 3 * v;
+          const double* t = S.mount_T;
+          const double* R = S.mount_T + 3;
+          H.att_of_vert[off2 + v] = (int)H.att_vert.size();
+          H.att_vert.push_back(off2 + v);
+          H.att_body.push_back(S.mount_body);
+          for (int r = 0; r < 3; ++r) H.att_local.push_back(t[r] + R[3 * r] * X[0] + R[3 * r + 1] * X[1] + R[3 * r + 2] * X[2]);
+        }
+      for (int i = 0; i < S.n_coated; ++i) { H.coat_vert.push_back(off2 + S.coated[i]); H.coat_pad.push_back(p); }
+      for (int i = 0; i < S.n_markers; ++i) {
+        for (int k = 0; k < 3; ++k) { H.mark_tri.push_back(off2 + S.marker_tri[3 * i + k]); H.mark_bary.push_back(S.marker_bary[3 * i + k]); }
+        H.mark_pad.push_back(p);
+      }
+      H.pad_mount.push_back(S.mount_body);
+      for (int k = 0; k < 12; ++k) H.pad_T.push_back(S.mount_T[k]);
+      off2 += S.n_verts;
+    }
+  }
+  H.NC = (int)H.att_vert.size();
+  H.NCOAT = (int)H.coat_vert.size();
+  H.NMARK = (int)H.mark_pad.size();
+  H.kin_of_body.assign(na, -1);
+  for (int b = 0; b < na; ++b)
+    if (sc->affine[b].kind == TAC_BODY_KINEMATIC) { H.kin_of_body[b] = (int)H.kin_body.size(); H.kin_body.push_back(b); }
+  H.NK = (int)H.kin_body.size();
+  for (int gv = H.V; gv < H.NVall; ++gv) {
+    int b = H.vert_aff[gv];
+    if (H.dof_slot[b] >= 0) H.affv_list.push_back(gv);
+    if (H.kin_of_body[b] >= 0) H.kin_vlist.push_back(gv);
+  }
+  if (H.NT + H.NE >= (1 << 29)) return fail(TAC_E_CAPACITY, "too many primitives");
+  return TAC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// workspace layout
+// ---------------------------------------------------------------------------------------------
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T) + 16;
+    return p;
+  }
+};
+
+struct tac_batch {
+  Dev D;
+  HostT H;
+  int device = 0;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  int* h_flag = nullptr;  // pinned
+  std::vector<EnvCtl> hctl;
+};
+
+static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
+  auto ti = [&](const std::vector<int>& v) { return C.take<int>(std::max<size_t>(v.size(), 1)); };
+  auto td = [&](const std::vector<double>& v) { return C.take<double>(std::max<size_t>(v.size(), 1)); };
+  D.tets = ti(H.tets); D.Dmi = td(H.Dmi); D.vol = td(H.vol); D.mu = td(H.mu); D.lam = td(H.lam); D.mass = td(H.mass);
+  D.sedge = ti(H.sedge); D.vadj_ptr = ti(H.vadj_ptr); D.vadj = ti(H.vadj); D.vdiag_ptr = ti(H.vdiag_ptr);
+  D.vdiag = ti(H.vdiag); D.eblk_ptr = ti(H.eblk_ptr); D.eblk = ti(H.eblk);
+  D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My);
+  D.bmass = td(H.bmass); D.bs1 = td(H.bs1); D.bvol = td(H.bvol); D.bkappa = td(H.bkappa);
+  D.vert_body = ti(H.vert_body); D.vert_aff = ti(H.vert_aff); D.vert_xbar = td(H.vert_xbar);
+  D.sverts = ti(H.sverts); D.tris = ti(H.tris); D.tri_body = ti(H.tri_body); D.edges = ti(H.edges);
+  D.edge_body = ti(H.edge_body); D.A_v = td(H.A_v); D.A_e = td(H.A_e); D.elen2 = td(H.elen2);
+  D.allowed = C.take<unsigned char>(std::max<size_t>(H.allowed.size(), 1));
+  D.att_vert = ti(H.att_vert); D.att_body = ti(H.att_body); D.att_local = td(H.att_local);
+  D.att_of_vert = ti(H.att_of_vert); D.kin_body = ti(H.kin_body); D.kin_of_body = ti(H.kin_of_body);
+  D.affv_list = ti(H.affv_list); D.kin_vlist = ti(H.kin_vlist);
+  D.coat_vert = ti(H.coat_vert); D.coat_pad = ti(H.coat_pad); D.mark_tri = ti(H.mark_tri);
+  D.mark_bary = td(H.mark_bary); D.mark_pad = ti(H.mark_pad); D.pad_mount = ti(H.pad_mount);
+  D.pad_T = td(H.pad_T); D.Xrest = td(H.Xrest);
+  const size_t e = (size_t)E, n = H.n;
+  D.ctl = C.take<EnvCtl>(e);
+  D.q = C.take<double>(e * n); D.qn = C.take<double>(e * n); D.vel = C.take<double>(e * n);
+  D.qt = C.take<double>(e * n); D.g = C.take<double>(e * n); D.p = C.take<double>(e * n);
+  D.r = C.take<double>(e * n); D.z = C.take<double>(e * n); D.dd = C.take<double>(e * n); D.Ad = C.take<double>(e * n);
+  D.ystat = C.take<double>(e * H.NA * 12); D.ystage = C.take<double>(e * H.NA * 12);
+  D.s_att = C.take<double>(e * H.NC * 3 + 1); D.lam_att = C.take<double>(e * H.NC * 3 + 1);
+  D.s_kin = C.take<double>(e * H.NK * 12 + 1); D.lam_kin = C.take<double>(e * H.NK * 12 + 1);
+  D.ykin = C.take<double>(e * H.NK * 12 + 1);
+  D.P = C.take<double>(e * H.NVall * 3); D.Pd = C.take<double>(e * H.NVall * 3);
+  D.Hd = C.take<double>(e * H.V * 9 + 1); D.Ho = C.take<double>(e * H.NEs * 9 + 1);
+  D.Hb = C.take<double>(e * H.ND * 144 + 1); D.Pinv_s = C.take<double>(e * H.V * 9 + 1);
+  D.Pinv_b = C.take<double>(e * H.ND * 144 + 1);
+  D.tetbuf = C.take<double>(e * TETBUF * H.T + 1);
+  D.cand_a = C.take<int>(e * D.cand_cap); D.cand_b = C.take<int>(e * D.cand_cap);
+  D.ent = C.take<int>(e * D.ent_cap * 2); D.big = C.take<int>(e * BIG_CAP);
+  D.act_info = C.take<int>(e * D.act_cap * 4); D.act_vid = C.take<int>(e * D.act_cap * 4);
+  D.act_g = C.take<double>(e * D.act_cap * 12); D.act_H = C.take<double>(e * D.act_cap * PH);
+  D.act_out = C.take<double>(e * D.act_cap * 12);
+  D.cptr = C.take<int>(e * (H.V + 1)); D.clist = C.take<int>(e * 4 * D.act_cap);
+  D.bptr = C.take<int>(e * (H.ND + 1)); D.blist = C.take<int>(e * 4 * D.act_cap);
+  D.eterm = C.take<double>(e * 8);
+  D.out_coat = C.take<double>(e * H.NCOAT * 3 + 1); D.out_mpos = C.take<double>(e * H.NMARK * 3 + 1);
+  D.out_mflow = C.take<double>(e * H.NMARK * 3 + 1);
+  D.any_active = C.take<int>(1);
+  return C.off + 256;
+}
+
+static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, const tac_scene_desc* sc) {
+  D.E = E; D.V = H.V; D.T = H.T; D.NA = H.NA; D.ND = H.ND; D.NVall = H.NVall; D.NSV = H.NSV; D.NT = H.NT;
+  D.NE = H.NE; D.NEs = H.NEs; D.NC = H.NC; D.NK = H.NK; D.NB = H.NB; D.n = H.n; D.npads = H.npads;
+  D.NCOAT = H.NCOAT; D.NMARK = H.NMARK; D.NAV = (int)H.affv_list.size(); D.NKV = (int)H.kin_vlist.size();
+  D.cand_cap = std::max(cfg->cand_capacity_per_env, 64);
+  D.act_cap = std::max(cfg->active_capacity_per_env, 16);
+  D.ent_cap = 16 * (H.NT + H.NE) + 4096;
+  D.dt = cfg->dt; D.dhat = cfg->dhat; D.kappa = cfg->kappa; D.tolN = cfg->newton_tol_rel; D.tolAL = cfg->al_tol_rel;
+  D.eta = cfg->pcg_eta; D.armijo = cfg->armijo_c; D.accd_s = cfg->accd_s; D.rho0 = cfg->al_rho0; D.cell = H.cell;
+  D.max_newton = cfg->max_newton; D.max_al = cfg->max_al_rounds; D.max_pcg = cfg->max_pcg;
+  D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier;
+  for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
+}
+
+static tac_status check_cfg(const tac_config* c) {
+  if (!(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
+      c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1))
+    return fail(TAC_E_INVALID, "invalid tac_config");
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_workspace_size(const tac_scene_desc* scene, int32_t n_envs, const tac_config* cfg, size_t* bytes) {
+  if (!scene || !cfg || !bytes || n_envs <= 0) return fail(TAC_E_INVALID, "null argument or n_envs <= 0");
+  tac_status s = check_cfg(cfg);
+  if (s) return s;
+  HostT H;
+  s = build_template(scene, cfg, H);
+  if (s) return s;
+  Dev D{};
+  fill_dims(D, H, cfg, n_envs, scene);
+  Carver C{nullptr};
+  *bytes = layout(C, D, H, n_envs);
+  return TAC_OK;
+}
+
+template <class T>
+static cudaError_t up(const T* dst, const std::vector<T>& v, cudaStream_t s) {
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpyAsync((void*)dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
+extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_envs, const tac_config* cfg, int32_t device,
+                                       void* workspace, size_t ws_bytes, void* stream, tac_batch** out) {
+  if (!scene || !cfg || !out || !workspace || n_envs <= 0) return fail(TAC_E_INVALID, "null argument or n_envs <= 0");
+  if (((uintptr_t)workspace) & 255) return fail(TAC_E_WORKSPACE, "workspace must be 256-byte aligned");
+  tac_status s = check_cfg(cfg);
+  if (s) return s;
+  CUDA_TRY(cudaSetDevice(device));
+  tac_batch* b = new tac_batch();
+  b->device = device;
+  s = build_template(scene, cfg, b->H);
+  if (s) { delete b; return s; }
+  fill_dims(b->D, b->H, cfg, n_envs, scene);
+  Carver C{(char*)workspace};
+  size_t need = layout(C, b->D, b->H, n_envs);
+  if (need > ws_bytes) {
+    delete b;
+    return fail(TAC_E_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  }
+  b->ws = (char*)workspace;
+  b->ws_bytes = ws_bytes;
+  cudaStream_t st = (cudaStream_t)stream;
+  const HostT& H = b->H;
+  Dev& D = b->D;
+  cudaError_t e = init_tables();
+  if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, need, st);
+#define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
+  UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
+  UP(eblk_ptr); UP(eblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
+  UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
+  UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
+  UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
+  UP(mark_bary); UP(mark_pad); UP(pad_mount); UP(pad_T); UP(Xrest);
+#undef UP
+  b->hctl.assign(n_envs, EnvCtl{});
+  for (auto& c : b->hctl) { c.phase = PHASE_IDLE; c.disabled = 1; c.status = ENV_DISABLED; c.L = 1.0; c.rho = cfg->al_rho0; }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(D.ctl, b->hctl.data(), sizeof(EnvCtl) * n_envs, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMallocHost(&b->h_flag, sizeof(int));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) { delete b; return fail(TAC_E_CUDA, std::string("create: ") + cudaGetErrorString(e)); }
+  *out = b;
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_batch_destroy(tac_batch* b) {
+  if (!b) return TAC_OK;
+  if (b->h_flag) cudaFreeHost(b->h_flag);
+  delete b;
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_batch_dims(const tac_batch* b, int32_t dims[10]) {
+  if (!b || !dims) return fail(TAC_E_INVALID, "null argument");
+  const HostT& H = b->H;
+  int d[10] = {H.V, H.T, H.NA, H.NK, H.NCOAT, H.NMARK, H.n, H.NVall, H.NT, H.NE};
+  for (int i = 0; i < 10; ++i) dims[i] = d[i];
+  return TAC_OK;
+}
+
+static tac_status check_range(tac_batch* b, int env0, int n) {
+  if (!b) return fail(TAC_E_INVALID, "null batch");
+  if (env0 < 0 || n <= 0 || env0 + n > b->D.E) return fail(TAC_E_INVALID, "env range out of bounds");
+  return TAC_OK;
+}
+
+static tac_status pull_ctl(tac_batch* b, cudaStream_t st) {
+  CUDA_TRY(cudaMemcpyAsync(b->hctl.data(), b->D.ctl, sizeof(EnvCtl) * b->D.E, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TAC_OK;
+}
+
+static tac_status write_status(tac_batch* b, int env0, int n, uint8_t* out, cudaStream_t st) {
+  if (!out) return TAC_OK;
+  std::vector<uint8_t> s(n);
+  for (int i = 0; i < n; ++i) s[i] = (uint8_t)b->hctl[env0 + i].status;
+  CUDA_TRY(cudaMemcpyAsync(out, s.data(), n, cudaMemcpyDefault, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_set_state(tac_batch* b, int32_t env0, int32_t n, const double* x, const double* xdot,
+                                    const double* y, const double* ydot, uint8_t* env_status, void* stream) {
+  tac_status s = check_range(b, env0, n);
+  if (s) return s;
+  if ((!x && b->D.V) || !y) return fail(TAC_E_INVALID, "x and y are required");
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& D = b->D;
+  const size_t pitch = (size_t)D.n * sizeof(double), w = (size_t)3 * D.V * sizeof(double);
+  if (D.V) {
+    CUDA_TRY(cudaMemcpy2DAsync(D.q + (size_t)env0 * D.n, pitch, x, w, w, n, cudaMemcpyDefault, st));
+    if (xdot) CUDA_TRY(cudaMemcpy2DAsync(D.vel + (size_t)env0 * D.n, pitch, xdot, w, w, n, cudaMemcpyDefault, st));
+    else CUDA_TRY(cudaMemset2DAsync(D.vel + (size_t)env0 * D.n, pitch, 0, w, n, st));
+  }
+  const size_t ybytes = (size_t)n * D.NA * 12 * sizeof(double);
+  CUDA_TRY(cudaMemcpyAsync(D.ystage + (size_t)env0 * D.NA * 12, y, ybytes, cudaMemcpyDefault, st));
+  launch_scatter_y(D, env0, n, 0, st);
+  if (ydot) {
+    CUDA_TRY(cudaMemcpyAsync(D.ystage + (size_t)env0 * D.NA * 12, ydot, ybytes, cudaMemcpyDefault, st));
+    launch_scatter_y(D, env0, n, 1, st);
+  } else {
+    launch_scatter_y(D, env0, n, 2, st);
+  }
+  launch_positions(D, env0, n, 0, 1, st);
+  launch_broad(D, env0, n, 0, 1, st);
+  launch_validate(D, env0, n, st);
+  CUDA_TRY(cudaGetLastError());
+  s = pull_ctl(b, st);
+  if (s) return s;
+  return write_status(b, env0, n, env_status, st);
+}
+
+extern "C" tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, const double* y_kin, void* stream) {
+  tac_status s = check_range(b, env0, n);
+  if (s) return s;
+  if (b->D.NK == 0) return TAC_OK;
+  if (!y_kin) return fail(TAC_E_INVALID, "y_kin is null");
+  CUDA_TRY(cudaMemcpyAsync(b->D.ykin + (size_t)env0 * b->D.NK * 12, y_kin, (size_t)n * b->D.NK * 12 * sizeof(double),
+                           cudaMemcpyDefault, (cudaStream_t)stream));
+  return TAC_OK;
+}
+
+static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st) {
+  Dev& D = b->D;
+  launch_positions(D, env0, ne, 0, 0, st);
+  launch_broad(D, env0, ne, 0, 0, st);
+  for (int it = 0; it <= D.max_newton + 1; ++it) {
+    launch_positions(D, env0, ne, 0, 0, st);
+    launch_narrow(D, env0, ne, 0, st);
+    launch_tets(D, env0, ne, 0, st);
+    launch_pairs(D, env0, ne, 0, st);
+    launch_assemble(D, env0, ne, 0, st);
+    launch_pcg(D, env0, ne, 0, st);
+    launch_positions(D, env0, ne, 1, 0, st);
+    launch_broad(D, env0, ne, 1, 0, st);
+    launch_ccd(D, env0, ne, 0, st);
+    launch_linesearch(D, env0, ne, st);
+    CUDA_TRY(cudaMemsetAsync(D.any_active, 0, sizeof(int), st));
+    launch_control(D, env0, ne, st);
+    CUDA_TRY(cudaMemcpyAsync(b->h_flag, D.any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    if (!*b->h_flag) break;
+  }
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_status, void* stream) {
+  if (!b || n_steps < 0) return fail(TAC_E_INVALID, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& D = b->D;
+  bool any_failed = false;
+  for (int s = 0; s < n_steps; ++s) {
+    launch_begin(D, 0, D.E, st);
+    tac_status r = newton_loop(b, 0, D.E, st);
+    if (r) return r;
+    launch_end(D, 0, D.E, st);
+    CUDA_TRY(cudaGetLastError());
+  }
+  tac_status r = pull_ctl(b, st);
+  if (r) return r;
+  for (auto& c : b->hctl)
+    if (c.phase == PHASE_FAILED) any_failed = true;
+  r = write_status(b, 0, D.E, env_status, st);
+  if (r) return r;
+  return any_failed ? fail(TAC_E_ENV_FAILED, "one or more envs failed (see env_status)") : TAC_OK;
+}
+
+extern "C" tac_status tac_get_state(tac_batch* b, int32_t env0, int32_t n, double* x, double* xdot, double* y,
+                                    double* ydot, void* stream) {
+  tac_status s = check_range(b, env0, n);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& D = b->D;
+  const size_t pitch = (size_t)D.n * sizeof(double), w = (size_t)3 * D.V * sizeof(double);
+  if (x && D.V) CUDA_TRY(cudaMemcpy2DAsync(x, w, D.q + (size_t)env0 * D.n, pitch, w, n, cudaMemcpyDefault, st));
+  if (xdot && D.V) CUDA_TRY(cudaMemcpy2DAsync(xdot, w, D.vel + (size_t)env0 * D.n, pitch, w, n, cudaMemcpyDefault, st));
+  const size_t ybytes = (size_t)n * D.NA * 12 * sizeof(double);
+  if (y) {
+    launch_gather_y(D, env0, n, 0, st);
+    CUDA_TRY(cudaMemcpyAsync(y, D.ystage + (size_t)env0 * D.NA * 12, ybytes, cudaMemcpyDefault, st));
+  }
+  if (ydot) {
+    launch_gather_y(D, env0, n, 1, st);
+    CUDA_TRY(cudaMemcpyAsync(ydot, D.ystage + (size_t)env0 * D.NA * 12, ybytes, cudaMemcpyDefault, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_t n, double* coated_disp,
+                                              double* marker_pos, double* marker_flow, void* stream) {
+  tac_status s = check_range(b, env0, n);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& D = b->D;
+  launch_readout(D, env0, n, st);
+  if (coated_disp && D.NCOAT)
+    CUDA_TRY(cudaMemcpyAsync(coated_disp, D.out_coat + (size_t)env0 * D.NCOAT * 3, (size_t)n * D.NCOAT * 3 * 8, cudaMemcpyDefault, st));
+  if (marker_pos && D.NMARK)
+    CUDA_TRY(cudaMemcpyAsync(marker_pos, D.out_mpos + (size_t)env0 * D.NMARK * 3, (size_t)n * D.NMARK * 3 * 8, cudaMemcpyDefault, st));
+  if (marker_flow && D.NMARK)
+    CUDA_TRY(cudaMemcpyAsync(marker_flow, D.out_mflow + (size_t)env0 * D.NMARK * 3, (size_t)n * D.NMARK * 3 * 8, cudaMemcpyDefault, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_get_stats(tac_batch* b, tac_env_stats* out, void* stream) {
+  if (!b || !out) return fail(TAC_E_INVALID, "null argument");
+  tac_status s = pull_ctl(b, (cudaStream_t)stream);
+  if (s) return s;
+  for (int e = 0; e < b->D.E; ++e) {
+    const EnvCtl& c = b->hctl[e];
+    out[e].status = c.status; out[e].newton_iters = c.newton; out[e].pcg_iters = c.pcg; out[e].ls_backtracks = c.ls_bt;
+    out[e].n_active = c.n_act; out[e].al_rounds = c.al_rounds; out[e].n_candidates = c.ncand;
+    out[e].alpha_min = c.alpha_min; out[e].energy = c.energy; out[e].constraint_residual = c.residual;
+  }
+  return TAC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// parity hooks: evaluate one env at a given (x, y) without changing its state
+// ---------------------------------------------------------------------------------------------
+struct DebugScope {
+  tac_batch* b; int e; cudaStream_t st;
+  std::vector<double> q, vel, ystat;
+  EnvCtl ctl;
+  bool ok = false;
+};
+
+static tac_status dbg_enter(DebugScope& S, const double* x, const double* y, const double* lam_att,
+                            const double* lam_kin, double rho) {
+  tac_batch* b = S.b;
+  Dev& D = b->D;
+  const int e = S.e;
+  S.q.resize(D.n); S.vel.resize(D.n); S.ystat.resize((size_t)D.NA * 12);
+  CUDA_TRY(cudaMemcpyAsync(S.q.data(), D.q + (size_t)e * D.n, D.n * 8, cudaMemcpyDeviceToHost, S.st));
+  CUDA_TRY(cudaMemcpyAsync(S.vel.data(), D.vel + (size_t)e * D.n, D.n * 8, cudaMemcpyDeviceToHost, S.st));
+  CUDA_TRY(cudaMemcpyAsync(S.ystat.data(), D.ystat + (size_t)e * D.NA * 12, D.NA * 96, cudaMemcpyDeviceToHost, S.st));
+  CUDA_TRY(cudaMemcpyAsync(&S.ctl, D.ctl + e, sizeof(EnvCtl), cudaMemcpyDeviceToHost, S.st));
+  CUDA_TRY(cudaStreamSynchronize(S.st));
+  S.ok = true;
+  // x̃ = q + Δt v and targets from the env's current state (k_begin), then overwrite the iterate
+  EnvCtl c = S.ctl;
+  c.disabled = 0;
+  CUDA_TRY(cudaMemcpyAsync(D.ctl + e, &c, sizeof(EnvCtl), cudaMemcpyHostToDevice, S.st));
+  launch_begin(D, e, 1, S.st);
+  if (D.V) CUDA_TRY(cudaMemcpyAsync(D.q + (size_t)e * D.n, x, (size_t)3 * D.V * 8, cudaMemcpyHostToDevice, S.st));
+  CUDA_TRY(cudaMemcpyAsync(D.ystage + (size_t)e * D.NA * 12, y, (size_t)D.NA * 96, cudaMemcpyHostToDevice, S.st));
+  launch_scatter_y(D, e, 1, 0, S.st);
+  if (lam_att && D.NC) CUDA_TRY(cudaMemcpyAsync(D.lam_att + (size_t)e * D.NC * 3, lam_att, (size_t)D.NC * 24, cudaMemcpyHostToDevice, S.st));
+  if (lam_kin && D.NK) CUDA_TRY(cudaMemcpyAsync(D.lam_kin + (size_t)e * D.NK * 12, lam_kin, (size_t)D.NK * 96, cudaMemcpyHostToDevice, S.st));
+  if (rho > 0) CUDA_TRY(cudaMemcpyAsync(&D.ctl[e].rho, &rho, sizeof(double), cudaMemcpyHostToDevice, S.st));
+  CUDA_TRY(cudaStreamSynchronize(S.st));
+  return TAC_OK;
+}
+
+static tac_status dbg_leave(DebugScope& S) {
+  if (!S.ok) return TAC_OK;
+  Dev& D = S.b->D;
+  const int e = S.e;
+  CUDA_TRY(cudaMemcpyAsync(D.q + (size_t)e * D.n, S.q.data(), D.n * 8, cudaMemcpyHostToDevice, S.st));
+  CUDA_TRY(cudaMemcpyAsync(D.vel + (size_t)e * D.n, S.vel.data(), D.n * 8, cudaMemcpyHostToDevice, S.st));
+  CUDA_TRY(cudaMemcpyAsync(D.ystat + (size_t)e * D.NA * 12, S.ystat.data(), D.NA * 96, cudaMemcpyHostToDevice, S.st));
+  CUDA_TRY(cudaMemcpyAsync(D.ctl + e, &S.ctl, sizeof(EnvCtl), cudaMemcpyHostToDevice, S.st));
+  CUDA_TRY(cudaStreamSynchronize(S.st));
+  return TAC_OK;
+}
+
+static tac_status dbg_assemble(tac_batch* b, int e, cudaStream_t st) {
+  Dev& D = b->D;
+  launch_positions(D, e, 1, 0, 1, st);
+  launch_broad(D, e, 1, 0, 1, st);
+  launch_narrow(D, e, 1, 1, st);
+  launch_tets(D, e, 1, 1, st);
+  launch_pairs(D, e, 1, 1, st);
+  launch_assemble(D, e, 1, 1, st);
+  CUDA_TRY(cudaGetLastError());
+  return TAC_OK;
+}
+
+#define DBG_CHECK(b, env)                                                        \
+  if (!(b) || (env) < 0 || (env) >= (b)->D.E) return fail(TAC_E_INVALID, "bad env"); \
+  if (!x || !y) return fail(TAC_E_INVALID, "x and y are required");
+
+extern "C" tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x, const double* y, const double* lam_att,
+                                     const double* lam_kin, double rho, const double* v_in, double* e_terms, double* grad,
+                                     double* hv, void* stream) {
+  DBG_CHECK(b, env);
+  DebugScope S{b, env, (cudaStream_t)stream};
+  tac_status s = dbg_enter(S, x, y, lam_att, lam_kin, rho);
+  Dev& D = b->D;
+  if (!s) s = dbg_assemble(b, env, S.st);
+  if (!s && e_terms) {
+    launch_energy(D, env, 1, 0.0, S.st);
+    double t[8];
+    cudaMemcpyAsync(t, D.eterm + (size_t)env * 8, 64, cudaMemcpyDeviceToHost, S.st);
+    cudaStreamSynchronize(S.st);
+    for (int i = 0; i < 6; ++i) e_terms[i] = t[i];
+  }
+  if (!s && grad) {
+    cudaMemcpyAsync(grad, D.g + (size_t)env * D.n, D.n * 8, cudaMemcpyDeviceToHost, S.st);
+    cudaStreamSynchronize(S.st);
+  }
+  if (!s && hv && v_in) {
+    cudaMemcpyAsync(D.dd + (size_t)env * D.n, v_in, D.n * 8, cudaMemcpyHostToDevice, S.st);
+    launch_spmv(D, env, D.dd + (size_t)env * D.n, D.Ad + (size_t)env * D.n, S.st);
+    cudaMemcpyAsync(hv, D.Ad + (size_t)env * D.n, D.n * 8, cudaMemcpyDeviceToHost, S.st);
+    if (cudaStreamSynchronize(S.st) != cudaSuccess) s = fail(TAC_E_CUDA, "debug spmv failed");
+  }
+  if (!s && cudaGetLastError() != cudaSuccess) s = fail(TAC_E_CUDA, "debug eval kernel failed");
+  tac_status s2 = dbg_leave(S);
+  return s ? s : s2;
+}
+
+static tac_status copy_pairs(tac_batch* b, int env, bool active, int32_t* pairs, int32_t cap, int32_t* count, cudaStream_t st) {
+  Dev& D = b->D;
+  EnvCtl c;
+  CUDA_TRY(cudaMemcpyAsync(&c, D.ctl + env, sizeof(EnvCtl), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (c.overflow) return fail(TAC_E_CAPACITY, "pair capacity exceeded");
+  int n = active ? c.n_act : c.ncand;
+  if (count) *count = n;
+  if (!pairs) return TAC_OK;
+  int m = std::min(n, cap);
+  if (active) {
+    std::vector<int> info((size_t)4 * std::max(m, 1));
+    CUDA_TRY(cudaMemcpy(info.data(), D.act_info + (size_t)env * D.act_cap * 4, (size_t)m * 16, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) { pairs[3 * i] = info[4 * i]; pairs[3 * i + 1] = info[4 * i + 2]; pairs[3 * i + 2] = info[4 * i + 3]; }
+  } else {
+    std::vector<int> a(std::max(m, 1)), bb(std::max(m, 1));
+    CUDA_TRY(cudaMemcpy(a.data(), D.cand_a + (size_t)env * D.cand_cap, (size_t)m * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(bb.data(), D.cand_b + (size_t)env * D.cand_cap, (size_t)m * 4, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) { pairs[3 * i] = (a[i] >> 30) & 1; pairs[3 * i + 1] = a[i] & ((1 << 30) - 1); pairs[3 * i + 2] = bb[i]; }
+  }
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_debug_active_pairs(tac_batch* b, int32_t env, const double* x, const double* y, int32_t* pairs,
+                                             int32_t cap, int32_t* count, void* stream) {
+  DBG_CHECK(b, env);
+  DebugScope S{b, env, (cudaStream_t)stream};
+  tac_status s = dbg_enter(S, x, y, nullptr, nullptr, 0.0);
+  Dev& D = b->D;
+  if (!s) {
+    launch_positions(D, env, 1, 0, 1, S.st);
+    launch_broad(D, env, 1, 0, 1, S.st);
+    launch_narrow(D, env, 1, 1, S.st);
+    s = copy_pairs(b, env, true, pairs, cap, count, S.st);
+  }
+  tac_status s2 = dbg_leave(S);
+  return s ? s : s2;
+}
+
+static tac_status dbg_set_p(tac_batch* b, int env, const double* p, cudaStream_t st) {
+  Dev& D = b->D;
+  if (p) CUDA_TRY(cudaMemcpyAsync(D.p + (size_t)env * D.n, p, D.n * 8, cudaMemcpyHostToDevice, st));
+  else CUDA_TRY(cudaMemsetAsync(D.p + (size_t)env * D.n, 0, D.n * 8, st));
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_debug_candidates(tac_batch* b, int32_t env, const double* x, const double* y, const double* p,
+                                           int32_t* pairs, int32_t cap, int32_t* count, void* stream) {
+  DBG_CHECK(b, env);
+  DebugScope S{b, env, (cudaStream_t)stream};
+  tac_status s = dbg_enter(S, x, y, nullptr, nullptr, 0.0);
+  Dev& D = b->D;
+  if (!s) s = dbg_set_p(b, env, p, S.st);
+  if (!s) {
+    launch_positions(D, env, 1, 1, 1, S.st);
+    launch_broad(D, env, 1, p ? 1 : 0, 1, S.st);
+    s = copy_pairs(b, env, false, pairs, cap, count, S.st);
+  }
+  tac_status s2 = dbg_leave(S);
+  return s ? s : s2;
+}
+
+extern "C" tac_status tac_debug_accd(tac_batch* b, int32_t env, const double* x, const double* y, const double* p,
+                                     double* alpha, void* stream) {
+  DBG_CHECK(b, env);
+  if (!p || !alpha) return fail(TAC_E_INVALID, "p and alpha are required");
+  DebugScope S{b, env, (cudaStream_t)stream};
+  tac_status s = dbg_enter(S, x, y, nullptr, nullptr, 0.0);
+  Dev& D = b->D;
+  if (!s) s = dbg_set_p(b, env, p, S.st);
+  if (!s) {
+    launch_positions(D, env, 1, 1, 1, S.st);
+    launch_broad(D, env, 1, 1, 1, S.st);
+    launch_ccd(D, env, 1, 1, S.st);
+    EnvCtl c;
+    cudaMemcpyAsync(&c, D.ctl + env, sizeof(EnvCtl), cudaMemcpyDeviceToHost, S.st);
+    if (cudaStreamSynchronize(S.st) != cudaSuccess) s = fail(TAC_E_CUDA, "debug accd failed");
+    else *alpha = c.alpha_ccd;
+  }
+  tac_status s2 = dbg_leave(S);
+  return s ? s : s2;
+}
+
+extern "C" tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, const double* y, double* p, int32_t* iters,
+                                    void* stream) {
+  DBG_CHECK(b, env);
+  DebugScope S{b, env, (cudaStream_t)stream};
+  tac_status s = dbg_enter(S, x, y, nullptr, nullptr, 0.0);
+  Dev& D = b->D;
+  if (!s) s = dbg_assemble(b, env, S.st);
+  if (!s) {
+    launch_pcg(D, env, 1, 1, S.st);
+    EnvCtl c;
+    cudaMemcpyAsync(&c, D.ctl + env, sizeof(EnvCtl), cudaMemcpyDeviceToHost, S.st);
+    if (p) cudaMemcpyAsync(p, D.p + (size_t)env * D.n, D.n * 8, cudaMemcpyDeviceToHost, S.st);
+    if (cudaStreamSynchronize(S.st) != cudaSuccess) s = fail(TAC_E_CUDA, "debug pcg failed");
+    else if (iters) *iters = c.pcg;
+  }
+  tac_status s2 = dbg_leave(S);
+  return s ? s : s2;
+}

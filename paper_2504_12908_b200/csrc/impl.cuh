@@ -1,0 +1,126 @@
+// impl.cuh — device-side batch layout shared by the kernels and the host API.
+//
+// Layout in HBM (one workspace, caller-owned):
+//   template (read-only, shared by all envs, L2-resident): tets, D_m⁻¹, V_e, Lamé, lumped masses,
+//     soft BSR pattern + element→block gather lists, affine M^y / moments, contact primitives,
+//     rest areas, body-pair mask, constraint lists, readout tables.
+//   per env (env-major; every per-env array is [E][...] contiguous per env):
+//     DoF vectors q, qⁿ, v, q̃, g, p, r, z, d, Hd (n = 3V + 12·ND doubles each), vertex positions,
+//     BSR values (3×3 per soft vertex and per soft edge), dense 12×12 per body, block-Jacobi
+//     inverses, per-tet gradient+Hessian (SoA [90][T]), candidate and active pair lists with their
+//     12×12 projected Hessians, broad-phase hash entries.
+#pragma once
+#include "common.cuh"
+
+namespace tac {
+
+constexpr int NTHREADS = 256;
+constexpr int NBUCKET = 4096;      // spatial-hash buckets per env (shared memory)
+constexpr int MAXCELLS = 32;       // targets spanning more cells go to the per-env "big" list
+constexpr int BIG_CAP = 512;
+constexpr int TETBUF = 90;         // 12 gradient + 78 packed Hessian
+constexpr int PH = 78;
+
+enum { PHASE_ACTIVE = 0, PHASE_DONE = 1, PHASE_FAILED = 2, PHASE_IDLE = 3 };
+enum { ENV_OK = 0, ENV_NEWTON_STALL = 1, ENV_AL_INFEASIBLE = 2, ENV_CAPACITY = 3, ENV_NONFINITE = 4,
+       ENV_BAD_STATE = 5, ENV_DISABLED = 6 };
+
+struct EnvCtl {
+  int phase, status, inner_conv, newton, pcg, ls_bt, al_rounds, n_act, ncand, overflow;
+  int disabled, pad_;
+  double alpha_ccd, alpha_min, rho, r_prev, L, energy, residual, gp, pnorm, alpha;
+};
+
+struct Dev {
+  // ---- dims ----
+  int E, V, T, NA, ND, NVall, NSV, NT, NE, NEs, NC, NK, NB, n, npads, NCOAT, NMARK;
+  int cand_cap, act_cap, ent_cap;
+  // ---- config ----
+  double dt, dhat, kappa, tolN, tolAL, eta, armijo, accd_s, rho0, cell;
+  int max_newton, max_al, max_pcg, max_accd, mollify;
+  double grav[3];
+  // ---- template ----
+  const int* tets;        // [T][4]
+  const double* Dmi;      // [T][9]
+  const double* vol;      // [T]
+  const double* mu;       // [T]
+  const double* lam;      // [T]
+  const double* mass;     // [V]
+  const int* sedge;       // [NEs][2] soft edges (i<j) = off-diagonal BSR blocks
+  const int* vadj_ptr;    // [V+1]
+  const int* vadj;        // entries 2*edge + (v is the edge's second vertex)
+  const int* vdiag_ptr;   // [V+1]
+  const int* vdiag;       // entries 4*tet + local
+  const int* eblk_ptr;    // [NEs+1]
+  const int* eblk;        // entries 16*tet + 4*a + b (local a ↔ edge.i, b ↔ edge.j)
+  const int* body_kind;   // [NA]
+  const int* dof_slot;    // [NA] (-1 static)
+  const int* dof_body;    // [ND]
+  const double* My;       // [NA][144]
+  const double* bmass;    // [NA]
+  const double* bs1;      // [NA][3]
+  const double* bvol;     // [NA]
+  const double* bkappa;   // [NA]
+  const int* vert_body;   // [NVall] global body id (pads first)
+  const int* vert_aff;    // [NVall] affine body or -1
+  const double* vert_xbar;// [NVall][3]
+  const int* sverts;      // [NSV]
+  const int* tris;        // [NT][3]
+  const int* tri_body;    // [NT]
+  const int* edges;       // [NE][2]
+  const int* edge_body;   // [NE]
+  const double* A_v;      // [NVall]
+  const double* A_e;      // [NE]
+  const double* elen2;    // [NE]
+  const unsigned char* allowed;  // [NB][NB]
+  const int* att_vert;    // [NC]
+  const int* att_body;    // [NC]
+  const double* att_local;// [NC][3]
+  const int* att_of_vert; // [V] (-1 if free)
+  const int* kin_body;    // [NK]
+  const int* kin_of_body; // [NA] (-1)
+  const int* affv_list;   // vertices of dof bodies (for embedded norms): [NAV]
+  int NAV;
+  const int* kin_vlist;   // vertices of kinematic bodies [NKV]
+  int NKV;
+  // readout
+  const int* coat_vert;   // [NCOAT] soft vertex id
+  const int* coat_pad;    // [NCOAT]
+  const int* mark_tri;    // [NMARK][3] soft vertex ids
+  const double* mark_bary;// [NMARK][3]
+  const int* mark_pad;    // [NMARK]
+  const int* pad_mount;   // [npads]
+  const double* pad_T;    // [npads][12]
+  const double* Xrest;    // [V][3] pad-frame rest positions
+  // ---- per env ----
+  EnvCtl* ctl;            // [E]
+  double *q, *qn, *vel, *qt, *g, *p, *r, *z, *dd, *Ad;   // [E][n]
+  double* ystat;          // [E][NA][12]
+  double* ystage;         // [E][NA][12] staging for host I/O
+  double *s_att, *lam_att;// [E][NC][3]
+  double *s_kin, *lam_kin, *ykin;  // [E][NK][12]
+  double *P, *Pd;         // [E][NVall][3] positions at q, displacement of p
+  double *Hd, *Ho;        // [E][V][9], [E][NEs][9]
+  double *Hb;             // [E][ND][144]
+  double *Pinv_s, *Pinv_b;// [E][V][9], [E][ND][144]
+  double* tetbuf;         // [E][90][T]
+  int *cand_a, *cand_b;   // [E][cand_cap] (cand_a bit 30 = EE)
+  int* ent;               // [E][ent_cap][2]
+  int* big;               // [E][BIG_CAP]
+  int* act_info;          // [E][act_cap][4] (kind, type, a, b)
+  int* act_vid;           // [E][act_cap][4]
+  double* act_g;          // [E][act_cap][12]
+  double* act_H;          // [E][act_cap][78]
+  double* act_out;        // [E][act_cap][12]
+  int* cptr;              // [E][V+1] soft contribution lists
+  int* clist;             // [E][4*act_cap]
+  int* bptr;              // [E][ND+1] body contribution lists
+  int* blist;             // [E][4*act_cap]
+  double* eterm;          // [E][8]
+  double* out_coat;       // [E][NCOAT][3]
+  double* out_mpos;       // [E][NMARK][3]
+  double* out_mflow;      // [E][NMARK][3]
+  int* any_active;        // [1]
+};
+
+}  // namespace tac

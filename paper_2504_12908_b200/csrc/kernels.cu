@@ -1,0 +1,1314 @@
+// kernels.cu — sm_100a fp64 kernels of the batched IPC + ABD Newton step.
+// One CTA per environment for every per-env phase (envs are independent); per-env
+// reductions are deterministic block reductions with a fixed thread→element assignment, so every
+// env's result is bitwise independent of the batch size and of how envs are sharded.
+#include <cfloat>
+#include "eigen.cuh"
+#include "elastic.cuh"
+#include "geometry.cuh"
+#include "impl.cuh"
+#include "launch.h"
+
+namespace tac {
+
+// ------------------------------------------------------------------------------------------
+// small helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ const double* body_y(const Dev& D, int e, int b) {
+  int s = D.dof_slot[b];
+  return s >= 0 ? D.q + (size_t)e * D.n + 3 * D.V + 12 * s : D.ystat + ((size_t)e * D.NA + b) * 12;
+}
+__device__ __forceinline__ double* envp(double* base, int e, size_t per) { return base + (size_t)e * per; }
+
+// f-factor of the affine Jacobian: column α of J_v is e_{i(α)} scaled by f(α) (1 for t, x̄_j for A_ij)
+__device__ __forceinline__ int jrow(int alpha) { return alpha < 3 ? alpha : (alpha - 3) / 3; }
+__device__ __forceinline__ double jf(int alpha, const double* xb) { return alpha < 3 ? 1.0 : xb[(alpha - 3) % 3]; }
+
+__device__ __forceinline__ void pair_vids(const Dev& D, int kind, int a, int b, int* vid) {
+  if (kind == 0) {
+    vid[0] = a; vid[1] = D.tris[3 * b]; vid[2] = D.tris[3 * b + 1]; vid[3] = D.tris[3 * b + 2];
+  } else {
+    vid[0] = D.edges[2 * a]; vid[1] = D.edges[2 * a + 1]; vid[2] = D.edges[2 * b]; vid[3] = D.edges[2 * b + 1];
+  }
+}
+__device__ __forceinline__ double pair_area(const Dev& D, int kind, int a, int b) {
+  return kind == 0 ? D.A_v[a] : 0.5 * (D.A_e[a] + D.A_e[b]);
+}
+__device__ __forceinline__ double pair_eps(const Dev& D, int kind, int a, int b) {
+  return kind == 0 ? 1.0 : 1e-3 * D.elen2[a] * D.elen2[b];
+}
+
+__device__ __forceinline__ bool env_skip(const Dev& D, int e, int force) {
+  return !force && D.ctl[e].phase != PHASE_ACTIVE;
+}
+
+// packed-upper (r,c) table for 12×12
+__constant__ unsigned char c_unpack_r[PH], c_unpack_c[PH];
+
+// ------------------------------------------------------------------------------------------
+// positions: P = φ(q) for every contact vertex; Pd = displacement of p (J_v p_b for bodies)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_positions(Dev D, int env0, int with_p, int force) {
+  const int e = env0 + blockIdx.x;
+  if (env_skip(D, e, force)) return;
+  const double* q = D.q + (size_t)e * D.n;
+  const double* p = D.p + (size_t)e * D.n;
+  double* P = D.P + (size_t)e * D.NVall * 3;
+  double* Pd = D.Pd + (size_t)e * D.NVall * 3;
+  for (int gv = threadIdx.x; gv < D.NVall; gv += blockDim.x) {
+    if (gv < D.V) {
+      P[3 * gv] = q[3 * gv]; P[3 * gv + 1] = q[3 * gv + 1]; P[3 * gv + 2] = q[3 * gv + 2];
+      if (with_p) { Pd[3 * gv] = p[3 * gv]; Pd[3 * gv + 1] = p[3 * gv + 1]; Pd[3 * gv + 2] = p[3 * gv + 2]; }
+    } else {
+      int b = D.vert_aff[gv];
+      v3 xb = ld3(D.vert_xbar + 3 * gv);
+      st3(P + 3 * gv, embed(body_y(D, e, b), xb));
+      if (with_p) {
+        int s = D.dof_slot[b];
+        v3 d = mk(0, 0, 0);
+        if (s >= 0) d = embed(p + 3 * D.V + 12 * s, xb);
+        st3(Pd + 3 * gv, d);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// broad phase: per-env spatial hash (shared-memory bucket table), deterministic candidate list
+// ------------------------------------------------------------------------------------------
+struct Grid {
+  double ox, oy, oz, inv_h;
+  __device__ int ci(double x, double o) const {
+    double f = floor((x - o) * inv_h);
+    int i = (int)fmin(fmax(f, 0.0), 1023.0);
+    return i;
+  }
+  __device__ void cell(v3 p, int* c) const { c[0] = ci(p.x, ox); c[1] = ci(p.y, oy); c[2] = ci(p.z, oz); }
+};
+__device__ __forceinline__ unsigned hcell(int i, int j, int k) {
+  return (((unsigned)i * 73856093u) ^ ((unsigned)j * 19349663u) ^ ((unsigned)k * 83492791u)) & (NBUCKET - 1);
+}
+__device__ __forceinline__ int ccode(int i, int j, int k) { return i | (j << 10) | (k << 20); }
+
+struct BoxCtx {
+  const double* P; const double* Pd; int swept;
+  __device__ void vbox(int gv, v3& lo, v3& hi) const {
+    v3 a = ld3(P + 3 * gv);
+    lo = a; hi = a;
+    if (swept) {
+      v3 d = ld3(Pd + 3 * gv);
+      v3 b = a + d;
+      lo = vmin(lo, b); hi = vmax(hi, b);
+    }
+  }
+  __device__ void box(const int* vs, int nv, v3& lo, v3& hi) const {
+    vbox(vs[0], lo, hi);
+    for (int i = 1; i < nv; ++i) { v3 l, h; vbox(vs[i], l, h); lo = vmin(lo, l); hi = vmax(hi, h); }
+  }
+};
+
+__device__ __forceinline__ bool overlap(v3 qlo, v3 qhi, v3 tlo_i, v3 thi_i) {
+  // query box raw, target box already inflated by d̂: lo_q ≤ hi_t + d̂ and lo_t − d̂ ≤ hi_q
+  return qlo.x <= thi_i.x && qlo.y <= thi_i.y && qlo.z <= thi_i.z && tlo_i.x <= qhi.x && tlo_i.y <= qhi.y &&
+         tlo_i.z <= qhi.z;
+}
+
+__device__ __forceinline__ void target_box(const Dev& D, const BoxCtx& B, int code, v3& lo, v3& hi) {
+  int t = code >> 1;
+  if ((code & 1) == 0) B.box(D.tris + 3 * t, 3, lo, hi);
+  else B.box(D.edges + 2 * t, 2, lo, hi);
+  v3 dh = mk(D.dhat, D.dhat, D.dhat);
+  lo = lo - dh; hi = hi + dh;
+}
+
+template <bool EMIT>
+__device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int* cnt_off, const int* ent, const int* big,
+                        int nbig, int qi, int* out_a, int* out_b) {
+  const bool pt = qi < D.NSV;
+  int qa, qbody, qv[2];
+  v3 qlo, qhi;
+  if (pt) {
+    qa = D.sverts[qi];
+    qbody = D.vert_body[qa];
+    B.vbox(qa, qlo, qhi);
+  } else {
+    qa = qi - D.NSV;
+    qbody = D.edge_body[qa];
+    qv[0] = D.edges[2 * qa]; qv[1] = D.edges[2 * qa + 1];
+    B.box(qv, 2, qlo, qhi);
+  }
+  const int want = pt ? 0 : 1;
+  const unsigned char* allow = D.allowed + (size_t)qbody * D.NB;
+  int lo[3], hi[3];
+  G.cell(qlo, lo); G.cell(qhi, hi);
+  long ncell = (long)(hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+  int count = 0;
+  const int kindbit = pt ? 0 : (1 << 30);
+  auto accept = [&](int code, v3 tlo, v3 thi) {
+    if (EMIT) { out_a[count] = kindbit | qa; out_b[count] = code >> 1; }
+    ++count;
+  };
+  if (ncell > 4096) {  // huge query box: brute force over all targets of the kind
+    int ntg = pt ? D.NT : D.NE;
+    for (int t = 0; t < ntg; ++t) {
+      if (!pt && t <= qa) continue;
+      int tb = pt ? D.tri_body[t] : D.edge_body[t];
+      if (!allow[tb]) continue;
+      int code = 2 * t + want;
+      v3 tlo, thi;
+      target_box(D, B, code, tlo, thi);
+      if (overlap(qlo, qhi, tlo, thi)) accept(code, tlo, thi);
+    }
+    return count;
+  }
+  for (int x = lo[0]; x <= hi[0]; ++x)
+    for (int y = lo[1]; y <= hi[1]; ++y)
+      for (int z = lo[2]; z <= hi[2]; ++z) {
+        unsigned h = hcell(x, y, z);
+        int cc = ccode(x, y, z);
+        for (int j = cnt_off[h]; j < cnt_off[h + 1]; ++j) {
+          if (ent[2 * j + 1] != cc) continue;
+          int code = ent[2 * j];
+          if ((code & 1) != want) continue;
+          int t = code >> 1;
+          if (!pt && t <= qa) continue;
+          int tb = pt ? D.tri_body[t] : D.edge_body[t];
+          if (!allow[tb]) continue;
+          v3 tlo, thi;
+          target_box(D, B, code, tlo, thi);
+          if (!overlap(qlo, qhi, tlo, thi)) continue;
+          int tl[3];
+          G.cell(tlo, tl);
+          if (max(lo[0], tl[0]) != x || max(lo[1], tl[1]) != y || max(lo[2], tl[2]) != z) continue;
+          accept(code, tlo, thi);
+        }
+      }
+  for (int j = 0; j < nbig; ++j) {
+    int code = big[j];
+    if ((code & 1) != want) continue;
+    int t = code >> 1;
+    if (!pt && t <= qa) continue;
+    int tb = pt ? D.tri_body[t] : D.edge_body[t];
+    if (!allow[tb]) continue;
+    v3 tlo, thi;
+    target_box(D, B, code, tlo, thi);
+    if (overlap(qlo, qhi, tlo, thi)) accept(code, tlo, thi);
+  }
+  return count;
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_broad(Dev D, int env0, int swept, int force) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (!force && (C.phase != PHASE_ACTIVE || (swept && C.inner_conv))) return;
+  __shared__ int cnt[NBUCKET + 1];
+  __shared__ int cur[NBUCKET];
+  __shared__ double red[32];
+  __shared__ int sh[33];
+  __shared__ int nbig_s, ovf_s;
+  BoxCtx B{D.P + (size_t)e * D.NVall * 3, D.Pd + (size_t)e * D.NVall * 3, swept};
+  int* ent = D.ent + (size_t)e * D.ent_cap * 2;
+  int* big = D.big + (size_t)e * BIG_CAP;
+  // grid origin: min corner over all surface vertices (start and end positions)
+  double mx = 1e300, my = 1e300, mz = 1e300;
+  for (int i = threadIdx.x; i < D.NSV; i += blockDim.x) {
+    v3 lo, hi;
+    B.vbox(D.sverts[i], lo, hi);
+    mx = fmin(mx, lo.x); my = fmin(my, lo.y); mz = fmin(mz, lo.z);
+  }
+  Grid G;
+  G.ox = block_min(mx, red) - D.dhat;
+  G.oy = block_min(my, red) - D.dhat;
+  G.oz = block_min(mz, red) - D.dhat;
+  G.inv_h = 1.0 / D.cell;
+  for (int i = threadIdx.x; i <= NBUCKET; i += blockDim.x) cnt[i] = 0;
+  if (threadIdx.x == 0) { nbig_s = 0; ovf_s = 0; }
+  __syncthreads();
+  const int ntarget = D.NT + D.NE;
+  // pass 1: count cell entries of every target (inflated box)
+  for (int i = threadIdx.x; i < ntarget; i += blockDim.x) {
+    int code = i < D.NT ? 2 * i : 2 * (i - D.NT) + 1;
+    v3 lo, hi;
+    target_box(D, B, code, lo, hi);
+    int l[3], h[3];
+    G.cell(lo, l); G.cell(hi, h);
+    long nc = (long)(h[0] - l[0] + 1) * (h[1] - l[1] + 1) * (h[2] - l[2] + 1);
+    if (nc > MAXCELLS) {
+      int k = atomicAdd(&nbig_s, 1);
+      if (k < BIG_CAP) big[k] = code; else ovf_s = 1;
+      continue;
+    }
+    for (int x = l[0]; x <= h[0]; ++x)
+      for (int y = l[1]; y <= h[1]; ++y)
+        for (int z = l[2]; z <= h[2]; ++z) atomicAdd(&cnt[hcell(x, y, z)], 1);
+  }
+  __syncthreads();
+  // exclusive scan of bucket counts (16 per thread for 256 threads)
+  {
+    const int per = (NBUCKET + blockDim.x - 1) / blockDim.x;
+    int b0 = threadIdx.x * per;
+    int s = 0;
+    for (int i = 0; i < per && b0 + i < NBUCKET; ++i) s += cnt[b0 + i];
+    int tot;
+    int ex = block_excl_scan(s, sh, &tot);
+    int run = ex;
+    for (int i = 0; i < per && b0 + i < NBUCKET; ++i) {
+      int c = cnt[b0 + i];
+      cnt[b0 + i] = run;
+      cur[b0 + i] = run;
+      run += c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[NBUCKET] = tot;
+    if (tot > D.ent_cap && threadIdx.x == 0) ovf_s = 1;
+    __syncthreads();
+  }
+  if (ovf_s) {
+    if (threadIdx.x == 0) { C.overflow = 1; C.ncand = 0; }
+    return;
+  }
+  // pass 2: fill entries
+  for (int i = threadIdx.x; i < ntarget; i += blockDim.x) {
+    int code = i < D.NT ? 2 * i : 2 * (i - D.NT) + 1;
+    v3 lo, hi;
+    target_box(D, B, code, lo, hi);
+    int l[3], h[3];
+    G.cell(lo, l); G.cell(hi, h);
+    long nc = (long)(h[0] - l[0] + 1) * (h[1] - l[1] + 1) * (h[2] - l[2] + 1);
+    if (nc > MAXCELLS) continue;
+    for (int x = l[0]; x <= h[0]; ++x)
+      for (int y = l[1]; y <= h[1]; ++y)
+        for (int z = l[2]; z <= h[2]; ++z) {
+          int pos = atomicAdd(&cur[hcell(x, y, z)], 1);
+          ent[2 * pos] = code;
+          ent[2 * pos + 1] = ccode(x, y, z);
+        }
+  }
+  __syncthreads();
+  const int nbig = min(nbig_s, BIG_CAP);
+  // queries: PT (surface vertices) then EE (edges), tile by tile, count → scan → emit → sort
+  int* ca = D.cand_a + (size_t)e * D.cand_cap;
+  int* cb = D.cand_b + (size_t)e * D.cand_cap;
+  const int nq = D.NSV + D.NE;
+  int total = 0;
+  for (int t0 = 0; t0 < nq; t0 += blockDim.x) {
+    int qi = t0 + threadIdx.x;
+    int c = (qi < nq) ? bp_query<false>(D, B, G, cnt, ent, big, nbig, qi, nullptr, nullptr) : 0;
+    int tot;
+    int ex = block_excl_scan(c, sh, &tot);
+    int base = total + ex;
+    if (c > 0 && base + c <= D.cand_cap) {
+      bp_query<true>(D, B, G, cnt, ent, big, nbig, qi, ca + base, cb + base);
+      // insertion sort of this query's segment by target index
+      for (int i = 1; i < c; ++i) {
+        int kb = cb[base + i], ka = ca[base + i];
+        int j = i - 1;
+        while (j >= 0 && cb[base + j] > kb) { cb[base + j + 1] = cb[base + j]; ca[base + j + 1] = ca[base + j]; --j; }
+        cb[base + j + 1] = kb; ca[base + j + 1] = ka;
+      }
+    }
+    total += tot;
+  }
+  if (threadIdx.x == 0) {
+    C.ncand = min(total, D.cand_cap);
+    if (total > D.cand_cap) C.overflow = 1;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// narrow phase: active set 𝒜 = {k ∈ C : s_k < d̂²} (strict) in canonical order, plus
+// deterministic soft-vertex and body contribution lists
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_narrow(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (env_skip(D, e, force)) return;
+  extern __shared__ int dsm[];
+  int* vcnt = dsm;                 // [V+1]
+  int* vcur = dsm + D.V + 1;       // [V]
+  __shared__ int sh[33];
+  const double* P = D.P + (size_t)e * D.NVall * 3;
+  const int* ca = D.cand_a + (size_t)e * D.cand_cap;
+  const int* cb = D.cand_b + (size_t)e * D.cand_cap;
+  int* info = D.act_info + (size_t)e * D.act_cap * 4;
+  int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
+  const double dh2 = D.dhat * D.dhat;
+  const int nc = C.ncand;
+  int total = 0;
+  for (int t0 = 0; t0 < nc; t0 += blockDim.x) {
+    int k = t0 + threadIdx.x;
+    int flag = 0, kind = 0, type = 0, a = 0, b = 0, vid[4];
+    if (k < nc) {
+      kind = (ca[k] >> 30) & 1; a = ca[k] & ((1 << 30) - 1); b = cb[k];
+      pair_vids(D, kind, a, b, vid);
+      v3 X[4];
+      for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]);
+      double d2;
+      type = classify(kind, X, &d2);
+      flag = d2 < dh2;
+    }
+    int tot;
+    int ex = block_excl_scan(flag, sh, &tot);
+    int pos = total + ex;
+    if (flag && pos < D.act_cap) {
+      info[4 * pos] = kind; info[4 * pos + 1] = type; info[4 * pos + 2] = a; info[4 * pos + 3] = b;
+      for (int s = 0; s < 4; ++s) avid[4 * pos + s] = vid[s];
+    }
+    total += tot;
+  }
+  const int nact = min(total, D.act_cap);
+  if (threadIdx.x == 0) { C.n_act = nact; if (total > D.act_cap) C.overflow = 1; }
+  // soft-vertex contribution lists: count, scan, fill, per-vertex sort (deterministic)
+  for (int v = threadIdx.x; v <= D.V; v += blockDim.x) vcnt[v] = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nact; k += blockDim.x)
+    for (int s = 0; s < 4; ++s) { int gv = avid[4 * k + s]; if (gv < D.V) atomicAdd(&vcnt[gv], 1); }
+  __syncthreads();
+  int* cptr = D.cptr + (size_t)e * (D.V + 1);
+  int* clist = D.clist + (size_t)e * 4 * D.act_cap;
+  {
+    int run_total = 0;
+    for (int t0 = 0; t0 < D.V; t0 += blockDim.x) {
+      int v = t0 + threadIdx.x;
+      int c = v < D.V ? vcnt[v] : 0;
+      int tot;
+      int ex = block_excl_scan(c, sh, &tot);
+      if (v < D.V) { cptr[v] = run_total + ex; vcur[v] = run_total + ex; }
+      run_total += tot;
+    }
+    if (threadIdx.x == 0) cptr[D.V] = run_total;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nact; k += blockDim.x)
+    for (int s = 0; s < 4; ++s) {
+      int gv = avid[4 * k + s];
+      if (gv < D.V) { int pos = atomicAdd(&vcur[gv], 1); clist[pos] = 4 * k + s; }
+    }
+  __syncthreads();
+  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
+    int b0 = cptr[v], b1 = cptr[v + 1];
+    for (int i = b0 + 1; i < b1; ++i) {
+      int key = clist[i], j = i - 1;
+      while (j >= b0 && clist[j] > key) { clist[j + 1] = clist[j]; --j; }
+      clist[j + 1] = key;
+    }
+  }
+  // body contribution lists: stable block scan per dof body
+  int* bptr = D.bptr + (size_t)e * (D.ND + 1);
+  int* blist = D.blist + (size_t)e * 4 * D.act_cap;
+  int run = 0;
+  for (int d = 0; d < D.ND; ++d) {
+    const int body = D.dof_body[d];
+    if (threadIdx.x == 0) bptr[d] = run;
+    for (int t0 = 0; t0 < nact; t0 += blockDim.x) {
+      int k = t0 + threadIdx.x;
+      int c = 0, mask = 0;
+      if (k < nact)
+        for (int s = 0; s < 4; ++s) {
+          int gv = avid[4 * k + s];
+          if (gv >= D.V && D.vert_aff[gv] == body) { ++c; mask |= 1 << s; }
+        }
+      int tot;
+      int ex = block_excl_scan(c, sh, &tot);
+      int pos = run + ex;
+      for (int s = 0; s < 4; ++s)
+        if (mask & (1 << s)) blist[pos++] = 4 * k + s;
+      run += tot;
+    }
+  }
+  if (threadIdx.x == 0) bptr[D.ND] = run;
+}
+
+// ------------------------------------------------------------------------------------------
+// Neo-Hookean tets: gradient + F-space-projected 12×12 (SoA [90][T] per env)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.y;
+  if (env_skip(D, e, force)) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= D.T) return;
+  const double* q = D.q + (size_t)e * D.n;
+  int4 tv = reinterpret_cast<const int4*>(D.tets)[t];
+  v3 x[4] = {ld3(q + 3 * tv.x), ld3(q + 3 * tv.y), ld3(q + 3 * tv.z), ld3(q + 3 * tv.w)};
+  double Dmi[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Dmi[i] = D.Dmi[9 * t + i];
+  double g[12], H[PH];
+  const double scale = D.dt * D.dt * D.vol[t];
+  nh_grad_hess(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, g, H);
+  double* out = D.tetbuf + (size_t)e * TETBUF * D.T;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) out[(size_t)i * D.T + t] = g[i];
+#pragma unroll
+  for (int i = 0; i < PH; ++i) out[(size_t)(12 + i) * D.T + t] = H[i];
+}
+
+// ------------------------------------------------------------------------------------------
+// barrier pairs: warp per pair; closed-form ∇s/∇²s, barrier + mollifier composition, full 12×12
+// PSD projection by warp Jacobi (readings R10-R12)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_pairs(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.x;
+  if (env_skip(D, e, force)) return;
+  __shared__ JacobiScratch JS[NTHREADS / 32];
+  __shared__ double GS[NTHREADS / 32][24];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const EnvCtl& C = D.ctl[e];
+  const double* P = D.P + (size_t)e * D.NVall * 3;
+  const int* info = D.act_info + (size_t)e * D.act_cap * 4;
+  const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
+  double* ag = D.act_g + (size_t)e * D.act_cap * 12;
+  double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  JacobiScratch& S = JS[w];
+  double* gs = GS[w];
+  double* gc = GS[w] + 12;
+  for (int k = w; k < C.n_act; k += nw) {
+    const int kind = info[4 * k], type = info[4 * k + 1], a = info[4 * k + 2], b = info[4 * k + 3];
+    v3 X[4];
+    for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * avid[4 * k + s]);
+    SubDist SD;
+    sd_make(SD, kind, type, X);
+    double B, B1, B2;
+    barrier_s(SD.s, D.dhat, &B, &B1, &B2);
+    const bool useM = (kind == 1) && D.mollify;
+    SubDist CC;
+    double m = 1.0, m1 = 0.0, m2 = 0.0;
+    if (useM) {
+      sd_make_cross(CC, X);
+      mollifier(CC.D, pair_eps(D, kind, a, b), &m, &m1, &m2);
+    }
+    const double scale = D.dt * D.dt * D.kappa * pair_area(D, kind, a, b);
+    if (lane < 12) {
+      gs[lane] = sd_grad(SD, lane);
+      gc[lane] = useM ? sd_grad(CC, lane, true) : 0.0;
+    }
+    __syncwarp();
+    if (lane < 12) ag[12 * k + lane] = scale * (m * B1 * gs[lane] + B * m1 * gc[lane]);
+    for (int i = lane; i < 144; i += 32) {
+      int r = i / 12, c = i % 12;
+      double h = 0.0;
+      if (r <= c) {
+        h = m * (B2 * gs[r] * gs[c] + B1 * sd_hess(SD, r, c));
+        if (useM && m1 != 0.0)
+          h += B * (m2 * gc[r] * gc[c] + m1 * sd_hess(CC, r, c, true)) + m1 * B1 * (gs[r] * gc[c] + gc[r] * gs[c]);
+        h *= scale;
+      }
+      S.A[i] = h;
+    }
+    __syncwarp();
+    for (int i = lane; i < 144; i += 32) {
+      int r = i / 12, c = i % 12;
+      if (r > c) S.A[i] = S.A[12 * c + r];
+    }
+    __syncwarp();
+    jacobi12_psd(S, lane, 32);
+    for (int i = lane; i < PH; i += 32) aH[(size_t)PH * k + i] = S.A[12 * c_unpack_r[i] + c_unpack_c[i]];
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// assembly: gradient g, soft BSR (diag + edge blocks), body 12×12 blocks, block-Jacobi inverses
+// ------------------------------------------------------------------------------------------
+__device__ void chol_inverse12(const double* A, double* Ainv, double* L /*144 scratch*/) {
+  // single thread: Cholesky A = L Lᵀ then Ainv = L⁻ᵀ L⁻¹
+  for (int i = 0; i < 144; ++i) L[i] = 0.0;
+  for (int j = 0; j < 12; ++j) {
+    double s = A[13 * j];
+    for (int k = 0; k < j; ++k) s -= L[12 * j + k] * L[12 * j + k];
+    double ljj = sqrt(fmax(s, 1e-300));
+    L[13 * j] = ljj;
+    for (int i = j + 1; i < 12; ++i) {
+      double t = A[12 * i + j];
+      for (int k = 0; k < j; ++k) t -= L[12 * i + k] * L[12 * j + k];
+      L[12 * i + j] = t / ljj;
+    }
+  }
+  for (int c = 0; c < 12; ++c) {
+    double y[12];
+    for (int i = 0; i < 12; ++i) {  // L y = e_c
+      double t = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) t -= L[12 * i + k] * y[k];
+      y[i] = t / L[13 * i];
+    }
+    for (int i = 11; i >= 0; --i) {  // Lᵀ x = y
+      double t = y[i];
+      for (int k = i + 1; k < 12; ++k) t -= L[12 * k + i] * y[k];
+      y[i] = t / L[13 * i];
+    }
+    for (int i = 0; i < 12; ++i) Ainv[12 * i + c] = y[i];
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.x;
+  if (env_skip(D, e, force)) return;
+  __shared__ JacobiScratch JS[NTHREADS / 32];
+  __shared__ double PB[NTHREADS / 32][144];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const EnvCtl& C = D.ctl[e];
+  const double* q = D.q + (size_t)e * D.n;
+  const double* qt = D.qt + (size_t)e * D.n;
+  double* g = D.g + (size_t)e * D.n;
+  const double* tb = D.tetbuf + (size_t)e * TETBUF * D.T;
+  const double* ag = D.act_g + (size_t)e * D.act_cap * 12;
+  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
+  const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
+  const int* bptr = D.bptr + (size_t)e * (D.ND + 1);
+  const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
+  const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
+  const double dt2 = D.dt * D.dt, rho = C.rho;
+  const double* s_att = D.s_att + (size_t)e * D.NC * 3;
+  const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
+  // ---- soft vertices ----
+  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
+    const double m = D.mass[v];
+    v3 x = ld3(q + 3 * v), xt = ld3(qt + 3 * v);
+    v3 gv = m * (x - xt) - (dt2 * m) * mk(D.grav[0], D.grav[1], D.grav[2]);
+    double dg = m;
+    int ci = D.att_of_vert[v];
+    if (ci >= 0) {
+      v3 r = x - ld3(s_att + 3 * ci);
+      gv += (rho * m) * r - m * ld3(lam_att + 3 * ci);
+      dg += rho * m;
+    }
+    double Hv[9] = {dg, 0, 0, 0, dg, 0, 0, 0, dg};
+    for (int j = D.vdiag_ptr[v]; j < D.vdiag_ptr[v + 1]; ++j) {
+      int ent = D.vdiag[j], t = ent >> 2, a = ent & 3;
+      gv += mk(tb[(size_t)(3 * a) * D.T + t], tb[(size_t)(3 * a + 1) * D.T + t], tb[(size_t)(3 * a + 2) * D.T + t]);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) Hv[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * a + c, 12)) * D.T + t];
+    }
+    double Pv[9];
+    for (int i = 0; i < 9; ++i) Pv[i] = Hv[i];
+    for (int j = cptr[v]; j < cptr[v + 1]; ++j) {
+      int k = clist[j] >> 2, s = clist[j] & 3;
+      gv += ld3(ag + 12 * k + 3 * s);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) Pv[3 * r + c] += aH[(size_t)PH * k + sym_idx(3 * s + r, 3 * s + c, 12)];
+    }
+    st3(g + 3 * v, gv);
+    double* hd = D.Hd + ((size_t)e * D.V + v) * 9;
+    for (int i = 0; i < 9; ++i) hd[i] = Hv[i];
+    inv33(Pv, D.Pinv_s + ((size_t)e * D.V + v) * 9);
+  }
+  // ---- soft edge blocks ----
+  for (int ei = threadIdx.x; ei < D.NEs; ei += blockDim.x) {
+    double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = D.eblk_ptr[ei]; j < D.eblk_ptr[ei + 1]; ++j) {
+      int ent = D.eblk[j], t = ent >> 4, a = (ent >> 2) & 3, b = ent & 3;
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) B[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * b + c, 12)) * D.T + t];
+    }
+    double* ho = D.Ho + ((size_t)e * D.NEs + ei) * 9;
+    for (int i = 0; i < 9; ++i) ho[i] = B[i];
+  }
+  // ---- affine DoF bodies: warp per body ----
+  for (int d = w; d < D.ND; d += nw) {
+    const int b = D.dof_body[d];
+    const double* y = q + 3 * D.V + 12 * d;
+    const double* yt = qt + 3 * D.V + 12 * d;
+    const double* M = D.My + (size_t)b * 144;
+    const int ki = D.kin_of_body[b];
+    const double* sk = ki >= 0 ? D.s_kin + ((size_t)e * D.NK + ki) * 12 : nullptr;
+    const double* lk = ki >= 0 ? D.lam_kin + ((size_t)e * D.NK + ki) * 12 : nullptr;
+    const double kv = dt2 * D.bkappa[b] * D.bvol[b];
+    JacobiScratch& S = JS[w];
+    // ortho 9×9 into the 12×12 scratch (zero padded), projected
+    for (int i = lane; i < 144; i += 32) {
+      int r = i / 12, c = i % 12;
+      S.A[i] = (r < 9 && c < 9) ? ortho_hess_entry(y + 3, kv, r, c) : 0.0;
+    }
+    __syncwarp();
+    jacobi12_psd(S, lane, 32);
+    double gb = 0.0;
+    if (lane < 12) {
+      int al = lane;
+      double acc = 0.0;
+      for (int be = 0; be < 12; ++be) acc += M[12 * al + be] * (y[be] - yt[be]);
+      if (ki >= 0) {
+        double a2 = 0.0, a3 = 0.0;
+        for (int be = 0; be < 12; ++be) { a2 += M[12 * al + be] * (y[be] - sk[be]); a3 += M[12 * al + be] * lk[be]; }
+        acc += rho * a2 - a3;
+      }
+      if (al < 3) acc -= dt2 * D.bmass[b] * D.grav[al];
+      else acc -= dt2 * D.grav[(al - 3) / 3] * D.bs1[3 * b + (al - 3) % 3];
+      if (al >= 3) {
+        double g9[9];
+        ortho_grad(y + 3, kv, g9);
+        acc += g9[al - 3];
+      }
+      gb = acc;
+    }
+    // body block Hb = M(1 + ρ[kin]) + ortho⁺
+    double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
+    const double fac = 1.0 + (ki >= 0 ? rho : 0.0);
+    for (int i = lane; i < 144; i += 32) {
+      int r = i / 12, c = i % 12;
+      double v = M[i] * fac;
+      if (r >= 3 && c >= 3) v += S.A[12 * (r - 3) + (c - 3)];
+      Hb[i] = v;
+      PB[w][i] = v;
+    }
+    __syncwarp();
+    // pair contributions (gradient, preconditioner block) in list order (deterministic per lane)
+    for (int j = bptr[d]; j < bptr[d + 1]; ++j) {
+      int k = blist[j] >> 2, s = blist[j] & 3;
+      const double* xs = D.vert_xbar + 3 * avid[4 * k + s];
+      if (lane < 12) gb += jf(lane, xs) * ag[12 * k + 3 * s + jrow(lane)];
+      for (int t = 0; t < 4; ++t) {
+        int gvt = avid[4 * k + t];
+        if (gvt < D.V || D.vert_aff[gvt] != b) continue;
+        const double* xt = D.vert_xbar + 3 * gvt;
+        for (int i = lane; i < 144; i += 32) {
+          int al = i / 12, be = i % 12;
+          PB[w][i] += jf(al, xs) * jf(be, xt) * aH[(size_t)PH * k + sym_idx(3 * s + jrow(al), 3 * t + jrow(be), 12)];
+        }
+      }
+    }
+    if (lane < 12) g[3 * D.V + 12 * d + lane] = gb;
+    __syncwarp();
+    if (lane == 0) chol_inverse12(PB[w], D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q);
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// matrix-free SpMV y = H x: soft BSR + affine 12×12 + pair 12×12 through J_v (deterministic)
+// ------------------------------------------------------------------------------------------
+__device__ void spmv(const Dev& D, int e, const double* x, double* y) {
+  const EnvCtl& C = D.ctl[e];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  double* ao = D.act_out + (size_t)e * D.act_cap * 12;
+  const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
+  // pass A: per pair out_k = H_k x_local
+  for (int k = threadIdx.x; k < C.n_act; k += blockDim.x) {
+    double xl[12];
+    for (int s = 0; s < 4; ++s) {
+      int gv = avid[4 * k + s];
+      v3 u = mk(0, 0, 0);
+      if (gv < D.V) u = ld3(x + 3 * gv);
+      else {
+        int sl = D.dof_slot[D.vert_aff[gv]];
+        if (sl >= 0) u = embed(x + 3 * D.V + 12 * sl, ld3(D.vert_xbar + 3 * gv));
+      }
+      xl[3 * s] = u.x; xl[3 * s + 1] = u.y; xl[3 * s + 2] = u.z;
+    }
+    const double* H = aH + (size_t)PH * k;
+    for (int r = 0; r < 12; ++r) {
+      double acc = 0.0;
+      for (int c = 0; c < 12; ++c) acc += H[sym_idx(r, c, 12)] * xl[c];
+      ao[12 * k + r] = acc;
+    }
+  }
+  __syncthreads();
+  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
+  const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
+  const double* Hd = D.Hd + (size_t)e * D.V * 9;
+  const double* Ho = D.Ho + (size_t)e * D.NEs * 9;
+  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
+    v3 acc = mul33(Hd + 9 * v, ld3(x + 3 * v));
+    for (int j = D.vadj_ptr[v]; j < D.vadj_ptr[v + 1]; ++j) {
+      int en = D.vadj[j], ei = en >> 1, second = en & 1;
+      int other = second ? D.sedge[2 * ei] : D.sedge[2 * ei + 1];
+      v3 xo = ld3(x + 3 * other);
+      acc += second ? mul33T(Ho + 9 * ei, xo) : mul33(Ho + 9 * ei, xo);
+    }
+    for (int j = cptr[v]; j < cptr[v + 1]; ++j) acc += ld3(ao + 12 * (clist[j] >> 2) + 3 * (clist[j] & 3));
+    st3(y + 3 * v, acc);
+  }
+  const int* bptr = D.bptr + (size_t)e * (D.ND + 1);
+  const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
+  for (int d = w; d < D.ND; d += nw) {
+    const double* xb = x + 3 * D.V + 12 * d;
+    const double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
+    double acc[12];
+    for (int i = 0; i < 12; ++i) acc[i] = 0.0;
+    for (int j = bptr[d] + lane; j < bptr[d + 1]; j += 32) {
+      int k = blist[j] >> 2, s = blist[j] & 3;
+      const double* xs = D.vert_xbar + 3 * avid[4 * k + s];
+      v3 o = ld3(ao + 12 * k + 3 * s);
+      for (int i = 0; i < 3; ++i) {
+        double oi = comp(o, i);
+        acc[i] += oi;
+        acc[3 + 3 * i] += oi * xs[0]; acc[4 + 3 * i] += oi * xs[1]; acc[5 + 3 * i] += oi * xs[2];
+      }
+    }
+    for (int i = 0; i < 12; ++i) acc[i] = warp_sum(acc[i]);
+    if (lane < 12) {
+      double s = 0.0;
+      for (int c = 0; c < 12; ++c) s += Hb[12 * lane + c] * xb[c];
+      double tot = 0.0;
+      for (int i = 0; i < 12; ++i) if (i == lane) tot = acc[i];
+      y[3 * D.V + 12 * d + lane] = s + tot;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void precond(const Dev& D, int e, const double* r, double* z) {
+  for (int v = threadIdx.x; v < D.V; v += blockDim.x)
+    st3(z + 3 * v, mul33(D.Pinv_s + ((size_t)e * D.V + v) * 9, ld3(r + 3 * v)));
+  for (int i = threadIdx.x; i < 12 * D.ND; i += blockDim.x) {
+    int d = i / 12, row = i % 12;
+    const double* Pi = D.Pinv_b + ((size_t)e * D.ND + d) * 144 + 12 * row;
+    const double* rb = r + 3 * D.V + 12 * d;
+    double s = 0.0;
+    for (int c = 0; c < 12; ++c) s += Pi[c] * rb[c];
+    z[3 * D.V + 12 * d + row] = s;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
+// block-Jacobi PCG: H p = −g from p₀ = 0, stop at rᵀz ≤ η² r₀ᵀz₀ or max_pcg; then the
+// Newton convergence test ‖p‖_emb,∞ ≤ τ_N L_env and gᵀp.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.x;
+  if (env_skip(D, e, force)) return;
+  __shared__ double red[32];
+  EnvCtl& C = D.ctl[e];
+  const int n = D.n;
+  const double* g = D.g + (size_t)e * n;
+  double* p = D.p + (size_t)e * n;
+  double* r = D.r + (size_t)e * n;
+  double* z = D.z + (size_t)e * n;
+  double* d = D.dd + (size_t)e * n;
+  double* Ad = D.Ad + (size_t)e * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
+  __syncthreads();
+  precond(D, e, r, z);
+  double part = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { d[i] = z[i]; part += r[i] * z[i]; }
+  double rz = block_sum(part, red);
+  const double rz0 = rz, stop = D.eta * D.eta * rz0;
+  int it = 0;
+  bool bad = !(rz0 == rz0);
+  while (!bad && it < D.max_pcg && rz > stop) {
+    spmv(D, e, d, Ad);
+    part = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
+    double dAd = block_sum(part, red);
+    double alpha = rz / dAd;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] += alpha * d[i]; r[i] -= alpha * Ad[i]; }
+    __syncthreads();
+    precond(D, e, r, z);
+    part = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) part += r[i] * z[i];
+    double rzn = block_sum(part, red);
+    double beta = rzn / rz;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = z[i] + beta * d[i];
+    __syncthreads();
+    rz = rzn;
+    ++it;
+    if (!(rz == rz) || !(dAd > 0.0)) bad = true;
+  }
+  // gᵀp and embedded ∞-norm
+  part = 0.0;
+  double pm = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) part += g[i] * p[i];
+  for (int i = threadIdx.x; i < 3 * D.V; i += blockDim.x) pm = fmax(pm, fabs(p[i]));
+  for (int i = threadIdx.x; i < D.NAV; i += blockDim.x) {
+    int gv = D.affv_list[i];
+    int sl = D.dof_slot[D.vert_aff[gv]];
+    v3 u = embed(p + 3 * D.V + 12 * sl, ld3(D.vert_xbar + 3 * gv));
+    pm = fmax(pm, fmax(fabs(u.x), fmax(fabs(u.y), fabs(u.z))));
+  }
+  double gp = block_sum(part, red);
+  pm = block_max(pm, red);
+  if (threadIdx.x == 0) {
+    C.pcg += it;
+    C.newton += 1;
+    C.gp = gp;
+    C.pnorm = pm;
+    if (bad || !(pm == pm)) { C.phase = PHASE_FAILED; C.status = ENV_NONFINITE; }
+    else C.inner_conv = (pm <= D.tolN * C.L) ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_spmv(Dev D, int env0, const double* x, double* y) {
+  const int e = env0 + blockIdx.x;
+  spmv(D, e, x, y);
+}
+
+// ------------------------------------------------------------------------------------------
+// additive CCD (reading R16): α_max = min(1, min over C′ of ACCD)
+// ------------------------------------------------------------------------------------------
+__device__ double accd_pair(int kind, v3* X, v3* Pd, double s, double tc, int max_iters) {
+  v3 mean = 0.25 * (Pd[0] + Pd[1] + Pd[2] + Pd[3]);
+  double n[4];
+  for (int i = 0; i < 4; ++i) { Pd[i] = Pd[i] - mean; n[i] = sqrt(dot(Pd[i], Pd[i])); }
+  double lp = kind == 0 ? n[0] + fmax(n[1], fmax(n[2], n[3])) : fmax(n[0], n[1]) + fmax(n[2], n[3]);
+  if (lp == 0.0) return 1.0;
+  double d2;
+  classify(kind, X, &d2);
+  double d = sqrt(d2);
+  double g = s * d, t = 0.0, tl = (1.0 - s) * d / lp;
+  int it = 0;
+  while (true) {
+    for (int i = 0; i < 4; ++i) X[i] = X[i] + tl * Pd[i];
+    classify(kind, X, &d2);
+    d = sqrt(d2);
+    if (t > 0.0 && d < g) break;
+    t += tl;
+    if (t > tc) return 1.0;
+    tl = (1.0 - s) * d / lp;
+    if (++it >= max_iters) break;
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_ccd(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (!force && (C.phase != PHASE_ACTIVE || C.inner_conv)) return;
+  __shared__ double red[32];
+  const double* P = D.P + (size_t)e * D.NVall * 3;
+  const double* Pd = D.Pd + (size_t)e * D.NVall * 3;
+  const int* ca = D.cand_a + (size_t)e * D.cand_cap;
+  const int* cb = D.cand_b + (size_t)e * D.cand_cap;
+  double amin = 1.0;
+  for (int k = threadIdx.x; k < C.ncand; k += blockDim.x) {
+    int kind = (ca[k] >> 30) & 1, a = ca[k] & ((1 << 30) - 1), b = cb[k], vid[4];
+    pair_vids(D, kind, a, b, vid);
+    v3 X[4], Q[4];
+    for (int s = 0; s < 4; ++s) { X[s] = ld3(P + 3 * vid[s]); Q[s] = ld3(Pd + 3 * vid[s]); }
+    amin = fmin(amin, accd_pair(kind, X, Q, D.accd_s, 1.0, D.max_accd));
+  }
+  amin = block_min(amin, red);
+  if (threadIdx.x == 0) C.alpha_ccd = fmin(1.0, amin);
+}
+
+// ------------------------------------------------------------------------------------------
+// energy at q + α p (line search): six deterministic block sums
+// ------------------------------------------------------------------------------------------
+__device__ void energy_terms(const Dev& D, int e, double alpha, double* red, double* terms, int* inverted) {
+  const EnvCtl& C = D.ctl[e];
+  const double* q = D.q + (size_t)e * D.n;
+  const double* p = D.p + (size_t)e * D.n;
+  const double* qt = D.qt + (size_t)e * D.n;
+  const double dt2 = D.dt * D.dt, rho = C.rho;
+  const v3 G = mk(D.grav[0], D.grav[1], D.grav[2]);
+  double ein = 0, eel = 0, eor = 0, egr = 0, eba = 0, eal = 0;
+  int inv = 0;
+  const double* s_att = D.s_att + (size_t)e * D.NC * 3;
+  const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
+  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
+    double m = D.mass[v];
+    v3 x = ld3(q + 3 * v) + alpha * ld3(p + 3 * v);
+    v3 dx = x - ld3(qt + 3 * v);
+    ein += 0.5 * m * dot(dx, dx);
+    egr -= dt2 * m * dot(G, x);
+    int ci = D.att_of_vert[v];
+    if (ci >= 0) {
+      v3 r = x - ld3(s_att + 3 * ci);
+      eal += 0.5 * rho * m * dot(r, r) - m * dot(ld3(lam_att + 3 * ci), r);
+    }
+  }
+  for (int t = threadIdx.x; t < D.T; t += blockDim.x) {
+    int4 tv = reinterpret_cast<const int4*>(D.tets)[t];
+    int ids[4] = {tv.x, tv.y, tv.z, tv.w};
+    v3 x[4];
+    for (int i = 0; i < 4; ++i) x[i] = ld3(q + 3 * ids[i]) + alpha * ld3(p + 3 * ids[i]);
+    bool bad = false;
+    double psi = nh_energy(x, D.Dmi + 9 * t, D.mu[t], D.lam[t], &bad);
+    if (bad) inv = 1; else eel += dt2 * D.vol[t] * psi;
+  }
+  for (int d = threadIdx.x; d < D.ND; d += blockDim.x) {
+    int b = D.dof_body[d];
+    double y[12], dy[12];
+    for (int i = 0; i < 12; ++i) {
+      y[i] = q[3 * D.V + 12 * d + i] + alpha * p[3 * D.V + 12 * d + i];
+      dy[i] = y[i] - qt[3 * D.V + 12 * d + i];
+    }
+    const double* M = D.My + (size_t)b * 144;
+    double s = 0.0;
+    for (int i = 0; i < 12; ++i) { double t = 0.0; for (int j = 0; j < 12; ++j) t += M[12 * i + j] * dy[j]; s += dy[i] * t; }
+    ein += 0.5 * s;
+    v3 As1 = mul33(y + 3, ld3(D.bs1 + 3 * b));
+    egr -= dt2 * dot(G, D.bmass[b] * mk(y[0], y[1], y[2]) + As1);
+    eor += ortho_energy(y + 3, dt2 * D.bkappa[b] * D.bvol[b]);
+    int ki = D.kin_of_body[b];
+    if (ki >= 0) {
+      const double* sk = D.s_kin + ((size_t)e * D.NK + ki) * 12;
+      const double* lk = D.lam_kin + ((size_t)e * D.NK + ki) * 12;
+      double r[12];
+      for (int i = 0; i < 12; ++i) r[i] = y[i] - sk[i];
+      double a1 = 0.0, a2 = 0.0;
+      for (int i = 0; i < 12; ++i) {
+        double Mr = 0.0;
+        for (int j = 0; j < 12; ++j) Mr += M[12 * i + j] * r[j];
+        a1 += r[i] * Mr; a2 += lk[i] * Mr;
+      }
+      eal += 0.5 * rho * a1 - a2;
+    }
+  }
+  // barrier over candidates active at the trial point
+  const double* P = D.P + (size_t)e * D.NVall * 3;
+  const double* Pd = D.Pd + (size_t)e * D.NVall * 3;
+  const int* ca = D.cand_a + (size_t)e * D.cand_cap;
+  const int* cb = D.cand_b + (size_t)e * D.cand_cap;
+  const double dh2 = D.dhat * D.dhat;
+  for (int k = threadIdx.x; k < C.ncand; k += blockDim.x) {
+    int kind = (ca[k] >> 30) & 1, a = ca[k] & ((1 << 30) - 1), b = cb[k], vid[4];
+    pair_vids(D, kind, a, b, vid);
+    v3 X[4];
+    for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]) + alpha * ld3(Pd + 3 * vid[s]);
+    double d2;
+    classify(kind, X, &d2);
+    if (!(d2 < dh2)) continue;
+    double B, B1, B2;
+    barrier_s(d2, D.dhat, &B, &B1, &B2);
+    double m = 1.0;
+    if (kind == 1 && D.mollify) {
+      v3 n = cross(X[1] - X[0], X[3] - X[2]);
+      double m1, m2;
+      mollifier(dot(n, n), pair_eps(D, kind, a, b), &m, &m1, &m2);
+    }
+    eba += dt2 * D.kappa * pair_area(D, kind, a, b) * m * B;
+  }
+  terms[0] = block_sum(ein, red);
+  terms[1] = block_sum(eel, red);
+  terms[2] = block_sum(eor, red);
+  terms[3] = block_sum(egr, red);
+  terms[4] = block_sum(eba, red);
+  terms[5] = block_sum(eal, red);
+  *inverted = __syncthreads_or(inv);
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_energy(Dev D, int env0, double alpha) {
+  const int e = env0 + blockIdx.x;
+  __shared__ double red[32];
+  double t[6];
+  int inv;
+  energy_terms(D, e, alpha, red, t, &inv);
+  if (threadIdx.x == 0) {
+    double* out = D.eterm + (size_t)e * 8;
+    for (int i = 0; i < 6; ++i) out[i] = t[i];
+    out[1] = inv ? 1.0 / 0.0 : out[1];
+    out[6] = inv;
+  }
+}
+
+// backtracking line search from α = min(1, α_ccd); Armijo c
+__global__ void __launch_bounds__(NTHREADS) k_linesearch(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (C.phase != PHASE_ACTIVE || C.inner_conv) return;
+  __shared__ double red[32];
+  double t[6];
+  int inv;
+  energy_terms(D, e, 0.0, red, t, &inv);
+  const double E0 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
+  double alpha = C.alpha_ccd;
+  const double gp = C.gp;
+  int bt = 0;
+  bool ok = false;
+  double E1 = E0;
+  while (true) {
+    energy_terms(D, e, alpha, red, t, &inv);
+    if (!inv) {
+      E1 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
+      if (E1 <= E0 + D.armijo * alpha * gp) { ok = true; break; }
+    }
+    alpha *= 0.5;
+    ++bt;
+    if (alpha < 1e-10) break;
+  }
+  if (ok) {
+    double* q = D.q + (size_t)e * D.n;
+    const double* p = D.p + (size_t)e * D.n;
+    for (int i = threadIdx.x; i < D.n; i += blockDim.x) q[i] += alpha * p[i];
+  }
+  if (threadIdx.x == 0) {
+    C.ls_bt += bt;
+    if (!ok) { C.phase = PHASE_FAILED; C.status = ENV_NEWTON_STALL; }
+    else { C.alpha_min = fmin(C.alpha_min, alpha); C.alpha = alpha; C.energy = E1; }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Newton / AL control (readings R13-R14): AL update when the inner solve has converged
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (C.phase != PHASE_ACTIVE) return;
+  __shared__ double red[32];
+  if (C.overflow) {
+    if (threadIdx.x == 0) { C.phase = PHASE_FAILED; C.status = ENV_CAPACITY; }
+    return;
+  }
+  double* q = D.q + (size_t)e * D.n;
+  if (C.inner_conv) {
+    const double* s_att = D.s_att + (size_t)e * D.NC * 3;
+    double res = 0.0;
+    for (int c = threadIdx.x; c < D.NC; c += blockDim.x) {
+      v3 r = ld3(q + 3 * D.att_vert[c]) - ld3(s_att + 3 * c);
+      res = fmax(res, sqrt(dot(r, r)));
+    }
+    for (int i = threadIdx.x; i < D.NKV; i += blockDim.x) {
+      int gv = D.kin_vlist[i], b = D.vert_aff[gv], ki = D.kin_of_body[b], d = D.dof_slot[b];
+      const double* y = q + 3 * D.V + 12 * d;
+      const double* sk = D.s_kin + ((size_t)e * D.NK + ki) * 12;
+      double dy[12];
+      for (int j = 0; j < 12; ++j) dy[j] = y[j] - sk[j];
+      v3 u = embed(dy, ld3(D.vert_xbar + 3 * gv));
+      res = fmax(res, sqrt(dot(u, u)));
+    }
+    res = block_max(res, red);
+    __syncthreads();
+    const bool done = res <= D.tolAL * C.L;
+    const int rounds = C.al_rounds + 1;
+    __syncthreads();
+    if (done) {
+      if (threadIdx.x == 0) { C.residual = res; C.al_rounds = rounds; C.phase = PHASE_DONE; C.inner_conv = 0; }
+      return;
+    }
+    if (rounds >= D.max_al) {
+      if (threadIdx.x == 0) { C.residual = res; C.al_rounds = rounds; C.phase = PHASE_FAILED; C.status = ENV_AL_INFEASIBLE; }
+      return;
+    }
+    double rho = C.rho;
+    if (res > 0.5 * C.r_prev) rho *= 2.0;
+    double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
+    for (int c = threadIdx.x; c < D.NC; c += blockDim.x) {
+      v3 r = ld3(q + 3 * D.att_vert[c]) - ld3(s_att + 3 * c);
+      st3(lam_att + 3 * c, ld3(lam_att + 3 * c) - rho * r);
+    }
+    for (int i = threadIdx.x; i < D.NK * 12; i += blockDim.x) {
+      int ki = i / 12, j = i % 12, b = D.kin_body[ki], d = D.dof_slot[b];
+      double r = q[3 * D.V + 12 * d + j] - D.s_kin[((size_t)e * D.NK + ki) * 12 + j];
+      D.lam_kin[((size_t)e * D.NK + ki) * 12 + j] -= rho * r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { C.rho = rho; C.r_prev = res; C.residual = res; C.al_rounds = rounds; C.inner_conv = 0; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (C.phase == PHASE_ACTIVE && C.newton >= D.max_newton) { C.phase = PHASE_FAILED; C.status = ENV_NEWTON_STALL; }
+    if (C.phase == PHASE_ACTIVE) atomicOr(D.any_active, 1);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// step begin / end
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (C.disabled) { if (threadIdx.x == 0) C.phase = PHASE_IDLE; return; }
+  double* q = D.q + (size_t)e * D.n;
+  double* qn = D.qn + (size_t)e * D.n;
+  double* qt = D.qt + (size_t)e * D.n;
+  const double* vel = D.vel + (size_t)e * D.n;
+  for (int i = threadIdx.x; i < D.n; i += blockDim.x) { qn[i] = q[i]; qt[i] = q[i] + D.dt * vel[i]; }
+  const double* yk = D.ykin + (size_t)e * D.NK * 12;
+  for (int i = threadIdx.x; i < D.NK * 12; i += blockDim.x) {
+    D.s_kin[(size_t)e * D.NK * 12 + i] = yk[i];
+    D.lam_kin[(size_t)e * D.NK * 12 + i] = 0.0;
+  }
+  for (int c = threadIdx.x; c < D.NC; c += blockDim.x) {
+    int b = D.att_body[c], ki = D.kin_of_body[b];
+    const double* y = ki >= 0 ? yk + 12 * ki : body_y(D, e, b);
+    st3(D.s_att + ((size_t)e * D.NC + c) * 3, embed(y, ld3(D.att_local + 3 * c)));
+    st3(D.lam_att + ((size_t)e * D.NC + c) * 3, mk(0, 0, 0));
+  }
+  if (threadIdx.x == 0) {
+    C.phase = PHASE_ACTIVE; C.status = ENV_OK; C.inner_conv = 0; C.newton = 0; C.pcg = 0; C.ls_bt = 0;
+    C.al_rounds = 0; C.n_act = 0; C.ncand = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;
+    C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_end(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (C.phase == PHASE_IDLE) return;
+  double* q = D.q + (size_t)e * D.n;
+  const double* qn = D.qn + (size_t)e * D.n;
+  double* vel = D.vel + (size_t)e * D.n;
+  const bool ok = C.phase == PHASE_DONE;
+  __syncthreads();
+  for (int i = threadIdx.x; i < D.n; i += blockDim.x) {
+    if (ok) vel[i] = (q[i] - qn[i]) / D.dt;
+    else q[i] = qn[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (!ok) {
+      if (C.phase == PHASE_ACTIVE) C.status = ENV_NEWTON_STALL;
+      C.phase = PHASE_FAILED;
+      C.disabled = 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// state I/O helpers, validation, readout
+// ------------------------------------------------------------------------------------------
+__global__ void k_scatter_y(Dev D, int env0, int which /*0: y→ystat+q, 1: ydot→vel, 2: zero vel bodies*/) {
+  const int e = env0 + blockIdx.x;
+  const double* st = D.ystage + (size_t)e * D.NA * 12;
+  for (int i = threadIdx.x; i < D.NA * 12; i += blockDim.x) {
+    int b = i / 12, j = i % 12, s = D.dof_slot[b];
+    if (which == 0) {
+      D.ystat[(size_t)e * D.NA * 12 + i] = st[i];
+      if (s >= 0) D.q[(size_t)e * D.n + 3 * D.V + 12 * s + j] = st[i];
+    } else if (s >= 0) {
+      D.vel[(size_t)e * D.n + 3 * D.V + 12 * s + j] = which == 1 ? st[i] : 0.0;
+    }
+  }
+}
+__global__ void k_gather_y(Dev D, int env0, int which /*0: y, 1: ydot*/) {
+  const int e = env0 + blockIdx.x;
+  double* st = D.ystage + (size_t)e * D.NA * 12;
+  for (int i = threadIdx.x; i < D.NA * 12; i += blockDim.x) {
+    int b = i / 12, j = i % 12, s = D.dof_slot[b];
+    if (which == 0) st[i] = s >= 0 ? D.q[(size_t)e * D.n + 3 * D.V + 12 * s + j] : D.ystat[(size_t)e * D.NA * 12 + i];
+    else st[i] = s >= 0 ? D.vel[(size_t)e * D.n + 3 * D.V + 12 * s + j] : 0.0;
+  }
+}
+
+// after set_state: L_env (bbox diagonal of all vertices), inversion and contact-distance checks
+__global__ void __launch_bounds__(NTHREADS) k_validate(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  __shared__ double red[32];
+  const double* P = D.P + (size_t)e * D.NVall * 3;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int gv = threadIdx.x; gv < D.NVall; gv += blockDim.x)
+    for (int c = 0; c < 3; ++c) { lo[c] = fmin(lo[c], P[3 * gv + c]); hi[c] = fmax(hi[c], P[3 * gv + c]); }
+  double L2 = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    double l = block_min(lo[c], red), h = block_max(hi[c], red);
+    L2 += (h - l) * (h - l);
+  }
+  const double* q = D.q + (size_t)e * D.n;
+  int bad = 0;
+  for (int t = threadIdx.x; t < D.T; t += blockDim.x) {
+    int4 tv = reinterpret_cast<const int4*>(D.tets)[t];
+    v3 x[4] = {ld3(q + 3 * tv.x), ld3(q + 3 * tv.y), ld3(q + 3 * tv.z), ld3(q + 3 * tv.w)};
+    double F[9];
+    deformation_gradient(x, D.Dmi + 9 * t, F);
+    if (!(det33(F) > 0.0)) bad = 1;
+  }
+  const int* ca = D.cand_a + (size_t)e * D.cand_cap;
+  const int* cb = D.cand_b + (size_t)e * D.cand_cap;
+  for (int k = threadIdx.x; k < C.ncand; k += blockDim.x) {
+    int kind = (ca[k] >> 30) & 1, a = ca[k] & ((1 << 30) - 1), b = cb[k], vid[4];
+    pair_vids(D, kind, a, b, vid);
+    v3 X[4];
+    for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]);
+    double d2;
+    classify(kind, X, &d2);
+    if (!(d2 > 0.0)) bad = 1;
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    C.L = sqrt(L2);
+    if (C.overflow) { C.status = ENV_CAPACITY; C.disabled = 1; C.phase = PHASE_IDLE; }
+    else if (bad) { C.status = ENV_BAD_STATE; C.disabled = 1; C.phase = PHASE_IDLE; }
+    else { C.status = ENV_OK; C.disabled = 0; C.phase = PHASE_IDLE; }
+    C.overflow = 0;
+  }
+}
+
+__global__ void k_readout(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  const double* q = D.q + (size_t)e * D.n;
+  auto delta = [&](int v, int pad) -> v3 {
+    int b = D.pad_mount[pad];
+    const double* T = D.pad_T + 12 * pad;
+    v3 x = ld3(q + 3 * v), loc;
+    if (b >= 0) {
+      const double* y = body_y(D, e, b);
+      double Ai[9];
+      inv33(y + 3, Ai);
+      loc = mul33(Ai, x - mk(y[0], y[1], y[2]));
+    } else loc = x;
+    return mul33T(T + 3, loc - ld3(T)) - ld3(D.Xrest + 3 * v);
+  };
+  for (int i = threadIdx.x; i < D.NCOAT; i += blockDim.x)
+    st3(D.out_coat + ((size_t)e * D.NCOAT + i) * 3, delta(D.coat_vert[i], D.coat_pad[i]));
+  for (int i = threadIdx.x; i < D.NMARK; i += blockDim.x) {
+    v3 pos = mk(0, 0, 0), fl = mk(0, 0, 0);
+    for (int j = 0; j < 3; ++j) {
+      int v = D.mark_tri[3 * i + j];
+      double a = D.mark_bary[3 * i + j];
+      pos += a * ld3(q + 3 * v);
+      fl += a * delta(v, D.mark_pad[i]);
+    }
+    st3(D.out_mpos + ((size_t)e * D.NMARK + i) * 3, pos);
+    st3(D.out_mflow + ((size_t)e * D.NMARK + i) * 3, fl);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host launchers
+// ------------------------------------------------------------------------------------------
+static bool g_tables_ready = false;
+cudaError_t init_tables() {
+  if (g_tables_ready) return cudaSuccess;
+  unsigned char r[PH], c[PH];
+  for (int i = 0; i < 12; ++i)
+    for (int j = i; j < 12; ++j) { int k = sym_idx(i, j, 12); r[k] = (unsigned char)i; c[k] = (unsigned char)j; }
+  cudaError_t err = cudaMemcpyToSymbol(c_unpack_r, r, PH);
+  if (err == cudaSuccess) err = cudaMemcpyToSymbol(c_unpack_c, c, PH);
+  if (err == cudaSuccess) g_tables_ready = true;
+  return err;
+}
+
+void launch_positions(const Dev& D, int env0, int ne, int with_p, int force, cudaStream_t s) {
+  k_positions<<<ne, NTHREADS, 0, s>>>(D, env0, with_p, force);
+}
+void launch_broad(const Dev& D, int env0, int ne, int swept, int force, cudaStream_t s) {
+  k_broad<<<ne, NTHREADS, 0, s>>>(D, env0, swept, force);
+}
+void launch_narrow(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  size_t smem = (size_t)(2 * D.V + 1) * sizeof(int);
+  k_narrow<<<ne, NTHREADS, smem, s>>>(D, env0, force);
+}
+void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  dim3 grid((D.T + NTHREADS - 1) / NTHREADS, ne);
+  if (D.T > 0) k_tets<<<grid, NTHREADS, 0, s>>>(D, env0, force);
+}
+void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  k_pairs<<<ne, NTHREADS, 0, s>>>(D, env0, force);
+}
+void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  k_assemble<<<ne, NTHREADS, 0, s>>>(D, env0, force);
+}
+void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  k_pcg<<<ne, NTHREADS, 0, s>>>(D, env0, force);
+}
+void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s) {
+  k_spmv<<<1, NTHREADS, 0, s>>>(D, env0, x, y);
+}
+void launch_ccd(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  k_ccd<<<ne, NTHREADS, 0, s>>>(D, env0, force);
+}
+void launch_energy(const Dev& D, int env0, int ne, double alpha, cudaStream_t s) {
+  k_energy<<<ne, NTHREADS, 0, s>>>(D, env0, alpha);
+}
+void launch_linesearch(const Dev& D, int env0, int ne, cudaStream_t s) {
+  k_linesearch<<<ne, NTHREADS, 0, s>>>(D, env0);
+}
+void launch_control(const Dev& D, int env0, int ne, cudaStream_t s) {
+  k_control<<<ne, NTHREADS, 0, s>>>(D, env0);
+}
+void launch_begin(const Dev& D, int env0, int ne, cudaStream_t s) { k_begin<<<ne, NTHREADS, 0, s>>>(D, env0); }
+void launch_end(const Dev& D, int env0, int ne, cudaStream_t s) { k_end<<<ne, NTHREADS, 0, s>>>(D, env0); }
+void launch_scatter_y(const Dev& D, int env0, int ne, int which, cudaStream_t s) {
+  k_scatter_y<<<ne, 128, 0, s>>>(D, env0, which);
+}
+void launch_gather_y(const Dev& D, int env0, int ne, int which, cudaStream_t s) {
+  k_gather_y<<<ne, 128, 0, s>>>(D, env0, which);
+}
+void launch_validate(const Dev& D, int env0, int ne, cudaStream_t s) { k_validate<<<ne, NTHREADS, 0, s>>>(D, env0); }
+void launch_readout(const Dev& D, int env0, int ne, cudaStream_t s) { k_readout<<<ne, 128, 0, s>>>(D, env0); }
+
+}  // namespace tac

@@ -1,0 +1,26 @@
+// launch.h — host-side launchers of the per-env kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include "impl.cuh"
+
+namespace tac {
+cudaError_t init_tables();
+void launch_positions(const Dev& D, int env0, int ne, int with_p, int force, cudaStream_t s);
+void launch_broad(const Dev& D, int env0, int ne, int swept, int force, cudaStream_t s);
+void launch_narrow(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s);
+void launch_ccd(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+void launch_energy(const Dev& D, int env0, int ne, double alpha, cudaStream_t s);
+void launch_linesearch(const Dev& D, int env0, int ne, cudaStream_t s);
+void launch_control(const Dev& D, int env0, int ne, cudaStream_t s);
+void launch_begin(const Dev& D, int env0, int ne, cudaStream_t s);
+void launch_end(const Dev& D, int env0, int ne, cudaStream_t s);
+void launch_scatter_y(const Dev& D, int env0, int ne, int which, cudaStream_t s);
+void launch_gather_y(const Dev& D, int env0, int ne, int which, cudaStream_t s);
+void launch_validate(const Dev& D, int env0, int ne, cudaStream_t s);
+void launch_readout(const Dev& D, int env0, int ne, cudaStream_t s);
+}  // namespace tac
