@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the batched IPC + ABD Newton step (Taccel, arXiv 2504.12908) on B200.
+
+A "step" is one backward-Euler time step of EVERY env of the workload (BASELINE.json configs[1],
+SURVEY §8(d) C2): peg insertion with dual low-res gel pads, 1024 envs per GPU, Δt = 0.02 s, the
+scripted 200-step episode from step 0.  Each timed step = set_targets (device-resident target
+table) + tac_step + tac_get_gel_deformation.  Envs are sharded across GPUs with no
+collective on the hot path (weak scaling: 1024 envs per GPU, global env ids seed the inputs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl taccel|reference]
+
+metric value = whole-job env-steps/s (all ranks) = N·E·K / max-over-ranks CUDA-event time.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "peg-insertion env-steps/s and ×real-time, dual sensors, at 1/2/4/8 B200"
+WORKLOAD = "C2: peg insertion, dual low-res sensors (2 pads x 8x6x3 lattice, 144 nodes/350 tets each), " \
+           "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="taccel", choices=["taccel", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--envs-per-gpu", type=int, default=1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="add the per-phase breakdown to the JSON line")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip() == "Active":
+                        reasons.add(nm)
+            except Exception:
+                pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------------
+# CPU oracle baseline (the oracle as it stands, single thread, bounded sample)
+# ----------------------------------------------------------------------------------------------
+def oracle_run(cfg_name, n_steps, warmup=0):
+    import torch
+    torch.set_num_threads(1)
+    from paper_2504_12908_b200 import scenes as S
+    from oracle import mesh as M
+    from oracle import solver as SO
+    sc = S.make_scene(cfg_name)
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=warmup + n_steps)
+    st = SO.State(ei.x0[0].copy(), np.zeros_like(ei.x0[0]), ei.y0[0].copy(), np.zeros_like(ei.y0[0]))
+    L = M.env_scale(mod, st.x, st.y)
+    for k in range(warmup):
+        st, _ = SO.step(mod, st, ei.ykin[k, 0], L_env=L)
+    t0 = time.perf_counter()
+    for k in range(warmup, warmup + n_steps):
+        st, _ = SO.step(mod, st, ei.ykin[k, 0], L_env=L)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg_name, n_steps=2):
+    secs = oracle_run(cfg_name, n_steps)
+    return {"value": n_steps / secs, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{cfg_name} env 0, steps 0-{n_steps - 1} (1 env), CPU oracle as it stands "
+                      f"(numpy/torch-autograd fp64, exact sparse direct Newton solve), 1 thread, {secs:.1f} s"}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    warm = a.warmup
+    secs = oracle_run(a.config, a.steps, warmup=warm)
+    v = a.steps / secs
+    dt = 0.02
+    line = {"metric": METRIC, "value": v, "unit": "env-steps/s", "impl": "reference", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": warm, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD + " — reference arm: the CPU oracle advancing env 0 (one env per step)",
+                       "envs_per_step": 1, "dt": dt},
+            "x_realtime": v * dt,
+            "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{a.config} env 0, steps {warm}-{warm + a.steps - 1}, 1 thread"},
+            "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------
+# the CUDA path
+# ----------------------------------------------------------------------------------------------
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2504_12908_b200 import scenes as S
+    from paper_2504_12908_b200 import taccel as T
+    from paper_2504_12908_b200.build import build
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.barrier()
+
+    sc = S.make_scene(a.config)
+    E = a.envs_per_gpu
+    W, K = a.warmup, a.steps
+    n_script = W + K + 1
+    ids = np.arange(rank * E, (rank + 1) * E)
+    ei = S.env_inputs(sc, ids, n_steps=n_script)
+    stream = torch.cuda.current_stream(dev)
+    batch = T.Batch(sc, E, device=local, stream=stream)
+    st = batch.set_state(ei.x0, ei.y0)
+    assert (st == 0).all(), f"bad initial states: {np.unique(st)}"
+    ykin_dev = torch.tensor(ei.ykin, device=dev)                     # (S, E, NK, 12) device-resident
+    out_dev = batch.get_gel_deformation()
+
+    def step_dev(k):
+        batch.set_targets(ykin_dev[k])
+        s = batch.step(1)
+        batch.get_gel_deformation(out=out_dev)
+        return s
+
+    fails = 0
+    for k in range(W):
+        fails += int((step_dev(k) != 0).sum())
+    saved = batch.get_state()                                          # for the e2e replay
+    stats0 = batch.stats()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    batch.profile(True)
+    batch.profile_read(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    ev0.record(stream)
+    for k in range(W, W + K):
+        fails += int((step_dev(k) != 0).sum())
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    prof = batch.profile_read(reset=True)
+    batch.profile(False)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    stats1 = batch.stats()
+
+    # per-step solver statistics over the timed region
+    d_newton = sum(s["newton_iters"] for s in stats1)  # last step only
+    pcg_iters = sum(s1["pcg_iters_total"] - s0["pcg_iters_total"] for s0, s1 in zip(stats0, stats1))
+    pcg_bytes = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
+
+    # ---- e2e: replay the same K steps through the C ABI with pinned HOST buffers ----
+    e2e = None
+    if not a.no_e2e:
+        x, xd, y, yd = saved
+        batch.set_state(x, y, xd, yd)
+        ykin_host = torch.from_numpy(np.ascontiguousarray(ei.ykin)).pin_memory()
+        outs = tuple(torch.empty(t.shape, dtype=torch.float64).pin_memory() for t in out_dev)
+        h2d = ykin_host[0].numel() * 8
+        d2h = sum(t.numel() * 8 for t in outs)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for k in range(W, W + K):
+            batch.set_targets(ykin_host[k])
+            batch.step(1)
+            batch.get_gel_deformation(out=outs)                      # device→host read of the result
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        ms_e2e = max(e0.elapsed_time(e1), 1e3 * wall)
+        e2e = {"value": None, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "_ms": ms_e2e}
+
+    # ---- max over ranks ----
+    tot = torch.tensor([ms, e2e["_ms"] if e2e else 0.0], device=dev, dtype=torch.float64)
+    cnt = torch.tensor([float(fails), float(pcg_iters), float(pcg_bytes)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    ms, ms_e2e = float(tot[0]), float(tot[1])
+    fails, pcg_iters, pcg_bytes = (float(v) for v in cnt)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    n_env_total = E * world
+    value = n_env_total * K / (ms / 1e3)
+    dt = sc.config.dt
+    peaks = load_peaks()
+    hbm_peak, peak_src = (peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (copy, burst)") if peaks else (6650.0, "fallback 6.65 TB/s")
+    # dominant kernel (largest share of device time) and its roofline
+    phases = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1] > 0}
+    dom = max(phases, key=lambda k: phases[k]["ms"]) if phases else None
+    launches = int(sum(v["launches"] for v in phases.values()))
+    roof = None
+    if "pcg" in phases and phases["pcg"]["ms"] > 0:
+        # rank-0 PCG launches: algorithmic bytes / kernel time (local rank's own counters)
+        pcg_ms = phases["pcg"]["ms"]
+        local_bytes = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
+        ach = local_bytes / (pcg_ms / 1e3) / 1e9
+        roof = {"kernel": "k_pcg (block-Jacobi PCG, one CTA per env)", "bound": "hbm", "achieved": ach,
+                "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                "peak_source": peak_src, "share_of_step": pcg_ms / ms,
+                "alg_bytes_per_launch": local_bytes / max(phases["pcg"]["launches"], 1),
+                "dominant_kernel": dom}
+    line = {
+        "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "envs_per_gpu": E, "envs_total": n_env_total, "dt": dt,
+                   "episode_steps_timed": f"{W}-{W + K - 1}", "parallelism": f"env-sharded x{world}",
+                   "l2": "inputs larger than L2: per-step working set ~%.1f GB/GPU > 126 MB L2" %
+                         (batch.workspace.numel() / 1e9)},
+        "x_realtime": value * dt,
+        "paper_context": "Taccel: 915 env-steps/s = 18.30x real-time, >4096 envs, 1x H100 FP64 (P:L230, Table 1) — context, not this workload",
+        "roofline": roof,
+        "gpu_launches": launches,
+        "solver": {"pcg_iters_per_step_per_env": pcg_iters / (K * n_env_total),
+                   "failed_env_steps": fails,
+                   "newton_iters_last_step_mean": d_newton / E},
+        "clocks": clk,
+    }
+    if e2e:
+        e2e["value"] = n_env_total * K / (ms_e2e / 1e3)
+        e2e.pop("_ms")
+        line["e2e"] = e2e
+    if a.phases:
+        line["phases"] = phases
+    if world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a.config)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -114,13 +114,17 @@ typedef struct {
   double pcg_eta;                /* PCG stops at rᵀz ≤ η² r₀ᵀz₀                                 */
   double armijo_c, accd_s, al_rho0;
   int32_t max_newton, max_al_rounds, max_pcg, max_accd_iters, ee_mollifier;
+  int32_t hessian_mode;          /* 0: PSD-projected element Hessians; 1: exact Hessian first, projected
+                                    fallback with back-off when PCG meets dᵀHd ≤ 0 or gᵀp ≥ 0 (DESIGN R14b) */
   int32_t cand_capacity_per_env, active_capacity_per_env;
 } tac_config;
 
 typedef struct {
   int32_t status;                /* tac_env_status of the last step */
-  int32_t newton_iters, pcg_iters, ls_backtracks, n_active, al_rounds, n_candidates;
-  double alpha_min, energy, constraint_residual;
+  int32_t newton_iters, pcg_iters, ls_backtracks, n_active, al_rounds, n_candidates;  /* last step */
+  double alpha_min, energy, constraint_residual;                                     /* last step */
+  int64_t pcg_iters_total;       /* cumulative since tac_batch_create                         */
+  double pcg_alg_bytes_total;    /* cumulative algorithmic PCG bytes (DESIGN.md §5 B_pcg model) */
 } tac_env_stats;
 
 struct tac_batch;
@@ -167,16 +171,27 @@ tac_status tac_get_stats(tac_batch* b, tac_env_stats* out /* [E] host */, void* 
 
 const char* tac_last_error(void);
 
+/* ---- tracing: CUDA-event phase timers on the launch stream ----------------------------------
+ * When enabled, every kernel launch of tac_step is bracketed by cudaEventRecord on `stream` and
+ * its device time is accumulated per phase.  tac_profile_read copies the per-phase totals (ms)
+ * and launch counts for the TAC_NPHASES phases (names from tac_profile_phase_name) and optionally
+ * resets them. */
+#define TAC_NPHASES 16
+tac_status tac_profile_enable(tac_batch* b, int32_t enable);
+tac_status tac_profile_read(tac_batch* b, double* ms, int64_t* launches, int32_t reset);
+const char* tac_profile_phase_name(int32_t phase);
+
 /* ---- parity hooks (exported, test-only; host buffers) ---------------------------------------
  * tac_debug_eval: at (x [V][3], y [NA][12]) of env `env`, with x̃/ỹ from the env's last set_state
  * and kinematic targets from the last set_targets, and AL multipliers lam_att [NC][3],
  * lam_kin [NK][12] (NULL → 0) and penalty rho (≤ 0 → al_rho0): the six energy terms
  * e_terms[6] = {inertia, elastic, ortho, gravity, barrier, AL}, the gradient grad [n] over
  * q = [x; y of non-static bodies] and hv = H·v_in [n] with H the PSD-projected Hessian (any
- * output may be NULL).  The active set is recomputed at (x, y) through the spatial hash. */
+ * output may be NULL); exact_hessian = 1 uses the unprojected element Hessians instead.  The
+ * active set is recomputed at (x, y) through the spatial hash. */
 tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x, const double* y, const double* lam_att,
-                          const double* lam_kin, double rho, const double* v_in, double* e_terms, double* grad,
-                          double* hv, void* stream);
+                          const double* lam_kin, double rho, int32_t exact_hessian, const double* v_in,
+                          double* e_terms, double* grad, double* hv, void* stream);
 /* Active pairs at (x, y): rows (kind, a, b) in canonical order. */
 tac_status tac_debug_active_pairs(tac_batch* b, int32_t env, const double* x, const double* y, int32_t* pairs,
                                   int32_t cap, int32_t* count, void* stream);

@@ -28,35 +28,61 @@ def _boxes(P0, P1, idx):
     return lo, hi
 
 
+def _overlap_matrix(qlo, qhi, tlo_i, thi_i):
+    """M[i, j] = query box i (raw) overlaps target box j (inflated by d̂)."""
+    return (np.all(qlo[:, None, :] <= thi_i[None, :, :], 2) & np.all(tlo_i[None, :, :] <= qhi[:, None, :], 2))
+
+
 def candidate_pairs(model: Model, P0, P1=None):
     """Brute-force candidate set over all allowed pairs (reading R8/R11): returns (kind, a, b) rows
     in canonical order.  Query box raw, target box inflated by d̂:  lo_q ≤ hi_t + d̂ and
-    lo_t − d̂ ≤ hi_q on every axis."""
+    lo_t − d̂ ≤ hi_q on every axis.  Evaluated body pair by body pair; primitives whose box misses
+    the other body's (inflated) bounding box are skipped, which cannot change the result because
+    the predicate is monotone in the boxes (fl(min lo − d̂) = min fl(lo − d̂))."""
     dhat = model.scene.config.dhat
     P1 = P0 if P1 is None else P1
-    out = []
-    # PT
+    NB = model.allowed.shape[0]
     sv = model.surf_verts
     vlo, vhi = _boxes(P0, P1, sv[:, None])
     tlo, thi = _boxes(P0, P1, model.tris)
-    tlo, thi = tlo - dhat, thi + dhat
-    vb = model.vert_body[sv]
-    for i, v in enumerate(sv):
-        ok = model.allowed[vb[i], model.tri_body]
-        ok &= np.all(vlo[i] <= thi, 1) & np.all(tlo <= vhi[i], 1)
-        for t in np.nonzero(ok)[0]:
-            out.append((0, int(v), int(t)))
-    # EE
     elo, ehi = _boxes(P0, P1, model.edges)
-    elo_i, ehi_i = elo - dhat, ehi + dhat
-    NE = len(model.edges)
-    for a in range(NE):
-        bs = np.arange(a + 1, NE)
-        ok = model.allowed[model.edge_body[a], model.edge_body[bs]]
-        ok &= np.all(elo[a] <= ehi_i[bs], 1) & np.all(elo_i[bs] <= ehi[a], 1)
-        for b in bs[ok]:
-            out.append((1, a, int(b)))
-    return np.asarray(out, np.int64).reshape(-1, 3)
+    vb, tb, eb = model.vert_body[sv], model.tri_body, model.edge_body
+
+    def body_box(lo, hi, mask):
+        return lo[mask].min(0), hi[mask].max(0)
+
+    out = []
+    for bq in range(NB):
+        for bt in range(NB):
+            if not model.allowed[bq, bt]:
+                continue
+            # PT: vertices of bq against triangles of bt
+            qm, tm = vb == bq, tb == bt
+            if qm.any() and tm.any():
+                Tlo, Thi = body_box(tlo, thi, tm)
+                Qlo, Qhi = body_box(vlo, vhi, qm)
+                qi = np.nonzero(qm & np.all(vlo <= Thi + dhat, 1) & np.all(Tlo - dhat <= vhi, 1))[0]
+                ti = np.nonzero(tm & np.all(Qlo <= thi + dhat, 1) & np.all(tlo - dhat <= Qhi, 1))[0]
+                if len(qi) and len(ti):
+                    Mx = _overlap_matrix(vlo[qi], vhi[qi], tlo[ti] - dhat, thi[ti] + dhat)
+                    ii, jj = np.nonzero(Mx)
+                    out += [(0, int(sv[qi[i]]), int(ti[j])) for i, j in zip(ii, jj)]
+            # EE: edges of bq (lower indices) against edges of bt, only for bq < bt
+            if bq < bt:
+                qm, tm = eb == bq, eb == bt
+                if qm.any() and tm.any():
+                    Tlo, Thi = body_box(elo, ehi, tm)
+                    Qlo, Qhi = body_box(elo, ehi, qm)
+                    qi = np.nonzero(qm & np.all(elo <= Thi + dhat, 1) & np.all(Tlo - dhat <= ehi, 1))[0]
+                    ti = np.nonzero(tm & np.all(Qlo <= ehi + dhat, 1) & np.all(elo - dhat <= Qhi, 1))[0]
+                    if len(qi) and len(ti):
+                        Mx = _overlap_matrix(elo[qi], ehi[qi], elo[ti] - dhat, ehi[ti] + dhat)
+                        ii, jj = np.nonzero(Mx)
+                        out += [(1, int(qi[i]), int(ti[j])) for i, j in zip(ii, jj)]
+    arr = np.asarray(out, np.int64).reshape(-1, 3)
+    if len(arr):
+        arr = arr[np.lexsort((arr[:, 2], arr[:, 1], arr[:, 0]))]
+    return arr
 
 
 def classify(model: Model, P, cand):

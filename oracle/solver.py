@@ -91,7 +91,8 @@ def any_inverted(model: Model, x):
 
 def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
     """Block-Jacobi PCG for H p = −g from p₀ = 0 (3×3 per soft vertex, 12×12 per body); stop
-    at rᵀz ≤ η² r₀ᵀz₀ or max_iter (reading R15; P:L325 names PCG)."""
+    at rᵀz ≤ η² r₀ᵀz₀ or max_iter (reading R15; P:L325 names PCG).  Returns (None, it) if a
+    search direction with dᵀHd ≤ 0 is met (H not SPD)."""
     n = len(g)
     V = model.V
     blocks = [(3 * v, 3) for v in range(V)] + [(3 * V + 12 * s, 12) for s in range(model.n_dof_bodies)]
@@ -116,7 +117,10 @@ def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
     it = 0
     while it < max_iter and rz > eta * eta * rz0:
         q = H @ d
-        a = rz / (d @ q)
+        dq = d @ q
+        if not (dq > 0):
+            return None, it + 1          # negative curvature: H is not SPD
+        a = rz / dq
         p += a * d
         r -= a * q
         z = prec(r)
@@ -125,6 +129,27 @@ def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
         rz = rz_new
         it += 1
     return p, it
+
+
+def _solve_spd(model, H, g, solver, cfg, stats):
+    """Newton direction from the EXACT Hessian if it is SPD (Cholesky succeeds / CG meets no
+    negative curvature) and the direction is a descent direction; None otherwise (reading R14b)."""
+    if solver == "direct":
+        Hd = H.toarray()
+        try:
+            Lc = np.linalg.cholesky(Hd)
+        except np.linalg.LinAlgError:
+            return None
+        import scipy.linalg as sla
+        p = sla.cho_solve((Lc, True), -g)
+    else:
+        p, it = block_jacobi_pcg(model, H, g, cfg.pcg_eta, cfg.max_pcg)
+        stats.pcg_iters += it
+        if p is None:
+            return None
+    if not (g @ p < 0):
+        return None
+    return p
 
 
 def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, trace=None):
@@ -137,20 +162,34 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
     x, y = st.x.copy(), st.y.copy()
     r_prev = np.inf
     done = False
+    hold = 0          # projected iterations left before the exact Hessian is tried again
+    nfail = 0         # consecutive failed exact attempts (back-off 2, 4, ... 64)
+    mode = cfg.hessian_mode
     for al_round in range(cfg.max_al_rounds):
         stats.al_rounds = al_round + 1
         converged = False
         while stats.newton_iters < cfg.max_newton:
             P = all_positions(model, x, y)
             pairs = C.active_pairs(model, P)
-            g, H = En.assemble(model, ctx, x, y, pairs)
-            if solver == "direct":
-                p = spla.spsolve(sp.csc_matrix(H), -g)
-            else:
-                p, it = block_jacobi_pcg(model, H, g, cfg.pcg_eta, cfg.max_pcg)
-                stats.pcg_iters += it
+            p = None
+            if mode == 1 and hold == 0:
+                g, H = En.assemble(model, ctx, x, y, pairs, project=False)
+                p = _solve_spd(model, H, g, solver, cfg, stats)
+                if p is None:
+                    nfail += 1
+                    hold = min(2 ** nfail, 64)
+                else:
+                    nfail = 0
+            if p is None:
+                g, H = En.assemble(model, ctx, x, y, pairs)
+                if solver == "direct":
+                    p = spla.spsolve(sp.csc_matrix(H), -g)
+                else:
+                    p, it = block_jacobi_pcg(model, H, g, cfg.pcg_eta, cfg.max_pcg)
+                    stats.pcg_iters += it
+                hold = max(hold - 1, 0)
             stats.newton_iters += 1
-            if not np.all(np.isfinite(p)):
+            if p is None or not np.all(np.isfinite(p)):
                 stats.status = NONFINITE
                 break
             if embedded_inf_norm(model, p) <= cfg.newton_tol_rel * L:
@@ -179,7 +218,8 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
                 break
             stats.alpha_min = min(stats.alpha_min, alpha)
             if trace is not None:
-                trace.append(dict(alpha=alpha, E0=E0, E1=E1, p_inf=embedded_inf_norm(model, p)))
+                trace.append(dict(alpha=alpha, E0=E0, E1=E1, p_inf=embedded_inf_norm(model, p), hold=hold,
+                                  n_act=len(pairs)))
             x, y = xt, yt
         if stats.status != ENV_OK:
             break

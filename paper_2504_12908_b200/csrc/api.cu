@@ -382,7 +382,52 @@ struct tac_batch {
   size_t ws_bytes = 0;
   int* h_flag = nullptr;  // pinned
   std::vector<EnvCtl> hctl;
+  // tracing
+  bool prof = false;
+  double prof_ms[TAC_NPHASES] = {0};
+  long long prof_n[TAC_NPHASES] = {0};
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> pending;  // (phase, event index of start; stop = +1)
+  size_t ev_used = 0;
 };
+
+enum { PH_POSITIONS = 0, PH_BROAD_STATIC, PH_NARROW, PH_TETS, PH_PAIRS, PH_ASSEMBLE, PH_PCG, PH_BROAD_SWEPT, PH_CCD,
+       PH_LINESEARCH, PH_CONTROL, PH_BEGIN, PH_END, PH_READOUT, PH_SETSTATE, PH_OTHER };
+static const char* kPhaseNames[TAC_NPHASES] = {"positions", "broad_static", "narrow", "nh_tets", "barrier_pairs",
+                                              "assemble", "pcg", "broad_swept", "accd", "line_search", "control",
+                                              "step_begin", "step_end", "readout", "set_state", "other"};
+
+struct ProfScope {
+  tac_batch* b; int ph; cudaStream_t st; int idx = -1;
+  ProfScope(tac_batch* b_, int ph_, cudaStream_t st_) : b(b_), ph(ph_), st(st_) {
+    if (!b->prof) return;
+    if (b->ev_used + 2 > b->ev_pool.size()) {
+      for (int i = 0; i < 64; ++i) { cudaEvent_t e; cudaEventCreate(&e); b->ev_pool.push_back(e); }
+    }
+    idx = (int)b->ev_used;
+    b->ev_used += 2;
+    cudaEventRecord(b->ev_pool[idx], st);
+  }
+  ~ProfScope() {
+    if (idx < 0) return;
+    cudaEventRecord(b->ev_pool[idx + 1], st);
+    b->pending.push_back({ph, idx});
+  }
+};
+
+// resolve recorded events (the stream must be synchronised)
+static void prof_flush(tac_batch* b) {
+  for (auto& pe : b->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, b->ev_pool[pe.second], b->ev_pool[pe.second + 1]) == cudaSuccess) {
+      b->prof_ms[pe.first] += ms;
+      b->prof_n[pe.first] += 1;
+    }
+  }
+  b->pending.clear();
+  b->ev_used = 0;
+}
+#define PROF(ph) ProfScope _ps_##__LINE__(b, ph, st)
 
 static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   auto ti = [&](const std::vector<int>& v) { return C.take<int>(std::max<size_t>(v.size(), 1)); };
@@ -440,13 +485,14 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.dt = cfg->dt; D.dhat = cfg->dhat; D.kappa = cfg->kappa; D.tolN = cfg->newton_tol_rel; D.tolAL = cfg->al_tol_rel;
   D.eta = cfg->pcg_eta; D.armijo = cfg->armijo_c; D.accd_s = cfg->accd_s; D.rho0 = cfg->al_rho0; D.cell = H.cell;
   D.max_newton = cfg->max_newton; D.max_al = cfg->max_al_rounds; D.max_pcg = cfg->max_pcg;
-  D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier;
+  D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
 }
 
 static tac_status check_cfg(const tac_config* c) {
   if (!(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
-      c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1))
+      c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1) || c->hessian_mode < 0 ||
+      c->hessian_mode > 1)
     return fail(TAC_E_INVALID, "invalid tac_config");
   return TAC_OK;
 }
@@ -517,6 +563,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
 extern "C" tac_status tac_batch_destroy(tac_batch* b) {
   if (!b) return TAC_OK;
   if (b->h_flag) cudaFreeHost(b->h_flag);
+  for (auto e : b->ev_pool) cudaEventDestroy(e);
   delete b;
   return TAC_OK;
 }
@@ -593,24 +640,25 @@ extern "C" tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, con
 
 static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st) {
   Dev& D = b->D;
-  launch_positions(D, env0, ne, 0, 0, st);
-  launch_broad(D, env0, ne, 0, 0, st);
+  { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 0, 0, st); }
+  { PROF(PH_BROAD_STATIC); launch_broad(D, env0, ne, 0, 0, st); }
   for (int it = 0; it <= D.max_newton + 1; ++it) {
-    launch_positions(D, env0, ne, 0, 0, st);
-    launch_narrow(D, env0, ne, 0, st);
-    launch_tets(D, env0, ne, 0, st);
-    launch_pairs(D, env0, ne, 0, st);
-    launch_assemble(D, env0, ne, 0, st);
-    launch_pcg(D, env0, ne, 0, st);
-    launch_positions(D, env0, ne, 1, 0, st);
-    launch_broad(D, env0, ne, 1, 0, st);
-    launch_ccd(D, env0, ne, 0, st);
-    launch_linesearch(D, env0, ne, st);
+    { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 0, 0, st); }
+    { PROF(PH_NARROW); launch_narrow(D, env0, ne, 0, st); }
+    { PROF(PH_TETS); launch_tets(D, env0, ne, 0, st); }
+    { PROF(PH_PAIRS); launch_pairs(D, env0, ne, 0, st); }
+    { PROF(PH_ASSEMBLE); launch_assemble(D, env0, ne, 0, st); }
+    { PROF(PH_PCG); launch_pcg(D, env0, ne, 0, st); }
+    { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 1, 0, st); }
+    { PROF(PH_BROAD_SWEPT); launch_broad(D, env0, ne, 1, 0, st); }
+    { PROF(PH_CCD); launch_ccd(D, env0, ne, 0, st); }
+    { PROF(PH_LINESEARCH); launch_linesearch(D, env0, ne, st); }
     CUDA_TRY(cudaMemsetAsync(D.any_active, 0, sizeof(int), st));
-    launch_control(D, env0, ne, st);
+    { PROF(PH_CONTROL); launch_control(D, env0, ne, st); }
     CUDA_TRY(cudaMemcpyAsync(b->h_flag, D.any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
+    if (b->prof) prof_flush(b);
     if (!*b->h_flag) break;
   }
   return TAC_OK;
@@ -622,13 +670,14 @@ extern "C" tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_statu
   Dev& D = b->D;
   bool any_failed = false;
   for (int s = 0; s < n_steps; ++s) {
-    launch_begin(D, 0, D.E, st);
+    { PROF(PH_BEGIN); launch_begin(D, 0, D.E, st); }
     tac_status r = newton_loop(b, 0, D.E, st);
     if (r) return r;
-    launch_end(D, 0, D.E, st);
+    { PROF(PH_END); launch_end(D, 0, D.E, st); }
     CUDA_TRY(cudaGetLastError());
   }
   tac_status r = pull_ctl(b, st);
+  if (b->prof) prof_flush(b);
   if (r) return r;
   for (auto& c : b->hctl)
     if (c.phase == PHASE_FAILED) any_failed = true;
@@ -665,7 +714,7 @@ extern "C" tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_
   if (s) return s;
   cudaStream_t st = (cudaStream_t)stream;
   Dev& D = b->D;
-  launch_readout(D, env0, n, st);
+  { PROF(PH_READOUT); launch_readout(D, env0, n, st); }
   if (coated_disp && D.NCOAT)
     CUDA_TRY(cudaMemcpyAsync(coated_disp, D.out_coat + (size_t)env0 * D.NCOAT * 3, (size_t)n * D.NCOAT * 3 * 8, cudaMemcpyDefault, st));
   if (marker_pos && D.NMARK)
@@ -673,6 +722,7 @@ extern "C" tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_
   if (marker_flow && D.NMARK)
     CUDA_TRY(cudaMemcpyAsync(marker_flow, D.out_mflow + (size_t)env0 * D.NMARK * 3, (size_t)n * D.NMARK * 3 * 8, cudaMemcpyDefault, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  if (b->prof) prof_flush(b);
   return TAC_OK;
 }
 
@@ -685,8 +735,29 @@ extern "C" tac_status tac_get_stats(tac_batch* b, tac_env_stats* out, void* stre
     out[e].status = c.status; out[e].newton_iters = c.newton; out[e].pcg_iters = c.pcg; out[e].ls_backtracks = c.ls_bt;
     out[e].n_active = c.n_act; out[e].al_rounds = c.al_rounds; out[e].n_candidates = c.ncand;
     out[e].alpha_min = c.alpha_min; out[e].energy = c.energy; out[e].constraint_residual = c.residual;
+    out[e].pcg_iters_total = c.pcg_total; out[e].pcg_alg_bytes_total = c.pcg_bytes;
   }
   return TAC_OK;
+}
+
+extern "C" tac_status tac_profile_enable(tac_batch* b, int32_t enable) {
+  if (!b) return fail(TAC_E_INVALID, "null batch");
+  b->prof = enable != 0;
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_profile_read(tac_batch* b, double* ms, int64_t* launches, int32_t reset) {
+  if (!b) return fail(TAC_E_INVALID, "null batch");
+  for (int i = 0; i < TAC_NPHASES; ++i) {
+    if (ms) ms[i] = b->prof_ms[i];
+    if (launches) launches[i] = b->prof_n[i];
+    if (reset) { b->prof_ms[i] = 0; b->prof_n[i] = 0; }
+  }
+  return TAC_OK;
+}
+
+extern "C" const char* tac_profile_phase_name(int32_t phase) {
+  return (phase >= 0 && phase < TAC_NPHASES) ? kPhaseNames[phase] : "";
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -700,7 +771,7 @@ struct DebugScope {
 };
 
 static tac_status dbg_enter(DebugScope& S, const double* x, const double* y, const double* lam_att,
-                            const double* lam_kin, double rho) {
+                            const double* lam_kin, double rho, int exact = 0) {
   tac_batch* b = S.b;
   Dev& D = b->D;
   const int e = S.e;
@@ -722,6 +793,8 @@ static tac_status dbg_enter(DebugScope& S, const double* x, const double* y, con
   if (lam_att && D.NC) CUDA_TRY(cudaMemcpyAsync(D.lam_att + (size_t)e * D.NC * 3, lam_att, (size_t)D.NC * 24, cudaMemcpyHostToDevice, S.st));
   if (lam_kin && D.NK) CUDA_TRY(cudaMemcpyAsync(D.lam_kin + (size_t)e * D.NK * 12, lam_kin, (size_t)D.NK * 96, cudaMemcpyHostToDevice, S.st));
   if (rho > 0) CUDA_TRY(cudaMemcpyAsync(&D.ctl[e].rho, &rho, sizeof(double), cudaMemcpyHostToDevice, S.st));
+  static int flag[2] = {0, 1};
+  CUDA_TRY(cudaMemcpyAsync(&D.ctl[e].exact, &flag[exact ? 1 : 0], sizeof(int), cudaMemcpyHostToDevice, S.st));
   CUDA_TRY(cudaStreamSynchronize(S.st));
   return TAC_OK;
 }
@@ -755,11 +828,11 @@ static tac_status dbg_assemble(tac_batch* b, int e, cudaStream_t st) {
   if (!x || !y) return fail(TAC_E_INVALID, "x and y are required");
 
 extern "C" tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x, const double* y, const double* lam_att,
-                                     const double* lam_kin, double rho, const double* v_in, double* e_terms, double* grad,
-                                     double* hv, void* stream) {
+                                     const double* lam_kin, double rho, int32_t exact_hessian, const double* v_in,
+                                     double* e_terms, double* grad, double* hv, void* stream) {
   DBG_CHECK(b, env);
   DebugScope S{b, env, (cudaStream_t)stream};
-  tac_status s = dbg_enter(S, x, y, lam_att, lam_kin, rho);
+  tac_status s = dbg_enter(S, x, y, lam_att, lam_kin, rho, exact_hessian);
   Dev& D = b->D;
   if (!s) s = dbg_assemble(b, env, S.st);
   if (!s && e_terms) {

@@ -70,7 +70,7 @@ HD double nh_energy(const v3* x, const double* Dmi, double mu, double lam, bool*
 
 // Gradient g[12] (slot-major: 3*k + c) and packed-upper projected Hessian H[78] of scale·Ψ(F(x)).
 HD void nh_grad_hess(const v3* x, const double* Dmi, double mu, double lam, double scale, double* psi_out,
-                     double* g, double* H) {
+                     double* g, double* H, bool project = true) {
   double F[9];
   deformation_gradient(x, Dmi, F);
   double J = det33(F);
@@ -109,7 +109,7 @@ HD void nh_grad_hess(const v3* x, const double* Dmi, double mu, double lam, doub
   const double kk = mu - lam * lnJ;
   // negative modes: collect up to 9 (λ_m, Q_m) and subtract
   double negl[9]; double negQ[9][9]; int nneg = 0;
-  {
+  if (project) {
     double A3[9];
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j)

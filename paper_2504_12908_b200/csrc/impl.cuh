@@ -28,6 +28,9 @@ enum { ENV_OK = 0, ENV_NEWTON_STALL = 1, ENV_AL_INFEASIBLE = 2, ENV_CAPACITY = 3
 struct EnvCtl {
   int phase, status, inner_conv, newton, pcg, ls_bt, al_rounds, n_act, ncand, overflow;
   int disabled, pad_;
+  int exact, hold, nfail, xfail;   // exact-Hessian-first control (reading R14b)
+  long long pcg_total;
+  double pcg_bytes;
   double alpha_ccd, alpha_min, rho, r_prev, L, energy, residual, gp, pnorm, alpha;
 };
 
@@ -37,7 +40,7 @@ struct Dev {
   int cand_cap, act_cap, ent_cap;
   // ---- config ----
   double dt, dhat, kappa, tolN, tolAL, eta, armijo, accd_s, rho0, cell;
-  int max_newton, max_al, max_pcg, max_accd, mollify;
+  int max_newton, max_al, max_pcg, max_accd, mollify, hmode;
   double grav[3];
   // ---- template ----
   const int* tets;        // [T][4]

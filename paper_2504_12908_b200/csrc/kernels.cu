@@ -200,7 +200,7 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
 __global__ void __launch_bounds__(NTHREADS) k_broad(Dev D, int env0, int swept, int force) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
-  if (!force && (C.phase != PHASE_ACTIVE || (swept && C.inner_conv))) return;
+  if (!force && (C.phase != PHASE_ACTIVE || (swept && (C.inner_conv || C.xfail)))) return;
   __shared__ int cnt[NBUCKET + 1];
   __shared__ int cur[NBUCKET];
   __shared__ double red[32];
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
   for (int i = 0; i < 9; ++i) Dmi[i] = D.Dmi[9 * t + i];
   double g[12], H[PH];
   const double scale = D.dt * D.dt * D.vol[t];
-  nh_grad_hess(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, g, H);
+  nh_grad_hess(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, g, H, !D.ctl[e].exact);
   double* out = D.tetbuf + (size_t)e * TETBUF * D.T;
 #pragma unroll
   for (int i = 0; i < 12; ++i) out[(size_t)i * D.T + t] = g[i];
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NTHREADS) k_pairs(Dev D, int env0, int force) 
       if (r > c) S.A[i] = S.A[12 * c + r];
     }
     __syncwarp();
-    jacobi12_psd(S, lane, 32);
+    if (!C.exact) jacobi12_psd(S, lane, 32);
     for (int i = lane; i < PH; i += 32) aH[(size_t)PH * k + i] = S.A[12 * c_unpack_r[i] + c_unpack_c[i]];
     __syncwarp();
   }
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
       S.A[i] = (r < 9 && c < 9) ? ortho_hess_entry(y + 3, kv, r, c) : 0.0;
     }
     __syncwarp();
-    jacobi12_psd(S, lane, 32);
+    if (!C.exact) jacobi12_psd(S, lane, 32);
     double gb = 0.0;
     if (lane < 12) {
       int al = lane;
@@ -792,6 +792,7 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
     part = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
     double dAd = block_sum(part, red);
+    if (!(dAd > 0.0)) { bad = true; break; }          // H not SPD along d (uniform across the block)
     double alpha = rz / dAd;
     for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] += alpha * d[i]; r[i] -= alpha * Ad[i]; }
     __syncthreads();
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
     __syncthreads();
     rz = rzn;
     ++it;
-    if (!(rz == rz) || !(dAd > 0.0)) bad = true;
+    if (!(rz == rz)) bad = true;
   }
   // gᵀp and embedded ∞-norm
   part = 0.0;
@@ -820,12 +821,22 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
   double gp = block_sum(part, red);
   pm = block_max(pm, red);
   if (threadIdx.x == 0) {
+    const bool exact_failed = C.exact && (bad || !(gp < 0.0) || !(pm == pm));
     C.pcg += it;
-    C.newton += 1;
+    C.pcg_total += it;
+    // algorithmic bytes per PCG iteration (SURVEY §8(d) model):
+    // 72(V+E_s) + 4E_s + 640P + 624·ND + 48V + 624·ND + 96n
+    const double bpi = 72.0 * (D.V + D.NEs) + 4.0 * D.NEs + 640.0 * C.n_act + 1248.0 * D.ND + 48.0 * D.V + 96.0 * D.n;
+    C.pcg_bytes += bpi * it;
     C.gp = gp;
     C.pnorm = pm;
-    if (bad || !(pm == pm)) { C.phase = PHASE_FAILED; C.status = ENV_NONFINITE; }
-    else C.inner_conv = (pm <= D.tolN * C.L) ? 1 : 0;
+    if (exact_failed) {
+      C.xfail = 1;                                        // retry projected next pass (not counted)
+    } else {
+      C.newton += 1;
+      if (bad || !(pm == pm)) { C.phase = PHASE_FAILED; C.status = ENV_NONFINITE; }
+      else C.inner_conv = (pm <= D.tolN * C.L) ? 1 : 0;
+    }
   }
 }
 
@@ -864,7 +875,7 @@ __device__ double accd_pair(int kind, v3* X, v3* Pd, double s, double tc, int ma
 __global__ void __launch_bounds__(NTHREADS) k_ccd(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
-  if (!force && (C.phase != PHASE_ACTIVE || C.inner_conv)) return;
+  if (!force && (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail)) return;
   __shared__ double red[32];
   const double* P = D.P + (size_t)e * D.NVall * 3;
   const double* Pd = D.Pd + (size_t)e * D.NVall * 3;
@@ -997,7 +1008,7 @@ __global__ void __launch_bounds__(NTHREADS) k_energy(Dev D, int env0, double alp
 __global__ void __launch_bounds__(NTHREADS) k_linesearch(Dev D, int env0) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
-  if (C.phase != PHASE_ACTIVE || C.inner_conv) return;
+  if (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail) return;
   __shared__ double red[32];
   double t[6];
   int inv;
@@ -1043,6 +1054,22 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
     return;
   }
   double* q = D.q + (size_t)e * D.n;
+  // exact-Hessian-first schedule (reading R14b): a failed exact attempt backs off 2, 4, .. 64
+  // projected iterations; a successful one resets the back-off
+  if (threadIdx.x == 0) {
+    if (C.xfail) {
+      C.nfail += 1;
+      C.hold = min(1 << min(C.nfail, 6), 64);
+      C.exact = 0;
+      C.xfail = 0;
+    } else if (!C.exact) {
+      if (C.hold > 0) C.hold -= 1;
+      if (C.hold == 0 && D.hmode == 1) C.exact = 1;
+    } else {
+      C.nfail = 0;
+    }
+  }
+  __syncthreads();
   if (C.inner_conv) {
     const double* s_att = D.s_att + (size_t)e * D.NC * 3;
     double res = 0.0;
@@ -1121,6 +1148,7 @@ __global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
     C.phase = PHASE_ACTIVE; C.status = ENV_OK; C.inner_conv = 0; C.newton = 0; C.pcg = 0; C.ls_bt = 0;
     C.al_rounds = 0; C.n_act = 0; C.ncand = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;
     C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
+    C.exact = D.hmode == 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0;
   }
 }
 

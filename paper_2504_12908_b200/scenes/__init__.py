@@ -69,11 +69,12 @@ class Config:
     armijo_c: float = 1.0e-4
     accd_s: float = 0.1
     al_rho0: float = 1.0e8
-    max_newton: int = 200
+    max_newton: int = 400
     max_al_rounds: int = 8
     max_pcg: int = 2000
     max_accd_iters: int = 10000
     ee_mollifier: int = 1
+    hessian_mode: int = 1          # 0: always PSD-projected; 1: exact first, projected fallback (R14b)
     cand_capacity_per_env: int = 16384
     active_capacity_per_env: int = 4096
 

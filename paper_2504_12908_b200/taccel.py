@@ -54,14 +54,15 @@ class Config(ctypes.Structure):
                 ("armijo_c", ctypes.c_double), ("accd_s", ctypes.c_double), ("al_rho0", ctypes.c_double),
                 ("max_newton", ctypes.c_int32), ("max_al_rounds", ctypes.c_int32), ("max_pcg", ctypes.c_int32),
                 ("max_accd_iters", ctypes.c_int32), ("ee_mollifier", ctypes.c_int32),
-                ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32)]
+                ("hessian_mode", ctypes.c_int32), ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32)]
 
 
 class EnvStats(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("newton_iters", ctypes.c_int32), ("pcg_iters", ctypes.c_int32),
                 ("ls_backtracks", ctypes.c_int32), ("n_active", ctypes.c_int32), ("al_rounds", ctypes.c_int32),
                 ("n_candidates", ctypes.c_int32), ("alpha_min", ctypes.c_double), ("energy", ctypes.c_double),
-                ("constraint_residual", ctypes.c_double)]
+                ("constraint_residual", ctypes.c_double), ("pcg_iters_total", ctypes.c_int64),
+                ("pcg_alg_bytes_total", ctypes.c_double)]
 
 
 def header_symbols():
@@ -93,17 +94,21 @@ def load():
             "tac_get_state": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp],
             "tac_get_gel_deformation": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp],
             "tac_get_stats": [vp, ctypes.POINTER(EnvStats), vp],
-            "tac_debug_eval": [vp, ctypes.c_int32, vp, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp, vp],
+            "tac_debug_eval": [vp, ctypes.c_int32, vp, vp, vp, vp, ctypes.c_double, ctypes.c_int32, vp, vp, vp, vp, vp],
             "tac_debug_active_pairs": [vp, ctypes.c_int32, vp, vp, vp, ctypes.c_int32, c_int_p, vp],
             "tac_debug_candidates": [vp, ctypes.c_int32, vp, vp, vp, vp, ctypes.c_int32, c_int_p, vp],
             "tac_debug_accd": [vp, ctypes.c_int32, vp, vp, vp, c_double_p, vp],
             "tac_debug_pcg": [vp, ctypes.c_int32, vp, vp, vp, c_int_p, vp],
+            "tac_profile_enable": [vp, ctypes.c_int32],
+            "tac_profile_read": [vp, c_double_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
             f.argtypes = args
             f.restype = ctypes.c_int
         lib.tac_last_error.restype = ctypes.c_char_p
+        lib.tac_profile_phase_name.restype = ctypes.c_char_p
+        lib.tac_profile_phase_name.argtypes = [ctypes.c_int32]
         _lib = lib
     return _lib
 
@@ -280,8 +285,20 @@ class Batch:
         _check(self.lib.tac_get_stats(self.handle, arr, self._s()))
         return [{k: getattr(s, k) for k, _ in EnvStats._fields_} for s in arr]
 
+    # ---- tracing ---------------------------------------------------------------------------------
+    NPHASES = 16
+
+    def profile(self, enable: bool = True):
+        _check(self.lib.tac_profile_enable(self.handle, 1 if enable else 0))
+
+    def profile_read(self, reset: bool = False):
+        ms = (ctypes.c_double * self.NPHASES)()
+        n = (ctypes.c_int64 * self.NPHASES)()
+        _check(self.lib.tac_profile_read(self.handle, ms, n, 1 if reset else 0))
+        return {self.lib.tac_profile_phase_name(i).decode(): (ms[i], n[i]) for i in range(self.NPHASES)}
+
     # ---- parity hooks (host numpy) ------------------------------------------------------------
-    def debug_eval(self, env, x, y, lam_att=None, lam_kin=None, rho=0.0, v=None):
+    def debug_eval(self, env, x, y, lam_att=None, lam_kin=None, rho=0.0, v=None, exact=False):
         x, y = _f64(x), _f64(y)
         et = np.zeros(6)
         g = np.zeros(self.n_dof)
@@ -289,7 +306,7 @@ class Batch:
         _check(self.lib.tac_debug_eval(self.handle, env, _ptr(x), _ptr(y),
                                        _ptr(_f64(lam_att)) if lam_att is not None else None,
                                        _ptr(_f64(lam_kin)) if lam_kin is not None else None, float(rho),
-                                       _ptr(_f64(v)) if v is not None else None, _ptr(et), _ptr(g), _ptr(hv), self._s()))
+                                       1 if exact else 0, _ptr(_f64(v)) if v is not None else None, _ptr(et), _ptr(g), _ptr(hv), self._s()))
         return et, g, hv
 
     def _pairs(self, fn, env, x, y, *extra):

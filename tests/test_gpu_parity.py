@@ -92,6 +92,10 @@ def test_energy_gradient_hvp_parity(name, seed, press):
     go, H = En.assemble(mod, ctx, x, y, pairs)
     assert rel_inf(g, go) <= REL
     assert rel_inf(hv, H @ v) <= REL
+    # unprojected (exact) Hessian, used first by hessian_mode 1 (reading R14b)
+    _, _, hv_x = b.debug_eval(0, x, y, ctx.lam_att, ctx.lam_kin, ctx.rho, v, exact=True)
+    _, Hx = En.assemble(mod, ctx, x, y, pairs, project=False)
+    assert rel_inf(hv_x, Hx @ v) <= REL
 
 
 @pytest.mark.parametrize("name,seed,press", CASES)

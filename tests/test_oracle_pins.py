@@ -531,3 +531,37 @@ def test_readout_rigid_motion_and_bary():
     pad.marker_tri = pad.marker_tri[:1]
     c, mp, mf = R.gel_deformation(mod, x2, y2)[0]
     assert np.array_equal(mp[0], x2[pad.marker_tri[0, 0]])
+
+
+def _naive_candidates(mod, P0, P1):
+    dhat = mod.scene.config.dhat
+    out = []
+    sv = mod.surf_verts
+    vlo, vhi = np.minimum(P0[sv], P1[sv]), np.maximum(P0[sv], P1[sv])
+    T = mod.tris
+    tlo = np.minimum(P0[T].min(1), P1[T].min(1)) - dhat
+    thi = np.maximum(P0[T].max(1), P1[T].max(1)) + dhat
+    for i, v in enumerate(sv):
+        for t in range(len(T)):
+            if mod.allowed[mod.vert_body[v], mod.tri_body[t]] and np.all(vlo[i] <= thi[t]) and np.all(tlo[t] <= vhi[i]):
+                out.append((0, v, t))
+    E = mod.edges
+    elo, ehi = np.minimum(P0[E].min(1), P1[E].min(1)), np.maximum(P0[E].max(1), P1[E].max(1))
+    for a in range(len(E)):
+        for b in range(a + 1, len(E)):
+            if mod.allowed[mod.edge_body[a], mod.edge_body[b]] and np.all(elo[a] <= ehi[b] + dhat) \
+                    and np.all(elo[b] - dhat <= ehi[a]):
+                out.append((1, a, b))
+    return np.asarray(out).reshape(-1, 3)
+
+
+@pytest.mark.parametrize("swept", [False, True])
+def test_candidates_equal_naive_loops(swept):
+    """The body-pruned brute force returns exactly the naive all-pairs AABB set (same predicate)."""
+    sc, mod, ctx, x, y = _press_state()
+    P = M.all_positions(mod, x, y)
+    rng = np.random.default_rng(10)
+    P1 = P + (rng.normal(size=P.shape) * 1e-4 if swept else 0.0)
+    got = C.candidate_pairs(mod, P, P1)
+    assert len(got) > 0
+    assert np.array_equal(got, _naive_candidates(mod, P, P1))
