@@ -162,6 +162,7 @@ def main():
     from paper_2504_12908_b200 import scenes as S
     from paper_2504_12908_b200 import taccel as T
     from paper_2504_12908_b200.build import build
+    from paper_2504_12908_b200.shard import env_range, reduce_run_stats
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -179,7 +180,7 @@ def main():
     E = a.envs_per_gpu
     W, K = a.warmup, a.steps
     n_script = W + K + 1
-    ids = np.arange(rank * E, (rank + 1) * E)
+    ids = np.asarray(list(env_range(rank, world, E)))
     ei = S.env_inputs(sc, ids, n_steps=n_script)
     stream = torch.cuda.current_stream(dev)
     batch = T.Batch(sc, E, device=local, stream=stream)
@@ -252,11 +253,8 @@ def main():
         e2e = {"value": None, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "_ms": ms_e2e}
 
     # ---- max over ranks ----
-    tot = torch.tensor([ms, e2e["_ms"] if e2e else 0.0], device=dev, dtype=torch.float64)
-    cnt = torch.tensor([float(fails), float(pcg_iters), float(pcg_bytes)], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    tot, cnt = reduce_run_stats([ms, e2e["_ms"] if e2e else 0.0], [float(fails), float(pcg_iters), float(pcg_bytes)],
+                                world, device=dev)
     ms, ms_e2e = float(tot[0]), float(tot[1])
     fails, pcg_iters, pcg_bytes = (float(v) for v in cnt)
     if rank != 0:

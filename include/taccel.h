@@ -109,6 +109,8 @@ typedef struct {
 /* Solver constants (proposals; the paper fixes none — DESIGN.md §3). */
 typedef struct {
   double dt, dhat, kappa;        /* Δt (s), barrier range d̂ (m), contact stiffness κ   */
+  double max_step_rel;           /* Newton steps longer than max_step_rel·L_env (embedded ∞-norm)
+                                    are scaled down to that length before CCD/line search (R17c)   */
   double newton_tol_rel;         /* converged iff ‖p‖_emb,∞ ≤ newton_tol_rel · L_env            */
   double al_tol_rel;             /* AL residual tolerance relative to L_env                     */
   double pcg_eta;                /* PCG stops at rᵀz ≤ η² r₀ᵀz₀                                 */
@@ -116,6 +118,10 @@ typedef struct {
   int32_t max_newton, max_al_rounds, max_pcg, max_accd_iters, ee_mollifier;
   int32_t hessian_mode;          /* 0: PSD-projected element Hessians; 1: exact Hessian first, projected
                                     fallback with back-off when PCG meets dᵀHd ≤ 0 or gᵀp ≥ 0 (DESIGN R14b) */
+  int32_t ls_expand;             /* line-search expansion bound K (power of 2; 1 = plain backtracking):
+                                    swept sets and ACCD cover [x, x + K·p]; after a full step α doubles
+                                    while the energy keeps decreasing (DESIGN R17b)                    */
+  int32_t hold_cap;              /* max projected iterations between exact-Hessian attempts           */
   int32_t cand_capacity_per_env, active_capacity_per_env;
 } tac_config;
 
@@ -125,6 +131,7 @@ typedef struct {
   double alpha_min, energy, constraint_residual;                                     /* last step */
   int64_t pcg_iters_total;       /* cumulative since tac_batch_create                         */
   double pcg_alg_bytes_total;    /* cumulative algorithmic PCG bytes (DESIGN.md §5 B_pcg model) */
+  double diag[4];                /* last Newton iteration: ACCD bound, gᵀp, E(q), E at the last trial α */
 } tac_env_stats;
 
 struct tac_batch;
@@ -195,10 +202,11 @@ tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x, const doub
 /* Active pairs at (x, y): rows (kind, a, b) in canonical order. */
 tac_status tac_debug_active_pairs(tac_batch* b, int32_t env, const double* x, const double* y, int32_t* pairs,
                                   int32_t cap, int32_t* count, void* stream);
-/* Candidate pairs (swept boxes over [q, q + p], p [n] or NULL for static) in canonical order. */
+/* Candidate pairs (swept boxes over [q, q + K·p] with K = ls_expand, p [n] or NULL for static) in
+ * canonical order. */
 tac_status tac_debug_candidates(tac_batch* b, int32_t env, const double* x, const double* y, const double* p,
                                 int32_t* pairs, int32_t cap, int32_t* count, void* stream);
-/* α_max = min(1, min ACCD over the swept candidates) along p [n]. */
+/* α_max = K · min(1, min ACCD over the swept candidates along K·p), in units of p [n]. */
 tac_status tac_debug_accd(tac_batch* b, int32_t env, const double* x, const double* y, const double* p,
                           double* alpha, void* stream);
 /* Block-Jacobi PCG solve of H p = −g at (x, y) (AL as in tac_debug_eval): p [n], iterations. */

@@ -131,6 +131,15 @@ def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
     return p, it
 
 
+def sweep_factor(cfg, p_inf):
+    """K_eff (reading R17b): the largest power of two ≤ ls_expand with K_eff·‖p‖_emb,∞ ≤ d̂, at
+    least 1 — the expansion sweep never reaches further than d̂ beyond a normal Newton step."""
+    K = 1
+    while 2 * K <= cfg.ls_expand and 2.0 * K * p_inf <= cfg.dhat:
+        K *= 2
+    return K
+
+
 def _solve_spd(model, H, g, solver, cfg, stats):
     """Newton direction from the EXACT Hessian if it is SPD (Cholesky succeeds / CG meets no
     negative curvature) and the direction is a descent direction; None otherwise (reading R14b)."""
@@ -177,7 +186,7 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
                 p = _solve_spd(model, H, g, solver, cfg, stats)
                 if p is None:
                     nfail += 1
-                    hold = min(2 ** nfail, 64)
+                    hold = min(2 ** nfail, cfg.hold_cap)
                 else:
                     nfail = 0
             if p is None:
@@ -192,27 +201,44 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
             if p is None or not np.all(np.isfinite(p)):
                 stats.status = NONFINITE
                 break
-            if embedded_inf_norm(model, p) <= cfg.newton_tol_rel * L:
+            p_inf = embedded_inf_norm(model, p)
+            if p_inf <= cfg.newton_tol_rel * L:
                 converged = True
                 break
+            if p_inf > cfg.max_step_rel * L:            # step cap (reading R17c)
+                p = p * (cfg.max_step_rel * L / p_inf)
             dx, dy = En.unpack(model, p, np.zeros_like(y))
             Pd = _disp_positions(model, dx, dy)
-            cand = C.candidate_pairs(model, P, P + Pd)
-            alpha = C.accd_bound(model, P, Pd, cand)
+            K = sweep_factor(cfg, embedded_inf_norm(model, p))
+            cand = C.candidate_pairs(model, P, P + K * Pd)
+            alpha_max = K * C.accd_bound(model, P, K * Pd, cand)
+            alpha = min(1.0, alpha_max)
             E0 = En.total_energy(model, ctx, x, y, pairs)
             gp = float(g @ p)
+
+            def trial(a):
+                xa, ya = x + a * dx, y + a * dy
+                if any_inverted(model, xa):
+                    return None, xa, ya
+                Pa = all_positions(model, xa, ya)
+                return En.total_energy(model, ctx, xa, ya, C.active_pairs(model, Pa, cand)), xa, ya
+
             while True:
-                xt, yt = x + alpha * dx, y + alpha * dy
-                ok = not any_inverted(model, xt)
-                if ok:
-                    Pt = all_positions(model, xt, yt)
-                    E1 = En.total_energy(model, ctx, xt, yt, C.active_pairs(model, Pt, cand))
-                    if E1 <= E0 + cfg.armijo_c * alpha * gp:
-                        break
+                E1, xt, yt = trial(alpha)
+                if E1 is not None and E1 <= E0 + cfg.armijo_c * alpha * gp:
+                    break
                 alpha *= 0.5
                 stats.ls_backtracks += 1
                 if alpha < 1e-10:
                     break
+            # expansion (reading R17b): after a full step, keep doubling α while the energy keeps
+            # decreasing, α stays under the ACCD bound of the K-times longer sweep and Armijo holds
+            if alpha == 1.0 and K > 1:
+                while 2.0 * alpha <= alpha_max:
+                    E2, x2, y2 = trial(2.0 * alpha)
+                    if E2 is None or not (E2 < E1) or not (E2 <= E0 + cfg.armijo_c * 2.0 * alpha * gp):
+                        break
+                    alpha, E1, xt, yt = 2.0 * alpha, E2, x2, y2
             if alpha < 1e-10:
                 stats.status = NEWTON_STALL
                 break

@@ -482,17 +482,19 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.cand_cap = std::max(cfg->cand_capacity_per_env, 64);
   D.act_cap = std::max(cfg->active_capacity_per_env, 16);
   D.ent_cap = 16 * (H.NT + H.NE) + 4096;
+  D.max_step = cfg->max_step_rel;
   D.dt = cfg->dt; D.dhat = cfg->dhat; D.kappa = cfg->kappa; D.tolN = cfg->newton_tol_rel; D.tolAL = cfg->al_tol_rel;
   D.eta = cfg->pcg_eta; D.armijo = cfg->armijo_c; D.accd_s = cfg->accd_s; D.rho0 = cfg->al_rho0; D.cell = H.cell;
   D.max_newton = cfg->max_newton; D.max_al = cfg->max_al_rounds; D.max_pcg = cfg->max_pcg;
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
+  D.hold_cap = std::max(cfg->hold_cap, 1); D.K = (double)std::max(cfg->ls_expand, 1);
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
 }
 
 static tac_status check_cfg(const tac_config* c) {
-  if (!(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
+  if (!(c->max_step_rel > 0) || !(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
       c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1) || c->hessian_mode < 0 ||
-      c->hessian_mode > 1)
+      c->hessian_mode > 1 || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0)
     return fail(TAC_E_INVALID, "invalid tac_config");
   return TAC_OK;
 }
@@ -551,7 +553,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   UP(mark_bary); UP(mark_pad); UP(pad_mount); UP(pad_T); UP(Xrest);
 #undef UP
   b->hctl.assign(n_envs, EnvCtl{});
-  for (auto& c : b->hctl) { c.phase = PHASE_IDLE; c.disabled = 1; c.status = ENV_DISABLED; c.L = 1.0; c.rho = cfg->al_rho0; }
+  for (auto& c : b->hctl) { c.phase = PHASE_IDLE; c.disabled = 1; c.status = ENV_DISABLED; c.L = 1.0; c.rho = cfg->al_rho0; c.Keff = 1.0; }
   if (e == cudaSuccess) e = cudaMemcpyAsync(D.ctl, b->hctl.data(), sizeof(EnvCtl) * n_envs, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMallocHost(&b->h_flag, sizeof(int));
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -736,6 +738,7 @@ extern "C" tac_status tac_get_stats(tac_batch* b, tac_env_stats* out, void* stre
     out[e].n_active = c.n_act; out[e].al_rounds = c.al_rounds; out[e].n_candidates = c.ncand;
     out[e].alpha_min = c.alpha_min; out[e].energy = c.energy; out[e].constraint_residual = c.residual;
     out[e].pcg_iters_total = c.pcg_total; out[e].pcg_alg_bytes_total = c.pcg_bytes;
+    out[e].diag[0] = c.alpha_ccd; out[e].diag[1] = c.gp; out[e].diag[2] = c.ls_E0; out[e].diag[3] = c.ls_E1;
   }
   return TAC_OK;
 }
@@ -934,7 +937,7 @@ extern "C" tac_status tac_debug_accd(tac_batch* b, int32_t env, const double* x,
     EnvCtl c;
     cudaMemcpyAsync(&c, D.ctl + env, sizeof(EnvCtl), cudaMemcpyDeviceToHost, S.st);
     if (cudaStreamSynchronize(S.st) != cudaSuccess) s = fail(TAC_E_CUDA, "debug accd failed");
-    else *alpha = c.alpha_ccd;
+    else *alpha = c.Keff * c.alpha_ccd;
   }
   tac_status s2 = dbg_leave(S);
   return s ? s : s2;

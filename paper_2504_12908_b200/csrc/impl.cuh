@@ -17,7 +17,7 @@ namespace tac {
 constexpr int NTHREADS = 256;
 constexpr int NBUCKET = 4096;      // spatial-hash buckets per env (shared memory)
 constexpr int MAXCELLS = 32;       // targets spanning more cells go to the per-env "big" list
-constexpr int BIG_CAP = 512;
+constexpr int BIG_CAP = 2048;
 constexpr int TETBUF = 90;         // 12 gradient + 78 packed Hessian
 constexpr int PH = 78;
 
@@ -31,6 +31,8 @@ struct EnvCtl {
   int exact, hold, nfail, xfail;   // exact-Hessian-first control (reading R14b)
   long long pcg_total;
   double pcg_bytes;
+  double Keff;
+  double ls_E0, ls_E1;
   double alpha_ccd, alpha_min, rho, r_prev, L, energy, residual, gp, pnorm, alpha;
 };
 
@@ -39,8 +41,10 @@ struct Dev {
   int E, V, T, NA, ND, NVall, NSV, NT, NE, NEs, NC, NK, NB, n, npads, NCOAT, NMARK;
   int cand_cap, act_cap, ent_cap;
   // ---- config ----
+  double max_step;     // relative step cap (reading R17c)
   double dt, dhat, kappa, tolN, tolAL, eta, armijo, accd_s, rho0, cell;
-  int max_newton, max_al, max_pcg, max_accd, mollify, hmode;
+  int max_newton, max_al, max_pcg, max_accd, mollify, hmode, hold_cap;
+  double K;                 // line-search expansion bound (reading R17b)
   double grav[3];
   // ---- template ----
   const int* tets;        // [T][4]

@@ -48,17 +48,43 @@ __constant__ unsigned char c_unpack_r[PH], c_unpack_c[PH];
 // ------------------------------------------------------------------------------------------
 // positions: P = φ(q) for every contact vertex; Pd = displacement of p (J_v p_b for bodies)
 // ------------------------------------------------------------------------------------------
+__device__ double embedded_inf_norm(const Dev& D, int e, const double* p, double* red) {
+  double pm = 0.0;
+  for (int i = threadIdx.x; i < 3 * D.V; i += blockDim.x) pm = fmax(pm, fabs(p[i]));
+  for (int i = threadIdx.x; i < D.NAV; i += blockDim.x) {
+    int gv = D.affv_list[i];
+    int sl = D.dof_slot[D.vert_aff[gv]];
+    v3 u = embed(p + 3 * D.V + 12 * sl, ld3(D.vert_xbar + 3 * gv));
+    pm = fmax(pm, fmax(fabs(u.x), fmax(fabs(u.y), fabs(u.z))));
+  }
+  return block_max(pm, red);
+}
+
+// K_eff (reading R17b): largest power of two ≤ ls_expand with K_eff·‖p‖_emb,∞ ≤ d̂
+__device__ __forceinline__ double sweep_factor(const Dev& D, double pinf) {
+  double K = 1.0;
+  while (2.0 * K <= D.K && 2.0 * K * pinf <= D.dhat) K *= 2.0;
+  return K;
+}
+
 __global__ void __launch_bounds__(NTHREADS) k_positions(Dev D, int env0, int with_p, int force) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
+  __shared__ double red[32];
   const double* q = D.q + (size_t)e * D.n;
   const double* p = D.p + (size_t)e * D.n;
   double* P = D.P + (size_t)e * D.NVall * 3;
   double* Pd = D.Pd + (size_t)e * D.NVall * 3;
+  double Kf = 1.0;
+  if (with_p) {
+    Kf = sweep_factor(D, embedded_inf_norm(D, e, p, red));
+    if (threadIdx.x == 0) D.ctl[e].Keff = Kf;
+  }
   for (int gv = threadIdx.x; gv < D.NVall; gv += blockDim.x) {
     if (gv < D.V) {
       P[3 * gv] = q[3 * gv]; P[3 * gv + 1] = q[3 * gv + 1]; P[3 * gv + 2] = q[3 * gv + 2];
-      if (with_p) { Pd[3 * gv] = p[3 * gv]; Pd[3 * gv + 1] = p[3 * gv + 1]; Pd[3 * gv + 2] = p[3 * gv + 2]; }
+      // Pd = K_eff·(displacement of p): the swept sets and ACCD cover α ∈ [0, K_eff]
+      if (with_p) { Pd[3 * gv] = Kf * p[3 * gv]; Pd[3 * gv + 1] = Kf * p[3 * gv + 1]; Pd[3 * gv + 2] = Kf * p[3 * gv + 2]; }
     } else {
       int b = D.vert_aff[gv];
       v3 xb = ld3(D.vert_xbar + 3 * gv);
@@ -67,7 +93,7 @@ __global__ void __launch_bounds__(NTHREADS) k_positions(Dev D, int env0, int wit
         int s = D.dof_slot[b];
         v3 d = mk(0, 0, 0);
         if (s >= 0) d = embed(p + 3 * D.V + 12 * s, xb);
-        st3(Pd + 3 * gv, d);
+        st3(Pd + 3 * gv, Kf * d);
       }
     }
   }
@@ -447,62 +473,112 @@ __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
 // barrier pairs: warp per pair; closed-form ∇s/∇²s, barrier + mollifier composition, full 12×12
 // PSD projection by warp Jacobi (readings R10-R12)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHREADS) k_pairs(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.x;
+constexpr int PAIR_WARPS = 4;          // warps per CTA in k_pairs
+constexpr int PAIRS_PER_WARP = 4;      // pairs handled sequentially by one warp
+constexpr int PAIRS_PER_CTA = PAIR_WARPS * PAIRS_PER_WARP;
+
+struct PairScratch {
+  JacobiScratch J;
+  double gv[9], gcv[9];       // variable-space ∇s and ∇c
+  double hv[81], hcv[81];     // variable-space ∇²s and ∇²c, index (3v+a)*9 + 3u+b
+  double gs[12], gc[12];      // slot-space ∇s and ∇c
+};
+
+// grid (ceil(act_cap / PAIRS_PER_CTA), envs): many CTAs per env so a single contact-heavy env is
+// spread over the whole GPU; CTAs past the env's active count exit at once.
+__global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.y;
   if (env_skip(D, e, force)) return;
-  __shared__ JacobiScratch JS[NTHREADS / 32];
-  __shared__ double GS[NTHREADS / 32][24];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const EnvCtl& C = D.ctl[e];
+  const int nact = C.n_act;
+  const int base = blockIdx.x * PAIRS_PER_CTA;
+  if (base >= nact) return;
+  __shared__ PairScratch PS[PAIR_WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double* P = D.P + (size_t)e * D.NVall * 3;
   const int* info = D.act_info + (size_t)e * D.act_cap * 4;
   const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
   double* ag = D.act_g + (size_t)e * D.act_cap * 12;
   double* aH = D.act_H + (size_t)e * D.act_cap * PH;
-  JacobiScratch& S = JS[w];
-  double* gs = GS[w];
-  double* gc = GS[w] + 12;
-  for (int k = w; k < C.n_act; k += nw) {
+  PairScratch& S = PS[w];
+  const bool project = !C.exact;
+  for (int j = 0; j < PAIRS_PER_WARP; ++j) {
+    const int k = base + w + PAIR_WARPS * j;
+    if (k >= nact) break;
     const int kind = info[4 * k], type = info[4 * k + 1], a = info[4 * k + 2], b = info[4 * k + 3];
     v3 X[4];
     for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * avid[4 * k + s]);
     SubDist SD;
     sd_make(SD, kind, type, X);
+    const int nvar = SD.sub == SUB_PP ? 1 : (SD.sub == SUB_PL ? 2 : 3);
     double B, B1, B2;
     barrier_s(SD.s, D.dhat, &B, &B1, &B2);
     const bool useM = (kind == 1) && D.mollify;
     SubDist CC;
+    sd_zero(CC);
     double m = 1.0, m1 = 0.0, m2 = 0.0;
     if (useM) {
       sd_make_cross(CC, X);
       mollifier(CC.D, pair_eps(D, kind, a, b), &m, &m1, &m2);
     }
+    const bool molterm = useM && m1 != 0.0;
     const double scale = D.dt * D.dt * D.kappa * pair_area(D, kind, a, b);
-    if (lane < 12) {
-      gs[lane] = sd_grad(SD, lane);
-      gc[lane] = useM ? sd_grad(CC, lane, true) : 0.0;
+    // 1) variable-space derivatives, one entry per lane
+    for (int i = lane; i < 81; i += 32) {
+      int va = i / 9, ub = i % 9, v = va / 3, u = ub / 3;
+      S.hv[i] = (v < nvar && u < nvar) ? sd_var2(SD, v, va % 3, u, ub % 3) : 0.0;
+      S.hcv[i] = (molterm && v > 0 && u > 0) ? sc_var2(CC, v, va % 3, u, ub % 3) : 0.0;
+    }
+    if (lane < 9) {
+      int v = lane / 3;
+      S.gv[lane] = v < nvar ? sd_var1(SD, v, lane % 3) : 0.0;
+      S.gcv[lane] = (useM && v > 0) ? sc_var1(CC, v, lane % 3) : 0.0;
     }
     __syncwarp();
-    if (lane < 12) ag[12 * k + lane] = scale * (m * B1 * gs[lane] + B * m1 * gc[lane]);
+    // 2) slot-space gradients (coefficients are ±1/0 combinations of the variables)
+    if (lane < 12) {
+      const int sl = lane / 3, ax = lane % 3;
+      double g1 = 0.0, g2 = 0.0;
+      for (int v = 0; v < 3; ++v) {
+        g1 += SD.coef[v][sl] * S.gv[3 * v + ax];
+        g2 += CC.coef[v][sl] * S.gcv[3 * v + ax];
+      }
+      S.gs[lane] = g1;
+      S.gc[lane] = useM ? g2 : 0.0;
+    }
+    __syncwarp();
+    if (lane < 12) ag[12 * k + lane] = scale * (m * B1 * S.gs[lane] + B * m1 * S.gc[lane]);
+    // 3) 12×12 (upper) from the variable blocks
     for (int i = lane; i < 144; i += 32) {
-      int r = i / 12, c = i % 12;
+      const int r = i / 12, c = i % 12;
       double h = 0.0;
       if (r <= c) {
-        h = m * (B2 * gs[r] * gs[c] + B1 * sd_hess(SD, r, c));
-        if (useM && m1 != 0.0)
-          h += B * (m2 * gc[r] * gc[c] + m1 * sd_hess(CC, r, c, true)) + m1 * B1 * (gs[r] * gc[c] + gc[r] * gs[c]);
+        const int k1 = r / 3, a1 = r % 3, k2 = c / 3, a2 = c % 3;
+        double hs = 0.0, hc = 0.0;
+        for (int v = 0; v < 3; ++v) {
+          const int cv = SD.coef[v][k1], cw = CC.coef[v][k1];
+          for (int u = 0; u < 3; ++u) {
+            const int idx = (3 * v + a1) * 9 + 3 * u + a2;
+            hs += (double)(cv * SD.coef[u][k2]) * S.hv[idx];
+            if (molterm) hc += (double)(cw * CC.coef[u][k2]) * S.hcv[idx];
+          }
+        }
+        h = m * (B2 * S.gs[r] * S.gs[c] + B1 * hs);
+        if (molterm) h += B * (m2 * S.gc[r] * S.gc[c] + m1 * hc) + m1 * B1 * (S.gs[r] * S.gc[c] + S.gc[r] * S.gs[c]);
         h *= scale;
       }
-      S.A[i] = h;
+      S.J.A[i] = h;
     }
     __syncwarp();
-    for (int i = lane; i < 144; i += 32) {
-      int r = i / 12, c = i % 12;
-      if (r > c) S.A[i] = S.A[12 * c + r];
+    if (project) {
+      for (int i = lane; i < 144; i += 32) {
+        int r = i / 12, c = i % 12;
+        if (r > c) S.J.A[i] = S.J.A[12 * c + r];
+      }
+      __syncwarp();
+      jacobi12_psd(S.J, lane, 32);
     }
-    __syncwarp();
-    if (!C.exact) jacobi12_psd(S, lane, 32);
-    for (int i = lane; i < PH; i += 32) aH[(size_t)PH * k + i] = S.A[12 * c_unpack_r[i] + c_unpack_c[i]];
+    for (int i = lane; i < PH; i += 32) aH[(size_t)PH * k + i] = S.J.A[12 * c_unpack_r[i] + c_unpack_c[i]];
     __syncwarp();
   }
 }
@@ -649,28 +725,60 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
       double v = M[i] * fac;
       if (r >= 3 && c >= 3) v += S.A[12 * (r - 3) + (c - 3)];
       Hb[i] = v;
-      PB[w][i] = v;
     }
     __syncwarp();
-    // pair contributions (gradient, preconditioner block) in list order (deterministic per lane)
-    for (int j = bptr[d]; j < bptr[d + 1]; ++j) {
-      int k = blist[j] >> 2, s = blist[j] & 3;
+    if (lane < 12) g[3 * D.V + 12 * d + lane] = gb;      // pair terms added below
+  }
+  __syncthreads();
+  // pair contributions to each body's gradient and preconditioner block: all warps split the
+  // body's contribution list (warp w takes entries w, w+nw, ...), partials summed in warp order
+  __shared__ double GB[NTHREADS / 32][12];
+  for (int d = 0; d < D.ND; ++d) {
+    const int b = D.dof_body[d];
+    double acc[5] = {0, 0, 0, 0, 0};   // entries i = lane + 32·t of the 144
+    double gacc = 0.0;
+    for (int j = bptr[d] + w; j < bptr[d + 1]; j += nw) {
+      const int k = blist[j] >> 2, s = blist[j] & 3;
       const double* xs = D.vert_xbar + 3 * avid[4 * k + s];
-      if (lane < 12) gb += jf(lane, xs) * ag[12 * k + 3 * s + jrow(lane)];
+      if (lane < 12) gacc += jf(lane, xs) * ag[12 * k + 3 * s + jrow(lane)];
       for (int t = 0; t < 4; ++t) {
-        int gvt = avid[4 * k + t];
+        const int gvt = avid[4 * k + t];
         if (gvt < D.V || D.vert_aff[gvt] != b) continue;
         const double* xt = D.vert_xbar + 3 * gvt;
-        for (int i = lane; i < 144; i += 32) {
-          int al = i / 12, be = i % 12;
-          PB[w][i] += jf(al, xs) * jf(be, xt) * aH[(size_t)PH * k + sym_idx(3 * s + jrow(al), 3 * t + jrow(be), 12)];
+        const double* Hk = aH + (size_t)PH * k;
+#pragma unroll
+        for (int tt = 0; tt < 5; ++tt) {
+          const int i = lane + 32 * tt;
+          if (i < 144) {
+            const int al = i / 12, be = i % 12;
+            acc[tt] += jf(al, xs) * jf(be, xt) * Hk[sym_idx(3 * s + jrow(al), 3 * t + jrow(be), 12)];
+          }
         }
       }
     }
-    if (lane < 12) g[3 * D.V + 12 * d + lane] = gb;
-    __syncwarp();
-    if (lane == 0) chol_inverse12(PB[w], D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q);
-    __syncwarp();
+#pragma unroll
+    for (int tt = 0; tt < 5; ++tt)
+      if (lane + 32 * tt < 144) PB[w][lane + 32 * tt] = acc[tt];
+    if (lane < 12) GB[w][lane] = gacc;
+    __syncthreads();
+    if (w == d % nw) {
+      const double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
+      double* T = JS[w].A;               // total block
+      for (int i = lane; i < 144; i += 32) {
+        double v = Hb[i];
+        for (int ww = 0; ww < nw; ++ww) v += PB[ww][i];
+        T[i] = v;
+      }
+      if (lane < 12) {
+        double v = g[3 * D.V + 12 * d + lane];
+        for (int ww = 0; ww < nw; ++ww) v += GB[ww][lane];
+        g[3 * D.V + 12 * d + lane] = v;
+      }
+      __syncwarp();
+      if (lane == 0) chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q);
+      __syncwarp();
+    }
+    __syncthreads();
   }
 }
 
@@ -809,17 +917,17 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
   }
   // gᵀp and embedded ∞-norm
   part = 0.0;
-  double pm = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) part += g[i] * p[i];
-  for (int i = threadIdx.x; i < 3 * D.V; i += blockDim.x) pm = fmax(pm, fabs(p[i]));
-  for (int i = threadIdx.x; i < D.NAV; i += blockDim.x) {
-    int gv = D.affv_list[i];
-    int sl = D.dof_slot[D.vert_aff[gv]];
-    v3 u = embed(p + 3 * D.V + 12 * sl, ld3(D.vert_xbar + 3 * gv));
-    pm = fmax(pm, fmax(fabs(u.x), fmax(fabs(u.y), fabs(u.z))));
-  }
+  double pm = embedded_inf_norm(D, e, p, red);
   double gp = block_sum(part, red);
-  pm = block_max(pm, red);
+  // step cap (reading R17c): scale p to max_step·L_env if longer (direction unchanged)
+  const double cap = D.max_step * C.L;
+  if (pm > cap && pm == pm) {
+    const double sc = cap / pm;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] *= sc;
+    __syncthreads();
+    gp *= sc;
+  }
   if (threadIdx.x == 0) {
     const bool exact_failed = C.exact && (bad || !(gp < 0.0) || !(pm == pm));
     C.pcg += it;
@@ -967,7 +1075,8 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
     int kind = (ca[k] >> 30) & 1, a = ca[k] & ((1 << 30) - 1), b = cb[k], vid[4];
     pair_vids(D, kind, a, b, vid);
     v3 X[4];
-    for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]) + alpha * ld3(Pd + 3 * vid[s]);
+    const double aK = alpha == 0.0 ? 0.0 : alpha / C.Keff;   // Pd holds K_eff·(displacement of p)
+    for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]) + aK * ld3(Pd + 3 * vid[s]);
     double d2;
     classify(kind, X, &d2);
     if (!(d2 < dh2)) continue;
@@ -1014,7 +1123,8 @@ __global__ void __launch_bounds__(NTHREADS) k_linesearch(Dev D, int env0) {
   int inv;
   energy_terms(D, e, 0.0, red, t, &inv);
   const double E0 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
-  double alpha = C.alpha_ccd;
+  const double alpha_max = C.Keff * C.alpha_ccd;  // ACCD bound along K_eff·p, in units of p
+  double alpha = fmin(1.0, alpha_max);
   const double gp = C.gp;
   int bt = 0;
   bool ok = false;
@@ -1029,6 +1139,18 @@ __global__ void __launch_bounds__(NTHREADS) k_linesearch(Dev D, int env0) {
     ++bt;
     if (alpha < 1e-10) break;
   }
+  // expansion (reading R17b): after a full step keep doubling α while the energy keeps decreasing,
+  // Armijo holds and α stays under the ACCD bound of the K-times longer sweep
+  if (ok && alpha == 1.0 && C.Keff > 1.0) {
+    while (2.0 * alpha <= alpha_max) {
+      energy_terms(D, e, 2.0 * alpha, red, t, &inv);
+      if (inv) break;
+      const double E2 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
+      if (!(E2 < E1) || !(E2 <= E0 + D.armijo * 2.0 * alpha * gp)) break;
+      alpha *= 2.0;
+      E1 = E2;
+    }
+  }
   if (ok) {
     double* q = D.q + (size_t)e * D.n;
     const double* p = D.p + (size_t)e * D.n;
@@ -1038,6 +1160,7 @@ __global__ void __launch_bounds__(NTHREADS) k_linesearch(Dev D, int env0) {
     C.ls_bt += bt;
     if (!ok) { C.phase = PHASE_FAILED; C.status = ENV_NEWTON_STALL; }
     else { C.alpha_min = fmin(C.alpha_min, alpha); C.alpha = alpha; C.energy = E1; }
+    C.ls_E0 = E0; C.ls_E1 = E1;
   }
 }
 
@@ -1059,7 +1182,7 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
   if (threadIdx.x == 0) {
     if (C.xfail) {
       C.nfail += 1;
-      C.hold = min(1 << min(C.nfail, 6), 64);
+      C.hold = min(1 << min(C.nfail, 20), D.hold_cap);
       C.exact = 0;
       C.xfail = 0;
     } else if (!C.exact) {
@@ -1148,7 +1271,7 @@ __global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
     C.phase = PHASE_ACTIVE; C.status = ENV_OK; C.inner_conv = 0; C.newton = 0; C.pcg = 0; C.ls_bt = 0;
     C.al_rounds = 0; C.n_act = 0; C.ncand = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;
     C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
-    C.exact = D.hmode == 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0;
+    C.exact = D.hmode == 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0; C.Keff = 1.0;
   }
 }
 
@@ -1305,7 +1428,8 @@ void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   if (D.T > 0) k_tets<<<grid, NTHREADS, 0, s>>>(D, env0, force);
 }
 void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  k_pairs<<<ne, NTHREADS, 0, s>>>(D, env0, force);
+  dim3 grid((D.act_cap + PAIRS_PER_CTA - 1) / PAIRS_PER_CTA, ne);
+  k_pairs<<<grid, PAIR_WARPS * 32, 0, s>>>(D, env0, force);
 }
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   k_assemble<<<ne, NTHREADS, 0, s>>>(D, env0, force);

@@ -63,6 +63,7 @@ class Config:
     dt: float = 0.02
     dhat: float = 1.0e-4
     kappa: float = 1.0e8
+    max_step_rel: float = 5.0e-2
     newton_tol_rel: float = 1.0e-7
     al_tol_rel: float = 1.0e-6
     pcg_eta: float = 1.0e-4
@@ -75,7 +76,9 @@ class Config:
     max_accd_iters: int = 10000
     ee_mollifier: int = 1
     hessian_mode: int = 1          # 0: always PSD-projected; 1: exact first, projected fallback (R14b)
-    cand_capacity_per_env: int = 16384
+    ls_expand: int = 16            # line-search expansion bound K (R17b); 1 = plain backtracking
+    hold_cap: int = 16             # max projected iterations between exact-Hessian attempts (R14b)
+    cand_capacity_per_env: int = 65536
     active_capacity_per_env: int = 4096
 
 

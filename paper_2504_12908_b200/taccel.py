@@ -50,11 +50,13 @@ class SceneDesc(ctypes.Structure):
 
 class Config(ctypes.Structure):
     _fields_ = [("dt", ctypes.c_double), ("dhat", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("max_step_rel", ctypes.c_double),
                 ("newton_tol_rel", ctypes.c_double), ("al_tol_rel", ctypes.c_double), ("pcg_eta", ctypes.c_double),
                 ("armijo_c", ctypes.c_double), ("accd_s", ctypes.c_double), ("al_rho0", ctypes.c_double),
                 ("max_newton", ctypes.c_int32), ("max_al_rounds", ctypes.c_int32), ("max_pcg", ctypes.c_int32),
                 ("max_accd_iters", ctypes.c_int32), ("ee_mollifier", ctypes.c_int32),
-                ("hessian_mode", ctypes.c_int32), ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32)]
+                ("hessian_mode", ctypes.c_int32), ("ls_expand", ctypes.c_int32),
+                ("hold_cap", ctypes.c_int32), ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32)]
 
 
 class EnvStats(ctypes.Structure):
@@ -62,7 +64,7 @@ class EnvStats(ctypes.Structure):
                 ("ls_backtracks", ctypes.c_int32), ("n_active", ctypes.c_int32), ("al_rounds", ctypes.c_int32),
                 ("n_candidates", ctypes.c_int32), ("alpha_min", ctypes.c_double), ("energy", ctypes.c_double),
                 ("constraint_residual", ctypes.c_double), ("pcg_iters_total", ctypes.c_int64),
-                ("pcg_alg_bytes_total", ctypes.c_double)]
+                ("pcg_alg_bytes_total", ctypes.c_double), ("diag", ctypes.c_double * 4)]
 
 
 def header_symbols():
@@ -283,7 +285,10 @@ class Batch:
     def stats(self):
         arr = (EnvStats * self.n_envs)()
         _check(self.lib.tac_get_stats(self.handle, arr, self._s()))
-        return [{k: getattr(s, k) for k, _ in EnvStats._fields_} for s in arr]
+        out = [{k: getattr(s, k) for k, _ in EnvStats._fields_} for s in arr]
+        for d in out:
+            d["diag"] = list(d["diag"])
+        return out
 
     # ---- tracing ---------------------------------------------------------------------------------
     NPHASES = 16

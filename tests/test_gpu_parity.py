@@ -119,15 +119,16 @@ def test_swept_candidates_and_accd(name, seed, press):
     sc, mod, ei, base, ctx, x, y = _perturbed(name, seed, press=press)
     b = _batch_for(sc, base, ei)
     rng = np.random.default_rng(seed + 7)
-    p = rng.normal(size=mod.n_dof) * 1e-4
+    p = rng.normal(size=mod.n_dof) * (3e-6 if seed % 2 else 1e-4)      # K_eff = 8 / 1
     p[3 * mod.V:] *= 0.05
     P = M.all_positions(mod, x, y)
     dx, dy = En.unpack(mod, p, np.zeros_like(y))
     Pd = SO._disp_positions(mod, dx, dy)
-    cand = C.candidate_pairs(mod, P, P + Pd)
+    K = SO.sweep_factor(sc.config, SO.embedded_inf_norm(mod, p))
+    cand = C.candidate_pairs(mod, P, P + K * Pd)
     got = b.debug_candidates(0, x, y, p)
     assert np.array_equal(got, cand)
-    a_ref = C.accd_bound(mod, P, Pd, cand)
+    a_ref = K * C.accd_bound(mod, P, K * Pd, cand)
     a_gpu = b.debug_accd(0, x, y, p)
     assert a_gpu == pytest.approx(a_ref, rel=1e-9)
 

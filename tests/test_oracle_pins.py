@@ -459,7 +459,7 @@ def test_free_fall_one_newton_step_exact():
     y0 = np.array([[0.1, 0.2, 0.3, *S.rot_z(0.4).ravel()]])
     yd0 = np.array([[0.5, -0.2, 0.1, *np.zeros(9)]])
     st = SO.State(np.zeros((0, 3)), np.zeros((0, 3)), y0, yd0)
-    new, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=0.02)
+    new, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=0.2)
     dt = sc.config.dt
     expect = y0[0, :3] + dt * yd0[0, :3] + dt * dt * sc.gravity
     assert stats.status == SO.ENV_OK and stats.newton_iters == 2    # one step + convergence check
