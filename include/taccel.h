@@ -187,6 +187,9 @@ const char* tac_last_error(void);
 tac_status tac_profile_enable(tac_batch* b, int32_t enable);
 tac_status tac_profile_read(tac_batch* b, double* ms, int64_t* launches, int32_t reset);
 const char* tac_profile_phase_name(int32_t phase);
+/* Newton iterations of the last time step: envs still active after each iteration and the host
+ * wall time of each iteration (ms); n = number of iterations (arrays filled up to cap). */
+tac_status tac_profile_iterations(tac_batch* b, int32_t* active, double* ms, int32_t cap, int32_t* n);
 
 /* ---- parity hooks (exported, test-only; host buffers) ---------------------------------------
  * tac_debug_eval: at (x [V][3], y [NA][12]) of env `env`, with x̃/ỹ from the env's last set_state

@@ -3,6 +3,7 @@
 // closed-form tet moments, BSR pattern + gather lists), workspace carving, and the host-driven
 // Newton loop (one 4-byte device→host flag per Newton iteration is the only crossing).
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -39,6 +40,8 @@ struct HostT {
   std::vector<int> tets;            // T*4
   std::vector<double> Dmi, vol, mu, lam, mass, Xrest;
   std::vector<int> sedge, vadj_ptr, vadj, vdiag_ptr, vdiag, eblk_ptr, eblk;
+  std::vector<int> rptr, rcol, rblk_ptr, rblk;   // row-ordered symmetric BSR (off-diagonal)
+  int NNZ = 0;
   std::vector<int> body_kind, dof_slot, dof_body;
   std::vector<double> My, bmass, bs1, bvol, bkappa;
   std::vector<int> vert_body, vert_aff;
@@ -314,6 +317,24 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
     flat(vadj, H.vadj_ptr, H.vadj);
     flat(vdiag, H.vdiag_ptr, H.vdiag);
     flat(eblk, H.eblk_ptr, H.eblk);
+    // row-ordered off-diagonal blocks: row v lists its neighbours u ascending; block (v,u) gathers
+    // tet entries 16t + 4a + b with local a ↔ v and b ↔ u
+    std::vector<std::vector<int>> nb(H.V);
+    for (auto& e2 : se) { nb[e2[0]].push_back(e2[1]); nb[e2[1]].push_back(e2[0]); }
+    std::map<std::array<int, 2>, int> rid;
+    H.rptr.assign(1, 0);
+    for (int v = 0; v < H.V; ++v) {
+      std::sort(nb[v].begin(), nb[v].end());
+      for (int u : nb[v]) { rid[{v, u}] = (int)H.rcol.size(); H.rcol.push_back(u); }
+      H.rptr.push_back((int)H.rcol.size());
+    }
+    H.NNZ = (int)H.rcol.size();
+    std::vector<std::vector<int>> rb(H.NNZ);
+    for (int t = 0; t < H.T; ++t)
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b)
+          if (a != b) rb[rid[{H.tets[4 * t + a], H.tets[4 * t + b]}]].push_back(16 * t + 4 * a + b);
+    flat(rb, H.rblk_ptr, H.rblk);
   }
   // constraints: ∂⁻G vertices and kinematic bodies
   H.att_of_vert.assign(H.V, -1);
@@ -389,6 +410,8 @@ struct tac_batch {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> pending;  // (phase, event index of start; stop = +1)
   size_t ev_used = 0;
+  std::vector<int> it_active;                // per Newton iteration of the last step: envs still active
+  std::vector<double> it_ms;                 // and host wall time of the iteration
 };
 
 enum { PH_POSITIONS = 0, PH_BROAD_STATIC, PH_NARROW, PH_TETS, PH_PAIRS, PH_ASSEMBLE, PH_PCG, PH_BROAD_SWEPT, PH_CCD,
@@ -435,6 +458,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.tets = ti(H.tets); D.Dmi = td(H.Dmi); D.vol = td(H.vol); D.mu = td(H.mu); D.lam = td(H.lam); D.mass = td(H.mass);
   D.sedge = ti(H.sedge); D.vadj_ptr = ti(H.vadj_ptr); D.vadj = ti(H.vadj); D.vdiag_ptr = ti(H.vdiag_ptr);
   D.vdiag = ti(H.vdiag); D.eblk_ptr = ti(H.eblk_ptr); D.eblk = ti(H.eblk);
+  D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
   D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My);
   D.bmass = td(H.bmass); D.bs1 = td(H.bs1); D.bvol = td(H.bvol); D.bkappa = td(H.bkappa);
   D.vert_body = ti(H.vert_body); D.vert_aff = ti(H.vert_aff); D.vert_xbar = td(H.vert_xbar);
@@ -457,15 +481,18 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.s_kin = C.take<double>(e * H.NK * 12 + 1); D.lam_kin = C.take<double>(e * H.NK * 12 + 1);
   D.ykin = C.take<double>(e * H.NK * 12 + 1);
   D.P = C.take<double>(e * H.NVall * 3); D.Pd = C.take<double>(e * H.NVall * 3);
-  D.Hd = C.take<double>(e * H.V * 9 + 1); D.Ho = C.take<double>(e * H.NEs * 9 + 1);
+  D.Hd = C.take<double>(e * H.V * 9 + 1); D.Ho = C.take<double>(e * H.NNZ * 9 + 1);
   D.Hb = C.take<double>(e * H.ND * 144 + 1); D.Pinv_s = C.take<double>(e * H.V * 9 + 1);
   D.Pinv_b = C.take<double>(e * H.ND * 144 + 1);
   D.tetbuf = C.take<double>(e * TETBUF * H.T + 1);
   D.cand_a = C.take<int>(e * D.cand_cap); D.cand_b = C.take<int>(e * D.cand_cap);
   D.ent = C.take<int>(e * D.ent_cap * 2); D.big = C.take<int>(e * BIG_CAP);
+  D.tbox = C.take<double>(e * (H.NT + H.NE) * 6);
   D.act_info = C.take<int>(e * D.act_cap * 4); D.act_vid = C.take<int>(e * D.act_cap * 4);
   D.act_g = C.take<double>(e * D.act_cap * 12); D.act_H = C.take<double>(e * D.act_cap * PH);
-  D.act_out = C.take<double>(e * D.act_cap * 12);
+  D.act_out = C.take<double>(1);
+  D.spos = C.take<int>(e * 4 * D.act_cap); D.sout = C.take<double>(e * 4 * D.act_cap * 3);
+  D.act_slot = C.take<int>(e * 4 * D.act_cap); D.act_xb = C.take<double>(e * 12 * D.act_cap);
   D.cptr = C.take<int>(e * (H.V + 1)); D.clist = C.take<int>(e * 4 * D.act_cap);
   D.bptr = C.take<int>(e * (H.ND + 1)); D.blist = C.take<int>(e * 4 * D.act_cap);
   D.eterm = C.take<double>(e * 8);
@@ -477,7 +504,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
 
 static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, const tac_scene_desc* sc) {
   D.E = E; D.V = H.V; D.T = H.T; D.NA = H.NA; D.ND = H.ND; D.NVall = H.NVall; D.NSV = H.NSV; D.NT = H.NT;
-  D.NE = H.NE; D.NEs = H.NEs; D.NC = H.NC; D.NK = H.NK; D.NB = H.NB; D.n = H.n; D.npads = H.npads;
+  D.NE = H.NE; D.NEs = H.NEs; D.NNZ = H.NNZ; D.NC = H.NC; D.NK = H.NK; D.NB = H.NB; D.n = H.n; D.npads = H.npads;
   D.NCOAT = H.NCOAT; D.NMARK = H.NMARK; D.NAV = (int)H.affv_list.size(); D.NKV = (int)H.kin_vlist.size();
   D.cand_cap = std::max(cfg->cand_capacity_per_env, 64);
   D.act_cap = std::max(cfg->active_capacity_per_env, 16);
@@ -546,7 +573,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, need, st);
 #define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
   UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
-  UP(eblk_ptr); UP(eblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
+  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
   UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
   UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
@@ -640,8 +667,15 @@ extern "C" tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, con
   return TAC_OK;
 }
 
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st) {
   Dev& D = b->D;
+  b->it_active.clear();
+  b->it_ms.clear();
+  double t0 = now_ms();
   { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 0, 0, st); }
   { PROF(PH_BROAD_STATIC); launch_broad(D, env0, ne, 0, 0, st); }
   for (int it = 0; it <= D.max_newton + 1; ++it) {
@@ -661,6 +695,10 @@ static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st) {
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
     if (b->prof) prof_flush(b);
+    double t1 = now_ms();
+    b->it_active.push_back(*b->h_flag);
+    b->it_ms.push_back(t1 - t0);
+    t0 = t1;
     if (!*b->h_flag) break;
   }
   return TAC_OK;
@@ -755,6 +793,17 @@ extern "C" tac_status tac_profile_read(tac_batch* b, double* ms, int64_t* launch
     if (ms) ms[i] = b->prof_ms[i];
     if (launches) launches[i] = b->prof_n[i];
     if (reset) { b->prof_ms[i] = 0; b->prof_n[i] = 0; }
+  }
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_profile_iterations(tac_batch* b, int32_t* active, double* ms, int32_t cap, int32_t* n) {
+  if (!b) return fail(TAC_E_INVALID, "null batch");
+  int m = (int)b->it_active.size();
+  if (n) *n = m;
+  for (int i = 0; i < std::min(m, cap); ++i) {
+    if (active) active[i] = b->it_active[i];
+    if (ms) ms[i] = b->it_ms[i];
   }
   return TAC_OK;
 }

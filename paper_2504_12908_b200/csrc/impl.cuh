@@ -38,6 +38,7 @@ struct EnvCtl {
 
 struct Dev {
   // ---- dims ----
+  int NNZ;                // off-diagonal soft blocks in row order (2·NEs)
   int E, V, T, NA, ND, NVall, NSV, NT, NE, NEs, NC, NK, NB, n, npads, NCOAT, NMARK;
   int cand_cap, act_cap, ent_cap;
   // ---- config ----
@@ -60,6 +61,10 @@ struct Dev {
   const int* vdiag;       // entries 4*tet + local
   const int* eblk_ptr;    // [NEs+1]
   const int* eblk;        // entries 16*tet + 4*a + b (local a ↔ edge.i, b ↔ edge.j)
+  const int* rptr;        // [V+1] row-ordered symmetric BSR
+  const int* rcol;        // [NNZ] column (neighbour vertex)
+  const int* rblk_ptr;    // [NNZ+1]
+  const int* rblk;        // entries 16*tet + 4*a + b (a ↔ row, b ↔ column)
   const int* body_kind;   // [NA]
   const int* dof_slot;    // [NA] (-1 static)
   const int* dof_body;    // [ND]
@@ -107,18 +112,23 @@ struct Dev {
   double *s_att, *lam_att;// [E][NC][3]
   double *s_kin, *lam_kin, *ykin;  // [E][NK][12]
   double *P, *Pd;         // [E][NVall][3] positions at q, displacement of p
-  double *Hd, *Ho;        // [E][V][9], [E][NEs][9]
+  double *Hd, *Ho;        // [E][V][9], [E][NNZ][9] (row-ordered off-diagonal blocks)
   double *Hb;             // [E][ND][144]
   double *Pinv_s, *Pinv_b;// [E][V][9], [E][ND][144]
   double* tetbuf;         // [E][90][T]
   int *cand_a, *cand_b;   // [E][cand_cap] (cand_a bit 30 = EE)
   int* ent;               // [E][ent_cap][2]
   int* big;               // [E][BIG_CAP]
+  double* tbox;           // [E][NT+NE][6] raw target boxes (broad-phase cache)
   int* act_info;          // [E][act_cap][4] (kind, type, a, b)
   int* act_vid;           // [E][act_cap][4]
   double* act_g;          // [E][act_cap][12]
   double* act_H;          // [E][act_cap][78]
-  double* act_out;        // [E][act_cap][12]
+  double* act_out;        // [E][act_cap][12] (unused)
+  int* act_slot;          // [E][4*act_cap] slot code: soft vertex ≥ 0, DoF body d → −1−d, static → INT_MIN
+  double* act_xb;         // [E][4*act_cap][3] rest position x̄ of affine slots
+  int* spos;              // [E][4*act_cap] slot → position in the soft output list (-1: not soft)
+  double* sout;           // [E][4*act_cap][3] per-slot soft outputs of the pair SpMV pass
   int* cptr;              // [E][V+1] soft contribution lists
   int* clist;             // [E][4*act_cap]
   int* bptr;              // [E][ND+1] body contribution lists

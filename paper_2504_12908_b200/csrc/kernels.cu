@@ -3,6 +3,7 @@
 // reductions are deterministic block reductions with a fixed thread→element assignment, so every
 // env's result is bitwise independent of the batch size and of how envs are sharded.
 #include <cfloat>
+#include <climits>
 #include "eigen.cuh"
 #include "elastic.cuh"
 #include "geometry.cuh"
@@ -118,6 +119,8 @@ __device__ __forceinline__ int ccode(int i, int j, int k) { return i | (j << 10)
 
 struct BoxCtx {
   const double* P; const double* Pd; int swept;
+  double* tb;      // raw target boxes [NT+NE][6] (lo, hi), filled in pass 1 of k_broad
+  int NT;
   __device__ void vbox(int gv, v3& lo, v3& hi) const {
     v3 a = ld3(P + 3 * gv);
     lo = a; hi = a;
@@ -139,10 +142,16 @@ __device__ __forceinline__ bool overlap(v3 qlo, v3 qhi, v3 tlo_i, v3 thi_i) {
          tlo_i.z <= qhi.z;
 }
 
-__device__ __forceinline__ void target_box(const Dev& D, const BoxCtx& B, int code, v3& lo, v3& hi) {
+__device__ __forceinline__ int tbox_index(const BoxCtx& B, int code) { return (code & 1) ? B.NT + (code >> 1) : (code >> 1); }
+__device__ __forceinline__ void raw_target_box(const Dev& D, const BoxCtx& B, int code, v3& lo, v3& hi) {
   int t = code >> 1;
   if ((code & 1) == 0) B.box(D.tris + 3 * t, 3, lo, hi);
   else B.box(D.edges + 2 * t, 2, lo, hi);
+}
+// inflated (by d̂) box of a target from the cache
+__device__ __forceinline__ void target_box(const Dev& D, const BoxCtx& B, int code, v3& lo, v3& hi) {
+  const double* c = B.tb + 6 * (size_t)tbox_index(B, code);
+  lo = mk(c[0], c[1], c[2]); hi = mk(c[3], c[4], c[5]);
   v3 dh = mk(D.dhat, D.dhat, D.dhat);
   lo = lo - dh; hi = hi + dh;
 }
@@ -160,8 +169,8 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
   } else {
     qa = qi - D.NSV;
     qbody = D.edge_body[qa];
-    qv[0] = D.edges[2 * qa]; qv[1] = D.edges[2 * qa + 1];
-    B.box(qv, 2, qlo, qhi);
+    const double* c = B.tb + 6 * (size_t)(B.NT + qa);
+    qlo = mk(c[0], c[1], c[2]); qhi = mk(c[3], c[4], c[5]);
   }
   const int want = pt ? 0 : 1;
   const unsigned char* allow = D.allowed + (size_t)qbody * D.NB;
@@ -223,7 +232,8 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
   return count;
 }
 
-__global__ void __launch_bounds__(NTHREADS) k_broad(Dev D, int env0, int swept, int force) {
+constexpr int BROAD_THREADS = 512;
+__global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int swept, int force) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
   if (!force && (C.phase != PHASE_ACTIVE || (swept && (C.inner_conv || C.xfail)))) return;
@@ -232,7 +242,8 @@ __global__ void __launch_bounds__(NTHREADS) k_broad(Dev D, int env0, int swept, 
   __shared__ double red[32];
   __shared__ int sh[33];
   __shared__ int nbig_s, ovf_s;
-  BoxCtx B{D.P + (size_t)e * D.NVall * 3, D.Pd + (size_t)e * D.NVall * 3, swept};
+  BoxCtx B{D.P + (size_t)e * D.NVall * 3, D.Pd + (size_t)e * D.NVall * 3, swept,
+           D.tbox + (size_t)e * (D.NT + D.NE) * 6, D.NT};
   int* ent = D.ent + (size_t)e * D.ent_cap * 2;
   int* big = D.big + (size_t)e * BIG_CAP;
   // grid origin: min corner over all surface vertices (start and end positions)
@@ -251,11 +262,15 @@ __global__ void __launch_bounds__(NTHREADS) k_broad(Dev D, int env0, int swept, 
   if (threadIdx.x == 0) { nbig_s = 0; ovf_s = 0; }
   __syncthreads();
   const int ntarget = D.NT + D.NE;
-  // pass 1: count cell entries of every target (inflated box)
+  // pass 1: raw boxes of every target into the cache; count cell entries (inflated box)
   for (int i = threadIdx.x; i < ntarget; i += blockDim.x) {
     int code = i < D.NT ? 2 * i : 2 * (i - D.NT) + 1;
     v3 lo, hi;
-    target_box(D, B, code, lo, hi);
+    raw_target_box(D, B, code, lo, hi);
+    double* c = B.tb + 6 * (size_t)i;
+    c[0] = lo.x; c[1] = lo.y; c[2] = lo.z; c[3] = hi.x; c[4] = hi.y; c[5] = hi.z;
+    v3 dh = mk(D.dhat, D.dhat, D.dhat);
+    lo = lo - dh; hi = hi + dh;
     int l[3], h[3];
     G.cell(lo, l); G.cell(hi, h);
     long nc = (long)(h[0] - l[0] + 1) * (h[1] - l[1] + 1) * (h[2] - l[2] + 1);
@@ -378,7 +393,20 @@ __global__ void __launch_bounds__(NTHREADS) k_narrow(Dev D, int env0, int force)
     int pos = total + ex;
     if (flag && pos < D.act_cap) {
       info[4 * pos] = kind; info[4 * pos + 1] = type; info[4 * pos + 2] = a; info[4 * pos + 3] = b;
-      for (int s = 0; s < 4; ++s) avid[4 * pos + s] = vid[s];
+      int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap + 4 * pos;
+      double* axb = D.act_xb + (size_t)e * 12 * D.act_cap + 12 * pos;
+      for (int s = 0; s < 4; ++s) {
+        avid[4 * pos + s] = vid[s];
+        int code;
+        if (vid[s] < D.V) code = vid[s];
+        else {
+          const int d = D.dof_slot[D.vert_aff[vid[s]]];
+          code = d >= 0 ? -1 - d : INT_MIN;
+          axb[3 * s] = D.vert_xbar[3 * vid[s]]; axb[3 * s + 1] = D.vert_xbar[3 * vid[s] + 1];
+          axb[3 * s + 2] = D.vert_xbar[3 * vid[s] + 2];
+        }
+        aslot[s] = code;
+      }
     }
     total += tot;
   }
@@ -411,6 +439,9 @@ __global__ void __launch_bounds__(NTHREADS) k_narrow(Dev D, int env0, int force)
       if (gv < D.V) { int pos = atomicAdd(&vcur[gv], 1); clist[pos] = 4 * k + s; }
     }
   __syncthreads();
+  int* spos = D.spos + (size_t)e * 4 * D.act_cap;
+  for (int i = threadIdx.x; i < 4 * nact; i += blockDim.x) spos[i] = -1;
+  __syncthreads();
   for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
     int b0 = cptr[v], b1 = cptr[v + 1];
     for (int i = b0 + 1; i < b1; ++i) {
@@ -418,6 +449,7 @@ __global__ void __launch_bounds__(NTHREADS) k_narrow(Dev D, int env0, int force)
       while (j >= b0 && clist[j] > key) { clist[j + 1] = clist[j]; --j; }
       clist[j + 1] = key;
     }
+    for (int i = b0; i < b1; ++i) spos[clist[i]] = i;     // slot → position of its soft output
   }
   // body contribution lists: stable block scan per dof body
   int* bptr = D.bptr + (size_t)e * (D.ND + 1);
@@ -578,7 +610,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
       __syncwarp();
       jacobi12_psd(S.J, lane, 32);
     }
-    for (int i = lane; i < PH; i += 32) aH[(size_t)PH * k + i] = S.J.A[12 * c_unpack_r[i] + c_unpack_c[i]];
+    for (int i = lane; i < PH; i += 32) aH[(size_t)i * D.act_cap + k] = S.J.A[12 * c_unpack_r[i] + c_unpack_c[i]];
     __syncwarp();
   }
 }
@@ -633,7 +665,8 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
   const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
   const int* bptr = D.bptr + (size_t)e * (D.ND + 1);
   const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
-  const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
+  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
+  const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
   const double dt2 = D.dt * D.dt, rho = C.rho;
   const double* s_att = D.s_att + (size_t)e * D.NC * 3;
   const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
@@ -662,22 +695,25 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
       int k = clist[j] >> 2, s = clist[j] & 3;
       gv += ld3(ag + 12 * k + 3 * s);
       for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) Pv[3 * r + c] += aH[(size_t)PH * k + sym_idx(3 * s + r, 3 * s + c, 12)];
+        for (int c = 0; c < 3; ++c) Pv[3 * r + c] += aH[(size_t)sym_idx(3 * s + r, 3 * s + c, 12) * D.act_cap + k];
     }
     st3(g + 3 * v, gv);
-    double* hd = D.Hd + ((size_t)e * D.V + v) * 9;
-    for (int i = 0; i < 9; ++i) hd[i] = Hv[i];
-    inv33(Pv, D.Pinv_s + ((size_t)e * D.V + v) * 9);
+    double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]
+    for (int i = 0; i < 9; ++i) hd[(size_t)i * D.V + v] = Hv[i];
+    double Pi[9];
+    inv33(Pv, Pi);
+    double* ps = D.Pinv_s + (size_t)e * D.V * 9;       // SoA [9][V]
+    for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
   }
   // ---- soft edge blocks ----
-  for (int ei = threadIdx.x; ei < D.NEs; ei += blockDim.x) {
+  for (int ei = threadIdx.x; ei < D.NNZ; ei += blockDim.x) {
     double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = D.eblk_ptr[ei]; j < D.eblk_ptr[ei + 1]; ++j) {
-      int ent = D.eblk[j], t = ent >> 4, a = (ent >> 2) & 3, b = ent & 3;
+    for (int j = D.rblk_ptr[ei]; j < D.rblk_ptr[ei + 1]; ++j) {
+      int ent = D.rblk[j], t = ent >> 4, a = (ent >> 2) & 3, b = ent & 3;
       for (int r = 0; r < 3; ++r)
         for (int c = 0; c < 3; ++c) B[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * b + c, 12)) * D.T + t];
     }
-    double* ho = D.Ho + ((size_t)e * D.NEs + ei) * 9;
+    double* ho = D.Ho + ((size_t)e * D.NNZ + ei) * 9;
     for (int i = 0; i < 9; ++i) ho[i] = B[i];
   }
   // ---- affine DoF bodies: warp per body ----
@@ -739,19 +775,19 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
     double gacc = 0.0;
     for (int j = bptr[d] + w; j < bptr[d + 1]; j += nw) {
       const int k = blist[j] >> 2, s = blist[j] & 3;
-      const double* xs = D.vert_xbar + 3 * avid[4 * k + s];
+      const double* xs = axb + 12 * k + 3 * s;
       if (lane < 12) gacc += jf(lane, xs) * ag[12 * k + 3 * s + jrow(lane)];
+      const int4 code4 = reinterpret_cast<const int4*>(aslot)[k];
+      const int codes[4] = {code4.x, code4.y, code4.z, code4.w};
       for (int t = 0; t < 4; ++t) {
-        const int gvt = avid[4 * k + t];
-        if (gvt < D.V || D.vert_aff[gvt] != b) continue;
-        const double* xt = D.vert_xbar + 3 * gvt;
-        const double* Hk = aH + (size_t)PH * k;
+        if (codes[t] != -1 - d) continue;
+        const double* xt = axb + 12 * k + 3 * t;
 #pragma unroll
         for (int tt = 0; tt < 5; ++tt) {
           const int i = lane + 32 * tt;
           if (i < 144) {
             const int al = i / 12, be = i % 12;
-            acc[tt] += jf(al, xs) * jf(be, xt) * Hk[sym_idx(3 * s + jrow(al), 3 * t + jrow(be), 12)];
+            acc[tt] += jf(al, xs) * jf(be, xt) * aH[(size_t)sym_idx(3 * s + jrow(al), 3 * t + jrow(be), 12) * D.act_cap + k];
           }
         }
       }
@@ -785,80 +821,141 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
 // ------------------------------------------------------------------------------------------
 // matrix-free SpMV y = H x: soft BSR + affine 12×12 + pair 12×12 through J_v (deterministic)
 // ------------------------------------------------------------------------------------------
-__device__ void spmv(const Dev& D, int e, const double* x, double* y) {
+// Pass A: each warp takes 32 consecutive active pairs (one per lane): out = H_k x_local; soft-slot
+// outputs go to their vertex-sorted position sout[spos] (written once, summed in pass B without
+// dependent loads); DoF-body slots are pulled back through J_vᵀ and warp-reduced in a fixed order
+// into per-warp partials part[w][d][12].  Pass B: soft rows (BSR + contiguous sout range) and body
+// rows (Hb x_b + Σ_w part[w][d]).  Deterministic for a fixed blockDim.
+__device__ void spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/) {
   const EnvCtl& C = D.ctl[e];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
-  double* ao = D.act_out + (size_t)e * D.act_cap * 12;
-  const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
-  // pass A: per pair out_k = H_k x_local
-  for (int k = threadIdx.x; k < C.n_act; k += blockDim.x) {
-    double xl[12];
-    for (int s = 0; s < 4; ++s) {
-      int gv = avid[4 * k + s];
-      v3 u = mk(0, 0, 0);
-      if (gv < D.V) u = ld3(x + 3 * gv);
-      else {
-        int sl = D.dof_slot[D.vert_aff[gv]];
-        if (sl >= 0) u = embed(x + 3 * D.V + 12 * sl, ld3(D.vert_xbar + 3 * gv));
+  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
+  const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
+  const int* spos = D.spos + (size_t)e * 4 * D.act_cap;
+  double* sout = D.sout + (size_t)e * 4 * D.act_cap * 3;
+  const int nact = C.n_act;
+  const int nb12 = D.ND * 12;
+  for (int i = threadIdx.x; i < nw * nb12; i += blockDim.x) part[i] = 0.0;
+  __syncthreads();
+  for (int base = 32 * w; base < nact; base += blockDim.x) {
+    const int k = base + lane;
+    double out[12];
+    int bd[4] = {-1, -1, -1, -1};
+    v3 xbs[4];
+    if (k < nact) {
+      double xl[12];
+      const int4 code4 = reinterpret_cast<const int4*>(aslot)[k];
+      const int codes[4] = {code4.x, code4.y, code4.z, code4.w};
+      for (int s = 0; s < 4; ++s) {
+        const int cd = codes[s];
+        v3 u = mk(0, 0, 0);
+        if (cd >= 0) u = ld3(x + 3 * cd);
+        else if (cd != INT_MIN) {
+          const int sl = -1 - cd;
+          xbs[s] = ld3(axb + 12 * k + 3 * s);
+          u = embed(x + 3 * D.V + 12 * sl, xbs[s]);
+          bd[s] = sl;
+        }
+        xl[3 * s] = u.x; xl[3 * s + 1] = u.y; xl[3 * s + 2] = u.z;
       }
-      xl[3 * s] = u.x; xl[3 * s + 1] = u.y; xl[3 * s + 2] = u.z;
+      const double* H = aH + k;                         // SoA: entry i at H[i·act_cap]
+      const size_t cap = D.act_cap;
+#pragma unroll
+      for (int r = 0; r < 12; ++r) out[r] = 0.0;
+#pragma unroll
+      for (int r = 0; r < 12; ++r)
+#pragma unroll
+        for (int c = r; c < 12; ++c) {
+          const double h = H[(size_t)sym_idx(r, c, 12) * cap];
+          out[r] += h * xl[c];
+          if (c != r) out[c] += h * xl[r];
+        }
+      for (int s = 0; s < 4; ++s) {
+        const int j = spos[4 * k + s];
+        if (j >= 0) { double* o = sout + 3 * j; o[0] = out[3 * s]; o[1] = out[3 * s + 1]; o[2] = out[3 * s + 2]; }
+      }
+    } else {
+      for (int r = 0; r < 12; ++r) out[r] = 0.0;
     }
-    const double* H = aH + (size_t)PH * k;
-    for (int r = 0; r < 12; ++r) {
-      double acc = 0.0;
-      for (int c = 0; c < 12; ++c) acc += H[sym_idx(r, c, 12)] * xl[c];
-      ao[12 * k + r] = acc;
+    const bool touches = bd[0] >= 0 || bd[1] >= 0 || bd[2] >= 0 || bd[3] >= 0;
+    if (__ballot_sync(0xffffffffu, touches) == 0u) continue;
+    for (int d = 0; d < D.ND; ++d) {
+      const bool mine = bd[0] == d || bd[1] == d || bd[2] == d || bd[3] == d;
+      if (__ballot_sync(0xffffffffu, mine) == 0u) continue;
+      double c[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) c[i] = 0.0;
+      if (mine)
+        for (int s = 0; s < 4; ++s) {
+          if (bd[s] != d) continue;
+          for (int i = 0; i < 3; ++i) {
+            const double oi = out[3 * s + i];
+            c[i] += oi;
+            c[3 + 3 * i] += oi * xbs[s].x; c[4 + 3 * i] += oi * xbs[s].y; c[5 + 3 * i] += oi * xbs[s].z;
+          }
+        }
+#pragma unroll
+      for (int i = 0; i < 12; ++i) c[i] = warp_sum(c[i]);
+      if (lane == 0)
+        for (int i = 0; i < 12; ++i) part[w * nb12 + 12 * d + i] += c[i];
     }
   }
   __syncthreads();
   const int* cptr = D.cptr + (size_t)e * (D.V + 1);
-  const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
-  const double* Hd = D.Hd + (size_t)e * D.V * 9;
-  const double* Ho = D.Ho + (size_t)e * D.NEs * 9;
-  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
-    v3 acc = mul33(Hd + 9 * v, ld3(x + 3 * v));
-    for (int j = D.vadj_ptr[v]; j < D.vadj_ptr[v + 1]; ++j) {
-      int en = D.vadj[j], ei = en >> 1, second = en & 1;
-      int other = second ? D.sedge[2 * ei] : D.sedge[2 * ei + 1];
-      v3 xo = ld3(x + 3 * other);
-      acc += second ? mul33T(Ho + 9 * ei, xo) : mul33(Ho + 9 * ei, xo);
-    }
-    for (int j = cptr[v]; j < cptr[v + 1]; ++j) acc += ld3(ao + 12 * (clist[j] >> 2) + 3 * (clist[j] & 3));
-    st3(y + 3 * v, acc);
-  }
-  const int* bptr = D.bptr + (size_t)e * (D.ND + 1);
-  const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
-  for (int d = w; d < D.ND; d += nw) {
-    const double* xb = x + 3 * D.V + 12 * d;
-    const double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
-    double acc[12];
-    for (int i = 0; i < 12; ++i) acc[i] = 0.0;
-    for (int j = bptr[d] + lane; j < bptr[d + 1]; j += 32) {
-      int k = blist[j] >> 2, s = blist[j] & 3;
-      const double* xs = D.vert_xbar + 3 * avid[4 * k + s];
-      v3 o = ld3(ao + 12 * k + 3 * s);
-      for (int i = 0; i < 3; ++i) {
-        double oi = comp(o, i);
-        acc[i] += oi;
-        acc[3 + 3 * i] += oi * xs[0]; acc[4 + 3 * i] += oi * xs[1]; acc[5 + 3 * i] += oi * xs[2];
+  const double* Hd = D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
+  const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
+  // soft rows: 4 lanes per row; lane q of the group takes blocks j = rptr[v]+q, +4, ... (adjacent
+  // lanes read adjacent 72-byte blocks), then a 2-step shuffle reduction; lane q==0 adds the
+  // diagonal block and the contiguous pair outputs and stores
+  {
+    const int q = lane & 3;
+    const int rows_per_pass = blockDim.x >> 2;
+    for (int v0 = 0; v0 < D.V; v0 += rows_per_pass) {
+      const int v = v0 + (threadIdx.x >> 2);
+      const bool live = v < D.V;
+      v3 acc = mk(0, 0, 0);
+      if (live) {
+        const int j1 = D.rptr[v + 1];
+        for (int j = D.rptr[v] + q; j < j1; j += 4) acc += mul33(Ho + 9 * j, ld3(x + 3 * D.rcol[j]));
+      }
+      for (int o = 1; o < 4; o <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+      }
+      if (live && q == 0) {
+        const v3 xv = ld3(x + 3 * v);
+        const size_t V = D.V;
+        acc += mk(Hd[v] * xv.x + Hd[V + v] * xv.y + Hd[2 * V + v] * xv.z,
+                  Hd[3 * V + v] * xv.x + Hd[4 * V + v] * xv.y + Hd[5 * V + v] * xv.z,
+                  Hd[6 * V + v] * xv.x + Hd[7 * V + v] * xv.y + Hd[8 * V + v] * xv.z);
+        for (int j = cptr[v]; j < cptr[v + 1]; ++j) acc += ld3(sout + 3 * j);
+        st3(y + 3 * v, acc);
       }
     }
-    for (int i = 0; i < 12; ++i) acc[i] = warp_sum(acc[i]);
-    if (lane < 12) {
-      double s = 0.0;
-      for (int c = 0; c < 12; ++c) s += Hb[12 * lane + c] * xb[c];
-      double tot = 0.0;
-      for (int i = 0; i < 12; ++i) if (i == lane) tot = acc[i];
-      y[3 * D.V + 12 * d + lane] = s + tot;
-    }
+  }
+  for (int i = threadIdx.x; i < nb12; i += blockDim.x) {
+    const int d = i / 12, row = i % 12;
+    const double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144 + 12 * row;
+    const double* xb = x + 3 * D.V + 12 * d;
+    double sacc = 0.0;
+    for (int c = 0; c < 12; ++c) sacc += Hb[c] * xb[c];
+    for (int ww = 0; ww < nw; ++ww) sacc += part[ww * nb12 + i];
+    y[3 * D.V + i] = sacc;
   }
   __syncthreads();
 }
 
 __device__ void precond(const Dev& D, int e, const double* r, double* z) {
-  for (int v = threadIdx.x; v < D.V; v += blockDim.x)
-    st3(z + 3 * v, mul33(D.Pinv_s + ((size_t)e * D.V + v) * 9, ld3(r + 3 * v)));
+  const double* Ps = D.Pinv_s + (size_t)e * D.V * 9;    // SoA [9][V]
+  const size_t V = D.V;
+  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
+    const v3 rv = ld3(r + 3 * v);
+    st3(z + 3 * v, mk(Ps[v] * rv.x + Ps[V + v] * rv.y + Ps[2 * V + v] * rv.z,
+                      Ps[3 * V + v] * rv.x + Ps[4 * V + v] * rv.y + Ps[5 * V + v] * rv.z,
+                      Ps[6 * V + v] * rv.x + Ps[7 * V + v] * rv.y + Ps[8 * V + v] * rv.z));
+  }
   for (int i = threadIdx.x; i < 12 * D.ND; i += blockDim.x) {
     int d = i / 12, row = i % 12;
     const double* Pi = D.Pinv_b + ((size_t)e * D.ND + d) * 144 + 12 * row;
@@ -874,18 +971,24 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z) {
 // block-Jacobi PCG: H p = −g from p₀ = 0, stop at rᵀz ≤ η² r₀ᵀz₀ or max_pcg; then the
 // Newton convergence test ‖p‖_emb,∞ ≤ τ_N L_env and gᵀp.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
+// vsm = 1: the five PCG vectors live in shared memory (n small enough), p is copied out at the end
+__global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force, int vsm) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
+  extern __shared__ double dsmem[];     // [nw][ND][12] body partials, then (vsm) p, r, z, d, Ad
+  double* bpart = dsmem;
   EnvCtl& C = D.ctl[e];
   const int n = D.n;
   const double* g = D.g + (size_t)e * n;
-  double* p = D.p + (size_t)e * n;
-  double* r = D.r + (size_t)e * n;
-  double* z = D.z + (size_t)e * n;
-  double* d = D.dd + (size_t)e * n;
-  double* Ad = D.Ad + (size_t)e * n;
+  double* const p_out = D.p + (size_t)e * n;
+  double *p, *r, *z, *d, *Ad;
+  if (vsm) {
+    double* base = dsmem + ((NTHREADS / 32) * D.ND * 12 + 1);
+    p = base; r = base + n; z = base + 2 * n; d = base + 3 * n; Ad = base + 4 * n;
+  } else {
+    p = p_out; r = D.r + (size_t)e * n; z = D.z + (size_t)e * n; d = D.dd + (size_t)e * n; Ad = D.Ad + (size_t)e * n;
+  }
   for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
   __syncthreads();
   precond(D, e, r, z);
@@ -896,7 +999,7 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
   int it = 0;
   bool bad = !(rz0 == rz0);
   while (!bad && it < D.max_pcg && rz > stop) {
-    spmv(D, e, d, Ad);
+    spmv(D, e, d, Ad, bpart);
     part = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
     double dAd = block_sum(part, red);
@@ -914,6 +1017,11 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
     rz = rzn;
     ++it;
     if (!(rz == rz)) bad = true;
+  }
+  if (vsm) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p_out[i] = p[i];
+    __syncthreads();
+    p = p_out;
   }
   // gᵀp and embedded ∞-norm
   part = 0.0;
@@ -950,7 +1058,8 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force) {
 
 __global__ void __launch_bounds__(NTHREADS) k_spmv(Dev D, int env0, const double* x, double* y) {
   const int e = env0 + blockIdx.x;
-  spmv(D, e, x, y);
+  extern __shared__ double part[];
+  spmv(D, e, x, y, part);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1240,7 +1349,7 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
   }
   if (threadIdx.x == 0) {
     if (C.phase == PHASE_ACTIVE && C.newton >= D.max_newton) { C.phase = PHASE_FAILED; C.status = ENV_NEWTON_STALL; }
-    if (C.phase == PHASE_ACTIVE) atomicOr(D.any_active, 1);
+    if (C.phase == PHASE_ACTIVE) atomicAdd(D.any_active, 1);
   }
 }
 
@@ -1417,7 +1526,7 @@ void launch_positions(const Dev& D, int env0, int ne, int with_p, int force, cud
   k_positions<<<ne, NTHREADS, 0, s>>>(D, env0, with_p, force);
 }
 void launch_broad(const Dev& D, int env0, int ne, int swept, int force, cudaStream_t s) {
-  k_broad<<<ne, NTHREADS, 0, s>>>(D, env0, swept, force);
+  k_broad<<<ne, BROAD_THREADS, 0, s>>>(D, env0, swept, force);
 }
 void launch_narrow(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   size_t smem = (size_t)(2 * D.V + 1) * sizeof(int);
@@ -1434,11 +1543,20 @@ void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   k_assemble<<<ne, NTHREADS, 0, s>>>(D, env0, force);
 }
+static size_t spmv_smem(const Dev& D) { return (size_t)(NTHREADS / 32) * D.ND * 12 * sizeof(double) + 8; }
 void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  k_pcg<<<ne, NTHREADS, 0, s>>>(D, env0, force);
+  const size_t with_vec = spmv_smem(D) + (size_t)5 * D.n * sizeof(double);
+  const int vsm = with_vec <= 200 * 1024 ? 1 : 0;
+  const size_t bytes = vsm ? with_vec : spmv_smem(D);
+  static size_t configured = 0;
+  if (bytes > 48 * 1024 && bytes > configured) {
+    cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    configured = bytes;
+  }
+  k_pcg<<<ne, NTHREADS, bytes, s>>>(D, env0, force, vsm);
 }
 void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s) {
-  k_spmv<<<1, NTHREADS, 0, s>>>(D, env0, x, y);
+  k_spmv<<<1, NTHREADS, spmv_smem(D), s>>>(D, env0, x, y);
 }
 void launch_ccd(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   k_ccd<<<ne, NTHREADS, 0, s>>>(D, env0, force);

@@ -103,6 +103,7 @@ def load():
             "tac_debug_pcg": [vp, ctypes.c_int32, vp, vp, vp, c_int_p, vp],
             "tac_profile_enable": [vp, ctypes.c_int32],
             "tac_profile_read": [vp, c_double_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32],
+            "tac_profile_iterations": [vp, c_int_p, c_double_p, ctypes.c_int32, c_int_p],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
@@ -301,6 +302,14 @@ class Batch:
         n = (ctypes.c_int64 * self.NPHASES)()
         _check(self.lib.tac_profile_read(self.handle, ms, n, 1 if reset else 0))
         return {self.lib.tac_profile_phase_name(i).decode(): (ms[i], n[i]) for i in range(self.NPHASES)}
+
+    def profile_iterations(self):
+        n = ctypes.c_int32()
+        _check(self.lib.tac_profile_iterations(self.handle, None, None, 0, ctypes.byref(n)))
+        act = (ctypes.c_int32 * max(n.value, 1))()
+        ms = (ctypes.c_double * max(n.value, 1))()
+        _check(self.lib.tac_profile_iterations(self.handle, act, ms, n.value, ctypes.byref(n)))
+        return list(act)[:n.value], list(ms)[:n.value]
 
     # ---- parity hooks (host numpy) ------------------------------------------------------------
     def debug_eval(self, env, x, y, lam_att=None, lam_kin=None, rho=0.0, v=None, exact=False):

@@ -21,6 +21,9 @@ for k in range(NS):
     print(k, f"{time.time()-t:.2f}s", dict(collections.Counter(st.tolist())), "newton max/mean %d/%.1f" % (nw.max(), nw.mean()),
           "pcg max/mean %d/%.0f" % (pc.max(), pc.mean()), "nact max", max(x["n_active"] for x in s),
           "ncand max", max(x["n_candidates"] for x in s), flush=True)
+    act, ms = b.profile_iterations()
+    print("    iters", len(act), "active:", act[:12], "... ms:", ["%.1f" % v for v in ms[:12]], "... tail ms/iter %.2f" %
+          (sum(ms[12:]) / max(len(ms) - 12, 1)), "bulk(first 12) %.0f ms, tail %.0f ms" % (sum(ms[:12]), sum(ms[12:])))
 print("first failures (step, status, newton, nact, ncand, al):")
 for i, v in list(first_fail.items())[:30]:
     print("  env", i, v)
