@@ -117,11 +117,14 @@ typedef struct {
   double armijo_c, accd_s, al_rho0;
   int32_t max_newton, max_al_rounds, max_pcg, max_accd_iters, ee_mollifier;
   int32_t hessian_mode;          /* 0: PSD-projected element Hessians; 1: exact Hessian first, projected
-                                    fallback with back-off when PCG meets dᵀHd ≤ 0 or gᵀp ≥ 0 (DESIGN R14b) */
+                                    fallback with back-off when PCG meets dᵀHd ≤ 0 or gᵀp ≥ 0 (DESIGN R14b);
+                                    2: exact Hessian with a mass-scaled Levenberg-Marquardt shift μM,
+                                    μ ← max(lm_mu0, 10μ) on failure, μ/10 after success (DESIGN R14c) */
   int32_t ls_expand;             /* line-search expansion bound K (power of 2; 1 = plain backtracking):
                                     swept sets and ACCD cover [x, x + K·p]; after a full step α doubles
                                     while the energy keeps decreasing (DESIGN R17b)                    */
   int32_t hold_cap;              /* max projected iterations between exact-Hessian attempts           */
+  double lm_mu0;                 /* first LM shift of hessian_mode 2                                  */
   int32_t cand_capacity_per_env, active_capacity_per_env;
 } tac_config;
 

@@ -131,6 +131,20 @@ def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
     return p, it
 
 
+def mass_matrix(model: Model):
+    """M over the DoFs: lumped m_v I₃ per soft vertex and M^y per non-static body."""
+    n = model.n_dof
+    rows, cols, vals = [np.arange(3 * model.V)], [np.arange(3 * model.V)], [np.repeat(model.mass, 3)]
+    for bi in range(len(model.body_xbar)):
+        s_ = model.dof_slot[bi]
+        if s_ < 0:
+            continue
+        idx = np.arange(3 * model.V + 12 * s_, 3 * model.V + 12 * s_ + 12)
+        R, Cc = np.meshgrid(idx, idx, indexing="ij")
+        rows.append(R.ravel()); cols.append(Cc.ravel()); vals.append(model.body_My[bi].ravel())
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n)).tocsr()
+
+
 def sweep_factor(cfg, p_inf):
     """K_eff (reading R17b): the largest power of two ≤ ls_expand with K_eff·‖p‖_emb,∞ ≤ d̂, at
     least 1 — the expansion sweep never reaches further than d̂ beyond a normal Newton step."""
@@ -156,7 +170,7 @@ def _solve_spd(model, H, g, solver, cfg, stats):
         stats.pcg_iters += it
         if p is None:
             return None
-    if not (g @ p < 0):
+    if not (g @ p < 0) and np.any(g):
         return None
     return p
 
@@ -174,6 +188,8 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
     hold = 0          # projected iterations left before the exact Hessian is tried again
     nfail = 0         # consecutive failed exact attempts (back-off 2, 4, ... 64)
     mode = cfg.hessian_mode
+    mu = 0.0          # mass-scaled Levenberg-Marquardt shift (hessian_mode 2, reading R14c)
+    Mreg = mass_matrix(model) if mode == 2 else None
     for al_round in range(cfg.max_al_rounds):
         stats.al_rounds = al_round + 1
         converged = False
@@ -181,6 +197,16 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
             P = all_positions(model, x, y)
             pairs = C.active_pairs(model, P)
             p = None
+            mu_used = 0.0
+            if mode == 2:
+                g, H = En.assemble(model, ctx, x, y, pairs, project=False)
+                while True:
+                    p = _solve_spd(model, H + mu * Mreg if mu > 0 else H, g, solver, cfg, stats)
+                    if p is not None or mu > 1e12:
+                        break
+                    mu = max(cfg.lm_mu0, 10.0 * mu)
+                mu_used = mu
+                mu = mu * 0.1 if mu * 0.1 >= cfg.lm_mu0 else 0.0
             if mode == 1 and hold == 0:
                 g, H = En.assemble(model, ctx, x, y, pairs, project=False)
                 p = _solve_spd(model, H, g, solver, cfg, stats)
@@ -202,7 +228,7 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
                 stats.status = NONFINITE
                 break
             p_inf = embedded_inf_norm(model, p)
-            if p_inf <= cfg.newton_tol_rel * L:
+            if p_inf <= cfg.newton_tol_rel * L and mu_used == 0.0:
                 converged = True
                 break
             if p_inf > cfg.max_step_rel * L:            # step cap (reading R17c)

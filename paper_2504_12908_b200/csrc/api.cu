@@ -484,6 +484,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.Hd = C.take<double>(e * H.V * 9 + 1); D.Ho = C.take<double>(e * H.NNZ * 9 + 1);
   D.Hb = C.take<double>(e * H.ND * 144 + 1); D.Pinv_s = C.take<double>(e * H.V * 9 + 1);
   D.Pinv_b = C.take<double>(e * H.ND * 144 + 1);
+  D.Dg_s = C.take<double>(e * H.V * 9 + 1); D.Dg_b = C.take<double>(e * H.ND * 144 + 1);
   D.tetbuf = C.take<double>(e * TETBUF * H.T + 1);
   D.cand_a = C.take<int>(e * D.cand_cap); D.cand_b = C.take<int>(e * D.cand_cap);
   D.ent = C.take<int>(e * D.ent_cap * 2); D.big = C.take<int>(e * BIG_CAP);
@@ -514,14 +515,14 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.eta = cfg->pcg_eta; D.armijo = cfg->armijo_c; D.accd_s = cfg->accd_s; D.rho0 = cfg->al_rho0; D.cell = H.cell;
   D.max_newton = cfg->max_newton; D.max_al = cfg->max_al_rounds; D.max_pcg = cfg->max_pcg;
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
-  D.hold_cap = std::max(cfg->hold_cap, 1); D.K = (double)std::max(cfg->ls_expand, 1);
+  D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.K = (double)std::max(cfg->ls_expand, 1);
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
 }
 
 static tac_status check_cfg(const tac_config* c) {
   if (!(c->max_step_rel > 0) || !(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
       c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1) || c->hessian_mode < 0 ||
-      c->hessian_mode > 1 || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0)
+      c->hessian_mode > 2 || !(c->lm_mu0 > 0) || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0)
     return fail(TAC_E_INVALID, "invalid tac_config");
   return TAC_OK;
 }

@@ -32,6 +32,7 @@ struct EnvCtl {
   long long pcg_total;
   double pcg_bytes;
   double Keff;
+  double mu;              // LM shift for the next solve (hessian_mode 2)
   double ls_E0, ls_E1;
   double alpha_ccd, alpha_min, rho, r_prev, L, energy, residual, gp, pnorm, alpha;
 };
@@ -46,6 +47,7 @@ struct Dev {
   double dt, dhat, kappa, tolN, tolAL, eta, armijo, accd_s, rho0, cell;
   int max_newton, max_al, max_pcg, max_accd, mollify, hmode, hold_cap;
   double K;                 // line-search expansion bound (reading R17b)
+  double lm_mu0;
   double grav[3];
   // ---- template ----
   const int* tets;        // [T][4]
@@ -115,6 +117,7 @@ struct Dev {
   double *Hd, *Ho;        // [E][V][9], [E][NNZ][9] (row-ordered off-diagonal blocks)
   double *Hb;             // [E][ND][144]
   double *Pinv_s, *Pinv_b;// [E][V][9], [E][ND][144]
+  double *Dg_s, *Dg_b;    // raw block-Jacobi diagonal blocks (before the LM shift and inversion)
   double* tetbuf;         // [E][90][T]
   int *cand_a, *cand_b;   // [E][cand_cap] (cand_a bit 30 = EE)
   int* ent;               // [E][ent_cap][2]

@@ -700,6 +700,10 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
     st3(g + 3 * v, gv);
     double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]
     for (int i = 0; i < 9; ++i) hd[(size_t)i * D.V + v] = Hv[i];
+    double* ds = D.Dg_s + (size_t)e * D.V * 9;         // raw diagonal block (SoA) for LM re-inversion
+    for (int i = 0; i < 9; ++i) ds[(size_t)i * D.V + v] = Pv[i];
+    const double sh = C.mu * m;                         // mass-scaled LM shift μ·m_v I (R14c)
+    Pv[0] += sh; Pv[4] += sh; Pv[8] += sh;
     double Pi[9];
     inv33(Pv, Pi);
     double* ps = D.Pinv_s + (size_t)e * D.V * 9;       // SoA [9][V]
@@ -810,6 +814,9 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
         for (int ww = 0; ww < nw; ++ww) v += GB[ww][lane];
         g[3 * D.V + 12 * d + lane] = v;
       }
+      double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
+      const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
+      for (int i = lane; i < 144; i += 32) { Db[i] = T[i]; T[i] += C.mu * Mb[i]; }
       __syncwarp();
       if (lane == 0) chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q);
       __syncwarp();
@@ -826,7 +833,8 @@ __global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int forc
 // dependent loads); DoF-body slots are pulled back through J_vᵀ and warp-reduced in a fixed order
 // into per-warp partials part[w][d][12].  Pass B: soft rows (BSR + contiguous sout range) and body
 // rows (Hb x_b + Σ_w part[w][d]).  Deterministic for a fixed blockDim.
-__device__ void spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/) {
+__device__ void spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
+                     double mu = 0.0) {
   const EnvCtl& C = D.ctl[e];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
@@ -931,6 +939,7 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
                   Hd[3 * V + v] * xv.x + Hd[4 * V + v] * xv.y + Hd[5 * V + v] * xv.z,
                   Hd[6 * V + v] * xv.x + Hd[7 * V + v] * xv.y + Hd[8 * V + v] * xv.z);
         for (int j = cptr[v]; j < cptr[v + 1]; ++j) acc += ld3(sout + 3 * j);
+        if (mu != 0.0) acc += (mu * D.mass[v]) * xv;
         st3(y + 3 * v, acc);
       }
     }
@@ -941,8 +950,36 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
     const double* xb = x + 3 * D.V + 12 * d;
     double sacc = 0.0;
     for (int c = 0; c < 12; ++c) sacc += Hb[c] * xb[c];
+    if (mu != 0.0) {
+      const double* Mr = D.My + (size_t)D.dof_body[d] * 144 + 12 * row;
+      for (int c = 0; c < 12; ++c) sacc += mu * Mr[c] * xb[c];
+    }
     for (int ww = 0; ww < nw; ++ww) sacc += part[ww * nb12 + i];
     y[3 * D.V + i] = sacc;
+  }
+  __syncthreads();
+}
+
+// block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c)
+__device__ void reinvert_precond(const Dev& D, int e, double mu, double* scratch /*smem 144*/) {
+  const double* ds = D.Dg_s + (size_t)e * D.V * 9;
+  double* ps = D.Pinv_s + (size_t)e * D.V * 9;
+  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
+    double Pv[9], Pi[9];
+    for (int i = 0; i < 9; ++i) Pv[i] = ds[(size_t)i * D.V + v];
+    const double sh = mu * D.mass[v];
+    Pv[0] += sh; Pv[4] += sh; Pv[8] += sh;
+    inv33(Pv, Pi);
+    for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
+  }
+  for (int d = 0; d < D.ND; ++d) {
+    if (threadIdx.x == 0) {
+      double T[144];
+      const double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
+      const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
+      for (int i = 0; i < 144; ++i) T[i] = Db[i] + mu * Mb[i];
+      chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, scratch);
+    }
   }
   __syncthreads();
 }
@@ -989,45 +1026,59 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force, in
   } else {
     p = p_out; r = D.r + (size_t)e * n; z = D.z + (size_t)e * n; d = D.dd + (size_t)e * n; Ad = D.Ad + (size_t)e * n;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
-  __syncthreads();
-  precond(D, e, r, z);
-  double part = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) { d[i] = z[i]; part += r[i] * z[i]; }
-  double rz = block_sum(part, red);
-  const double rz0 = rz, stop = D.eta * D.eta * rz0;
-  int it = 0;
-  bool bad = !(rz0 == rz0);
-  while (!bad && it < D.max_pcg && rz > stop) {
-    spmv(D, e, d, Ad, bpart);
-    part = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
-    double dAd = block_sum(part, red);
-    if (!(dAd > 0.0)) { bad = true; break; }          // H not SPD along d (uniform across the block)
-    double alpha = rz / dAd;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] += alpha * d[i]; r[i] -= alpha * Ad[i]; }
+  // hessian_mode 2 (reading R14c): solve (H + μM) p = −g; on negative curvature or a non-descent
+  // direction raise μ ← max(μ₀, 10μ), re-invert the block-Jacobi blocks and restart (same launch)
+  double mu = C.mu;
+  bool bad = false;
+  int it_total = 0;
+  double gp = 0.0;
+  bool zero_g = false;
+  __shared__ double chol_scratch[144];
+  for (int attempt = 0;; ++attempt) {
+    if (attempt > 0) reinvert_precond(D, e, mu, chol_scratch);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
     __syncthreads();
     precond(D, e, r, z);
+    double part = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { d[i] = z[i]; part += r[i] * z[i]; }
+    double rz = block_sum(part, red);
+    const double rz0 = rz, stop = D.eta * D.eta * rz0;
+    zero_g = rz0 == 0.0;                                 // g = 0: p = 0 is the (converged) answer
+    int it = 0;
+    bad = !(rz0 == rz0);
+    while (!bad && it < D.max_pcg && rz > stop) {
+      spmv(D, e, d, Ad, bpart, mu);
+      part = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
+      double dAd = block_sum(part, red);
+      if (!(dAd > 0.0)) { bad = true; break; }          // not SPD along d (uniform across the block)
+      double alpha = rz / dAd;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] += alpha * d[i]; r[i] -= alpha * Ad[i]; }
+      __syncthreads();
+      precond(D, e, r, z);
+      part = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) part += r[i] * z[i];
+      double rzn = block_sum(part, red);
+      double beta = rzn / rz;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = z[i] + beta * d[i];
+      __syncthreads();
+      rz = rzn;
+      ++it;
+      if (!(rz == rz)) bad = true;
+    }
+    it_total += it;
     part = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) part += r[i] * z[i];
-    double rzn = block_sum(part, red);
-    double beta = rzn / rz;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = z[i] + beta * d[i];
-    __syncthreads();
-    rz = rzn;
-    ++it;
-    if (!(rz == rz)) bad = true;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) part += g[i] * p[i];
+    gp = block_sum(part, red);
+    if (D.hmode != 2 || (!bad && (gp < 0.0 || zero_g)) || mu > 1e12) break;
+    mu = fmax(D.lm_mu0, 10.0 * mu);
   }
   if (vsm) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) p_out[i] = p[i];
     __syncthreads();
     p = p_out;
   }
-  // gᵀp and embedded ∞-norm
-  part = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) part += g[i] * p[i];
   double pm = embedded_inf_norm(D, e, p, red);
-  double gp = block_sum(part, red);
   // step cap (reading R17c): scale p to max_step·L_env if longer (direction unchanged)
   const double cap = D.max_step * C.L;
   if (pm > cap && pm == pm) {
@@ -1037,21 +1088,23 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force, in
     gp *= sc;
   }
   if (threadIdx.x == 0) {
-    const bool exact_failed = C.exact && (bad || !(gp < 0.0) || !(pm == pm));
-    C.pcg += it;
-    C.pcg_total += it;
+    const bool exact_failed = D.hmode == 1 && C.exact && (bad || !(gp < 0.0) || !(pm == pm));
+    C.pcg += it_total;
+    C.pcg_total += it_total;
     // algorithmic bytes per PCG iteration (SURVEY §8(d) model):
     // 72(V+E_s) + 4E_s + 640P + 624·ND + 48V + 624·ND + 96n
     const double bpi = 72.0 * (D.V + D.NEs) + 4.0 * D.NEs + 640.0 * C.n_act + 1248.0 * D.ND + 48.0 * D.V + 96.0 * D.n;
-    C.pcg_bytes += bpi * it;
+    C.pcg_bytes += bpi * it_total;
     C.gp = gp;
     C.pnorm = pm;
     if (exact_failed) {
       C.xfail = 1;                                        // retry projected next pass (not counted)
     } else {
       C.newton += 1;
-      if (bad || !(pm == pm)) { C.phase = PHASE_FAILED; C.status = ENV_NONFINITE; }
-      else C.inner_conv = (pm <= D.tolN * C.L) ? 1 : 0;
+      const double mu_used = D.hmode == 2 ? mu : 0.0;
+      if (D.hmode == 2) C.mu = (mu * 0.1 >= D.lm_mu0) ? mu * 0.1 : 0.0;
+      if (bad || !(pm == pm) || !(gp < 0.0 || zero_g)) { C.phase = PHASE_FAILED; C.status = ENV_NONFINITE; }
+      else C.inner_conv = (pm <= D.tolN * C.L && mu_used == 0.0) ? 1 : 0;
     }
   }
 }
@@ -1380,7 +1433,7 @@ __global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
     C.phase = PHASE_ACTIVE; C.status = ENV_OK; C.inner_conv = 0; C.newton = 0; C.pcg = 0; C.ls_bt = 0;
     C.al_rounds = 0; C.n_act = 0; C.ncand = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;
     C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
-    C.exact = D.hmode == 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0; C.Keff = 1.0;
+    C.exact = D.hmode >= 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0; C.Keff = 1.0; C.mu = 0.0;
   }
 }
 

@@ -75,9 +75,10 @@ class Config:
     max_pcg: int = 2000
     max_accd_iters: int = 10000
     ee_mollifier: int = 1
-    hessian_mode: int = 1          # 0: always PSD-projected; 1: exact first, projected fallback (R14b)
+    hessian_mode: int = 2          # 0: PSD-projected; 1: exact first + projected fallback (R14b); 2: exact + LM shift (R14c)
     ls_expand: int = 16            # line-search expansion bound K (R17b); 1 = plain backtracking
     hold_cap: int = 16             # max projected iterations between exact-Hessian attempts (R14b)
+    lm_mu0: float = 1.0            # first mass-scaled shift of hessian_mode 2 (R14c)
     cand_capacity_per_env: int = 65536
     active_capacity_per_env: int = 4096
 

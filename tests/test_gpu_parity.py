@@ -235,3 +235,32 @@ def test_bad_state_detected_and_isolated():
     b.set_targets(ei.ykin[0])
     st = b.step(1)
     assert st[0] == 0 and st[1] == 5
+
+
+def _free_body_scene(gravity):
+    V, Tr = S.box_surface((0.01, 0.01, 0.01))
+    body = S.AffineBody(V, Tr, kind=S.DYNAMIC)
+    return S.Scene("C1", [], [body], np.array(gravity, float), S.Config(dt=0.01), n_steps=1)
+
+
+def test_free_fall_and_fixed_point_through_abi():
+    """Closed forms through the C ABI: a free affine body moves by Δt v⁰ + Δt² g in one Newton
+    step; with no forces the state is a fixed point."""
+    sc = _free_body_scene((0, 0, -9.81))
+    b = T.Batch(sc, 2)
+    y0 = np.array([[[0.1, 0.2, 0.3, *S.rot_z(0.4).ravel()]], [[0.0, 0.0, 1.0, *np.eye(3).ravel()]]])
+    yd0 = np.array([[[0.5, -0.2, 0.1, *np.zeros(9)]], [[0.0] * 12]])
+    b.set_state(np.zeros((2, 0, 3)), y0, None, yd0)
+    assert (b.step(1) == 0).all()
+    y = b.get_state()[2].cpu().numpy()
+    dt = sc.config.dt
+    for e in range(2):
+        expect = y0[e, 0, :3] + dt * yd0[e, 0, :3] + dt * dt * sc.gravity
+        assert np.abs(y[e, 0, :3] - expect).max() <= 1e-15
+        assert np.abs(y[e, 0, 3:] - y0[e, 0, 3:]).max() <= 1e-15
+    sc0 = _free_body_scene((0, 0, 0))
+    b0 = T.Batch(sc0, 1)
+    b0.set_state(np.zeros((1, 0, 3)), y0[:1])
+    assert b0.step(1)[0] == 0
+    assert np.array_equal(b0.get_state()[2].cpu().numpy(), y0[:1])
+    assert b0.stats()[0]["newton_iters"] == 1
