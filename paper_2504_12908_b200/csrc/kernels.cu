@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
 // narrow phase: active set 𝒜 = {k ∈ C : s_k < d̂²} (strict) in canonical order, plus
 // deterministic soft-vertex and body contribution lists
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHREADS) k_narrow(Dev D, int env0, int force) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
   if (env_skip(D, e, force)) return;
@@ -648,7 +648,7 @@ __device__ void chol_inverse12(const double* A, double* Ainv, double* L /*144 sc
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS) k_assemble(Dev D, int env0, int force) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ JacobiScratch JS[NTHREADS / 32];
@@ -961,7 +961,7 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
 }
 
 // block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c)
-__device__ void reinvert_precond(const Dev& D, int e, double mu, double* scratch /*smem 144*/) {
+__device__ void reinvert_precond(const Dev& D, int e, double mu, double* scratch /*smem 144*/, double* T /*smem 144*/) {
   const double* ds = D.Dg_s + (size_t)e * D.V * 9;
   double* ps = D.Pinv_s + (size_t)e * D.V * 9;
   for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
@@ -973,13 +973,12 @@ __device__ void reinvert_precond(const Dev& D, int e, double mu, double* scratch
     for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
   }
   for (int d = 0; d < D.ND; ++d) {
-    if (threadIdx.x == 0) {
-      double T[144];
-      const double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
-      const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
-      for (int i = 0; i < 144; ++i) T[i] = Db[i] + mu * Mb[i];
-      chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, scratch);
-    }
+    const double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
+    const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
+    __syncthreads();
+    for (int i = threadIdx.x; i < 144; i += blockDim.x) T[i] = Db[i] + mu * Mb[i];
+    __syncthreads();
+    if (threadIdx.x == 0) chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, scratch);
   }
   __syncthreads();
 }
@@ -1009,7 +1008,7 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z) {
 // Newton convergence test ‖p‖_emb,∞ ≤ τ_N L_env and gᵀp.
 // ------------------------------------------------------------------------------------------
 // vsm = 1: the five PCG vectors live in shared memory (n small enough), p is copied out at the end
-__global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force, int vsm) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force, int vsm) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
@@ -1033,9 +1032,9 @@ __global__ void __launch_bounds__(NTHREADS) k_pcg(Dev D, int env0, int force, in
   int it_total = 0;
   double gp = 0.0;
   bool zero_g = false;
-  __shared__ double chol_scratch[144];
+  __shared__ double chol_scratch[144], chol_T[144];
   for (int attempt = 0;; ++attempt) {
-    if (attempt > 0) reinvert_precond(D, e, mu, chol_scratch);
+    if (attempt > 0) reinvert_precond(D, e, mu, chol_scratch, chol_T);
     for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
     __syncthreads();
     precond(D, e, r, z);
@@ -1142,7 +1141,7 @@ __device__ double accd_pair(int kind, v3* X, v3* Pd, double s, double tc, int ma
   return t;
 }
 
-__global__ void __launch_bounds__(NTHREADS) k_ccd(Dev D, int env0, int force) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_ccd(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
   if (!force && (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail)) return;
@@ -1261,7 +1260,7 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
   *inverted = __syncthreads_or(inv);
 }
 
-__global__ void __launch_bounds__(NTHREADS) k_energy(Dev D, int env0, double alpha) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_energy(Dev D, int env0, double alpha) {
   const int e = env0 + blockIdx.x;
   __shared__ double red[32];
   double t[6];
@@ -1276,7 +1275,7 @@ __global__ void __launch_bounds__(NTHREADS) k_energy(Dev D, int env0, double alp
 }
 
 // backtracking line search from α = min(1, α_ccd); Armijo c
-__global__ void __launch_bounds__(NTHREADS) k_linesearch(Dev D, int env0) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
   if (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail) return;
