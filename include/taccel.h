@@ -125,6 +125,9 @@ typedef struct {
                                     while the energy keeps decreasing (DESIGN R17b)                    */
   int32_t hold_cap;              /* max projected iterations between exact-Hessian attempts           */
   double lm_mu0;                 /* first LM shift of hessian_mode 2                                  */
+  double bp_margin;              /* δ (m): candidate lists are built with targets inflated by d̂+2δ and
+                                    reused while every surface vertex stays within δ of its box at the
+                                    last build; 0 = rebuild every Newton iteration (DESIGN R11b)       */
   int32_t cand_capacity_per_env, active_capacity_per_env;
 } tac_config;
 

@@ -489,6 +489,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.cand_a = C.take<int>(e * D.cand_cap); D.cand_b = C.take<int>(e * D.cand_cap);
   D.ent = C.take<int>(e * D.ent_cap * 2); D.big = C.take<int>(e * BIG_CAP);
   D.tbox = C.take<double>(e * (H.NT + H.NE) * 6);
+  D.vref = C.take<double>(e * H.NSV * 6 + 1);
   D.act_info = C.take<int>(e * D.act_cap * 4); D.act_vid = C.take<int>(e * D.act_cap * 4);
   D.act_g = C.take<double>(e * D.act_cap * 12); D.act_H = C.take<double>(e * D.act_cap * PH);
   D.act_out = C.take<double>(1);
@@ -515,14 +516,14 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.eta = cfg->pcg_eta; D.armijo = cfg->armijo_c; D.accd_s = cfg->accd_s; D.rho0 = cfg->al_rho0; D.cell = H.cell;
   D.max_newton = cfg->max_newton; D.max_al = cfg->max_al_rounds; D.max_pcg = cfg->max_pcg;
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
-  D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.K = (double)std::max(cfg->ls_expand, 1);
+  D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.bp_margin = cfg->bp_margin; D.K = (double)std::max(cfg->ls_expand, 1);
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
 }
 
 static tac_status check_cfg(const tac_config* c) {
   if (!(c->max_step_rel > 0) || !(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
       c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1) || c->hessian_mode < 0 ||
-      c->hessian_mode > 2 || !(c->lm_mu0 > 0) || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0)
+      c->hessian_mode > 2 || !(c->lm_mu0 > 0) || !(c->bp_margin >= 0) || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0)
     return fail(TAC_E_INVALID, "invalid tac_config");
   return TAC_OK;
 }
@@ -859,6 +860,8 @@ static tac_status dbg_leave(DebugScope& S) {
   CUDA_TRY(cudaMemcpyAsync(D.q + (size_t)e * D.n, S.q.data(), D.n * 8, cudaMemcpyHostToDevice, S.st));
   CUDA_TRY(cudaMemcpyAsync(D.vel + (size_t)e * D.n, S.vel.data(), D.n * 8, cudaMemcpyHostToDevice, S.st));
   CUDA_TRY(cudaMemcpyAsync(D.ystat + (size_t)e * D.NA * 12, S.ystat.data(), D.NA * 96, cudaMemcpyHostToDevice, S.st));
+  S.ctl.bp_ref = 0;                         // the debug build replaced the candidate list
+  S.ctl.bp_valid = 0;
   CUDA_TRY(cudaMemcpyAsync(D.ctl + e, &S.ctl, sizeof(EnvCtl), cudaMemcpyHostToDevice, S.st));
   CUDA_TRY(cudaStreamSynchronize(S.st));
   return TAC_OK;

@@ -83,6 +83,7 @@ struct SubDist {
   double s;             // squared distance
   double N, D, we, ww;  // PL
   v3 n; double u;       // TRI: n = e1×e2, u = w·n, D = n·n
+  double iD, iD2, iD3;  // 1/D, 1/D², 1/D³ (derivatives multiply instead of divide)
 };
 
 HD void sd_zero(SubDist& S) {
@@ -106,9 +107,11 @@ HD void sd_finish(SubDist& S, const v3* X) {
     v3 c = cross(S.w, S.e1);
     S.N = dot(c, c);
     S.s = S.N / S.D;
+    S.iD = 1.0 / S.D; S.iD2 = S.iD * S.iD; S.iD3 = S.iD2 * S.iD;
   } else {
     S.n = cross(S.e1, S.e2); S.u = dot(S.w, S.n); S.D = dot(S.n, S.n);
     S.s = S.u * S.u / S.D;
+    S.iD = 1.0 / S.D; S.iD2 = S.iD * S.iD; S.iD3 = S.iD2 * S.iD;
   }
 }
 
@@ -226,20 +229,20 @@ HD double tri_D2(const SubDist& S, int v, int a, int u, int b) {
 // variable-space derivatives of s
 HD double sd_var1(const SubDist& S, int v, int a) {
   if (S.sub == SUB_PP) return v == 0 ? 2.0 * comp(S.w, a) : 0.0;
-  if (S.sub == SUB_PL) return pl_N1(S, v, a) / S.D - S.N * pl_D1(S, v, a) / (S.D * S.D);
-  return 2.0 * S.u * tri_u1(S, v, a) / S.D - S.u * S.u * tri_D1(S, v, a) / (S.D * S.D);
+  if (S.sub == SUB_PL) return pl_N1(S, v, a) * S.iD - S.N * pl_D1(S, v, a) * S.iD2;
+  return 2.0 * S.u * tri_u1(S, v, a) * S.iD - S.u * S.u * tri_D1(S, v, a) * S.iD2;
 }
 HD double sd_var2(const SubDist& S, int v, int a, int u, int b) {
   if (S.sub == SUB_PP) return (v == 0 && u == 0 && a == b) ? 2.0 : 0.0;
   if (S.sub == SUB_PL) {
-    double D = S.D, N = S.N;
-    return pl_N2(S, v, a, u, b) / D - (pl_N1(S, v, a) * pl_D1(S, u, b) + pl_D1(S, v, a) * pl_N1(S, u, b)) / (D * D) -
-           N * pl_D2(v, a, u, b) / (D * D) + 2.0 * N * pl_D1(S, v, a) * pl_D1(S, u, b) / (D * D * D);
+    const double N = S.N;
+    return pl_N2(S, v, a, u, b) * S.iD - (pl_N1(S, v, a) * pl_D1(S, u, b) + pl_D1(S, v, a) * pl_N1(S, u, b)) * S.iD2 -
+           N * pl_D2(v, a, u, b) * S.iD2 + 2.0 * N * pl_D1(S, v, a) * pl_D1(S, u, b) * S.iD3;
   }
-  double D = S.D, U = S.u;
+  const double U = S.u;
   double ua = tri_u1(S, v, a), ub = tri_u1(S, u, b), Da = tri_D1(S, v, a), Db = tri_D1(S, u, b);
-  return 2.0 * (ua * ub + U * tri_u2(S, v, a, u, b)) / D - 2.0 * U * (ua * Db + Da * ub) / (D * D) -
-         U * U * tri_D2(S, v, a, u, b) / (D * D) + 2.0 * U * U * Da * Db / (D * D * D);
+  return 2.0 * (ua * ub + U * tri_u2(S, v, a, u, b)) * S.iD - 2.0 * U * (ua * Db + Da * ub) * S.iD2 -
+         U * U * tri_D2(S, v, a, u, b) * S.iD2 + 2.0 * U * U * Da * Db * S.iD3;
 }
 // cross-product magnitude c = D of an sd_make_cross evaluator, and its derivatives
 HD double sc_var1(const SubDist& S, int v, int a) { return tri_D1(S, v, a); }

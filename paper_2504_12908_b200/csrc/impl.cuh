@@ -29,6 +29,7 @@ struct EnvCtl {
   int phase, status, inner_conv, newton, pcg, ls_bt, al_rounds, n_act, ncand, overflow;
   int disabled, pad_;
   int exact, hold, nfail, xfail;   // exact-Hessian-first control (reading R14b)
+  int bp_ref, bp_valid;            // reusable candidate list state (reading R11b)
   long long pcg_total;
   double pcg_bytes;
   double Keff;
@@ -48,6 +49,7 @@ struct Dev {
   int max_newton, max_al, max_pcg, max_accd, mollify, hmode, hold_cap;
   double K;                 // line-search expansion bound (reading R17b)
   double lm_mu0;
+  double bp_margin;         // δ of the reusable candidate list (0 = rebuild every iteration)
   double grav[3];
   // ---- template ----
   const int* tets;        // [T][4]
@@ -123,6 +125,7 @@ struct Dev {
   int* ent;               // [E][ent_cap][2]
   int* big;               // [E][BIG_CAP]
   double* tbox;           // [E][NT+NE][6] raw target boxes (broad-phase cache)
+  double* vref;           // [E][NSV][6] reference boxes of surface vertices at the last build
   int* act_info;          // [E][act_cap][4] (kind, type, a, b)
   int* act_vid;           // [E][act_cap][4]
   double* act_g;          // [E][act_cap][12]

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(NTHREADS) k_positions(Dev D, int env0, int wit
   for (int gv = threadIdx.x; gv < D.NVall; gv += blockDim.x) {
     if (gv < D.V) {
       P[3 * gv] = q[3 * gv]; P[3 * gv + 1] = q[3 * gv + 1]; P[3 * gv + 2] = q[3 * gv + 2];
+      // (validity of a reusable candidate list is checked below, after all positions exist)
       // Pd = K_eff·(displacement of p): the swept sets and ACCD cover α ∈ [0, K_eff]
       if (with_p) { Pd[3 * gv] = Kf * p[3 * gv]; Pd[3 * gv + 1] = Kf * p[3 * gv + 1]; Pd[3 * gv + 2] = Kf * p[3 * gv + 2]; }
     } else {
@@ -97,6 +98,27 @@ __global__ void __launch_bounds__(NTHREADS) k_positions(Dev D, int env0, int wit
         st3(Pd + 3 * gv, Kf * d);
       }
     }
+  }
+  // reading R11b: the candidate list stays valid while every surface vertex's current sweep
+  // [P, P + Pd] lies inside its reference box grown by δ
+  if (D.bp_margin > 0.0) {
+    __syncthreads();
+    const double* rb = D.vref + (size_t)e * D.NSV * 6;
+    const double dm = D.bp_margin;
+    int ok = D.ctl[e].bp_ref;
+    if (ok) {
+      for (int i = threadIdx.x; i < D.NSV; i += blockDim.x) {
+        const int gv = D.sverts[i];
+        v3 a = ld3(P + 3 * gv), b = a;
+        if (with_p) b = a + ld3(Pd + 3 * gv);
+        const double* r = rb + 6 * i;
+        if (!(fmin(a.x, b.x) >= r[0] - dm && fmin(a.y, b.y) >= r[1] - dm && fmin(a.z, b.z) >= r[2] - dm &&
+              fmax(a.x, b.x) <= r[3] + dm && fmax(a.y, b.y) <= r[4] + dm && fmax(a.z, b.z) <= r[5] + dm))
+          ok = 0;
+      }
+    }
+    ok = __syncthreads_and(ok);
+    if (threadIdx.x == 0) D.ctl[e].bp_valid = ok;
   }
 }
 
@@ -121,6 +143,7 @@ struct BoxCtx {
   const double* P; const double* Pd; int swept;
   double* tb;      // raw target boxes [NT+NE][6] (lo, hi), filled in pass 1 of k_broad
   int NT;
+  double infl;     // target inflation: d̂ (exact) or d̂ + 2δ (reusable list, reading R11b)
   __device__ void vbox(int gv, v3& lo, v3& hi) const {
     v3 a = ld3(P + 3 * gv);
     lo = a; hi = a;
@@ -152,7 +175,7 @@ __device__ __forceinline__ void raw_target_box(const Dev& D, const BoxCtx& B, in
 __device__ __forceinline__ void target_box(const Dev& D, const BoxCtx& B, int code, v3& lo, v3& hi) {
   const double* c = B.tb + 6 * (size_t)tbox_index(B, code);
   lo = mk(c[0], c[1], c[2]); hi = mk(c[3], c[4], c[5]);
-  v3 dh = mk(D.dhat, D.dhat, D.dhat);
+  v3 dh = mk(B.infl, B.infl, B.infl);
   lo = lo - dh; hi = hi + dh;
 }
 
@@ -237,13 +260,27 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
   if (!force && (C.phase != PHASE_ACTIVE || (swept && (C.inner_conv || C.xfail)))) return;
+  // reading R11b: reuse the candidate list while every surface vertex stays within δ of the
+  // reference box it had at the last (margin-inflated) build
+  if (!force && D.bp_margin > 0.0 && C.bp_valid) return;
+  const double margin = force ? 0.0 : D.bp_margin;
   __shared__ int cnt[NBUCKET + 1];
   __shared__ int cur[NBUCKET];
   __shared__ double red[32];
   __shared__ int sh[33];
   __shared__ int nbig_s, ovf_s;
   BoxCtx B{D.P + (size_t)e * D.NVall * 3, D.Pd + (size_t)e * D.NVall * 3, swept,
-           D.tbox + (size_t)e * (D.NT + D.NE) * 6, D.NT};
+           D.tbox + (size_t)e * (D.NT + D.NE) * 6, D.NT, D.dhat + 2.0 * margin};
+  // reference boxes of the surface vertices for the reuse test
+  if (margin > 0.0) {
+    double* rb = D.vref + (size_t)e * D.NSV * 6;
+    for (int i = threadIdx.x; i < D.NSV; i += blockDim.x) {
+      v3 lo, hi;
+      B.vbox(D.sverts[i], lo, hi);
+      rb[6 * i] = lo.x; rb[6 * i + 1] = lo.y; rb[6 * i + 2] = lo.z; rb[6 * i + 3] = hi.x; rb[6 * i + 4] = hi.y; rb[6 * i + 5] = hi.z;
+    }
+  }
+  if (threadIdx.x == 0) C.bp_ref = margin > 0.0 ? 1 : 0;
   int* ent = D.ent + (size_t)e * D.ent_cap * 2;
   int* big = D.big + (size_t)e * BIG_CAP;
   // grid origin: min corner over all surface vertices (start and end positions)
@@ -254,9 +291,9 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     mx = fmin(mx, lo.x); my = fmin(my, lo.y); mz = fmin(mz, lo.z);
   }
   Grid G;
-  G.ox = block_min(mx, red) - D.dhat;
-  G.oy = block_min(my, red) - D.dhat;
-  G.oz = block_min(mz, red) - D.dhat;
+  G.ox = block_min(mx, red) - B.infl;
+  G.oy = block_min(my, red) - B.infl;
+  G.oz = block_min(mz, red) - B.infl;
   G.inv_h = 1.0 / D.cell;
   for (int i = threadIdx.x; i <= NBUCKET; i += blockDim.x) cnt[i] = 0;
   if (threadIdx.x == 0) { nbig_s = 0; ovf_s = 0; }
@@ -269,7 +306,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     raw_target_box(D, B, code, lo, hi);
     double* c = B.tb + 6 * (size_t)i;
     c[0] = lo.x; c[1] = lo.y; c[2] = lo.z; c[3] = hi.x; c[4] = hi.y; c[5] = hi.z;
-    v3 dh = mk(D.dhat, D.dhat, D.dhat);
+    v3 dh = mk(B.infl, B.infl, B.infl);
     lo = lo - dh; hi = hi + dh;
     int l[3], h[3];
     G.cell(lo, l); G.cell(hi, h);
@@ -1430,7 +1467,7 @@ __global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
   }
   if (threadIdx.x == 0) {
     C.phase = PHASE_ACTIVE; C.status = ENV_OK; C.inner_conv = 0; C.newton = 0; C.pcg = 0; C.ls_bt = 0;
-    C.al_rounds = 0; C.n_act = 0; C.ncand = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;
+    C.al_rounds = 0; C.n_act = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;  // (ncand: reusable list)
     C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
     C.exact = D.hmode >= 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0; C.Keff = 1.0; C.mu = 0.0;
   }

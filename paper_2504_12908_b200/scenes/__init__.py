@@ -79,6 +79,7 @@ class Config:
     ls_expand: int = 16            # line-search expansion bound K (R17b); 1 = plain backtracking
     hold_cap: int = 16             # max projected iterations between exact-Hessian attempts (R14b)
     lm_mu0: float = 1.0            # first mass-scaled shift of hessian_mode 2 (R14c)
+    bp_margin: float = 1.0e-4      # δ of the reusable candidate list (R11b); 0 = rebuild every iteration
     cand_capacity_per_env: int = 65536
     active_capacity_per_env: int = 4096
 

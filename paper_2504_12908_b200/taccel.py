@@ -56,7 +56,8 @@ class Config(ctypes.Structure):
                 ("max_newton", ctypes.c_int32), ("max_al_rounds", ctypes.c_int32), ("max_pcg", ctypes.c_int32),
                 ("max_accd_iters", ctypes.c_int32), ("ee_mollifier", ctypes.c_int32),
                 ("hessian_mode", ctypes.c_int32), ("ls_expand", ctypes.c_int32),
-                ("hold_cap", ctypes.c_int32), ("lm_mu0", ctypes.c_double), ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32)]
+                ("hold_cap", ctypes.c_int32), ("lm_mu0", ctypes.c_double), ("bp_margin", ctypes.c_double),
+                ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32)]
 
 
 class EnvStats(ctypes.Structure):
