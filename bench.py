@@ -277,8 +277,15 @@ def main():
         pcg_ms = phases["pcg"]["ms"]
         local_bytes = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
         ach = local_bytes / (pcg_ms / 1e3) / 1e9
+        traffic, tsrc = None, None
+        tfile = os.path.join(ROOT, "profiles", "r1_pcg_traffic.json")
+        if os.path.exists(tfile):
+            tj = json.load(open(tfile))
+            traffic = tj["dram_bytes_per_launch"]
+            tsrc = (f"{os.path.relpath(tfile, ROOT)}: ncu dram__bytes_read+write per k_pcg launch over one C2 step; "
+                    f"traffic/algorithmic = {tj['traffic_over_alg']:.2f} for that step")
         roof = {"kernel": "k_pcg (block-Jacobi PCG, one CTA per env)", "bound": "hbm", "achieved": ach,
-                "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic, "traffic_source": tsrc,
                 "peak_source": peak_src, "share_of_step": pcg_ms / ms,
                 "alg_bytes_per_launch": local_bytes / max(phases["pcg"]["launches"], 1),
                 "dominant_kernel": dom}
