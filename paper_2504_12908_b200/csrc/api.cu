@@ -46,7 +46,7 @@ struct HostT {
   std::vector<double> My, bmass, bs1, bvol, bkappa;
   std::vector<int> vert_body, vert_aff;
   std::vector<double> vert_xbar;
-  std::vector<int> sverts, tris, tri_body, edges, edge_body;
+  std::vector<int> sverts, tris, tri_body, edges, edge_body, body_sv_ptr;
   std::vector<double> A_v, A_e, elen2;
   std::vector<unsigned char> allowed;
   std::vector<int> att_vert, att_body, att_of_vert, kin_body, kin_of_body, affv_list, kin_vlist;
@@ -173,6 +173,7 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
   H.V = off;
   H.T = (int)H.vol.size();
   if (H.V > 8000) return fail(TAC_E_CAPACITY, "more than 8000 soft vertices per env");
+  if (ns + na > 32) return fail(TAC_E_CAPACITY, "more than 32 bodies per env");
   // ---- affine ----
   int nd = 0;
   for (int b = 0; b < na; ++b) {
@@ -244,6 +245,9 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
     for (int v : H.tris) is_s[v] = 1;
     for (int v = 0; v < H.NVall; ++v) if (is_s[v]) H.sverts.push_back(v);
     H.NSV = (int)H.sverts.size();
+    H.body_sv_ptr.assign(H.NB + 1, 0);
+    for (int v : H.sverts) H.body_sv_ptr[H.vert_body[v] + 1]++;
+    for (int b = 0; b < H.NB; ++b) H.body_sv_ptr[b + 1] += H.body_sv_ptr[b];
   }
   // rest areas A_v, A_e (1/3 of incident rest triangle areas) and rest edge lengths
   H.A_v.assign(H.NVall, 0.0);
@@ -462,7 +466,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My);
   D.bmass = td(H.bmass); D.bs1 = td(H.bs1); D.bvol = td(H.bvol); D.bkappa = td(H.bkappa);
   D.vert_body = ti(H.vert_body); D.vert_aff = ti(H.vert_aff); D.vert_xbar = td(H.vert_xbar);
-  D.sverts = ti(H.sverts); D.tris = ti(H.tris); D.tri_body = ti(H.tri_body); D.edges = ti(H.edges);
+  D.sverts = ti(H.sverts); D.body_sv_ptr = ti(H.body_sv_ptr); D.tris = ti(H.tris); D.tri_body = ti(H.tri_body); D.edges = ti(H.edges);
   D.edge_body = ti(H.edge_body); D.A_v = td(H.A_v); D.A_e = td(H.A_e); D.elen2 = td(H.elen2);
   D.allowed = C.take<unsigned char>(std::max<size_t>(H.allowed.size(), 1));
   D.att_vert = ti(H.att_vert); D.att_body = ti(H.att_body); D.att_local = td(H.att_local);
@@ -576,7 +580,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
 #define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
   UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
   UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
-  UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
+  UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(body_sv_ptr); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
   UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
   UP(mark_bary); UP(mark_pad); UP(pad_mount); UP(pad_T); UP(Xrest);

@@ -81,6 +81,7 @@ struct Dev {
   const int* vert_aff;    // [NVall] affine body or -1
   const double* vert_xbar;// [NVall][3]
   const int* sverts;      // [NSV]
+  const int* body_sv_ptr; // [NB+1] range of each body's surface vertices in sverts
   const int* tris;        // [NT][3]
   const int* tri_body;    // [NT]
   const int* edges;       // [NE][2]

@@ -179,9 +179,32 @@ __device__ __forceinline__ void target_box(const Dev& D, const BoxCtx& B, int co
   lo = lo - dh; hi = hi + dh;
 }
 
+constexpr int MAXB = 32;   // bodies per env (pads + affine)
+// body-level culling (exact: the box predicate is monotone).  A target (inflated box) can only
+// meet queries of bodies whose raw box it overlaps; a query (raw box) only targets inside some
+// allowed body's box grown by the inflation.
+__device__ __forceinline__ bool target_reaches(const Dev& D, double (*bb)[6], int tbody, v3 tlo_i, v3 thi_i) {
+  for (int b = 0; b < D.NB; ++b) {
+    if (!D.allowed[(size_t)b * D.NB + tbody]) continue;
+    if (bb[b][0] <= thi_i.x && bb[b][1] <= thi_i.y && bb[b][2] <= thi_i.z && tlo_i.x <= bb[b][3] &&
+        tlo_i.y <= bb[b][4] && tlo_i.z <= bb[b][5])
+      return true;
+  }
+  return false;
+}
+__device__ __forceinline__ bool query_reaches(const Dev& D, double (*bb)[6], int qbody, v3 qlo, v3 qhi, double infl) {
+  for (int b = 0; b < D.NB; ++b) {
+    if (!D.allowed[(size_t)qbody * D.NB + b]) continue;
+    if (qlo.x <= bb[b][3] + infl && qlo.y <= bb[b][4] + infl && qlo.z <= bb[b][5] + infl &&
+        bb[b][0] - infl <= qhi.x && bb[b][1] - infl <= qhi.y && bb[b][2] - infl <= qhi.z)
+      return true;
+  }
+  return false;
+}
+
 template <bool EMIT>
 __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int* cnt_off, const int* ent, const int* big,
-                        int nbig, int qi, int* out_a, int* out_b) {
+                        int nbig, int qi, int* out_a, int* out_b, double (*bb)[6]) {
   const bool pt = qi < D.NSV;
   int qa, qbody, qv[2];
   v3 qlo, qhi;
@@ -196,6 +219,7 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
     qlo = mk(c[0], c[1], c[2]); qhi = mk(c[3], c[4], c[5]);
   }
   const int want = pt ? 0 : 1;
+  if (!query_reaches(D, bb, qbody, qlo, qhi, B.infl)) return 0;
   const unsigned char* allow = D.allowed + (size_t)qbody * D.NB;
   int lo[3], hi[3];
   G.cell(qlo, lo); G.cell(qhi, hi);
@@ -283,17 +307,31 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   if (threadIdx.x == 0) C.bp_ref = margin > 0.0 ? 1 : 0;
   int* ent = D.ent + (size_t)e * D.ent_cap * 2;
   int* big = D.big + (size_t)e * BIG_CAP;
-  // grid origin: min corner over all surface vertices (start and end positions)
-  double mx = 1e300, my = 1e300, mz = 1e300;
-  for (int i = threadIdx.x; i < D.NSV; i += blockDim.x) {
-    v3 lo, hi;
-    B.vbox(D.sverts[i], lo, hi);
-    mx = fmin(mx, lo.x); my = fmin(my, lo.y); mz = fmin(mz, lo.z);
+  // body boxes (surface vertices of each body are a contiguous range of sverts): warp per body
+  __shared__ double bb[MAXB][6];
+  {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int b = w; b < D.NB; b += nw) {
+      double l0 = 1e300, l1 = 1e300, l2 = 1e300, h0 = -1e300, h1 = -1e300, h2 = -1e300;
+      for (int i = D.body_sv_ptr[b] + lane; i < D.body_sv_ptr[b + 1]; i += 32) {
+        v3 lo, hi;
+        B.vbox(D.sverts[i], lo, hi);
+        l0 = fmin(l0, lo.x); l1 = fmin(l1, lo.y); l2 = fmin(l2, lo.z);
+        h0 = fmax(h0, hi.x); h1 = fmax(h1, hi.y); h2 = fmax(h2, hi.z);
+      }
+      l0 = warp_min(l0); l1 = warp_min(l1); l2 = warp_min(l2);
+      h0 = warp_max(h0); h1 = warp_max(h1); h2 = warp_max(h2);
+      if (lane == 0) { bb[b][0] = l0; bb[b][1] = l1; bb[b][2] = l2; bb[b][3] = h0; bb[b][4] = h1; bb[b][5] = h2; }
+    }
   }
+  __syncthreads();
+  // grid origin: min corner over all bodies
+  double mx = 1e300, my = 1e300, mz = 1e300;
+  for (int b = 0; b < D.NB; ++b) { mx = fmin(mx, bb[b][0]); my = fmin(my, bb[b][1]); mz = fmin(mz, bb[b][2]); }
   Grid G;
-  G.ox = block_min(mx, red) - B.infl;
-  G.oy = block_min(my, red) - B.infl;
-  G.oz = block_min(mz, red) - B.infl;
+  G.ox = mx - B.infl;
+  G.oy = my - B.infl;
+  G.oz = mz - B.infl;
   G.inv_h = 1.0 / D.cell;
   for (int i = threadIdx.x; i <= NBUCKET; i += blockDim.x) cnt[i] = 0;
   if (threadIdx.x == 0) { nbig_s = 0; ovf_s = 0; }
@@ -308,6 +346,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     c[0] = lo.x; c[1] = lo.y; c[2] = lo.z; c[3] = hi.x; c[4] = hi.y; c[5] = hi.z;
     v3 dh = mk(B.infl, B.infl, B.infl);
     lo = lo - dh; hi = hi + dh;
+    if (!target_reaches(D, bb, i < D.NT ? D.tri_body[i] : D.edge_body[i - D.NT], lo, hi)) continue;
     int l[3], h[3];
     G.cell(lo, l); G.cell(hi, h);
     long nc = (long)(h[0] - l[0] + 1) * (h[1] - l[1] + 1) * (h[2] - l[2] + 1);
@@ -350,6 +389,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     int code = i < D.NT ? 2 * i : 2 * (i - D.NT) + 1;
     v3 lo, hi;
     target_box(D, B, code, lo, hi);
+    if (!target_reaches(D, bb, i < D.NT ? D.tri_body[i] : D.edge_body[i - D.NT], lo, hi)) continue;
     int l[3], h[3];
     G.cell(lo, l); G.cell(hi, h);
     long nc = (long)(h[0] - l[0] + 1) * (h[1] - l[1] + 1) * (h[2] - l[2] + 1);
@@ -371,12 +411,12 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   int total = 0;
   for (int t0 = 0; t0 < nq; t0 += blockDim.x) {
     int qi = t0 + threadIdx.x;
-    int c = (qi < nq) ? bp_query<false>(D, B, G, cnt, ent, big, nbig, qi, nullptr, nullptr) : 0;
+    int c = (qi < nq) ? bp_query<false>(D, B, G, cnt, ent, big, nbig, qi, nullptr, nullptr, bb) : 0;
     int tot;
     int ex = block_excl_scan(c, sh, &tot);
     int base = total + ex;
     if (c > 0 && base + c <= D.cand_cap) {
-      bp_query<true>(D, B, G, cnt, ent, big, nbig, qi, ca + base, cb + base);
+      bp_query<true>(D, B, G, cnt, ent, big, nbig, qi, ca + base, cb + base, bb);
       // insertion sort of this query's segment by target index
       for (int i = 1; i < c; ++i) {
         int kb = cb[base + i], ka = ca[base + i];
