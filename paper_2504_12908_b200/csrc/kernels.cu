@@ -591,7 +591,37 @@ struct PairScratch {
   double gv[9], gcv[9];       // variable-space ∇s and ∇c
   double hv[81], hcv[81];     // variable-space ∇²s and ∇²c, index (3v+a)*9 + 3u+b
   double gs[12], gc[12];      // slot-space ∇s and ∇c
+  // table-driven variable-space derivatives (array-indexed, no select chains)
+  double W[3], E1[3], E2[3], Nn[3];   // sub-distance variables (PL: E1 = e)
+  double U1[9], D1[9];                // TRI: ∂u/∂var, ∂D/∂var;  PL: ∂N/∂var, ∂D/∂var;  PP: ∂s/∂w
+  double CE1[3], CE2[3], CN[3], CD1[9];  // mollifier c = ‖e1×e2‖²
 };
+
+__device__ __forceinline__ double skewv(const double* x, int a, int b) {   // ([x]×)_{ab}
+  if (a == b) return 0.0;
+  const double v = x[3 - a - b];
+  return ((b - a + 3) % 3 == 2) ? v : -v;
+}
+__device__ __forceinline__ double dot3a(const double* x, const double* y) { return x[0] * y[0] + x[1] * y[1] + x[2] * y[2]; }
+// ∂²D/∂var_v[a]∂var_u[b] for D = ‖e1×e2‖² (v, u ∈ {1, 2}; [x]×ᵀ[y]× = (x·y)I − y xᵀ)
+__device__ __forceinline__ double tri_D2_fast(const double* e1, const double* e2, const double* n, int v, int a, int u, int b) {
+  if (v == 0 || u == 0) return 0.0;
+  const double dab = a == b ? 1.0 : 0.0;
+  double r;
+  if (v == 1 && u == 1) r = dot3a(e2, e2) * dab - e2[a] * e2[b];
+  else if (v == 2 && u == 2) r = dot3a(e1, e1) * dab - e1[a] * e1[b];
+  else if (v == 1) r = -(dot3a(e2, e1) * dab - e1[a] * e2[b]) - skewv(n, a, b);
+  else r = -(dot3a(e1, e2) * dab - e2[a] * e1[b]) - skewv(n, b, a);
+  return 2.0 * r;
+}
+// ∂²u/∂var_v[a]∂var_u[b] for u = w·(e1×e2)
+__device__ __forceinline__ double tri_u2_fast(const double* w, const double* e1, const double* e2, int v, int a, int u, int b) {
+  if (v == u) return 0.0;
+  if (v > u) { int t = v; v = u; u = t; t = a; a = b; b = t; }
+  if (v == 0 && u == 1) return -skewv(e2, a, b);
+  if (v == 0 && u == 2) return skewv(e1, a, b);
+  return -skewv(w, a, b);
+}
 
 // grid (ceil(act_cap / PAIRS_PER_CTA), envs): many CTAs per env so a single contact-heavy env is
 // spread over the whole GPU; CTAs past the env's active count exit at once.
@@ -632,16 +662,72 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
     }
     const bool molterm = useM && m1 != 0.0;
     const double scale = D.dt * D.dt * D.kappa * pair_area(D, kind, a, b);
-    // 1) variable-space derivatives, one entry per lane
-    for (int i = lane; i < 81; i += 32) {
-      int va = i / 9, ub = i % 9, v = va / 3, u = ub / 3;
-      S.hv[i] = (v < nvar && u < nvar) ? sd_var2(SD, v, va % 3, u, ub % 3) : 0.0;
-      S.hcv[i] = (molterm && v > 0 && u > 0) ? sc_var2(CC, v, va % 3, u, ub % 3) : 0.0;
+    // 1) variable-space derivatives (table-driven): vectors to shared memory, then first-derivative
+    //    tables (9 lanes), then the 81 second-derivative entries (all lanes)
+    if (lane == 0) {
+      S.W[0] = SD.w.x; S.W[1] = SD.w.y; S.W[2] = SD.w.z;
+      S.E1[0] = SD.e1.x; S.E1[1] = SD.e1.y; S.E1[2] = SD.e1.z;
+      S.E2[0] = SD.e2.x; S.E2[1] = SD.e2.y; S.E2[2] = SD.e2.z;
+      S.Nn[0] = SD.n.x; S.Nn[1] = SD.n.y; S.Nn[2] = SD.n.z;
+      S.CE1[0] = CC.e1.x; S.CE1[1] = CC.e1.y; S.CE1[2] = CC.e1.z;
+      S.CE2[0] = CC.e2.x; S.CE2[1] = CC.e2.y; S.CE2[2] = CC.e2.z;
+      S.CN[0] = CC.n.x; S.CN[1] = CC.n.y; S.CN[2] = CC.n.z;
     }
+    __syncwarp();
     if (lane < 9) {
-      int v = lane / 3;
-      S.gv[lane] = v < nvar ? sd_var1(SD, v, lane % 3) : 0.0;
-      S.gcv[lane] = (useM && v > 0) ? sc_var1(CC, v, lane % 3) : 0.0;
+      const int v = lane / 3, a = lane % 3, a1 = (a + 1) % 3, a2 = (a + 2) % 3;
+      double u1 = 0.0, d1 = 0.0, cd1 = 0.0;
+      if (SD.sub == SUB_TRI) {
+        if (v == 0) u1 = S.Nn[a];
+        else if (v == 1) u1 = S.E2[a1] * S.W[a2] - S.E2[a2] * S.W[a1];                 // (e2×w)_a
+        else u1 = S.W[a1] * S.E1[a2] - S.W[a2] * S.E1[a1];                             // (w×e1)_a
+        if (v == 1) d1 = 2.0 * (S.E2[a1] * S.Nn[a2] - S.E2[a2] * S.Nn[a1]);            // 2(e2×n)_a
+        else if (v == 2) d1 = 2.0 * (S.Nn[a1] * S.E1[a2] - S.Nn[a2] * S.E1[a1]);       // 2(n×e1)_a
+      } else if (SD.sub == SUB_PL) {
+        if (v == 0) u1 = 2.0 * (SD.D * S.W[a] - SD.we * S.E1[a]);
+        else if (v == 1) u1 = 2.0 * (SD.ww * S.E1[a] - SD.we * S.W[a]);
+        if (v == 1) d1 = 2.0 * S.E1[a];
+      } else if (v == 0) {
+        u1 = 2.0 * S.W[a];
+      }
+      if (useM) {
+        if (v == 1) cd1 = 2.0 * (S.CE2[a1] * S.CN[a2] - S.CE2[a2] * S.CN[a1]);
+        else if (v == 2) cd1 = 2.0 * (S.CN[a1] * S.CE1[a2] - S.CN[a2] * S.CE1[a1]);
+      }
+      S.U1[lane] = u1; S.D1[lane] = d1; S.CD1[lane] = cd1;
+      double g1;
+      if (SD.sub == SUB_TRI) g1 = 2.0 * SD.u * u1 * SD.iD - SD.u * SD.u * d1 * SD.iD2;
+      else if (SD.sub == SUB_PL) g1 = u1 * SD.iD - SD.N * d1 * SD.iD2;
+      else g1 = u1;
+      S.gv[lane] = g1;
+      S.gcv[lane] = cd1;
+    }
+    __syncwarp();
+    for (int i = lane; i < 81; i += 32) {
+      const int va = i / 9, ub = i % 9, v = va / 3, u = ub / 3, a_ = va % 3, b_ = ub % 3;
+      double h = 0.0;
+      if (v < nvar && u < nvar) {
+        const double ua = S.U1[va], ubb = S.U1[ub], Da = S.D1[va], Db = S.D1[ub];
+        const double dab = a_ == b_ ? 1.0 : 0.0;
+        if (SD.sub == SUB_TRI) {
+          const double U = SD.u;
+          h = 2.0 * (ua * ubb + U * tri_u2_fast(S.W, S.E1, S.E2, v, a_, u, b_)) * SD.iD -
+              2.0 * U * (ua * Db + Da * ubb) * SD.iD2 - U * U * tri_D2_fast(S.E1, S.E2, S.Nn, v, a_, u, b_) * SD.iD2 +
+              2.0 * U * U * Da * Db * SD.iD3;
+        } else if (SD.sub == SUB_PL) {
+          double N2;
+          if (v == 0 && u == 0) N2 = 2.0 * (SD.D * dab - S.E1[a_] * S.E1[b_]);
+          else if (v == 1 && u == 1) N2 = 2.0 * (SD.ww * dab - S.W[a_] * S.W[b_]);
+          else if (v == 0) N2 = 2.0 * (2.0 * S.W[a_] * S.E1[b_] - S.E1[a_] * S.W[b_] - SD.we * dab);
+          else N2 = 2.0 * (2.0 * S.W[b_] * S.E1[a_] - S.E1[b_] * S.W[a_] - SD.we * dab);
+          const double D2 = (v == 1 && u == 1) ? 2.0 * dab : 0.0;
+          h = N2 * SD.iD - (ua * Db + Da * ubb) * SD.iD2 - SD.N * D2 * SD.iD2 + 2.0 * SD.N * Da * Db * SD.iD3;
+        } else {
+          h = (v == 0 && u == 0) ? 2.0 * dab : 0.0;
+        }
+      }
+      S.hv[i] = h;
+      S.hcv[i] = (molterm && v > 0 && u > 0) ? tri_D2_fast(S.CE1, S.CE2, S.CN, v, a_, u, b_) : 0.0;
     }
     __syncwarp();
     // 2) slot-space gradients (coefficients are ±1/0 combinations of the variables)
