@@ -171,6 +171,16 @@ tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, const double* 
 /* Advance every enabled env by n_steps time steps.  Host-blocking.  env_status [E] (may be NULL). */
 tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_status, void* stream);
 
+/* Scheduled multi-step mode: advance every enabled env through n_steps time steps, env k of step s
+ * using kinematic targets y_kin_sched [n_steps][E][NK][12].  Envs advance independently: an env that
+ * converged its step starts the next one at once (no lockstep wait for the slowest env); each env's
+ * trajectory is bitwise identical to calling tac_set_targets + tac_step per step.  After each step of
+ * each env its gel deformation is written to coated_disp [n_steps][E][Σcoated][3], marker_pos and
+ * marker_flow [n_steps][E][Σmarkers][3] (all three NULL = no readout).  Buffers may be host or device
+ * memory (host buffers are staged through stream-ordered device allocations).  Host-blocking. */
+tac_status tac_step_schedule(tac_batch* b, int32_t n_steps, const double* y_kin_sched, double* coated_disp,
+                             double* marker_pos, double* marker_flow, uint8_t* env_status, void* stream);
+
 tac_status tac_get_state(tac_batch* b, int32_t env0, int32_t n, double* x, double* xdot, double* y,
                          double* ydot, void* stream);
 

@@ -677,14 +677,21 @@ static double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st) {
+struct Sched {
+  const double* sched;
+  int nsteps;
+  double *oc, *om, *of;
+};
+
+static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st, const Sched* sc = nullptr) {
   Dev& D = b->D;
   b->it_active.clear();
   b->it_ms.clear();
   double t0 = now_ms();
   { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 0, 0, st); }
   { PROF(PH_BROAD_STATIC); launch_broad(D, env0, ne, 0, 0, st); }
-  for (int it = 0; it <= D.max_newton + 1; ++it) {
+  const long max_it = (long)(D.max_newton + 2) * (sc ? sc->nsteps : 1);
+  for (long it = 0; it < max_it; ++it) {
     { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 0, 0, st); }
     { PROF(PH_NARROW); launch_narrow(D, env0, ne, 0, st); }
     { PROF(PH_TETS); launch_tets(D, env0, ne, 0, st); }
@@ -697,6 +704,7 @@ static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st) {
     { PROF(PH_LINESEARCH); launch_linesearch(D, env0, ne, st); }
     CUDA_TRY(cudaMemsetAsync(D.any_active, 0, sizeof(int), st));
     { PROF(PH_CONTROL); launch_control(D, env0, ne, st); }
+    if (sc) { PROF(PH_END); launch_advance(D, env0, ne, sc->sched, sc->nsteps, sc->oc, sc->om, sc->of, st); }
     CUDA_TRY(cudaMemcpyAsync(b->h_flag, D.any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
@@ -725,6 +733,69 @@ extern "C" tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_statu
   tac_status r = pull_ctl(b, st);
   if (b->prof) prof_flush(b);
   if (r) return r;
+  for (auto& c : b->hctl)
+    if (c.phase == PHASE_FAILED) any_failed = true;
+  r = write_status(b, 0, D.E, env_status, st);
+  if (r) return r;
+  return any_failed ? fail(TAC_E_ENV_FAILED, "one or more envs failed (see env_status)") : TAC_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+extern "C" tac_status tac_step_schedule(tac_batch* b, int32_t n_steps, const double* y_kin_sched, double* coated_disp,
+                                        double* marker_pos, double* marker_flow, uint8_t* env_status, void* stream) {
+  if (!b || n_steps <= 0) return fail(TAC_E_INVALID, "bad arguments");
+  if (b->D.NK > 0 && !y_kin_sched) return fail(TAC_E_INVALID, "y_kin_sched is required when the scene has kinematic bodies");
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& D = b->D;
+  const size_t sbytes = (size_t)n_steps * D.E * D.NK * 12 * sizeof(double);
+  const size_t cbytes = (size_t)n_steps * D.E * D.NCOAT * 3 * sizeof(double);
+  const size_t mbytes = (size_t)n_steps * D.E * D.NMARK * 3 * sizeof(double);
+  // stage host buffers through stream-ordered device allocations
+  double* dsched = D.ykin;
+  void* tmp_s = nullptr;
+  if (D.NK > 0) {
+    if (is_device_ptr(y_kin_sched)) dsched = const_cast<double*>(y_kin_sched);
+    else {
+      CUDA_TRY(cudaMallocAsync(&tmp_s, sbytes, st));
+      CUDA_TRY(cudaMemcpyAsync(tmp_s, y_kin_sched, sbytes, cudaMemcpyDefault, st));
+      dsched = (double*)tmp_s;
+    }
+  }
+  const bool want_out = coated_disp && marker_pos && marker_flow;
+  double *oc = nullptr, *om = nullptr, *of = nullptr;
+  void* tmp_o = nullptr;
+  const bool out_dev = want_out && is_device_ptr(coated_disp);
+  if (want_out) {
+    if (out_dev) { oc = coated_disp; om = marker_pos; of = marker_flow; }
+    else {
+      CUDA_TRY(cudaMallocAsync(&tmp_o, cbytes + 2 * mbytes + 64, st));
+      oc = (double*)tmp_o;
+      om = (double*)((char*)tmp_o + cbytes);
+      of = (double*)((char*)tmp_o + cbytes + mbytes);
+    }
+  }
+  { PROF(PH_BEGIN); launch_begin_sched(D, 0, D.E, dsched, st); }
+  Sched sc{dsched, n_steps, oc, om, of};
+  tac_status r = newton_loop(b, 0, D.E, st, &sc);
+  if (r) return r;
+  CUDA_TRY(cudaGetLastError());
+  if (want_out && !out_dev) {
+    CUDA_TRY(cudaMemcpyAsync(coated_disp, oc, cbytes, cudaMemcpyDefault, st));
+    CUDA_TRY(cudaMemcpyAsync(marker_pos, om, mbytes, cudaMemcpyDefault, st));
+    CUDA_TRY(cudaMemcpyAsync(marker_flow, of, mbytes, cudaMemcpyDefault, st));
+  }
+  if (tmp_s) CUDA_TRY(cudaFreeAsync(tmp_s, st));
+  if (tmp_o) CUDA_TRY(cudaFreeAsync(tmp_o, st));
+  r = pull_ctl(b, st);
+  if (r) return r;
+  if (b->prof) prof_flush(b);
+  bool any_failed = false;
   for (auto& c : b->hctl)
     if (c.phase == PHASE_FAILED) any_failed = true;
   r = write_status(b, 0, D.E, env_status, st);

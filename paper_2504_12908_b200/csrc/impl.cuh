@@ -30,6 +30,7 @@ struct EnvCtl {
   int disabled, pad_;
   int exact, hold, nfail, xfail;   // exact-Hessian-first control (reading R14b)
   int bp_ref, bp_valid;            // reusable candidate list state (reading R11b)
+  int step, pad2_;                 // step index in a scheduled multi-step call
   long long pcg_total;
   double pcg_bytes;
   double Keff;

@@ -1571,16 +1571,15 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
 // ------------------------------------------------------------------------------------------
 // step begin / end
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+// step setup of one env (block-level): x̃ = xⁿ + Δt ẋⁿ, targets s^y = yk (this step's kinematic
+// targets [NK][12]) and s^x of ∂⁻G from the mount links, AL reset, per-step counters
+__device__ void begin_env(const Dev& D, int e, const double* yk) {
   EnvCtl& C = D.ctl[e];
-  if (C.disabled) { if (threadIdx.x == 0) C.phase = PHASE_IDLE; return; }
   double* q = D.q + (size_t)e * D.n;
   double* qn = D.qn + (size_t)e * D.n;
   double* qt = D.qt + (size_t)e * D.n;
   const double* vel = D.vel + (size_t)e * D.n;
   for (int i = threadIdx.x; i < D.n; i += blockDim.x) { qn[i] = q[i]; qt[i] = q[i] + D.dt * vel[i]; }
-  const double* yk = D.ykin + (size_t)e * D.NK * 12;
   for (int i = threadIdx.x; i < D.NK * 12; i += blockDim.x) {
     D.s_kin[(size_t)e * D.NK * 12 + i] = yk[i];
     D.lam_kin[(size_t)e * D.NK * 12 + i] = 0.0;
@@ -1591,18 +1590,26 @@ __global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
     st3(D.s_att + ((size_t)e * D.NC + c) * 3, embed(y, ld3(D.att_local + 3 * c)));
     st3(D.lam_att + ((size_t)e * D.NC + c) * 3, mk(0, 0, 0));
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     C.phase = PHASE_ACTIVE; C.status = ENV_OK; C.inner_conv = 0; C.newton = 0; C.pcg = 0; C.ls_bt = 0;
     C.al_rounds = 0; C.n_act = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;  // (ncand: reusable list)
     C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
     C.exact = D.hmode >= 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0; C.Keff = 1.0; C.mu = 0.0;
   }
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(NTHREADS) k_end(Dev D, int env0) {
+__global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
-  if (C.phase == PHASE_IDLE) return;
+  if (C.disabled) { if (threadIdx.x == 0) C.phase = PHASE_IDLE; return; }
+  begin_env(D, e, D.ykin + (size_t)e * D.NK * 12);
+}
+
+// end of a step (block-level): ẋ = (xⁿ⁺¹ − xⁿ)/Δt, or rollback to xⁿ and disable on failure
+__device__ void end_env(const Dev& D, int e) {
+  EnvCtl& C = D.ctl[e];
   double* q = D.q + (size_t)e * D.n;
   const double* qn = D.qn + (size_t)e * D.n;
   double* vel = D.vel + (size_t)e * D.n;
@@ -1620,6 +1627,13 @@ __global__ void __launch_bounds__(NTHREADS) k_end(Dev D, int env0) {
       C.disabled = 1;
     }
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_end(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  if (D.ctl[e].phase == PHASE_IDLE) return;
+  end_env(D, e);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1692,8 +1706,8 @@ __global__ void __launch_bounds__(NTHREADS) k_validate(Dev D, int env0) {
   }
 }
 
-__global__ void k_readout(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+// gel-surface readout of one env into caller buffers (block-level); R18 / P:L153
+__device__ void readout_env(const Dev& D, int e, double* oc, double* om, double* of) {
   const double* q = D.q + (size_t)e * D.n;
   auto delta = [&](int v, int pad) -> v3 {
     int b = D.pad_mount[pad];
@@ -1707,8 +1721,7 @@ __global__ void k_readout(Dev D, int env0) {
     } else loc = x;
     return mul33T(T + 3, loc - ld3(T)) - ld3(D.Xrest + 3 * v);
   };
-  for (int i = threadIdx.x; i < D.NCOAT; i += blockDim.x)
-    st3(D.out_coat + ((size_t)e * D.NCOAT + i) * 3, delta(D.coat_vert[i], D.coat_pad[i]));
+  for (int i = threadIdx.x; i < D.NCOAT; i += blockDim.x) st3(oc + 3 * i, delta(D.coat_vert[i], D.coat_pad[i]));
   for (int i = threadIdx.x; i < D.NMARK; i += blockDim.x) {
     v3 pos = mk(0, 0, 0), fl = mk(0, 0, 0);
     for (int j = 0; j < 3; ++j) {
@@ -1717,8 +1730,49 @@ __global__ void k_readout(Dev D, int env0) {
       pos += a * ld3(q + 3 * v);
       fl += a * delta(v, D.mark_pad[i]);
     }
-    st3(D.out_mpos + ((size_t)e * D.NMARK + i) * 3, pos);
-    st3(D.out_mflow + ((size_t)e * D.NMARK + i) * 3, fl);
+    st3(om + 3 * i, pos);
+    st3(of + 3 * i, fl);
+  }
+}
+
+__global__ void k_readout(Dev D, int env0) {
+  const int e = env0 + blockIdx.x;
+  readout_env(D, e, D.out_coat + (size_t)e * D.NCOAT * 3, D.out_mpos + (size_t)e * D.NMARK * 3,
+              D.out_mflow + (size_t)e * D.NMARK * 3);
+}
+
+// ------------------------------------------------------------------------------------------
+// scheduled multi-step mode: each env advances through its own step sequence; an env that finished
+// step k (DONE/FAILED) is finalised, read out into the per-step buffers and immediately starts step
+// k+1 with its scheduled targets, so converged envs do not wait for the slowest env
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHREADS) k_begin_sched(Dev D, int env0, const double* sched) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  if (threadIdx.x == 0) C.step = 0;
+  if (C.disabled) { if (threadIdx.x == 0) C.phase = PHASE_IDLE; return; }
+  begin_env(D, e, sched + (size_t)e * D.NK * 12);
+}
+
+__global__ void __launch_bounds__(NTHREADS) k_advance(Dev D, int env0, const double* sched, int nsteps, double* oc,
+                                                      double* om, double* of) {
+  const int e = env0 + blockIdx.x;
+  EnvCtl& C = D.ctl[e];
+  const int ph = C.phase;
+  if (ph != PHASE_DONE && ph != PHASE_FAILED) return;
+  end_env(D, e);
+  const int k = C.step;
+  if (oc) {
+    readout_env(D, e, oc + ((size_t)k * D.E + e) * D.NCOAT * 3, om + ((size_t)k * D.E + e) * D.NMARK * 3,
+                of + ((size_t)k * D.E + e) * D.NMARK * 3);
+  }
+  __syncthreads();
+  if (ph == PHASE_DONE && k + 1 < nsteps) {
+    begin_env(D, e, sched + ((size_t)(k + 1) * D.E + e) * D.NK * 12);
+    if (threadIdx.x == 0) { C.step = k + 1; atomicAdd(D.any_active, 1); }
+  } else if (threadIdx.x == 0) {
+    C.step = k + 1;
+    if (ph == PHASE_DONE) C.phase = PHASE_IDLE;   // schedule finished (failures stay FAILED/disabled)
   }
 }
 
@@ -1795,5 +1849,12 @@ void launch_gather_y(const Dev& D, int env0, int ne, int which, cudaStream_t s) 
 }
 void launch_validate(const Dev& D, int env0, int ne, cudaStream_t s) { k_validate<<<ne, NTHREADS, 0, s>>>(D, env0); }
 void launch_readout(const Dev& D, int env0, int ne, cudaStream_t s) { k_readout<<<ne, 128, 0, s>>>(D, env0); }
+void launch_begin_sched(const Dev& D, int env0, int ne, const double* sched, cudaStream_t s) {
+  k_begin_sched<<<ne, NTHREADS, 0, s>>>(D, env0, sched);
+}
+void launch_advance(const Dev& D, int env0, int ne, const double* sched, int nsteps, double* oc, double* om,
+                    double* of, cudaStream_t s) {
+  k_advance<<<ne, NTHREADS, 0, s>>>(D, env0, sched, nsteps, oc, om, of);
+}
 
 }  // namespace tac

@@ -94,6 +94,7 @@ def load():
             "tac_set_state": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp, vp],
             "tac_set_targets": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp],
             "tac_step": [vp, ctypes.c_int32, vp, vp],
+            "tac_step_schedule": [vp, ctypes.c_int32, vp, vp, vp, vp, vp, vp],
             "tac_get_state": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp],
             "tac_get_gel_deformation": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp],
             "tac_get_stats": [vp, ctypes.POINTER(EnvStats), vp],
@@ -259,6 +260,19 @@ class Batch:
     def step(self, n_steps: int = 1, raise_on_failure: bool = False):
         st = np.zeros(self.n_envs, np.uint8)
         code = self.lib.tac_step(self.handle, n_steps, _ptr(st), self._s())
+        if code not in (0, 3) or (code == 3 and raise_on_failure):
+            _check(code)
+        return st
+
+    def step_schedule(self, y_kin_sched, out=None, raise_on_failure: bool = False):
+        """Advance all envs through len(y_kin_sched) steps, each env independently (no lockstep);
+        `out` = (coated [S,E,NC,3], marker_pos [S,E,NM,3], marker_flow [S,E,NM,3]) or None."""
+        sched = _f64(y_kin_sched)
+        n_steps = sched.shape[0]
+        st = np.zeros(self.n_envs, np.uint8)
+        c, mp, mf = out if out is not None else (None, None, None)
+        code = self.lib.tac_step_schedule(self.handle, n_steps, _ptr(sched), _ptr(c), _ptr(mp), _ptr(mf), _ptr(st),
+                                          self._s())
         if code not in (0, 3) or (code == 3 and raise_on_failure):
             _check(code)
         return st

@@ -264,3 +264,28 @@ def test_free_fall_and_fixed_point_through_abi():
     assert b0.step(1)[0] == 0
     assert np.array_equal(b0.get_state()[2].cpu().numpy(), y0[:1])
     assert b0.stats()[0]["newton_iters"] == 1
+
+
+@pytest.mark.parametrize("name,E,K", [("C1", 3, 4), ("C2", 6, 5)])
+def test_schedule_matches_lockstep_bitwise(name, E, K):
+    """tac_step_schedule (envs advance independently) == tac_set_targets + tac_step per step, bitwise,
+    including the per-step gel readout."""
+    sc = S.make_scene(name)
+    ei = S.env_inputs(sc, range(E), n_steps=K)
+    a = T.Batch(sc, E)
+    a.set_state(ei.x0, ei.y0)
+    ref = []
+    for k in range(K):
+        a.set_targets(ei.ykin[k])
+        assert (a.step(1) == 0).all()
+        ref.append([t.cpu().numpy() for t in a.get_gel_deformation()])
+    xa = a.get_state()[0].cpu().numpy()
+    b = T.Batch(sc, E)
+    b.set_state(ei.x0, ei.y0)
+    out = (np.zeros((K, E, b.n_coated, 3)), np.zeros((K, E, b.n_markers, 3)), np.zeros((K, E, b.n_markers, 3)))
+    st = b.step_schedule(ei.ykin, out=out)
+    assert (st == 0).all()
+    assert np.array_equal(b.get_state()[0].cpu().numpy(), xa)
+    for k in range(K):
+        for j in range(3):
+            assert np.array_equal(out[j][k], ref[k][j])
