@@ -501,6 +501,12 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.act_slot = C.take<int>(e * 4 * D.act_cap); D.act_xb = C.take<double>(e * 12 * D.act_cap);
   D.cptr = C.take<int>(e * (H.V + 1)); D.clist = C.take<int>(e * 4 * D.act_cap);
   D.bptr = C.take<int>(e * (H.ND + 1)); D.blist = C.take<int>(e * 4 * D.act_cap);
+  D.act_res = C.take<int>(e * D.act_cap); D.res_list = C.take<int>(e * D.act_cap);
+  D.rcnt = C.take<int>(e * H.V + 1); D.cpl_ptr = C.take<int>(e * (H.V + 1));
+  D.cpl_v = C.take<int>(e * D.cpl_cap + 1); D.cpl_d = C.take<int>(e * D.cpl_cap + 1);
+  D.cpl_val = C.take<double>(e * 36 * D.cpl_cap + 1); D.cpl_out = C.take<double>(e * 3 * D.cpl_cap + 1);
+  D.srec = C.take<double>(e * 4 * D.act_cap * SREC); D.snb = C.take<int>(e * 4 * D.act_cap * 2);
+  D.sbody = C.take<int>(e * 4 * D.act_cap); D.brec = C.take<double>(e * D.act_cap * 2 * BREC);
   D.eterm = C.take<double>(e * 8);
   D.out_coat = C.take<double>(e * H.NCOAT * 3 + 1); D.out_mpos = C.take<double>(e * H.NMARK * 3 + 1);
   D.out_mflow = C.take<double>(e * H.NMARK * 3 + 1);
@@ -515,6 +521,8 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.cand_cap = std::max(cfg->cand_capacity_per_env, 64);
   D.act_cap = std::max(cfg->active_capacity_per_env, 16);
   D.ent_cap = 16 * (H.NT + H.NE) + 4096;
+  // every coupling (v, d) owns at least one soft slot of an active pair, and each (v, d) occurs once
+  D.cpl_cap = (int)std::max<long long>(1, std::min<long long>((long long)H.V * H.ND, 4LL * D.act_cap));
   D.max_step = cfg->max_step_rel;
   D.dt = cfg->dt; D.dhat = cfg->dhat; D.kappa = cfg->kappa; D.tolN = cfg->newton_tol_rel; D.tolAL = cfg->al_tol_rel;
   D.eta = cfg->pcg_eta; D.armijo = cfg->armijo_c; D.accd_s = cfg->accd_s; D.rho0 = cfg->al_rho0; D.cell = H.cell;

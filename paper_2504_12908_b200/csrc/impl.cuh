@@ -20,6 +20,8 @@ constexpr int MAXCELLS = 32;       // targets spanning more cells go to the per-
 constexpr int BIG_CAP = 2048;
 constexpr int TETBUF = 90;         // 12 gradient + 78 packed Hessian
 constexpr int PH = 78;
+constexpr int SREC = 66;          // per soft slot record: g 3 | H_ss 9 | coupling 36 | soft neighbours 18
+constexpr int BREC = 90;          // per (pair, body) record: packed JᵀHJ 78 | Jᵀg 12
 
 enum { PHASE_ACTIVE = 0, PHASE_DONE = 1, PHASE_FAILED = 2, PHASE_IDLE = 3 };
 enum { ENV_OK = 0, ENV_NEWTON_STALL = 1, ENV_AL_INFEASIBLE = 2, ENV_CAPACITY = 3, ENV_NONFINITE = 4,
@@ -31,6 +33,7 @@ struct EnvCtl {
   int exact, hold, nfail, xfail;   // exact-Hessian-first control (reading R14b)
   int bp_ref, bp_valid;            // reusable candidate list state (reading R11b)
   int step, pad2_;                 // step index in a scheduled multi-step call
+  int n_res, n_cpl;                // residual pairs (matrix-free in the SpMV) and soft–body couplings
   long long pcg_total;
   double pcg_bytes;
   double Keff;
@@ -43,7 +46,7 @@ struct Dev {
   // ---- dims ----
   int NNZ;                // off-diagonal soft blocks in row order (2·NEs)
   int E, V, T, NA, ND, NVall, NSV, NT, NE, NEs, NC, NK, NB, n, npads, NCOAT, NMARK;
-  int cand_cap, act_cap, ent_cap;
+  int cand_cap, act_cap, ent_cap, cpl_cap;
   // ---- config ----
   double max_step;     // relative step cap (reading R17c)
   double dt, dhat, kappa, tolN, tolAL, eta, armijo, accd_s, rho0, cell;
@@ -137,6 +140,22 @@ struct Dev {
   double* act_xb;         // [E][4*act_cap][3] rest position x̄ of affine slots
   int* spos;              // [E][4*act_cap] slot → position in the soft output list (-1: not soft)
   double* sout;           // [E][4*act_cap][3] per-slot soft outputs of the pair SpMV pass
+  // contact condensation: each active pair whose slots are soft vertices adjacent in the
+  // BSR pattern and at most one DoF body is folded at assembly into the soft BSR blocks (soft–soft),
+  // the body's 12×12 (J_sᵀH_stJ_t), and one 3×12 coupling block C_vd = Σ H_st J_t per (soft vertex v,
+  // body d); the remaining "residual" pairs stay matrix-free (12×12 through J) in the SpMV
+  int* act_res;           // [E][act_cap] 1 = residual pair
+  int* res_list;          // [E][act_cap] residual pair indices (ascending)
+  int* rcnt;              // [E][V] residual slots of v = first rcnt[v] entries of its clist range
+  int* cpl_ptr;           // [E][V+1] coupling blocks of soft vertex v (ascending body)
+  int* cpl_v;             // [E][cpl_cap]
+  int* cpl_d;             // [E][cpl_cap]
+  double* cpl_val;        // [E][36][cpl_cap] SoA, C_vd row-major 3×12
+  double* cpl_out;        // [E][cpl_cap][3] SpMV scratch: C_vd x_d
+  double* srec;           // [E][4*act_cap][SREC] per soft slot, vertex-sorted position (k_pairs)
+  int* snb;               // [E][4*act_cap][2] BSR block of each soft neighbour record (-1 none)
+  int* sbody;             // [E][4*act_cap] DoF body of the coupling record (-1 none / residual)
+  double* brec;           // [E][act_cap][2][BREC] per (pair, DoF body) records (k_pairs)
   int* cptr;              // [E][V+1] soft contribution lists
   int* clist;             // [E][4*act_cap]
   int* bptr;              // [E][ND+1] body contribution lists

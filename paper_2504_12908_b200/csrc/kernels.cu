@@ -2,6 +2,7 @@
 // One CTA per environment for every per-env phase (envs are independent); per-env
 // reductions are deterministic block reductions with a fixed thread→element assignment, so every
 // env's result is bitwise independent of the batch size and of how envs are sharded.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include "eigen.cuh"
@@ -437,6 +438,31 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
 // narrow phase: active set 𝒜 = {k ∈ C : s_k < d̂²} (strict) in canonical order, plus
 // deterministic soft-vertex and body contribution lists
 // ------------------------------------------------------------------------------------------
+// contact condensation test (impl.cuh): a pair stays matrix-free ("residual") if two of its soft
+// slots are not adjacent in the soft BSR pattern or its slots span two different DoF bodies
+__device__ bool pair_is_residual(const Dev& D, const int* vid) {
+  int body = -1;
+  for (int s = 0; s < 4; ++s) {
+    const int v = vid[s];
+    if (v < D.V) {
+      for (int t = s + 1; t < 4; ++t) {
+        const int w = vid[t];
+        if (w >= D.V) continue;
+        bool adj = false;
+        for (int j = D.rptr[v]; j < D.rptr[v + 1] && !adj; ++j) adj = D.rcol[j] == w;
+        if (!adj) return true;
+      }
+    } else {
+      const int d = D.dof_slot[D.vert_aff[v]];
+      if (d >= 0) {
+        if (body >= 0 && body != d) return true;
+        body = d;
+      }
+    }
+  }
+  return false;
+}
+
 __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
@@ -484,11 +510,28 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
         }
         aslot[s] = code;
       }
+      D.act_res[(size_t)e * D.act_cap + pos] = pair_is_residual(D, vid) ? 1 : 0;
     }
     total += tot;
   }
   const int nact = min(total, D.act_cap);
   if (threadIdx.x == 0) { C.n_act = nact; if (total > D.act_cap) C.overflow = 1; }
+  __syncthreads();
+  // residual pairs (kept matrix-free in the SpMV), ascending
+  {
+    const int* ares = D.act_res + (size_t)e * D.act_cap;
+    int* rl = D.res_list + (size_t)e * D.act_cap;
+    int run = 0;
+    for (int t0 = 0; t0 < nact; t0 += blockDim.x) {
+      const int k = t0 + threadIdx.x;
+      const int f = k < nact ? ares[k] : 0;
+      int tot;
+      const int ex = block_excl_scan(f, sh, &tot);
+      if (f) rl[run + ex] = k;
+      run += tot;
+    }
+    if (threadIdx.x == 0) C.n_res = run;
+  }
   // soft-vertex contribution lists: count, scan, fill, per-vertex sort (deterministic)
   for (int v = threadIdx.x; v <= D.V; v += blockDim.x) vcnt[v] = 0;
   __syncthreads();
@@ -519,35 +562,51 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
   int* spos = D.spos + (size_t)e * 4 * D.act_cap;
   for (int i = threadIdx.x; i < 4 * nact; i += blockDim.x) spos[i] = -1;
   __syncthreads();
-  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
-    int b0 = cptr[v], b1 = cptr[v + 1];
-    for (int i = b0 + 1; i < b1; ++i) {
-      int key = clist[i], j = i - 1;
-      while (j >= b0 && clist[j] > key) { clist[j + 1] = clist[j]; --j; }
-      clist[j + 1] = key;
+  // per-vertex sort: residual-pair slots first, then by (pair, slot); only residual slots get an
+  // output position (the SpMV's matrix-free pass writes them, the soft row sums the first rcnt[v])
+  {
+    const int* ares = D.act_res + (size_t)e * D.act_cap;
+    int* rc = D.rcnt + (size_t)e * D.V;
+    for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
+      int b0 = cptr[v], b1 = cptr[v + 1], nr = 0;
+      for (int i = b0; i < b1; ++i) {
+        const int res = ares[clist[i] >> 2];
+        nr += res;
+        clist[i] |= (res ? 0 : 1) << 30;
+      }
+      for (int i = b0 + 1; i < b1; ++i) {
+        int key = clist[i], j = i - 1;
+        while (j >= b0 && clist[j] > key) { clist[j + 1] = clist[j]; --j; }
+        clist[j + 1] = key;
+      }
+      for (int i = b0; i < b1; ++i) clist[i] &= (1 << 30) - 1;
+      for (int i = b0; i < b1; ++i) spos[clist[i]] = i;   // soft slot → its vertex-sorted position
+      rc[v] = nr;
     }
-    for (int i = b0; i < b1; ++i) spos[clist[i]] = i;     // slot → position of its soft output
   }
-  // body contribution lists: stable block scan per dof body
+  // body contribution lists: pairs touching each DoF body, ascending, entry (k << 1) | record index
+  // (record 0 = the pair's lower DoF body, 1 = the higher)
   int* bptr = D.bptr + (size_t)e * (D.ND + 1);
   int* blist = D.blist + (size_t)e * 4 * D.act_cap;
+  const int* aslot_all = D.act_slot + (size_t)e * 4 * D.act_cap;
   int run = 0;
   for (int d = 0; d < D.ND; ++d) {
-    const int body = D.dof_body[d];
     if (threadIdx.x == 0) bptr[d] = run;
     for (int t0 = 0; t0 < nact; t0 += blockDim.x) {
-      int k = t0 + threadIdx.x;
-      int c = 0, mask = 0;
-      if (k < nact)
+      const int k = t0 + threadIdx.x;
+      int c = 0, rec = 0;
+      if (k < nact) {
+        const int4 c4 = reinterpret_cast<const int4*>(aslot_all)[k];
+        const int codes[4] = {c4.x, c4.y, c4.z, c4.w};
         for (int s = 0; s < 4; ++s) {
-          int gv = avid[4 * k + s];
-          if (gv >= D.V && D.vert_aff[gv] == body) { ++c; mask |= 1 << s; }
+          const int cd = codes[s];
+          if (cd == -1 - d) c = 1;
+          else if (cd < 0 && cd != INT_MIN && -1 - cd < d) rec = 1;
         }
+      }
       int tot;
-      int ex = block_excl_scan(c, sh, &tot);
-      int pos = run + ex;
-      for (int s = 0; s < 4; ++s)
-        if (mask & (1 << s)) blist[pos++] = 4 * k + s;
+      const int ex = block_excl_scan(c, sh, &tot);
+      if (c) blist[run + ex] = (k << 1) | rec;
       run += tot;
     }
   }
@@ -585,6 +644,7 @@ __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
 constexpr int PAIR_WARPS = 4;          // warps per CTA in k_pairs
 constexpr int PAIRS_PER_WARP = 4;      // pairs handled sequentially by one warp
 constexpr int PAIRS_PER_CTA = PAIR_WARPS * PAIRS_PER_WARP;
+constexpr int PAIR_GRID_X = 12;       // CTAs per env (each loops over pair chunks)
 
 struct PairScratch {
   JacobiScratch J;
@@ -595,6 +655,7 @@ struct PairScratch {
   double W[3], E1[3], E2[3], Nn[3];   // sub-distance variables (PL: E1 = e)
   double U1[9], D1[9];                // TRI: ∂u/∂var, ∂D/∂var;  PL: ∂N/∂var, ∂D/∂var;  PP: ∂s/∂w
   double CE1[3], CE2[3], CN[3], CD1[9];  // mollifier c = ‖e1×e2‖²
+  double gf[12], xb[12];              // final scaled gradient; rest positions x̄ of affine slots
 };
 
 __device__ __forceinline__ double skewv(const double* x, int a, int b) {   // ([x]×)_{ab}
@@ -630,8 +691,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
   const int nact = C.n_act;
-  const int base = blockIdx.x * PAIRS_PER_CTA;
-  if (base >= nact) return;
+  if ((int)blockIdx.x * PAIRS_PER_CTA >= nact) return;
   __shared__ PairScratch PS[PAIR_WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double* P = D.P + (size_t)e * D.NVall * 3;
@@ -641,6 +701,8 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
   double* aH = D.act_H + (size_t)e * D.act_cap * PH;
   PairScratch& S = PS[w];
   const bool project = !C.exact;
+  // CTA b takes the pair chunks b, b + gridDim.x, ... (a fixed small grid: empty CTAs cost launch time)
+  for (int base = blockIdx.x * PAIRS_PER_CTA; base < nact; base += gridDim.x * PAIRS_PER_CTA)
   for (int j = 0; j < PAIRS_PER_WARP; ++j) {
     const int k = base + w + PAIR_WARPS * j;
     if (k >= nact) break;
@@ -742,7 +804,11 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
       S.gc[lane] = useM ? g2 : 0.0;
     }
     __syncwarp();
-    if (lane < 12) ag[12 * k + lane] = scale * (m * B1 * S.gs[lane] + B * m1 * S.gc[lane]);
+    if (lane < 12) {
+      const double gfin = scale * (m * B1 * S.gs[lane] + B * m1 * S.gc[lane]);
+      ag[12 * k + lane] = gfin;
+      S.gf[lane] = gfin;
+    }
     // 3) 12×12 (upper) from the variable blocks
     for (int i = lane; i < 144; i += 32) {
       const int r = i / 12, c = i % 12;
@@ -773,7 +839,91 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
       __syncwarp();
       jacobi12_psd(S.J, lane, 32);
     }
-    for (int i = lane; i < PH; i += 32) aH[(size_t)i * D.act_cap + k] = S.J.A[12 * c_unpack_r[i] + c_unpack_c[i]];
+    const bool res = D.act_res[(size_t)e * D.act_cap + k] != 0;
+    if (res)      // residual pairs stay matrix-free in the SpMV: packed upper 12×12, AoS (coalesced)
+      for (int i = lane; i < PH; i += 32) aH[(size_t)k * PH + i] = S.J.A[12 * c_unpack_r[i] + c_unpack_c[i]];
+    // 4) condensed records (contact condensation, impl.cuh), read by k_assemble without touching H
+    for (int i = lane; i < 144; i += 32) {
+      const int r = i / 12, c = i % 12;
+      if (r > c) S.J.A[i] = S.J.A[12 * c + r];
+    }
+    if (lane < 12) S.xb[lane] = D.act_xb[((size_t)e * D.act_cap + k) * 12 + lane];
+    __syncwarp();
+    const int4 c4 = reinterpret_cast<const int4*>(D.act_slot + (size_t)e * 4 * D.act_cap)[k];
+    const int codes[4] = {c4.x, c4.y, c4.z, c4.w};
+    int bd0 = -1, bd1 = -1;              // DoF bodies of the pair (≤2: one per primitive), ascending
+    for (int t = 0; t < 4; ++t) {
+      const int cd = codes[t];
+      if (cd < 0 && cd != INT_MIN) {
+        const int d = -1 - cd;
+        if (bd0 < 0) bd0 = d;
+        else if (d != bd0) bd1 = d;
+      }
+    }
+    if (bd1 >= 0 && bd1 < bd0) { const int tmp = bd0; bd0 = bd1; bd1 = tmp; }
+    const double* A = S.J.A;
+    // per soft slot s, at its vertex-sorted position j: [g_s 3 | H_ss 9 | C_s = Σ_{t on body} H_st J_t 36 |
+    // H_st for the (≤2) other soft slots t 18]; couplings and neighbour blocks are zero for residual pairs
+    for (int s = 0; s < 4; ++s) {
+      if (codes[s] < 0) continue;
+      const int j = D.spos[(size_t)e * 4 * D.act_cap + 4 * k + s];
+      int nbt[2] = {-1, -1}, nn = 0;
+      for (int t = 0; t < 4; ++t)
+        if (t != s && codes[t] >= 0 && nn < 2) nbt[nn++] = t;
+      double* rec = D.srec + ((size_t)e * 4 * D.act_cap + j) * SREC;
+      for (int i = lane; i < SREC; i += 32) {
+        double v = 0.0;
+        if (i < 3) v = S.gf[3 * s + i];
+        else if (i < 12) v = A[12 * (3 * s + (i - 3) / 3) + 3 * s + (i - 3) % 3];
+        else if (i < 48) {
+          if (!res && bd0 >= 0) {
+            const int r = (i - 12) / 12, be = (i - 12) % 12, jr = jrow(be);
+            for (int t = 0; t < 4; ++t)
+              if (codes[t] == -1 - bd0) v += A[12 * (3 * s + r) + 3 * t + jr] * (be < 3 ? 1.0 : S.xb[3 * t + (be - 3) % 3]);
+          }
+        } else {
+          const int nb = (i - 48) / 9, rc = (i - 48) % 9, t = nbt[nb];
+          if (!res && t >= 0) v = A[12 * (3 * s + rc / 3) + 3 * t + rc % 3];
+        }
+        rec[i] = v;
+      }
+      if (lane < 2) {
+        int jb = -1;
+        const int t = nbt[lane];
+        if (!res && t >= 0) {
+          const int v = codes[s], wv = codes[t];
+          for (int q = D.rptr[v]; q < D.rptr[v + 1]; ++q)
+            if (D.rcol[q] == wv) { jb = q; break; }
+        }
+        D.snb[((size_t)e * 4 * D.act_cap + j) * 2 + lane] = jb;
+      }
+      if (lane == 0) D.sbody[(size_t)e * 4 * D.act_cap + j] = res ? -1 : bd0;
+    }
+    // per DoF body of the pair (ascending, ≤2): packed Σ_{s,t on body} J_sᵀ H_st J_t (78) and Σ_s J_sᵀ g_s (12)
+    for (int rb = 0; rb < 2; ++rb) {
+      const int bd = rb == 0 ? bd0 : bd1;
+      if (bd < 0) break;
+      double* out = D.brec + (((size_t)e * D.act_cap + k) * 2 + rb) * BREC;
+      for (int i = lane; i < BREC; i += 32) {
+        double v = 0.0;
+        if (i < PH) {
+          const int al = c_unpack_r[i], be = c_unpack_c[i], ra = jrow(al), rbw = jrow(be);
+          for (int s = 0; s < 4; ++s) {
+            if (codes[s] != -1 - bd) continue;
+            const double fs = al < 3 ? 1.0 : S.xb[3 * s + (al - 3) % 3];
+            double inner = 0.0;
+            for (int t = 0; t < 4; ++t)
+              if (codes[t] == -1 - bd) inner += (be < 3 ? 1.0 : S.xb[3 * t + (be - 3) % 3]) * A[12 * (3 * s + ra) + 3 * t + rbw];
+            v += fs * inner;
+          }
+        } else {
+          const int al = i - PH, ra = jrow(al);
+          for (int s = 0; s < 4; ++s)
+            if (codes[s] == -1 - bd) v += (al < 3 ? 1.0 : S.xb[3 * s + (al - 3) % 3]) * S.gf[3 * s + ra];
+        }
+        out[i] = v;
+      }
+    }
     __syncwarp();
   }
 }
@@ -781,6 +931,29 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
 // ------------------------------------------------------------------------------------------
 // assembly: gradient g, soft BSR (diag + edge blocks), body 12×12 blocks, block-Jacobi inverses
 // ------------------------------------------------------------------------------------------
+#ifdef TAC_CLOCKS   // per-section clock64 accumulators of k_pcg (tools/pcg_clocks.py; not in the product build)
+__device__ unsigned long long g_clk[32];
+#define CLK_INIT long long clk_t = clock64();
+#define CLK_COUNT atomicAdd(&g_clk[15], 1ull);
+#define CLKN(i) atomicAdd(&g_clk[i], 1ull);
+#define CLKT(i) { const long long t_ = clock64(); atomicAdd(&g_clk[i], (unsigned long long)(t_ - clk_t)); atomicMax(&g_clk[i + 4], (unsigned long long)(t_ - clk_t)); clk_t = t_; }
+#define CLKR clk_t = clock64();
+#define CLK(i) if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_clk[i], (unsigned long long)(t_ - clk_t)); clk_t = t_; }
+extern "C" int tac_debug_clocks(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_clk, sizeof(g_clk));
+  unsigned long long z[32] = {};
+  return (int)cudaMemcpyToSymbol(g_clk, z, sizeof(g_clk));
+}
+#else
+#define CLK_INIT
+#define CLK(i)
+#define CLK_COUNT ;
+#define CLKN(i) ;
+#define CLKT(i)
+#define CLKR
+#endif
+
 __device__ void chol_inverse12(const double* A, double* Ainv, double* L /*144 scratch*/) {
   // single thread: Cholesky A = L Lᵀ then Ainv = L⁻ᵀ L⁻¹
   for (int i = 0; i < 144; ++i) L[i] = 0.0;
@@ -816,8 +989,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
   if (env_skip(D, e, force)) return;
   __shared__ JacobiScratch JS[NTHREADS / 32];
   __shared__ double PB[NTHREADS / 32][144];
+  __shared__ int shs[33];
+  extern __shared__ double dsm_asm[];   // contact-vertex list [V] ints
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const EnvCtl& C = D.ctl[e];
+  EnvCtl& C = D.ctl[e];
   const double* q = D.q + (size_t)e * D.n;
   const double* qt = D.qt + (size_t)e * D.n;
   double* g = D.g + (size_t)e * D.n;
@@ -830,49 +1005,13 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
   const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
   const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
   const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
+  const int* ares = D.act_res + (size_t)e * D.act_cap;
   const double dt2 = D.dt * D.dt, rho = C.rho;
   const double* s_att = D.s_att + (size_t)e * D.NC * 3;
   const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
-  // ---- soft vertices ----
-  for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
-    const double m = D.mass[v];
-    v3 x = ld3(q + 3 * v), xt = ld3(qt + 3 * v);
-    v3 gv = m * (x - xt) - (dt2 * m) * mk(D.grav[0], D.grav[1], D.grav[2]);
-    double dg = m;
-    int ci = D.att_of_vert[v];
-    if (ci >= 0) {
-      v3 r = x - ld3(s_att + 3 * ci);
-      gv += (rho * m) * r - m * ld3(lam_att + 3 * ci);
-      dg += rho * m;
-    }
-    double Hv[9] = {dg, 0, 0, 0, dg, 0, 0, 0, dg};
-    for (int j = D.vdiag_ptr[v]; j < D.vdiag_ptr[v + 1]; ++j) {
-      int ent = D.vdiag[j], t = ent >> 2, a = ent & 3;
-      gv += mk(tb[(size_t)(3 * a) * D.T + t], tb[(size_t)(3 * a + 1) * D.T + t], tb[(size_t)(3 * a + 2) * D.T + t]);
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) Hv[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * a + c, 12)) * D.T + t];
-    }
-    double Pv[9];
-    for (int i = 0; i < 9; ++i) Pv[i] = Hv[i];
-    for (int j = cptr[v]; j < cptr[v + 1]; ++j) {
-      int k = clist[j] >> 2, s = clist[j] & 3;
-      gv += ld3(ag + 12 * k + 3 * s);
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) Pv[3 * r + c] += aH[(size_t)sym_idx(3 * s + r, 3 * s + c, 12) * D.act_cap + k];
-    }
-    st3(g + 3 * v, gv);
-    double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]
-    for (int i = 0; i < 9; ++i) hd[(size_t)i * D.V + v] = Hv[i];
-    double* ds = D.Dg_s + (size_t)e * D.V * 9;         // raw diagonal block (SoA) for LM re-inversion
-    for (int i = 0; i < 9; ++i) ds[(size_t)i * D.V + v] = Pv[i];
-    const double sh = C.mu * m;                         // mass-scaled LM shift μ·m_v I (R14c)
-    Pv[0] += sh; Pv[4] += sh; Pv[8] += sh;
-    double Pi[9];
-    inv33(Pv, Pi);
-    double* ps = D.Pinv_s + (size_t)e * D.V * 9;       // SoA [9][V]
-    for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
-  }
-  // ---- soft edge blocks ----
+  const size_t cap = D.act_cap;
+  CLK_INIT
+  // ---- soft edge blocks (elastic) ----
   for (int ei = threadIdx.x; ei < D.NNZ; ei += blockDim.x) {
     double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = D.rblk_ptr[ei]; j < D.rblk_ptr[ei + 1]; ++j) {
@@ -883,6 +1022,146 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
     double* ho = D.Ho + ((size_t)e * D.NNZ + ei) * 9;
     for (int i = 0; i < 9; ++i) ho[i] = B[i];
   }
+  __syncthreads();
+  CLK(10)
+  // ---- soft vertices: gradient, diagonal blocks, and the condensed contact terms of row v ----
+  int* cpp = D.cpl_ptr + (size_t)e * (D.V + 1);
+  int* cplv = D.cpl_v + (size_t)e * D.cpl_cap;
+  int* cpld = D.cpl_d + (size_t)e * D.cpl_cap;
+  double* cval = D.cpl_val + (size_t)e * 36 * D.cpl_cap;
+  double* Hoe = D.Ho + (size_t)e * D.NNZ * 9;
+  const int* rcnt = D.rcnt + (size_t)e * D.V;
+  const double* srec = D.srec + (size_t)e * 4 * D.act_cap * SREC;
+  const int* snb = D.snb + (size_t)e * 4 * D.act_cap * 2;
+  const int* sbody = D.sbody + (size_t)e * 4 * D.act_cap;
+  int* cvl = reinterpret_cast<int*>(dsm_asm);        // [V] soft vertices with contact records
+  int cpl_run = 0, nct = 0;
+  // phase 1 (thread per vertex): inertia, gravity, AL and elastic terms; body mask of the condensed
+  // records; coupling offsets and the contact-vertex list by block scans
+  for (int v0 = 0; v0 < D.V; v0 += blockDim.x) {
+    const int v = v0 + threadIdx.x;
+    unsigned bmask = 0u;
+    int hasc = 0;
+    if (v < D.V) {
+      const double m = D.mass[v];
+      v3 x = ld3(q + 3 * v), xt = ld3(qt + 3 * v);
+      v3 gv = m * (x - xt) - (dt2 * m) * mk(D.grav[0], D.grav[1], D.grav[2]);
+      double dg = m;
+      int ci = D.att_of_vert[v];
+      if (ci >= 0) {
+        v3 r = x - ld3(s_att + 3 * ci);
+        gv += (rho * m) * r - m * ld3(lam_att + 3 * ci);
+        dg += rho * m;
+      }
+      double Hv[9] = {dg, 0, 0, 0, dg, 0, 0, 0, dg};
+      for (int j = D.vdiag_ptr[v]; j < D.vdiag_ptr[v + 1]; ++j) {
+        int ent = D.vdiag[j], t = ent >> 2, a = ent & 3;
+        gv += mk(tb[(size_t)(3 * a) * D.T + t], tb[(size_t)(3 * a + 1) * D.T + t], tb[(size_t)(3 * a + 2) * D.T + t]);
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) Hv[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * a + c, 12)) * D.T + t];
+      }
+      const int j0 = cptr[v], j1 = cptr[v + 1];
+      hasc = j1 > j0;
+      for (int j = j0 + rcnt[v]; j < j1; ++j) { const int d = sbody[j]; if (d >= 0) bmask |= 1u << d; }
+      st3(g + 3 * v, gv);
+      double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]: SpMV diagonal (contact added in phase 2)
+      double* ds = D.Dg_s + (size_t)e * D.V * 9;         // raw diagonal block (SoA) for LM re-inversion
+      for (int i = 0; i < 9; ++i) { hd[(size_t)i * D.V + v] = Hv[i]; ds[(size_t)i * D.V + v] = Hv[i]; }
+      if (!hasc) {
+        const double sh = C.mu * m;                       // mass-scaled LM shift μ·m_v I (R14c)
+        Hv[0] += sh; Hv[4] += sh; Hv[8] += sh;
+        double Pi[9];
+        inv33(Hv, Pi);
+        double* ps = D.Pinv_s + (size_t)e * D.V * 9;     // SoA [9][V]
+        for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
+      }
+    }
+    int tot, totc;
+    const int ex = block_excl_scan(__popc(bmask), shs, &tot);
+    const int exc = block_excl_scan(hasc, shs, &totc);
+    if (v < D.V) {
+      cpp[v] = cpl_run + ex;
+      if (hasc) cvl[nct + exc] = v;
+      for (unsigned mm = bmask; mm; mm &= mm - 1) {
+        const int d = __ffs(mm) - 1, pos = cpl_run + ex + __popc(bmask & ((1u << d) - 1u));
+        cplv[pos] = v; cpld[pos] = d;
+      }
+    }
+    cpl_run += tot;
+    nct += totc;
+  }
+  __syncthreads();
+  // phase 2 (8-lane group per contact vertex): sum the vertex's condensed records, field-parallel
+  // (lane l8 owns fields l8 + 8i of [g 3 | H_ss 9 | C 36]); entries in vertex-sorted order
+  {
+    const int l8 = threadIdx.x & 7, grp = threadIdx.x >> 3, ngrp = blockDim.x >> 3;
+    double* hd = D.Hd + (size_t)e * D.V * 9;
+    double* ds = D.Dg_s + (size_t)e * D.V * 9;
+    for (int ci = grp; ci < nct; ci += ngrp) {
+      const int v = cvl[ci];
+      const int j0 = cptr[v], jr = j0 + rcnt[v], j1 = cptr[v + 1];
+      unsigned bmask = 0u;
+      for (int j = jr; j < j1; ++j) { const int d = sbody[j]; if (d >= 0) bmask |= 1u << d; }
+      const int dlo = bmask ? __ffs(bmask) - 1 : -1;
+      double aa[6] = {0, 0, 0, 0, 0, 0}, an[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+      for (int j = j0; j < j1; ++j) {
+        const double* rec = srec + (size_t)j * SREC;
+        const bool nr = j >= jr;
+        const bool cp = nr && sbody[j] == dlo;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const int f = l8 + 8 * i;
+          const double val = rec[f];
+          if (f < 12) { aa[i] += val; if (nr) an[i] += val; }
+          else if (cp) an[i] += val;
+        }
+      }
+      const int base = cpp[v];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const int f = l8 + 8 * i;
+        if (f < 3) g[3 * v + f] += aa[i];
+        else if (f < 12) { hd[(size_t)(f - 3) * D.V + v] += an[i]; ds[(size_t)(f - 3) * D.V + v] += aa[i]; }
+        else if (dlo >= 0) cval[(size_t)(f - 12) * D.cpl_cap + base] = an[i];
+      }
+      // further bodies of this vertex (rare), ascending
+      for (unsigned mm = bmask & (bmask - 1u); mm; mm &= mm - 1) {
+        const int d = __ffs(mm) - 1, pos = base + __popc(bmask & ((1u << d) - 1u));
+        for (int f = 12 + l8; f < 48; f += 8) {
+          double a = 0.0;
+          for (int j = jr; j < j1; ++j)
+            if (sbody[j] == d) a += srec[(size_t)j * SREC + f];
+          cval[(size_t)(f - 12) * D.cpl_cap + pos] = a;
+        }
+      }
+      // soft–soft contact blocks folded into row v's BSR blocks (lane l8 owns element l8, lane 0 also 8)
+      for (int j = jr; j < j1; ++j)
+        for (int nb = 0; nb < 2; ++nb) {
+          const int jb = snb[2 * j + nb];
+          if (jb < 0) continue;
+          double* hb = Hoe + (size_t)jb * 9;
+          const double* rec = srec + (size_t)j * SREC + 48 + 9 * nb;
+          hb[l8] += rec[l8];
+          if (l8 == 0) hb[8] += rec[8];
+        }
+    }
+  }
+  __syncthreads();
+  // phase 3: block-Jacobi inverses of the contact vertices
+  for (int ci = threadIdx.x; ci < nct; ci += blockDim.x) {
+    const int v = cvl[ci];
+    const double* ds = D.Dg_s + (size_t)e * D.V * 9;
+    double Pv[9], Pi[9];
+    for (int i = 0; i < 9; ++i) Pv[i] = ds[(size_t)i * D.V + v];
+    const double sh = C.mu * D.mass[v];
+    Pv[0] += sh; Pv[4] += sh; Pv[8] += sh;
+    inv33(Pv, Pi);
+    double* ps = D.Pinv_s + (size_t)e * D.V * 9;
+    for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
+  }
+  if (threadIdx.x == 0) { cpp[D.V] = cpl_run; C.n_cpl = cpl_run; }
+  CLK(11)
   // ---- affine DoF bodies: warp per body ----
   for (int d = w; d < D.ND; d += nw) {
     const int b = D.dof_body[d];
@@ -933,50 +1212,52 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
     if (lane < 12) g[3 * D.V + 12 * d + lane] = gb;      // pair terms added below
   }
   __syncthreads();
-  // pair contributions to each body's gradient and preconditioner block: all warps split the
-  // body's contribution list (warp w takes entries w, w+nw, ...), partials summed in warp order
+  // pair contributions to each body's gradient and diagonal block: all warps split the body's
+  // contribution list (warp w takes entries w, w+nw, ...), partials summed in warp order.  Pass 0
+  // folds the condensed (non-residual) pairs into Hb (the SpMV's body block); pass 1 adds the
+  // residual pairs, which the SpMV applies matrix-free, for the preconditioner block only
   __shared__ double GB[NTHREADS / 32][12];
+  CLK(12)
   for (int d = 0; d < D.ND; ++d) {
-    const int b = D.dof_body[d];
-    double acc[5] = {0, 0, 0, 0, 0};   // entries i = lane + 32·t of the 144
-    double gacc = 0.0;
-    for (int j = bptr[d] + w; j < bptr[d + 1]; j += nw) {
-      const int k = blist[j] >> 2, s = blist[j] & 3;
-      const double* xs = axb + 12 * k + 3 * s;
-      if (lane < 12) gacc += jf(lane, xs) * ag[12 * k + 3 * s + jrow(lane)];
-      const int4 code4 = reinterpret_cast<const int4*>(aslot)[k];
-      const int codes[4] = {code4.x, code4.y, code4.z, code4.w};
-      for (int t = 0; t < 4; ++t) {
-        if (codes[t] != -1 - d) continue;
-        const double* xt = axb + 12 * k + 3 * t;
+    double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
+    double* T = JS[d % nw].A;            // running total block of body d
+    for (int pass = 0; pass < (C.n_res > 0 ? 2 : 1); ++pass) {
+      double acc[5] = {0, 0, 0, 0, 0};   // entries i = lane + 32·t of the 144
+      double gacc = 0.0;
+      const double* brec = D.brec + (size_t)e * D.act_cap * 2 * BREC;
+#pragma unroll 4
+      for (int j = bptr[d] + w; j < bptr[d + 1]; j += nw) {
+        const int k = blist[j] >> 1, rb = blist[j] & 1;
+        const double* rec = brec + ((size_t)k * 2 + rb) * BREC;
+        if (pass == 0 && lane < 12) gacc += rec[PH + lane];
+        if ((ares[k] != 0) != (pass == 1)) continue;
 #pragma unroll
         for (int tt = 0; tt < 5; ++tt) {
           const int i = lane + 32 * tt;
-          if (i < 144) {
-            const int al = i / 12, be = i % 12;
-            acc[tt] += jf(al, xs) * jf(be, xt) * aH[(size_t)sym_idx(3 * s + jrow(al), 3 * t + jrow(be), 12) * D.act_cap + k];
-          }
+          if (i < 144) acc[tt] += rec[sym_idx(i / 12, i % 12, 12)];
         }
       }
-    }
 #pragma unroll
-    for (int tt = 0; tt < 5; ++tt)
-      if (lane + 32 * tt < 144) PB[w][lane + 32 * tt] = acc[tt];
-    if (lane < 12) GB[w][lane] = gacc;
-    __syncthreads();
+      for (int tt = 0; tt < 5; ++tt)
+        if (lane + 32 * tt < 144) PB[w][lane + 32 * tt] = acc[tt];
+      if (pass == 0 && lane < 12) GB[w][lane] = gacc;
+      __syncthreads();
+      if (w == d % nw) {
+        for (int i = lane; i < 144; i += 32) {
+          double v = pass == 0 ? Hb[i] : T[i];
+          for (int ww = 0; ww < nw; ++ww) v += PB[ww][i];
+          T[i] = v;
+          if (pass == 0) Hb[i] = v;
+        }
+        if (pass == 0 && lane < 12) {
+          double v = g[3 * D.V + 12 * d + lane];
+          for (int ww = 0; ww < nw; ++ww) v += GB[ww][lane];
+          g[3 * D.V + 12 * d + lane] = v;
+        }
+      }
+      __syncthreads();
+    }
     if (w == d % nw) {
-      const double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
-      double* T = JS[w].A;               // total block
-      for (int i = lane; i < 144; i += 32) {
-        double v = Hb[i];
-        for (int ww = 0; ww < nw; ++ww) v += PB[ww][i];
-        T[i] = v;
-      }
-      if (lane < 12) {
-        double v = g[3 * D.V + 12 * d + lane];
-        for (int ww = 0; ww < nw; ++ww) v += GB[ww][lane];
-        g[3 * D.V + 12 * d + lane] = v;
-      }
       double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
       const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
       for (int i = lane; i < 144; i += 32) { Db[i] = T[i]; T[i] += C.mu * Mb[i]; }
@@ -986,16 +1267,20 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
     }
     __syncthreads();
   }
+  CLK(13)
+  if (threadIdx.x == 0) CLKN(14)
 }
 
 // ------------------------------------------------------------------------------------------
-// matrix-free SpMV y = H x: soft BSR + affine 12×12 + pair 12×12 through J_v (deterministic)
+// SpMV y = H x with the contact terms condensed at assembly (k_assemble): soft BSR (elastic +
+// soft–soft contact blocks) + 3×3 diagonals, body 12×12 (incl. same-body pair terms), 3×12
+// soft–body coupling blocks, and the few residual pairs matrix-free through J_v (deterministic)
 // ------------------------------------------------------------------------------------------
-// Pass A: each warp takes 32 consecutive active pairs (one per lane): out = H_k x_local; soft-slot
-// outputs go to their vertex-sorted position sout[spos] (written once, summed in pass B without
-// dependent loads); DoF-body slots are pulled back through J_vᵀ and warp-reduced in a fixed order
-// into per-warp partials part[w][d][12].  Pass B: soft rows (BSR + contiguous sout range) and body
-// rows (Hb x_b + Σ_w part[w][d]).  Deterministic for a fixed blockDim.
+// Pass A1: residual pairs (one per lane): out = H_k x_local; soft-slot outputs go to their
+// vertex-sorted position sout[spos]; DoF-body slots are pulled back through J_vᵀ and warp-reduced
+// in a fixed order into per-warp partials part[w][d][12].  Pass A2: couplings (one per lane):
+// C_vd x_d → cpl_out[c], C_vdᵀ x_v → part.  Pass B: soft rows (BSR + diagonal + contiguous sout
+// and cpl_out ranges) and body rows (Hb x_b + Σ_w part[w][d]).  Deterministic for a fixed blockDim.
 __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
                      double mu = 0.0) {
   const EnvCtl& C = D.ctl[e];
@@ -1005,16 +1290,21 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
   const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
   const int* spos = D.spos + (size_t)e * 4 * D.act_cap;
   double* sout = D.sout + (size_t)e * 4 * D.act_cap * 3;
-  const int nact = C.n_act;
+  const int* rl = D.res_list + (size_t)e * D.act_cap;
+  const int nres = C.n_res, ncpl = C.n_cpl;
   const int nb12 = D.ND * 12;
+  CLK_INIT
   for (int i = threadIdx.x; i < nw * nb12; i += blockDim.x) part[i] = 0.0;
   __syncthreads();
-  for (int base = 32 * w; base < nact; base += blockDim.x) {
-    const int k = base + lane;
+  CLK(0)
+  // pass A1: residual pairs, matrix-free 12×12 (one pair per lane)
+  for (int base = 32 * w; base < nres; base += blockDim.x) {
+    const int idx = base + lane;
     double out[12];
     int bd[4] = {-1, -1, -1, -1};
     v3 xbs[4];
-    if (k < nact) {
+    if (idx < nres) {
+      const int k = rl[idx];
       double xl[12];
       const int4 code4 = reinterpret_cast<const int4*>(aslot)[k];
       const int codes[4] = {code4.x, code4.y, code4.z, code4.w};
@@ -1030,15 +1320,14 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
         }
         xl[3 * s] = u.x; xl[3 * s + 1] = u.y; xl[3 * s + 2] = u.z;
       }
-      const double* H = aH + k;                         // SoA: entry i at H[i·act_cap]
-      const size_t cap = D.act_cap;
+      const double* H = aH + (size_t)k * PH;            // packed upper 12×12 (AoS)
 #pragma unroll
       for (int r = 0; r < 12; ++r) out[r] = 0.0;
 #pragma unroll
       for (int r = 0; r < 12; ++r)
 #pragma unroll
         for (int c = r; c < 12; ++c) {
-          const double h = H[(size_t)sym_idx(r, c, 12) * cap];
+          const double h = H[sym_idx(r, c, 12)];
           out[r] += h * xl[c];
           if (c != r) out[c] += h * xl[r];
         }
@@ -1072,8 +1361,54 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
         for (int i = 0; i < 12; ++i) part[w * nb12 + 12 * d + i] += c[i];
     }
   }
+  // pass A2: soft–body couplings (one per lane): soft output C_vd x_d → cpl_out[c] (summed by row v
+  // in pass B), body output C_vdᵀ x_v warp-reduced per body into part[w][d]
+  {
+    const int* cplv = D.cpl_v + (size_t)e * D.cpl_cap;
+    const int* cpld = D.cpl_d + (size_t)e * D.cpl_cap;
+    const double* cval = D.cpl_val + (size_t)e * 36 * D.cpl_cap;
+    double* cout = D.cpl_out + (size_t)e * 3 * D.cpl_cap;
+    const size_t ccap = D.cpl_cap;
+    for (int base = 32 * w; base < ncpl; base += blockDim.x) {
+      const int c = base + lane;
+      double ob[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) ob[i] = 0.0;
+      int bd = -1;
+      if (c < ncpl) {
+        const int v = cplv[c];
+        bd = cpld[c];
+        const v3 xv = ld3(x + 3 * v);
+        const double* xb = x + 3 * D.V + 12 * bd;
+        double so[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int b = 0; b < 12; ++b) {
+          const double xbb = xb[b];
+          const double c0 = cval[(size_t)b * ccap + c], c1 = cval[(size_t)(12 + b) * ccap + c], c2 = cval[(size_t)(24 + b) * ccap + c];
+          so[0] += c0 * xbb; so[1] += c1 * xbb; so[2] += c2 * xbb;
+          ob[b] = c0 * xv.x + c1 * xv.y + c2 * xv.z;
+        }
+        cout[3 * c] = so[0]; cout[3 * c + 1] = so[1]; cout[3 * c + 2] = so[2];
+      }
+      if (__ballot_sync(0xffffffffu, bd >= 0) == 0u) continue;
+      for (int d = 0; d < D.ND; ++d) {
+        const bool mine = bd == d;
+        if (__ballot_sync(0xffffffffu, mine) == 0u) continue;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          const double t = warp_sum(mine ? ob[i] : 0.0);
+          if (lane == 0) part[w * nb12 + 12 * d + i] += t;
+        }
+      }
+    }
+  }
+  CLK(1)
   __syncthreads();
+  CLK(2)
   const int* cptr = D.cptr + (size_t)e * (D.V + 1);
+  const int* rcnt = D.rcnt + (size_t)e * D.V;
+  const int* cpp = D.cpl_ptr + (size_t)e * (D.V + 1);
+  const double* cout = D.cpl_out + (size_t)e * 3 * D.cpl_cap;
   const double* Hd = D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
   const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
   // soft rows: 4 lanes per row; lane q of the group takes blocks j = rptr[v]+q, +4, ... (adjacent
@@ -1101,12 +1436,14 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
         acc += mk(Hd[v] * xv.x + Hd[V + v] * xv.y + Hd[2 * V + v] * xv.z,
                   Hd[3 * V + v] * xv.x + Hd[4 * V + v] * xv.y + Hd[5 * V + v] * xv.z,
                   Hd[6 * V + v] * xv.x + Hd[7 * V + v] * xv.y + Hd[8 * V + v] * xv.z);
-        for (int j = cptr[v]; j < cptr[v + 1]; ++j) acc += ld3(sout + 3 * j);
+        for (int j = cptr[v], j1r = cptr[v] + rcnt[v]; j < j1r; ++j) acc += ld3(sout + 3 * j);
+        for (int j = cpp[v]; j < cpp[v + 1]; ++j) acc += ld3(cout + 3 * j);
         if (mu != 0.0) acc += (mu * D.mass[v]) * xv;
         st3(y + 3 * v, acc);
       }
     }
   }
+  CLK(3)
   for (int i = threadIdx.x; i < nb12; i += blockDim.x) {
     const int d = i / 12, row = i % 12;
     const double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144 + 12 * row;
@@ -1121,6 +1458,7 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
     y[3 * D.V + i] = sacc;
   }
   __syncthreads();
+  CLK(4)
 }
 
 // block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c)
@@ -1210,20 +1548,27 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force,
     bad = !(rz0 == rz0);
     while (!bad && it < D.max_pcg && rz > stop) {
       spmv(D, e, d, Ad, bpart, mu);
+      CLK_INIT
       part = 0.0;
       for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
       double dAd = block_sum(part, red);
+      CLK(5)
       if (!(dAd > 0.0)) { bad = true; break; }          // not SPD along d (uniform across the block)
       double alpha = rz / dAd;
       for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] += alpha * d[i]; r[i] -= alpha * Ad[i]; }
       __syncthreads();
+      CLK(6)
       precond(D, e, r, z);
+      CLK(7)
       part = 0.0;
       for (int i = threadIdx.x; i < n; i += blockDim.x) part += r[i] * z[i];
       double rzn = block_sum(part, red);
+      CLK(8)
       double beta = rzn / rz;
       for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = z[i] + beta * d[i];
       __syncthreads();
+      CLK(9)
+      if (threadIdx.x == 0) CLK_COUNT
       rz = rzn;
       ++it;
       if (!(rz == rz)) bad = true;
@@ -1806,11 +2151,14 @@ void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   if (D.T > 0) k_tets<<<grid, NTHREADS, 0, s>>>(D, env0, force);
 }
 void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  dim3 grid((D.act_cap + PAIRS_PER_CTA - 1) / PAIRS_PER_CTA, ne);
+  dim3 grid(std::min((D.act_cap + PAIRS_PER_CTA - 1) / PAIRS_PER_CTA, PAIR_GRID_X), ne);
   k_pairs<<<grid, PAIR_WARPS * 32, 0, s>>>(D, env0, force);
 }
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  k_assemble<<<ne, NTHREADS, 0, s>>>(D, env0, force);
+  const int bytes = (D.V + 2) * (int)sizeof(int);
+  static int attr = 0;
+  if (bytes > attr) { cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); attr = bytes; }
+  k_assemble<<<ne, NTHREADS, bytes, s>>>(D, env0, force);
 }
 static size_t spmv_smem(const Dev& D) { return (size_t)(NTHREADS / 32) * D.ND * 12 * sizeof(double) + 8; }
 void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {

@@ -1,0 +1,33 @@
+"""Per-section clock64 cycles of one k_pcg iteration (thread 0 of each CTA, averaged over iterations).
+Needs the instrumented build: nvcc ... -DTAC_CLOCKS (see tools/build_clocks.sh); usage: pcg_clocks.py E W K."""
+import ctypes, sys
+import numpy as np, torch
+sys.path.insert(0, "/root/repo")
+from paper_2504_12908_b200 import scenes as S, taccel as T
+E, W, K = (int(a) for a in sys.argv[1:4])
+NAMES = ["zero+sync", "pairs", "sync", "soft rows", "body rows+sync", "dAd sum", "p,r upd", "precond", "rz sum", "d upd"]
+sc = S.make_scene("C2")
+ei = S.env_inputs(sc, np.arange(E), n_steps=W + K)
+b = T.Batch(sc, E)
+b.set_state(ei.x0, ei.y0)
+yk = torch.tensor(ei.ykin, device="cuda")
+b.step_schedule(yk[:W])
+lib = T.load()
+buf = (ctypes.c_ulonglong * 32)()
+lib.tac_debug_clocks(buf)
+b.step_schedule(yk[W:W + K])
+lib.tac_debug_clocks(buf)
+n = buf[15]
+tot = sum(buf[i] for i in range(10))
+print(f"E={E}: {n} CTA-iterations, {tot / max(n, 1):.0f} cycles/iteration")
+for i, nm in enumerate(NAMES):
+    print(f"  {nm:16s} {buf[i] / max(n, 1):9.0f} cyc  {100 * buf[i] / max(tot, 1):5.1f}%")
+na = max(buf[14], 1)
+print(f"k_assemble: {buf[14]} CTA launches")
+for i, nm in zip(range(10, 14), ["edge blocks", "vertex loop", "body warps", "body pair terms"]):
+    print(f"  {nm:16s} {buf[i] / na:9.0f} cyc")
+nt = 256 * na
+for i, nm in zip(range(16, 20), ["tets+init (per thread)", "records (per thread)", "tail (per thread)", "scan (CTA)"]):
+    print(f"  {nm:24s} {buf[i] / (na if i == 19 else nt):9.0f} cyc   max {buf[i + 4] if i < 19 else 0}")
+s = b.stats()
+print("n_active mean", np.mean([x["n_active"] for x in s]), "max", max(x["n_active"] for x in s))
