@@ -690,6 +690,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
   const int e = env0 + blockIdx.y;
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
+  if (C.exact) return;                                    // exact Hessians: k_pairs_x (thread per pair)
   const int nact = C.n_act;
   if ((int)blockIdx.x * PAIRS_PER_CTA >= nact) return;
   __shared__ PairScratch PS[PAIR_WARPS];
@@ -927,6 +928,413 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
     __syncwarp();
   }
 }
+
+// ------------------------------------------------------------------------------------------
+// barrier pairs, exact Hessian (hessian_mode ≥ 1 with C.exact; the LM default R14c): ONE THREAD
+// PER PAIR, everything in registers.  Every sub-distance variable (w, e1, e2; and the EE mollifier's
+// a1−a0, b1−b0) is a ±1 combination of the slots with zero coefficient sum, so the pair energy is a
+// function of the relative coordinates y_j = x_j − x_0 (j = 1..3).  The thread builds the scaled
+// gradient G_y (9) and Hessian H_y (9×9, packed upper 45) of κA_k m b(d) in y-space, then expands
+// exactly the slot-space blocks the condensed records need (same record layout as k_pairs):
+//   slot s row-block of H:  Q_s[(l,b)][r] = Σ_j σ_j(s) H_y[(j,r),(l,b)],  σ_j(0) = −1, σ_j(s) = δ_js
+//   H_st[r][b] = Σ_l σ_l(t) Q_s[(l,b)][r];  g_s = Σ_j σ_j(s) G_y[j]
+//   body pull-back weights w_l(β) = on_l f(β,l) − on_0 f(β,0), f(β,t) = 1 (β<3) or x̄_t[(β−3)%3]:
+//   C_s[r][β] = Σ_l w_l(β) Q_s[(l,ρβ)][r],  body block [α,β] = Σ_{j,l} w_j(α) w_l(β) H_y[(j,ρα),(l,ρβ)]
+// (P:L393 barrier, P:L419 weights; readings R7, R10-R12.)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ constexpr int s9(int r, int c) {      // packed upper index of a 9×9, r ≤ c
+  return r * 9 - (r * (r - 1)) / 2 + (c - r);
+}
+__device__ __forceinline__ double hy_at(const double* Hy, int r, int c) { return r <= c ? Hy[s9(r, c)] : Hy[s9(c, r)]; }
+
+// H_y += Σ_{v,u} cy[v][j] cy[u][l] · wgt · h(v,a,u,b) for the sub-distance SUB (var-space second
+// derivatives as in k_pairs, evaluated with compile-time indices)
+template <int SUB>
+__device__ __forceinline__ void scatter_sub(double* Hy, const double (*cy)[3], double wgt, const double* W,
+                                            const double* E1, const double* E2, const double* Nn, const double* u1,
+                                            const double* d1, const SubDist& SD) {
+  constexpr int NV = SUB == SUB_TRI ? 3 : (SUB == SUB_PL ? 2 : 1);
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int u = 0; u < NV; ++u)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          double h;
+          const double dab = a == b ? 1.0 : 0.0;
+          if constexpr (SUB == SUB_TRI) {
+            const double ua = u1[3 * v + a], ub = u1[3 * u + b], Da = d1[3 * v + a], Db = d1[3 * u + b], U = SD.u;
+            h = 2.0 * (ua * ub + U * tri_u2_fast(W, E1, E2, v, a, u, b)) * SD.iD - 2.0 * U * (ua * Db + Da * ub) * SD.iD2 -
+                U * U * tri_D2_fast(E1, E2, Nn, v, a, u, b) * SD.iD2 + 2.0 * U * U * Da * Db * SD.iD3;
+          } else if constexpr (SUB == SUB_PL) {
+            const double ua = u1[3 * v + a], ub = u1[3 * u + b], Da = d1[3 * v + a], Db = d1[3 * u + b];
+            double N2;
+            if (v == 0 && u == 0) N2 = 2.0 * (SD.D * dab - E1[a] * E1[b]);
+            else if (v == 1 && u == 1) N2 = 2.0 * (SD.ww * dab - W[a] * W[b]);
+            else if (v == 0) N2 = 2.0 * (2.0 * W[a] * E1[b] - E1[a] * W[b] - SD.we * dab);
+            else N2 = 2.0 * (2.0 * W[b] * E1[a] - E1[b] * W[a] - SD.we * dab);
+            const double D2 = (v == 1 && u == 1) ? 2.0 * dab : 0.0;
+            h = N2 * SD.iD - (ua * Db + Da * ub) * SD.iD2 - SD.N * D2 * SD.iD2 + 2.0 * SD.N * Da * Db * SD.iD3;
+          } else {
+            h = 2.0 * dab;
+          }
+          const double t = wgt * h;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const double tj = cy[v][j] * t;
+#pragma unroll
+            for (int l = 0; l < 3; ++l)
+              if (3 * j + a <= 3 * l + b) Hy[s9(3 * j + a, 3 * l + b)] += cy[u][l] * tj;
+          }
+        }
+}
+
+// sub-distance of a classified pair in y-coordinates (y_j = x_j − x_0): the variables' slot
+// coefficients cy[v][j] (v = w, e1, e2; j = slot j+1) by selects, no runtime-indexed arrays
+// (same variables as sd_make, geometry.cuh)
+__device__ __forceinline__ v3 slot_sel(const v3* X, int s) {
+  return s == 0 ? X[0] : (s == 1 ? X[1] : (s == 2 ? X[2] : X[3]));
+}
+__device__ __forceinline__ void sd_make_y(int kind, int type, const v3* X, SubDist& S, double (*cy)[3]) {
+  int w0 = 0, w1 = 0, e0 = -1, e1 = -1, f0 = -1, f1 = -1;   // w = x_w0 − x_w1, e1 = x_e1 − x_e0, e2 = x_f1 − x_f0
+  if (kind == 0) {
+    if (type == PT_T) { S.sub = SUB_TRI; w0 = 0; w1 = 1; e0 = 1; e1 = 2; f0 = 1; f1 = 3; }
+    else if (type < PT_V0) { const int i = type - PT_E0; S.sub = SUB_PL; w0 = 0; w1 = 1 + i; e0 = 1 + i; e1 = 1 + (i + 1) % 3; }
+    else { S.sub = SUB_PP; w0 = 0; w1 = 1 + type - PT_V0; }
+  } else {
+    const int ss = type / 3, ts = type % 3;
+    if (ss == 1 && ts == 1) { S.sub = SUB_TRI; w0 = 0; w1 = 2; e0 = 0; e1 = 1; f0 = 2; f1 = 3; }
+    else if (ss == 1) { S.sub = SUB_PL; w0 = ts == 0 ? 2 : 3; w1 = 0; e0 = 0; e1 = 1; }
+    else if (ts == 1) { S.sub = SUB_PL; w0 = ss == 0 ? 0 : 1; w1 = 2; e0 = 2; e1 = 3; }
+    else { S.sub = SUB_PP; w0 = ss == 0 ? 0 : 1; w1 = ts == 0 ? 2 : 3; }
+  }
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    cy[0][j] = (w0 == j + 1 ? 1.0 : 0.0) - (w1 == j + 1 ? 1.0 : 0.0);
+    cy[1][j] = e0 < 0 ? 0.0 : (e1 == j + 1 ? 1.0 : 0.0) - (e0 == j + 1 ? 1.0 : 0.0);
+    cy[2][j] = f0 < 0 ? 0.0 : (f1 == j + 1 ? 1.0 : 0.0) - (f0 == j + 1 ? 1.0 : 0.0);
+  }
+  S.w = slot_sel(X, w0) - slot_sel(X, w1);
+  S.e1 = e0 < 0 ? mk(0, 0, 0) : slot_sel(X, e1) - slot_sel(X, e0);
+  S.e2 = f0 < 0 ? mk(0, 0, 0) : slot_sel(X, f1) - slot_sel(X, f0);
+  if (S.sub == SUB_PP) {
+    S.s = dot(S.w, S.w);
+  } else if (S.sub == SUB_PL) {
+    S.ww = dot(S.w, S.w); S.D = dot(S.e1, S.e1); S.we = dot(S.w, S.e1);
+    const v3 c = cross(S.w, S.e1);
+    S.N = dot(c, c);
+    S.s = S.N / S.D;
+    S.iD = 1.0 / S.D; S.iD2 = S.iD * S.iD; S.iD3 = S.iD2 * S.iD;
+  } else {
+    S.n = cross(S.e1, S.e2); S.u = dot(S.w, S.n); S.D = dot(S.n, S.n);
+    S.s = S.u * S.u / S.D;
+    S.iD = 1.0 / S.D; S.iD2 = S.iD * S.iD; S.iD3 = S.iD2 * S.iD;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.y;
+  if (env_skip(D, e, force)) return;
+  const EnvCtl& C = D.ctl[e];
+  if (!C.exact) return;                                   // projected Hessians: k_pairs (warp Jacobi)
+  const int nact = C.n_act;
+  const double* P = D.P + (size_t)e * D.NVall * 3;
+  const int* info = D.act_info + (size_t)e * D.act_cap * 4;
+  const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
+  double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  const size_t e4 = (size_t)e * 4 * D.act_cap;
+  __shared__ double sHy[45][128];                         // H_y of this thread's pair (records phase)
+  const int tx = threadIdx.x;
+#define HYS(r, c) ((r) <= (c) ? sHy[s9(r, c)][tx] : sHy[s9(c, r)][tx])
+  for (int k = blockIdx.x * blockDim.x + tx; k < nact; k += gridDim.x * blockDim.x) {
+    double Gy[9];
+    {
+      const int4 inf = reinterpret_cast<const int4*>(info)[k];
+      const int kind = inf.x, type = inf.y, pa = inf.z, pb = inf.w;
+      const int4 vv = reinterpret_cast<const int4*>(avid)[k];
+      SubDist SD;
+      double cy[3][3];
+      double m = 1.0, m1 = 0.0, m2 = 0.0;
+      const bool useM = (kind == 1) && D.mollify;
+      v3 CE1v = mk(0, 0, 0), CE2v = mk(0, 0, 0), CNv = mk(0, 0, 0);   // mollifier c = ‖(a1−a0)×(b1−b0)‖²
+      {
+        const v3 X[4] = {ld3(P + 3 * vv.x), ld3(P + 3 * vv.y), ld3(P + 3 * vv.z), ld3(P + 3 * vv.w)};
+        sd_make_y(kind, type, X, SD, cy);
+        if (useM) {
+          CE1v = X[1] - X[0]; CE2v = X[3] - X[2]; CNv = cross(CE1v, CE2v);
+          mollifier(dot(CNv, CNv), pair_eps(D, kind, pa, pb), &m, &m1, &m2);
+        }
+      }
+      double B, B1, B2;
+      barrier_s(SD.s, D.dhat, &B, &B1, &B2);
+      const bool molterm = useM && m1 != 0.0;
+      const double scale = D.dt * D.dt * D.kappa * pair_area(D, kind, pa, pb);
+      const double W[3] = {SD.w.x, SD.w.y, SD.w.z}, E1[3] = {SD.e1.x, SD.e1.y, SD.e1.z},
+                   E2[3] = {SD.e2.x, SD.e2.y, SD.e2.z}, Nn[3] = {SD.n.x, SD.n.y, SD.n.z};
+      // var-space first derivatives (var v, component a): u1 (∂u / ∂N), d1 (∂D), g = ∂s
+      double u1[9], d1[9], gys[9];
+      {
+        double gv[9];
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const int a1 = (a + 1) % 3, a2 = (a + 2) % 3;
+            double uu = 0.0, dd = 0.0, g1;
+            if (SD.sub == SUB_TRI) {
+              if (v == 0) uu = Nn[a];
+              else if (v == 1) uu = E2[a1] * W[a2] - E2[a2] * W[a1];
+              else uu = W[a1] * E1[a2] - W[a2] * E1[a1];
+              if (v == 1) dd = 2.0 * (E2[a1] * Nn[a2] - E2[a2] * Nn[a1]);
+              else if (v == 2) dd = 2.0 * (Nn[a1] * E1[a2] - Nn[a2] * E1[a1]);
+              g1 = 2.0 * SD.u * uu * SD.iD - SD.u * SD.u * dd * SD.iD2;
+            } else if (SD.sub == SUB_PL) {
+              if (v == 0) uu = 2.0 * (SD.D * W[a] - SD.we * E1[a]);
+              else if (v == 1) uu = 2.0 * (SD.ww * E1[a] - SD.we * W[a]);
+              if (v == 1) dd = 2.0 * E1[a];
+              g1 = uu * SD.iD - SD.N * dd * SD.iD2;
+            } else {
+              uu = v == 0 ? 2.0 * W[a] : 0.0;
+              g1 = uu;
+            }
+            u1[3 * v + a] = uu; d1[3 * v + a] = dd; gv[3 * v + a] = g1;
+          }
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            gys[3 * j + a] = cy[0][j] * gv[a] + cy[1][j] * gv[3 + a] + cy[2][j] * gv[6 + a];
+      }
+      double Hy[45];
+      // H_y = scale [ m (B2 gs gsᵀ + B1 ∇²s) + (mollifier) B (m2 gc gcᵀ + m1 ∇²c) + m1 B1 (gs gcᵀ + gc gsᵀ) ]
+      {
+        double gyc[9];
+        const double CE1[3] = {CE1v.x, CE1v.y, CE1v.z}, CE2[3] = {CE2v.x, CE2v.y, CE2v.z}, CN[3] = {CNv.x, CNv.y, CNv.z};
+        // cross variables in y: a1 − a0 = y1, b1 − b0 = y3 − y2 (EE slot order a0, a1, b0, b1)
+        constexpr double cyc[3][3] = {{0, 0, 0}, {1, 0, 0}, {0, -1, 1}};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const int a1 = (a + 1) % 3, a2 = (a + 2) % 3;
+          const double c1 = useM ? 2.0 * (CE2[a1] * CN[a2] - CE2[a2] * CN[a1]) : 0.0;   // ∂c/∂(a1−a0)
+          const double c2 = useM ? 2.0 * (CN[a1] * CE1[a2] - CN[a2] * CE1[a1]) : 0.0;   // ∂c/∂(b1−b0)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) gyc[3 * j + a] = cyc[1][j] * c1 + cyc[2][j] * c2;
+        }
+        const double r1 = scale * m * B2, rc = molterm ? scale * B * m2 : 0.0, rx = molterm ? scale * m1 * B1 : 0.0;
+#pragma unroll
+        for (int r = 0; r < 9; ++r)
+#pragma unroll
+          for (int c = r; c < 9; ++c)
+            Hy[s9(r, c)] = r1 * gys[r] * gys[c] + rc * gyc[r] * gyc[c] + rx * (gys[r] * gyc[c] + gyc[r] * gys[c]);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Gy[i] = scale * (m * B1 * gys[i] + B * m1 * gyc[i]);
+        if (molterm) {                 // B m1 ∇²c, c = ‖e1×e2‖² on the cross variables (vars 1, 2)
+          const double wC = scale * B * m1;
+#pragma unroll
+          for (int v = 1; v < 3; ++v)
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int u = 1; u < 3; ++u)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                  const double t = wC * tri_D2_fast(CE1, CE2, CN, v, a, u, b);
+#pragma unroll
+                  for (int j = 0; j < 3; ++j) {
+                    const double tj = cyc[v][j] * t;
+#pragma unroll
+                    for (int l = 0; l < 3; ++l)
+                      if (3 * j + a <= 3 * l + b) Hy[s9(3 * j + a, 3 * l + b)] += cyc[u][l] * tj;
+                  }
+                }
+        }
+      }
+      {
+        const double wS = scale * m * B1;
+        if (SD.sub == SUB_TRI) scatter_sub<SUB_TRI>(Hy, cy, wS, W, E1, E2, Nn, u1, d1, SD);
+        else if (SD.sub == SUB_PL) scatter_sub<SUB_PL>(Hy, cy, wS, W, E1, E2, Nn, u1, d1, SD);
+        else scatter_sub<SUB_PP>(Hy, cy, wS, W, E1, E2, Nn, u1, d1, SD);
+      }
+#pragma unroll
+      for (int i = 0; i < 45; ++i) sHy[i][tx] = Hy[i];
+    }
+    // ---- records (H_y from shared memory) ----
+    const int4 c4 = reinterpret_cast<const int4*>(D.act_slot + e4)[k];
+    const int codes[4] = {c4.x, c4.y, c4.z, c4.w};
+    const bool res = D.act_res[(size_t)e * D.act_cap + k] != 0;
+    int bd0 = -1, bd1 = -1;            // DoF bodies of the pair (≤2), ascending
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int cd = codes[t];
+      if (cd < 0 && cd != INT_MIN) {
+        const int d = -1 - cd;
+        if (bd0 < 0) bd0 = d;
+        else if (d != bd0) bd1 = d;
+      }
+    }
+    if (bd1 >= 0 && bd1 < bd0) { const int tmp = bd0; bd0 = bd1; bd1 = tmp; }
+    const double* axb = D.act_xb + ((size_t)e * D.act_cap + k) * 12;
+    // residual pairs: packed upper slot-space 12×12 for the matrix-free SpMV pass
+    if (res) {
+      double* Hk = aH + (size_t)k * PH;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+#pragma unroll
+        for (int t = s; t < 4; ++t)
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              if (t == s && b < r) continue;
+              double v = 0.0;          // Σ_{j,l} σ_j(s) σ_l(t) H_y[(j,r),(l,b)]
+#pragma unroll
+              for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int l = 0; l < 3; ++l) {
+                  const int sj = s == 0 ? -1 : (s == j + 1 ? 1 : 0), tl = t == 0 ? -1 : (t == l + 1 ? 1 : 0);
+                  if (sj * tl != 0) v += (double)(sj * tl) * HYS(3 * j + r, 3 * l + b);
+                }
+              Hk[sym_idx(3 * s + r, 3 * t + b, 12)] = v;
+            }
+      }
+    }
+    // body pull-back weights (non-residual pairs touch ≤ 1 DoF body)
+    double wc[3], wm[9];
+    auto weights = [&](int bd) {
+      const bool on0 = codes[0] == -1 - bd;
+      const double x00 = on0 ? axb[0] : 0.0, x01 = on0 ? axb[1] : 0.0, x02 = on0 ? axb[2] : 0.0;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        const bool on = codes[l + 1] == -1 - bd;
+        wc[l] = (on ? 1.0 : 0.0) - (on0 ? 1.0 : 0.0);
+        wm[3 * l] = (on ? axb[3 * (l + 1)] : 0.0) - x00;
+        wm[3 * l + 1] = (on ? axb[3 * (l + 1) + 1] : 0.0) - x01;
+        wm[3 * l + 2] = (on ? axb[3 * (l + 1) + 2] : 0.0) - x02;
+      }
+    };
+    if (bd0 >= 0) weights(bd0);
+    // per soft slot s, at its vertex-sorted position j: [g_s 3 | H_ss 9 | C_s 36 | H_st (≤2 soft t) 18]
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (codes[s] < 0) continue;
+      const int j = D.spos[e4 + 4 * k + s];
+      double Q[27];                    // Q[(l,b)·3 + r] = Σ_j σ_j(s) H_y[(j,r),(l,b)]  (slot-s row block)
+#pragma unroll
+      for (int lb = 0; lb < 9; ++lb)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          double q = 0.0;
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) {
+            const int sj = s == 0 ? -1 : (s == jj + 1 ? 1 : 0);
+            if (sj != 0) q += (double)sj * HYS(3 * jj + r, lb);
+          }
+          Q[3 * lb + r] = q;
+        }
+      double* rec = D.srec + ((size_t)e * 4 * D.act_cap + j) * SREC;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double gg = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          const int sj = s == 0 ? -1 : (s == jj + 1 ? 1 : 0);
+          if (sj != 0) gg += (double)sj * Gy[3 * jj + a];
+        }
+        rec[a] = gg;
+      }
+      // slot-space block H_st from Q
+      auto Hst = [&](int t, int r, int b) {
+        double v = 0.0;
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          const int tl = t == 0 ? -1 : (t == l + 1 ? 1 : 0);
+          if (tl != 0) v += (double)tl * Q[3 * (3 * l + b) + r];
+        }
+        return v;
+      };
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) rec[3 + 3 * r + b] = Hst(s, r, b);
+      // C_s = Σ_{t on bd0} H_st J_t (zero for residual pairs)
+      const bool cpl = !res && bd0 >= 0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int be = 0; be < 12; ++be) {
+          double v = 0.0;
+          if (cpl) {
+            const int rb = be < 3 ? be : (be - 3) / 3;
+#pragma unroll
+            for (int l = 0; l < 3; ++l) v += (be < 3 ? wc[l] : wm[3 * l + (be - 3) % 3]) * Q[3 * (3 * l + rb) + r];
+          }
+          rec[12 + 12 * r + be] = v;
+        }
+      // soft neighbours (the other soft slots, ascending; zero for residual pairs)
+      int nn = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t == s || codes[t] < 0 || nn >= 2) continue;
+        const int nb = nn++;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) rec[48 + 9 * nb + 3 * r + b] = res ? 0.0 : Hst(t, r, b);
+        int jb = -1;
+        if (!res) {
+          const int v = codes[s], wv = codes[t];
+          for (int q = D.rptr[v]; q < D.rptr[v + 1]; ++q)
+            if (D.rcol[q] == wv) { jb = q; break; }
+        }
+        D.snb[((size_t)e * 4 * D.act_cap + j) * 2 + nb] = jb;
+      }
+      for (int nb = nn; nb < 2; ++nb) {
+        for (int i = 0; i < 9; ++i) rec[48 + 9 * nb + i] = 0.0;
+        D.snb[((size_t)e * 4 * D.act_cap + j) * 2 + nb] = -1;
+      }
+      D.sbody[(size_t)e * 4 * D.act_cap + j] = res ? -1 : bd0;
+    }
+    // per DoF body of the pair (ascending, ≤2): packed Σ_{s,t on body} J_sᵀ H_st J_t (78) and Σ_s J_sᵀ g_s (12)
+    for (int rbi = 0; rbi < 2; ++rbi) {
+      const int bd = rbi == 0 ? bd0 : bd1;
+      if (bd < 0) break;
+      if (rbi == 1) weights(bd);
+      double* out = D.brec + (((size_t)e * D.act_cap + k) * 2 + rbi) * BREC;
+#pragma unroll
+      for (int be = 0; be < 12; ++be) {
+        const int rb = be < 3 ? be : (be - 3) / 3;
+        double zc[9];                  // zc[(j,r)] = Σ_l w_l(β) H_y[(j,r),(l,ρβ)]
+#pragma unroll
+        for (int jr = 0; jr < 9; ++jr) {
+          double z = 0.0;
+#pragma unroll
+          for (int l = 0; l < 3; ++l) z += (be < 3 ? wc[l] : wm[3 * l + (be - 3) % 3]) * HYS(jr, 3 * l + rb);
+          zc[jr] = z;
+        }
+#pragma unroll
+        for (int al = 0; al <= be; ++al) {
+          const int ra = al < 3 ? al : (al - 3) / 3;
+          double v = 0.0;
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * zc[3 * jj + ra];
+          out[sym_idx(al, be, 12)] = v;
+        }
+      }
+#pragma unroll
+      for (int al = 0; al < 12; ++al) {
+        const int ra = al < 3 ? al : (al - 3) / 3;
+        double v = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * Gy[3 * jj + ra];
+        out[PH + al] = v;
+      }
+    }
+  }
+#undef HYS
+}
+
 
 // ------------------------------------------------------------------------------------------
 // assembly: gradient g, soft BSR (diag + edge blocks), body 12×12 blocks, block-Jacobi inverses
@@ -2151,8 +2559,16 @@ void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   if (D.T > 0) k_tets<<<grid, NTHREADS, 0, s>>>(D, env0, force);
 }
 void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  dim3 grid(std::min((D.act_cap + PAIRS_PER_CTA - 1) / PAIRS_PER_CTA, PAIR_GRID_X), ne);
-  k_pairs<<<grid, PAIR_WARPS * 32, 0, s>>>(D, env0, force);
+  // hessian_mode 2 (R14c) keeps every env on exact Hessians; modes 0/1 (and debug evaluations,
+  // force = 1) may hold projected envs, which the warp-Jacobi kernel serves
+  if (D.hmode != 2 || force) {
+    dim3 grid(std::min((D.act_cap + PAIRS_PER_CTA - 1) / PAIRS_PER_CTA, PAIR_GRID_X), ne);
+    k_pairs<<<grid, PAIR_WARPS * 32, 0, s>>>(D, env0, force);
+  }
+  if (D.hmode != 0 || force) {
+    dim3 grid(std::min((D.act_cap + 127) / 128, 8), ne);
+    k_pairs_x<<<grid, 128, 0, s>>>(D, env0, force);
+  }
 }
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   const int bytes = (D.V + 2) * (int)sizeof(int);
