@@ -22,6 +22,7 @@ constexpr int TETBUF = 90;         // 12 gradient + 78 packed Hessian
 constexpr int PH = 78;
 constexpr int SREC = 66;          // per soft slot record: g 3 | H_ss 9 | coupling 36 | soft neighbours 18
 constexpr int BREC = 90;          // per (pair, body) record: packed JᵀHJ 78 | Jᵀg 12
+constexpr int BPART = 12 + 2 * PH; // per (32-pair chunk, body) partial: Jᵀg 12 | condensed JᵀHJ 78 | residual JᵀHJ 78
 
 enum { PHASE_ACTIVE = 0, PHASE_DONE = 1, PHASE_FAILED = 2, PHASE_IDLE = 3 };
 enum { ENV_OK = 0, ENV_NEWTON_STALL = 1, ENV_AL_INFEASIBLE = 2, ENV_CAPACITY = 3, ENV_NONFINITE = 4,
@@ -71,6 +72,7 @@ struct Dev {
   const int* eblk;        // entries 16*tet + 4*a + b (local a ↔ edge.i, b ↔ edge.j)
   const int* rptr;        // [V+1] row-ordered symmetric BSR
   const int* rcol;        // [NNZ] column (neighbour vertex)
+  const int* rupx;        // [NNZ] 2·(soft edge id) + 1 if the block is the transpose of the edge's upper block
   const int* rblk_ptr;    // [NNZ+1]
   const int* rblk;        // entries 16*tet + 4*a + b (a ↔ row, b ↔ column)
   const int* body_kind;   // [NA]
@@ -155,7 +157,8 @@ struct Dev {
   double* srec;           // [E][4*act_cap][SREC] per soft slot, vertex-sorted position (k_pairs)
   int* snb;               // [E][4*act_cap][2] BSR block of each soft neighbour record (-1 none)
   int* sbody;             // [E][4*act_cap] DoF body of the coupling record (-1 none / residual)
-  double* brec;           // [E][act_cap][2][BREC] per (pair, DoF body) records (k_pairs)
+  double* brec;           // [E][act_cap][2][BREC] per (pair, DoF body) records (k_pairs, projected envs)
+  double* bpart;          // [E][ceil(act_cap/32)][ND][BPART] per 32-pair chunk body partial sums
   int* cptr;              // [E][V+1] soft contribution lists
   int* clist;             // [E][4*act_cap]
   int* bptr;              // [E][ND+1] body contribution lists

@@ -929,6 +929,45 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
   }
 }
 
+// chunk partials of the body records for projected envs (k_pairs writes per-pair records brec):
+// partial[chunk][d] = Σ over the chunk's 32 pairs in pair order (same layout as k_pairs_x)
+__global__ void k_bpart_proj(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.y;
+  if (env_skip(D, e, force)) return;
+  const EnvCtl& C = D.ctl[e];
+  if (C.exact) return;
+  const int nact = C.n_act, k0 = 32 * blockIdx.x;
+  if (k0 >= nact) return;
+  const int k1 = min(k0 + 32, nact);
+  const size_t nchunk = (size_t)(D.act_cap + 31) >> 5;
+  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
+  const int* ares = D.act_res + (size_t)e * D.act_cap;
+  for (int t = threadIdx.x; t < D.ND * BPART; t += blockDim.x) {
+    const int d = t / BPART, i = t % BPART;
+    double sum = 0.0;
+    for (int k = k0; k < k1; ++k) {
+      int bd0 = -1, bd1 = -1;
+      for (int s = 0; s < 4; ++s) {
+        const int cd = aslot[4 * k + s];
+        if (cd < 0 && cd != INT_MIN) {
+          const int dd = -1 - cd;
+          if (bd0 < 0) bd0 = dd;
+          else if (dd != bd0) bd1 = dd;
+        }
+      }
+      if (bd1 >= 0 && bd1 < bd0) { const int tmp = bd0; bd0 = bd1; bd1 = tmp; }
+      const int rb = bd0 == d ? 0 : (bd1 == d ? 1 : -1);
+      if (rb < 0) continue;
+      const double* rec = D.brec + (((size_t)e * D.act_cap + k) * 2 + rb) * BREC;
+      const bool res = ares[k] != 0;
+      if (i < 12) sum += rec[PH + i];
+      else if (i < 12 + PH) { if (!res) sum += rec[i - 12]; }
+      else if (res) sum += rec[i - 12 - PH];
+    }
+    D.bpart[(((size_t)e * nchunk + blockIdx.x) * D.ND + d) * BPART + i] = sum;
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // barrier pairs, exact Hessian (hessian_mode ≥ 1 with C.exact; the LM default R14c): ONE THREAD
 // PER PAIR, everything in registers.  Every sub-distance variable (w, e1, e2; and the EE mollifier's
@@ -1048,8 +1087,31 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
   __shared__ double sHy[45][128];                         // H_y of this thread's pair (records phase)
   const int tx = threadIdx.x;
 #define HYS(r, c) ((r) <= (c) ? sHy[s9(r, c)][tx] : sHy[s9(c, r)][tx])
-  for (int k = blockIdx.x * blockDim.x + tx; k < nact; k += gridDim.x * blockDim.x) {
+  const int lane = tx & 31;
+  const size_t nchunk = (size_t)(D.act_cap + 31) >> 5;
+  // warp-uniform sweep: lane l of a warp takes pair kb + l (the warp's 32-pair chunk kb/32)
+  for (int kb = blockIdx.x * blockDim.x + (tx & ~31); kb < nact; kb += gridDim.x * blockDim.x) {
+    const int k = kb + lane;
+    const bool live = k < nact;
     double Gy[9];
+    int codes[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+    bool res = false;
+    int bd0 = -1, bd1 = -1;            // DoF bodies of the pair (≤2), ascending
+    const double* axb = D.act_xb + ((size_t)e * D.act_cap + (live ? k : 0)) * 12;
+    double wc[3], wm[9];               // body pull-back weights (non-residual pairs touch ≤ 1 DoF body)
+    auto weights = [&](int bd) {
+      const bool on0 = codes[0] == -1 - bd;
+      const double x00 = on0 ? axb[0] : 0.0, x01 = on0 ? axb[1] : 0.0, x02 = on0 ? axb[2] : 0.0;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        const bool on = codes[l + 1] == -1 - bd;
+        wc[l] = (on ? 1.0 : 0.0) - (on0 ? 1.0 : 0.0);
+        wm[3 * l] = (on ? axb[3 * (l + 1)] : 0.0) - x00;
+        wm[3 * l + 1] = (on ? axb[3 * (l + 1) + 1] : 0.0) - x01;
+        wm[3 * l + 2] = (on ? axb[3 * (l + 1) + 2] : 0.0) - x02;
+      }
+    };
+    if (live) {
     {
       const int4 inf = reinterpret_cast<const int4*>(info)[k];
       const int kind = inf.x, type = inf.y, pa = inf.z, pb = inf.w;
@@ -1162,9 +1224,8 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
     }
     // ---- records (H_y from shared memory) ----
     const int4 c4 = reinterpret_cast<const int4*>(D.act_slot + e4)[k];
-    const int codes[4] = {c4.x, c4.y, c4.z, c4.w};
-    const bool res = D.act_res[(size_t)e * D.act_cap + k] != 0;
-    int bd0 = -1, bd1 = -1;            // DoF bodies of the pair (≤2), ascending
+    codes[0] = c4.x; codes[1] = c4.y; codes[2] = c4.z; codes[3] = c4.w;
+    res = D.act_res[(size_t)e * D.act_cap + k] != 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int cd = codes[t];
@@ -1175,7 +1236,6 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
       }
     }
     if (bd1 >= 0 && bd1 < bd0) { const int tmp = bd0; bd0 = bd1; bd1 = tmp; }
-    const double* axb = D.act_xb + ((size_t)e * D.act_cap + k) * 12;
     // residual pairs: packed upper slot-space 12×12 for the matrix-free SpMV pass
     if (res) {
       double* Hk = aH + (size_t)k * PH;
@@ -1200,20 +1260,6 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
             }
       }
     }
-    // body pull-back weights (non-residual pairs touch ≤ 1 DoF body)
-    double wc[3], wm[9];
-    auto weights = [&](int bd) {
-      const bool on0 = codes[0] == -1 - bd;
-      const double x00 = on0 ? axb[0] : 0.0, x01 = on0 ? axb[1] : 0.0, x02 = on0 ? axb[2] : 0.0;
-#pragma unroll
-      for (int l = 0; l < 3; ++l) {
-        const bool on = codes[l + 1] == -1 - bd;
-        wc[l] = (on ? 1.0 : 0.0) - (on0 ? 1.0 : 0.0);
-        wm[3 * l] = (on ? axb[3 * (l + 1)] : 0.0) - x00;
-        wm[3 * l + 1] = (on ? axb[3 * (l + 1) + 1] : 0.0) - x01;
-        wm[3 * l + 2] = (on ? axb[3 * (l + 1) + 2] : 0.0) - x02;
-      }
-    };
     if (bd0 >= 0) weights(bd0);
     // per soft slot s, at its vertex-sorted position j: [g_s 3 | H_ss 9 | C_s 36 | H_st (≤2 soft t) 18]
 #pragma unroll
@@ -1296,12 +1342,36 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
       }
       D.sbody[(size_t)e * 4 * D.act_cap + j] = res ? -1 : bd0;
     }
-    // per DoF body of the pair (ascending, ≤2): packed Σ_{s,t on body} J_sᵀ H_st J_t (78) and Σ_s J_sᵀ g_s (12)
-    for (int rbi = 0; rbi < 2; ++rbi) {
-      const int bd = rbi == 0 ? bd0 : bd1;
-      if (bd < 0) break;
-      if (rbi == 1) weights(bd);
-      double* out = D.brec + (((size_t)e * D.act_cap + k) * 2 + rbi) * BREC;
+    }  // live
+    // per (32-pair chunk, DoF body) partial sums of the body records, deterministic warp trees:
+    // [Σ J_sᵀ g_s 12 | condensed packed Σ J_sᵀ H_st J_t 78 | residual-pair packed 78] (k_assemble sums
+    // the chunks of a body in chunk order)
+    const size_t chunk = (size_t)kb >> 5;
+    for (int d = 0; d < D.ND; ++d) {
+      const bool mine = bd0 == d || bd1 == d;
+      double* out = D.bpart + (((size_t)e * nchunk + chunk) * D.ND + d) * BPART;
+      if (__ballot_sync(0xffffffffu, mine) == 0u) {
+        for (int i = lane; i < BPART; i += 32) out[i] = 0.0;
+        continue;
+      }
+      const bool anyres = __ballot_sync(0xffffffffu, mine && res) != 0u;
+      if (mine) weights(d);
+      else {
+#pragma unroll
+        for (int l = 0; l < 3; ++l) wc[l] = 0.0;
+#pragma unroll
+        for (int l = 0; l < 9; ++l) wm[l] = 0.0;
+      }
+#pragma unroll
+      for (int al = 0; al < 12; ++al) {
+        const int ra = al < 3 ? al : (al - 3) / 3;
+        double v = 0.0;
+        if (mine)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * Gy[3 * jj + ra];
+        v = warp_sum(v);
+        if (lane == al) out[al] = v;
+      }
 #pragma unroll
       for (int be = 0; be < 12; ++be) {
         const int rb = be < 3 ? be : (be - 3) / 3;
@@ -1309,8 +1379,9 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
 #pragma unroll
         for (int jr = 0; jr < 9; ++jr) {
           double z = 0.0;
+          if (mine)
 #pragma unroll
-          for (int l = 0; l < 3; ++l) z += (be < 3 ? wc[l] : wm[3 * l + (be - 3) % 3]) * HYS(jr, 3 * l + rb);
+            for (int l = 0; l < 3; ++l) z += (be < 3 ? wc[l] : wm[3 * l + (be - 3) % 3]) * HYS(jr, 3 * l + rb);
           zc[jr] = z;
         }
 #pragma unroll
@@ -1319,17 +1390,17 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
           double v = 0.0;
 #pragma unroll
           for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * zc[3 * jj + ra];
-          out[sym_idx(al, be, 12)] = v;
+          const int idx = sym_idx(al, be, 12);
+          const double vc = warp_sum(res ? 0.0 : v);
+          if (lane == (idx & 31)) out[12 + idx] = vc;
+          if (anyres) {
+            const double vr = warp_sum(res ? v : 0.0);
+            if (lane == (idx & 31)) out[12 + PH + idx] = vr;
+          }
         }
       }
-#pragma unroll
-      for (int al = 0; al < 12; ++al) {
-        const int ra = al < 3 ? al : (al - 3) / 3;
-        double v = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * Gy[3 * jj + ra];
-        out[PH + al] = v;
-      }
+      if (!anyres)
+        for (int i = lane; i < PH; i += 32) out[12 + PH + i] = 0.0;
     }
   }
 #undef HYS
@@ -1396,7 +1467,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ JacobiScratch JS[NTHREADS / 32];
-  __shared__ double PB[NTHREADS / 32][144];
   __shared__ int shs[33];
   extern __shared__ double dsm_asm[];   // contact-vertex list [V] ints
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1620,60 +1690,47 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
     if (lane < 12) g[3 * D.V + 12 * d + lane] = gb;      // pair terms added below
   }
   __syncthreads();
-  // pair contributions to each body's gradient and diagonal block: all warps split the body's
-  // contribution list (warp w takes entries w, w+nw, ...), partials summed in warp order.  Pass 0
-  // folds the condensed (non-residual) pairs into Hb (the SpMV's body block); pass 1 adds the
-  // residual pairs, which the SpMV applies matrix-free, for the preconditioner block only
-  __shared__ double GB[NTHREADS / 32][12];
+  // pair contributions to each body's gradient and diagonal block, from the per-chunk partials
+  // (k_pairs_x / k_bpart_proj) summed in chunk order: the condensed pairs go into Hb (the SpMV's body
+  // block), the residual pairs (applied matrix-free by the SpMV) only into the preconditioner block
   CLK(12)
-  for (int d = 0; d < D.ND; ++d) {
-    double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
-    double* T = JS[d % nw].A;            // running total block of body d
-    for (int pass = 0; pass < (C.n_res > 0 ? 2 : 1); ++pass) {
-      double acc[5] = {0, 0, 0, 0, 0};   // entries i = lane + 32·t of the 144
-      double gacc = 0.0;
-      const double* brec = D.brec + (size_t)e * D.act_cap * 2 * BREC;
+  {
+    const int nch = (C.n_act + 31) >> 5;
+    const size_t nchunk = (size_t)(D.act_cap + 31) >> 5;
+    const double* bp = D.bpart + (size_t)e * nchunk * D.ND * BPART;
+    for (int t = threadIdx.x; t < D.ND * 156; t += blockDim.x) {
+      const int d = t / 156, i = t % 156;
+      if (i < 144) {
+        const int si = sym_idx(i / 12, i % 12, 12);
+        double sc = 0.0, sr = 0.0;
 #pragma unroll 4
-      for (int j = bptr[d] + w; j < bptr[d + 1]; j += nw) {
-        const int k = blist[j] >> 1, rb = blist[j] & 1;
-        const double* rec = brec + ((size_t)k * 2 + rb) * BREC;
-        if (pass == 0 && lane < 12) gacc += rec[PH + lane];
-        if ((ares[k] != 0) != (pass == 1)) continue;
-#pragma unroll
-        for (int tt = 0; tt < 5; ++tt) {
-          const int i = lane + 32 * tt;
-          if (i < 144) acc[tt] += rec[sym_idx(i / 12, i % 12, 12)];
+        for (int ch = 0; ch < nch; ++ch) {
+          const double* qq = bp + ((size_t)ch * D.ND + d) * BPART;
+          sc += qq[12 + si];
+          sr += qq[12 + PH + si];
         }
+        double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144;
+        const double hv = Hb[i] + sc;
+        Hb[i] = hv;
+        D.Dg_b[((size_t)e * D.ND + d) * 144 + i] = hv + sr;
+      } else {
+        const int a = i - 144;
+        double sg = 0.0;
+#pragma unroll 4
+        for (int ch = 0; ch < nch; ++ch) sg += bp[((size_t)ch * D.ND + d) * BPART + a];
+        g[3 * D.V + 12 * d + a] += sg;
       }
-#pragma unroll
-      for (int tt = 0; tt < 5; ++tt)
-        if (lane + 32 * tt < 144) PB[w][lane + 32 * tt] = acc[tt];
-      if (pass == 0 && lane < 12) GB[w][lane] = gacc;
-      __syncthreads();
-      if (w == d % nw) {
-        for (int i = lane; i < 144; i += 32) {
-          double v = pass == 0 ? Hb[i] : T[i];
-          for (int ww = 0; ww < nw; ++ww) v += PB[ww][i];
-          T[i] = v;
-          if (pass == 0) Hb[i] = v;
-        }
-        if (pass == 0 && lane < 12) {
-          double v = g[3 * D.V + 12 * d + lane];
-          for (int ww = 0; ww < nw; ++ww) v += GB[ww][lane];
-          g[3 * D.V + 12 * d + lane] = v;
-        }
-      }
-      __syncthreads();
     }
-    if (w == d % nw) {
-      double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
-      const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
-      for (int i = lane; i < 144; i += 32) { Db[i] = T[i]; T[i] += C.mu * Mb[i]; }
-      __syncwarp();
-      if (lane == 0) chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q);
-      __syncwarp();
-    }
-    __syncthreads();
+  }
+  __syncthreads();
+  for (int d = w; d < D.ND; d += nw) {
+    double* T = JS[w].A;
+    const double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
+    const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
+    for (int i = lane; i < 144; i += 32) T[i] = Db[i] + C.mu * Mb[i];
+    __syncwarp();
+    if (lane == 0) chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q);
+    __syncwarp();
   }
   CLK(13)
   if (threadIdx.x == 0) CLKN(14)
@@ -1689,8 +1746,17 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
 // in a fixed order into per-warp partials part[w][d][12].  Pass A2: couplings (one per lane):
 // C_vd x_d → cpl_out[c], C_vdᵀ x_v → part.  Pass B: soft rows (BSR + diagonal + contiguous sout
 // and cpl_out ranges) and body rows (Hb x_b + Σ_w part[w][d]).  Deterministic for a fixed blockDim.
+// env-resident copy of the condensed soft matrix in shared memory (k_pcg_r): upper edge blocks U
+// (one per soft edge; the lower block is its transpose), SoA diagonal blocks, body blocks, the
+// block-Jacobi inverses and the row/contribution index arrays
+struct SmemMat {
+  const double *U, *Hd, *Hb, *Ps, *Pb;
+  double* cout;                                   // [3·ncpl] coupling outputs C_vd x_d (pass A2 → B)
+  const int *rptr, *rcol, *rupx, *cptr, *rcnt, *cpp;
+};
+
 __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
-                     double mu = 0.0) {
+                     double mu = 0.0, const SmemMat* R = nullptr) {
   const EnvCtl& C = D.ctl[e];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
@@ -1775,7 +1841,7 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
     const int* cplv = D.cpl_v + (size_t)e * D.cpl_cap;
     const int* cpld = D.cpl_d + (size_t)e * D.cpl_cap;
     const double* cval = D.cpl_val + (size_t)e * 36 * D.cpl_cap;
-    double* cout = D.cpl_out + (size_t)e * 3 * D.cpl_cap;
+    double* cout = R ? R->cout : D.cpl_out + (size_t)e * 3 * D.cpl_cap;
     const size_t ccap = D.cpl_cap;
     for (int base = 32 * w; base < ncpl; base += blockDim.x) {
       const int c = base + lane;
@@ -1813,12 +1879,13 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
   CLK(1)
   __syncthreads();
   CLK(2)
-  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
-  const int* rcnt = D.rcnt + (size_t)e * D.V;
-  const int* cpp = D.cpl_ptr + (size_t)e * (D.V + 1);
-  const double* cout = D.cpl_out + (size_t)e * 3 * D.cpl_cap;
-  const double* Hd = D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
+  const int* cptr = R ? R->cptr : D.cptr + (size_t)e * (D.V + 1);
+  const int* rcnt = R ? R->rcnt : D.rcnt + (size_t)e * D.V;
+  const int* cpp = R ? R->cpp : D.cpl_ptr + (size_t)e * (D.V + 1);
+  const double* cout = R ? R->cout : D.cpl_out + (size_t)e * 3 * D.cpl_cap;
+  const double* Hd = R ? R->Hd : D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
   const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
+  const int* rptr = R ? R->rptr : D.rptr;
   // soft rows: 4 lanes per row; lane q of the group takes blocks j = rptr[v]+q, +4, ... (adjacent
   // lanes read adjacent 72-byte blocks), then a 2-step shuffle reduction; lane q==0 adds the
   // diagonal block and the contiguous pair outputs and stores
@@ -1830,8 +1897,17 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
       const bool live = v < D.V;
       v3 acc = mk(0, 0, 0);
       if (live) {
-        const int j1 = D.rptr[v + 1];
-        for (int j = D.rptr[v] + q; j < j1; j += 4) acc += mul33(Ho + 9 * j, ld3(x + 3 * D.rcol[j]));
+        const int j1 = rptr[v + 1];
+        if (R) {
+          for (int j = rptr[v] + q; j < j1; j += 4) {
+            const int ux = R->rupx[j];
+            const double* Bk = R->U + 9 * (ux >> 1);
+            const v3 xu = ld3(x + 3 * R->rcol[j]);
+            acc += (ux & 1) ? mul33T(Bk, xu) : mul33(Bk, xu);
+          }
+        } else {
+          for (int j = rptr[v] + q; j < j1; j += 4) acc += mul33(Ho + 9 * j, ld3(x + 3 * D.rcol[j]));
+        }
       }
       for (int o = 1; o < 4; o <<= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -1854,7 +1930,7 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
   CLK(3)
   for (int i = threadIdx.x; i < nb12; i += blockDim.x) {
     const int d = i / 12, row = i % 12;
-    const double* Hb = D.Hb + ((size_t)e * D.ND + d) * 144 + 12 * row;
+    const double* Hb = (R ? R->Hb + (size_t)d * 144 : D.Hb + ((size_t)e * D.ND + d) * 144) + 12 * row;
     const double* xb = x + 3 * D.V + 12 * d;
     double sacc = 0.0;
     for (int c = 0; c < 12; ++c) sacc += Hb[c] * xb[c];
@@ -1892,8 +1968,8 @@ __device__ void reinvert_precond(const Dev& D, int e, double mu, double* scratch
   __syncthreads();
 }
 
-__device__ void precond(const Dev& D, int e, const double* r, double* z) {
-  const double* Ps = D.Pinv_s + (size_t)e * D.V * 9;    // SoA [9][V]
+__device__ void precond(const Dev& D, int e, const double* r, double* z, const SmemMat* R = nullptr) {
+  const double* Ps = R ? R->Ps : D.Pinv_s + (size_t)e * D.V * 9;    // SoA [9][V]
   const size_t V = D.V;
   for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
     const v3 rv = ld3(r + 3 * v);
@@ -1903,7 +1979,7 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z) {
   }
   for (int i = threadIdx.x; i < 12 * D.ND; i += blockDim.x) {
     int d = i / 12, row = i % 12;
-    const double* Pi = D.Pinv_b + ((size_t)e * D.ND + d) * 144 + 12 * row;
+    const double* Pi = (R ? R->Pb + (size_t)d * 144 : D.Pinv_b + ((size_t)e * D.ND + d) * 144) + 12 * row;
     const double* rb = r + 3 * D.V + 12 * d;
     double s = 0.0;
     for (int c = 0; c < 12; ++c) s += Pi[c] * rb[c];
@@ -1917,11 +1993,78 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z) {
 // Newton convergence test ‖p‖_emb,∞ ≤ τ_N L_env and gᵀp.
 // ------------------------------------------------------------------------------------------
 // vsm = 1: the five PCG vectors live in shared memory (n small enough), p is copied out at the end
+__device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb);
+
 __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force, int vsm) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
   extern __shared__ double dsmem[];     // [nw][ND][12] body partials, then (vsm) p, r, z, d, Ad
+  pcg_body(D, e, vsm, dsmem, red, nullptr, nullptr, nullptr);
+}
+
+// shared-memory bytes of k_pcg_r for this batch (0 if the env does not fit one CTA)
+constexpr int PCG_R_THREADS = 512;
+__host__ __device__ inline size_t pcg_r_ncpl(const Dev& D) {          // coupling bound: ≤ 1 per (v, d)
+  const size_t a = (size_t)D.V * D.ND, b = (size_t)D.cpl_cap;
+  return a < b ? a : b;
+}
+__host__ __device__ inline size_t pcg_r_bytes(const Dev& D) {
+  const size_t nd = (size_t)(PCG_R_THREADS / 32) * D.ND * 12 + 1 + 5 * (size_t)D.n + 9 * (size_t)D.NEs +
+                    18 * (size_t)D.V + 288 * (size_t)D.ND + 3 * pcg_r_ncpl(D);
+  const size_t ni = 3 * ((size_t)D.V + 1) + (size_t)D.V + 2 * (size_t)D.NNZ;
+  return nd * sizeof(double) + ni * sizeof(int);
+}
+
+// env-resident PCG: one CTA (512 threads) per env with the condensed soft matrix, diagonal and body
+// blocks, preconditioner and index arrays staged once into shared memory; only the (few) residual
+// pairs and the soft–body couplings are read from global memory per iteration
+__global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.x;
+  if (env_skip(D, e, force)) return;
+  __shared__ double red[32];
+  extern __shared__ double dsmem[];
+  const int V = D.V, ND = D.ND, n = D.n, NNZ = D.NNZ;
+  double* base = dsmem + ((PCG_R_THREADS / 32) * ND * 12 + 1) + 5 * (size_t)n;   // after bpart + vectors
+  double* U = base;
+  double* Hd = U + 9 * (size_t)D.NEs;
+  double* Ps = Hd + 9 * (size_t)V;
+  double* Pb = Ps + 9 * (size_t)V;
+  double* Hb = Pb + 144 * (size_t)ND;
+  double* couts = Hb + 144 * (size_t)ND;
+  int* rptr = reinterpret_cast<int*>(couts + 3 * pcg_r_ncpl(D));
+  int* cptr = rptr + V + 1;
+  int* cpp = cptr + V + 1;
+  int* rcnt = cpp + V + 1;
+  int* rcol = rcnt + V;
+  int* rupx = rcol + NNZ;
+  const double* Ho = D.Ho + (size_t)e * NNZ * 9;
+  for (int j = threadIdx.x; j < NNZ; j += blockDim.x) { rcol[j] = D.rcol[j]; rupx[j] = D.rupx[j]; }
+  for (int v = threadIdx.x; v <= V; v += blockDim.x) {
+    rptr[v] = D.rptr[v];
+    cptr[v] = D.cptr[(size_t)e * (V + 1) + v];
+    cpp[v] = D.cpl_ptr[(size_t)e * (V + 1) + v];
+    if (v < V) rcnt[v] = D.rcnt[(size_t)e * V + v];
+  }
+  for (int i = threadIdx.x; i < 9 * V; i += blockDim.x) {
+    Hd[i] = D.Hd[(size_t)e * V * 9 + i];
+    Ps[i] = D.Pinv_s[(size_t)e * V * 9 + i];
+  }
+  for (int i = threadIdx.x; i < 144 * ND; i += blockDim.x) {
+    Pb[i] = D.Pinv_b[(size_t)e * ND * 144 + i];
+    Hb[i] = D.Hb[(size_t)e * ND * 144 + i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 9 * NNZ; i += blockDim.x) {   // upper edge blocks (coalesced read of Ho)
+    const int ux = rupx[i / 9];
+    if (!(ux & 1)) U[9 * (ux >> 1) + i % 9] = Ho[i];
+  }
+  __syncthreads();
+  SmemMat R{U, Hd, Hb, Ps, Pb, couts, rptr, rcol, rupx, cptr, rcnt, cpp};
+  pcg_body(D, e, 1, dsmem, red, &R, Ps, Pb);
+}
+
+__device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb) {
   double* bpart = dsmem;
   EnvCtl& C = D.ctl[e];
   const int n = D.n;
@@ -1929,7 +2072,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force,
   double* const p_out = D.p + (size_t)e * n;
   double *p, *r, *z, *d, *Ad;
   if (vsm) {
-    double* base = dsmem + ((NTHREADS / 32) * D.ND * 12 + 1);
+    double* base = dsmem + ((blockDim.x / 32) * D.ND * 12 + 1);
     p = base; r = base + n; z = base + 2 * n; d = base + 3 * n; Ad = base + 4 * n;
   } else {
     p = p_out; r = D.r + (size_t)e * n; z = D.z + (size_t)e * n; d = D.dd + (size_t)e * n; Ad = D.Ad + (size_t)e * n;
@@ -1943,10 +2086,17 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force,
   bool zero_g = false;
   __shared__ double chol_scratch[144], chol_T[144];
   for (int attempt = 0;; ++attempt) {
-    if (attempt > 0) reinvert_precond(D, e, mu, chol_scratch, chol_T);
+    if (attempt > 0) {
+      reinvert_precond(D, e, mu, chol_scratch, chol_T);
+      if (R) {                                            // refresh the resident inverses
+        for (int i = threadIdx.x; i < 9 * D.V; i += blockDim.x) Rw_Ps[i] = D.Pinv_s[(size_t)e * D.V * 9 + i];
+        for (int i = threadIdx.x; i < 144 * D.ND; i += blockDim.x) Rw_Pb[i] = D.Pinv_b[(size_t)e * D.ND * 144 + i];
+        __syncthreads();
+      }
+    }
     for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
     __syncthreads();
-    precond(D, e, r, z);
+    precond(D, e, r, z, R);
     double part = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) { d[i] = z[i]; part += r[i] * z[i]; }
     double rz = block_sum(part, red);
@@ -1955,7 +2105,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force,
     int it = 0;
     bad = !(rz0 == rz0);
     while (!bad && it < D.max_pcg && rz > stop) {
-      spmv(D, e, d, Ad, bpart, mu);
+      spmv(D, e, d, Ad, bpart, mu, R);
       CLK_INIT
       part = 0.0;
       for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
@@ -1966,7 +2116,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force,
       for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] += alpha * d[i]; r[i] -= alpha * Ad[i]; }
       __syncthreads();
       CLK(6)
-      precond(D, e, r, z);
+      precond(D, e, r, z, R);
       CLK(7)
       part = 0.0;
       for (int i = threadIdx.x; i < n; i += blockDim.x) part += r[i] * z[i];
@@ -2564,6 +2714,7 @@ void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   if (D.hmode != 2 || force) {
     dim3 grid(std::min((D.act_cap + PAIRS_PER_CTA - 1) / PAIRS_PER_CTA, PAIR_GRID_X), ne);
     k_pairs<<<grid, PAIR_WARPS * 32, 0, s>>>(D, env0, force);
+    k_bpart_proj<<<dim3((D.act_cap + 31) / 32, ne), 256, 0, s>>>(D, env0, force);
   }
   if (D.hmode != 0 || force) {
     dim3 grid(std::min((D.act_cap + 127) / 128, 8), ne);
@@ -2585,6 +2736,13 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   if (bytes > 48 * 1024 && bytes > configured) {
     cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     configured = bytes;
+  }
+  const size_t rb = pcg_r_bytes(D);
+  if (rb <= 227 * 1024) {                                 // env-resident PCG (one CTA per SM)
+    static size_t rconf = 0;
+    if (rb > rconf) { cudaFuncSetAttribute(k_pcg_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb); rconf = rb; }
+    k_pcg_r<<<ne, PCG_R_THREADS, rb, s>>>(D, env0, force);
+    return;
   }
   k_pcg<<<ne, NTHREADS, bytes, s>>>(D, env0, force, vsm);
 }
