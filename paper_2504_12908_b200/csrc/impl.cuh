@@ -131,6 +131,7 @@ struct Dev {
   int *cand_a, *cand_b;   // [E][cand_cap] (cand_a bit 30 = EE)
   int* ent;               // [E][ent_cap][2]
   int* big;               // [E][BIG_CAP]
+  int* qcnt;              // [E][NSV+NE] broad-phase query counts → segment offsets
   double* tbox;           // [E][NT+NE][6] raw target boxes (broad-phase cache)
   double* vref;           // [E][NSV][6] reference boxes of surface vertices at the last build
   int* act_info;          // [E][act_cap][4] (kind, type, a, b)

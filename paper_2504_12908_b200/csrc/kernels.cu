@@ -405,17 +405,26 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   }
   __syncthreads();
   const int nbig = min(nbig_s, BIG_CAP);
-  // queries: PT (surface vertices) then EE (edges), tile by tile, count → scan → emit → sort
+  // queries: PT (surface vertices) then EE (edges).  Count every query (no per-tile barrier), one
+  // block scan over the counts in query order, then emit each query's segment and sort it by target
   int* ca = D.cand_a + (size_t)e * D.cand_cap;
   int* cb = D.cand_b + (size_t)e * D.cand_cap;
   const int nq = D.NSV + D.NE;
-  int total = 0;
-  for (int t0 = 0; t0 < nq; t0 += blockDim.x) {
-    int qi = t0 + threadIdx.x;
-    int c = (qi < nq) ? bp_query<false>(D, B, G, cnt, ent, big, nbig, qi, nullptr, nullptr, bb) : 0;
-    int tot;
-    int ex = block_excl_scan(c, sh, &tot);
-    int base = total + ex;
+  int* qc = D.qcnt + (size_t)e * (D.NSV + D.NE);
+  for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) qc[qi] = bp_query<false>(D, B, G, cnt, ent, big, nbig, qi, nullptr, nullptr, bb);
+  __syncthreads();
+  int total;
+  {
+    const int per = (nq + blockDim.x - 1) / blockDim.x;
+    const int q0 = min((int)threadIdx.x * per, nq), q1 = min(q0 + per, nq);
+    int sum = 0;
+    for (int q = q0; q < q1; ++q) sum += qc[q];
+    int ex = block_excl_scan(sum, sh, &total);
+    for (int q = q0; q < q1; ++q) { const int c = qc[q]; qc[q] = ex; ex += c; }
+  }
+  __syncthreads();
+  for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) {
+    const int base = qc[qi], c = (qi + 1 < nq ? qc[qi + 1] : total) - base;
     if (c > 0 && base + c <= D.cand_cap) {
       bp_query<true>(D, B, G, cnt, ent, big, nbig, qi, ca + base, cb + base, bb);
       // insertion sort of this query's segment by target index
@@ -426,7 +435,6 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
         cb[base + j + 1] = kb; ca[base + j + 1] = ka;
       }
     }
-    total += tot;
   }
   if (threadIdx.x == 0) {
     C.ncand = min(total, D.cand_cap);
@@ -1262,9 +1270,13 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
     }
     if (bd0 >= 0) weights(bd0);
     // per soft slot s, at its vertex-sorted position j: [g_s 3 | H_ss 9 | C_s 36 | H_st (≤2 soft t) 18]
-#pragma unroll
+    auto csel = [&](int t) { return t == 0 ? codes[0] : (t == 1 ? codes[1] : (t == 2 ? codes[2] : codes[3])); };
+#pragma unroll 1
     for (int s = 0; s < 4; ++s) {
-      if (codes[s] < 0) continue;
+      const int cs = csel(s);
+      if (cs < 0) continue;
+      const double sg[3] = {s == 0 ? -1.0 : (s == 1 ? 1.0 : 0.0), s == 0 ? -1.0 : (s == 2 ? 1.0 : 0.0),
+                            s == 0 ? -1.0 : (s == 3 ? 1.0 : 0.0)};
       const int j = D.spos[e4 + 4 * k + s];
       double Q[27];                    // Q[(l,b)·3 + r] = Σ_j σ_j(s) H_y[(j,r),(l,b)]  (slot-s row block)
 #pragma unroll
@@ -1273,10 +1285,7 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
         for (int r = 0; r < 3; ++r) {
           double q = 0.0;
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj) {
-            const int sj = s == 0 ? -1 : (s == jj + 1 ? 1 : 0);
-            if (sj != 0) q += (double)sj * HYS(3 * jj + r, lb);
-          }
+          for (int jj = 0; jj < 3; ++jj) q += sg[jj] * HYS(3 * jj + r, lb);
           Q[3 * lb + r] = q;
         }
       double* rec = D.srec + ((size_t)e * 4 * D.act_cap + j) * SREC;
@@ -1284,20 +1293,14 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
       for (int a = 0; a < 3; ++a) {
         double gg = 0.0;
 #pragma unroll
-        for (int jj = 0; jj < 3; ++jj) {
-          const int sj = s == 0 ? -1 : (s == jj + 1 ? 1 : 0);
-          if (sj != 0) gg += (double)sj * Gy[3 * jj + a];
-        }
+        for (int jj = 0; jj < 3; ++jj) gg += sg[jj] * Gy[3 * jj + a];
         rec[a] = gg;
       }
       // slot-space block H_st from Q
       auto Hst = [&](int t, int r, int b) {
         double v = 0.0;
 #pragma unroll
-        for (int l = 0; l < 3; ++l) {
-          const int tl = t == 0 ? -1 : (t == l + 1 ? 1 : 0);
-          if (tl != 0) v += (double)tl * Q[3 * (3 * l + b) + r];
-        }
+        for (int l = 0; l < 3; ++l) v += (t == 0 ? -1.0 : (t == l + 1 ? 1.0 : 0.0)) * Q[3 * (3 * l + b) + r];
         return v;
       };
 #pragma unroll
@@ -1320,9 +1323,9 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
         }
       // soft neighbours (the other soft slots, ascending; zero for residual pairs)
       int nn = 0;
-#pragma unroll
+#pragma unroll 1
       for (int t = 0; t < 4; ++t) {
-        if (t == s || codes[t] < 0 || nn >= 2) continue;
+        if (t == s || csel(t) < 0 || nn >= 2) continue;
         const int nb = nn++;
 #pragma unroll
         for (int r = 0; r < 3; ++r)
@@ -1330,7 +1333,7 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
           for (int b = 0; b < 3; ++b) rec[48 + 9 * nb + 3 * r + b] = res ? 0.0 : Hst(t, r, b);
         int jb = -1;
         if (!res) {
-          const int v = codes[s], wv = codes[t];
+          const int v = cs, wv = csel(t);
           for (int q = D.rptr[v]; q < D.rptr[v + 1]; ++q)
             if (D.rcol[q] == wv) { jb = q; break; }
         }
@@ -1362,17 +1365,24 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
 #pragma unroll
         for (int l = 0; l < 9; ++l) wm[l] = 0.0;
       }
-#pragma unroll
+      // rolled loops (instruction-cache footprint); runtime indices resolved by selects
+      auto wsel = [&](int al, int jj) {
+        if (al < 3) return wc[jj];
+        const int q = (al - 3) % 3;
+        return q == 0 ? wm[3 * jj] : (q == 1 ? wm[3 * jj + 1] : wm[3 * jj + 2]);
+      };
+#pragma unroll 1
       for (int al = 0; al < 12; ++al) {
         const int ra = al < 3 ? al : (al - 3) / 3;
         double v = 0.0;
         if (mine)
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * Gy[3 * jj + ra];
+          for (int jj = 0; jj < 3; ++jj)
+            v += wsel(al, jj) * (ra == 0 ? Gy[3 * jj] : (ra == 1 ? Gy[3 * jj + 1] : Gy[3 * jj + 2]));
         v = warp_sum(v);
         if (lane == al) out[al] = v;
       }
-#pragma unroll
+#pragma unroll 1
       for (int be = 0; be < 12; ++be) {
         const int rb = be < 3 ? be : (be - 3) / 3;
         double zc[9];                  // zc[(j,r)] = Σ_l w_l(β) H_y[(j,r),(l,ρβ)]
@@ -1381,15 +1391,16 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
           double z = 0.0;
           if (mine)
 #pragma unroll
-            for (int l = 0; l < 3; ++l) z += (be < 3 ? wc[l] : wm[3 * l + (be - 3) % 3]) * HYS(jr, 3 * l + rb);
+            for (int l = 0; l < 3; ++l) z += wsel(be, l) * HYS(jr, 3 * l + rb);
           zc[jr] = z;
         }
-#pragma unroll
+#pragma unroll 1
         for (int al = 0; al <= be; ++al) {
           const int ra = al < 3 ? al : (al - 3) / 3;
           double v = 0.0;
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * zc[3 * jj + ra];
+          for (int jj = 0; jj < 3; ++jj)
+            v += wsel(al, jj) * (ra == 0 ? zc[3 * jj] : (ra == 1 ? zc[3 * jj + 1] : zc[3 * jj + 2]));
           const int idx = sym_idx(al, be, 12);
           const double vc = warp_sum(res ? 0.0 : v);
           if (lane == (idx & 31)) out[12 + idx] = vc;
@@ -1461,6 +1472,46 @@ __device__ void chol_inverse12(const double* A, double* Ainv, double* L /*144 sc
     }
     for (int i = 0; i < 12; ++i) Ainv[12 * i + c] = y[i];
   }
+}
+
+// the same factorisation and solves as chol_inverse12 (identical operation order per entry), spread
+// over a warp: lanes i > j form column j of L from row dot products; lane c solves column c
+__device__ void chol_inverse12_warp(const double* A, double* Ainv, double* L /*144 scratch*/, int lane) {
+  for (int j = 0; j < 12; ++j) {
+    if (lane == 0) {
+      double s = A[13 * j];
+      for (int k = 0; k < j; ++k) s -= L[12 * j + k] * L[12 * j + k];
+      L[13 * j] = sqrt(fmax(s, 1e-300));
+    }
+    __syncwarp();
+    if (lane > j && lane < 12) {
+      double t = A[12 * lane + j];
+      for (int k = 0; k < j; ++k) t -= L[12 * lane + k] * L[12 * j + k];
+      L[12 * lane + j] = t / L[13 * j];
+    }
+    __syncwarp();
+  }
+  if (lane < 12) {
+    const int c = lane;
+    double y[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {  // L y = e_c
+      double t = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) t -= L[12 * i + k] * y[k];
+      y[i] = t / L[13 * i];
+    }
+#pragma unroll
+    for (int i = 11; i >= 0; --i) {  // Lᵀ x = y
+      double t = y[i];
+#pragma unroll
+      for (int k = i + 1; k < 12; ++k) t -= L[12 * k + i] * y[k];
+      y[i] = t / L[13 * i];
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) Ainv[12 * i + c] = y[i];
+  }
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int force) {
@@ -1729,7 +1780,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
     const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
     for (int i = lane; i < 144; i += 32) T[i] = Db[i] + C.mu * Mb[i];
     __syncwarp();
-    if (lane == 0) chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q);
+    chol_inverse12_warp(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, JS[w].Q, lane);
     __syncwarp();
   }
   CLK(13)
@@ -1945,10 +1996,12 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
   CLK(4)
 }
 
-// block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c)
-__device__ void reinvert_precond(const Dev& D, int e, double mu, double* scratch /*smem 144*/, double* T /*smem 144*/) {
+// block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c).  The 3×3 soft
+// blocks are thread-parallel; warp 0 inverts the body blocks one by one (warp Cholesky) meanwhile.
+// Outputs: ps [9][V] SoA and pb [ND][144] (global, or the resident shared-memory copies)
+__device__ void reinvert_precond(const Dev& D, int e, double mu, double* ps, double* pb, double* scratch /*smem 144*/,
+                                 double* T /*smem 144*/) {
   const double* ds = D.Dg_s + (size_t)e * D.V * 9;
-  double* ps = D.Pinv_s + (size_t)e * D.V * 9;
   for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
     double Pv[9], Pi[9];
     for (int i = 0; i < 9; ++i) Pv[i] = ds[(size_t)i * D.V + v];
@@ -1957,13 +2010,16 @@ __device__ void reinvert_precond(const Dev& D, int e, double mu, double* scratch
     inv33(Pv, Pi);
     for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
   }
-  for (int d = 0; d < D.ND; ++d) {
-    const double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
-    const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
-    __syncthreads();
-    for (int i = threadIdx.x; i < 144; i += blockDim.x) T[i] = Db[i] + mu * Mb[i];
-    __syncthreads();
-    if (threadIdx.x == 0) chol_inverse12(T, D.Pinv_b + ((size_t)e * D.ND + d) * 144, scratch);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int d = 0; d < D.ND; ++d) {
+      const double* Db = D.Dg_b + ((size_t)e * D.ND + d) * 144;
+      const double* Mb = D.My + (size_t)D.dof_body[d] * 144;
+      for (int i = lane; i < 144; i += 32) T[i] = Db[i] + mu * Mb[i];
+      __syncwarp();
+      chol_inverse12_warp(T, pb + (size_t)d * 144, scratch, lane);
+      __syncwarp();
+    }
   }
   __syncthreads();
 }
@@ -2087,12 +2143,8 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
   __shared__ double chol_scratch[144], chol_T[144];
   for (int attempt = 0;; ++attempt) {
     if (attempt > 0) {
-      reinvert_precond(D, e, mu, chol_scratch, chol_T);
-      if (R) {                                            // refresh the resident inverses
-        for (int i = threadIdx.x; i < 9 * D.V; i += blockDim.x) Rw_Ps[i] = D.Pinv_s[(size_t)e * D.V * 9 + i];
-        for (int i = threadIdx.x; i < 144 * D.ND; i += blockDim.x) Rw_Pb[i] = D.Pinv_b[(size_t)e * D.ND * 144 + i];
-        __syncthreads();
-      }
+      if (R) reinvert_precond(D, e, mu, Rw_Ps, Rw_Pb, chol_scratch, chol_T);      // resident copies
+      else reinvert_precond(D, e, mu, D.Pinv_s + (size_t)e * D.V * 9, D.Pinv_b + (size_t)e * D.ND * 144, chol_scratch, chol_T);
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
     __syncthreads();
