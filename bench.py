@@ -274,16 +274,20 @@ def main():
         local_bytes = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
         ach = local_bytes / (pcg_ms / 1e3) / 1e9
         traffic, tsrc = None, None
-        tfile = os.path.join(ROOT, "profiles", "r1_pcg_traffic.json")
+        tfile = os.path.join(ROOT, "profiles", "r1s2_pcg_traffic.json")
         if os.path.exists(tfile):
             tj = json.load(open(tfile))
             traffic = tj["dram_bytes_per_launch"]
-            tsrc = (f"{os.path.relpath(tfile, ROOT)}: ncu dram__bytes_read+write per k_pcg launch over one C2 step; "
-                    f"traffic/algorithmic = {tj['traffic_over_alg']:.2f} for that step")
-        roof = {"kernel": "k_pcg (block-Jacobi PCG, one CTA per env)", "bound": "hbm", "achieved": ach,
+            tsrc = (f"{os.path.relpath(tfile, ROOT)}: ncu dram__bytes_read+write per {tj['kernel']} launch over one C2 "
+                    f"step; traffic/algorithmic = {tj['traffic_over_alg']:.3f} for that step (operator staged on chip "
+                    f"once per launch, reused by every PCG iteration)")
+        roof = {"kernel": "k_pcg_r (env-resident block-Jacobi PCG, one CTA per env)", "bound": "hbm", "achieved": ach,
                 "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic, "traffic_source": tsrc,
                 "peak_source": peak_src, "share_of_step": pcg_ms / ms,
                 "alg_bytes_per_launch": local_bytes / max(phases["pcg"]["launches"], 1),
+                "alg_model": "per PCG iteration per env: 72(V+E_s)+4E_s+640*P_res+296*N_cpl+1248*ND+48V+96n "
+                             "(condensed operator streamed once per iteration; DESIGN.md sec 5)",
+                "note": "frac > 1 would mean on-chip reuse beats streaming the operator from HBM every iteration",
                 "dominant_kernel": dom}
     line = {
         "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K, "warmup": W,

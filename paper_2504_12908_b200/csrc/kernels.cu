@@ -1806,8 +1806,11 @@ struct SmemMat {
   const int *rptr, *rcol, *rupx, *cptr, *rcnt, *cpp;
 };
 
-__device__ void spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
-                     double mu = 0.0, const SmemMat* R = nullptr) {
+// what: 1 = zero the body partials + barrier, 2 = pass A (+ barrier), 4 = pass B, 8 = final barrier.
+// Returns this thread's partial Σ x_i y_i over the rows it wrote (for fused PCG dot products).
+constexpr int SPMV_ALL = 15;
+__device__ double spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
+                       double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL) {
   const EnvCtl& C = D.ctl[e];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
@@ -1819,9 +1822,13 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
   const int nres = C.n_res, ncpl = C.n_cpl;
   const int nb12 = D.ND * 12;
   CLK_INIT
-  for (int i = threadIdx.x; i < nw * nb12; i += blockDim.x) part[i] = 0.0;
-  __syncthreads();
+  double xy = 0.0;
+  if (what & 1) {
+    for (int i = threadIdx.x; i < nw * nb12; i += blockDim.x) part[i] = 0.0;
+    __syncthreads();
+  }
   CLK(0)
+  if (what & 2) {
   // pass A1: residual pairs, matrix-free 12×12 (one pair per lane)
   for (int base = 32 * w; base < nres; base += blockDim.x) {
     const int idx = base + lane;
@@ -1929,7 +1936,9 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
   }
   CLK(1)
   __syncthreads();
+  }
   CLK(2)
+  if (!(what & 4)) return 0.0;
   const int* cptr = R ? R->cptr : D.cptr + (size_t)e * (D.V + 1);
   const int* rcnt = R ? R->rcnt : D.rcnt + (size_t)e * D.V;
   const int* cpp = R ? R->cpp : D.cpl_ptr + (size_t)e * (D.V + 1);
@@ -1975,6 +1984,7 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
         for (int j = cpp[v]; j < cpp[v + 1]; ++j) acc += ld3(cout + 3 * j);
         if (mu != 0.0) acc += (mu * D.mass[v]) * xv;
         st3(y + 3 * v, acc);
+        xy += xv.x * acc.x + xv.y * acc.y + xv.z * acc.z;
       }
     }
   }
@@ -1991,9 +2001,11 @@ __device__ void spmv(const Dev& D, int e, const double* x, double* y, double* pa
     }
     for (int ww = 0; ww < nw; ++ww) sacc += part[ww * nb12 + i];
     y[3 * D.V + i] = sacc;
+    xy += xb[row] * sacc;
   }
-  __syncthreads();
+  if (what & 8) __syncthreads();
   CLK(4)
+  return xy;
 }
 
 // block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c).  The 3×3 soft
@@ -2156,7 +2168,69 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     zero_g = rz0 == 0.0;                                 // g = 0: p = 0 is the (converged) answer
     int it = 0;
     bad = !(rz0 == rz0);
-    while (!bad && it < D.max_pcg && rz > stop) {
+    if (R) {
+      // fused resident iteration, 4 barriers: [pass A | B2 | pass B + dᵀAd partials | B3 | α, p/r update,
+      // block-Jacobi z and rᵀz partials per vertex / body | B4 | β, d update | B1].  Per-warp partials in
+      // red[0..15] (dᵀAd) and red[16..31] (rᵀz), summed in warp order by every thread (deterministic)
+      const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+      const int V = D.V, nb12 = 12 * D.ND;
+      for (int i = threadIdx.x; i < nwp * nb12; i += blockDim.x) bpart[i] = 0.0;
+      __syncthreads();
+      while (!bad && it < D.max_pcg && rz > stop) {
+        double loc = spmv(D, e, d, Ad, bpart, mu, R, 2 | 4);
+        loc = warp_sum(loc);
+        if (lane == 0) red[wi] = loc;
+        __syncthreads();                                  // B3
+        double dAd = 0.0;
+        for (int k = 0; k < nwp; ++k) dAd += red[k];
+        if (!(dAd > 0.0)) { bad = true; __syncthreads(); break; }   // uniform; red[] reads done
+        const double alpha = rz / dAd;
+        double loc2 = 0.0;
+        for (int v = threadIdx.x; v < V; v += blockDim.x) {
+          v3 rv = ld3(r + 3 * v);
+          const v3 dv = ld3(d + 3 * v), av = ld3(Ad + 3 * v);
+          double* pv = p + 3 * v;
+          pv[0] += alpha * dv.x; pv[1] += alpha * dv.y; pv[2] += alpha * dv.z;
+          rv = mk(rv.x - alpha * av.x, rv.y - alpha * av.y, rv.z - alpha * av.z);
+          st3(r + 3 * v, rv);
+          const double* Ps = R->Ps;
+          const v3 zv = mk(Ps[v] * rv.x + Ps[V + v] * rv.y + Ps[2 * V + v] * rv.z,
+                           Ps[3 * V + v] * rv.x + Ps[4 * V + v] * rv.y + Ps[5 * V + v] * rv.z,
+                           Ps[6 * V + v] * rv.x + Ps[7 * V + v] * rv.y + Ps[8 * V + v] * rv.z);
+          st3(z + 3 * v, zv);
+          loc2 += rv.x * zv.x + rv.y * zv.y + rv.z * zv.z;
+        }
+        for (int db = wi; db < D.ND; db += nwp) {         // body db: lanes 0..11 own its rows
+          const int o = 3 * V + 12 * db;
+          if (lane < 12) {
+            p[o + lane] += alpha * d[o + lane];
+            r[o + lane] -= alpha * Ad[o + lane];
+          }
+          __syncwarp();
+          if (lane < 12) {
+            const double* Pi = R->Pb + (size_t)db * 144 + 12 * lane;
+            double zz = 0.0;
+            for (int c = 0; c < 12; ++c) zz += Pi[c] * r[o + c];
+            z[o + lane] = zz;
+            loc2 += r[o + lane] * zz;
+          }
+          __syncwarp();
+        }
+        for (int i = threadIdx.x; i < nwp * nb12; i += blockDim.x) bpart[i] = 0.0;   // read before B3
+        loc2 = warp_sum(loc2);
+        if (lane == 0) red[16 + wi] = loc2;
+        __syncthreads();                                  // B4
+        double rzn = 0.0;
+        for (int k = 0; k < nwp; ++k) rzn += red[16 + k];
+        const double beta = rzn / rz;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = z[i] + beta * d[i];
+        __syncthreads();                                  // B1
+        rz = rzn;
+        ++it;
+        if (!(rz == rz)) bad = true;
+      }
+    }
+    while (!R && !bad && it < D.max_pcg && rz > stop) {
       spmv(D, e, d, Ad, bpart, mu, R);
       CLK_INIT
       part = 0.0;
@@ -2208,9 +2282,11 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     const bool exact_failed = D.hmode == 1 && C.exact && (bad || !(gp < 0.0) || !(pm == pm));
     C.pcg += it_total;
     C.pcg_total += it_total;
-    // algorithmic bytes per PCG iteration (SURVEY §8(d) model):
-    // 72(V+E_s) + 4E_s + 640P + 624·ND + 48V + 624·ND + 96n
-    const double bpi = 72.0 * (D.V + D.NEs) + 4.0 * D.NEs + 640.0 * C.n_act + 1248.0 * D.ND + 48.0 * D.V + 96.0 * D.n;
+    // algorithmic bytes per PCG iteration of the condensed operator (SURVEY §8(d) model with the
+    // contact condensation): 72(V+E_s) + 4E_s [soft BSR] + 640·P_res [residual pairs]
+    // + 296·N_cpl [3×12 couplings + ids] + 624·ND [body blocks] + 48V + 624·ND [preconditioner] + 96n
+    const double bpi = 72.0 * (D.V + D.NEs) + 4.0 * D.NEs + 640.0 * C.n_res + 296.0 * C.n_cpl + 1248.0 * D.ND +
+                       48.0 * D.V + 96.0 * D.n;
     C.pcg_bytes += bpi * it_total;
     C.gp = gp;
     C.pnorm = pm;

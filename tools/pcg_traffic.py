@@ -1,5 +1,5 @@
 """One C2 step (after W warm-up steps) inside cudaProfilerStart/Stop, for
-`ncu --profile-from-start off -k regex:k_pcg --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum`.
+`ncu --profile-from-start off -k regex:k_pcg_r --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum`.
 Prints the algorithmic PCG bytes of that step (device counters) so traffic/algorithmic can be compared."""
 import json, sys
 import numpy as np, torch
