@@ -29,8 +29,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "peg-insertion env-steps/s and ×real-time, dual sensors, at 1/2/4/8 B200"
-WORKLOAD = "C2: peg insertion, dual low-res sensors (2 pads x 8x6x3 lattice, 144 nodes/350 tets each), " \
-           "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s"
+WORKLOADS = {
+    "C2": "C2: peg insertion, dual low-res sensors (2 pads x 8x6x3 lattice, 144 nodes/350 tets each), "
+          "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s",
+    "C3": "C3: peg insertion, dual high-res sensors (2 pads x 19x16x5 lattice, 1520 nodes/5400 tets each), "
+          "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s",
+}
+WORKLOAD = WORKLOADS["C2"]
 
 
 def parse():
@@ -142,7 +147,7 @@ def run_reference(a):
     line = {"metric": METRIC, "value": v, "unit": "env-steps/s", "impl": "reference", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": warm, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD + " — reference arm: the CPU oracle advancing env 0 (one env per step)",
+            "config": {"workload": WORKLOADS.get(a.config, a.config) + " — reference arm: the CPU oracle advancing env 0 (one env per step)",
                        "envs_per_step": 1, "dt": dt},
             "x_realtime": v * dt,
             "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
@@ -293,7 +298,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "envs_per_gpu": E, "envs_total": n_env_total, "dt": dt,
+        "config": {"workload": WORKLOADS.get(a.config, a.config), "envs_per_gpu": E, "envs_total": n_env_total, "dt": dt,
                    "stepping": "tac_step_schedule: device-resident target table, per-step readout, envs advance independently",
                    "episode_steps_timed": f"{W}-{W + K - 1}", "parallelism": f"env-sharded x{world}",
                    "l2": "inputs larger than L2: per-step working set ~%.1f GB/GPU > 126 MB L2" %
