@@ -99,7 +99,7 @@ typedef struct {
 } tac_affine_desc;
 
 typedef struct {
-  int32_t n_soft, n_affine;
+  int32_t n_soft, n_affine;       /* n_soft + n_affine ≤ 32 (TAC_E_INVALID otherwise: body masks are 32-bit) */
   const tac_soft_desc* soft;
   const tac_affine_desc* affine;
   const uint8_t* collide;        /* [(n_soft+n_affine)^2] extra body-pair mask (1 = may collide), or NULL */

@@ -121,6 +121,7 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
   H.NA = na;
   H.npads = ns;
   H.NB = ns + na;
+  if (H.NB > 32) return fail(TAC_E_INVALID, "more than 32 bodies (soft + affine) per env");
   // ---- soft ----
   std::vector<std::vector<std::array<int, 3>>> soft_tris(ns);
   int off = 0;

@@ -135,9 +135,13 @@ struct Grid {
   }
   __device__ void cell(v3 p, int* c) const { c[0] = ci(p.x, ox); c[1] = ci(p.y, oy); c[2] = ci(p.z, oz); }
 };
-__device__ __forceinline__ unsigned hcell(int i, int j, int k) {
-  return (((unsigned)i * 73856093u) ^ ((unsigned)j * 19349663u) ^ ((unsigned)k * 83492791u)) & (NBUCKET - 1);
+// bucket of (cell, target kind): triangles and edges of the same cell hash apart, so a PT query only
+// scans triangle entries and an EE query only edge entries (up to collisions)
+__device__ __forceinline__ unsigned hcell(int i, int j, int k, int kind) {
+  return (((unsigned)i * 73856093u) ^ ((unsigned)j * 19349663u) ^ ((unsigned)k * 83492791u) ^ (kind ? 0x9E3779B9u : 0u)) &
+         (NBUCKET - 1);
 }
+constexpr int ENT_CODE_BITS = 26;      // hash entry: target code (2t + kind) | body id << 26
 __device__ __forceinline__ int ccode(int i, int j, int k) { return i | (j << 10) | (k << 20); }
 
 struct BoxCtx {
@@ -222,6 +226,8 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
   const int want = pt ? 0 : 1;
   if (!query_reaches(D, bb, qbody, qlo, qhi, B.infl)) return 0;
   const unsigned char* allow = D.allowed + (size_t)qbody * D.NB;
+  unsigned amask = 0u;                 // bodies this query may touch (NB ≤ MAXB = 32)
+  for (int b = 0; b < D.NB; ++b) amask |= allow[b] ? (1u << b) : 0u;
   int lo[3], hi[3];
   G.cell(qlo, lo); G.cell(qhi, hi);
   long ncell = (long)(hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
@@ -247,16 +253,16 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
   for (int x = lo[0]; x <= hi[0]; ++x)
     for (int y = lo[1]; y <= hi[1]; ++y)
       for (int z = lo[2]; z <= hi[2]; ++z) {
-        unsigned h = hcell(x, y, z);
+        unsigned h = hcell(x, y, z, want);
         int cc = ccode(x, y, z);
         for (int j = cnt_off[h]; j < cnt_off[h + 1]; ++j) {
           if (ent[2 * j + 1] != cc) continue;
-          int code = ent[2 * j];
+          const int e0 = ent[2 * j];
+          const int code = e0 & ((1 << ENT_CODE_BITS) - 1);
           if ((code & 1) != want) continue;
           int t = code >> 1;
           if (!pt && t <= qa) continue;
-          int tb = pt ? D.tri_body[t] : D.edge_body[t];
-          if (!allow[tb]) continue;
+          if (!((amask >> (e0 >> ENT_CODE_BITS)) & 1u)) continue;
           v3 tlo, thi;
           target_box(D, B, code, tlo, thi);
           if (!overlap(qlo, qhi, tlo, thi)) continue;
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     }
     for (int x = l[0]; x <= h[0]; ++x)
       for (int y = l[1]; y <= h[1]; ++y)
-        for (int z = l[2]; z <= h[2]; ++z) atomicAdd(&cnt[hcell(x, y, z)], 1);
+        for (int z = l[2]; z <= h[2]; ++z) atomicAdd(&cnt[hcell(x, y, z, code & 1)], 1);
   }
   __syncthreads();
   // exclusive scan of bucket counts (16 per thread for 256 threads)
@@ -398,8 +404,8 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     for (int x = l[0]; x <= h[0]; ++x)
       for (int y = l[1]; y <= h[1]; ++y)
         for (int z = l[2]; z <= h[2]; ++z) {
-          int pos = atomicAdd(&cur[hcell(x, y, z)], 1);
-          ent[2 * pos] = code;
+          int pos = atomicAdd(&cur[hcell(x, y, z, code & 1)], 1);
+          ent[2 * pos] = code | ((i < D.NT ? D.tri_body[i] : D.edge_body[i - D.NT]) << ENT_CODE_BITS);
           ent[2 * pos + 1] = ccode(x, y, z);
         }
   }
