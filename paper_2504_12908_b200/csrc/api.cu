@@ -42,6 +42,7 @@ struct HostT {
   std::vector<int> sedge, vadj_ptr, vadj, vdiag_ptr, vdiag, eblk_ptr, eblk;
   std::vector<int> rptr, rcol, rblk_ptr, rblk;   // row-ordered symmetric BSR (off-diagonal)
   std::vector<int> rupx;                         // [NNZ] 2·(edge id) + (block stored transposed)
+  std::vector<int> eup;                          // [NEs] row-ordered index of the edge's upper block
   int NNZ = 0;
   std::vector<int> body_kind, dof_slot, dof_body;
   std::vector<double> My, bmass, bs1, bvol, bkappa;
@@ -335,6 +336,7 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
         rid[{v, u}] = (int)H.rcol.size();
         H.rcol.push_back(u);
         H.rupx.push_back(2 * sid[{std::min(u, v), std::max(u, v)}] + (u < v ? 1 : 0));
+        if (u > v) { H.eup.resize(H.NEs); H.eup[sid[{v, u}]] = (int)H.rcol.size() - 1; }
       }
       H.rptr.push_back((int)H.rcol.size());
     }
@@ -468,7 +470,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.tets = ti(H.tets); D.Dmi = td(H.Dmi); D.vol = td(H.vol); D.mu = td(H.mu); D.lam = td(H.lam); D.mass = td(H.mass);
   D.sedge = ti(H.sedge); D.vadj_ptr = ti(H.vadj_ptr); D.vadj = ti(H.vadj); D.vdiag_ptr = ti(H.vdiag_ptr);
   D.vdiag = ti(H.vdiag); D.eblk_ptr = ti(H.eblk_ptr); D.eblk = ti(H.eblk);
-  D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rupx = ti(H.rupx); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
+  D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rupx = ti(H.rupx); D.eup = ti(H.eup); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
   D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My);
   D.bmass = td(H.bmass); D.bs1 = td(H.bs1); D.bvol = td(H.bvol); D.bkappa = td(H.bkappa);
   D.vert_body = ti(H.vert_body); D.vert_aff = ti(H.vert_aff); D.vert_xbar = td(H.vert_xbar);
@@ -515,6 +517,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.sbody = C.take<int>(e * 4 * D.act_cap); D.brec = C.take<double>(e * D.act_cap * 2 * BREC);
   D.bpart = C.take<double>(e * (size_t)((D.act_cap + 31) / 32) * std::max(H.ND, 1) * BPART);
   D.qcnt = C.take<int>(e * (size_t)(H.NSV + H.NE) + 1);
+  D.lsl = C.take<int>(e * (size_t)D.cand_cap);
   D.eterm = C.take<double>(e * 8);
   D.out_coat = C.take<double>(e * H.NCOAT * 3 + 1); D.out_mpos = C.take<double>(e * H.NMARK * 3 + 1);
   D.out_mflow = C.take<double>(e * H.NMARK * 3 + 1);
@@ -595,7 +598,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, need, st);
 #define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
   UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
-  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
+  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(eup); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
   UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(body_sv_ptr); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
   UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);

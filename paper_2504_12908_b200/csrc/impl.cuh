@@ -72,6 +72,7 @@ struct Dev {
   const int* eblk;        // entries 16*tet + 4*a + b (local a ↔ edge.i, b ↔ edge.j)
   const int* rptr;        // [V+1] row-ordered symmetric BSR
   const int* rcol;        // [NNZ] column (neighbour vertex)
+  const int* eup;         // [NEs] row-ordered index of each soft edge's upper block (i < j, row i)
   const int* rupx;        // [NNZ] 2·(soft edge id) + 1 if the block is the transpose of the edge's upper block
   const int* rblk_ptr;    // [NNZ+1]
   const int* rblk;        // entries 16*tet + 4*a + b (a ↔ row, b ↔ column)
@@ -132,6 +133,7 @@ struct Dev {
   int* ent;               // [E][ent_cap][2]
   int* big;               // [E][BIG_CAP]
   int* qcnt;              // [E][NSV+NE] broad-phase query counts → segment offsets
+  int* lsl;               // [E][cand_cap] line-search candidate list (energy_terms lmode 1/2)
   double* tbox;           // [E][NT+NE][6] raw target boxes (broad-phase cache)
   double* vref;           // [E][NSV][6] reference boxes of surface vertices at the last build
   int* act_info;          // [E][act_cap][4] (kind, type, a, b)

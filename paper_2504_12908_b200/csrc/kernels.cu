@@ -2078,13 +2078,22 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force,
 }
 
 // shared-memory bytes of k_pcg_r for this batch (0 if the env does not fit one CTA)
-constexpr int PCG_R_THREADS = 512;
+constexpr int PCG_R_THREADS = 512;   // upper bound; the launch picks pcg_r_threads(V)
+// threads of k_pcg_r: 4 lanes per soft row, as few row passes as fit in 512 threads with the rows
+// split evenly over the passes (C2: V = 288 → 3 passes × 96 rows = 384 threads)
+__host__ __device__ inline int pcg_r_threads(int V) {
+  for (int passes = 1;; ++passes) {
+    const int rows = (V + passes - 1) / passes;
+    const int t = ((4 * rows + 31) / 32) * 32;
+    if (t <= PCG_R_THREADS) return t < 128 ? 128 : t;
+  }
+}
 __host__ __device__ inline size_t pcg_r_ncpl(const Dev& D) {          // coupling bound: ≤ 1 per (v, d)
   const size_t a = (size_t)D.V * D.ND, b = (size_t)D.cpl_cap;
   return a < b ? a : b;
 }
 __host__ __device__ inline size_t pcg_r_bytes(const Dev& D) {
-  const size_t nd = (size_t)(PCG_R_THREADS / 32) * D.ND * 12 + 1 + 5 * (size_t)D.n + 9 * (size_t)D.NEs +
+  const size_t nd = (size_t)(pcg_r_threads(D.V) / 32) * D.ND * 12 + 1 + 5 * (size_t)D.n + 9 * (size_t)D.NEs +
                     18 * (size_t)D.V + 288 * (size_t)D.ND + 3 * pcg_r_ncpl(D);
   const size_t ni = 3 * ((size_t)D.V + 1) + (size_t)D.V + 2 * (size_t)D.NNZ;
   return nd * sizeof(double) + ni * sizeof(int);
@@ -2099,7 +2108,7 @@ __global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int
   __shared__ double red[32];
   extern __shared__ double dsmem[];
   const int V = D.V, ND = D.ND, n = D.n, NNZ = D.NNZ;
-  double* base = dsmem + ((PCG_R_THREADS / 32) * ND * 12 + 1) + 5 * (size_t)n;   // after bpart + vectors
+  double* base = dsmem + ((blockDim.x / 32) * ND * 12 + 1) + 5 * (size_t)n;   // after bpart + vectors
   double* U = base;
   double* Hd = U + 9 * (size_t)D.NEs;
   double* Ps = Hd + 9 * (size_t)V;
@@ -2129,10 +2138,8 @@ __global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int
     Hb[i] = D.Hb[(size_t)e * ND * 144 + i];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 9 * NNZ; i += blockDim.x) {   // upper edge blocks (coalesced read of Ho)
-    const int ux = rupx[i / 9];
-    if (!(ux & 1)) U[9 * (ux >> 1) + i % 9] = Ho[i];
-  }
+  for (int i = threadIdx.x; i < 9 * D.NEs; i += blockDim.x)    // upper edge blocks (72-byte runs of Ho)
+    U[i] = Ho[9 * (size_t)D.eup[i / 9] + i % 9];
   __syncthreads();
   SmemMat R{U, Hd, Hb, Ps, Pb, couts, rptr, rcol, rupx, cptr, rcnt, cpp};
   pcg_body(D, e, 1, dsmem, red, &R, Ps, Pb);
@@ -2365,7 +2372,27 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_ccd(Dev D, int env0, int force)
 // ------------------------------------------------------------------------------------------
 // energy at q + α p (line search): six deterministic block sums
 // ------------------------------------------------------------------------------------------
-__device__ void energy_terms(const Dev& D, int e, double alpha, double* red, double* terms, int* inverted) {
+// six deterministic block sums in one pass (2 barriers): per-warp partials → red6[6][32] → warp sums
+__device__ __forceinline__ void block_sum6(double* v, double* red6) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) red6[32 * i + wid] = v[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 6; ++i) v[i] = warp_sum(lane < nw ? red6[32 * i + lane] : 0.0);
+}
+
+// Energy terms at q + αp.  lmode 0: barrier over every candidate of C′; 1: the same, and build the
+// line-search list lsl of candidates that can be active for some α ∈ [0, K_eff·α_ccd] —
+// d(0) − α_ccd·(max_A ‖Pd‖ + max_B ‖Pd‖) < d̂ (a primitive distance moves at most by the largest vertex
+// displacement of each side) — in candidate order; 2: barrier over the list only (exact: the other
+// candidates have d > d̂ at every trial α of this line search)
+__device__ void energy_terms(const Dev& D, int e, double alpha, double* red, double* terms, int* inverted,
+                             int lmode = 0, int* lsl = nullptr, int* nls = nullptr, int* sh = nullptr) {
   const EnvCtl& C = D.ctl[e];
   const double* q = D.q + (size_t)e * D.n;
   const double* p = D.p + (size_t)e * D.n;
@@ -2432,37 +2459,59 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
   const int* ca = D.cand_a + (size_t)e * D.cand_cap;
   const int* cb = D.cand_b + (size_t)e * D.cand_cap;
   const double dh2 = D.dhat * D.dhat;
-  for (int k = threadIdx.x; k < C.ncand; k += blockDim.x) {
-    int kind = (ca[k] >> 30) & 1, a = ca[k] & ((1 << 30) - 1), b = cb[k], vid[4];
-    pair_vids(D, kind, a, b, vid);
-    v3 X[4];
-    const double aK = alpha == 0.0 ? 0.0 : alpha / C.Keff;   // Pd holds K_eff·(displacement of p)
-    for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]) + aK * ld3(Pd + 3 * vid[s]);
-    double d2;
-    classify(kind, X, &d2);
-    if (!(d2 < dh2)) continue;
-    double B, B1, B2;
-    barrier_s(d2, D.dhat, &B, &B1, &B2);
-    double m = 1.0;
-    if (kind == 1 && D.mollify) {
-      v3 n = cross(X[1] - X[0], X[3] - X[2]);
-      double m1, m2;
-      mollifier(dot(n, n), pair_eps(D, kind, a, b), &m, &m1, &m2);
+  const int ncl = lmode == 2 ? *nls : C.ncand;
+  const int ncl_r = (ncl + blockDim.x - 1) / blockDim.x * blockDim.x;   // tile-aligned (list scan)
+  int run = 0;
+  for (int kk = threadIdx.x; kk < ncl_r; kk += blockDim.x) {
+    int keep = 0;
+    const int k = lmode == 2 ? (kk < ncl ? lsl[kk] : 0) : kk;
+    if (kk < ncl) {
+      int kind = (ca[k] >> 30) & 1, a = ca[k] & ((1 << 30) - 1), b = cb[k], vid[4];
+      pair_vids(D, kind, a, b, vid);
+      v3 X[4];
+      const double aK = alpha == 0.0 ? 0.0 : alpha / C.Keff;   // Pd holds K_eff·(displacement of p)
+      for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]) + aK * ld3(Pd + 3 * vid[s]);
+      double d2;
+      classify(kind, X, &d2);
+      if (lmode == 1) {
+        double mA = 0.0, mB = 0.0;
+        const int na = kind == 0 ? 1 : 2;
+        for (int s = 0; s < 4; ++s) {
+          const v3 u = ld3(Pd + 3 * vid[s]);
+          const double l = sqrt(dot(u, u));
+          if (s < na) mA = fmax(mA, l); else mB = fmax(mB, l);
+        }
+        keep = sqrt(d2) - C.alpha_ccd * (mA + mB) < D.dhat * (1.0 + 1e-9);
+      }
+      if (d2 < dh2) {
+        double B, B1, B2;
+        barrier_s(d2, D.dhat, &B, &B1, &B2);
+        double m = 1.0;
+        if (kind == 1 && D.mollify) {
+          v3 n = cross(X[1] - X[0], X[3] - X[2]);
+          double m1, m2;
+          mollifier(dot(n, n), pair_eps(D, kind, a, b), &m, &m1, &m2);
+        }
+        eba += dt2 * D.kappa * pair_area(D, kind, a, b) * m * B;
+      }
     }
-    eba += dt2 * D.kappa * pair_area(D, kind, a, b) * m * B;
+    if (lmode == 1) {
+      int tot;
+      const int ex = block_excl_scan(keep, sh, &tot);
+      if (keep) lsl[run + ex] = k;
+      run += tot;
+    }
   }
-  terms[0] = block_sum(ein, red);
-  terms[1] = block_sum(eel, red);
-  terms[2] = block_sum(eor, red);
-  terms[3] = block_sum(egr, red);
-  terms[4] = block_sum(eba, red);
-  terms[5] = block_sum(eal, red);
+  if (lmode == 1 && threadIdx.x == 0) *nls = run;
+  double v6[6] = {ein, eel, eor, egr, eba, eal};
+  block_sum6(v6, red);
+  for (int i = 0; i < 6; ++i) terms[i] = v6[i];
   *inverted = __syncthreads_or(inv);
 }
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_energy(Dev D, int env0, double alpha) {
   const int e = env0 + blockIdx.x;
-  __shared__ double red[32];
+  __shared__ double red[6 * 32];
   double t[6];
   int inv;
   energy_terms(D, e, alpha, red, t, &inv);
@@ -2479,10 +2528,13 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
   if (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail) return;
-  __shared__ double red[32];
+  __shared__ double red[6 * 32];
+  __shared__ int sh[33], nls;
+  int* lsl = D.lsl + (size_t)e * D.cand_cap;
   double t[6];
   int inv;
-  energy_terms(D, e, 0.0, red, t, &inv);
+  energy_terms(D, e, 0.0, red, t, &inv, 1, lsl, &nls, sh);
+  __syncthreads();
   const double E0 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
   const double alpha_max = C.Keff * C.alpha_ccd;  // ACCD bound along K_eff·p, in units of p
   double alpha = fmin(1.0, alpha_max);
@@ -2491,7 +2543,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
   bool ok = false;
   double E1 = E0;
   while (true) {
-    energy_terms(D, e, alpha, red, t, &inv);
+    energy_terms(D, e, alpha, red, t, &inv, 2, lsl, &nls);
     if (!inv) {
       E1 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
       if (E1 <= E0 + D.armijo * alpha * gp) { ok = true; break; }
@@ -2504,7 +2556,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
   // Armijo holds and α stays under the ACCD bound of the K-times longer sweep
   if (ok && alpha == 1.0 && C.Keff > 1.0) {
     while (2.0 * alpha <= alpha_max) {
-      energy_terms(D, e, 2.0 * alpha, red, t, &inv);
+      energy_terms(D, e, 2.0 * alpha, red, t, &inv, 2, lsl, &nls);
       if (inv) break;
       const double E2 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
       if (!(E2 < E1) || !(E2 <= E0 + D.armijo * 2.0 * alpha * gp)) break;
@@ -2875,7 +2927,7 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   if (rb <= 227 * 1024) {                                 // env-resident PCG (one CTA per SM)
     static size_t rconf = 0;
     if (rb > rconf) { cudaFuncSetAttribute(k_pcg_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb); rconf = rb; }
-    k_pcg_r<<<ne, PCG_R_THREADS, rb, s>>>(D, env0, force);
+    k_pcg_r<<<ne, pcg_r_threads(D.V), rb, s>>>(D, env0, force);
     return;
   }
   k_pcg<<<ne, NTHREADS, bytes, s>>>(D, env0, force, vsm);
