@@ -40,6 +40,20 @@ __device__ __forceinline__ double pair_eps(const Dev& D, int kind, int a, int b)
   return kind == 0 ? 1.0 : 1e-3 * D.elen2[a] * D.elen2[b];
 }
 
+// distance between the axis-aligned boxes of the pair's two primitives (PT: {x0} vs {x1,x2,x3}; EE:
+// {x0,x1} vs {x2,x3}) — a lower bound of the primitive distance, used to skip exact classification
+// where it cannot change a result
+__device__ __forceinline__ double prim_box_dist(int kind, const v3* X) {
+  v3 alo = X[0], ahi = X[0], blo = X[3], bhi = X[3];
+  if (kind == 1) { alo = vmin(alo, X[1]); ahi = vmax(ahi, X[1]); }
+  else { blo = vmin(blo, X[1]); bhi = vmax(bhi, X[1]); }
+  blo = vmin(blo, X[2]); bhi = vmax(bhi, X[2]);
+  const double gx = fmax(0.0, fmax(blo.x - ahi.x, alo.x - bhi.x));
+  const double gy = fmax(0.0, fmax(blo.y - ahi.y, alo.y - bhi.y));
+  const double gz = fmax(0.0, fmax(blo.z - ahi.z, alo.z - bhi.z));
+  return sqrt(gx * gx + gy * gy + gz * gz);
+}
+
 __device__ __forceinline__ bool env_skip(const Dev& D, int e, int force) {
   return !force && D.ctl[e].phase != PHASE_ACTIVE;
 }
@@ -501,9 +515,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
       pair_vids(D, kind, a, b, vid);
       v3 X[4];
       for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]);
-      double d2;
-      type = classify(kind, X, &d2);
-      flag = d2 < dh2;
+      if (prim_box_dist(kind, X) < D.dhat * (1.0 + 1e-9)) {   // else d ≥ box distance > d̂: inactive
+        double d2;
+        type = classify(kind, X, &d2);
+        flag = d2 < dh2;
+      }
     }
     int tot;
     int ex = block_excl_scan(flag, sh, &tot);
@@ -2330,6 +2346,8 @@ __device__ double accd_pair(int kind, v3* X, v3* Pd, double s, double tc, int ma
   for (int i = 0; i < 4; ++i) { Pd[i] = Pd[i] - mean; n[i] = sqrt(dot(Pd[i], Pd[i])); }
   double lp = kind == 0 ? n[0] + fmax(n[1], fmax(n[2], n[3])) : fmax(n[0], n[1]) + fmax(n[2], n[3]);
   if (lp == 0.0) return 1.0;
+  // the first advance t_l = (1−s)·d/l_p already exceeds t_c when the box distance does: ACCD returns 1
+  if ((1.0 - s) * prim_box_dist(kind, X) > tc * lp * (1.0 + 1e-10)) return 1.0;
   double d2;
   classify(kind, X, &d2);
   double d = sqrt(d2);
@@ -2471,8 +2489,7 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
       v3 X[4];
       const double aK = alpha == 0.0 ? 0.0 : alpha / C.Keff;   // Pd holds K_eff·(displacement of p)
       for (int s = 0; s < 4; ++s) X[s] = ld3(P + 3 * vid[s]) + aK * ld3(Pd + 3 * vid[s]);
-      double d2;
-      classify(kind, X, &d2);
+      double reach = 0.0;              // lmode 1: α_ccd·(max_A ‖Pd‖ + max_B ‖Pd‖)
       if (lmode == 1) {
         double mA = 0.0, mB = 0.0;
         const int na = kind == 0 ? 1 : 2;
@@ -2481,7 +2498,13 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
           const double l = sqrt(dot(u, u));
           if (s < na) mA = fmax(mA, l); else mB = fmax(mB, l);
         }
-        keep = sqrt(d2) - C.alpha_ccd * (mA + mB) < D.dhat * (1.0 + 1e-9);
+        reach = C.alpha_ccd * (mA + mB);
+      }
+      // box-distance lower bound: neither active now nor (lmode 1) reachable within this search
+      double d2 = dh2 * 4.0;
+      if (prim_box_dist(kind, X) - reach < D.dhat * (1.0 + 1e-9)) {
+        classify(kind, X, &d2);
+        if (lmode == 1) keep = sqrt(d2) - reach < D.dhat * (1.0 + 1e-9);
       }
       if (d2 < dh2) {
         double B, B1, B2;
