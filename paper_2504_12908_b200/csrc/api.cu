@@ -526,6 +526,8 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
 }
 
 static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, const tac_scene_desc* sc) {
+  D.maxrl = 0;
+  for (size_t v = 0; v + 1 < H.rptr.size(); ++v) D.maxrl = std::max(D.maxrl, H.rptr[v + 1] - H.rptr[v]);
   D.E = E; D.V = H.V; D.T = H.T; D.NA = H.NA; D.ND = H.ND; D.NVall = H.NVall; D.NSV = H.NSV; D.NT = H.NT;
   D.NE = H.NE; D.NEs = H.NEs; D.NNZ = H.NNZ; D.NC = H.NC; D.NK = H.NK; D.NB = H.NB; D.n = H.n; D.npads = H.npads;
   D.NCOAT = H.NCOAT; D.NMARK = H.NMARK; D.NAV = (int)H.affv_list.size(); D.NKV = (int)H.kin_vlist.size();

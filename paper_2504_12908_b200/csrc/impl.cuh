@@ -46,6 +46,7 @@ struct EnvCtl {
 struct Dev {
   // ---- dims ----
   int NNZ;                // off-diagonal soft blocks in row order (2·NEs)
+  int maxrl;              // longest soft BSR row (blocks)
   int E, V, T, NA, ND, NVall, NSV, NT, NE, NEs, NC, NK, NB, n, npads, NCOAT, NMARK;
   int cand_cap, act_cap, ent_cap, cpl_cap;
   // ---- config ----

@@ -1586,6 +1586,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
   const int* snb = D.snb + (size_t)e * 4 * D.act_cap * 2;
   const int* sbody = D.sbody + (size_t)e * 4 * D.act_cap;
   int* cvl = reinterpret_cast<int*>(dsm_asm);        // [V] soft vertices with contact records
+  double* accs = dsm_asm + (D.V + 3) / 2;             // [ngrp][maxrl][9] soft–soft block sums
   int cpl_run = 0, nct = 0;
   // phase 1 (thread per vertex): inertia, gravity, AL and elastic terms; body mask of the condensed
   // records; coupling offsets and the contact-vertex list by block scans
@@ -1642,6 +1643,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
     nct += totc;
   }
   __syncthreads();
+  CLK(16)
   // phase 2 (8-lane group per contact vertex): sum the vertex's condensed records, field-parallel
   // (lane l8 owns fields l8 + 8i of [g 3 | H_ss 9 | C 36]); entries in vertex-sorted order
   {
@@ -1686,19 +1688,45 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
           cval[(size_t)(f - 12) * D.cpl_cap + pos] = a;
         }
       }
-      // soft–soft contact blocks folded into row v's BSR blocks (lane l8 owns element l8, lane 0 also 8)
-      for (int j = jr; j < j1; ++j)
-        for (int nb = 0; nb < 2; ++nb) {
-          const int jb = snb[2 * j + nb];
-          if (jb < 0) continue;
-          double* hb = Hoe + (size_t)jb * 9;
-          const double* rec = srec + (size_t)j * SREC + 48 + 9 * nb;
-          hb[l8] += rec[l8];
-          if (l8 == 0) hb[8] += rec[8];
+      // soft–soft contact blocks folded into row v's BSR blocks (lane l8 owns element l8, lane 0 also 8):
+      // summed per block of row v in shared memory in record order, then one read-modify-write per
+      // touched block (independent, so the global round trips overlap)
+      if (D.maxrl <= 32) {
+        const int r0 = D.rptr[v], rl = D.rptr[v + 1] - r0;
+        double* acc = accs + (size_t)grp * D.maxrl * 9;
+        for (int sl = 0; sl < rl; ++sl) { acc[9 * sl + l8] = 0.0; if (l8 == 0) acc[9 * sl + 8] = 0.0; }
+        unsigned touched = 0u;
+        for (int j = jr; j < j1; ++j)
+          for (int nb = 0; nb < 2; ++nb) {
+            const int jb = snb[2 * j + nb];
+            if (jb < 0) continue;
+            const int sl = jb - r0;
+            touched |= 1u << sl;
+            const double* rec = srec + (size_t)j * SREC + 48 + 9 * nb;
+            acc[9 * sl + l8] += rec[l8];
+            if (l8 == 0) acc[9 * sl + 8] += rec[8];
+          }
+        for (unsigned m = touched; m; m &= m - 1u) {
+          const int sl = __ffs(m) - 1;
+          double* hb = Hoe + (size_t)(r0 + sl) * 9;
+          hb[l8] += acc[9 * sl + l8];
+          if (l8 == 0) hb[8] += acc[9 * sl + 8];
         }
+      } else {
+        for (int j = jr; j < j1; ++j)
+          for (int nb = 0; nb < 2; ++nb) {
+            const int jb = snb[2 * j + nb];
+            if (jb < 0) continue;
+            double* hb = Hoe + (size_t)jb * 9;
+            const double* rec = srec + (size_t)j * SREC + 48 + 9 * nb;
+            hb[l8] += rec[l8];
+            if (l8 == 0) hb[8] += rec[8];
+          }
+      }
     }
   }
   __syncthreads();
+  CLK(17)
   // phase 3: block-Jacobi inverses of the contact vertices
   for (int ci = threadIdx.x; ci < nct; ci += blockDim.x) {
     const int v = cvl[ci];
@@ -2931,7 +2959,7 @@ void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   }
 }
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  const int bytes = (D.V + 2) * (int)sizeof(int);
+  const int bytes = ((D.V + 3) / 2) * (int)sizeof(double) + (D.maxrl <= 32 ? (NTHREADS / 8) * D.maxrl * 9 * (int)sizeof(double) : 0);
   static int attr = 0;
   if (bytes > attr) { cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); attr = bytes; }
   k_assemble<<<ne, NTHREADS, bytes, s>>>(D, env0, force);

@@ -26,8 +26,6 @@ na = max(buf[14], 1)
 print(f"k_assemble: {buf[14]} CTA launches")
 for i, nm in zip(range(10, 14), ["edge blocks", "vertex loop", "body warps", "body pair terms"]):
     print(f"  {nm:16s} {buf[i] / na:9.0f} cyc")
-nt = 256 * na
-for i, nm in zip(range(16, 20), ["tets+init (per thread)", "records (per thread)", "tail (per thread)", "scan (CTA)"]):
-    print(f"  {nm:24s} {buf[i] / (na if i == 19 else nt):9.0f} cyc   max {buf[i + 4] if i < 19 else 0}")
+print(f"  vertex loop split: phase 1 {buf[16] / na:9.0f}  phase 2 {buf[17] / na:9.0f} cyc (phase 3 = rest)")
 s = b.stats()
 print("n_active mean", np.mean([x["n_active"] for x in s]), "max", max(x["n_active"] for x in s))
