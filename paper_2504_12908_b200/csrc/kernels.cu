@@ -10,6 +10,7 @@
 #include "geometry.cuh"
 #include "impl.cuh"
 #include "launch.h"
+#include <cstdlib>
 
 namespace tac {
 
@@ -1851,6 +1852,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
 // (one per soft edge; the lower block is its transpose), SoA diagonal blocks, body blocks, the
 // block-Jacobi inverses and the row/contribution index arrays
 struct SmemMat {
+  int lpr;                                        // soft-row lanes per row in the SpMV
   const double *U, *Hd, *Hb, *Ps, *Pb;
   double* cout;                                   // [3·ncpl] coupling outputs C_vd x_d (pass A2 → B)
   const int *rptr, *rcol, *rupx, *cptr, *rcnt, *cpp;
@@ -1996,20 +1998,22 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
   const double* Hd = R ? R->Hd : D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
   const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
   const int* rptr = R ? R->rptr : D.rptr;
-  // soft rows: 4 lanes per row; lane q of the group takes blocks j = rptr[v]+q, +4, ... (adjacent
-  // lanes read adjacent 72-byte blocks), then a 2-step shuffle reduction; lane q==0 adds the
-  // diagonal block and the contiguous pair outputs and stores
+  // soft rows: lpr lanes per row (streamed operator: 4; resident: 1, measured best); lane q of the
+  // group takes blocks j = rptr[v]+q, +lpr, ... (adjacent lanes read adjacent 72-byte blocks), then a
+  // shuffle reduction; lane q==0 adds the diagonal block and the contiguous pair outputs and stores
   {
-    const int q = lane & 3;
-    const int rows_per_pass = blockDim.x >> 2;
+    const int lpr = R ? R->lpr : 4;                  // lanes per row (1, 2 or 4)
+    const int q = lane & (lpr - 1);
+    const int rows_per_pass = blockDim.x / lpr;
     for (int v0 = 0; v0 < D.V; v0 += rows_per_pass) {
-      const int v = v0 + (threadIdx.x >> 2);
+      const int v = v0 + threadIdx.x / lpr;
       const bool live = v < D.V;
       v3 acc = mk(0, 0, 0);
       if (live) {
         const int j1 = rptr[v + 1];
         if (R) {
-          for (int j = rptr[v] + q; j < j1; j += 4) {
+#pragma unroll 4
+          for (int j = rptr[v] + q; j < j1; j += lpr) {
             const int ux = R->rupx[j];
             const double* Bk = R->U + 9 * (ux >> 1);
             const v3 xu = ld3(x + 3 * R->rcol[j]);
@@ -2019,7 +2023,7 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
           for (int j = rptr[v] + q; j < j1; j += 4) acc += mul33(Ho + 9 * j, ld3(x + 3 * D.rcol[j]));
         }
       }
-      for (int o = 1; o < 4; o <<= 1) {
+      for (int o = 1; o < lpr; o <<= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
         acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
@@ -2136,8 +2140,8 @@ __host__ __device__ inline size_t pcg_r_ncpl(const Dev& D) {          // couplin
   const size_t a = (size_t)D.V * D.ND, b = (size_t)D.cpl_cap;
   return a < b ? a : b;
 }
-__host__ __device__ inline size_t pcg_r_bytes(const Dev& D) {
-  const size_t nd = (size_t)(pcg_r_threads(D.V) / 32) * D.ND * 12 + 1 + 5 * (size_t)D.n + 9 * (size_t)D.NEs +
+__host__ __device__ inline size_t pcg_r_bytes(const Dev& D, int threads) {
+  const size_t nd = (size_t)(threads / 32) * D.ND * 12 + 1 + 5 * (size_t)D.n + 9 * (size_t)D.NEs +
                     18 * (size_t)D.V + 288 * (size_t)D.ND + 3 * pcg_r_ncpl(D);
   const size_t ni = 3 * ((size_t)D.V + 1) + (size_t)D.V + 2 * (size_t)D.NNZ;
   return nd * sizeof(double) + ni * sizeof(int);
@@ -2146,7 +2150,7 @@ __host__ __device__ inline size_t pcg_r_bytes(const Dev& D) {
 // env-resident PCG: one CTA (512 threads) per env with the condensed soft matrix, diagonal and body
 // blocks, preconditioner and index arrays staged once into shared memory; only the (few) residual
 // pairs and the soft–body couplings are read from global memory per iteration
-__global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int force) {
+__global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int force, int lpr) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
@@ -2185,7 +2189,7 @@ __global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int
   for (int i = threadIdx.x; i < 9 * D.NEs; i += blockDim.x)    // upper edge blocks (72-byte runs of Ho)
     U[i] = Ho[9 * (size_t)D.eup[i / 9] + i % 9];
   __syncthreads();
-  SmemMat R{U, Hd, Hb, Ps, Pb, couts, rptr, rcol, rupx, cptr, rcnt, cpp};
+  SmemMat R{lpr, U, Hd, Hb, Ps, Pb, couts, rptr, rcol, rupx, cptr, rcnt, cpp};
   pcg_body(D, e, 1, dsmem, red, &R, Ps, Pb);
 }
 
@@ -2974,11 +2978,16 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
     cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     configured = bytes;
   }
-  const size_t rb = pcg_r_bytes(D);
-  if (rb <= 227 * 1024) {                                 // env-resident PCG (one CTA per SM)
+  // env-resident PCG (one CTA per SM) when the condensed operator fits; lanes per soft row and the
+  // thread count can be overridden for experiments (TAC_PCG_LPR ∈ {1,2,4}, TAC_PCG_THREADS ≤ 512)
+  static const int lpr = getenv("TAC_PCG_LPR") ? atoi(getenv("TAC_PCG_LPR")) : 1;
+  static const int thr_env = getenv("TAC_PCG_THREADS") ? atoi(getenv("TAC_PCG_THREADS")) : 0;
+  const int thr = (thr_env >= 128 && thr_env <= PCG_R_THREADS && thr_env % 32 == 0) ? thr_env : pcg_r_threads(D.V);
+  const size_t rb = pcg_r_bytes(D, thr);
+  if (rb <= 227 * 1024) {
     static size_t rconf = 0;
     if (rb > rconf) { cudaFuncSetAttribute(k_pcg_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb); rconf = rb; }
-    k_pcg_r<<<ne, pcg_r_threads(D.V), rb, s>>>(D, env0, force);
+    k_pcg_r<<<ne, thr, rb, s>>>(D, env0, force, lpr == 2 || lpr == 4 ? lpr : 1);
     return;
   }
   k_pcg<<<ne, NTHREADS, bytes, s>>>(D, env0, force, vsm);
