@@ -2043,7 +2043,8 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
     }
   }
   CLK(3)
-  for (int i = threadIdx.x; i < nb12; i += blockDim.x) {
+  // body rows: taken by the highest thread indices (idle in the soft-row pass when V < blockDim)
+  for (int i = blockDim.x - 1 - threadIdx.x; i < nb12; i += blockDim.x) {
     const int d = i / 12, row = i % 12;
     const double* Hb = (R ? R->Hb + (size_t)d * 144 : D.Hb + ((size_t)e * D.ND + d) * 144) + 12 * row;
     const double* xb = x + 3 * D.V + 12 * d;
@@ -2261,7 +2262,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
           st3(z + 3 * v, zv);
           loc2 += rv.x * zv.x + rv.y * zv.y + rv.z * zv.z;
         }
-        for (int db = wi; db < D.ND; db += nwp) {         // body db: lanes 0..11 own its rows
+        for (int db = nwp - 1 - wi; db >= 0 && db < D.ND; db += nwp) {   // body db (last warps): lanes 0..11 own its rows
           const int o = 3 * V + 12 * db;
           if (lane < 12) {
             p[o + lane] += alpha * d[o + lane];
