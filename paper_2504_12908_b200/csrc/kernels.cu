@@ -1862,7 +1862,7 @@ struct SmemMat {
 // Returns this thread's partial Σ x_i y_i over the rows it wrote (for fused PCG dot products).
 constexpr int SPMV_ALL = 15;
 __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
-                       double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL) {
+                       double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL, int stream_lpr = 4) {
   const EnvCtl& C = D.ctl[e];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
@@ -2002,7 +2002,7 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
   // group takes blocks j = rptr[v]+q, +lpr, ... (adjacent lanes read adjacent 72-byte blocks), then a
   // shuffle reduction; lane q==0 adds the diagonal block and the contiguous pair outputs and stores
   {
-    const int lpr = R ? R->lpr : 4;                  // lanes per row (1, 2 or 4)
+    const int lpr = R ? R->lpr : stream_lpr;          // lanes per row (1, 2 or 4)
     const int q = lane & (lpr - 1);
     const int rows_per_pass = blockDim.x / lpr;
     for (int v0 = 0; v0 < D.V; v0 += rows_per_pass) {
@@ -2020,7 +2020,8 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
             acc += (ux & 1) ? mul33T(Bk, xu) : mul33(Bk, xu);
           }
         } else {
-          for (int j = rptr[v] + q; j < j1; j += 4) acc += mul33(Ho + 9 * j, ld3(x + 3 * D.rcol[j]));
+#pragma unroll 4
+          for (int j = rptr[v] + q; j < j1; j += lpr) acc += mul33(Ho + 9 * j, ld3(x + 3 * D.rcol[j]));
         }
       }
       for (int o = 1; o < lpr; o <<= 1) {
@@ -2116,14 +2117,15 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z, const S
 // Newton convergence test ‖p‖_emb,∞ ≤ τ_N L_env and gᵀp.
 // ------------------------------------------------------------------------------------------
 // vsm = 1: the five PCG vectors live in shared memory (n small enough), p is copied out at the end
-__device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb);
+__device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb,
+                         int fused = 0, int stream_lpr = 4);
 
-__global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force, int vsm) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force, int vsm, int fused, int lpr) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
   extern __shared__ double dsmem[];     // [nw][ND][12] body partials, then (vsm) p, r, z, d, Ad
-  pcg_body(D, e, vsm, dsmem, red, nullptr, nullptr, nullptr);
+  pcg_body(D, e, vsm, dsmem, red, nullptr, nullptr, nullptr, fused, lpr);
 }
 
 // shared-memory bytes of k_pcg_r for this batch (0 if the env does not fit one CTA)
@@ -2194,7 +2196,8 @@ __global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int
   pcg_body(D, e, 1, dsmem, red, &R, Ps, Pb);
 }
 
-__device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb) {
+__device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb,
+                         int fused, int stream_lpr) {
   double* bpart = dsmem;
   EnvCtl& C = D.ctl[e];
   const int n = D.n;
@@ -2230,8 +2233,8 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     zero_g = rz0 == 0.0;                                 // g = 0: p = 0 is the (converged) answer
     int it = 0;
     bad = !(rz0 == rz0);
-    if (R) {
-      // fused resident iteration, 4 barriers: [pass A | B2 | pass B + dᵀAd partials | B3 | α, p/r update,
+    if (R || fused) {
+      // fused iteration (resident or streamed operator), 4 barriers: [pass A | B2 | pass B + dᵀAd partials | B3 | α, p/r update,
       // block-Jacobi z and rᵀz partials per vertex / body | B4 | β, d update | B1].  Per-warp partials in
       // red[0..15] (dᵀAd) and red[16..31] (rᵀz), summed in warp order by every thread (deterministic)
       const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nwp = blockDim.x >> 5;
@@ -2239,10 +2242,13 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
       for (int i = threadIdx.x; i < nwp * nb12; i += blockDim.x) bpart[i] = 0.0;
       __syncthreads();
       while (!bad && it < D.max_pcg && rz > stop) {
-        double loc = spmv(D, e, d, Ad, bpart, mu, R, 2 | 4);
+        CLK_INIT
+        double loc = spmv(D, e, d, Ad, bpart, mu, R, 2 | 4, stream_lpr);
         loc = warp_sum(loc);
         if (lane == 0) red[wi] = loc;
+        CLK(5)
         __syncthreads();                                  // B3
+        CLK(6)
         double dAd = 0.0;
         for (int k = 0; k < nwp; ++k) dAd += red[k];
         if (!(dAd > 0.0)) { bad = true; __syncthreads(); break; }   // uniform; red[] reads done
@@ -2255,7 +2261,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
           pv[0] += alpha * dv.x; pv[1] += alpha * dv.y; pv[2] += alpha * dv.z;
           rv = mk(rv.x - alpha * av.x, rv.y - alpha * av.y, rv.z - alpha * av.z);
           st3(r + 3 * v, rv);
-          const double* Ps = R->Ps;
+          const double* Ps = R ? R->Ps : D.Pinv_s + (size_t)e * V * 9;
           const v3 zv = mk(Ps[v] * rv.x + Ps[V + v] * rv.y + Ps[2 * V + v] * rv.z,
                            Ps[3 * V + v] * rv.x + Ps[4 * V + v] * rv.y + Ps[5 * V + v] * rv.z,
                            Ps[6 * V + v] * rv.x + Ps[7 * V + v] * rv.y + Ps[8 * V + v] * rv.z);
@@ -2270,7 +2276,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
           }
           __syncwarp();
           if (lane < 12) {
-            const double* Pi = R->Pb + (size_t)db * 144 + 12 * lane;
+            const double* Pi = (R ? R->Pb : D.Pinv_b + (size_t)e * D.ND * 144) + (size_t)db * 144 + 12 * lane;
             double zz = 0.0;
             for (int c = 0; c < 12; ++c) zz += Pi[c] * r[o + c];
             z[o + lane] = zz;
@@ -2281,18 +2287,22 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
         for (int i = threadIdx.x; i < nwp * nb12; i += blockDim.x) bpart[i] = 0.0;   // read before B3
         loc2 = warp_sum(loc2);
         if (lane == 0) red[16 + wi] = loc2;
+        CLK(7)
         __syncthreads();                                  // B4
+        CLK(8)
         double rzn = 0.0;
         for (int k = 0; k < nwp; ++k) rzn += red[16 + k];
         const double beta = rzn / rz;
         for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = z[i] + beta * d[i];
         __syncthreads();                                  // B1
+        CLK(9)
+        if (threadIdx.x == 0) CLK_COUNT
         rz = rzn;
         ++it;
         if (!(rz == rz)) bad = true;
       }
     }
-    while (!R && !bad && it < D.max_pcg && rz > stop) {
+    while (!R && !fused && !bad && it < D.max_pcg && rz > stop) {
       spmv(D, e, d, Ad, bpart, mu, R);
       CLK_INIT
       part = 0.0;
@@ -2985,13 +2995,16 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   static const int thr_env = getenv("TAC_PCG_THREADS") ? atoi(getenv("TAC_PCG_THREADS")) : 0;
   const int thr = (thr_env >= 128 && thr_env <= PCG_R_THREADS && thr_env % 32 == 0) ? thr_env : pcg_r_threads(D.V);
   const size_t rb = pcg_r_bytes(D, thr);
-  if (rb <= 227 * 1024) {
+  static const int resident = getenv("TAC_PCG_RESIDENT") ? atoi(getenv("TAC_PCG_RESIDENT")) : 1;   // 0: always stream
+  if (resident && rb <= 227 * 1024) {
     static size_t rconf = 0;
     if (rb > rconf) { cudaFuncSetAttribute(k_pcg_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb); rconf = rb; }
     k_pcg_r<<<ne, thr, rb, s>>>(D, env0, force, lpr == 2 || lpr == 4 ? lpr : 1);
     return;
   }
-  k_pcg<<<ne, NTHREADS, bytes, s>>>(D, env0, force, vsm);
+  static const int sfused = getenv("TAC_PCG_STREAM_FUSED") ? atoi(getenv("TAC_PCG_STREAM_FUSED")) : 1;
+  static const int slpr = getenv("TAC_PCG_STREAM_LPR") ? atoi(getenv("TAC_PCG_STREAM_LPR")) : 1;
+  k_pcg<<<ne, NTHREADS, bytes, s>>>(D, env0, force, vsm, sfused, slpr == 2 || slpr == 4 ? slpr : 1);
 }
 void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s) {
   k_spmv<<<1, NTHREADS, spmv_smem(D), s>>>(D, env0, x, y);

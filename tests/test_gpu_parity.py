@@ -289,3 +289,18 @@ def test_schedule_matches_lockstep_bitwise(name, E, K):
     for k in range(K):
         for j in range(3):
             assert np.array_equal(out[j][k], ref[k][j])
+
+
+def test_streamed_pcg_path_parity():
+    """The streamed-operator PCG (k_pcg, used when an env's operator does not fit one SM, e.g. C3)
+    against the oracle PCG and direct solve on the same cases, forced with TAC_PCG_RESIDENT=0 in a
+    fresh process (the launch choice is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TAC_PCG_RESIDENT="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "pcg_matches_oracle",
+                        os.path.join(here, "test_gpu_parity.py")], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout

@@ -5,7 +5,7 @@ import numpy as np, torch
 sys.path.insert(0, "/root/repo")
 from paper_2504_12908_b200 import scenes as S, taccel as T
 E, W, K = (int(a) for a in sys.argv[1:4])
-NAMES = ["zero+sync", "pairs", "sync", "soft rows", "body rows+sync", "dAd sum", "p,r upd", "precond", "rz sum", "d upd"]
+NAMES = ["zero+sync", "pass A (pairs, couplings)", "B2 barrier", "soft rows", "body rows", "dAd warp sum", "B3 wait", "update+precond+rz", "B4 wait", "beta, d upd, B1"]
 sc = S.make_scene("C2")
 ei = S.env_inputs(sc, np.arange(E), n_steps=W + K)
 b = T.Batch(sc, E)
