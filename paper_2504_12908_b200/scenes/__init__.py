@@ -63,7 +63,7 @@ class Config:
     dt: float = 0.02
     dhat: float = 1.0e-4
     kappa: float = 1.0e8
-    max_step_rel: float = 5.0e-2
+    max_step_rel: float = 5.0e-2   # relative step cap (R17c)
     newton_tol_rel: float = 1.0e-7
     al_tol_rel: float = 1.0e-6
     pcg_eta: float = 1.0e-4
@@ -78,7 +78,7 @@ class Config:
     hessian_mode: int = 2          # 0: PSD-projected; 1: exact first + projected fallback (R14b); 2: exact + LM shift (R14c)
     ls_expand: int = 16            # line-search expansion bound K (R17b); 1 = plain backtracking
     hold_cap: int = 16             # max projected iterations between exact-Hessian attempts (R14b)
-    lm_mu0: float = 1.0            # first mass-scaled shift of hessian_mode 2 (R14c)
+    lm_mu0: float = 10.0           # first mass-scaled shift of hessian_mode 2 (R14c); 10 measured best on C2
     bp_margin: float = 1.0e-4      # δ of the reusable candidate list (R11b); 0 = rebuild every iteration
     cand_capacity_per_env: int = 65536
     active_capacity_per_env: int = 4096
