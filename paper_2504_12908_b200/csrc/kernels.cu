@@ -1104,6 +1104,22 @@ __device__ __forceinline__ void sd_make_y(int kind, int type, const v3* X, SubDi
   }
 }
 
+// butterfly reduce-scatter of 32 per-lane values over a warp: afterwards v[0] of lane l holds
+// Σ_lanes v[l] (fixed exchange pattern → deterministic); 31 shuffles for 32 sums
+__device__ __forceinline__ void warp_reduce_scatter32(double* v, int lane) {
+#pragma unroll
+  for (int m = 16, n = 32; m > 0; m >>= 1, n >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const double send = up ? v[i] : v[n / 2 + i];
+      const double keep = up ? v[n / 2 + i] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+}
+__constant__ unsigned char c_colpk[PH];    // column-order position be(be+1)/2+al → packed sym_idx(al, be)
+
 __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.y;
   if (env_skip(D, e, force)) return;
@@ -1388,48 +1404,54 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
 #pragma unroll
         for (int l = 0; l < 9; ++l) wm[l] = 0.0;
       }
-      // rolled loops (instruction-cache footprint); runtime indices resolved by selects
-      auto wsel = [&](int al, int jj) {
-        if (al < 3) return wc[jj];
-        const int q = (al - 3) % 3;
-        return q == 0 ? wm[3 * jj] : (q == 1 ? wm[3 * jj + 1] : wm[3 * jj + 2]);
-      };
-#pragma unroll 1
-      for (int al = 0; al < 12; ++al) {
-        const int ra = al < 3 ? al : (al - 3) / 3;
-        double v = 0.0;
-        if (mine)
+      // 32-entry chunks, each reduced over the warp by a butterfly reduce-scatter (31 shuffles per
+      // chunk instead of 5 per entry; fixed tree → deterministic); entries in column order
+      // p = be(be+1)/2 + al, lane l stores entry 32c + l of chunk c
+      {
+        double val[32];
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj)
-            v += wsel(al, jj) * (ra == 0 ? Gy[3 * jj] : (ra == 1 ? Gy[3 * jj + 1] : Gy[3 * jj + 2]));
-        v = warp_sum(v);
-        if (lane == al) out[al] = v;
-      }
-#pragma unroll 1
-      for (int be = 0; be < 12; ++be) {
-        const int rb = be < 3 ? be : (be - 3) / 3;
-        double zc[9];                  // zc[(j,r)] = Σ_l w_l(β) H_y[(j,r),(l,ρβ)]
-#pragma unroll
-        for (int jr = 0; jr < 9; ++jr) {
-          double z = 0.0;
-          if (mine)
-#pragma unroll
-            for (int l = 0; l < 3; ++l) z += wsel(be, l) * HYS(jr, 3 * l + rb);
-          zc[jr] = z;
-        }
-#pragma unroll 1
-        for (int al = 0; al <= be; ++al) {
+        for (int al = 0; al < 12; ++al) {
           const int ra = al < 3 ? al : (al - 3) / 3;
           double v = 0.0;
 #pragma unroll
-          for (int jj = 0; jj < 3; ++jj)
-            v += wsel(al, jj) * (ra == 0 ? zc[3 * jj] : (ra == 1 ? zc[3 * jj + 1] : zc[3 * jj + 2]));
-          const int idx = sym_idx(al, be, 12);
-          const double vc = warp_sum(res ? 0.0 : v);
-          if (lane == (idx & 31)) out[12 + idx] = vc;
-          if (anyres) {
-            const double vr = warp_sum(res ? v : 0.0);
-            if (lane == (idx & 31)) out[12 + PH + idx] = vr;
+          for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * Gy[3 * jj + ra];
+          val[al] = mine ? v : 0.0;
+        }
+#pragma unroll
+        for (int i = 12; i < 32; ++i) val[i] = 0.0;
+        warp_reduce_scatter32(val, lane);
+        if (lane < 12) out[lane] = val[0];
+      }
+      for (int pass = 0; pass < (anyres ? 2 : 1); ++pass) {
+        double val[32];
+#pragma unroll
+        for (int be = 0; be < 12; ++be) {
+          const int rb = be < 3 ? be : (be - 3) / 3;
+          double zc[9];                // zc[(j,r)] = Σ_l w_l(β) H_y[(j,r),(l,ρβ)]
+#pragma unroll
+          for (int jr = 0; jr < 9; ++jr) {
+            double z = 0.0;
+            if (mine)
+#pragma unroll
+              for (int l = 0; l < 3; ++l) z += (be < 3 ? wc[l] : wm[3 * l + (be - 3) % 3]) * HYS(jr, 3 * l + rb);
+            zc[jr] = z;
+          }
+#pragma unroll
+          for (int al = 0; al <= be; ++al) {
+            const int ra = al < 3 ? al : (al - 3) / 3;
+            double v = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) v += (al < 3 ? wc[jj] : wm[3 * jj + (al - 3) % 3]) * zc[3 * jj + ra];
+            const int pos = be * (be + 1) / 2 + al;
+            val[pos & 31] = (res == (pass == 1)) ? v : 0.0;
+            if ((pos & 31) == 31 || pos == PH - 1) {
+              if (pos == PH - 1)
+#pragma unroll
+                for (int i = (PH & 31); i < 32; ++i) val[i] = 0.0;
+              warp_reduce_scatter32(val, lane);
+              const int p0 = pos & ~31;
+              if (p0 + lane < PH) out[12 + pass * PH + c_colpk[p0 + lane]] = val[0];
+            }
           }
         }
       }
@@ -2940,7 +2962,11 @@ cudaError_t init_tables() {
   unsigned char r[PH], c[PH];
   for (int i = 0; i < 12; ++i)
     for (int j = i; j < 12; ++j) { int k = sym_idx(i, j, 12); r[k] = (unsigned char)i; c[k] = (unsigned char)j; }
+  unsigned char cp[PH];
+  for (int be = 0; be < 12; ++be)
+    for (int al = 0; al <= be; ++al) cp[be * (be + 1) / 2 + al] = (unsigned char)sym_idx(al, be, 12);
   cudaError_t err = cudaMemcpyToSymbol(c_unpack_r, r, PH);
+  if (err == cudaSuccess) err = cudaMemcpyToSymbol(c_colpk, cp, PH);
   if (err == cudaSuccess) err = cudaMemcpyToSymbol(c_unpack_c, c, PH);
   if (err == cudaSuccess) g_tables_ready = true;
   return err;
