@@ -1559,10 +1559,11 @@ __device__ void chol_inverse12_warp(const double* A, double* Ainv, double* L /*1
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int force) {
+// soft part of the assembly (elastic edge and diagonal blocks, gradient, condensed contact terms,
+// 3×3 block-Jacobi inverses); register-light, so it runs at higher occupancy than the body part
+__global__ void __launch_bounds__(NTHREADS, 3) k_assemble_soft(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
-  __shared__ JacobiScratch JS[NTHREADS / 32];
   __shared__ int shs[33];
   extern __shared__ double dsm_asm[];   // contact-vertex list [V] ints
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1764,6 +1765,35 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble(Dev D, int env0, int f
   }
   if (threadIdx.x == 0) { cpp[D.V] = cpl_run; C.n_cpl = cpl_run; }
   CLK(11)
+}
+
+// body part of the assembly: inertia, orthogonality, gravity and AL terms of the DoF bodies, the
+// pairs' body blocks (k_pairs_x partials) and the 12×12 block-Jacobi inverses
+__global__ void __launch_bounds__(NTHREADS, 2) k_assemble_body(Dev D, int env0, int force) {
+  const int e = env0 + blockIdx.x;
+  if (env_skip(D, e, force)) return;
+  __shared__ JacobiScratch JS[NTHREADS / 32];
+  __shared__ int shs[33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  EnvCtl& C = D.ctl[e];
+  const double* q = D.q + (size_t)e * D.n;
+  const double* qt = D.qt + (size_t)e * D.n;
+  double* g = D.g + (size_t)e * D.n;
+  const double* tb = D.tetbuf + (size_t)e * TETBUF * D.T;
+  const double* ag = D.act_g + (size_t)e * D.act_cap * 12;
+  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
+  const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
+  const int* bptr = D.bptr + (size_t)e * (D.ND + 1);
+  const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
+  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
+  const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
+  const int* ares = D.act_res + (size_t)e * D.act_cap;
+  const double dt2 = D.dt * D.dt, rho = C.rho;
+  const double* s_att = D.s_att + (size_t)e * D.NC * 3;
+  const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
+  const size_t cap = D.act_cap;
+  CLK_INIT
   // ---- affine DoF bodies: warp per body ----
   for (int d = w; d < D.ND; d += nw) {
     const int b = D.dof_body[d];
@@ -3002,8 +3032,9 @@ void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   const int bytes = ((D.V + 3) / 2) * (int)sizeof(double) + (D.maxrl <= 32 ? (NTHREADS / 8) * D.maxrl * 9 * (int)sizeof(double) : 0);
   static int attr = 0;
-  if (bytes > attr) { cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); attr = bytes; }
-  k_assemble<<<ne, NTHREADS, bytes, s>>>(D, env0, force);
+  if (bytes > attr) { cudaFuncSetAttribute(k_assemble_soft, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); attr = bytes; }
+  k_assemble_soft<<<ne, NTHREADS, bytes, s>>>(D, env0, force);
+  if (D.ND > 0) k_assemble_body<<<ne, NTHREADS, 0, s>>>(D, env0, force);
 }
 static size_t spmv_smem(const Dev& D) { return (size_t)(NTHREADS / 32) * D.ND * 12 * sizeof(double) + 8; }
 void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
