@@ -517,6 +517,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.sbody = C.take<int>(e * 4 * D.act_cap); D.brec = C.take<double>(e * D.act_cap * 2 * BREC);
   D.bpart = C.take<double>(e * (size_t)((D.act_cap + 31) / 32) * std::max(H.ND, 1) * BPART);
   D.qcnt = C.take<int>(e * (size_t)(H.NSV + H.NE) + 1);
+  D.qtmp = C.take<int>(e * (size_t)(H.NSV + H.NE) * 2 * 32 + 1);
   D.lsl = C.take<int>(e * (size_t)D.cand_cap);
   D.eterm = C.take<double>(e * 8);
   D.out_coat = C.take<double>(e * H.NCOAT * 3 + 1); D.out_mpos = C.take<double>(e * H.NMARK * 3 + 1);

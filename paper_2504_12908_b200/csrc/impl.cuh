@@ -134,6 +134,7 @@ struct Dev {
   int* ent;               // [E][ent_cap][2]
   int* big;               // [E][BIG_CAP]
   int* qcnt;              // [E][NSV+NE] broad-phase query counts → segment offsets
+  int* qtmp;              // [E][NSV+NE][2][32] per-query candidate slots of the broad phase
   int* lsl;               // [E][cand_cap] line-search candidate list (energy_terms lmode 1/2)
   double* tbox;           // [E][NT+NE][6] raw target boxes (broad-phase cache)
   double* vref;           // [E][NSV][6] reference boxes of surface vertices at the last build

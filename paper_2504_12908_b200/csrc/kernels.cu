@@ -156,7 +156,8 @@ __device__ __forceinline__ unsigned hcell(int i, int j, int k, int kind) {
   return (((unsigned)i * 73856093u) ^ ((unsigned)j * 19349663u) ^ ((unsigned)k * 83492791u) ^ (kind ? 0x9E3779B9u : 0u)) &
          (NBUCKET - 1);
 }
-constexpr int ENT_CODE_BITS = 26;      // hash entry: target code (2t + kind) | body id << 26
+constexpr int ENT_CODE_BITS = 26;
+constexpr int QTMP = 32;              // per-query candidate slot of the broad phase (larger: re-run)      // hash entry: target code (2t + kind) | body id << 26
 __device__ __forceinline__ int ccode(int i, int j, int k) { return i | (j << 10) | (k << 20); }
 
 struct BoxCtx {
@@ -224,7 +225,7 @@ __device__ __forceinline__ bool query_reaches(const Dev& D, double (*bb)[6], int
 
 template <bool EMIT>
 __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int* cnt_off, const int* ent, const int* big,
-                        int nbig, int qi, int* out_a, int* out_b, double (*bb)[6]) {
+                        int nbig, int qi, int* out_a, int* out_b, double (*bb)[6], int out_cap = INT_MAX) {
   const bool pt = qi < D.NSV;
   int qa, qbody, qv[2];
   v3 qlo, qhi;
@@ -249,7 +250,7 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
   int count = 0;
   const int kindbit = pt ? 0 : (1 << 30);
   auto accept = [&](int code, v3 tlo, v3 thi) {
-    if (EMIT) { out_a[count] = kindbit | qa; out_b[count] = code >> 1; }
+    if (EMIT && count < out_cap) { out_a[count] = kindbit | qa; out_b[count] = code >> 1; }
     ++count;
   };
   if (ncell > 4096) {  // huge query box: brute force over all targets of the kind
@@ -426,13 +427,29 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   }
   __syncthreads();
   const int nbig = min(nbig_s, BIG_CAP);
-  // queries: PT (surface vertices) then EE (edges).  Count every query (no per-tile barrier), one
-  // block scan over the counts in query order, then emit each query's segment and sort it by target
+  // queries: PT (surface vertices) then EE (edges).  Each query runs once, emitting into a private
+  // slot of QTMP entries (sorted by target there) and recording its count; one block scan in query
+  // order; then the slots are copied to the candidate list.  A query with more than QTMP candidates
+  // is re-run straight into the list.
   int* ca = D.cand_a + (size_t)e * D.cand_cap;
   int* cb = D.cand_b + (size_t)e * D.cand_cap;
   const int nq = D.NSV + D.NE;
   int* qc = D.qcnt + (size_t)e * (D.NSV + D.NE);
-  for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) qc[qi] = bp_query<false>(D, B, G, cnt, ent, big, nbig, qi, nullptr, nullptr, bb);
+  int* qta = D.qtmp + (size_t)e * (D.NSV + D.NE) * 2 * QTMP;
+  auto sort_seg = [](int* sa, int* sb, int c) {           // insertion sort by target index
+    for (int i = 1; i < c; ++i) {
+      int kb = sb[i], ka = sa[i];
+      int j = i - 1;
+      while (j >= 0 && sb[j] > kb) { sb[j + 1] = sb[j]; sa[j + 1] = sa[j]; --j; }
+      sb[j + 1] = kb; sa[j + 1] = ka;
+    }
+  };
+  for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) {
+    int* ta = qta + (size_t)qi * 2 * QTMP;
+    const int c = bp_query<true>(D, B, G, cnt, ent, big, nbig, qi, ta, ta + QTMP, bb, QTMP);
+    if (c <= QTMP) sort_seg(ta, ta + QTMP, c);
+    qc[qi] = c;
+  }
   __syncthreads();
   int total;
   {
@@ -446,15 +463,13 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   __syncthreads();
   for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) {
     const int base = qc[qi], c = (qi + 1 < nq ? qc[qi + 1] : total) - base;
-    if (c > 0 && base + c <= D.cand_cap) {
+    if (c <= 0 || base + c > D.cand_cap) continue;
+    if (c <= QTMP) {
+      const int* ta = qta + (size_t)qi * 2 * QTMP;
+      for (int i = 0; i < c; ++i) { ca[base + i] = ta[i]; cb[base + i] = ta[QTMP + i]; }
+    } else {
       bp_query<true>(D, B, G, cnt, ent, big, nbig, qi, ca + base, cb + base, bb);
-      // insertion sort of this query's segment by target index
-      for (int i = 1; i < c; ++i) {
-        int kb = cb[base + i], ka = ca[base + i];
-        int j = i - 1;
-        while (j >= 0 && cb[base + j] > kb) { cb[base + j + 1] = cb[base + j]; ca[base + j + 1] = ca[base + j]; --j; }
-        cb[base + j + 1] = kb; ca[base + j + 1] = ka;
-      }
+      sort_seg(ca + base, cb + base, c);
     }
   }
   if (threadIdx.x == 0) {
