@@ -615,48 +615,42 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
     int* rc = D.rcnt + (size_t)e * D.V;
     for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
       int b0 = cptr[v], b1 = cptr[v + 1], nr = 0;
-      for (int i = b0; i < b1; ++i) {
-        const int res = ares[clist[i] >> 2];
-        nr += res;
-        clist[i] |= (res ? 0 : 1) << 30;
+      if (b1 - b0 <= 32) {                                // sort a private copy (L1), not global memory
+        int kk[32];
+        const int c = b1 - b0;
+        for (int i = 0; i < c; ++i) {
+          const int key = clist[b0 + i];
+          const int res = ares[key >> 2];
+          nr += res;
+          kk[i] = key | ((res ? 0 : 1) << 30);
+        }
+        for (int i = 1; i < c; ++i) {
+          int key = kk[i], j = i - 1;
+          while (j >= 0 && kk[j] > key) { kk[j + 1] = kk[j]; --j; }
+          kk[j + 1] = key;
+        }
+        for (int i = 0; i < c; ++i) {
+          const int key = kk[i] & ((1 << 30) - 1);
+          clist[b0 + i] = key;
+          spos[key] = b0 + i;                             // soft slot → its vertex-sorted position
+        }
+      } else {
+        for (int i = b0; i < b1; ++i) {
+          const int res = ares[clist[i] >> 2];
+          nr += res;
+          clist[i] |= (res ? 0 : 1) << 30;
+        }
+        for (int i = b0 + 1; i < b1; ++i) {
+          int key = clist[i], j = i - 1;
+          while (j >= b0 && clist[j] > key) { clist[j + 1] = clist[j]; --j; }
+          clist[j + 1] = key;
+        }
+        for (int i = b0; i < b1; ++i) clist[i] &= (1 << 30) - 1;
+        for (int i = b0; i < b1; ++i) spos[clist[i]] = i;
       }
-      for (int i = b0 + 1; i < b1; ++i) {
-        int key = clist[i], j = i - 1;
-        while (j >= b0 && clist[j] > key) { clist[j + 1] = clist[j]; --j; }
-        clist[j + 1] = key;
-      }
-      for (int i = b0; i < b1; ++i) clist[i] &= (1 << 30) - 1;
-      for (int i = b0; i < b1; ++i) spos[clist[i]] = i;   // soft slot → its vertex-sorted position
       rc[v] = nr;
     }
   }
-  // body contribution lists: pairs touching each DoF body, ascending, entry (k << 1) | record index
-  // (record 0 = the pair's lower DoF body, 1 = the higher)
-  int* bptr = D.bptr + (size_t)e * (D.ND + 1);
-  int* blist = D.blist + (size_t)e * 4 * D.act_cap;
-  const int* aslot_all = D.act_slot + (size_t)e * 4 * D.act_cap;
-  int run = 0;
-  for (int d = 0; d < D.ND; ++d) {
-    if (threadIdx.x == 0) bptr[d] = run;
-    for (int t0 = 0; t0 < nact; t0 += blockDim.x) {
-      const int k = t0 + threadIdx.x;
-      int c = 0, rec = 0;
-      if (k < nact) {
-        const int4 c4 = reinterpret_cast<const int4*>(aslot_all)[k];
-        const int codes[4] = {c4.x, c4.y, c4.z, c4.w};
-        for (int s = 0; s < 4; ++s) {
-          const int cd = codes[s];
-          if (cd == -1 - d) c = 1;
-          else if (cd < 0 && cd != INT_MIN && -1 - cd < d) rec = 1;
-        }
-      }
-      int tot;
-      const int ex = block_excl_scan(c, sh, &tot);
-      if (c) blist[run + ex] = (k << 1) | rec;
-      run += tot;
-    }
-  }
-  if (threadIdx.x == 0) bptr[D.ND] = run;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1591,8 +1585,6 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_assemble_soft(Dev D, int env0, 
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
   const int* cptr = D.cptr + (size_t)e * (D.V + 1);
   const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
-  const int* bptr = D.bptr + (size_t)e * (D.ND + 1);
-  const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
   const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
   const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
   const int* ares = D.act_res + (size_t)e * D.act_cap;
@@ -1799,8 +1791,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble_body(Dev D, int env0, 
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
   const int* cptr = D.cptr + (size_t)e * (D.V + 1);
   const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
-  const int* bptr = D.bptr + (size_t)e * (D.ND + 1);
-  const int* blist = D.blist + (size_t)e * 4 * D.act_cap;
   const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
   const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
   const int* ares = D.act_res + (size_t)e * D.act_cap;
