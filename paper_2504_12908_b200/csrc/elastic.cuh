@@ -69,8 +69,11 @@ HD double nh_energy(const v3* x, const double* Dmi, double mu, double lam, bool*
 }
 
 // Gradient g[12] (slot-major: 3*k + c) and packed-upper projected Hessian H[78] of scale·Ψ(F(x)).
-HD void nh_grad_hess(const v3* x, const double* Dmi, double mu, double lam, double scale, double* psi_out,
-                     double* g, double* H, bool project = true) {
+// Outputs go through store functors: gst(i, value) for the 12 gradient entries, hst(packed index, value)
+// for the 78 Hessian entries (k_tets stores straight to its SoA buffer, no local arrays)
+template <class GStore, class HStore>
+HD void nh_grad_hess_t(const v3* x, const double* Dmi, double mu, double lam, double scale, double* psi_out,
+                       GStore gst, HStore hst, bool project) {
   double F[9];
   deformation_gradient(x, Dmi, F);
   double J = det33(F);
@@ -89,27 +92,31 @@ HD void nh_grad_hess(const v3* x, const double* Dmi, double mu, double lam, doub
   double cP = lam * lnJ - mu;
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) P[3 * a + b] = mu * F[3 * a + b] + cP * Fi[3 * b + a];
-  for (int k = 0; k < 4; ++k) st3(g + 3 * k, scale * mul33(P, beta[k]));
+  for (int k = 0; k < 4; ++k) {
+    const v3 gk = scale * mul33(P, beta[k]);
+    gst(3 * k, gk.x); gst(3 * k + 1, gk.y); gst(3 * k + 2, gk.z);
+  }
   // h_k = F⁻ᵀ β_k
   v3 h[4];
   for (int k = 0; k < 4; ++k) h[k] = mul33T(Fi, beta[k]);
-  // SVD via eig(FᵀF): F = U Σ Vᵀ
-  double C[9], sig2[3], Vm[9];
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) C[3 * a + b] = F[a] * F[b] + F[3 + a] * F[3 + b] + F[6 + a] * F[6 + b];
-  sym3_eig(C, sig2, Vm);
-  double sg[3];
-  for (int i = 0; i < 3; ++i) sg[i] = sqrt(fmax(sig2[i], 0.0));
-  double U[9];  // U = F V Σ⁻¹ (columns)
-  for (int i = 0; i < 3; ++i) {
-    v3 vi = mk(Vm[i], Vm[3 + i], Vm[6 + i]);
-    v3 ui = (1.0 / sg[i]) * mul33(F, vi);
-    U[i] = ui.x; U[3 + i] = ui.y; U[6 + i] = ui.z;
-  }
   const double kk = mu - lam * lnJ;
-  // negative modes: collect up to 9 (λ_m, Q_m) and subtract
+  // negative modes: collect up to 9 (λ_m, Q_m) and subtract (projected Hessians only; the exact
+  // Hessian of the default LM Newton, R14c, needs no singular values)
   double negl[9]; double negQ[9][9]; int nneg = 0;
   if (project) {
+    // SVD via eig(FᵀF): F = U Σ Vᵀ
+    double C[9], sig2[3], Vm[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) C[3 * a + b] = F[a] * F[b] + F[3 + a] * F[3 + b] + F[6 + a] * F[6 + b];
+    sym3_eig(C, sig2, Vm);
+    double sg[3];
+    for (int i = 0; i < 3; ++i) sg[i] = sqrt(fmax(sig2[i], 0.0));
+    double U[9];  // U = F V Σ⁻¹ (columns)
+    for (int i = 0; i < 3; ++i) {
+      v3 vi = mk(Vm[i], Vm[3 + i], Vm[6 + i]);
+      v3 ui = (1.0 / sg[i]) * mul33(F, vi);
+      U[i] = ui.x; U[3 + i] = ui.y; U[6 + i] = ui.z;
+    }
     double A3[9];
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j)
@@ -156,9 +163,14 @@ HD void nh_grad_hess(const v3* x, const double* Dmi, double mu, double lam, doub
       double v = lam * comp(h[k], c) * comp(h[l], d) + kk * comp(h[l], c) * comp(h[k], d);
       if (c == d) v += mu * dot(beta[k], beta[l]);
       for (int m = 0; m < nneg; ++m) v -= negl[m] * comp(qb[m][k], c) * comp(qb[m][l], d);
-      H[sym_idx(r, s, 12)] = scale * v;
+      hst(sym_idx(r, s, 12), scale * v);
     }
   }
+}
+HD void nh_grad_hess(const v3* x, const double* Dmi, double mu, double lam, double scale, double* psi_out,
+                     double* g, double* H, bool project = true) {
+  nh_grad_hess_t(x, Dmi, mu, lam, scale, psi_out, [&](int i, double v) { g[i] = v; },
+                 [&](int i, double v) { H[i] = v; }, project);
 }
 
 // ABD orthogonality energy E = κ V ‖AAᵀ − I‖²_F (reading R9 of the garbled ARAP term P:L116):

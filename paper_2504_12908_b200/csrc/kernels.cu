@@ -667,14 +667,13 @@ __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
   double Dmi[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) Dmi[i] = D.Dmi[9 * t + i];
-  double g[12], H[PH];
   const double scale = D.dt * D.dt * D.vol[t];
-  nh_grad_hess(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, g, H, !D.ctl[e].exact);
-  double* out = D.tetbuf + (size_t)e * TETBUF * D.T;
-#pragma unroll
-  for (int i = 0; i < 12; ++i) out[(size_t)i * D.T + t] = g[i];
-#pragma unroll
-  for (int i = 0; i < PH; ++i) out[(size_t)(12 + i) * D.T + t] = H[i];
+  double* out = D.tetbuf + (size_t)e * TETBUF * D.T + t;     // SoA [90][T], stored as computed
+  const size_t T = D.T;
+  auto gst = [&](int i, double v) { out[(size_t)i * T] = v; };
+  auto hst = [&](int i, double v) { out[(size_t)(12 + i) * T] = v; };
+  if (D.ctl[e].exact) nh_grad_hess_t(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, gst, hst, false);
+  else nh_grad_hess_t(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, gst, hst, true);
 }
 
 // ------------------------------------------------------------------------------------------
