@@ -2541,33 +2541,41 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
     double psi = nh_energy(x, D.Dmi + 9 * t, D.mu[t], D.lam[t], &bad);
     if (bad) inv = 1; else eel += dt2 * D.vol[t] * psi;
   }
-  for (int d = threadIdx.x; d < D.ND; d += blockDim.x) {
-    int b = D.dof_body[d];
-    double y[12], dy[12];
-    for (int i = 0; i < 12; ++i) {
-      y[i] = q[3 * D.V + 12 * d + i] + alpha * p[3 * D.V + 12 * d + i];
-      dy[i] = y[i] - qt[3 * D.V + 12 * d + i];
-    }
-    const double* M = D.My + (size_t)b * 144;
-    double s = 0.0;
-    for (int i = 0; i < 12; ++i) { double t = 0.0; for (int j = 0; j < 12; ++j) t += M[12 * i + j] * dy[j]; s += dy[i] * t; }
-    ein += 0.5 * s;
-    v3 As1 = mul33(y + 3, ld3(D.bs1 + 3 * b));
-    egr -= dt2 * dot(G, D.bmass[b] * mk(y[0], y[1], y[2]) + As1);
-    eor += ortho_energy(y + 3, dt2 * D.bkappa[b] * D.bvol[b]);
-    int ki = D.kin_of_body[b];
-    if (ki >= 0) {
-      const double* sk = D.s_kin + ((size_t)e * D.NK + ki) * 12;
-      const double* lk = D.lam_kin + ((size_t)e * D.NK + ki) * 12;
-      double r[12];
-      for (int i = 0; i < 12; ++i) r[i] = y[i] - sk[i];
+  // affine DoF bodies: warp per body, lane i < 12 owns DoF i (row i of M^y); products through shuffles
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    for (int d = wid; d < D.ND; d += nwb) {
+      const int b = D.dof_body[d];
+      const int i = lane < 12 ? lane : 11;
+      const size_t o = 3 * (size_t)D.V + 12 * (size_t)d + i;
+      const double yi = q[o] + alpha * p[o];
+      const double dyi = yi - qt[o];
+      const double* Mrow = D.My + (size_t)b * 144 + 12 * i;
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < 12; ++j) t += Mrow[j] * __shfl_sync(0xffffffffu, dyi, j);
+      const double s = warp_sum(lane < 12 ? dyi * t : 0.0);
+      const int ki = D.kin_of_body[b];
       double a1 = 0.0, a2 = 0.0;
-      for (int i = 0; i < 12; ++i) {
+      if (ki >= 0) {
+        const double ri = yi - D.s_kin[((size_t)e * D.NK + ki) * 12 + i];
+        const double li = D.lam_kin[((size_t)e * D.NK + ki) * 12 + i];
         double Mr = 0.0;
-        for (int j = 0; j < 12; ++j) Mr += M[12 * i + j] * r[j];
-        a1 += r[i] * Mr; a2 += lk[i] * Mr;
+#pragma unroll
+        for (int j = 0; j < 12; ++j) Mr += Mrow[j] * __shfl_sync(0xffffffffu, ri, j);
+        a1 = warp_sum(lane < 12 ? ri * Mr : 0.0);
+        a2 = warp_sum(lane < 12 ? li * Mr : 0.0);
       }
-      eal += 0.5 * rho * a1 - a2;
+      double yv[12];
+#pragma unroll
+      for (int j = 0; j < 12; ++j) yv[j] = __shfl_sync(0xffffffffu, yi, j);
+      if (lane == 0) {
+        ein += 0.5 * s;
+        const v3 As1 = mul33(yv + 3, ld3(D.bs1 + 3 * b));
+        egr -= dt2 * dot(G, D.bmass[b] * mk(yv[0], yv[1], yv[2]) + As1);
+        eor += ortho_energy(yv + 3, dt2 * D.bkappa[b] * D.bvol[b]);
+        if (ki >= 0) eal += 0.5 * rho * a1 - a2;
+      }
     }
   }
   // barrier over candidates active at the trial point
