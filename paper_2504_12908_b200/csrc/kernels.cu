@@ -1573,6 +1573,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_assemble_soft(Dev D, int env0, 
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ int shs[33];
+  __shared__ int next_cv;
   extern __shared__ double dsm_asm[];   // contact-vertex list [V] ints
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   EnvCtl& C = D.ctl[e];
@@ -1677,10 +1678,19 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_assemble_soft(Dev D, int env0, 
   // phase 2 (8-lane group per contact vertex): sum the vertex's condensed records, field-parallel
   // (lane l8 owns fields l8 + 8i of [g 3 | H_ss 9 | C 36]); entries in vertex-sorted order
   {
-    const int l8 = threadIdx.x & 7, grp = threadIdx.x >> 3, ngrp = blockDim.x >> 3;
+    const int l8 = threadIdx.x & 7, grp = threadIdx.x >> 3;
     double* hd = D.Hd + (size_t)e * D.V * 9;
     double* ds = D.Dg_s + (size_t)e * D.V * 9;
-    for (int ci = grp; ci < nct; ci += ngrp) {
+    // dynamic assignment of contact vertices to 8-lane groups (a vertex is summed by one group in a
+    // fixed record order, so results do not depend on the assignment)
+    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+    if (threadIdx.x == 0) next_cv = 0;
+    __syncthreads();
+    for (;;) {
+      int ci = 0;
+      if (l8 == 0) ci = atomicAdd(&next_cv, 1);
+      ci = __shfl_sync(gmask, ci, threadIdx.x & 24);
+      if (ci >= nct) break;
       const int v = cvl[ci];
       const int j0 = cptr[v], jr = j0 + rcnt[v], j1 = cptr[v + 1];
       unsigned bmask = 0u;
