@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   __shared__ int cur[NBUCKET];
   __shared__ double red[32];
   __shared__ int sh[33];
-  __shared__ int nbig_s, ovf_s;
+  __shared__ int nbig_s, ovf_s, next_q;
   BoxCtx B{D.P + (size_t)e * D.NVall * 3, D.Pd + (size_t)e * D.NVall * 3, swept,
            D.tbox + (size_t)e * (D.NT + D.NE) * 6, D.NT, D.dhat + 2.0 * margin};
   // reference boxes of the surface vertices for the reuse test
@@ -444,7 +444,16 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
       sb[j + 1] = kb; sa[j + 1] = ka;
     }
   };
-  for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) {
+  // queries handed out 32 at a time to warps (dynamic balance; each query's output depends only on qi)
+  if (threadIdx.x == 0) next_q = 0;
+  __syncthreads();
+  for (;;) {
+    int qb = 0;
+    if ((threadIdx.x & 31) == 0) qb = atomicAdd(&next_q, 32);
+    qb = __shfl_sync(0xffffffffu, qb, 0);
+    if (qb >= nq) break;
+    const int qi = qb + (threadIdx.x & 31);
+    if (qi >= nq) continue;
     int* ta = qta + (size_t)qi * 2 * QTMP;
     const int c = bp_query<true>(D, B, G, cnt, ent, big, nbig, qi, ta, ta + QTMP, bb, QTMP);
     if (c <= QTMP) sort_seg(ta, ta + QTMP, c);
