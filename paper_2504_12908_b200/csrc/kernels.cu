@@ -470,7 +470,15 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     for (int q = q0; q < q1; ++q) { const int c = qc[q]; qc[q] = ex; ex += c; }
   }
   __syncthreads();
-  for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) {
+  if (threadIdx.x == 0) next_q = 0;
+  __syncthreads();
+  for (;;) {
+    int qb = 0;
+    if ((threadIdx.x & 31) == 0) qb = atomicAdd(&next_q, 32);
+    qb = __shfl_sync(0xffffffffu, qb, 0);
+    if (qb >= nq) break;
+    const int qi = qb + (threadIdx.x & 31);
+    if (qi >= nq) continue;
     const int base = qc[qi], c = (qi + 1 < nq ? qc[qi + 1] : total) - base;
     if (c <= 0 || base + c > D.cand_cap) continue;
     if (c <= QTMP) {
@@ -2494,7 +2502,18 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_ccd(Dev D, int env0, int force)
   const int* ca = D.cand_a + (size_t)e * D.cand_cap;
   const int* cb = D.cand_b + (size_t)e * D.cand_cap;
   double amin = 1.0;
-  for (int k = threadIdx.x; k < C.ncand; k += blockDim.x) {
+  // candidates handed to warps 32 at a time (dynamic balance; the minimum is order-independent)
+  __shared__ int next_k;
+  if (threadIdx.x == 0) next_k = 0;
+  __syncthreads();
+  const int nck = C.ncand;
+  for (;;) {
+    int kb = 0;
+    if ((threadIdx.x & 31) == 0) kb = atomicAdd(&next_k, 32);
+    kb = __shfl_sync(0xffffffffu, kb, 0);
+    if (kb >= nck) break;
+    const int k = kb + (threadIdx.x & 31);
+    if (k >= nck) continue;
     int kind = (ca[k] >> 30) & 1, a = ca[k] & ((1 << 30) - 1), b = cb[k], vid[4];
     pair_vids(D, kind, a, b, vid);
     v3 X[4], Q[4];
