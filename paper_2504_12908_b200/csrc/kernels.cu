@@ -227,7 +227,7 @@ template <bool EMIT>
 __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int* cnt_off, const int* ent, const int* big,
                         int nbig, int qi, int* out_a, int* out_b, double (*bb)[6], int out_cap = INT_MAX) {
   const bool pt = qi < D.NSV;
-  int qa, qbody, qv[2];
+  int qa, qbody;
   v3 qlo, qhi;
   if (pt) {
     qa = D.sverts[qi];
@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   const double margin = force ? 0.0 : D.bp_margin;
   __shared__ int cnt[NBUCKET + 1];
   __shared__ int cur[NBUCKET];
-  __shared__ double red[32];
   __shared__ int sh[33];
   __shared__ int nbig_s, ovf_s, next_q;
   BoxCtx B{D.P + (size_t)e * D.NVall * 3, D.Pd + (size_t)e * D.NVall * 3, swept,
@@ -1592,23 +1591,15 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_assemble_soft(Dev D, int env0, 
   __shared__ int shs[33];
   __shared__ int next_cv;
   extern __shared__ double dsm_asm[];   // contact-vertex list [V] ints
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   EnvCtl& C = D.ctl[e];
   const double* q = D.q + (size_t)e * D.n;
   const double* qt = D.qt + (size_t)e * D.n;
   double* g = D.g + (size_t)e * D.n;
   const double* tb = D.tetbuf + (size_t)e * TETBUF * D.T;
-  const double* ag = D.act_g + (size_t)e * D.act_cap * 12;
-  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
   const int* cptr = D.cptr + (size_t)e * (D.V + 1);
-  const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
-  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
-  const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
-  const int* ares = D.act_res + (size_t)e * D.act_cap;
   const double dt2 = D.dt * D.dt, rho = C.rho;
   const double* s_att = D.s_att + (size_t)e * D.NC * 3;
   const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
-  const size_t cap = D.act_cap;
   CLK_INIT
   // ---- soft edge blocks (elastic) ----
   for (int ei = threadIdx.x; ei < D.NNZ; ei += blockDim.x) {
@@ -1806,24 +1797,12 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble_body(Dev D, int env0, 
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ JacobiScratch JS[NTHREADS / 32];
-  __shared__ int shs[33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   EnvCtl& C = D.ctl[e];
   const double* q = D.q + (size_t)e * D.n;
   const double* qt = D.qt + (size_t)e * D.n;
   double* g = D.g + (size_t)e * D.n;
-  const double* tb = D.tetbuf + (size_t)e * TETBUF * D.T;
-  const double* ag = D.act_g + (size_t)e * D.act_cap * 12;
-  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
-  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
-  const int* clist = D.clist + (size_t)e * 4 * D.act_cap;
-  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
-  const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
-  const int* ares = D.act_res + (size_t)e * D.act_cap;
   const double dt2 = D.dt * D.dt, rho = C.rho;
-  const double* s_att = D.s_att + (size_t)e * D.NC * 3;
-  const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
-  const size_t cap = D.act_cap;
   CLK_INIT
   // ---- affine DoF bodies: warp per body ----
   for (int d = w; d < D.ND; d += nw) {
