@@ -1585,7 +1585,8 @@ __device__ void chol_inverse12_warp(const double* A, double* Ainv, double* L /*1
 
 // soft part of the assembly (elastic edge and diagonal blocks, gradient, condensed contact terms,
 // 3×3 block-Jacobi inverses); register-light, so it runs at higher occupancy than the body part
-__global__ void __launch_bounds__(NTHREADS, 3) k_assemble_soft(Dev D, int env0, int force) {
+constexpr int ASM_SOFT_MAX = 320;
+__global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int env0, int force) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ int shs[33];
@@ -3059,10 +3060,12 @@ void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   }
 }
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  const int bytes = ((D.V + 3) / 2) * (int)sizeof(double) + (D.maxrl <= 32 ? (NTHREADS / 8) * D.maxrl * 9 * (int)sizeof(double) : 0);
+  // threads: one per soft vertex in a single pass when V ≤ 320 (rounded to warps), else 256
+  const int thr = D.V <= ASM_SOFT_MAX ? std::max(128, (D.V + 31) / 32 * 32) : NTHREADS;
+  const int bytes = ((D.V + 3) / 2) * (int)sizeof(double) + (D.maxrl <= 32 ? (thr / 8) * D.maxrl * 9 * (int)sizeof(double) : 0);
   static int attr = 0;
   if (bytes > attr) { cudaFuncSetAttribute(k_assemble_soft, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); attr = bytes; }
-  k_assemble_soft<<<ne, NTHREADS, bytes, s>>>(D, env0, force);
+  k_assemble_soft<<<ne, thr, bytes, s>>>(D, env0, force);
   if (D.ND > 0) k_assemble_body<<<ne, NTHREADS, 0, s>>>(D, env0, force);
 }
 static size_t spmv_smem(const Dev& D) { return (size_t)(NTHREADS / 32) * D.ND * 12 * sizeof(double) + 8; }
