@@ -501,17 +501,16 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
 // contact condensation test (impl.cuh): a pair stays matrix-free ("residual") if two of its soft
 // slots are not adjacent in the soft BSR pattern or its slots span two different DoF bodies
 __device__ bool pair_is_residual(const Dev& D, const int* vid) {
-  int body = -1;
+  // soft slots of one primitive are BSR-adjacent (triangle and edge edges are tet edges), and the two
+  // primitives of a pair lie on different bodies (no self contact, reading R8), so two soft slots are
+  // non-adjacent exactly when they lie on different soft bodies — no search of the BSR rows is needed
+  int sbody = -1, body = -1;
   for (int s = 0; s < 4; ++s) {
     const int v = vid[s];
     if (v < D.V) {
-      for (int t = s + 1; t < 4; ++t) {
-        const int w = vid[t];
-        if (w >= D.V) continue;
-        bool adj = false;
-        for (int j = D.rptr[v]; j < D.rptr[v + 1] && !adj; ++j) adj = D.rcol[j] == w;
-        if (!adj) return true;
-      }
+      const int b = D.vert_body[v];
+      if (sbody >= 0 && b != sbody) return true;
+      sbody = b;
     } else {
       const int d = D.dof_slot[D.vert_aff[v]];
       if (d >= 0) {
