@@ -240,6 +240,9 @@ def main():
         outs = tuple(torch.empty(t.shape, dtype=torch.float64).pin_memory() for t in out_dev)
         h2d = ykin_host.numel() * 8 // K
         d2h = sum(t.numel() * 8 for t in outs) // K
+        # one untimed replay warms the stream-ordered staging pool, then the timed replay
+        batch.step_schedule(ykin_host, out=outs)
+        batch.set_state(x, y, xd, yd)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()

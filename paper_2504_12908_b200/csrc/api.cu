@@ -598,6 +598,15 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   const HostT& H = b->H;
   Dev& D = b->D;
   cudaError_t e = init_tables();
+  // host-buffer calls (tac_step_schedule with host pointers) stage through stream-ordered allocations;
+  // keep freed pool memory mapped so repeated calls do not re-map it
+  if (e == cudaSuccess) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, need, st);
 #define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
   UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
