@@ -303,6 +303,8 @@ def main():
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS.get(a.config, a.config), "envs_per_gpu": E, "envs_total": n_env_total, "dt": dt,
                    "stepping": "tac_step_schedule: device-resident target table, per-step readout, envs advance independently",
+                   "timing_note": "per-kernel CUDA events are recorded inside the device-timed region (roofline, gpu_launches; "
+                                  "about 2% overhead); the e2e replay runs without them",
                    "episode_steps_timed": f"{W}-{W + K - 1}", "parallelism": f"env-sharded x{world}",
                    "l2": "inputs larger than L2: per-step working set ~%.1f GB/GPU > 126 MB L2" %
                          (batch.workspace.numel() / 1e9)},
