@@ -43,6 +43,7 @@ struct HostT {
   std::vector<int> rptr, rcol, rblk_ptr, rblk;   // row-ordered symmetric BSR (off-diagonal)
   std::vector<int> rupx;                         // [NNZ] 2·(edge id) + (block stored transposed)
   std::vector<int> eup;                          // [NEs] row-ordered index of the edge's upper block
+  std::vector<int> tri_blk, edge_blk;            // [NT][6], [NE][2] BSR index of (v_i, v_j) within a soft primitive (-1)
   int NNZ = 0;
   std::vector<int> body_kind, dof_slot, dof_body;
   std::vector<double> My, bmass, bs1, bvol, bkappa;
@@ -341,6 +342,27 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
       H.rptr.push_back((int)H.rcol.size());
     }
     H.NNZ = (int)H.rcol.size();
+    // BSR block of each ordered vertex pair of a soft contact primitive (k_pairs_x's soft-neighbour
+    // records): triangles (0,1),(0,2),(1,0),(1,2),(2,0),(2,1); edges (0,1),(1,0)
+    auto blk = [&](int v, int u) {
+      if (v >= H.V || u >= H.V) return -1;
+      for (int q = H.rptr[v]; q < H.rptr[v + 1]; ++q)
+        if (H.rcol[q] == u) return q;
+      return -1;
+    };
+    H.tri_blk.assign((size_t)H.NT * 6, -1);
+    for (int t = 0; t < H.NT; ++t) {
+      const int* tv = &H.tris[3 * t];
+      int o = 0;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+          if (i != j) H.tri_blk[6 * (size_t)t + o++] = blk(tv[i], tv[j]);
+    }
+    H.edge_blk.assign((size_t)H.NE * 2, -1);
+    for (int e2 = 0; e2 < H.NE; ++e2) {
+      H.edge_blk[2 * (size_t)e2] = blk(H.edges[2 * e2], H.edges[2 * e2 + 1]);
+      H.edge_blk[2 * (size_t)e2 + 1] = blk(H.edges[2 * e2 + 1], H.edges[2 * e2]);
+    }
     std::vector<std::vector<int>> rb(H.NNZ);
     for (int t = 0; t < H.T; ++t)
       for (int a = 0; a < 4; ++a)
@@ -470,7 +492,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.tets = ti(H.tets); D.Dmi = td(H.Dmi); D.vol = td(H.vol); D.mu = td(H.mu); D.lam = td(H.lam); D.mass = td(H.mass);
   D.sedge = ti(H.sedge); D.vadj_ptr = ti(H.vadj_ptr); D.vadj = ti(H.vadj); D.vdiag_ptr = ti(H.vdiag_ptr);
   D.vdiag = ti(H.vdiag); D.eblk_ptr = ti(H.eblk_ptr); D.eblk = ti(H.eblk);
-  D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rupx = ti(H.rupx); D.eup = ti(H.eup); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
+  D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rupx = ti(H.rupx); D.eup = ti(H.eup); D.tri_blk = ti(H.tri_blk); D.edge_blk = ti(H.edge_blk); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
   D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My);
   D.bmass = td(H.bmass); D.bs1 = td(H.bs1); D.bvol = td(H.bvol); D.bkappa = td(H.bkappa);
   D.vert_body = ti(H.vert_body); D.vert_aff = ti(H.vert_aff); D.vert_xbar = td(H.vert_xbar);
@@ -610,7 +632,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, need, st);
 #define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
   UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
-  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(eup); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
+  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(eup); UP(tri_blk); UP(edge_blk); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
   UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(body_sv_ptr); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
   UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);

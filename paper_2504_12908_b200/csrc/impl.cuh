@@ -73,6 +73,8 @@ struct Dev {
   const int* eblk;        // entries 16*tet + 4*a + b (local a ↔ edge.i, b ↔ edge.j)
   const int* rptr;        // [V+1] row-ordered symmetric BSR
   const int* rcol;        // [NNZ] column (neighbour vertex)
+  const int* tri_blk;     // [NT][6] BSR index of (v_i, v_j) of a soft triangle, ordered pairs (0,1),(0,2),(1,0),(1,2),(2,0),(2,1)
+  const int* edge_blk;    // [NE][2] BSR index of (v0, v1), (v1, v0) of a soft edge
   const int* eup;         // [NEs] row-ordered index of each soft edge's upper block (i < j, row i)
   const int* rupx;        // [NNZ] 2·(soft edge id) + 1 if the block is the transpose of the edge's upper block
   const int* rblk_ptr;    // [NNZ+1]

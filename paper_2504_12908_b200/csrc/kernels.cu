@@ -1394,10 +1394,14 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
 #pragma unroll
           for (int b = 0; b < 3; ++b) rec[48 + 9 * nb + 3 * r + b] = res ? 0.0 : Hst(t, r, b);
         int jb = -1;
-        if (!res) {
-          const int v = cs, wv = csel(t);
-          for (int q = D.rptr[v]; q < D.rptr[v + 1]; ++q)
-            if (D.rcol[q] == wv) { jb = q; break; }
+        if (!res) {        // non-residual: all soft slots on one primitive → template block table
+          const int4 inf = reinterpret_cast<const int4*>(info)[k];
+          if (inf.x == 0) {
+            const int i = s - 1, j = t - 1;
+            jb = D.tri_blk[6 * (size_t)inf.w + 2 * i + (j < i ? j : j - 1)];
+          } else {
+            jb = D.edge_blk[2 * (size_t)(s < 2 ? inf.z : inf.w) + (s & 1)];
+          }
         }
         D.snb[((size_t)e * 4 * D.act_cap + j) * 2 + nb] = jb;
       }
