@@ -2219,7 +2219,7 @@ __host__ __device__ inline size_t pcg_r_bytes(const Dev& D, int threads) {
 // env-resident PCG: one CTA (512 threads) per env with the condensed soft matrix, diagonal and body
 // blocks, preconditioner and index arrays staged once into shared memory; only the (few) residual
 // pairs and the soft–body couplings are read from global memory per iteration
-__global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int force, int lpr) {
+__device__ __forceinline__ void pcg_r_body(const Dev& D, int env0, int force, int lpr) {
   const int e = env0 + blockIdx.x;
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
@@ -2260,6 +2260,12 @@ __global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r(Dev D, int env0, int
   __syncthreads();
   SmemMat R{lpr, U, Hd, Hb, Ps, Pb, couts, rptr, rcol, rupx, cptr, rcnt, cpp};
   pcg_body(D, e, 1, dsmem, red, &R, Ps, Pb);
+}
+// the env-resident PCG at two register budgets: ≤ 384 threads (C2: 168 registers per thread, no
+// spills) and ≤ 512 threads (128 registers)
+__global__ void __launch_bounds__(384, 1) k_pcg_r(Dev D, int env0, int force, int lpr) { pcg_r_body(D, env0, force, lpr); }
+__global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r512(Dev D, int env0, int force, int lpr) {
+  pcg_r_body(D, env0, force, lpr);
 }
 
 __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb,
@@ -3090,8 +3096,14 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   static const int resident = getenv("TAC_PCG_RESIDENT") ? atoi(getenv("TAC_PCG_RESIDENT")) : 1;   // 0: always stream
   if (resident && rb <= 227 * 1024) {
     static size_t rconf = 0;
-    if (rb > rconf) { cudaFuncSetAttribute(k_pcg_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb); rconf = rb; }
-    k_pcg_r<<<ne, thr, rb, s>>>(D, env0, force, lpr == 2 || lpr == 4 ? lpr : 1);
+    if (rb > rconf) {
+      cudaFuncSetAttribute(k_pcg_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
+      cudaFuncSetAttribute(k_pcg_r512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
+      rconf = rb;
+    }
+    static const int lb512 = getenv("TAC_PCG_R_LB512") ? atoi(getenv("TAC_PCG_R_LB512")) : 0;
+    if (thr <= 384 && !lb512) k_pcg_r<<<ne, thr, rb, s>>>(D, env0, force, lpr == 2 || lpr == 4 ? lpr : 1);
+    else k_pcg_r512<<<ne, thr, rb, s>>>(D, env0, force, lpr == 2 || lpr == 4 ? lpr : 1);
     return;
   }
   static const int sfused = getenv("TAC_PCG_STREAM_FUSED") ? atoi(getenv("TAC_PCG_STREAM_FUSED")) : 1;
