@@ -12,6 +12,9 @@ Workloads follow SURVEY.md §8(d) (the configs of BASELINE.json):
   C1c  soft cube resting on a static plate (statics variant)
   C2   peg insertion, dual low-res pads (8x6x3 lattice), 1024 envs
   C3   as C2 with high-res pads (19x16x5 lattice), 4096 envs
+  P1   single point-triangle pair: a tet's lowest vertex d̂/2 above a static box (barrier pins)
+  P2   single edge-edge pair: two tets' edges crossing at gap d̂/2 (perpendicular; P2m: nearly
+       parallel, inside the mollifier range) — also the soft–soft (matrix-free) contact case
 Per-env randomness uses numpy's Philox keyed by (250412908 + cfg index, global env id), so an
 env's inputs never depend on how envs are sharded across GPUs.
 
@@ -27,7 +30,7 @@ from typing import List, Optional
 import numpy as np
 
 DYNAMIC, KINEMATIC, STATIC = 0, 1, 2
-CFG_INDEX = {"C1": 1, "C1b": 11, "C1c": 12, "C2": 2, "C3": 3}
+CFG_INDEX = {"C1": 1, "C1b": 11, "C1c": 12, "C2": 2, "C3": 3, "P1": 21, "P2": 22, "P2m": 23}
 SEED_BASE = 250412908
 
 
@@ -305,7 +308,37 @@ def scene_C2(high_res=False):
                  n_steps=200)
 
 
+def scene_pair(name: str) -> Scene:
+    """Hand-placed single-pair scenes (geometry only; the expected values are derived by hand in
+    tests/test_oracle_pins.py).  dt = 0.01 s, no gravity, gap h = d̂/2 (d̂ = 1e-4 m).
+      P1: tet with vertices (0,0,0), (a,0,a), (−a/2, ±a√3/2, a), a = 2 mm (only the apex points down),
+          above the top face of a static 30×30×5 mm box (box pose from env_inputs: the apex sits over
+          box-frame point (7, 3) mm, away from the top face's diagonal) → one PT pair.
+      P2: tet A with its ridge edge (±a,0,0) on top, tet B with its valley edge at angle θ at z = h
+          on the bottom, a = b = 1 mm, θ = 90° → one EE pair (mollifier inactive).
+      P2m: as P2 with a = b = 10 mm and sin θ = 0.02 → one EE pair with c/ε× = 1000 sin²θ = 0.4."""
+    cfg = Config(dt=0.01)
+    h = 0.5 * cfg.dhat
+    tet = np.array([[0, 1, 2, 3]], np.int32)
+    if name == "P1":
+        a = 2 * MM
+        X = np.array([[0, 0, 0], [a, 0, a], [-a / 2, a * math.sqrt(3) / 2, a], [-a / 2, -a * math.sqrt(3) / 2, a]])
+        bV, bT = box_surface((30 * MM, 30 * MM, 5 * MM))
+        return Scene(name, [SoftPad(rest_pos=X, tets=tet)], [AffineBody(bV, bT, kind=STATIC)], np.zeros(3), cfg, n_steps=1)
+    if name in ("P2", "P2m"):
+        a = b = (1 * MM if name == "P2" else 10 * MM)
+        th = math.pi / 2 if name == "P2" else math.asin(0.02)
+        c, s = math.cos(th), math.sin(th)
+        XA = np.array([[-a, 0, 0], [a, 0, 0], [0, -a, -a], [0, a, -a]])
+        XB = np.array([[-b * c, -b * s, h], [b * c, b * s, h], [b * s, -b * c, h + b], [-b * s, b * c, h + b]])
+        return Scene(name, [SoftPad(rest_pos=XA, tets=tet), SoftPad(rest_pos=XB, tets=tet.copy())], [], np.zeros(3), cfg,
+                     n_steps=1)
+    raise ValueError(name)
+
+
 def make_scene(name: str) -> Scene:
+    if name in ("P1", "P2", "P2m"):
+        return scene_pair(name)
     if name in ("C1", "C1b", "C1c"):
         return scene_C1(name)
     if name == "C2":
@@ -412,7 +445,10 @@ def env_inputs(scene: Scene, env_ids, n_steps: Optional[int] = None) -> EnvInput
     n_steps = scene.n_steps if n_steps is None else n_steps
     ys, tks, xs = [], [], []
     for e in env_ids:
-        if scene.name.startswith("C1"):
+        if scene.name.startswith("P"):
+            y0 = np.stack([pose([-7 * MM, -3 * MM, -0.5 * scene.config.dhat - 2.5 * MM])]) if scene.affine else np.zeros((0, 12))
+            y0, tk = y0, np.zeros((n_steps, 0, 12))
+        elif scene.name.startswith("C1"):
             y0, tk = _c1_env(scene, int(e), n_steps)
         else:
             y0, tk = _c2_env(scene, int(e), n_steps)

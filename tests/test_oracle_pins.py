@@ -454,17 +454,46 @@ def _free_body_scene(gravity=(0, 0, -9.81)):
     return sc, M.prepare(sc)
 
 
-def test_free_fall_one_newton_step_exact():
+def test_free_fall_exact_at_scene_scale():
+    """Free affine body under gravity: the step's minimiser is t¹ = t⁰ + Δt v⁰ + Δt² g,
+    A¹ = A⁰ (a quadratic problem).  L_env is the cube's own scale (bounding-box diagonal), so the
+    R17c step cap (0.05·L_env) splits the ≈5 mm move into several capped Newton steps; the converged
+    position must still be the closed form."""
     sc, mod = _free_body_scene()
     y0 = np.array([[0.1, 0.2, 0.3, *S.rot_z(0.4).ravel()]])
     yd0 = np.array([[0.5, -0.2, 0.1, *np.zeros(9)]])
     st = SO.State(np.zeros((0, 3)), np.zeros((0, 3)), y0, yd0)
-    new, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=0.2)
+    L = M.env_scale(mod, st.x, st.y)
+    w = 0.01 * (math.cos(0.4) + math.sin(0.4))                       # 10 mm cube yawed 0.4 rad: bbox
+    assert L == pytest.approx(math.sqrt(2 * w * w + 0.01 ** 2), rel=1e-12)
+    new, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=L)
     dt = sc.config.dt
     expect = y0[0, :3] + dt * yd0[0, :3] + dt * dt * sc.gravity
-    assert stats.status == SO.ENV_OK and stats.newton_iters == 2    # one step + convergence check
-    assert np.allclose(new.y[0, :3], expect, rtol=0, atol=1e-15)
-    assert np.allclose(new.y[0, 3:], y0[0, 3:], atol=1e-15)
+    assert stats.status == SO.ENV_OK
+    assert np.allclose(new.y[0, :3], expect, rtol=0, atol=1e-14)
+    assert np.allclose(new.y[0, 3:], y0[0, 3:], atol=1e-14)
+
+
+def test_step_cap_limits_newton_step_length():
+    """Reading R17c: a Newton step longer than max_step_rel·L_env (embedded ∞-norm) is scaled to
+    exactly that length — the free-fall move (≈5 mm ≫ 0.05·17.3 mm) takes ⌈5 mm / 0.87 mm⌉ capped
+    steps, each of length 0.05·L_env, then one full step and the convergence check."""
+    sc, mod = _free_body_scene()
+    y0 = np.array([[0.1, 0.2, 0.3, *S.rot_z(0.4).ravel()]])
+    yd0 = np.array([[0.5, -0.2, 0.1, *np.zeros(9)]])
+    st = SO.State(np.zeros((0, 3)), np.zeros((0, 3)), y0, yd0)
+    L = M.env_scale(mod, st.x, st.y)
+    trace = []
+    new, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=L, trace=trace)
+    steps = [t for t in trace if "p_inf" in t]
+    cap = sc.config.max_step_rel * L
+    move = np.abs(sc.config.dt * yd0[0, :3] + sc.config.dt ** 2 * sc.gravity).max()   # translation only
+    n_cap = int(math.floor(move / cap))
+    assert len(steps) >= n_cap + 1
+    for t in steps[:n_cap]:
+        assert t["p_inf"] == pytest.approx(cap, rel=1e-12) and t["alpha"] == 1.0
+    assert steps[-1]["p_inf"] < cap
+    assert stats.newton_iters == len(steps) + 1
 
 
 def test_fixed_point_without_forces():
@@ -565,3 +594,127 @@ def test_candidates_equal_naive_loops(swept):
     got = C.candidate_pairs(mod, P, P1)
     assert len(got) > 0
     assert np.array_equal(got, _naive_candidates(mod, P, P1))
+
+
+# ------------------------------------------------------------------------------------ single pairs
+
+def _pair_state(name):
+    sc = S.make_scene(name)
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=1)
+    x, y = ei.x0[0], ei.y0[0]
+    ctx = En.make_context(mod, x, np.zeros_like(x), y, np.zeros_like(y), np.zeros((0, 12)), sc.config.dt)
+    return sc, mod, ctx, x, y
+
+
+def _area(P, tri):
+    i, j, k = tri
+    return 0.5 * np.linalg.norm(np.cross(P[j] - P[i], P[k] - P[i]))
+
+
+def _b_half():
+    """b(d̂/2) from the golden closed form: (d̂²/4) ln 2."""
+    g = GOLD["barrier"]
+    return g["b_at_half_over_dhat2"] * g["dhat"] ** 2
+
+
+def test_single_pt_pair_barrier_value():
+    """One point–triangle pair (scene P1: a tet apex d̂/2 above a static box face): the barrier term
+    equals Δt²·κ·A_k·b(d) with A_k = A_v(apex) = ⅓ of the rest areas of the apex's three incident
+    faces (reading R12, P:L106 Eq. fullspace_ipc weight A_k; S:L213 'a single pair gives κA_k b')."""
+    sc, mod, ctx, x, y = _pair_state("P1")
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    assert len(pairs) == 1 and pairs.kind[0] == 0 and pairs.a[0] == 0 and pairs.typ[0] == 0   # interior
+    X = sc.soft[0].rest_pos
+    A_v = (_area(X, (0, 1, 3)) + _area(X, (0, 1, 2)) + _area(X, (0, 2, 3))) / 3.0
+    cfg = sc.config
+    expect = cfg.dt ** 2 * cfg.kappa * A_v * _b_half()
+    assert En.energy_terms(mod, ctx, x, y, pairs)["barrier"] == pytest.approx(expect, rel=1e-12)
+
+
+def test_single_ee_pair_barrier_value():
+    """One edge–edge pair (scene P2: two edges crossing at right angles at gap d̂/2): barrier =
+    Δt²·κ·½(A_e(a)+A_e(b))·b(d), A_e = ⅓ of the two incident rest face areas; the mollifier is 1
+    (c = ‖e₁×e₂‖² = 1000·ε×) (reading R12, R7)."""
+    sc, mod, ctx, x, y = _pair_state("P2")
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    assert len(pairs) == 1 and pairs.kind[0] == 1
+    XA, XB = sc.soft[0].rest_pos, sc.soft[1].rest_pos
+    A_ea = (_area(XA, (0, 1, 2)) + _area(XA, (0, 1, 3))) / 3.0     # faces incident to the ridge edge (0,1)
+    A_eb = (_area(XB, (0, 1, 2)) + _area(XB, (0, 1, 3))) / 3.0     # faces incident to the valley edge (0,1)
+    assert A_ea == pytest.approx(2 * math.sqrt(2) / 3 * 1e-6, rel=1e-12)   # a = 1 mm: √2 a² per face
+    cfg = sc.config
+    expect = cfg.dt ** 2 * cfg.kappa * 0.5 * (A_ea + A_eb) * _b_half()
+    assert En.energy_terms(mod, ctx, x, y, pairs)["barrier"] == pytest.approx(expect, rel=1e-12)
+
+
+def test_single_ee_pair_mollifier_value():
+    """Nearly parallel edges (scene P2m, sin θ = 0.02, unstretched): c/ε× = ‖e₁×e₂‖² /
+    (1e-3‖ē₁‖²‖ē₂‖²) = 1000 sin²θ = 0.4, so m = (2 − 0.4)·0.4 = 0.64 multiplies the pair's barrier
+    (reading R7: ε× = 1e-3 of the rest squared lengths' product)."""
+    sc, mod, ctx, x, y = _pair_state("P2m")
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    assert len(pairs) == 1 and pairs.kind[0] == 1
+    assert math.sqrt(pairs.d2[0]) == pytest.approx(0.5 * sc.config.dhat, rel=1e-12)
+    XA, XB = sc.soft[0].rest_pos, sc.soft[1].rest_pos
+    A_ea = (_area(XA, (0, 1, 2)) + _area(XA, (0, 1, 3))) / 3.0
+    A_eb = (_area(XB, (0, 1, 2)) + _area(XB, (0, 1, 3))) / 3.0
+    ratio = 1000 * 0.02 ** 2
+    m = (2 - ratio) * ratio
+    cfg = sc.config
+    expect = cfg.dt ** 2 * cfg.kappa * 0.5 * (A_ea + A_eb) * m * _b_half()
+    assert En.energy_terms(mod, ctx, x, y, pairs)["barrier"] == pytest.approx(expect, rel=1e-10)
+
+
+# ------------------------------------------------------------------------------------ whole-step pins
+
+def test_statics_contact_force_equals_weight():
+    """Statics: a soft 8 mm cube (C1c, ρ = 1e3) dropped 50 µm onto a static plate
+    settles with an upward contact force equal to its weight ρ·(8 mm)³·g within 3%.  The contact
+    force is measured independently of the solver: −∂E_barrier/∂z of a rigid vertical translation of
+    all cube vertices (central differences of the barrier term), divided by Δt² (E carries Δt²·κ·Σ…)."""
+    sc = S.make_scene("C1c")
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=1)
+    st = SO.State(ei.x0[0].copy(), np.zeros_like(ei.x0[0]), ei.y0[0].copy(), np.zeros_like(ei.y0[0]))
+    L = M.env_scale(mod, st.x, st.y)
+    for _ in range(6):
+        st, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=L)
+        assert stats.status == SO.ENV_OK
+    ctx = En.make_context(mod, st.x, st.v, st.y, st.ydot, np.zeros((0, 12)), sc.config.dt)
+
+    def e_barrier(dz):
+        x = st.x.copy()
+        x[:, 2] += dz
+        return En.energy_terms(mod, ctx, x, st.y, C.active_pairs(mod, M.all_positions(mod, x, st.y)))["barrier"]
+
+    h = 1e-9
+    force_z = -(e_barrier(h) - e_barrier(-h)) / (2 * h) / sc.config.dt ** 2
+    weight = 1e3 * (8e-3) ** 3 * 9.81
+    assert abs(force_z / weight - 1.0) <= 0.03, force_z / weight
+
+
+def test_energy_monotone_within_step():
+    """Every accepted Newton iterate lowers E (Armijo, S:L391 'monotone energy within a step'), and
+    the next iteration starts from the accepted energy (same AL round: λ, ρ fixed)."""
+    sc = S.make_scene("C1")
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=3)
+    st = SO.State(ei.x0[0].copy(), np.zeros_like(ei.x0[0]), ei.y0[0].copy(), np.zeros_like(ei.y0[0]))
+    L = M.env_scale(mod, st.x, st.y)
+    n_checked = 0
+    for k in range(3):
+        trace = []
+        st, stats = SO.step(mod, st, ei.ykin[k, 0], L_env=L, trace=trace)
+        assert stats.status == SO.ENV_OK
+        prev = None
+        for t in trace:
+            if "al_round" in t:
+                prev = None
+                continue
+            assert t["E1"] <= t["E0"]
+            if prev is not None:
+                assert t["E0"] == pytest.approx(prev, rel=1e-12, abs=1e-18)
+            prev = t["E1"]
+            n_checked += 1
+    assert n_checked >= 3
