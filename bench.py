@@ -1,17 +1,26 @@
 #!/usr/bin/env python
 """bench.py — throughput of the batched IPC + ABD Newton step (Taccel, arXiv 2504.12908) on B200.
 
-A "step" is one backward-Euler time step of EVERY env of the workload (BASELINE.json configs[1],
-SURVEY §8(d) C2): peg insertion with dual low-res gel pads, 1024 envs per GPU, Δt = 0.02 s, the
-scripted 200-step episode from step 0.  The K timed steps run through tac_step_schedule with the
-device-resident target table of the scripted episode and the per-step gel readout (coated
-displacements, marker positions/flows of every env after every step) written to device buffers;
-envs advance through the schedule independently (no lockstep wait).  Envs are sharded across GPUs
-with no collective on the hot path (weak scaling: 1024 envs per GPU, global env ids seed the inputs).
+Metric (BASELINE.json): peg-insertion env-steps/s and ×real-time, dual sensors, at 1/2/4/8 B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl taccel|reference]
+A "step" is one backward-Euler time step of EVERY env of the workload, advanced in LOCKSTEP the way an
+RL loop drives the C ABI: per step tac_set_targets (from a device-resident target table of the scripted
+episode), tac_step (host-blocking; all envs finish the step) and tac_get_gel_deformation (coated-vertex
+displacements, marker positions and flows of every env, into device buffers).
 
-metric value = whole-job env-steps/s (all ranks) = N·E·K / max-over-ranks CUDA-event time.
+Workloads:
+  C3  (primary line; BASELINE configs[2], the 1/2/4/8-GPU axis): peg insertion with dual HIGH-res pads,
+      4096 envs in total, env-sharded over the N GPUs (strong scaling: rank r owns [⌊rE/N⌋, ⌊(r+1)E/N⌋)).
+  C2  (alongside; BASELINE configs[1]): dual low-res pads, 1024 envs per GPU (weak scaling).
+Both run the scripted 200-step episode; the timed steps are W..W+K-1 (closing phase, pads pressing
+the peg; contact-rich from step ~3).  Inputs are larger than L2 (per-step working set ≫ 126 MB).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl taccel|reference] [--config C3|C2]
+                  [--envs-total E | --envs-per-gpu E] [--no-alongside]
+
+With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL); the world size must equal --gpus.
+value = whole-job env-steps/s = Σ_ranks envs · K / (max over ranks of the CUDA-event time).
 """
 import argparse
 import json
@@ -35,21 +44,30 @@ WORKLOADS = {
     "C3": "C3: peg insertion, dual high-res sensors (2 pads x 19x16x5 lattice, 1520 nodes/5400 tets each), "
           "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s",
 }
-WORKLOAD = WORKLOADS["C2"]
+DEFAULTS = {  # config: (scaling, envs, default steps)
+    "C3": ("strong", 4096, 10),
+    "C2": ("weak", 1024, 20),
+}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="taccel", choices=["taccel", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--envs-per-gpu", type=int, default=1024)
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--envs-total", type=int, default=None, help="strong scaling: total envs split over the ranks")
+    ap.add_argument("--envs-per-gpu", type=int, default=None, help="weak scaling: envs per rank")
+    ap.add_argument("--no-alongside", action="store_true", help="skip the C2 line reported alongside C3")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-schedule", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phases", action="store_true", help="add the per-phase breakdown to the JSON line")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = DEFAULTS[a.config][2]
+    return a
 
 
 def load_peaks():
@@ -57,6 +75,18 @@ def load_peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return None
+
+
+def relaunch_distributed(a):
+    """--gpus N > 1 without a torchrun environment: run this script under torch.distributed.run."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -108,50 +138,138 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------------------------
-# CPU oracle baseline (the oracle as it stands, single thread, bounded sample)
+# CPU oracle baseline: the oracle as it stands (numpy/torch-autograd fp64, exact direct Newton
+# solve), one env per process, one thread per process, on every host core (bounded sample)
 # ----------------------------------------------------------------------------------------------
-def oracle_run(cfg_name, n_steps, warmup=0):
+def _oracle_job(args):
+    """One oracle process: env `env_id` of `cfg_name` from its initial state, `n_steps` full steps, or
+    (n_newton > 0) only the first n_newton Newton iterations of step 0 (the step is cut there).
+    Returns (seconds, env-steps done, Newton iterations done)."""
+    cfg_name, env_id, n_steps, n_newton = args
+    import dataclasses
     import torch
     torch.set_num_threads(1)
     from paper_2504_12908_b200 import scenes as S
     from oracle import mesh as M
     from oracle import solver as SO
     sc = S.make_scene(cfg_name)
+    if n_newton > 0:
+        sc.config = dataclasses.replace(sc.config, max_newton=n_newton)
     mod = M.prepare(sc)
-    ei = S.env_inputs(sc, [0], n_steps=warmup + n_steps)
+    ei = S.env_inputs(sc, [env_id], n_steps=max(n_steps, 1))
     st = SO.State(ei.x0[0].copy(), np.zeros_like(ei.x0[0]), ei.y0[0].copy(), np.zeros_like(ei.y0[0]))
     L = M.env_scale(mod, st.x, st.y)
-    for k in range(warmup):
-        st, _ = SO.step(mod, st, ei.ykin[k, 0], L_env=L)
     t0 = time.perf_counter()
-    for k in range(warmup, warmup + n_steps):
-        st, _ = SO.step(mod, st, ei.ykin[k, 0], L_env=L)
-    return time.perf_counter() - t0
+    done, newton = 0, 0
+    for k in range(max(n_steps, 1)):
+        yk = ei.ykin[k, 0] if ei.ykin.shape[2] else np.zeros((0, 12))
+        st, stats = SO.step(mod, st, yk, L_env=L)
+        newton += stats.newton_iters
+        done += 1
+    return time.perf_counter() - t0, done, newton
 
 
-def cpu_baseline(cfg_name, n_steps=2):
-    secs = oracle_run(cfg_name, n_steps)
-    return {"value": n_steps / secs, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
-            "sample": f"{cfg_name} env 0, steps 0-{n_steps - 1} (1 env), CPU oracle as it stands "
-                      f"(numpy/torch-autograd fp64, exact sparse direct Newton solve), 1 thread, {secs:.1f} s"}
+def oracle_pool(jobs):
+    """Run oracle jobs in one single-thread process each (spawned, all host cores); returns the
+    per-job results and the wall time."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(len(jobs)) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_job, jobs)
+        wall = time.perf_counter() - t0
+    return res, wall
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+ORACLE_SAMPLE = {  # cfg: (full steps per process, Newton iterations per process (0 = full steps))
+    "C2": (3, 0),
+    "C3": (1, 2),
+}
+
+
+def oracle_rate(cfg_name, cores, env0, newton_per_step):
+    """The bounded oracle sample of one bench "step": `cores` processes × ORACLE_SAMPLE[cfg].  C2: full
+    env-steps (env-steps/s = Σ steps / max process time).  C3: an oracle env-step takes minutes
+    (profiles/r2_oracle_newton_C3.json), so each process runs the first 2 Newton iterations of its env's
+    step and the rate is EXTRAPOLATED: env-steps/s = cores / (seconds per Newton iteration ×
+    Newton iterations per env-step)."""
+    n_steps, n_newton = ORACLE_SAMPLE[cfg_name]
+    res, wall = oracle_pool([(cfg_name, env0 + i, n_steps, n_newton) for i in range(cores)])
+    tmax = max(r[0] for r in res)
+    if n_newton == 0:
+        return sum(r[1] for r in res) / tmax, wall, tmax, None
+    s_per_it = statistics.mean(r[0] / max(r[2], 1) for r in res)
+    return cores / (s_per_it * newton_per_step), wall, tmax, s_per_it
+
+
+def oracle_newton_per_step(cfg_name):
+    """Oracle Newton iterations per env-step from the committed offline oracle run (env 0, first steps)."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", f"r2_oracle_newton_{cfg_name}.json")))
+        return statistics.mean(r["newton_iters"] for r in j["steps"]), "profiles/r2_oracle_newton_%s.json" % cfg_name
+    except Exception:
+        return 12.0, "oracle C3 env 0 step 0 (12 Newton iterations, measured offline)"
+
+
+def cpu_baseline(cfg_name, gpu_newton_mean):
+    """nproc single-thread oracle processes (one env each) on the host cores, plus the C1 run
+    (BASELINE configs[0]) in seconds on one core."""
+    cores = cpu_cores()
+    nps, src = (gpu_newton_mean, "the GPU run's mean Newton iterations per env-step over the same timed steps") \
+        if gpu_newton_mean else oracle_newton_per_step(cfg_name)
+    v, wall, tmax, s_it = oracle_rate(cfg_name, cores, 0, nps)
+    n_steps, n_newton = ORACLE_SAMPLE[cfg_name]
+    if n_newton:
+        sample = (f"{cfg_name}: {cores} processes x 1 thread, envs 0-{cores - 1}, the first {n_newton} Newton iterations of "
+                  f"episode step 0 each ({s_it:.2f} s per Newton iteration); EXTRAPOLATED to env-steps with "
+                  f"{nps:.2f} Newton iterations per env-step ({src}); max process time {tmax:.1f} s")
+    else:
+        sample = (f"{cfg_name}: {cores} processes x 1 thread, envs 0-{cores - 1}, episode steps 0-{n_steps - 1} each; "
+                  f"max process time {tmax:.1f} s")
+    c1_s = _oracle_job(("C1", 0, 10, 0))[0]
+    return {"value": v, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
+            "sample": sample + "; the CPU oracle as it stands (numpy/torch-autograd fp64, exact sparse direct Newton solve)",
+            "x_realtime": v * 0.02, "c1_oracle_seconds": c1_s,
+            "c1_note": "BASELINE configs[0]: C1 (1 env, 490-tet pad pressed 1 mm by a kinematic cube), all 10 steps "
+                       "at dt=0.01 on 1 core"}
 
 
 def run_reference(a):
+    """Reference arm of this tier = the CPU oracle as it stands, on the host cores (rank 0 only):
+    each timed step is one bounded oracle sample of the workload (oracle_rate)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    warm = a.warmup
-    secs = oracle_run(a.config, a.steps, warmup=warm)
-    v = a.steps / secs
-    dt = 0.02
-    line = {"metric": METRIC, "value": v, "unit": "env-steps/s", "impl": "reference", "n_gpus": a.gpus,
-            "steps": a.steps, "warmup": warm, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
+    cores = cpu_cores()
+    nps, src = oracle_newton_per_step(a.config)
+    W = min(a.warmup, 1)
+    for w in range(W):
+        oracle_rate(a.config, cores, 100000 + w * cores, nps)
+    secs = 0.0
+    n_equiv = 0.0
+    for k in range(a.steps):
+        v, wall, tmax, s_it = oracle_rate(a.config, cores, k * cores, nps)
+        secs += cores / v                      # seconds of this sample's env-step equivalents
+        n_equiv += cores
+    v = n_equiv / secs
+    n_steps, n_newton = ORACLE_SAMPLE[a.config]
+    sample = (f"{a.config}: per timed step {cores} processes x 1 thread, distinct env ids, " +
+              (f"the first {n_newton} Newton iterations of episode step 0 each, extrapolated with {nps:.2f} oracle Newton "
+               f"iterations per env-step ({src})" if n_newton else f"episode steps 0-{n_steps - 1} each"))
+    line = {"metric": METRIC, "value": v, "unit": "env-steps/s", "impl": "reference", "n_gpus": 0,
+            "steps": a.steps, "warmup": W, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS.get(a.config, a.config) + " — reference arm: the CPU oracle advancing env 0 (one env per step)",
-                       "envs_per_step": 1, "dt": dt},
-            "x_realtime": v * dt,
-            "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{a.config} env 0, steps {warm}-{warm + a.steps - 1}, 1 thread"},
+            "config": {"workload": WORKLOADS[a.config] + " — reference arm: the CPU oracle, one env per host core",
+                       "envs_per_step": cores, "dt": 0.02},
+            "x_realtime": v * 0.02,
+            "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -159,21 +277,204 @@ def run_reference(a):
 # ----------------------------------------------------------------------------------------------
 # the CUDA path
 # ----------------------------------------------------------------------------------------------
+def _pcts(v):
+    if not len(v):
+        return None
+    v = np.asarray(v, float)
+    return {"mean": float(v.mean()), "p50": float(np.percentile(v, 50)), "p99": float(np.percentile(v, 99)),
+            "max": float(v.max())}
+
+
+def run_config(cfg_name, a, rank, world, dev, envs_total=None, envs_per_gpu=None, steps=None, primary=True):
+    import torch
+    import torch.distributed as dist
+    from paper_2504_12908_b200 import scenes as S
+    from paper_2504_12908_b200 import taccel as T
+    from paper_2504_12908_b200.shard import env_range, reduce_run_stats, split_range
+
+    scaling = DEFAULTS[cfg_name][0]
+    if envs_per_gpu is not None:
+        scaling = "weak"
+    elif envs_total is not None:
+        scaling = "strong"
+    if scaling == "strong":
+        total = envs_total or DEFAULTS[cfg_name][1]
+        ids = np.asarray(list(split_range(rank, world, total)))
+    else:
+        per = envs_per_gpu or DEFAULTS[cfg_name][1]
+        ids = np.asarray(list(env_range(rank, world, per)))
+    E = len(ids)
+    W, K = a.warmup, (steps or a.steps)
+    sc = S.make_scene(cfg_name)
+    ei = S.env_inputs(sc, ids, n_steps=W + K)
+    stream = torch.cuda.current_stream(dev)
+    batch = T.Batch(sc, E, device=dev.index, stream=stream)
+    st = batch.set_state(ei.x0, ei.y0)
+    assert (st == 0).all(), f"bad initial states: {np.unique(st)}"
+    ykin_dev = torch.tensor(ei.ykin, device=dev)                     # (S, E, NK, 12) device-resident
+    NC, NM = batch.n_coated, batch.n_markers
+    out_dev = [(torch.empty((E, NC, 3), dtype=torch.float64, device=dev), torch.empty((E, NM, 3), dtype=torch.float64, device=dev),
+                torch.empty((E, NM, 3), dtype=torch.float64, device=dev)) for _ in range(K)]
+    fails = 0
+
+    def lockstep(k0, n, targets, outs, stats_out=None):
+        f = 0
+        for k in range(n):
+            batch.set_targets(targets[k0 + k])
+            f += int((batch.step(1) != 0).sum())
+            batch.get_gel_deformation(out=outs[k])
+            if stats_out is not None:
+                stats_out.append(batch.stats())
+        return f
+
+    # warm-up (untimed): W lockstep steps
+    fails += lockstep(0, W, ykin_dev, [out_dev[0]] * W)
+    saved = batch.get_state()
+    stats0 = batch.stats()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed: K lockstep steps, device-resident inputs/outputs ----
+    clocks = Clocks(dev.index)
+    clocks.start()
+    batch.profile(True)
+    batch.profile_read(reset=True)
+    per_step = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev0.record(stream)
+    fails += lockstep(W, K, ykin_dev, out_dev, per_step)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    prof = batch.profile_read(reset=True)
+    batch.profile(False)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    stats1 = batch.stats()
+    pcg_local = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
+    pcg_iters_local = sum(s1["pcg_iters_total"] - s0["pcg_iters_total"] for s0, s1 in zip(stats0, stats1))
+    newton = [s["newton_iters"] for ss in per_step for s in ss]
+    pcg_per_step = [s["pcg_iters"] for ss in per_step for s in ss]
+    n_active = [s["n_active"] for ss in per_step for s in ss]
+    n_res = [s["n_residual"] for ss in per_step for s in ss]
+    min_d = min((s["min_dist"] for ss in per_step for s in ss), default=float("inf"))
+
+    # ---- scheduled mode (context): the same K steps, envs advance independently ----
+    ms_sched = 0.0
+    if not a.no_schedule:
+        x, xd, y, yd = saved
+        batch.set_state(x, y, xd, yd)
+        outs = tuple(torch.empty((K, E) + t.shape[1:], dtype=torch.float64, device=dev) for t in out_dev[0])
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        batch.step_schedule(ykin_dev[W:W + K], out=outs)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_sched = e0.elapsed_time(e1)
+
+    # ---- e2e: the same K lockstep steps through the C ABI with pinned HOST buffers (targets in,
+    #      per-step gel readout out, both copied inside the timed region) ----
+    ms_e2e, h2d, d2h = 0.0, 0, 0
+    if not a.no_e2e:
+        x, xd, y, yd = saved
+        batch.set_state(x, y, xd, yd)
+        yk_host = torch.from_numpy(np.ascontiguousarray(ei.ykin[W:W + K])).pin_memory()
+        outs_h = [tuple(torch.empty(t.shape, dtype=torch.float64).pin_memory() for t in out_dev[0]) for _ in range(K)]
+        h2d = yk_host[0].numel() * 8
+        d2h = sum(t.numel() * 8 for t in outs_h[0])
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        lockstep(0, K, yk_host, outs_h)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        ms_e2e = max(e0.elapsed_time(e1), 1e3 * wall)
+
+    tot, cnt, mins = reduce_run_stats([ms, ms_e2e, ms_sched], [float(fails), float(pcg_iters_local), float(E)], world,
+                                      device=dev, mins=[min_d])
+    ms, ms_e2e, ms_sched = (float(v) for v in tot)
+    fails, pcg_iters_all, n_env_total = (float(v) for v in cnt)
+    n_env_total = int(n_env_total)
+    dt = sc.config.dt
+    value = n_env_total * K / (ms / 1e3)
+    res = {"cfg": cfg_name, "E_local": E, "n_env_total": n_env_total, "scaling": scaling, "K": K, "W": W, "ms": ms,
+           "value": value, "dt": dt, "clocks": clk, "fails": fails, "min_dist": float(mins[0]),
+           "workspace_gb": batch.workspace.numel() / 1e9, "pcg_kernel": batch.pcg_kernel, "prof": prof}
+    res["e2e"] = None if a.no_e2e else {"value": n_env_total * K / (ms_e2e / 1e3), "unit": "env-steps/s",
+                                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                                        "path": "tac_set_targets (pinned host) + tac_step + tac_get_gel_deformation (pinned host) per step"}
+    res["schedule"] = None if a.no_schedule else {"value": n_env_total * K / (ms_sched / 1e3), "ms_per_step": ms_sched / K,
+                                                  "mode": "tac_step_schedule: envs advance independently through the same K steps"}
+    res["solver"] = {"newton_iters_per_env_step": _pcts(newton), "pcg_iters_per_env_step": _pcts(pcg_per_step),
+                     "pcg_iters_per_newton_iter": pcg_iters_all / max(sum(newton) * world, 1) if newton else None,
+                     "active_pairs_per_env": _pcts(n_active), "residual_pairs_per_env": _pcts(n_res),
+                     "failed_env_steps": fails, "min_dist_m": float(mins[0]),
+                     "sample": "rank-0 per-env stats of every timed step" if world > 1 else "every env, every timed step"}
+    # roofline of the dominant kernel (PCG), from this rank's counters and CUDA events
+    phases = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1] > 0}
+    res["phases"] = phases
+    res["launches"] = int(sum(v["launches"] for v in phases.values()))
+    res["roofline"] = roofline(cfg_name, res["pcg_kernel"], phases, pcg_local, ms, K)
+    return res
+
+
+def roofline(cfg_name, kernel, phases, pcg_bytes, ms_step_total, K):
+    if "pcg" not in phases or phases["pcg"]["ms"] <= 0:
+        return None
+    peaks = load_peaks()
+    if peaks:
+        peak, src = peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (1 GiB copy, read+write bytes, burst)"
+    else:
+        peak, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    pcg_ms = phases["pcg"]["ms"]
+    launches = max(phases["pcg"]["launches"], 1)
+    ach = pcg_bytes / (pcg_ms / 1e3) / 1e9
+    traffic, tsrc = None, None
+    tfile = os.path.join(ROOT, "profiles", "r2_pcg_traffic.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile)).get(cfg_name)
+        if tj and tj.get("kernel") == kernel.split(" ")[0]:
+            traffic = tj["dram_bytes_per_launch"]
+            tsrc = (f"profiles/r2_pcg_traffic.json: ncu dram__bytes_read.sum+write.sum per {tj['kernel']} launch, "
+                    f"{tj['what']}")
+    resident = kernel.startswith("k_pcg_r")
+    return {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": traffic, "traffic_source": tsrc, "peak_source": src,
+            "share_of_step": pcg_ms / ms_step_total, "alg_bytes_per_launch": pcg_bytes / launches,
+            "alg_model": "per PCG iteration per env: 72(V+E_s)+4E_s+640*P_res+296*N_cpl+1248*ND+48V+96n "
+                         "(SURVEY sec 8(d) B_pcg on the condensed operator; DESIGN.md sec 5)",
+            "reading": ("effective algorithmic bandwidth: the operator is staged in shared memory once per launch "
+                        "and reused by every PCG iteration, so frac > 1 means on-chip reuse beats streaming it from HBM "
+                        "each iteration; measured DRAM traffic is the `traffic` field") if resident else
+                       ("streamed operator: achieved = algorithmic bytes / kernel time, an HBM-bandwidth fraction "
+                        "when the operator is re-read from L2/HBM every iteration")}
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
         return
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(a))
     import torch
     import torch.distributed as dist
-    from paper_2504_12908_b200 import scenes as S
-    from paper_2504_12908_b200 import taccel as T
     from paper_2504_12908_b200.build import build
-    from paper_2504_12908_b200.shard import env_range, reduce_run_stats
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == a.gpus, f"world size {world} != --gpus {a.gpus}"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -183,148 +484,58 @@ def main():
     if world > 1:
         dist.barrier()
 
-    sc = S.make_scene(a.config)
-    E = a.envs_per_gpu
-    W, K = a.warmup, a.steps
-    n_script = W + K
-    ids = np.asarray(list(env_range(rank, world, E)))
-    ei = S.env_inputs(sc, ids, n_steps=n_script)
-    stream = torch.cuda.current_stream(dev)
-    batch = T.Batch(sc, E, device=local, stream=stream)
-    st = batch.set_state(ei.x0, ei.y0)
-    assert (st == 0).all(), f"bad initial states: {np.unique(st)}"
-    ykin_dev = torch.tensor(ei.ykin, device=dev)                     # (S, E, NK, 12) device-resident
-    NC3, NM3 = batch.n_coated, batch.n_markers
-    out_dev = (torch.empty((K, E, NC3, 3), dtype=torch.float64, device=dev),
-               torch.empty((K, E, NM3, 3), dtype=torch.float64, device=dev),
-               torch.empty((K, E, NM3, 3), dtype=torch.float64, device=dev))
-
-    fails = 0
-    if W:
-        fails += int((batch.step_schedule(ykin_dev[:W]) != 0).sum())
-    saved = batch.get_state()                                          # for the e2e replay
-    stats0 = batch.stats()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    clocks = Clocks(local)
-    clocks.start()
-    batch.profile(True)
-    batch.profile_read(reset=True)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize(dev)
-    ev0.record(stream)
-    fails += int((batch.step_schedule(ykin_dev[W:W + K], out=out_dev) != 0).sum())
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    prof = batch.profile_read(reset=True)
-    batch.profile(False)
-    clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    stats1 = batch.stats()
-
-    # per-step solver statistics over the timed region
-    d_newton = sum(s["newton_iters"] for s in stats1)  # last step only
-    pcg_iters = sum(s1["pcg_iters_total"] - s0["pcg_iters_total"] for s0, s1 in zip(stats0, stats1))
-    pcg_bytes = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
-
-    # ---- e2e: replay the same K steps through the C ABI with pinned HOST buffers (targets in,
-    #      per-step gel readout out, both copied inside the timed region) ----
-    e2e = None
-    if not a.no_e2e:
-        x, xd, y, yd = saved
-        batch.set_state(x, y, xd, yd)
-        ykin_host = torch.from_numpy(np.ascontiguousarray(ei.ykin[W:W + K])).pin_memory()
-        outs = tuple(torch.empty(t.shape, dtype=torch.float64).pin_memory() for t in out_dev)
-        h2d = ykin_host.numel() * 8 // K
-        d2h = sum(t.numel() * 8 for t in outs) // K
-        # one untimed replay warms the stream-ordered staging pool, then the timed replay
-        batch.step_schedule(ykin_host, out=outs)
-        batch.set_state(x, y, xd, yd)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        e0.record(stream)
-        batch.step_schedule(ykin_host, out=outs)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        wall = time.perf_counter() - t0
-        ms_e2e = max(e0.elapsed_time(e1), 1e3 * wall)
-        e2e = {"value": None, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "_ms": ms_e2e}
-
-    # ---- max over ranks ----
-    tot, cnt = reduce_run_stats([ms, e2e["_ms"] if e2e else 0.0], [float(fails), float(pcg_iters), float(pcg_bytes)],
-                                world, device=dev)
-    ms, ms_e2e = float(tot[0]), float(tot[1])
-    fails, pcg_iters, pcg_bytes = (float(v) for v in cnt)
+    main_res = run_config(a.config, a, rank, world, dev, envs_total=a.envs_total, envs_per_gpu=a.envs_per_gpu)
+    side = None
+    if not a.no_alongside and a.config != "C2":
+        side = run_config("C2", a, rank, world, dev, steps=DEFAULTS["C2"][2], primary=False)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        nm = main_res["solver"]["newton_iters_per_env_step"]
+        cpu = cpu_baseline(a.config, nm["mean"] if nm else None)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-
-    n_env_total = E * world
-    value = n_env_total * K / (ms / 1e3)
-    dt = sc.config.dt
-    peaks = load_peaks()
-    hbm_peak, peak_src = (peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (copy, burst)") if peaks else (6650.0, "fallback 6.65 TB/s")
-    # dominant kernel (largest share of device time) and its roofline
-    phases = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1] > 0}
-    dom = max(phases, key=lambda k: phases[k]["ms"]) if phases else None
-    launches = int(sum(v["launches"] for v in phases.values()))
-    roof = None
-    if "pcg" in phases and phases["pcg"]["ms"] > 0:
-        # rank-0 PCG launches: algorithmic bytes / kernel time (local rank's own counters)
-        pcg_ms = phases["pcg"]["ms"]
-        local_bytes = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
-        ach = local_bytes / (pcg_ms / 1e3) / 1e9
-        traffic, tsrc = None, None
-        tfile = os.path.join(ROOT, "profiles", "r1s2_pcg_traffic.json")
-        if os.path.exists(tfile):
-            tj = json.load(open(tfile))
-            traffic = tj["dram_bytes_per_launch"]
-            tsrc = (f"{os.path.relpath(tfile, ROOT)}: ncu dram__bytes_read+write per {tj['kernel']} launch over one C2 "
-                    f"step; traffic/algorithmic = {tj['traffic_over_alg']:.3f} for that step (operator staged on chip "
-                    f"once per launch, reused by every PCG iteration)")
-        roof = {"kernel": "k_pcg_r (env-resident block-Jacobi PCG, one CTA per env)", "bound": "hbm", "achieved": ach,
-                "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic, "traffic_source": tsrc,
-                "peak_source": peak_src, "share_of_step": pcg_ms / ms,
-                "alg_bytes_per_launch": local_bytes / max(phases["pcg"]["launches"], 1),
-                "alg_model": "per PCG iteration per env: 72(V+E_s)+4E_s+640*P_res+296*N_cpl+1248*ND+48V+96n "
-                             "(condensed operator streamed once per iteration; DESIGN.md sec 5)",
-                "note": "frac > 1 would mean on-chip reuse beats streaming the operator from HBM every iteration",
-                "dominant_kernel": dom}
+    r = main_res
+    E_note = (f"{r['n_env_total']} envs in total split over {world} GPU(s)" if r["scaling"] == "strong"
+              else f"{r['E_local']} envs per GPU")
     line = {
-        "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": r["value"], "unit": "env-steps/s", "n_gpus": world, "steps": r["K"], "warmup": r["W"],
+        "ms_per_step": r["ms"] / r["K"], "higher_is_better": True, "scaling": r["scaling"], "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS.get(a.config, a.config), "envs_per_gpu": E, "envs_total": n_env_total, "dt": dt,
-                   "stepping": "tac_step_schedule: device-resident target table, per-step readout, envs advance independently",
-                   "timing_note": "per-kernel CUDA events are recorded inside the device-timed region (roofline, gpu_launches; "
-                                  "about 2% overhead); the e2e replay runs without them",
-                   "episode_steps_timed": f"{W}-{W + K - 1}", "parallelism": f"env-sharded x{world}",
-                   "l2": "inputs larger than L2: per-step working set ~%.1f GB/GPU > 126 MB L2" %
-                         (batch.workspace.numel() / 1e9)},
-        "x_realtime": value * dt,
-        "paper_context": "Taccel: 915 env-steps/s = 18.30x real-time, >4096 envs, 1x H100 FP64 (P:L230, Table 1) — context, not this workload",
-        "roofline": roof,
-        "gpu_launches": launches,
-        "solver": {"pcg_iters_per_step_per_env": pcg_iters / (K * n_env_total),
-                   "failed_env_steps": fails,
-                   "newton_iters_last_step_mean": d_newton / E},
-        "clocks": clk,
+        "config": {"workload": WORKLOADS[r["cfg"]], "envs_total": r["n_env_total"], "envs_per_gpu": r["E_local"],
+                   "envs": E_note, "dt": r["dt"],
+                   "stepping": "lockstep: per step tac_set_targets (device target table) + tac_step + tac_get_gel_deformation "
+                               "(device buffers) for every env",
+                   "episode_steps_timed": f"{r['W']}-{r['W'] + r['K'] - 1}", "parallelism": f"env-sharded x{world}",
+                   "l2": "inputs larger than L2: per-step working set ~%.1f GB/GPU > 126 MB L2" % r["workspace_gb"],
+                   "timing_note": "per-kernel CUDA events are recorded inside the device-timed region (roofline, "
+                                  "gpu_launches) and per-env stats are read after every timed step; the e2e replay runs "
+                                  "without events"},
+        "x_realtime": r["value"] * r["dt"],
+        "paper_context": "Taccel: 915 env-steps/s = 18.30x real-time (low-res peg, >4096 envs) and 64 envs at 0.25x "
+                         "(high-res peg), 1x H100 FP64 (P:L230, P:L49 Table 1) — context, not this workload",
+        "roofline": r["roofline"],
+        "gpu_launches": r["launches"],
+        "solver": r["solver"],
+        "schedule": r["schedule"],
+        "clocks": r["clocks"],
     }
-    if e2e:
-        e2e["value"] = n_env_total * K / (ms_e2e / 1e3)
-        e2e.pop("_ms")
-        line["e2e"] = e2e
+    if r["e2e"]:
+        line["e2e"] = r["e2e"]
+    if side:
+        line["alongside"] = {
+            "config": {"workload": WORKLOADS["C2"], "envs_per_gpu": side["E_local"], "envs_total": side["n_env_total"],
+                       "scaling": side["scaling"], "episode_steps_timed": f"{side['W']}-{side['W'] + side['K'] - 1}"},
+            "value": side["value"], "unit": "env-steps/s", "x_realtime": side["value"] * side["dt"],
+            "ms_per_step": side["ms"] / side["K"], "steps": side["K"], "e2e": side["e2e"], "schedule": side["schedule"],
+            "roofline": side["roofline"], "solver": side["solver"], "gpu_launches": side["launches"], "clocks": side["clocks"]}
+        if a.phases:
+            line["alongside"]["phases"] = side["phases"]
     if a.phases:
-        line["phases"] = phases
-    if world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(a.config)
+        line["phases"] = r["phases"]
+    if cpu:
+        line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -138,6 +138,12 @@ typedef struct {
   int64_t pcg_iters_total;       /* cumulative since tac_batch_create                         */
   double pcg_alg_bytes_total;    /* cumulative algorithmic PCG bytes (DESIGN.md §5 B_pcg model) */
   double diag[4];                /* last Newton iteration: ACCD bound, gᵀp, E(q), E at the last trial α */
+  double min_dist;               /* end of the last step: min primitive distance over the candidate pairs
+                                    closer than d̂ (+inf if none) — the intersection-free certificate d > 0 */
+  int32_t n_residual;            /* last Newton iteration: active pairs kept matrix-free in the SpMV (two
+                                    soft bodies or two DoF bodies in one pair) */
+  int32_t n_couplings;           /* last Newton iteration: condensed 3×12 soft–body coupling blocks */
+  double lm_mu;                  /* LM shift μ of the last solve (hessian_mode 2; 0 = pure Newton) */
 } tac_env_stats;
 
 struct tac_batch;
@@ -228,9 +234,22 @@ tac_status tac_debug_candidates(tac_batch* b, int32_t env, const double* x, cons
 /* α_max = K · min(1, min ACCD over the swept candidates along K·p), in units of p [n]. */
 tac_status tac_debug_accd(tac_batch* b, int32_t env, const double* x, const double* y, const double* p,
                           double* alpha, void* stream);
-/* Block-Jacobi PCG solve of H p = −g at (x, y) (AL as in tac_debug_eval): p [n], iterations. */
-tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, const double* y, double* p,
-                         int32_t* iters, void* stream);
+/* Block-Jacobi PCG solve at (x, y) (AL as in tac_debug_eval) with the kernel tac_step uses:
+ * exact_hessian = 0: H p = −g with the PSD-projected H (mu ignored);
+ * exact_hessian = 1: (H + μM) p = −g with the EXACT H and M the mass matrix (reading R14c), starting
+ * from μ = mu; if the solve meets negative curvature or gᵀp ≥ 0 the kernel raises μ ← max(μ₀, 10μ)
+ * and re-solves in the same launch, exactly as in tac_step.  Outputs: p [n], PCG iterations of all
+ * attempts, and the μ of the accepted solve (mu_used, may be NULL). */
+tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, const double* y, int32_t exact_hessian,
+                         double mu, double* p, int32_t* iters, double* mu_used, void* stream);
+/* Fault injection (test-only): env `env` fails with `status` (TAC_ENV_NEWTON_STALL..TAC_ENV_NONFINITE)
+ * at the end of the first Newton iteration of its next step — rolled back to the state at the start of
+ * that step and DISABLED, exactly like a detected failure; other envs are unaffected. */
+tac_status tac_debug_inject_fault(tac_batch* b, int32_t env, int32_t status, void* stream);
+
+/* Name of the PCG kernel tac_step launches for this batch (env-resident "k_pcg_r"/"k_pcg_r512" when the
+ * condensed operator fits one SM's shared memory, else the streamed-operator "k_pcg"). */
+const char* tac_pcg_kernel_name(const tac_batch* b);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,23 @@ static tac_status fail(tac_status s, const std::string& msg) { g_err = msg; retu
 
 extern "C" const char* tac_last_error(void) { return g_err.c_str(); }
 
+// every entry point runs on the batch's device and restores the caller's current device on return
+struct DevGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; cudaGetLastError(); }
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+#define ON_DEVICE(b)                                                                          \
+  DevGuard _dg((b)->device);                                                                  \
+  if (_dg.err != cudaSuccess) return fail(TAC_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_dg.err))
+
 // ---------------------------------------------------------------------------------------------
 // host template
 // ---------------------------------------------------------------------------------------------
@@ -602,7 +619,8 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (((uintptr_t)workspace) & 255) return fail(TAC_E_WORKSPACE, "workspace must be 256-byte aligned");
   tac_status s = check_cfg(cfg);
   if (s) return s;
-  CUDA_TRY(cudaSetDevice(device));
+  DevGuard _dg(device);
+  if (_dg.err != cudaSuccess) return fail(TAC_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_dg.err));
   tac_batch* b = new tac_batch();
   b->device = device;
   s = build_template(scene, cfg, b->H);
@@ -650,6 +668,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
 
 extern "C" tac_status tac_batch_destroy(tac_batch* b) {
   if (!b) return TAC_OK;
+  DevGuard _dg(b->device);
   if (b->h_flag) cudaFreeHost(b->h_flag);
   for (auto e : b->ev_pool) cudaEventDestroy(e);
   delete b;
@@ -689,6 +708,7 @@ extern "C" tac_status tac_set_state(tac_batch* b, int32_t env0, int32_t n, const
                                     const double* y, const double* ydot, uint8_t* env_status, void* stream) {
   tac_status s = check_range(b, env0, n);
   if (s) return s;
+  ON_DEVICE(b);
   if ((!x && b->D.V) || !y) return fail(TAC_E_INVALID, "x and y are required");
   cudaStream_t st = (cudaStream_t)stream;
   Dev& D = b->D;
@@ -719,6 +739,7 @@ extern "C" tac_status tac_set_state(tac_batch* b, int32_t env0, int32_t n, const
 extern "C" tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, const double* y_kin, void* stream) {
   tac_status s = check_range(b, env0, n);
   if (s) return s;
+  ON_DEVICE(b);
   if (b->D.NK == 0) return TAC_OK;
   if (!y_kin) return fail(TAC_E_INVALID, "y_kin is null");
   CUDA_TRY(cudaMemcpyAsync(b->D.ykin + (size_t)env0 * b->D.NK * 12, y_kin, (size_t)n * b->D.NK * 12 * sizeof(double),
@@ -773,6 +794,7 @@ static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st, c
 
 extern "C" tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_status, void* stream) {
   if (!b || n_steps < 0) return fail(TAC_E_INVALID, "bad arguments");
+  ON_DEVICE(b);
   cudaStream_t st = (cudaStream_t)stream;
   Dev& D = b->D;
   bool any_failed = false;
@@ -803,6 +825,7 @@ static bool is_device_ptr(const void* p) {
 extern "C" tac_status tac_step_schedule(tac_batch* b, int32_t n_steps, const double* y_kin_sched, double* coated_disp,
                                         double* marker_pos, double* marker_flow, uint8_t* env_status, void* stream) {
   if (!b || n_steps <= 0) return fail(TAC_E_INVALID, "bad arguments");
+  ON_DEVICE(b);
   if (b->D.NK > 0 && !y_kin_sched) return fail(TAC_E_INVALID, "y_kin_sched is required when the scene has kinematic bodies");
   cudaStream_t st = (cudaStream_t)stream;
   Dev& D = b->D;
@@ -860,6 +883,7 @@ extern "C" tac_status tac_get_state(tac_batch* b, int32_t env0, int32_t n, doubl
                                     double* ydot, void* stream) {
   tac_status s = check_range(b, env0, n);
   if (s) return s;
+  ON_DEVICE(b);
   cudaStream_t st = (cudaStream_t)stream;
   Dev& D = b->D;
   const size_t pitch = (size_t)D.n * sizeof(double), w = (size_t)3 * D.V * sizeof(double);
@@ -882,6 +906,7 @@ extern "C" tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_
                                               double* marker_pos, double* marker_flow, void* stream) {
   tac_status s = check_range(b, env0, n);
   if (s) return s;
+  ON_DEVICE(b);
   cudaStream_t st = (cudaStream_t)stream;
   Dev& D = b->D;
   { PROF(PH_READOUT); launch_readout(D, env0, n, st); }
@@ -898,6 +923,7 @@ extern "C" tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_
 
 extern "C" tac_status tac_get_stats(tac_batch* b, tac_env_stats* out, void* stream) {
   if (!b || !out) return fail(TAC_E_INVALID, "null argument");
+  ON_DEVICE(b);
   tac_status s = pull_ctl(b, (cudaStream_t)stream);
   if (s) return s;
   for (int e = 0; e < b->D.E; ++e) {
@@ -907,6 +933,9 @@ extern "C" tac_status tac_get_stats(tac_batch* b, tac_env_stats* out, void* stre
     out[e].alpha_min = c.alpha_min; out[e].energy = c.energy; out[e].constraint_residual = c.residual;
     out[e].pcg_iters_total = c.pcg_total; out[e].pcg_alg_bytes_total = c.pcg_bytes;
     out[e].diag[0] = c.alpha_ccd; out[e].diag[1] = c.gp; out[e].diag[2] = c.ls_E0; out[e].diag[3] = c.ls_E1;
+    out[e].min_dist = c.min_d2 < b->D.dhat * b->D.dhat ? std::sqrt(c.min_d2) : HUGE_VAL;
+    out[e].n_residual = c.n_res; out[e].n_couplings = c.n_cpl;
+    out[e].lm_mu = c.mu_used;
   }
   return TAC_OK;
 }
@@ -977,6 +1006,8 @@ static tac_status dbg_enter(DebugScope& S, const double* x, const double* y, con
   if (rho > 0) CUDA_TRY(cudaMemcpyAsync(&D.ctl[e].rho, &rho, sizeof(double), cudaMemcpyHostToDevice, S.st));
   static int flag[2] = {0, 1};
   CUDA_TRY(cudaMemcpyAsync(&D.ctl[e].exact, &flag[exact ? 1 : 0], sizeof(int), cudaMemcpyHostToDevice, S.st));
+  static const double zero = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&D.ctl[e].mu, &zero, sizeof(double), cudaMemcpyHostToDevice, S.st));
   CUDA_TRY(cudaStreamSynchronize(S.st));
   return TAC_OK;
 }
@@ -1009,7 +1040,8 @@ static tac_status dbg_assemble(tac_batch* b, int e, cudaStream_t st) {
 
 #define DBG_CHECK(b, env)                                                        \
   if (!(b) || (env) < 0 || (env) >= (b)->D.E) return fail(TAC_E_INVALID, "bad env"); \
-  if (!x || !y) return fail(TAC_E_INVALID, "x and y are required");
+  if (!x || !y) return fail(TAC_E_INVALID, "x and y are required");                   \
+  ON_DEVICE(b)
 
 extern "C" tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x, const double* y, const double* lam_att,
                                      const double* lam_kin, double rho, int32_t exact_hessian, const double* v_in,
@@ -1124,12 +1156,14 @@ extern "C" tac_status tac_debug_accd(tac_batch* b, int32_t env, const double* x,
   return s ? s : s2;
 }
 
-extern "C" tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, const double* y, double* p, int32_t* iters,
-                                    void* stream) {
+extern "C" tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, const double* y, int32_t exact_hessian,
+                                    double mu, double* p, int32_t* iters, double* mu_used, void* stream) {
   DBG_CHECK(b, env);
+  if (mu < 0) return fail(TAC_E_INVALID, "mu must be >= 0");
   DebugScope S{b, env, (cudaStream_t)stream};
-  tac_status s = dbg_enter(S, x, y, nullptr, nullptr, 0.0);
+  tac_status s = dbg_enter(S, x, y, nullptr, nullptr, 0.0, exact_hessian);
   Dev& D = b->D;
+  if (!s) CUDA_TRY(cudaMemcpyAsync(&D.ctl[env].mu, &mu, sizeof(double), cudaMemcpyHostToDevice, S.st));
   if (!s) s = dbg_assemble(b, env, S.st);
   if (!s) {
     launch_pcg(D, env, 1, 1, S.st);
@@ -1137,8 +1171,28 @@ extern "C" tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, 
     cudaMemcpyAsync(&c, D.ctl + env, sizeof(EnvCtl), cudaMemcpyDeviceToHost, S.st);
     if (p) cudaMemcpyAsync(p, D.p + (size_t)env * D.n, D.n * 8, cudaMemcpyDeviceToHost, S.st);
     if (cudaStreamSynchronize(S.st) != cudaSuccess) s = fail(TAC_E_CUDA, "debug pcg failed");
-    else if (iters) *iters = c.pcg;
+    else {
+      if (iters) *iters = c.pcg;
+      if (mu_used) *mu_used = c.mu_used;
+    }
   }
   tac_status s2 = dbg_leave(S);
   return s ? s : s2;
+}
+
+extern "C" tac_status tac_debug_inject_fault(tac_batch* b, int32_t env, int32_t status, void* stream) {
+  if (!b || env < 0 || env >= b->D.E) return fail(TAC_E_INVALID, "bad env");
+  if (status < TAC_ENV_NEWTON_STALL || status > TAC_ENV_NONFINITE) return fail(TAC_E_INVALID, "status must be 1..4");
+  ON_DEVICE(b);
+  cudaStream_t st = (cudaStream_t)stream;
+  int v = status;
+  CUDA_TRY(cudaMemcpyAsync(&b->D.ctl[env].fault, &v, sizeof(int), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TAC_OK;
+}
+
+extern "C" const char* tac_pcg_kernel_name(const tac_batch* b) {
+  if (!b) return "";
+  DevGuard _dg(b->device);
+  return pcg_path_name(pcg_path(b->D));
 }

@@ -41,6 +41,9 @@ struct EnvCtl {
   double mu;              // LM shift for the next solve (hessian_mode 2)
   double ls_E0, ls_E1;
   double alpha_ccd, alpha_min, rho, r_prev, L, energy, residual, gp, pnorm, alpha;
+  double min_d2;          // min squared primitive distance over the candidates classified by the last narrow phase
+  double mu_used;         // LM shift of the last solve (hessian_mode 2)
+  int fault, pad3_;       // test-only fault injection (tac_debug_inject_fault): env status forced at k_control
 };
 
 struct Dev {

@@ -538,6 +538,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
   const double dh2 = D.dhat * D.dhat;
   const int nc = C.ncand;
   int total = 0;
+  double mind2 = 1.0 / 0.0;
   for (int t0 = 0; t0 < nc; t0 += blockDim.x) {
     int k = t0 + threadIdx.x;
     int flag = 0, kind = 0, type = 0, a = 0, b = 0, vid[4];
@@ -550,6 +551,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
         double d2;
         type = classify(kind, X, &d2);
         flag = d2 < dh2;
+        mind2 = fmin(mind2, d2);
       }
     }
     int tot;
@@ -576,7 +578,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
     total += tot;
   }
   const int nact = min(total, D.act_cap);
-  if (threadIdx.x == 0) { C.n_act = nact; if (total > D.act_cap) C.overflow = 1; }
+  {
+    __shared__ double redm[32];
+    mind2 = block_min(mind2, redm);
+  }
+  if (threadIdx.x == 0) { C.n_act = nact; C.min_d2 = mind2; if (total > D.act_cap) C.overflow = 1; }
   __syncthreads();
   // residual pairs (kept matrix-free in the SpMV), ascending
   {
@@ -2261,7 +2267,7 @@ __device__ __forceinline__ void pcg_r_body(const Dev& D, int env0, int force, in
   SmemMat R{lpr, U, Hd, Hb, Ps, Pb, couts, rptr, rcol, rupx, cptr, rcnt, cpp};
   pcg_body(D, e, 1, dsmem, red, &R, Ps, Pb);
 }
-// the env-resident PCG at two register budgets: ≤ 384 threads (C2: 168 registers per thread, no
+// the env-resident PCG at two register budgets: ≤ 384 threads (C2: 168 registers per thread, 256 B of
 // spills) and ≤ 512 threads (128 registers)
 __global__ void __launch_bounds__(384, 1) k_pcg_r(Dev D, int env0, int force, int lpr) { pcg_r_body(D, env0, force, lpr); }
 __global__ void __launch_bounds__(PCG_R_THREADS, 1) k_pcg_r512(Dev D, int env0, int force, int lpr) {
@@ -2439,6 +2445,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     } else {
       C.newton += 1;
       const double mu_used = D.hmode == 2 ? mu : 0.0;
+      C.mu_used = mu_used;
       if (D.hmode == 2) C.mu = (mu * 0.1 >= D.lm_mu0) ? mu * 0.1 : 0.0;
       if (bad || !(pm == pm) || !(gp < 0.0 || zero_g)) { C.phase = PHASE_FAILED; C.status = ENV_NONFINITE; }
       else C.inner_conv = (pm <= D.tolN * C.L && mu_used == 0.0) ? 1 : 0;
@@ -2746,6 +2753,11 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
     if (threadIdx.x == 0) { C.phase = PHASE_FAILED; C.status = ENV_CAPACITY; }
     return;
   }
+  if (C.fault) {                                           // test-only fault injection (tac_debug_inject_fault)
+    __syncthreads();
+    if (threadIdx.x == 0) { C.phase = PHASE_FAILED; C.status = C.fault; C.fault = 0; }
+    return;
+  }
   double* q = D.q + (size_t)e * D.n;
   // exact-Hessian-first schedule (reading R14b): a failed exact attempt backs off 2, 4, .. 64
   // projected iterations; a successful one resets the back-off
@@ -2849,7 +2861,7 @@ __device__ void begin_env(const Dev& D, int e, const double* yk) {
 __global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
-  if (C.disabled) { if (threadIdx.x == 0) C.phase = PHASE_IDLE; return; }
+  if (C.disabled) { if (threadIdx.x == 0) { C.phase = PHASE_IDLE; C.status = ENV_DISABLED; } return; }
   begin_env(D, e, D.ykin + (size_t)e * D.NK * 12);
 }
 
@@ -2996,7 +3008,7 @@ __global__ void __launch_bounds__(NTHREADS) k_begin_sched(Dev D, int env0, const
   const int e = env0 + blockIdx.x;
   EnvCtl& C = D.ctl[e];
   if (threadIdx.x == 0) C.step = 0;
-  if (C.disabled) { if (threadIdx.x == 0) C.phase = PHASE_IDLE; return; }
+  if (C.disabled) { if (threadIdx.x == 0) { C.phase = PHASE_IDLE; C.status = ENV_DISABLED; } return; }
   begin_env(D, e, sched + (size_t)e * D.NK * 12);
 }
 
@@ -3025,9 +3037,18 @@ __global__ void __launch_bounds__(NTHREADS) k_advance(Dev D, int env0, const dou
 // ------------------------------------------------------------------------------------------
 // host launchers
 // ------------------------------------------------------------------------------------------
-static bool g_tables_ready = false;
+// per-device state: the __constant__ tables and the dynamic-shared-memory attributes exist once per
+// device (CUDA keeps module state per device), so both are tracked per device id
+constexpr int MAX_DEVICES = 64;
+static int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < MAX_DEVICES) ? d : 0;
+}
+static bool g_tables_ready[MAX_DEVICES] = {};
 cudaError_t init_tables() {
-  if (g_tables_ready) return cudaSuccess;
+  const int dev = cur_device();
+  if (g_tables_ready[dev]) return cudaSuccess;
   unsigned char r[PH], c[PH];
   for (int i = 0; i < 12; ++i)
     for (int j = i; j < 12; ++j) { int k = sym_idx(i, j, 12); r[k] = (unsigned char)i; c[k] = (unsigned char)j; }
@@ -3037,8 +3058,22 @@ cudaError_t init_tables() {
   cudaError_t err = cudaMemcpyToSymbol(c_unpack_r, r, PH);
   if (err == cudaSuccess) err = cudaMemcpyToSymbol(c_colpk, cp, PH);
   if (err == cudaSuccess) err = cudaMemcpyToSymbol(c_unpack_c, c, PH);
-  if (err == cudaSuccess) g_tables_ready = true;
+  if (err == cudaSuccess) g_tables_ready[dev] = true;
   return err;
+}
+
+// raise a kernel's dynamic shared-memory limit to `bytes` on the current device (cached per device
+// and kernel); false if the device cannot give that much
+template <class K>
+static bool ensure_smem(K kernel, size_t* cache /*[MAX_DEVICES]*/, size_t bytes) {
+  const int dev = cur_device();
+  if (bytes <= 48 * 1024 || bytes <= cache[dev]) return true;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cache[dev] = bytes;
+  return true;
 }
 
 void launch_positions(const Dev& D, int env0, int ne, int with_p, int force, cudaStream_t s) {
@@ -3072,43 +3107,72 @@ void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) 
   // threads: one per soft vertex in a single pass when V ≤ 320 (rounded to warps), else 256
   const int thr = D.V <= ASM_SOFT_MAX ? std::max(128, (D.V + 31) / 32 * 32) : NTHREADS;
   const int bytes = ((D.V + 3) / 2) * (int)sizeof(double) + (D.maxrl <= 32 ? (thr / 8) * D.maxrl * 9 * (int)sizeof(double) : 0);
-  static int attr = 0;
-  if (bytes > attr) { cudaFuncSetAttribute(k_assemble_soft, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); attr = bytes; }
+  static size_t attr[MAX_DEVICES] = {};
+  ensure_smem(k_assemble_soft, attr, bytes);
   k_assemble_soft<<<ne, thr, bytes, s>>>(D, env0, force);
   if (D.ND > 0) k_assemble_body<<<ne, NTHREADS, 0, s>>>(D, env0, force);
 }
 static size_t spmv_smem(const Dev& D) { return (size_t)(NTHREADS / 32) * D.ND * 12 * sizeof(double) + 8; }
-void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
-  const size_t with_vec = spmv_smem(D) + (size_t)5 * D.n * sizeof(double);
-  const int vsm = with_vec <= 200 * 1024 ? 1 : 0;
-  const size_t bytes = vsm ? with_vec : spmv_smem(D);
-  static size_t configured = 0;
-  if (bytes > 48 * 1024 && bytes > configured) {
-    cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    configured = bytes;
-  }
-  // env-resident PCG (one CTA per SM) when the condensed operator fits; lanes per soft row and the
-  // thread count can be overridden for experiments (TAC_PCG_LPR ∈ {1,2,4}, TAC_PCG_THREADS ≤ 512)
-  static const int lpr = getenv("TAC_PCG_LPR") ? atoi(getenv("TAC_PCG_LPR")) : 1;
+
+// which PCG kernel serves this batch: the env-resident k_pcg_r / k_pcg_r512 when the condensed operator,
+// the kernel's static shared memory and the vectors fit the device's opt-in shared memory per block,
+// else the streamed-operator k_pcg.  Env overrides for experiments: TAC_PCG_RESIDENT=0 (always stream),
+// TAC_PCG_R_LB512=1 (512-thread register budget), TAC_PCG_LPR ∈ {1,2,4}, TAC_PCG_THREADS ≤ 512.
+struct PcgPlan { int path; int threads; size_t bytes; int lpr; };
+static PcgPlan pcg_plan(const Dev& D) {
+  static const int lpr_env = getenv("TAC_PCG_LPR") ? atoi(getenv("TAC_PCG_LPR")) : 1;
   static const int thr_env = getenv("TAC_PCG_THREADS") ? atoi(getenv("TAC_PCG_THREADS")) : 0;
+  static const int resident = getenv("TAC_PCG_RESIDENT") ? atoi(getenv("TAC_PCG_RESIDENT")) : 1;
+  static const int lb512 = getenv("TAC_PCG_R_LB512") ? atoi(getenv("TAC_PCG_R_LB512")) : 0;
+  const int lpr = (lpr_env == 2 || lpr_env == 4) ? lpr_env : 1;
   const int thr = (thr_env >= 128 && thr_env <= PCG_R_THREADS && thr_env % 32 == 0) ? thr_env : pcg_r_threads(D.V);
   const size_t rb = pcg_r_bytes(D, thr);
-  static const int resident = getenv("TAC_PCG_RESIDENT") ? atoi(getenv("TAC_PCG_RESIDENT")) : 1;   // 0: always stream
-  if (resident && rb <= 227 * 1024) {
-    static size_t rconf = 0;
-    if (rb > rconf) {
-      cudaFuncSetAttribute(k_pcg_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
-      cudaFuncSetAttribute(k_pcg_r512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
-      rconf = rb;
-    }
-    static const int lb512 = getenv("TAC_PCG_R_LB512") ? atoi(getenv("TAC_PCG_R_LB512")) : 0;
-    if (thr <= 384 && !lb512) k_pcg_r<<<ne, thr, rb, s>>>(D, env0, force, lpr == 2 || lpr == 4 ? lpr : 1);
-    else k_pcg_r512<<<ne, thr, rb, s>>>(D, env0, force, lpr == 2 || lpr == 4 ? lpr : 1);
-    return;
+  if (resident) {
+    const bool use512 = thr > 384 || lb512;
+    cudaFuncAttributes fa;
+    int optin = 0;
+    const cudaError_t e1 = use512 ? cudaFuncGetAttributes(&fa, k_pcg_r512) : cudaFuncGetAttributes(&fa, k_pcg_r);
+    const cudaError_t e2 = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cur_device());
+    if (e1 == cudaSuccess && e2 == cudaSuccess && rb + fa.sharedSizeBytes <= (size_t)optin)
+      return PcgPlan{use512 ? PCG_RESIDENT512 : PCG_RESIDENT, thr, rb, lpr};
+    cudaGetLastError();
   }
+  const size_t with_vec = spmv_smem(D) + (size_t)5 * D.n * sizeof(double);
+  const int vsm = with_vec <= 200 * 1024 ? 1 : 0;
+  return PcgPlan{vsm ? PCG_STREAM_VSM : PCG_STREAM, NTHREADS, vsm ? with_vec : spmv_smem(D), lpr};
+}
+
+int pcg_path(const Dev& D) { return pcg_plan(D).path; }
+const char* pcg_path_name(int path) {
+  switch (path) {
+    case PCG_RESIDENT: return "k_pcg_r";
+    case PCG_RESIDENT512: return "k_pcg_r512";
+    case PCG_STREAM_VSM: return "k_pcg (streamed operator, vectors in shared memory)";
+    case PCG_STREAM: return "k_pcg (streamed operator)";
+    default: return "";
+  }
+}
+
+void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  PcgPlan pl = pcg_plan(D);
+  if (pl.path == PCG_RESIDENT || pl.path == PCG_RESIDENT512) {
+    static size_t c384[MAX_DEVICES] = {}, c512[MAX_DEVICES] = {};
+    const bool ok = pl.path == PCG_RESIDENT ? ensure_smem(k_pcg_r, c384, pl.bytes) : ensure_smem(k_pcg_r512, c512, pl.bytes);
+    if (ok) {
+      if (pl.path == PCG_RESIDENT) k_pcg_r<<<ne, pl.threads, pl.bytes, s>>>(D, env0, force, pl.lpr);
+      else k_pcg_r512<<<ne, pl.threads, pl.bytes, s>>>(D, env0, force, pl.lpr);
+      return;
+    }
+    const size_t with_vec = spmv_smem(D) + (size_t)5 * D.n * sizeof(double);   // attribute refused: stream
+    pl = PcgPlan{with_vec <= 200 * 1024 ? PCG_STREAM_VSM : PCG_STREAM, NTHREADS,
+                 with_vec <= 200 * 1024 ? with_vec : spmv_smem(D), pl.lpr};
+  }
+  static size_t cst[MAX_DEVICES] = {};
+  ensure_smem(k_pcg, cst, pl.bytes);
   static const int sfused = getenv("TAC_PCG_STREAM_FUSED") ? atoi(getenv("TAC_PCG_STREAM_FUSED")) : 1;
   static const int slpr = getenv("TAC_PCG_STREAM_LPR") ? atoi(getenv("TAC_PCG_STREAM_LPR")) : 1;
-  k_pcg<<<ne, NTHREADS, bytes, s>>>(D, env0, force, vsm, sfused, slpr == 2 || slpr == 4 ? slpr : 1);
+  k_pcg<<<ne, NTHREADS, pl.bytes, s>>>(D, env0, force, pl.path == PCG_STREAM_VSM ? 1 : 0, sfused,
+                                        slpr == 2 || slpr == 4 ? slpr : 1);
 }
 void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s) {
   k_spmv<<<1, NTHREADS, spmv_smem(D), s>>>(D, env0, x, y);

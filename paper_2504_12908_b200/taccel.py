@@ -65,7 +65,9 @@ class EnvStats(ctypes.Structure):
                 ("ls_backtracks", ctypes.c_int32), ("n_active", ctypes.c_int32), ("al_rounds", ctypes.c_int32),
                 ("n_candidates", ctypes.c_int32), ("alpha_min", ctypes.c_double), ("energy", ctypes.c_double),
                 ("constraint_residual", ctypes.c_double), ("pcg_iters_total", ctypes.c_int64),
-                ("pcg_alg_bytes_total", ctypes.c_double), ("diag", ctypes.c_double * 4)]
+                ("pcg_alg_bytes_total", ctypes.c_double), ("diag", ctypes.c_double * 4),
+                ("min_dist", ctypes.c_double), ("n_residual", ctypes.c_int32), ("n_couplings", ctypes.c_int32),
+                ("lm_mu", ctypes.c_double)]
 
 
 def header_symbols():
@@ -102,7 +104,8 @@ def load():
             "tac_debug_active_pairs": [vp, ctypes.c_int32, vp, vp, vp, ctypes.c_int32, c_int_p, vp],
             "tac_debug_candidates": [vp, ctypes.c_int32, vp, vp, vp, vp, ctypes.c_int32, c_int_p, vp],
             "tac_debug_accd": [vp, ctypes.c_int32, vp, vp, vp, c_double_p, vp],
-            "tac_debug_pcg": [vp, ctypes.c_int32, vp, vp, vp, c_int_p, vp],
+            "tac_debug_pcg": [vp, ctypes.c_int32, vp, vp, ctypes.c_int32, ctypes.c_double, vp, c_int_p, c_double_p, vp],
+            "tac_debug_inject_fault": [vp, ctypes.c_int32, ctypes.c_int32, vp],
             "tac_profile_enable": [vp, ctypes.c_int32],
             "tac_profile_read": [vp, c_double_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32],
             "tac_profile_iterations": [vp, c_int_p, c_double_p, ctypes.c_int32, c_int_p],
@@ -113,6 +116,8 @@ def load():
             f.restype = ctypes.c_int
         lib.tac_last_error.restype = ctypes.c_char_p
         lib.tac_profile_phase_name.restype = ctypes.c_char_p
+        lib.tac_pcg_kernel_name.restype = ctypes.c_char_p
+        lib.tac_pcg_kernel_name.argtypes = [vp]
         lib.tac_profile_phase_name.argtypes = [ctypes.c_int32]
         _lib = lib
     return _lib
@@ -356,8 +361,17 @@ class Batch:
         _check(self.lib.tac_debug_accd(self.handle, env, _ptr(_f64(x)), _ptr(_f64(y)), _ptr(_f64(p)), ctypes.byref(a), self._s()))
         return a.value
 
-    def debug_pcg(self, env, x, y):
+    def debug_pcg(self, env, x, y, exact=False, mu=0.0, with_mu=False):
         p = np.zeros(self.n_dof)
         it = ctypes.c_int32()
-        _check(self.lib.tac_debug_pcg(self.handle, env, _ptr(_f64(x)), _ptr(_f64(y)), _ptr(p), ctypes.byref(it), self._s()))
-        return p, it.value
+        mu_used = ctypes.c_double()
+        _check(self.lib.tac_debug_pcg(self.handle, env, _ptr(_f64(x)), _ptr(_f64(y)), 1 if exact else 0, float(mu), _ptr(p),
+                                      ctypes.byref(it), ctypes.byref(mu_used), self._s()))
+        return (p, it.value, mu_used.value) if with_mu else (p, it.value)
+
+    def debug_inject_fault(self, env, status):
+        _check(self.lib.tac_debug_inject_fault(self.handle, env, int(status), self._s()))
+
+    @property
+    def pcg_kernel(self) -> str:
+        return self.lib.tac_pcg_kernel_name(self.handle).decode()

@@ -18,8 +18,8 @@ def _worker(rank, world, port, out):
     sc = S.make_scene("C2")
     ids = list(env_range(rank, world, 3))
     ei = S.env_inputs(sc, ids, n_steps=2)
-    t, c = reduce_run_stats([10.0 * (rank + 1), 1.0], [rank + 1.0, 5.0], world)
-    out[rank] = (ids, ei.x0.copy(), ei.y0.copy(), ei.ykin.copy(), t.numpy().copy(), c.numpy().copy())
+    t, c, m = reduce_run_stats([10.0 * (rank + 1), 1.0], [rank + 1.0, 5.0], world, mins=[1e-5 * (2 - rank), float("inf")])
+    out[rank] = (ids, ei.x0.copy(), ei.y0.copy(), ei.ykin.copy(), t.numpy().copy(), c.numpy().copy(), m.numpy().copy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -32,13 +32,14 @@ def test_two_rank_sharding_and_reduction():
     sc = S.make_scene("C2")
     full = S.env_inputs(sc, range(6), n_steps=2)
     for r in range(world):
-        ids, x0, y0, yk, t, c = out[r]
+        ids, x0, y0, yk, t, c, m = out[r]
         assert ids == [3 * r, 3 * r + 1, 3 * r + 2]
         assert np.array_equal(x0, full.x0[3 * r:3 * r + 3])
         assert np.array_equal(y0, full.y0[3 * r:3 * r + 3])
         assert np.array_equal(yk, full.ykin[:, 3 * r:3 * r + 3])
         assert np.array_equal(t, [20.0, 1.0])            # MAX over ranks
         assert np.array_equal(c, [3.0, 10.0])            # SUM over ranks
+        assert np.array_equal(m, [1e-5, float("inf")])   # MIN over ranks (min contact distance)
 
 
 def test_split_ranges_cover_exactly():

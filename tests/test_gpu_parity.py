@@ -234,7 +234,7 @@ def test_bad_state_detected_and_isolated():
     assert st[0] == 0 and st[1] == 5
     b.set_targets(ei.ykin[0])
     st = b.step(1)
-    assert st[0] == 0 and st[1] == 5
+    assert st[0] == 0 and st[1] == 6                     # DISABLED until the next set_state
 
 
 def _free_body_scene(gravity):
