@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <numeric>
 #include <string>
@@ -73,7 +74,81 @@ struct HostT {
   std::vector<double> att_local;
   std::vector<int> coat_vert, coat_pad, mark_tri, mark_pad, pad_mount;
   std::vector<double> mark_bary, pad_T;
+  // cluster PCG plan (k_pcg_cl): soft rows split into cl_nc contiguous ranges of cl_rpr rows
+  int cl_nc = 0, cl_rpr = 0, cl_threads = 0, cl_nvt = 0, cl_nle_max = 0, cl_nlb_max = 0, cl_cplcap = 0;
+  size_t cl_smem_bytes = 0;
+  std::vector<int> cl_eptr, cl_edge, cl_bptr, cl_lrptr, cl_blk;   // cl_blk: 2 ints per block
 };
+
+// Cluster PCG plan for nc CTAs per env (pcg_cluster.cuh): rows [r·rpr, (r+1)·rpr) on rank r; each rank
+// stores the upper blocks of the soft edges touching its rows and, per row, (2·local edge + transposed,
+// rank << 16 | local row of the column vertex).  False if the rank does not fit one CTA.
+static bool plan_cluster(HostT& H, int nc, size_t budget) {
+  const int V = H.V, ND = H.ND;
+  if (V == 0) return false;
+  const int rpr = (V + nc - 1) / nc;
+  if (rpr > 65535) return false;
+  const int nvt = (rpr + 31) / 32 * 32;
+  const int threads = nvt + 32 * ((ND + 1) / 2);
+  if (threads > CL_MAX_THREADS) return false;
+  std::vector<int> eptr(1, 0), edge, bptr(1, 0), lrptr, blk;
+  int nle_max = 0, nlb_max = 0;
+  for (int r = 0; r < nc; ++r) {
+    const int v0 = r * rpr, v1 = std::min(V, v0 + rpr);
+    std::vector<int> es;
+    for (int v = v0; v < v1; ++v)
+      for (int j = H.rptr[v]; j < H.rptr[v + 1]; ++j) es.push_back(H.rupx[j] >> 1);
+    std::sort(es.begin(), es.end());
+    es.erase(std::unique(es.begin(), es.end()), es.end());
+    std::map<int, int> loc;
+    for (size_t i = 0; i < es.size(); ++i) loc[es[i]] = (int)i;
+    edge.insert(edge.end(), es.begin(), es.end());
+    eptr.push_back((int)edge.size());
+    int nb = 0;
+    for (int v = v0; v < v0 + rpr; ++v) {
+      lrptr.push_back(nb);
+      if (v >= v1) continue;
+      for (int j = H.rptr[v]; j < H.rptr[v + 1]; ++j) {
+        const int col = H.rcol[j];
+        blk.push_back(2 * loc[H.rupx[j] >> 1] + (H.rupx[j] & 1));
+        blk.push_back(((col / rpr) << 16) | (col % rpr));
+        ++nb;
+      }
+    }
+    lrptr.push_back(nb);
+    bptr.push_back(bptr.back() + nb);
+    nle_max = std::max(nle_max, (int)es.size());
+    nlb_max = std::max(nlb_max, nb);
+  }
+  const int nw = threads / 32;
+  const size_t base = cl_smem(rpr, nle_max, nlb_max, ND, nw, 0).end;
+  if (base > budget) return false;
+  const long want = (long)rpr * std::max(ND, 0);
+  const long fit = (long)((budget - base) / 320);
+  H.cl_cplcap = (int)std::max(0L, std::min(want, fit));
+  H.cl_nc = nc; H.cl_rpr = rpr; H.cl_threads = threads; H.cl_nvt = nvt; H.cl_nle_max = nle_max; H.cl_nlb_max = nlb_max;
+  H.cl_smem_bytes = cl_smem(rpr, nle_max, nlb_max, ND, nw, H.cl_cplcap).end;
+  H.cl_eptr = eptr; H.cl_edge = edge; H.cl_bptr = bptr; H.cl_lrptr = lrptr; H.cl_blk = blk;
+  return true;
+}
+
+// smallest cluster (1, 2, 4, 8, 16 CTAs per env) whose ranks fit the opt-in shared memory of sm_100
+// (227 KB per CTA, minus the kernel's static shared memory and a margin); TAC_PCG_CLUSTER=n forces n
+static void choose_cluster(HostT& H) {
+  const size_t budget = 227 * 1024 - 4 * 1024;
+  static const int force_nc = getenv("TAC_PCG_CLUSTER") ? atoi(getenv("TAC_PCG_CLUSTER")) : -1;
+  H.cl_nc = 0;
+  if (force_nc == 0) return;
+  for (int nc : {1, 2, 4, 8, 16}) {
+    if (force_nc > 0 && nc != force_nc) continue;
+    if (plan_cluster(H, nc, budget)) {
+      if (getenv("TAC_DEBUG_PLAN"))
+        fprintf(stderr, "cluster plan: nc=%d rpr=%d threads=%d nle_max=%d nlb_max=%d cplcap=%d smem=%zu\n", H.cl_nc, H.cl_rpr,
+                H.cl_threads, H.cl_nle_max, H.cl_nlb_max, H.cl_cplcap, H.cl_smem_bytes);
+      return;
+    }
+  }
+}
 
 static std::array<double, 3> sub3(const double* a, const double* b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
 static std::array<double, 3> cross3(std::array<double, 3> a, std::array<double, 3> b) {
@@ -428,6 +503,7 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
     if (H.kin_of_body[b] >= 0) H.kin_vlist.push_back(gv);
   }
   if (H.NT + H.NE >= (1 << 29)) return fail(TAC_E_CAPACITY, "too many primitives");
+  choose_cluster(H);
   return TAC_OK;
 }
 
@@ -522,6 +598,8 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.coat_vert = ti(H.coat_vert); D.coat_pad = ti(H.coat_pad); D.mark_tri = ti(H.mark_tri);
   D.mark_bary = td(H.mark_bary); D.mark_pad = ti(H.mark_pad); D.pad_mount = ti(H.pad_mount);
   D.pad_T = td(H.pad_T); D.Xrest = td(H.Xrest);
+  D.cl.eptr = ti(H.cl_eptr); D.cl.edge = ti(H.cl_edge); D.cl.bptr = ti(H.cl_bptr); D.cl.lrptr = ti(H.cl_lrptr);
+  D.cl.blk = reinterpret_cast<const int2*>(ti(H.cl_blk));
   const size_t e = (size_t)E, n = H.n;
   D.ctl = C.take<EnvCtl>(e);
   D.q = C.take<double>(e * n); D.qn = C.take<double>(e * n); D.vel = C.take<double>(e * n);
@@ -583,6 +661,8 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
   D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.bp_margin = cfg->bp_margin; D.K = (double)std::max(cfg->ls_expand, 1);
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
+  D.cl.nc = H.cl_nc; D.cl.rpr = H.cl_rpr; D.cl.threads = H.cl_threads; D.cl.nvt = H.cl_nvt;
+  D.cl.nle_max = H.cl_nle_max; D.cl.nlb_max = H.cl_nlb_max; D.cl.cplcap = H.cl_cplcap; D.cl.smem = H.cl_smem_bytes;
 }
 
 static tac_status check_cfg(const tac_config* c) {
@@ -656,6 +736,11 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
   UP(mark_bary); UP(mark_pad); UP(pad_mount); UP(pad_T); UP(Xrest);
 #undef UP
+  if (e == cudaSuccess) e = up(D.cl.eptr, H.cl_eptr, st);
+  if (e == cudaSuccess) e = up(D.cl.edge, H.cl_edge, st);
+  if (e == cudaSuccess) e = up(D.cl.bptr, H.cl_bptr, st);
+  if (e == cudaSuccess) e = up(D.cl.lrptr, H.cl_lrptr, st);
+  if (e == cudaSuccess) e = up(reinterpret_cast<const int*>(D.cl.blk), H.cl_blk, st);
   b->hctl.assign(n_envs, EnvCtl{});
   for (auto& c : b->hctl) { c.phase = PHASE_IDLE; c.disabled = 1; c.status = ENV_DISABLED; c.L = 1.0; c.rho = cfg->al_rho0; c.Keff = 1.0; }
   if (e == cudaSuccess) e = cudaMemcpyAsync(D.ctl, b->hctl.data(), sizeof(EnvCtl) * n_envs, cudaMemcpyHostToDevice, st);

@@ -46,6 +46,45 @@ struct EnvCtl {
   int fault, pad3_;       // test-only fault injection (tac_debug_inject_fault): env status forced at k_control
 };
 
+// ---- env-resident cluster PCG (pcg_cluster.cuh): plan built on the host from the soft BSR pattern ----
+constexpr int CL_MAX_THREADS = 384;
+constexpr int CL_MAX_NC = 16;
+struct ClSmem {            // carve of the dynamic shared memory (offsets in bytes, host and device agree)
+  size_t U, u, hd, ub, pbody, wpart, hb, blk, rptr, cpp, cpld, cval, red, end;
+};
+__host__ __device__ inline size_t cl_align(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ inline ClSmem cl_smem(int rpr, int nle, int nlb, int nd, int nw, int cplcap) {
+  ClSmem s;
+  size_t o = 0;
+  s.U = o; o = cl_align(o + 72 * (size_t)nle);
+  s.u = o; o = cl_align(o + 24 * (size_t)rpr);
+  s.hd = o; o = cl_align(o + 72 * (size_t)rpr);
+  s.ub = o; o = cl_align(o + 96 * (size_t)nd);
+  s.pbody = o; o = cl_align(o + 96 * (size_t)nd);
+  s.wpart = o; o = cl_align(o + 96 * (size_t)nd * nw);
+  s.hb = o; o = cl_align(o + 2 * 1152 * (size_t)nd);      // bodies: (H_b + μM^y) and its block-Jacobi inverse
+  s.blk = o; o = cl_align(o + 8 * (size_t)nlb);
+  s.rptr = o; o = cl_align(o + 4 * (size_t)(rpr + 1));
+  s.cpp = o; o = cl_align(o + 4 * (size_t)(rpr + 1));
+  s.cpld = o; o = cl_align(o + 4 * (size_t)cplcap);
+  s.cval = o; o = cl_align(o + 288 * (size_t)cplcap);
+  s.red = o; o = cl_align(o + 8 * (64 + 8));
+  s.end = o;
+  return s;
+}
+
+// host-built plan (template data, shared by all envs of the batch)
+struct ClPlan {
+  int nc, rpr, threads, nvt, nle_max, nlb_max, cplcap;
+  size_t smem;
+  const int* eptr;      // [nc+1] local-edge list offsets
+  const int* edge;      // local edges → global soft edge id
+  const int* bptr;      // [nc+1] local-block list offsets
+  const int* lrptr;     // [nc][rpr+1] block-row pointers relative to the rank's list
+  const int2* blk;      // {2·local edge + transposed, rank << 16 | local row of the column vertex}
+};
+
+
 struct Dev {
   // ---- dims ----
   int NNZ;                // off-diagonal soft blocks in row order (2·NEs)
@@ -178,6 +217,7 @@ struct Dev {
   double* out_mpos;       // [E][NMARK][3]
   double* out_mflow;      // [E][NMARK][3]
   int* any_active;        // [1]
+  ClPlan cl;              // cluster PCG plan (cl.nc = 0: not available for this template)
 };
 
 }  // namespace tac

@@ -2188,6 +2188,8 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z, const S
 // block-Jacobi PCG: H p = −g from p₀ = 0, stop at rᵀz ≤ η² r₀ᵀz₀ or max_pcg; then the
 // Newton convergence test ‖p‖_emb,∞ ≤ τ_N L_env and gᵀp.
 // ------------------------------------------------------------------------------------------
+__device__ void pcg_finish(const Dev& D, int e, double* p, double* red, double mu, bool bad, bool zero_g, int it_total,
+                           double gp);
 // vsm = 1: the five PCG vectors live in shared memory (n small enough), p is copied out at the end
 __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb,
                          int fused = 0, int stream_lpr = 4);
@@ -2419,6 +2421,15 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     __syncthreads();
     p = p_out;
   }
+  pcg_finish(D, e, p, red, mu, bad, zero_g, it_total, gp);
+}
+
+// end of a PCG launch (block-level, one CTA per env): embedded ∞-norm of the direction, step cap
+// (R17c), Newton convergence test (R14) and the per-env statistics
+__device__ void pcg_finish(const Dev& D, int e, double* p, double* red, double mu, bool bad, bool zero_g, int it_total,
+                           double gp) {
+  EnvCtl& C = D.ctl[e];
+  const int n = D.n;
   double pm = embedded_inf_norm(D, e, p, red);
   // step cap (reading R17c): scale p to max_step·L_env if longer (direction unchanged)
   const double cap = D.max_step * C.L;
@@ -2452,6 +2463,14 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     }
   }
 }
+
+__device__ __noinline__ void pcg_finish_noinline(const Dev& D, int e, double* p, double* red, double mu, bool bad, bool zero_g,
+                                                 int it_total, double gp) {
+  pcg_finish(D, e, p, red, mu, bad, zero_g, it_total, gp);
+}
+}  // namespace tac
+#include "pcg_cluster.cuh"
+namespace tac {
 
 __global__ void __launch_bounds__(NTHREADS) k_spmv(Dev D, int env0, const double* x, double* y) {
   const int e = env0 + blockIdx.x;
@@ -3119,14 +3138,73 @@ static size_t spmv_smem(const Dev& D) { return (size_t)(NTHREADS / 32) * D.ND * 
 // else the streamed-operator k_pcg.  Env overrides for experiments: TAC_PCG_RESIDENT=0 (always stream),
 // TAC_PCG_R_LB512=1 (512-thread register budget), TAC_PCG_LPR ∈ {1,2,4}, TAC_PCG_THREADS ≤ 512.
 struct PcgPlan { int path; int threads; size_t bytes; int lpr; };
+
+template <int NC>
+static cudaError_t cl_attr(size_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(k_pcg_cl<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && NC > 8) e = cudaFuncSetAttribute(k_pcg_cl<NC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
+template <int NC>
+static size_t cl_static_smem() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_pcg_cl<NC>) != cudaSuccess) { cudaGetLastError(); return (size_t)1 << 30; }
+  return fa.sharedSizeBytes;
+}
+// the cluster plan fits: static + dynamic shared memory within the opt-in limit, attributes accepted
+// and at least one cluster can be resident (cached per device)
+static bool cl_fits(const Dev& D) {
+  static int ok[MAX_DEVICES][5] = {};             // 0 unknown, 1 yes, 2 no (per device, per cluster size)
+  const int dev = cur_device();
+  const int k = D.cl.nc == 1 ? 0 : D.cl.nc == 2 ? 1 : D.cl.nc == 4 ? 2 : D.cl.nc == 8 ? 3 : 4;
+  static size_t sized[MAX_DEVICES][5] = {};
+  if (ok[dev][k] == 2 && sized[dev][k] >= D.cl.smem) return false;
+  if (ok[dev][k] == 1 && sized[dev][k] >= D.cl.smem) return true;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  size_t st = 0;
+  cudaError_t e = cudaSuccess;
+  switch (D.cl.nc) {
+    case 1: st = cl_static_smem<1>(); e = cl_attr<1>(D.cl.smem); break;
+    case 2: st = cl_static_smem<2>(); e = cl_attr<2>(D.cl.smem); break;
+    case 4: st = cl_static_smem<4>(); e = cl_attr<4>(D.cl.smem); break;
+    case 8: st = cl_static_smem<8>(); e = cl_attr<8>(D.cl.smem); break;
+    case 16: st = cl_static_smem<16>(); e = cl_attr<16>(D.cl.smem); break;
+    default: e = cudaErrorInvalidValue;
+  }
+  bool good = e == cudaSuccess && st + D.cl.smem <= (size_t)optin;
+  if (!good) cudaGetLastError();
+  ok[dev][k] = good ? 1 : 2;
+  sized[dev][k] = D.cl.smem;
+  return good;
+}
+
+template <int NC>
+static void launch_cl(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ne * NC);
+  cfg.blockDim = dim3(D.cl.threads);
+  cfg.dynamicSmemBytes = D.cl.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = NC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = NC > 1 ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_pcg_cl<NC>, D, D.cl, env0, force);
+}
 static PcgPlan pcg_plan(const Dev& D) {
   static const int lpr_env = getenv("TAC_PCG_LPR") ? atoi(getenv("TAC_PCG_LPR")) : 1;
   static const int thr_env = getenv("TAC_PCG_THREADS") ? atoi(getenv("TAC_PCG_THREADS")) : 0;
   static const int resident = getenv("TAC_PCG_RESIDENT") ? atoi(getenv("TAC_PCG_RESIDENT")) : 1;
   static const int lb512 = getenv("TAC_PCG_R_LB512") ? atoi(getenv("TAC_PCG_R_LB512")) : 0;
+  static const int cluster_env = getenv("TAC_PCG_CLUSTER") ? atoi(getenv("TAC_PCG_CLUSTER")) : -1;
   const int lpr = (lpr_env == 2 || lpr_env == 4) ? lpr_env : 1;
   const int thr = (thr_env >= 128 && thr_env <= PCG_R_THREADS && thr_env % 32 == 0) ? thr_env : pcg_r_threads(D.V);
   const size_t rb = pcg_r_bytes(D, thr);
+  if (resident && cluster_env != 0 && D.cl.nc > 0 && cl_fits(D)) return PcgPlan{PCG_CLUSTER, D.cl.threads, D.cl.smem, 1};
   if (resident) {
     const bool use512 = thr > 384 || lb512;
     cudaFuncAttributes fa;
@@ -3149,12 +3227,22 @@ const char* pcg_path_name(int path) {
     case PCG_RESIDENT512: return "k_pcg_r512";
     case PCG_STREAM_VSM: return "k_pcg (streamed operator, vectors in shared memory)";
     case PCG_STREAM: return "k_pcg (streamed operator)";
+    case PCG_CLUSTER: return "k_pcg_cl";
     default: return "";
   }
 }
 
 void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   PcgPlan pl = pcg_plan(D);
+  if (pl.path == PCG_CLUSTER) {
+    switch (D.cl.nc) {
+      case 1: launch_cl<1>(D, env0, ne, force, s); return;
+      case 2: launch_cl<2>(D, env0, ne, force, s); return;
+      case 4: launch_cl<4>(D, env0, ne, force, s); return;
+      case 8: launch_cl<8>(D, env0, ne, force, s); return;
+      case 16: launch_cl<16>(D, env0, ne, force, s); return;
+    }
+  }
   if (pl.path == PCG_RESIDENT || pl.path == PCG_RESIDENT512) {
     static size_t c384[MAX_DEVICES] = {}, c512[MAX_DEVICES] = {};
     const bool ok = pl.path == PCG_RESIDENT ? ensure_smem(k_pcg_r, c384, pl.bytes) : ensure_smem(k_pcg_r512, c512, pl.bytes);
