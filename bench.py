@@ -173,6 +173,8 @@ def oracle_pool(jobs):
     """Run oracle jobs in one single-thread process each (spawned, all host cores); returns the
     per-job results and the wall time."""
     import multiprocessing as mp
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "NUMEXPR_NUM_THREADS"):
+        os.environ[k] = "1"                           # one thread per oracle process (spawned children inherit)
     ctx = mp.get_context("spawn")
     with ctx.Pool(len(jobs)) as pool:
         t0 = time.perf_counter()

@@ -640,6 +640,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.out_coat = C.take<double>(e * H.NCOAT * 3 + 1); D.out_mpos = C.take<double>(e * H.NMARK * 3 + 1);
   D.out_mflow = C.take<double>(e * H.NMARK * 3 + 1);
   D.any_active = C.take<int>(1);
+  D.act_list = C.take<int>(2 * e);
   return C.off + 256;
 }
 
@@ -661,6 +662,7 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
   D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.bp_margin = cfg->bp_margin; D.K = (double)std::max(cfg->ls_expand, 1);
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
+  D.elist = nullptr; D.elist_out = nullptr;
   D.cl.nc = H.cl_nc; D.cl.rpr = H.cl_rpr; D.cl.threads = H.cl_threads; D.cl.nvt = H.cl_nvt;
   D.cl.nle_max = H.cl_nle_max; D.cl.nlb_max = H.cl_nlb_max; D.cl.cplcap = H.cl_cplcap; D.cl.smem = H.cl_smem_bytes;
 }
@@ -842,28 +844,36 @@ struct Sched {
   double *oc, *om, *of;
 };
 
+// Newton iterations until every env of [env0, env0+ne) converged or failed.  After the first
+// iteration the kernels run over the compacted list of envs k_control left active (grid = their
+// count, read back with the one 4-byte flag per iteration), so the tail of a lockstep step — a few
+// slow envs — does not pay for thousands of early-exiting CTAs per launch.  TAC_COMPACT=0 disables it.
 static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st, const Sched* sc = nullptr) {
   Dev& D = b->D;
+  static const int compact = getenv("TAC_COMPACT") ? atoi(getenv("TAC_COMPACT")) : 1;
   b->it_active.clear();
   b->it_ms.clear();
   double t0 = now_ms();
   { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 0, 0, st); }
   { PROF(PH_BROAD_STATIC); launch_broad(D, env0, ne, 0, 0, st); }
   const long max_it = (long)(D.max_newton + 2) * (sc ? sc->nsteps : 1);
+  Dev L = D;                              // per-iteration launch copy (active-env list)
+  int n_run = ne, e0 = env0;
   for (long it = 0; it < max_it; ++it) {
-    { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 0, 0, st); }
-    { PROF(PH_NARROW); launch_narrow(D, env0, ne, 0, st); }
-    { PROF(PH_TETS); launch_tets(D, env0, ne, 0, st); }
-    { PROF(PH_PAIRS); launch_pairs(D, env0, ne, 0, st); }
-    { PROF(PH_ASSEMBLE); launch_assemble(D, env0, ne, 0, st); }
-    { PROF(PH_PCG); launch_pcg(D, env0, ne, 0, st); }
-    { PROF(PH_POSITIONS); launch_positions(D, env0, ne, 1, 0, st); }
-    { PROF(PH_BROAD_SWEPT); launch_broad(D, env0, ne, 1, 0, st); }
-    { PROF(PH_CCD); launch_ccd(D, env0, ne, 0, st); }
-    { PROF(PH_LINESEARCH); launch_linesearch(D, env0, ne, st); }
+    L.elist_out = compact ? D.act_list + (size_t)((it + 1) & 1) * D.E : nullptr;
+    { PROF(PH_POSITIONS); launch_positions(L, e0, n_run, 0, 0, st); }
+    { PROF(PH_NARROW); launch_narrow(L, e0, n_run, 0, st); }
+    { PROF(PH_TETS); launch_tets(L, e0, n_run, 0, st); }
+    { PROF(PH_PAIRS); launch_pairs(L, e0, n_run, 0, st); }
+    { PROF(PH_ASSEMBLE); launch_assemble(L, e0, n_run, 0, st); }
+    { PROF(PH_PCG); launch_pcg(L, e0, n_run, 0, st); }
+    { PROF(PH_POSITIONS); launch_positions(L, e0, n_run, 1, 0, st); }
+    { PROF(PH_BROAD_SWEPT); launch_broad(L, e0, n_run, 1, 0, st); }
+    { PROF(PH_CCD); launch_ccd(L, e0, n_run, 0, st); }
+    { PROF(PH_LINESEARCH); launch_linesearch(L, e0, n_run, st); }
     CUDA_TRY(cudaMemsetAsync(D.any_active, 0, sizeof(int), st));
-    { PROF(PH_CONTROL); launch_control(D, env0, ne, st); }
-    if (sc) { PROF(PH_END); launch_advance(D, env0, ne, sc->sched, sc->nsteps, sc->oc, sc->om, sc->of, st); }
+    { PROF(PH_CONTROL); launch_control(L, e0, n_run, st); }
+    if (sc) { PROF(PH_END); launch_advance(L, e0, n_run, sc->sched, sc->nsteps, sc->oc, sc->om, sc->of, st); }
     CUDA_TRY(cudaMemcpyAsync(b->h_flag, D.any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
@@ -873,6 +883,11 @@ static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st, c
     b->it_ms.push_back(t1 - t0);
     t0 = t1;
     if (!*b->h_flag) break;
+    if (compact) {
+      L.elist = D.act_list + (size_t)((it + 1) & 1) * D.E;
+      n_run = *b->h_flag;
+      e0 = 0;
+    }
   }
   return TAC_OK;
 }

@@ -216,7 +216,10 @@ struct Dev {
   double* out_coat;       // [E][NCOAT][3]
   double* out_mpos;       // [E][NMARK][3]
   double* out_mflow;      // [E][NMARK][3]
-  int* any_active;        // [1]
+  int* any_active;        // [1] envs still active after k_control (count)
+  int* act_list;          // [2][E] compacted active-env lists (double-buffered by Newton iteration parity)
+  const int* elist;       // per launch: env list of this launch (nullptr = env0 + blockIdx)
+  int* elist_out;         // per launch: list k_control / k_advance append the next iteration's active envs to
   ClPlan cl;              // cluster PCG plan (cl.nc = 0: not available for this template)
 };
 

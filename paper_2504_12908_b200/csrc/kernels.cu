@@ -22,6 +22,14 @@ __device__ __forceinline__ const double* body_y(const Dev& D, int e, int b) {
   return s >= 0 ? D.q + (size_t)e * D.n + 3 * D.V + 12 * s : D.ystat + ((size_t)e * D.NA + b) * 12;
 }
 __device__ __forceinline__ double* envp(double* base, int e, size_t per) { return base + (size_t)e * per; }
+// env of a CTA: env0 + b, or the b-th entry of the compacted active-env list of this Newton iteration
+__device__ __forceinline__ int env_at(const Dev& D, int env0, int b) { return D.elist ? D.elist[b] : env0 + b; }
+// append env e to the active-env list of the next Newton iteration (order is irrelevant: every per-env
+// result depends only on the env) and count it
+__device__ __forceinline__ void mark_active(const Dev& D, int e) {
+  const int slot = atomicAdd(D.any_active, 1);
+  if (D.elist_out) D.elist_out[slot] = e;
+}
 
 // f-factor of the affine Jacobian: column α of J_v is e_{i(α)} scaled by f(α) (1 for t, x̄_j for A_ij)
 __device__ __forceinline__ int jrow(int alpha) { return alpha < 3 ? alpha : (alpha - 3) / 3; }
@@ -85,7 +93,7 @@ __device__ __forceinline__ double sweep_factor(const Dev& D, double pinf) {
 }
 
 __global__ void __launch_bounds__(NTHREADS) k_positions(Dev D, int env0, int with_p, int force) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
   const double* q = D.q + (size_t)e * D.n;
@@ -304,7 +312,7 @@ __device__ int bp_query(const Dev& D, const BoxCtx& B, const Grid& G, const int*
 
 constexpr int BROAD_THREADS = 512;
 __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int swept, int force) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (!force && (C.phase != PHASE_ACTIVE || (swept && (C.inner_conv || C.xfail)))) return;
   // reading R11b: reuse the candidate list while every surface vertex stays within δ of the
@@ -523,7 +531,7 @@ __device__ bool pair_is_residual(const Dev& D, const int* vid) {
 }
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (env_skip(D, e, force)) return;
   extern __shared__ int dsm[];
@@ -678,7 +686,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
 // Neo-Hookean tets: gradient + F-space-projected 12×12 (SoA [90][T] per env)
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.y;
+  const int e = env_at(D, env0, blockIdx.y);
   if (env_skip(D, e, force)) return;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= D.T) return;
@@ -747,7 +755,7 @@ __device__ __forceinline__ double tri_u2_fast(const double* w, const double* e1,
 // grid (ceil(act_cap / PAIRS_PER_CTA), envs): many CTAs per env so a single contact-heavy env is
 // spread over the whole GPU; CTAs past the env's active count exit at once.
 __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.y;
+  const int e = env_at(D, env0, blockIdx.y);
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
   if (C.exact) return;                                    // exact Hessians: k_pairs_x (thread per pair)
@@ -992,7 +1000,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
 // chunk partials of the body records for projected envs (k_pairs writes per-pair records brec):
 // partial[chunk][d] = Σ over the chunk's 32 pairs in pair order (same layout as k_pairs_x)
 __global__ void k_bpart_proj(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.y;
+  const int e = env_at(D, env0, blockIdx.y);
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
   if (C.exact) return;
@@ -1150,7 +1158,7 @@ __device__ __forceinline__ void warp_reduce_scatter32(double* v, int lane) {
 __constant__ unsigned char c_colpk[PH];    // column-order position be(be+1)/2+al → packed sym_idx(al, be)
 
 __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.y;
+  const int e = env_at(D, env0, blockIdx.y);
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
   if (!C.exact) return;                                   // projected Hessians: k_pairs (warp Jacobi)
@@ -1596,7 +1604,7 @@ __device__ void chol_inverse12_warp(const double* A, double* Ainv, double* L /*1
 // 3×3 block-Jacobi inverses); register-light, so it runs at higher occupancy than the body part
 constexpr int ASM_SOFT_MAX = 320;
 __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   if (env_skip(D, e, force)) return;
   __shared__ int shs[33];
   __shared__ int next_cv;
@@ -1804,7 +1812,7 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
 // body part of the assembly: inertia, orthogonality, gravity and AL terms of the DoF bodies, the
 // pairs' body blocks (k_pairs_x partials) and the 12×12 block-Jacobi inverses
 __global__ void __launch_bounds__(NTHREADS, 2) k_assemble_body(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   if (env_skip(D, e, force)) return;
   __shared__ JacobiScratch JS[NTHREADS / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -2195,7 +2203,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
                          int fused = 0, int stream_lpr = 4);
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force, int vsm, int fused, int lpr) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
   extern __shared__ double dsmem[];     // [nw][ND][12] body partials, then (vsm) p, r, z, d, Ad
@@ -2228,7 +2236,7 @@ __host__ __device__ inline size_t pcg_r_bytes(const Dev& D, int threads) {
 // blocks, preconditioner and index arrays staged once into shared memory; only the (few) residual
 // pairs and the soft–body couplings are read from global memory per iteration
 __device__ __forceinline__ void pcg_r_body(const Dev& D, int env0, int force, int lpr) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
   extern __shared__ double dsmem[];
@@ -2473,7 +2481,7 @@ __device__ __noinline__ void pcg_finish_noinline(const Dev& D, int e, double* p,
 namespace tac {
 
 __global__ void __launch_bounds__(NTHREADS) k_spmv(Dev D, int env0, const double* x, double* y) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   extern __shared__ double part[];
   spmv(D, e, x, y, part);
 }
@@ -2508,7 +2516,7 @@ __device__ double accd_pair(int kind, v3* X, v3* Pd, double s, double tc, int ma
 }
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_ccd(Dev D, int env0, int force) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (!force && (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail)) return;
   __shared__ double red[32];
@@ -2693,7 +2701,7 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
 }
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_energy(Dev D, int env0, double alpha) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   __shared__ double red[6 * 32];
   double t[6];
   int inv;
@@ -2708,7 +2716,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_energy(Dev D, int env0, double 
 
 // backtracking line search from α = min(1, α_ccd); Armijo c
 __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail) return;
   __shared__ double red[6 * 32];
@@ -2764,7 +2772,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
 // Newton / AL control (readings R13-R14): AL update when the inner solve has converged
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (C.phase != PHASE_ACTIVE) return;
   __shared__ double red[32];
@@ -2841,7 +2849,7 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
   }
   if (threadIdx.x == 0) {
     if (C.phase == PHASE_ACTIVE && C.newton >= D.max_newton) { C.phase = PHASE_FAILED; C.status = ENV_NEWTON_STALL; }
-    if (C.phase == PHASE_ACTIVE) atomicAdd(D.any_active, 1);
+    if (C.phase == PHASE_ACTIVE) mark_active(D, e);
   }
 }
 
@@ -2878,7 +2886,7 @@ __device__ void begin_env(const Dev& D, int e, const double* yk) {
 }
 
 __global__ void __launch_bounds__(NTHREADS) k_begin(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (C.disabled) { if (threadIdx.x == 0) { C.phase = PHASE_IDLE; C.status = ENV_DISABLED; } return; }
   begin_env(D, e, D.ykin + (size_t)e * D.NK * 12);
@@ -2908,7 +2916,7 @@ __device__ void end_env(const Dev& D, int e) {
 }
 
 __global__ void __launch_bounds__(NTHREADS) k_end(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   if (D.ctl[e].phase == PHASE_IDLE) return;
   end_env(D, e);
 }
@@ -2917,7 +2925,7 @@ __global__ void __launch_bounds__(NTHREADS) k_end(Dev D, int env0) {
 // state I/O helpers, validation, readout
 // ------------------------------------------------------------------------------------------
 __global__ void k_scatter_y(Dev D, int env0, int which /*0: y→ystat+q, 1: ydot→vel, 2: zero vel bodies*/) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   const double* st = D.ystage + (size_t)e * D.NA * 12;
   for (int i = threadIdx.x; i < D.NA * 12; i += blockDim.x) {
     int b = i / 12, j = i % 12, s = D.dof_slot[b];
@@ -2930,7 +2938,7 @@ __global__ void k_scatter_y(Dev D, int env0, int which /*0: y→ystat+q, 1: ydot
   }
 }
 __global__ void k_gather_y(Dev D, int env0, int which /*0: y, 1: ydot*/) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   double* st = D.ystage + (size_t)e * D.NA * 12;
   for (int i = threadIdx.x; i < D.NA * 12; i += blockDim.x) {
     int b = i / 12, j = i % 12, s = D.dof_slot[b];
@@ -2941,7 +2949,7 @@ __global__ void k_gather_y(Dev D, int env0, int which /*0: y, 1: ydot*/) {
 
 // after set_state: L_env (bbox diagonal of all vertices), inversion and contact-distance checks
 __global__ void __launch_bounds__(NTHREADS) k_validate(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   __shared__ double red[32];
   const double* P = D.P + (size_t)e * D.NVall * 3;
@@ -3013,7 +3021,7 @@ __device__ void readout_env(const Dev& D, int e, double* oc, double* om, double*
 }
 
 __global__ void k_readout(Dev D, int env0) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   readout_env(D, e, D.out_coat + (size_t)e * D.NCOAT * 3, D.out_mpos + (size_t)e * D.NMARK * 3,
               D.out_mflow + (size_t)e * D.NMARK * 3);
 }
@@ -3024,7 +3032,7 @@ __global__ void k_readout(Dev D, int env0) {
 // k+1 with its scheduled targets, so converged envs do not wait for the slowest env
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NTHREADS) k_begin_sched(Dev D, int env0, const double* sched) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (threadIdx.x == 0) C.step = 0;
   if (C.disabled) { if (threadIdx.x == 0) { C.phase = PHASE_IDLE; C.status = ENV_DISABLED; } return; }
@@ -3033,7 +3041,7 @@ __global__ void __launch_bounds__(NTHREADS) k_begin_sched(Dev D, int env0, const
 
 __global__ void __launch_bounds__(NTHREADS) k_advance(Dev D, int env0, const double* sched, int nsteps, double* oc,
                                                       double* om, double* of) {
-  const int e = env0 + blockIdx.x;
+  const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   const int ph = C.phase;
   if (ph != PHASE_DONE && ph != PHASE_FAILED) return;
@@ -3046,7 +3054,7 @@ __global__ void __launch_bounds__(NTHREADS) k_advance(Dev D, int env0, const dou
   __syncthreads();
   if (ph == PHASE_DONE && k + 1 < nsteps) {
     begin_env(D, e, sched + ((size_t)(k + 1) * D.E + e) * D.NK * 12);
-    if (threadIdx.x == 0) { C.step = k + 1; atomicAdd(D.any_active, 1); }
+    if (threadIdx.x == 0) { C.step = k + 1; mark_active(D, e); }
   } else if (threadIdx.x == 0) {
     C.step = k + 1;
     if (ph == PHASE_DONE) C.phase = PHASE_IDLE;   // schedule finished (failures stay FAILED/disabled)

@@ -40,19 +40,28 @@ __device__ __forceinline__ void cl_sum2(double& a, double& b, double* red, doubl
   a = warp_sum(a);
   b = warp_sum(b);
   if (lane == 0) { red[8 + 2 * w] = a; red[8 + 2 * w + 1] = b; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if constexpr (NC == 1) {                       // one CTA: every thread sums the warp partials in order
+    __syncthreads();
     double ta = 0.0, tb = 0.0;
     for (int k = 0; k < nw; ++k) { ta += red[8 + 2 * k]; tb += red[8 + 2 * k + 1]; }
-    red[2 * slot] = ta;
-    red[2 * slot + 1] = tb;
-  }
-  cl_barrier<NC>();
-  double ta = 0.0, tb = 0.0;
+    a = ta;
+    b = tb;
+    (void)slot; (void)rred;
+  } else {                                       // CTA totals, then every rank's totals in rank order
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double ta = 0.0, tb = 0.0;
+      for (int k = 0; k < nw; ++k) { ta += red[8 + 2 * k]; tb += red[8 + 2 * k + 1]; }
+      red[2 * slot] = ta;
+      red[2 * slot + 1] = tb;
+    }
+    cl_barrier<NC>();
+    double ta = 0.0, tb = 0.0;
 #pragma unroll
-  for (int r = 0; r < NC; ++r) { ta += rred[r][2 * slot]; tb += rred[r][2 * slot + 1]; }
-  a = ta;
-  b = tb;
+    for (int r = 0; r < NC; ++r) { ta += rred[r][2 * slot]; tb += rred[r][2 * slot + 1]; }
+    a = ta;
+    b = tb;
+  }
 }
 
 // residual (matrix-free) pairs of one env, one pair per lane over all warps of CTA 0: soft-slot outputs
@@ -176,7 +185,7 @@ __device__ __noinline__ void cl_reinvert_bodies(const Dev& D, int e, double mu, 
 template <int NC>
 __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_constant__ Dev D, const __grid_constant__ ClPlan Pl, int env0, int force) {
   const int rank = NC == 1 ? 0 : (int)cg::this_cluster().block_rank();
-  const int e = env0 + (int)blockIdx.x / NC;
+  const int e = D.elist ? D.elist[blockIdx.x / NC] : env0 + (int)blockIdx.x / NC;
   EnvCtl& C = D.ctl[e];
   if (env_skip(D, e, force)) return;            // uniform over the cluster (all CTAs read the same phase)
   extern __shared__ __align__(16) unsigned char cl_dsm[];
@@ -267,6 +276,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       sHb[i] = D.Hb[(size_t)e * ND * 144 + i] + mu_in * D.My[(size_t)D.dof_body[d] * 144 + i % 144];
       sPb[i] = D.Pinv_b[(size_t)e * ND * 144 + i];
     }
+  __syncthreads();                                      // staged body blocks / couplings visible
 
   // residual (matrix-free) pairs: CTA 0 (cl_residual_pairs); their soft-slot outputs are added after barrier A
   const double* sout = D.sout + (size_t)e * 4 * D.act_cap * 3;
@@ -410,12 +420,14 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
           gloc += rb * ubr;
         }
       }
-      // per-CTA body partial: Σ over warps in order (after the CTA barrier inside cl_sum2's first stage)
-      __syncthreads();
-      for (int i = tid; i < 12 * ND; i += blockDim.x) {
-        double t = 0.0;
-        for (int k = 0; k < nw; ++k) t += wpart[(size_t)k * ND * 12 + i];
-        pbody[i] = t;
+      // per-CTA body partial (clusters): Σ over warps in order, read by CTA 0 after barrier A
+      if constexpr (NC > 1) {
+        __syncthreads();
+        for (int i = tid; i < 12 * ND; i += blockDim.x) {
+          double t = 0.0;
+          for (int k = 0; k < nw; ++k) t += wpart[(size_t)k * ND * 12 + i];
+          pbody[i] = t;
+        }
       }
       // ---------------- barrier A: γ, δ over the cluster
       cl_sum2<NC>(gloc, dloc, red, rred, 0);
@@ -442,8 +454,12 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       }
       if (!vt) {
         if (bown) {
+          if constexpr (NC == 1) {
+            for (int k = 0; k < nw; ++k) wb += wpart[((size_t)k * ND + bd) * 12 + brow];
+          } else {
 #pragma unroll
-          for (int rr = 0; rr < NC; ++rr) wb += rpb[rr][12 * bd + brow];
+            for (int rr = 0; rr < NC; ++rr) wb += rpb[rr][12 * bd + brow];
+          }
           pb = ubr + beta * pb;
           sb = wb + beta * sb;
           xb += alpha * pb;
@@ -466,6 +482,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       }
     }
     it_total += it;
+    if constexpr (NC == 1) __syncthreads();             // warp partials of the last reduction are read
     // gᵀx over the cluster (descent test of the LM rule)
     double gl = 0.0, dummy = 0.0;
     if (vown) gl = dot(ld3(g + 3 * v), x);

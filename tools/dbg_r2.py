@@ -50,6 +50,49 @@ def c3_fail(k_end=38):
             break
 
 
+def pcg():
+    """debug_pcg with the cluster kernel vs the oracle PCG, per block (C1 press, C2)."""
+    from oracle import contact as C, energy as En, mesh as M, solver as SO
+    for name in ("C1", "C2"):
+        sc = S.make_scene(name)
+        mod = M.prepare(sc)
+        ei = S.env_inputs(sc, [0], n_steps=1)
+        rng = np.random.default_rng(11)
+        xn, yn = ei.x0[0], ei.y0[0]
+        v = rng.normal(size=xn.shape) * 1e-3
+        x = xn + rng.normal(size=xn.shape) * 2e-5
+        y = yn.copy()
+        if name == "C1":
+            y[1, 2] -= 0.2e-3 - 0.04e-3
+        ctx = En.make_context(mod, xn, v, yn, np.zeros_like(yn), ei.ykin[0, 0], sc.config.dt)
+        b = T.Batch(sc, 1)
+        b.set_state(xn[None], yn[None], v[None])
+        b.set_targets(ei.ykin[0])
+        print(name, "kernel", b.pcg_kernel)
+        p_gpu, it, mu = b.debug_pcg(0, x, y, with_mu=True)
+        pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+        g, H = En.assemble(mod, ctx, x, y, pairs)
+        p_ref, it_ref = SO.block_jacobi_pcg(mod, H, g, sc.config.pcg_eta, sc.config.max_pcg)
+        V = mod.V
+        d = np.abs(p_gpu - p_ref)
+        print("  it", it, it_ref, "mu", mu, "max|p|", np.abs(p_ref).max(), "soft diff", d[:3 * V].max(), "body diff", d[3 * V:].max() if len(d) > 3 * V else 0)
+        print("  body gpu", p_gpu[3 * V:3 * V + 12])
+        print("  body ref", p_ref[3 * V:3 * V + 12])
+        print("  argmax", d.argmax(), p_gpu[d.argmax()], p_ref[d.argmax()])
+
+
+def sched(E=8, K=12):
+    sc = S.make_scene("C2")
+    ei = S.env_inputs(sc, np.arange(E), n_steps=K)
+    b = T.Batch(sc, E)
+    b.set_state(ei.x0, ei.y0)
+    yk = torch.tensor(ei.ykin, device="cuda")
+    for k in range(K // 2):
+        b.set_targets(yk[k])
+        print("lockstep", k, b.step(1), flush=True)
+    print("schedule", b.step_schedule(yk[K // 2:]), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "capacity"
-    {"capacity": capacity, "c3": c3_fail}[which]()
+    {"capacity": capacity, "c3": c3_fail, "pcg": pcg, "sched": sched}[which]()
