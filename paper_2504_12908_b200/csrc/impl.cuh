@@ -68,7 +68,7 @@ __host__ __device__ inline ClSmem cl_smem(int rpr, int nle, int nlb, int nd, int
   s.cpp = o; o = cl_align(o + 4 * (size_t)(rpr + 1));
   s.cpld = o; o = cl_align(o + 4 * (size_t)cplcap);
   s.cval = o; o = cl_align(o + 288 * (size_t)cplcap);
-  s.red = o; o = cl_align(o + 8 * (64 + 8));
+  s.red = o; o = cl_align(o + 8 * (8 + 2 * 32));
   s.end = o;
   return s;
 }

@@ -11,14 +11,14 @@
 // body, lane = row: its Hb row and block-Jacobi inverse row in registers) and the few matrix-free
 // ("residual") contact pairs.
 //
-// Iteration: Chronopoulos–Gear PCG (one fused reduction of γ = rᵀu and δ = uᵀAu per iteration) —
-//   u = M⁻¹r, w = Au, γ = (r,u), δ = (w,u), β = γ/γ₋, α = γ/(δ − βγ/α₋), p = u + βp, s = w + βs,
-//   x += αp, r −= αs,
-// the same iterates as standard PCG in exact arithmetic (same stopping test rᵀz ≤ η²r₀ᵀz₀, same
-// negative-curvature test pᵀAp = δ − βγ/α₋ ≤ 0).  Two cluster barriers per iteration: A after the SpMV
-// partials (γ, δ, body coupling sums), B after u is rewritten.  All sums run in fixed orders (warp
-// butterflies, warps in order, ranks in order), so results are bitwise reproducible and independent of
-// the batch size.
+// Iteration: standard (Hestenes–Stiefel) block-Jacobi PCG, the oracle's algorithm (R15):
+//   q = Ad; α = rᵀz / dᵀq (dᵀq ≤ 0 → not SPD); x += αd; r −= αq; z = M⁻¹r; β = rᵀz_new / rᵀz; d = z + βd,
+// with three fused phases per iteration separated by barriers: A after the SpMV and dᵀq partials (and
+// the body coupling sums), B after the x/r/z update and rᵀz partials, C after d is rewritten.  (A
+// single-reduction Chronopoulos–Gear variant was tried: its recurrence for dᵀAd lost positivity on
+// near-singular exact contact Hessians, escalating the LM shift where the oracle's PCG did not.)  All
+// sums run in fixed orders (warp butterflies, warps in order, ranks in order), so results are bitwise
+// reproducible and independent of the batch size.
 #include <cooperative_groups.h>
 
 namespace tac {
@@ -34,24 +34,29 @@ __device__ __forceinline__ void cl_barrier() {
 // sum of two per-thread values over the whole cluster, identical in every thread (fixed order).
 // `red` = this CTA's scratch (≥ 2·nwarps + 4 doubles); slot selects the CTA-total pair (0 or 1) so
 // back-to-back reductions do not overwrite totals other CTAs may still be reading.
+// sum of two per-thread values over the whole cluster, identical in every thread (fixed order).
+// `red` = this CTA's scratch (72 doubles): totals in [2·slot, 2·slot+2), warp partials in
+// [8 + 32·slot, 8 + 32·slot + 2·nwarps) — separate regions per slot, so two reductions back to back
+// (the PCG's dᵀq and rᵀz) never overwrite values another warp or CTA may still be reading.
 template <int NC>
 __device__ __forceinline__ void cl_sum2(double& a, double& b, double* red, double* const* rred, int slot) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* part = red + 8 + 32 * slot;
   a = warp_sum(a);
   b = warp_sum(b);
-  if (lane == 0) { red[8 + 2 * w] = a; red[8 + 2 * w + 1] = b; }
+  if (lane == 0) { part[2 * w] = a; part[2 * w + 1] = b; }
   if constexpr (NC == 1) {                       // one CTA: every thread sums the warp partials in order
     __syncthreads();
     double ta = 0.0, tb = 0.0;
-    for (int k = 0; k < nw; ++k) { ta += red[8 + 2 * k]; tb += red[8 + 2 * k + 1]; }
+    for (int k = 0; k < nw; ++k) { ta += part[2 * k]; tb += part[2 * k + 1]; }
     a = ta;
     b = tb;
-    (void)slot; (void)rred;
+    (void)rred;
   } else {                                       // CTA totals, then every rank's totals in rank order
     __syncthreads();
     if (threadIdx.x == 0) {
       double ta = 0.0, tb = 0.0;
-      for (int k = 0; k < nw; ++k) { ta += red[8 + 2 * k]; tb += red[8 + 2 * k + 1]; }
+      for (int k = 0; k < nw; ++k) { ta += part[2 * k]; tb += part[2 * k + 1]; }
       red[2 * slot] = ta;
       red[2 * slot + 1] = tb;
     }
@@ -306,36 +311,45 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       }
       cl_reinvert_bodies(D, e, mu, rank == 0, !vt && (tid - Pl.nvt) < 32, sHb, sPb);
     }
-    // x = 0, r = −g, u = M⁻¹ r
+    // x = 0, r = −g, z = M⁻¹ r, d = z (d lives in shared memory: the SpMV gathers neighbours' d)
     if (vown) {
       x = mk(0, 0, 0);
       r = -ld3(g + 3 * v);
       uu = mk(Ps[0] * r.x + Ps[1] * r.y + Ps[2] * r.z, Ps[3] * r.x + Ps[4] * r.y + Ps[5] * r.z,
-              Ps[6] * r.x + Ps[7] * r.y + Ps[8] * r.z);
+              Ps[6] * r.x + Ps[7] * r.y + Ps[8] * r.z);          // uu = d
       st3(usm + 3 * vl, uu);
-      pp = mk(0, 0, 0); ss = mk(0, 0, 0);
     }
+    double zb = 0.0;
     if (bown) {
-      xb = 0.0; pb = 0.0; sb = 0.0;
+      xb = 0.0;
       rb = -g[3 * V + 12 * bd + brow];
     }
     if (!vt) {
-      double u_ = 0.0;
+      double z_ = 0.0;
 #pragma unroll
-      for (int c = 0; c < 12; ++c) u_ += (bown ? sPb[144 * bd + 12 * brow + c] : 0.0) * __shfl_sync(0xffffffffu, rb, hl | c);
-      ubr = u_;
+      for (int c = 0; c < 12; ++c) z_ += (bown ? sPb[144 * bd + 12 * brow + c] : 0.0) * __shfl_sync(0xffffffffu, rb, hl | c);
+      zb = z_;
+      ubr = z_;                                                    // d_b = z_b
       if (bown) ub[12 * bd + brow] = ubr;
     }
-    cl_barrier<NC>();
+    double rz;
+    {
+      double a0 = vown ? dot(r, uu) : 0.0, b0 = 0.0;
+      if (bown) a0 = rb * zb;
+      cl_sum2<NC>(a0, b0, red, rred, 0);
+      rz = a0;
+    }
+    const double stop = D.eta * D.eta * rz;
+    zero_g = rz == 0.0;
+    bad = !(rz == rz);
     if constexpr (NC > 1) {
       for (int i = tid; i < 12 * ND; i += blockDim.x) ub[i] = ub0[i];
-      __syncthreads();
     }
-    double gam_prev = 1.0, alpha_prev = 1.0, stop = 0.0;
+    __syncthreads();
     int it = 0;
-    for (;;) {
-      // ---------------- SpMV w = (H + μM) u and the partials of γ = rᵀu, δ = uᵀ(H + μM)u
-      double dloc = 0.0, gloc = 0.0;
+    while (!bad && it < D.max_pcg && rz > stop) {
+      // ---------------- q = (H + μM) d and the partials of dᵀq
+      double dloc = 0.0;
       v3 w = mk(0, 0, 0);
       if (vown) {
         const double* hd = sHd + vl;
@@ -350,7 +364,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
           w += (bk.x & 1) ? mul33T(Bk, uj) : mul33(Bk, uj);
         }
         if (mu != 0.0) w += (mu * mv) * uu;
-        double cu = 0.0;                                  // u_vᵀ C u_d (counted for the body side)
+        double cu = 0.0;                                  // d_vᵀ C d_b (counted again for the body side)
         for (int c = cpp[vl] - c0, c1 = cpp[vl + 1] - c0; c < c1; ++c) {
           const int d = cstaged ? cpld[c] : cd_g[c0 + c];
           const double* ud = ub + 12 * d;
@@ -367,9 +381,8 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
           cu += dot(uu, cu3);
         }
         dloc = dot(uu, w) + cu;
-        gloc = dot(r, uu);
       }
-      // body coupling partials Σ_c Cᵀ u_v per warp (fixed butterfly), one body at a time
+      // body coupling partials Σ_c Cᵀ d_v per warp (fixed butterfly), one body at a time
       if (vt && ND > 0) {
         int cb = vown ? cpp[vl] - c0 : 0, ce = vown ? cpp[vl + 1] - c0 : 0;
         for (int d = 0; d < ND; ++d) {
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       }
       // residual pairs (CTA 0): outputs to sout (soft slots) and the warp partials (body slots)
       if (rank == 0 && nres > 0) dloc += cl_residual_pairs<NC>(D, e, nres, rpr, usm, ub, wpart, ru);
-      // body rows (CTA 0): own part (H_b + μM) u_b
+      // body rows (CTA 0): own part (H_b + μM) d_b
       double wb = 0.0;
       if (!vt) {
         double hu = 0.0;
@@ -417,7 +430,6 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
         if (bown) {
           wb = hu;
           dloc += ubr * hu;
-          gloc += rb * ubr;
         }
       }
       // per-CTA body partial (clusters): Σ over warps in order, read by CTA 0 after barrier A
@@ -429,28 +441,19 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
           pbody[i] = t;
         }
       }
-      // ---------------- barrier A: γ, δ over the cluster
-      cl_sum2<NC>(gloc, dloc, red, rred, 0);
-      const double gam = gloc, del = dloc;
-      if (it == 0) {
-        stop = D.eta * D.eta * gam;
-        zero_g = gam == 0.0;
-      }
-      if (!(gam == gam) || !(del == del)) { bad = true; break; }
-      if (it >= D.max_pcg || !(gam > stop)) break;
-      const double beta = it == 0 ? 0.0 : gam / gam_prev;
-      const double pAp = it == 0 ? del : del - beta * gam / alpha_prev;
-      if (!(pAp > 0.0)) { bad = true; break; }
-      const double alpha = gam / pAp;
+      // ---------------- barrier A: dᵀq over the cluster → α
+      double dq = dloc, unused = 0.0;
+      cl_sum2<NC>(dq, unused, red, rred, 0);
+      if (!(dq > 0.0)) { bad = true; break; }            // not SPD along d (uniform over the cluster)
+      const double alpha = rz / dq;
+      double rzl = 0.0;
       if (vown) {
         for (int j = ccp[v], j1 = ccp[v] + rcn[v]; j < j1; ++j) w += ld3(sout + 3 * j);   // residual pair outputs
-        pp = uu + beta * pp;
-        ss = w + beta * ss;
-        x += alpha * pp;
-        r = r - alpha * ss;
-        uu = mk(Ps[0] * r.x + Ps[1] * r.y + Ps[2] * r.z, Ps[3] * r.x + Ps[4] * r.y + Ps[5] * r.z,
-                Ps[6] * r.x + Ps[7] * r.y + Ps[8] * r.z);
-        st3(usm + 3 * vl, uu);
+        x += alpha * uu;
+        r = r - alpha * w;
+        pp = mk(Ps[0] * r.x + Ps[1] * r.y + Ps[2] * r.z, Ps[3] * r.x + Ps[4] * r.y + Ps[5] * r.z,
+                Ps[6] * r.x + Ps[7] * r.y + Ps[8] * r.z);          // pp = z
+        rzl = dot(r, pp);
       }
       if (!vt) {
         if (bown) {
@@ -460,21 +463,31 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
 #pragma unroll
             for (int rr = 0; rr < NC; ++rr) wb += rpb[rr][12 * bd + brow];
           }
-          pb = ubr + beta * pb;
-          sb = wb + beta * sb;
-          xb += alpha * pb;
-          rb -= alpha * sb;
+          xb += alpha * ubr;
+          rb -= alpha * wb;
         }
-        double u_ = 0.0;
+        double z_ = 0.0;
 #pragma unroll
-        for (int c = 0; c < 12; ++c) u_ += (bown ? sPb[144 * bd + 12 * brow + c] : 0.0) * __shfl_sync(0xffffffffu, rb, hl | c);
-        ubr = u_;
-        if (bown) ub[12 * bd + brow] = ubr;
+        for (int c = 0; c < 12; ++c) z_ += (bown ? sPb[144 * bd + 12 * brow + c] : 0.0) * __shfl_sync(0xffffffffu, rb, hl | c);
+        zb = z_;
+        if (bown) rzl = rb * zb;
       }
-      gam_prev = gam;
-      alpha_prev = alpha;
+      // ---------------- barrier B: rᵀz over the cluster → β
+      double rzn = rzl, unused2 = 0.0;
+      cl_sum2<NC>(rzn, unused2, red, rred, 1);
+      const double beta = rzn / rz;
+      rz = rzn;
       ++it;
-      // ---------------- barrier B: u (and the bodies' u) visible to the cluster
+      if (!(rz == rz)) { bad = true; break; }
+      if (vown) {
+        uu = pp + beta * uu;
+        st3(usm + 3 * vl, uu);
+      }
+      if (bown) {
+        ubr = zb + beta * ubr;
+        ub[12 * bd + brow] = ubr;
+      }
+      // ---------------- barrier C: d (and the bodies' d) visible to the cluster
       cl_barrier<NC>();
       if constexpr (NC > 1) {
         for (int i = tid; i < 12 * ND; i += blockDim.x) ub[i] = ub0[i];
@@ -482,7 +495,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       }
     }
     it_total += it;
-    if constexpr (NC == 1) __syncthreads();             // warp partials of the last reduction are read
+    cl_barrier<NC>();                                   // every read of the last reduction's values is done
     // gᵀx over the cluster (descent test of the LM rule)
     double gl = 0.0, dummy = 0.0;
     if (vown) gl = dot(ld3(g + 3 * v), x);
