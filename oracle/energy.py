@@ -28,7 +28,7 @@ from .mesh import Model, affine_jacobian
 
 torch.set_default_dtype(torch.float64)
 
-TERMS = ("inertia", "elastic", "ortho", "gravity", "barrier", "al")
+TERMS = ("inertia", "elastic", "ortho", "gravity", "barrier", "al", "friction")
 
 
 # ---------------------------------------------------------------------------------------------
@@ -89,6 +89,7 @@ class Context:
     lam_att: np.ndarray       # (NC,3)
     lam_kin: np.ndarray       # (NK,12)
     rho: float
+    fric: object = None       # oracle.friction.FrictionData (lagged at xⁿ) when μ > 0
 
 
 def attached_targets(model: Model, y_pose: np.ndarray) -> np.ndarray:
@@ -107,12 +108,16 @@ def make_context(model: Model, x_n, v_n, y_n, ydot_n, y_targets_kin, dt, lam_att
     y_pose = np.array(y_n, np.float64, copy=True)
     for i, b in enumerate(model.kin_bodies):
         y_pose[b] = y_targets_kin[i]
+    fric = None
+    if getattr(cfg, "mu_friction", 0.0) > 0.0:
+        from . import friction as Fr
+        fric = Fr.lagged(model, x_n, y_n)
     return Context(x_tilde=x_n + dt * v_n, y_tilde=y_n + dt * ydot_n, y_static=np.array(y_n, copy=True),
                    s_att=attached_targets(model, y_pose),
                    s_kin=np.array(y_targets_kin, np.float64).reshape(-1, 12),
                    lam_att=np.zeros((len(model.att_vert), 3)) if lam_att is None else lam_att,
                    lam_kin=np.zeros((len(model.kin_bodies), 12)) if lam_kin is None else lam_kin,
-                   rho=cfg.al_rho0 if rho is None else rho)
+                   rho=cfg.al_rho0 if rho is None else rho, fric=fric)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -261,6 +266,25 @@ def energy_terms(model: Model, ctx: Context, x, y, pairs: Pairs):
             out["al"] += float(0.5 * ctx.rho * r @ (M @ r) - _T(ctx.lam_kin[k]) @ (M @ r))
     # barrier
     out["barrier"] = float(sum(_pair_values(model, x, y, pairs)))
+    # lagged friction Δt² Σ_k D_k (oracle/friction.py)
+    out["friction"] = float(sum(_friction_values(model, ctx, x, y)))
+    return out
+
+
+def _friction_values(model, ctx, x, y):
+    fr = ctx.fric
+    if fr is None or len(fr) == 0:
+        return []
+    from . import friction as Fr
+    from .mesh import all_positions
+    P = all_positions(model, x, y)
+    dt2 = model.scene.config.dt ** 2
+    out = []
+    for k in range(len(fr)):
+        X = P[fr.vids[k]]
+        rest = Fr.tangential_sq(X, fr.Xn[k], fr.gamma[k], fr.nhat[k]) == 0.0
+        out.append(dt2 * float(Fr.pair_energy(_T(X.ravel()), _T(fr.Xn[k].ravel()), _T(fr.gamma[k]), _T(fr.nhat[k]),
+                                              float(fr.mu_lam[k]), fr.eps, rest)))
     return out
 
 
@@ -399,6 +423,30 @@ def assemble(model: Model, ctx: Context, x, y, pairs: Pairs, project=True):
                     if len(rj) == 0:
                         continue
                     add_block(ri, rj, Ji.T @ Hp[j, 3 * si:3 * si + 3, 3 * sj:3 * sj + 3] @ Jj)
+    # lagged friction pairs: gradient and Hessian of Δt²·D_k by autograd on the 12 slot positions (the
+    # Hessian of μλ f0(‖u‖) is PSD for the paper's f1, so no projection), pulled back like the barrier
+    fr = ctx.fric
+    if fr is not None and len(fr):
+        from . import friction as Fr
+        from .mesh import all_positions
+        P = all_positions(model, x, y)
+        for k in range(len(fr)):
+            X = P[fr.vids[k]]
+            rest = Fr.tangential_sq(X, fr.Xn[k], fr.gamma[k], fr.nhat[k]) == 0.0
+            args = (_T(fr.Xn[k].ravel()), _T(fr.gamma[k]), _T(fr.nhat[k]), float(fr.mu_lam[k]), fr.eps, rest)
+            fk = lambda z: dt2 * Fr.pair_energy(z, *args)
+            Xt = _T(X.ravel())
+            gk = torch.autograd.functional.jacobian(fk, Xt).numpy()
+            Hk = torch.autograd.functional.hessian(fk, Xt).numpy()
+            maps = [vertex_dof_map(model, v) for v in fr.vids[k]]
+            for si, (ri, Ji) in enumerate(maps):
+                if len(ri) == 0:
+                    continue
+                g[ri] += Ji.T @ gk[3 * si:3 * si + 3]
+                for sj, (rj, Jj) in enumerate(maps):
+                    if len(rj) == 0:
+                        continue
+                    add_block(ri, rj, Ji.T @ Hk[3 * si:3 * si + 3, 3 * sj:3 * sj + 3] @ Jj)
     if rows:
         H = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n)).tocsr()
     else:

@@ -718,3 +718,155 @@ def test_energy_monotone_within_step():
             prev = t["E1"]
             n_checked += 1
     assert n_checked >= 3
+
+
+# ------------------------------------------------------------------------------------ lagged friction
+
+from oracle import friction as Fr
+
+
+def test_friction_f0_f1_closed_forms():
+    """f1 continuous at ε_vΔt (left limit −1 + 2 = 1), f1(0⁺) = 0, f0(0) = ε/3 and
+    f0(ε) = ε (the paper's f0(x) = ∫_ε^x f1 + ε at x = 0 and x = ε), and df0/dx = f1 (the written-out
+    antiderivative against the paper's f1)."""
+    eps = 1e-3 * 0.01
+    e = T(np.array([eps]))
+    assert float(Fr.f1(e * (1 - 1e-12), eps)) == pytest.approx(1.0, abs=1e-11) and float(Fr.f1(e, eps)) == 1.0
+    assert float(Fr.f1(T(np.array([1e-30])), eps)) == pytest.approx(0.0, abs=1e-20)
+    assert float(Fr.f0(T(np.array([0.0])), eps)) == pytest.approx(eps / 3, rel=1e-14)
+    assert float(Fr.f0(e, eps)) == pytest.approx(eps, rel=1e-14)
+    xs = T(np.array([0.1, 0.5, 0.99, 1.5, 3.0]) * eps).requires_grad_(True)
+    (d,) = torch.autograd.grad(Fr.f0(xs, eps).sum(), xs)
+    assert np.allclose(d.numpy(), Fr.f1(xs.detach(), eps).numpy(), rtol=1e-12, atol=1e-15)
+
+
+def test_closest_point_weights_give_the_pair_distance():
+    """Γ_k X is the separation of the closest points: ‖Γ_k X‖² equals the classified squared distance
+    for PT and EE pairs of every type (random configurations)."""
+    rng = np.random.default_rng(5)
+    seen_pt, seen_ee = set(), set()
+    for _ in range(3000):
+        X = rng.normal(size=(4, 3))
+        for kind in (0, 1):
+            if kind == 0:
+                typ, d2 = D.pt_type(X[0], X[1], X[2], X[3])
+                seen_pt.add(int(typ))
+            else:
+                typ, d2 = D.ee_type(X[0], X[1], X[2], X[3])
+                seen_ee.add(int(typ))
+            g = Fr.closest_weights(kind, int(typ), X)
+            sep = g @ X
+            assert abs(sep @ sep - float(d2)) <= 1e-10 * float(d2), (kind, typ)
+            assert abs(g.sum()) < 1e-12                       # a difference of two points
+    assert seen_pt == set(range(7)) and {0, 1, 2, 3, 4, 5, 6, 7, 8} >= seen_ee >= {1, 3, 4, 5, 7}
+
+
+def _fric_pair_state(mu=0.5):
+    import dataclasses
+    sc = S.make_scene("P1")
+    sc.config = dataclasses.replace(sc.config, mu_friction=mu)
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=1)
+    return sc, mod, ei.x0[0], ei.y0[0]
+
+
+def test_friction_lagged_force_and_plateau():
+    """Single PT pair (scene P1, apex d̂/2 above a static face): λⁿ = κ A_v |b′(d̂/2)| with b′(d̂/2) from
+    the golden closed form; sliding the apex tangentially by 2ε_vΔt, the friction force has
+    magnitude μλⁿ exactly (dynamic plateau) and opposes the slide; with no slide it is 0."""
+    sc, mod, x, y = _fric_pair_state(0.5)
+    cfg = sc.config
+    ctx = En.make_context(mod, x, np.zeros_like(x), y, np.zeros_like(y), np.zeros((0, 12)), cfg.dt)
+    fr = ctx.fric
+    assert len(fr) == 1
+    X = sc.soft[0].rest_pos
+    A_v = (_area(X, (0, 1, 3)) + _area(X, (0, 1, 2)) + _area(X, (0, 2, 3))) / 3.0
+    lam = cfg.kappa * A_v * abs(GOLD["barrier"]["db_at_half_over_dhat"] * cfg.dhat)
+    assert fr.mu_lam[0] == pytest.approx(0.5 * lam, rel=1e-12)
+    assert np.allclose(np.abs(fr.nhat[0]), [0, 0, 1], atol=1e-12)
+    eps = cfg.eps_v * cfg.dt
+    for slide, expect in ((0.0, 0.0), (2 * eps, 0.5 * lam)):
+        xs = x.copy()
+        xs[0] += slide * np.array([0.6, 0.8, 0.0])            # apex only, in the tangent plane
+        pairs = C.active_pairs(mod, M.all_positions(mod, xs, y))
+        g, _ = En.assemble(mod, ctx, xs, y, pairs, project=False)
+        ctx0 = dataclasses_replace(ctx, fric=None)
+        g0, _ = En.assemble(mod, ctx0, xs, y, pairs, project=False)
+        f = -(g - g0)[:3] / cfg.dt ** 2                       # friction force on the apex (E carries Δt²·D)
+        assert np.linalg.norm(f) == pytest.approx(expect, rel=1e-12, abs=1e-30)
+        if slide:
+            assert f @ np.array([0.6, 0.8, 0.0]) < 0
+
+
+def dataclasses_replace(obj, **kw):
+    import dataclasses
+    return dataclasses.replace(obj, **kw)
+
+
+def test_friction_gradient_and_hvp_vs_finite_differences():
+    """Total energy with friction (C1 press, μ = 0.5, lagged at xⁿ, iterate slid away from xⁿ):
+    gradient and exact-Hessian HVP against central differences."""
+    import dataclasses
+    sc, mod, ctx, x, y = _press_state()
+    sc.config = dataclasses.replace(sc.config, mu_friction=0.5)
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=1)
+    yn = ei.y0[0].copy()
+    yn[1, 2] -= 0.2e-3 - 0.04e-3
+    ctx = En.make_context(mod, ei.x0[0], np.zeros_like(ei.x0[0]), yn, np.zeros_like(yn), ei.ykin[0, 0], sc.config.dt)
+    assert len(ctx.fric) > 10
+    rng = np.random.default_rng(3)
+    x = ei.x0[0] + rng.normal(size=ei.x0[0].shape) * 3e-6
+    y = yn.copy()
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    g, H = En.assemble(mod, ctx, x, y, pairs, project=False)
+    q = En.pack(mod, x, y)
+
+    def E(qq):
+        xx, yy = En.unpack(mod, qq, y)
+        return En.energy_terms(mod, ctx, xx, yy, C.active_pairs(mod, M.all_positions(mod, xx, yy)))["friction"]
+
+    gf, _ = En.assemble(mod, dataclasses.replace(ctx, fric=None), x, y, pairs, project=False)
+    gfr = g - gf
+    idx = rng.choice(3 * mod.V, 12, replace=False)
+    h = 1e-9
+    for i in idx:
+        e = np.zeros_like(q)
+        e[i] = h
+        fd = (E(q + e) - E(q - e)) / (2 * h)
+        assert fd == pytest.approx(gfr[i], rel=1e-5, abs=1e-6 * np.abs(gfr).max())
+
+
+def _incline(mu, tan_theta):
+    import dataclasses
+    th = math.atan(tan_theta)
+    pV, pT = S.box_surface((0.04, 0.04, 0.01))
+    cV, cT = S.box_surface((0.01, 0.01, 0.01))
+    plate = S.AffineBody(pV, pT, kind=S.STATIC)
+    cube = S.AffineBody(cV, cT, kind=S.DYNAMIC)
+    g = 9.81 * np.array([math.sin(th), 0.0, -math.cos(th)])      # plane inclined by θ about y
+    cfg = dataclasses.replace(S.Config(dt=0.01), mu_friction=mu, eps_v=1e-3)
+    sc = S.Scene("C1", [], [plate, cube], g, cfg, n_steps=1)
+    y0 = np.array([S.pose([0, 0, -0.005]), S.pose([0.0013, 0.0007, 0.005 + 0.5e-4], S.rot_z(0.3))])
+    return sc, M.prepare(sc), y0
+
+
+@pytest.mark.parametrize("mu", [0.2, 0.5])
+def test_friction_incline_stick_and_slip(mu):
+    """A stiff cube on a plane inclined by θ (gravity tilted): with tan θ = 0.9μ it sticks (per-step
+    slide < 10·ε_vΔt after settling), with tan θ = 1.1μ it slides with growing per-step displacement
+    (Coulomb threshold tan θ = μ)."""
+    out = {}
+    for label, t in (("stick", 0.9 * mu), ("slip", 1.1 * mu)):
+        sc, mod, y0 = _incline(mu, t)
+        st = SO.State(np.zeros((0, 3)), np.zeros((0, 3)), y0.copy(), np.zeros_like(y0))
+        L = M.env_scale(mod, st.x, st.y)
+        xs = []
+        for k in range(12):
+            st, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=L)
+            assert stats.status == SO.ENV_OK, (label, k)
+            xs.append(st.y[1, 0])
+        out[label] = np.diff(np.array(xs))
+    eps_dt = 1e-3 * 0.01
+    assert np.all(np.abs(out["stick"][4:]) < 10 * eps_dt), out["stick"]
+    assert np.all(out["slip"][4:] > 0) and np.all(np.diff(out["slip"][4:]) > 0), out["slip"]
