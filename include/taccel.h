@@ -129,6 +129,9 @@ typedef struct {
                                     reused while every surface vertex stays within δ of its box at the
                                     last build; 0 = rebuild every Newton iteration (DESIGN R11b)       */
   int32_t cand_capacity_per_env, active_capacity_per_env;
+  double mu_friction;            /* Coulomb coefficient μ of the lagged friction potential D_k; 0 = frictionless.
+                                    μ > 0 requires hessian_mode 2 (the friction Hessian is PSD and is not projected) */
+  double eps_v;                  /* ε_v (m/s) of the friction transition f1 */
 } tac_config;
 
 typedef struct {
@@ -144,6 +147,8 @@ typedef struct {
                                     soft bodies or two DoF bodies in one pair) */
   int32_t n_couplings;           /* last Newton iteration: condensed 3×12 soft–body coupling blocks */
   double lm_mu;                  /* LM shift μ of the last solve (hessian_mode 2; 0 = pure Newton) */
+  int32_t n_friction;            /* lagged friction pairs of the last step (the active set at its start xⁿ) */
+  int32_t pad_;
 } tac_env_stats;
 
 struct tac_batch;
@@ -217,10 +222,12 @@ tac_status tac_profile_iterations(tac_batch* b, int32_t* active, double* ms, int
  * tac_debug_eval: at (x [V][3], y [NA][12]) of env `env`, with x̃/ỹ from the env's last set_state
  * and kinematic targets from the last set_targets, and AL multipliers lam_att [NC][3],
  * lam_kin [NK][12] (NULL → 0) and penalty rho (≤ 0 → al_rho0): the six energy terms
- * e_terms[6] = {inertia, elastic, ortho, gravity, barrier, AL}, the gradient grad [n] over
+ * e_terms[7] = {inertia, elastic, ortho, gravity, barrier, AL, friction}, the gradient grad [n] over
  * q = [x; y of non-static bodies] and hv = H·v_in [n] with H the PSD-projected Hessian (any
  * output may be NULL); exact_hessian = 1 uses the unprojected element Hessians instead.  The
- * active set is recomputed at (x, y) through the spatial hash. */
+ * active set is recomputed at (x, y) through the spatial hash.  With friction (μ > 0) the lagged
+ * friction pairs and their data are frozen at the env's current state xⁿ (as at the start of a step),
+ * and exact_hessian must be 1. */
 tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x, const double* y, const double* lam_att,
                           const double* lam_kin, double rho, int32_t exact_hessian, const double* v_in,
                           double* e_terms, double* grad, double* hv, void* stream);

@@ -639,6 +639,11 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.eterm = C.take<double>(e * 8);
   D.out_coat = C.take<double>(e * H.NCOAT * 3 + 1); D.out_mpos = C.take<double>(e * H.NMARK * 3 + 1);
   D.out_mflow = C.take<double>(e * H.NMARK * 3 + 1);
+  {
+    const size_t fc = D.mu_f > 0.0 ? (size_t)D.act_cap : 1;
+    D.fr_info = C.take<int>(e * fc * 4); D.fr_vid = C.take<int>(e * fc * 4); D.fr_slot = C.take<int>(e * fc * 4);
+    D.fr_res = C.take<int>(e * fc); D.fr_xb = C.take<double>(e * fc * 12); D.fr_dat = C.take<double>(e * fc * 16);
+  }
   D.any_active = C.take<int>(1);
   D.act_list = C.take<int>(2 * e);
   return C.off + 256;
@@ -661,6 +666,7 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.max_newton = cfg->max_newton; D.max_al = cfg->max_al_rounds; D.max_pcg = cfg->max_pcg;
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
   D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.bp_margin = cfg->bp_margin; D.K = (double)std::max(cfg->ls_expand, 1);
+  D.mu_f = cfg->mu_friction; D.eps_v = cfg->eps_v;
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
   D.elist = nullptr; D.elist_out = nullptr;
   D.cl.nc = H.cl_nc; D.cl.rpr = H.cl_rpr; D.cl.threads = H.cl_threads; D.cl.nvt = H.cl_nvt;
@@ -670,8 +676,11 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
 static tac_status check_cfg(const tac_config* c) {
   if (!(c->max_step_rel > 0) || !(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
       c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1) || c->hessian_mode < 0 ||
-      c->hessian_mode > 2 || !(c->lm_mu0 > 0) || !(c->bp_margin >= 0) || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0)
+      c->hessian_mode > 2 || !(c->lm_mu0 > 0) || !(c->bp_margin >= 0) || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0 ||
+      !(c->mu_friction >= 0) || !(c->eps_v > 0))
     return fail(TAC_E_INVALID, "invalid tac_config");
+  if (c->mu_friction > 0 && c->hessian_mode != 2)
+    return fail(TAC_E_INVALID, "friction (mu_friction > 0) requires hessian_mode 2");
   return TAC_OK;
 }
 
@@ -1029,13 +1038,14 @@ extern "C" tac_status tac_get_stats(tac_batch* b, tac_env_stats* out, void* stre
   for (int e = 0; e < b->D.E; ++e) {
     const EnvCtl& c = b->hctl[e];
     out[e].status = c.status; out[e].newton_iters = c.newton; out[e].pcg_iters = c.pcg; out[e].ls_backtracks = c.ls_bt;
-    out[e].n_active = c.n_act; out[e].al_rounds = c.al_rounds; out[e].n_candidates = c.ncand;
+    out[e].n_active = c.n_act - c.n_fr; out[e].al_rounds = c.al_rounds; out[e].n_candidates = c.ncand;
     out[e].alpha_min = c.alpha_min; out[e].energy = c.energy; out[e].constraint_residual = c.residual;
     out[e].pcg_iters_total = c.pcg_total; out[e].pcg_alg_bytes_total = c.pcg_bytes;
     out[e].diag[0] = c.alpha_ccd; out[e].diag[1] = c.gp; out[e].diag[2] = c.ls_E0; out[e].diag[3] = c.ls_E1;
     out[e].min_dist = c.min_d2 < b->D.dhat * b->D.dhat ? std::sqrt(c.min_d2) : HUGE_VAL;
     out[e].n_residual = c.n_res; out[e].n_couplings = c.n_cpl;
     out[e].lm_mu = c.mu_used;
+    out[e].n_friction = c.n_fr; out[e].pad_ = 0;
   }
   return TAC_OK;
 }
@@ -1098,6 +1108,11 @@ static tac_status dbg_enter(DebugScope& S, const double* x, const double* y, con
   c.disabled = 0;
   CUDA_TRY(cudaMemcpyAsync(D.ctl + e, &c, sizeof(EnvCtl), cudaMemcpyHostToDevice, S.st));
   launch_begin(D, e, 1, S.st);
+  if (D.mu_f > 0.0) {                 // lagged friction frozen at the env's state xⁿ (as at a step start)
+    launch_positions(D, e, 1, 0, 1, S.st);
+    launch_broad(D, e, 1, 0, 1, S.st);
+    launch_narrow(D, e, 1, 1, S.st);
+  }
   if (D.V) CUDA_TRY(cudaMemcpyAsync(D.q + (size_t)e * D.n, x, (size_t)3 * D.V * 8, cudaMemcpyHostToDevice, S.st));
   CUDA_TRY(cudaMemcpyAsync(D.ystage + (size_t)e * D.NA * 12, y, (size_t)D.NA * 96, cudaMemcpyHostToDevice, S.st));
   launch_scatter_y(D, e, 1, 0, S.st);
@@ -1147,6 +1162,7 @@ extern "C" tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x,
                                      const double* lam_kin, double rho, int32_t exact_hessian, const double* v_in,
                                      double* e_terms, double* grad, double* hv, void* stream) {
   DBG_CHECK(b, env);
+  if (b->D.mu_f > 0.0 && !exact_hessian) return fail(TAC_E_INVALID, "friction batches evaluate the exact Hessian only");
   DebugScope S{b, env, (cudaStream_t)stream};
   tac_status s = dbg_enter(S, x, y, lam_att, lam_kin, rho, exact_hessian);
   Dev& D = b->D;
@@ -1156,7 +1172,7 @@ extern "C" tac_status tac_debug_eval(tac_batch* b, int32_t env, const double* x,
     double t[8];
     cudaMemcpyAsync(t, D.eterm + (size_t)env * 8, 64, cudaMemcpyDeviceToHost, S.st);
     cudaStreamSynchronize(S.st);
-    for (int i = 0; i < 6; ++i) e_terms[i] = t[i];
+    for (int i = 0; i < 7; ++i) e_terms[i] = t[i];
   }
   if (!s && grad) {
     cudaMemcpyAsync(grad, D.g + (size_t)env * D.n, D.n * 8, cudaMemcpyDeviceToHost, S.st);
@@ -1179,7 +1195,7 @@ static tac_status copy_pairs(tac_batch* b, int env, bool active, int32_t* pairs,
   CUDA_TRY(cudaMemcpyAsync(&c, D.ctl + env, sizeof(EnvCtl), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (c.overflow) return fail(TAC_E_CAPACITY, "pair capacity exceeded");
-  int n = active ? c.n_act : c.ncand;
+  int n = active ? c.n_act - c.n_fr : c.ncand;         // barrier pairs (friction entries follow them)
   if (count) *count = n;
   if (!pairs) return TAC_OK;
   int m = std::min(n, cap);
@@ -1260,6 +1276,7 @@ extern "C" tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, 
                                     double mu, double* p, int32_t* iters, double* mu_used, void* stream) {
   DBG_CHECK(b, env);
   if (mu < 0) return fail(TAC_E_INVALID, "mu must be >= 0");
+  if (b->D.mu_f > 0.0 && !exact_hessian) return fail(TAC_E_INVALID, "friction batches solve with the exact Hessian only");
   DebugScope S{b, env, (cudaStream_t)stream};
   tac_status s = dbg_enter(S, x, y, nullptr, nullptr, 0.0, exact_hessian);
   Dev& D = b->D;

@@ -44,6 +44,7 @@ struct EnvCtl {
   double min_d2;          // min squared primitive distance over the candidates classified by the last narrow phase
   double mu_used;         // LM shift of the last solve (hessian_mode 2)
   int fault, pad3_;       // test-only fault injection (tac_debug_inject_fault): env status forced at k_control
+  int n_fr, fr_frozen;    // lagged friction pairs of this step (appended after the barrier pairs), frozen at xⁿ
 };
 
 // ---- env-resident cluster PCG (pcg_cluster.cuh): plan built on the host from the soft BSR pattern ----
@@ -98,6 +99,7 @@ struct Dev {
   double K;                 // line-search expansion bound (reading R17b)
   double lm_mu0;
   double bp_margin;         // δ of the reusable candidate list (0 = rebuild every iteration)
+  double mu_f, eps_v;       // lagged friction: μ (0 = off) and ε_v
   double grav[3];
   // ---- template ----
   const int* tets;        // [T][4]
@@ -216,6 +218,14 @@ struct Dev {
   double* out_coat;       // [E][NCOAT][3]
   double* out_mpos;       // [E][NMARK][3]
   double* out_mflow;      // [E][NMARK][3]
+  // lagged friction (reading R20): the active pairs at xⁿ, frozen once per step, appended after the
+  // barrier pairs of every Newton iteration's active list (kind + 2)
+  int* fr_info;           // [E][act_cap][4] (kind, type, a, b) at xⁿ
+  int* fr_vid;            // [E][act_cap][4]
+  int* fr_slot;           // [E][act_cap][4]
+  int* fr_res;            // [E][act_cap]
+  double* fr_xb;          // [E][act_cap][12]
+  double* fr_dat;         // [E][act_cap][16] Δt²μλⁿ | n̂ 3 | Γ weights of slots 1..3 | yⁿ_j = x_j − x_0 (j = 1..3) 9
   int* any_active;        // [1] envs still active after k_control (count)
   int* act_list;          // [2][E] compacted active-env lists (double-buffered by Newton iteration parity)
   const int* elist;       // per launch: env list of this launch (nullptr = env0 + blockIdx)

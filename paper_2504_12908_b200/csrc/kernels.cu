@@ -503,6 +503,129 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
 }
 
 // ------------------------------------------------------------------------------------------
+// lagged friction (reading R20): at the first narrow phase of a step (positions = xⁿ) the
+// barrier's active pairs are frozen as friction pairs — contact normal n̂ and closest-point weights Γ
+// (PT: p − Σβ_i t_i; EE: (1−s)a₀ + s a₁ − (1−t)b₀ − t b₁), λⁿ = κ A_k m_k |b′(d_k)| and the slots'
+// relative positions yⁿ_j = x_j − x_0; every narrow phase of the step appends them after the barrier
+// pairs (kind + 2) so the pair kernels, condensation and SpMV carry them like contact pairs
+// ------------------------------------------------------------------------------------------
+__device__ void closest_weights(int kind, int type, const v3* X, double* g) {
+  g[0] = 1.0; g[1] = 0.0; g[2] = 0.0; g[3] = 0.0;
+  if (kind == 0) {
+    if (type == PT_T) {
+      const v3 e1 = X[2] - X[1], e2 = X[3] - X[1], w = X[0] - X[1];
+      const double a11 = dot(e1, e1), a12 = dot(e1, e2), a22 = dot(e2, e2), b1 = dot(e1, w), b2 = dot(e2, w);
+      const double det = a11 * a22 - a12 * a12;
+      const double be1 = (a22 * b1 - a12 * b2) / det, be2 = (a11 * b2 - a12 * b1) / det;
+      g[1] = -(1.0 - be1 - be2); g[2] = -be1; g[3] = -be2;
+    } else if (type < PT_V0) {
+      const int i = type - PT_E0, j = (i + 1) % 3;
+      const v3 a = X[1 + i], e = X[1 + j] - a;
+      const double t = dot(X[0] - a, e) / dot(e, e);
+      g[1 + i] -= 1.0 - t;
+      g[1 + j] -= t;
+    } else {
+      g[1 + type - PT_V0] = -1.0;
+    }
+    return;
+  }
+  const int ss = type / 3, ts = type % 3;
+  const v3 d1 = X[1] - X[0], d2 = X[3] - X[2], r = X[0] - X[2];
+  double sp, tp;
+  if (ss == 1 && ts == 1) {
+    const double A = dot(d1, d1), B = dot(d1, d2), E = dot(d2, d2), Cc = dot(d1, r), F = dot(d2, r);
+    const double den = A * E - B * B;
+    sp = (B * F - Cc * E) / den;
+    tp = (A * F - B * Cc) / den;
+  } else if (ss == 1) {
+    tp = ts == 0 ? 0.0 : 1.0;
+    sp = dot((ts == 0 ? X[2] : X[3]) - X[0], d1) / dot(d1, d1);
+  } else if (ts == 1) {
+    sp = ss == 0 ? 0.0 : 1.0;
+    tp = dot((ss == 0 ? X[0] : X[1]) - X[2], d2) / dot(d2, d2);
+  } else {
+    sp = ss == 0 ? 0.0 : 1.0;
+    tp = ts == 0 ? 0.0 : 1.0;
+  }
+  g[0] = 1.0 - sp; g[1] = sp; g[2] = -(1.0 - tp); g[3] = -tp;
+}
+
+// block-level (k_narrow): freeze the friction pairs once per step, append them after the nbar barrier
+// pairs; returns the total number of active-list entries
+__device__ int friction_pairs(const Dev& D, int e, int nbar) {
+  EnvCtl& C = D.ctl[e];
+  const size_t ea = (size_t)e * D.act_cap;
+  int* info = D.act_info + ea * 4;
+  int* avid = D.act_vid + ea * 4;
+  int* aslot = D.act_slot + ea * 4;
+  int* ares = D.act_res + ea;
+  double* axb = D.act_xb + ea * 12;
+  if (!C.fr_frozen) {
+    const double* P = D.P + (size_t)e * D.NVall * 3;
+    for (int k = threadIdx.x; k < nbar; k += blockDim.x) {
+      const int4 inf = reinterpret_cast<const int4*>(info)[k];
+      const int4 vv = reinterpret_cast<const int4*>(avid)[k];
+      const v3 X[4] = {ld3(P + 3 * vv.x), ld3(P + 3 * vv.y), ld3(P + 3 * vv.z), ld3(P + 3 * vv.w)};
+      double gw[4];
+      closest_weights(inf.x, inf.y, X, gw);
+      const v3 sep = gw[0] * X[0] + gw[1] * X[1] + gw[2] * X[2] + gw[3] * X[3];
+      const double d = sqrt(dot(sep, sep));
+      const v3 nh = (1.0 / d) * sep;
+      const double dm = d - D.dhat, lg = log(d / D.dhat);
+      const double b1 = -2.0 * dm * lg - dm * dm / d;                 // b′(d)
+      double m = 1.0;
+      if (inf.x == 1 && D.mollify) {
+        const v3 cn = cross(X[1] - X[0], X[3] - X[2]);
+        double m1, m2;
+        mollifier(dot(cn, cn), pair_eps(D, inf.x, inf.z, inf.w), &m, &m1, &m2);
+      }
+      const double lam = D.kappa * pair_area(D, inf.x, inf.z, inf.w) * m * fabs(b1);
+      double* fd = D.fr_dat + (ea + k) * 16;
+      fd[0] = D.dt * D.dt * D.mu_f * lam;
+      fd[1] = nh.x; fd[2] = nh.y; fd[3] = nh.z;
+      fd[4] = gw[1]; fd[5] = gw[2]; fd[6] = gw[3];
+      for (int j = 0; j < 3; ++j) { const v3 y = X[j + 1] - X[0]; fd[7 + 3 * j] = y.x; fd[8 + 3 * j] = y.y; fd[9 + 3 * j] = y.z; }
+      reinterpret_cast<int4*>(D.fr_info + ea * 4)[k] = inf;
+      reinterpret_cast<int4*>(D.fr_vid + ea * 4)[k] = vv;
+      reinterpret_cast<int4*>(D.fr_slot + ea * 4)[k] = reinterpret_cast<const int4*>(aslot)[k];
+      D.fr_res[ea + k] = ares[k];
+      for (int i = 0; i < 12; ++i) D.fr_xb[(ea + k) * 12 + i] = axb[12 * k + i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { C.n_fr = nbar; C.fr_frozen = 1; }
+    __syncthreads();
+  }
+  const int nfr = C.n_fr;
+  const int n = min(nbar + nfr, D.act_cap);
+  for (int k = threadIdx.x; k < n - nbar; k += blockDim.x) {
+    const int pos = nbar + k;
+    int4 inf = reinterpret_cast<const int4*>(D.fr_info + ea * 4)[k];
+    inf.x += 2;
+    reinterpret_cast<int4*>(info)[pos] = inf;
+    reinterpret_cast<int4*>(avid)[pos] = reinterpret_cast<const int4*>(D.fr_vid + ea * 4)[k];
+    reinterpret_cast<int4*>(aslot)[pos] = reinterpret_cast<const int4*>(D.fr_slot + ea * 4)[k];
+    ares[pos] = D.fr_res[ea + k];
+    for (int i = 0; i < 12; ++i) axb[12 * pos + i] = D.fr_xb[(ea + k) * 12 + i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { C.n_act = n; if (nbar + nfr > D.act_cap) C.overflow = 1; }
+  __syncthreads();
+  return n;
+}
+
+// friction energy of one frozen pair at slot positions X: Δt²μλ f0(‖(I − n̂n̂ᵀ) Σ_j Γ_j (y_j − yⁿ_j)‖)
+__device__ __forceinline__ double friction_energy(const double* fd, const v3* X, double eps) {
+  v3 w = mk(0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) w += fd[4 + j] * ((X[j + 1] - X[0]) - ld3(fd + 7 + 3 * j));
+  const v3 nh = ld3(fd + 1);
+  const v3 v = w - dot(nh, w) * nh;
+  const double z = sqrt(dot(v, v));
+  const double f0 = z < eps ? -z * z * z / (3.0 * eps * eps) + z * z / eps + eps / 3.0 : z;
+  return fd[0] * f0;
+}
+
+// ------------------------------------------------------------------------------------------
 // narrow phase: active set 𝒜 = {k ∈ C : s_k < d̂²} (strict) in canonical order, plus
 // deterministic soft-vertex and body contribution lists
 // ------------------------------------------------------------------------------------------
@@ -585,13 +708,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
     }
     total += tot;
   }
-  const int nact = min(total, D.act_cap);
+  int nact = min(total, D.act_cap);
   {
     __shared__ double redm[32];
     mind2 = block_min(mind2, redm);
   }
   if (threadIdx.x == 0) { C.n_act = nact; C.min_d2 = mind2; if (total > D.act_cap) C.overflow = 1; }
   __syncthreads();
+  if (D.mu_f > 0.0) nact = friction_pairs(D, e, nact);
   // residual pairs (kept matrix-free in the SpMV), ascending
   {
     const int* ares = D.act_res + (size_t)e * D.act_cap;
@@ -1196,7 +1320,39 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
       }
     };
     if (live) {
-    {
+    if (reinterpret_cast<const int4*>(info)[k].x >= 2) {
+      // lagged friction pair (reading R20): φ(w) = Δt²μλ f0(‖P_T w‖), w = Σ_j Γ_j (y_j − yⁿ_j); in
+      // y-space G_y[j] = Γ_j ∇φ, H_y[j][l] = Γ_j Γ_l ∇²φ with ∇φ = (f1(z)/z) P_T w and
+      // ∇²φ = (f1(z)/z) P_T + (f1′(z) − f1(z)/z) ûûᵀ (PSD for the paper's f1; z = ‖P_T w‖, û = P_T w / z)
+      const int4 vv = reinterpret_cast<const int4*>(avid)[k];
+      const v3 X[4] = {ld3(P + 3 * vv.x), ld3(P + 3 * vv.y), ld3(P + 3 * vv.z), ld3(P + 3 * vv.w)};
+      const double* fd = D.fr_dat + ((size_t)e * D.act_cap + (k - (C.n_act - C.n_fr))) * 16;
+      const double eps = D.eps_v * D.dt;
+      v3 w = mk(0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) w += fd[4 + j] * ((X[j + 1] - X[0]) - ld3(fd + 7 + 3 * j));
+      const v3 nh = ld3(fd + 1);
+      const v3 vt = w - dot(nh, w) * nh;
+      const double z2 = dot(vt, vt), z = sqrt(z2), sc = fd[0];
+      double a, bq;                                    // ∇²φ = sc (a P_T + bq v vᵀ)
+      if (z < eps) { a = -z / (eps * eps) + 2.0 / eps; bq = z > 0.0 ? -1.0 / (eps * eps * z) : 0.0; }
+      else { a = 1.0 / z; bq = -1.0 / (z * z2); }
+      const double V3[3] = {vt.x, vt.y, vt.z}, N3[3] = {nh.x, nh.y, nh.z};
+      double Hw[9];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Hw[3 * r + c] = sc * (a * ((r == c ? 1.0 : 0.0) - N3[r] * N3[c]) + bq * V3[r] * V3[c]);
+      const double gam[3] = {fd[4], fd[5], fd[6]};
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) Gy[3 * j + r] = gam[j] * sc * a * V3[r];
+#pragma unroll
+      for (int r = 0; r < 9; ++r)
+#pragma unroll
+        for (int c = r; c < 9; ++c) sHy[s9(r, c)][tx] = gam[r / 3] * gam[c / 3] * Hw[3 * (r % 3) + (c % 3)];
+    } else {
       const int4 inf = reinterpret_cast<const int4*>(info)[k];
       const int kind = inf.x, type = inf.y, pa = inf.z, pb = inf.w;
       const int4 vv = reinterpret_cast<const int4*>(avid)[k];
@@ -1410,7 +1566,7 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
         int jb = -1;
         if (!res) {        // non-residual: all soft slots on one primitive → template block table
           const int4 inf = reinterpret_cast<const int4*>(info)[k];
-          if (inf.x == 0) {
+          if ((inf.x & 1) == 0) {
             const int i = s - 1, j = t - 1;
             jb = D.tri_blk[6 * (size_t)inf.w + 2 * i + (j < i ? j : j - 1)];
           } else {
@@ -2551,17 +2707,18 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_ccd(Dev D, int env0, int force)
 // energy at q + α p (line search): six deterministic block sums
 // ------------------------------------------------------------------------------------------
 // six deterministic block sums in one pass (2 barriers): per-warp partials → red6[6][32] → warp sums
-__device__ __forceinline__ void block_sum6(double* v, double* red6) {
+constexpr int NTERMS = 7;                 // inertia, elastic, ortho, gravity, barrier, AL, friction
+__device__ __forceinline__ void block_sum_terms(double* v, double* red) {   // red: [NTERMS][32]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
-  for (int i = 0; i < 6; ++i) v[i] = warp_sum(v[i]);
+  for (int i = 0; i < NTERMS; ++i) v[i] = warp_sum(v[i]);
   __syncthreads();
   if (lane == 0)
 #pragma unroll
-    for (int i = 0; i < 6; ++i) red6[32 * i + wid] = v[i];
+    for (int i = 0; i < NTERMS; ++i) red[32 * i + wid] = v[i];
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < 6; ++i) v[i] = warp_sum(lane < nw ? red6[32 * i + lane] : 0.0);
+  for (int i = 0; i < NTERMS; ++i) v[i] = warp_sum(lane < nw ? red[32 * i + lane] : 0.0);
 }
 
 // Energy terms at q + αp.  lmode 0: barrier over every candidate of C′; 1: the same, and build the
@@ -2694,23 +2851,39 @@ __device__ void energy_terms(const Dev& D, int e, double alpha, double* red, dou
     }
   }
   if (lmode == 1 && threadIdx.x == 0) *nls = run;
-  double v6[6] = {ein, eel, eor, egr, eba, eal};
-  block_sum6(v6, red);
-  for (int i = 0; i < 6; ++i) terms[i] = v6[i];
+  // lagged friction pairs at the trial positions (reading R20)
+  double efr = 0.0;
+  if (D.mu_f > 0.0) {
+    const int nfr = C.n_fr, nb = C.n_act - C.n_fr;
+    const int* fv = D.fr_vid + (size_t)e * D.act_cap * 4;
+    const double aK = alpha == 0.0 ? 0.0 : alpha / C.Keff;
+    const double eps = D.eps_v * D.dt;
+    for (int k = threadIdx.x; k < nfr; k += blockDim.x) {
+      const int4 vv = reinterpret_cast<const int4*>(fv)[k];
+      const int ids[4] = {vv.x, vv.y, vv.z, vv.w};
+      v3 X[4];
+      for (int s2 = 0; s2 < 4; ++s2) X[s2] = ld3(P + 3 * ids[s2]) + aK * ld3(Pd + 3 * ids[s2]);
+      efr += friction_energy(D.fr_dat + ((size_t)e * D.act_cap + k) * 16, X, eps);
+    }
+    (void)nb;
+  }
+  double v7[NTERMS] = {ein, eel, eor, egr, eba, eal, efr};
+  block_sum_terms(v7, red);
+  for (int i = 0; i < NTERMS; ++i) terms[i] = v7[i];
   *inverted = __syncthreads_or(inv);
 }
 
 __global__ void __launch_bounds__(NTHREADS, 2) k_energy(Dev D, int env0, double alpha) {
   const int e = env_at(D, env0, blockIdx.x);
-  __shared__ double red[6 * 32];
-  double t[6];
+  __shared__ double red[NTERMS * 32];
+  double t[NTERMS];
   int inv;
   energy_terms(D, e, alpha, red, t, &inv);
   if (threadIdx.x == 0) {
     double* out = D.eterm + (size_t)e * 8;
-    for (int i = 0; i < 6; ++i) out[i] = t[i];
+    for (int i = 0; i < NTERMS; ++i) out[i] = t[i];
     out[1] = inv ? 1.0 / 0.0 : out[1];
-    out[6] = inv;
+    out[7] = inv;
   }
 }
 
@@ -2719,14 +2892,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
   const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail) return;
-  __shared__ double red[6 * 32];
+  __shared__ double red[NTERMS * 32];
   __shared__ int sh[33], nls;
   int* lsl = D.lsl + (size_t)e * D.cand_cap;
-  double t[6];
+  double t[NTERMS];
   int inv;
   energy_terms(D, e, 0.0, red, t, &inv, 1, lsl, &nls, sh);
   __syncthreads();
-  const double E0 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
+  const double E0 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5] + t[6];
   const double alpha_max = C.Keff * C.alpha_ccd;  // ACCD bound along K_eff·p, in units of p
   double alpha = fmin(1.0, alpha_max);
   const double gp = C.gp;
@@ -2736,7 +2909,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
   while (true) {
     energy_terms(D, e, alpha, red, t, &inv, 2, lsl, &nls);
     if (!inv) {
-      E1 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
+      E1 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5] + t[6];
       if (E1 <= E0 + D.armijo * alpha * gp) { ok = true; break; }
     }
     alpha *= 0.5;
@@ -2749,7 +2922,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
     while (2.0 * alpha <= alpha_max) {
       energy_terms(D, e, 2.0 * alpha, red, t, &inv, 2, lsl, &nls);
       if (inv) break;
-      const double E2 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
+      const double E2 = t[0] + t[1] + t[2] + t[3] + t[4] + t[5] + t[6];
       if (!(E2 < E1) || !(E2 <= E0 + D.armijo * 2.0 * alpha * gp)) break;
       alpha *= 2.0;
       E1 = E2;
@@ -2881,6 +3054,7 @@ __device__ void begin_env(const Dev& D, int e, const double* yk) {
     C.al_rounds = 0; C.n_act = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;  // (ncand: reusable list)
     C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
     C.exact = D.hmode >= 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0; C.Keff = 1.0; C.mu = 0.0;
+    C.n_fr = 0; C.fr_frozen = 0;
   }
   __syncthreads();
 }

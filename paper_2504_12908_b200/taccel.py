@@ -57,7 +57,8 @@ class Config(ctypes.Structure):
                 ("max_accd_iters", ctypes.c_int32), ("ee_mollifier", ctypes.c_int32),
                 ("hessian_mode", ctypes.c_int32), ("ls_expand", ctypes.c_int32),
                 ("hold_cap", ctypes.c_int32), ("lm_mu0", ctypes.c_double), ("bp_margin", ctypes.c_double),
-                ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32)]
+                ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32),
+                ("mu_friction", ctypes.c_double), ("eps_v", ctypes.c_double)]
 
 
 class EnvStats(ctypes.Structure):
@@ -67,7 +68,7 @@ class EnvStats(ctypes.Structure):
                 ("constraint_residual", ctypes.c_double), ("pcg_iters_total", ctypes.c_int64),
                 ("pcg_alg_bytes_total", ctypes.c_double), ("diag", ctypes.c_double * 4),
                 ("min_dist", ctypes.c_double), ("n_residual", ctypes.c_int32), ("n_couplings", ctypes.c_int32),
-                ("lm_mu", ctypes.c_double)]
+                ("lm_mu", ctypes.c_double), ("n_friction", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 def header_symbols():
@@ -334,7 +335,7 @@ class Batch:
     # ---- parity hooks (host numpy) ------------------------------------------------------------
     def debug_eval(self, env, x, y, lam_att=None, lam_kin=None, rho=0.0, v=None, exact=False):
         x, y = _f64(x), _f64(y)
-        et = np.zeros(6)
+        et = np.zeros(7)
         g = np.zeros(self.n_dof)
         hv = np.zeros(self.n_dof) if v is not None else None
         _check(self.lib.tac_debug_eval(self.handle, env, _ptr(x), _ptr(y),

@@ -296,3 +296,109 @@ def test_cluster_pcg_split_over_ctas(nc):
                        env=env, capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+# ------------------------------------------------------------------------------------------ friction
+
+def _with_friction(sc, mu=0.5):
+    sc.config = dataclasses.replace(sc.config, mu_friction=mu, eps_v=1e-3)
+    return sc
+
+
+@pytest.mark.parametrize("name,slide", [("C1", 0.0), ("C1", 3e-6), ("P1", 2e-5), ("P2", 1e-6)])
+def test_friction_energy_gradient_hvp_parity(name, slide):
+    """Lagged friction D_k (reading R20) through the C ABI: the seven energy terms (friction
+    included), the gradient and the (exact, PSD) Hessian-vector product at an iterate slid away from
+    xⁿ match the oracle within 1e-9; the friction pairs are frozen at the env's state xⁿ on both sides."""
+    sc = _with_friction(S.make_scene(name))
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=1)
+    xn, yn = ei.x0[0].copy(), ei.y0[0].copy()
+    if name == "C1":
+        yn[1, 2] -= 0.2e-3 - 0.04e-3                      # cube 40 µm above the pad: PT and EE pairs
+    rng = np.random.default_rng(21)
+    x = xn + rng.normal(size=xn.shape) * slide
+    if name == "P1":
+        x[0] += slide * np.array([0.6, 0.8, 0.0])       # apex slides past the dynamic plateau
+    y = yn.copy()
+    yk = ei.ykin[0, 0] if ei.ykin.shape[2] else np.zeros((0, 12))
+    if name == "C1":
+        y[1, :3] += np.array([2e-6, -1e-6, -5e-6])        # the kinematic cube's iterate moves too
+    ctx = En.make_context(mod, xn, np.zeros_like(xn), yn, np.zeros_like(yn), yk, sc.config.dt)
+    assert len(ctx.fric) > 0
+    b = T.Batch(sc, 1)
+    assert b.set_state(xn[None], yn[None])[0] == 0
+    if ei.ykin.shape[2]:
+        b.set_targets(ei.ykin[0])
+    pairs = C.active_pairs(mod, M.all_positions(mod, x, y))
+    v = rng.normal(size=mod.n_dof)
+    et, g, hv = b.debug_eval(0, x, y, ctx.lam_att, ctx.lam_kin, ctx.rho, v, exact=True)
+    terms = En.energy_terms(mod, ctx, x, y, pairs)
+    assert terms["friction"] > 0
+    for i, k in enumerate(En.TERMS):
+        assert abs(et[i] - terms[k]) <= REL * max(abs(terms[k]), 1e-300) + 1e-300, (k, et[i], terms[k])
+    go, H = En.assemble(mod, ctx, x, y, pairs, project=False)
+    assert rel_inf(g, go) <= REL
+    assert rel_inf(hv, H @ v) <= REL
+
+
+@pytest.mark.parametrize("name,n_steps", [("C1", 10)])
+def test_friction_trajectory_parity(name, n_steps):
+    """C1 with μ = 0.5: 10 steps through tac_step against the oracle (positions within 1e-6·L_env)."""
+    sc = _with_friction(S.make_scene(name))
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=n_steps)
+    b = T.Batch(sc, 1)
+    assert b.set_state(ei.x0, ei.y0)[0] == 0
+    st = SO.State(ei.x0[0].copy(), np.zeros_like(ei.x0[0]), ei.y0[0].copy(), np.zeros_like(ei.y0[0]))
+    L = M.env_scale(mod, st.x, st.y)
+    nfr = 0
+    for k in range(n_steps):
+        b.set_targets(ei.ykin[k])
+        assert b.step(1)[0] == 0
+        st, stats = SO.step(mod, st, ei.ykin[k, 0], L_env=L)
+        assert stats.status == 0
+        x, _, y, _ = (t.cpu().numpy()[0] for t in b.get_state())
+        err = np.abs(M.all_positions(mod, x, y) - M.all_positions(mod, st.x, st.y)).max() / L
+        assert err <= 1e-6, (k, err)
+        nfr = max(nfr, b.stats()[0]["n_friction"])
+    assert nfr > 0
+
+
+def _incline_scene(mu, tan_theta):
+    import math
+    th = math.atan(tan_theta)
+    pV, pT = S.box_surface((0.04, 0.04, 0.01))
+    cV, cT = S.box_surface((0.01, 0.01, 0.01))
+    g = 9.81 * np.array([math.sin(th), 0.0, -math.cos(th)])
+    cfg = dataclasses.replace(S.Config(dt=0.01), mu_friction=mu, eps_v=1e-3)
+    sc = S.Scene("C1", [], [S.AffineBody(pV, pT, kind=S.STATIC), S.AffineBody(cV, cT, kind=S.DYNAMIC)], g, cfg, n_steps=1)
+    y0 = np.array([S.pose([0, 0, -0.005]), S.pose([0.0013, 0.0007, 0.005 + 0.5e-4], S.rot_z(0.3))])
+    return sc, y0
+
+
+@pytest.mark.parametrize("mu", [0.2, 0.5])
+def test_friction_incline_stick_slip_matches_oracle(mu):
+    """The incline pin on the GPU: a cube on a plane tilted to tan θ = 0.9μ sticks and at
+    1.1μ slides with growing per-step displacement; both trajectories match the oracle step by step."""
+    eps_dt = 1e-3 * 0.01
+    for t, stick in ((0.9 * mu, True), (1.1 * mu, False)):
+        sc, y0 = _incline_scene(mu, t)
+        mod = M.prepare(sc)
+        b = T.Batch(sc, 1)
+        assert b.set_state(np.zeros((1, 0, 3)), y0[None])[0] == 0
+        st = SO.State(np.zeros((0, 3)), np.zeros((0, 3)), y0.copy(), np.zeros_like(y0))
+        L = M.env_scale(mod, st.x, st.y)
+        xs = []
+        for k in range(12):
+            assert b.step(1)[0] == 0
+            st, stats = SO.step(mod, st, np.zeros((0, 12)), L_env=L)
+            y = b.get_state()[2].cpu().numpy()[0]
+            err = np.abs(M.all_positions(mod, np.zeros((0, 3)), y) - M.all_positions(mod, np.zeros((0, 3)), st.y)).max() / L
+            assert err <= 1e-6, (mu, t, k, err)
+            xs.append(y[1, 0])
+        dx = np.diff(np.array(xs))[4:]
+        if stick:
+            assert np.all(np.abs(dx) < 10 * eps_dt), dx
+        else:
+            assert np.all(dx > 0) and np.all(np.diff(dx) > 0), dx
