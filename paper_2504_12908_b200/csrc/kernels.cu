@@ -3386,8 +3386,11 @@ static PcgPlan pcg_plan(const Dev& D) {
   const int lpr = (lpr_env == 2 || lpr_env == 4) ? lpr_env : 1;
   const int thr = (thr_env >= 128 && thr_env <= PCG_R_THREADS && thr_env % 32 == 0) ? thr_env : pcg_r_threads(D.V);
   const size_t rb = pcg_r_bytes(D, thr);
-  if (resident && cluster_env != 0 && D.cl.nc > 0 && cl_fits(D)) return PcgPlan{PCG_CLUSTER, D.cl.threads, D.cl.smem, 1};
-  if (resident) {
+  // preference: the single-CTA env-resident k_pcg_r (measured faster than k_pcg_cl with one CTA on C2:
+  // 229 vs 285 ms / 10 steps), then the cluster-resident k_pcg_cl for envs that do not fit one SM
+  // (TAC_PCG_CLUSTER=n forces the cluster kernel with n CTAs per env), then the streamed k_pcg
+  const bool force_cl = cluster_env > 0;
+  if (resident && !force_cl) {
     const bool use512 = thr > 384 || lb512;
     cudaFuncAttributes fa;
     int optin = 0;
@@ -3397,6 +3400,7 @@ static PcgPlan pcg_plan(const Dev& D) {
       return PcgPlan{use512 ? PCG_RESIDENT512 : PCG_RESIDENT, thr, rb, lpr};
     cudaGetLastError();
   }
+  if (resident && cluster_env != 0 && D.cl.nc > 0 && cl_fits(D)) return PcgPlan{PCG_CLUSTER, D.cl.threads, D.cl.smem, 1};
   const size_t with_vec = spmv_smem(D) + (size_t)5 * D.n * sizeof(double);
   const int vsm = with_vec <= 200 * 1024 ? 1 : 0;
   return PcgPlan{vsm ? PCG_STREAM_VSM : PCG_STREAM, NTHREADS, vsm ? with_vec : spmv_smem(D), lpr};

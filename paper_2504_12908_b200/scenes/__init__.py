@@ -12,6 +12,13 @@ Workloads follow SURVEY.md §8(d) (the configs of BASELINE.json):
   C1c  soft cube resting on a static plate (statics variant)
   C2   peg insertion, dual low-res pads (8x6x3 lattice), 1024 envs
   C3   as C2 with high-res pads (19x16x5 lattice), 4096 envs
+  C4   parallel-gripper grasp: two 40x40x4 mm pads (14x14x3) squeeze one of 8 procedural star-shaped
+       objects (perturbed level-3 icospheres, 642 v / 1280 t) resting on a static table; "C4:k" = shape k
+       (homogeneous batch per shape, 256 envs each, 2048 envs in total)
+  C5   Allegro-like hand: palm + 4 fingers x 4 kinematic link boxes (17 kinematic bodies), four 24x24x3 mm
+       fingertip pads (9x9x4) in a four-sided precision grasp of a dynamic 16x30x22 mm tile whose two 30x22
+       faces carry a seeded 0.3 mm engraving (48x36 cells), on a static table; link targets from the
+       forward kinematics of a 16-joint script (fk_hand)
   P1   single point-triangle pair: a tet's lowest vertex d̂/2 above a static box (barrier pins)
   P2   single edge-edge pair: two tets' edges crossing at gap d̂/2 (perpendicular; P2m: nearly
        parallel, inside the mollifier range) — also the soft–soft (matrix-free) contact case
@@ -30,7 +37,7 @@ from typing import List, Optional
 import numpy as np
 
 DYNAMIC, KINEMATIC, STATIC = 0, 1, 2
-CFG_INDEX = {"C1": 1, "C1b": 11, "C1c": 12, "C2": 2, "C3": 3, "P1": 21, "P2": 22, "P2m": 23}
+CFG_INDEX = {"C1": 1, "C1b": 11, "C1c": 12, "C2": 2, "C3": 3, "C4": 4, "C5": 5, "P1": 21, "P2": 22, "P2m": 23}
 SEED_BASE = 250412908
 
 
@@ -338,7 +345,200 @@ def scene_pair(name: str) -> Scene:
     raise ValueError(name)
 
 
+def icosphere(level: int):
+    """Unit icosphere: icosahedron subdivided `level` times, vertices projected to the sphere;
+    outward-oriented triangles (level 3: 642 vertices / 1280 triangles)."""
+    t = (1.0 + math.sqrt(5.0)) / 2.0
+    V = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+         (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    V = [np.array(v, np.float64) / np.linalg.norm(v) for v in V]
+    F = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6),
+         (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7),
+         (9, 8, 1)]
+    for _ in range(level):
+        mid = {}
+
+        def m(a, b):
+            key = (min(a, b), max(a, b))
+            if key not in mid:
+                v = V[a] + V[b]
+                V.append(v / np.linalg.norm(v))
+                mid[key] = len(V) - 1
+            return mid[key]
+        F = [f for (a, b, c) in F for f in ((a, m(a, b), m(c, a)), (b, m(b, c), m(a, b)), (c, m(c, a), m(b, c)),
+                                            (m(a, b), m(b, c), m(c, a)))]
+    return np.array(V), np.array(F, np.int32)
+
+
+def star_object(shape: int):
+    """C4 object `shape` (0..7): a level-3 icosphere with radius R ~ U[20, 30] mm and a seeded low-order
+    radial perturbation r(u) = R (1 + 0.15 h(u)), h a sum of quadratic/cubic ridge functions of u
+    normalised to max |h| = 1 (star-shaped, smooth)."""
+    rng = np.random.Generator(np.random.Philox(key=(SEED_BASE + CFG_INDEX["C4"]) * (1 << 32) + 1_000_000 + shape))
+    U, F = icosphere(3)
+    R = rng.uniform(20.0, 30.0) * MM
+    h = np.zeros(len(U))
+    for k in range(6):
+        a = rng.normal(size=3)
+        a /= np.linalg.norm(a)
+        h += rng.uniform(-1, 1) * (U @ a) ** (2 + k % 2)
+    h /= np.abs(h).max()
+    return U * (R * (1.0 + 0.15 * h))[:, None], F
+
+
+def scene_C4(shape: int = 0):
+    """C4: parallel gripper — two 40x40x4 mm pads (14x14x3 lattice) on kinematic finger
+    boxes (6x44x44 mm) squeeze star object `shape` (dynamic) standing on a static 200x200x20 mm table
+    (top face at z = 0).  dt = 0.02 s."""
+    cfg = Config(dt=0.02)
+    tV, tT = box_surface((200 * MM, 200 * MM, 20 * MM), spacing=25 * MM)
+    table = AffineBody(tV, tT, kind=STATIC)
+    oV, oT = star_object(shape)
+    obj = AffineBody(oV, oT, kind=DYNAMIC)
+    fV, fT = box_surface((6 * MM, 44 * MM, 44 * MM))
+    R_l = np.array([[0.0, 0.0, 1.0], [0.0, 1.0, 0.0], [-1.0, 0.0, 0.0]])
+    R_r = np.array([[0.0, 0.0, -1.0], [0.0, 1.0, 0.0], [1.0, 0.0, 0.0]])
+    pad_l = make_pad(14, 14, 3, (40 * MM, 40 * MM, 4 * MM), mount_body=2, mount_T=pose([3 * MM, 0, 0], R_l))
+    pad_r = make_pad(14, 14, 3, (40 * MM, 40 * MM, 4 * MM), mount_body=3, mount_T=pose([-3 * MM, 0, 0], R_r))
+    return Scene(f"C4:{shape}", [pad_l, pad_r],
+                 [table, obj, AffineBody(fV, fT, kind=KINEMATIC), AffineBody(fV.copy(), fT.copy(), kind=KINEMATIC)],
+                 np.array([0, 0, -9.81]), cfg, n_steps=200)
+
+
+# ---- C5: Allegro-like hand ------------------------------------------------------------------------
+HAND_L = (20 * MM, 25 * MM, 20 * MM, 24 * MM)          # link lengths: proximal, 2 middle links, distal
+HAND_FINGERS = ("thumb", "index", "middle", "ring")
+HAND_APPROACH = {"thumb": (1.0, 0.0), "index": (-1.0, 0.0), "middle": (0.0, -1.0), "ring": (0.0, 1.0)}
+TILE = (16 * MM, 30 * MM, 22 * MM)                     # x (between the engraved faces), y, z
+
+
+def engraved_tile(seed_shape: int = 0):
+    """The C5 tile: a 16x30x22 mm box whose two x-faces (30x22 mm) carry a seeded 0.3 mm-deep engraving
+    on a 48x36 cell grid (random rectangles and a ring), as a watertight cell-union surface."""
+    rng = np.random.Generator(np.random.Philox(key=(SEED_BASE + CFG_INDEX["C5"]) * (1 << 32) + 2_000_000 + seed_shape))
+    hx, hy, hz = TILE[0] / 2, TILE[1] / 2, TILE[2] / 2
+    d = 0.3 * MM
+    xl = np.array([-hx, -hx + d, hx - d, hx])
+    yl = np.linspace(-hy, hy, 49)
+    zl = np.linspace(-hz, hz, 37)
+    solid = np.ones((3, 48, 36), bool)
+    yc, zc = (yl[:-1] + yl[1:]) / 2, (zl[:-1] + zl[1:]) / 2
+    for side in (0, 2):
+        eng = np.zeros((48, 36), bool)
+        for _ in range(6):                              # random grooves/pockets, away from the rim
+            j0, k0 = rng.integers(2, 40), rng.integers(2, 28)
+            eng[j0:j0 + rng.integers(2, 7), k0:k0 + rng.integers(2, 7)] = True
+        r = np.hypot(yc[:, None] - rng.uniform(-5, 5) * MM, zc[None, :] - rng.uniform(-3, 3) * MM)
+        eng |= (r > 4.0 * MM) & (r < 5.2 * MM)         # a ring
+        eng[:2, :] = eng[-2:, :] = False
+        eng[:, :2] = eng[:, -2:] = False
+        solid[side] = ~eng
+    return cell_union_surface(xl, yl, zl, solid)
+
+
+def _rx(t):
+    c, s = math.cos(t), math.sin(t)
+    return np.array([[1.0, 0, 0], [0, c, -s], [0, s, c]])
+
+
+def hand_base_frames():
+    """Per finger: the base frame of its chain in the palm frame (x = approach direction toward the
+    tile, z = up), placed so that with zero joint angles the distal link hangs straight down with its
+    pad's coated face 0.2 mm from the tile face, the pad centre level with the tile centre."""
+    L0, L1, L2, L3 = HAND_L
+    out = {}
+    for f in HAND_FINGERS:
+        ax, ay = HAND_APPROACH[f]
+        R = np.array([[ax, -ay, 0.0], [ay, ax, 0.0], [0.0, 0.0, 1.0]])      # columns: x_l = a, y_l, z_l = up
+        face = TILE[0] / 2 if ay == 0 else TILE[1] / 2
+        dist = face + 0.2 * MM + 3 * MM + 4 * MM        # tile face, gap, pad thickness, half the distal link
+        c_distal = -dist * np.array([ax, ay, 0.0])      # palm frame origin above the tile centre
+        base = c_distal + np.array([0, 0, L0 + L1 + L2 + L3 / 2])
+        out[f] = (base, R)
+    return out
+
+
+def fk_hand(y_palm, q):
+    """Forward kinematics (homogeneous products) of the 4 fingers: q (4, 4) joint angles per finger
+    (abduction about the base's z, then three flexions about the local y; positive flexion moves the
+    finger tip toward the tile).  Returns the 16 link body poses (12-vectors, world), finger-major:
+    proximal, middle, middle-2, distal; each link's body frame is the centre of its segment."""
+    L = HAND_L
+    out = []
+    for fi, f in enumerate(HAND_FINGERS):
+        base, Rb = hand_base_frames()[f]
+        T = compose(y_palm, pose(base, Rb))
+        T = compose(T, pose([0, 0, 0], rot_z(q[fi, 0])))
+        for j in range(4):
+            if j > 0:
+                T = compose(T, pose([0, 0, -L[j - 1]], rot_y(-q[fi, j])))
+            out.append(compose(T, pose([0, 0, -L[j] / 2])))
+    return np.stack(out)
+
+
+def scene_C5():
+    """C5: Allegro-like hand — palm (60x60x15 mm) and 4 fingers of 4 kinematic link boxes,
+    four fingertip pads (24x24x3 mm, 9x9x4 lattice) on the distal links' inner faces, a dynamic engraved
+    tile (16x30x22 mm) standing on a static table.  Bodies: table, tile, palm, 16 links.  dt = 0.02 s."""
+    cfg = Config(dt=0.02)
+    tV, tT = box_surface((200 * MM, 200 * MM, 20 * MM), spacing=25 * MM)
+    tileV, tileT = engraved_tile()
+    pV, pT = box_surface((60 * MM, 60 * MM, 15 * MM))
+    bodies = [AffineBody(tV, tT, kind=STATIC), AffineBody(tileV, tileT, kind=DYNAMIC), AffineBody(pV, pT, kind=KINEMATIC)]
+    L = HAND_L
+    pads = []
+    R_pad = np.array([[0.0, 0.0, 1.0], [0.0, 1.0, 0.0], [-1.0, 0.0, 0.0]])   # pad z → link x (toward the tile)
+    for fi, f in enumerate(HAND_FINGERS):
+        for j in range(4):
+            size = (8 * MM, 24 * MM, L[j]) if j == 3 else (8 * MM, 12 * MM, L[j] - 1 * MM)
+            V, T = box_surface(size)
+            bodies.append(AffineBody(V, T, kind=KINEMATIC))
+        pads.append(make_pad(9, 9, 4, (24 * MM, 24 * MM, 3 * MM), mount_body=3 + 4 * fi + 3,
+                             mount_T=pose([4 * MM, 0, 0], R_pad)))
+    return Scene("C5", pads, bodies, np.array([0, 0, -9.81]), cfg, n_steps=200)
+
+
+def hand_palm_pose():
+    L0, L1, L2, L3 = HAND_L
+    return pose([0, 0, TILE[2] / 2 + 0.08 * MM + L3 / 2 + L2 + L1 + L0 + 7.5 * MM])
+
+
+def hand_script(env_id: int, n_steps: int):
+    """C5 joint script (16 joints): steps 0-79 each finger closes its pad onto the tile by τ_d ~ U[0.5, 1.5]
+    mm (per pad) with the parallelogram flexion q1 = a, q2 = −a, q3 = 0 (the tip translates by L1 sin a,
+    the pad stays parallel to the face); steps 80-199 the abduction joints oscillate ±2° together."""
+    rng = env_rng("C5", env_id)
+    tau = rng.uniform(0.5, 1.5, 4) * MM
+    L1 = HAND_L[1]
+    qs = []
+    for k in range(n_steps):
+        q = np.zeros((4, 4))
+        for fi in range(4):
+            reach = (0.2 * MM + tau[fi]) * min(k + 1, 80) / 80.0
+            a = math.asin(reach / L1)
+            q[fi, 1], q[fi, 2] = a, -a
+            if k >= 80:
+                q[fi, 0] = math.radians(2.0) * math.sin(2 * math.pi * (k + 1 - 80) / 120.0)
+        qs.append(q)
+    return np.stack(qs)
+
+
+def _c5_env(scene, env_id, n_steps):
+    y_palm = hand_palm_pose()
+    y_table = pose([0, 0, -10 * MM])
+    y_tile = pose([0, 0, TILE[2] / 2 + 0.08 * MM])
+    links0 = fk_hand(y_palm, np.zeros((4, 4)))
+    y0 = np.concatenate([np.stack([y_table, y_tile, y_palm]), links0])
+    qs = hand_script(env_id, n_steps)
+    tk = np.stack([np.concatenate([y_palm[None], fk_hand(y_palm, q)]) for q in qs])
+    return y0, tk
+
+
 def make_scene(name: str) -> Scene:
+    if name == "C5":
+        return scene_C5()
+    if name == "C4" or name.startswith("C4:"):
+        return scene_C4(int(name.split(":")[1]) if ":" in name else 0)
     if name in ("P1", "P2", "P2m"):
         return scene_pair(name)
     if name in ("C1", "C1b", "C1c"):
@@ -355,7 +555,7 @@ def make_scene(name: str) -> Scene:
 # ----------------------------------------------------------------------------------------------
 
 def env_rng(name: str, env_id: int) -> np.random.Generator:
-    key = (SEED_BASE + CFG_INDEX[name]) * (1 << 32) + int(env_id)
+    key = (SEED_BASE + CFG_INDEX[name.split(":")[0]]) * (1 << 32) + int(env_id)
     return np.random.Generator(np.random.Philox(key=key))
 
 
@@ -441,6 +641,38 @@ def _c2_env(scene, env_id, n_steps):
     return y0, np.stack(tk)
 
 
+def _c4_env(scene, env_id, n_steps):
+    """C4 per-env script: gripper yaw θ ~ U[0, 2π) about the object's vertical axis, press τ_d ~ U[0.5, 1.5]
+    mm, wiggle amplitude A_x ~ U[0.5, 1.5] mm.  Steps 0-59 close from a 0.2 mm gap to τ_d; steps 60-199 the
+    closed gripper oscillates along its squeeze axis, x = A_x sin(2π·2(k−60)/140)."""
+    rng = env_rng(scene.name, env_id)
+    th = rng.uniform(0.0, 2.0 * math.pi)
+    tau_d = rng.uniform(0.5, 1.5) * MM
+    A_x = rng.uniform(0.5, 1.5) * MM
+    oV = scene.affine[1].rest_pos
+    zc = -oV[:, 2].min() + 0.08 * MM                        # object's lowest vertex 0.08 mm above the table
+    R = rot_z(th)
+    dirv = R @ np.array([1.0, 0.0, 0.0])
+    s_pos, s_neg = (oV @ dirv).max(), (-(oV @ dirv)).max()    # support distances along ±squeeze axis
+    pad_th, gap0, half = 4 * MM, 0.2 * MM, 3 * MM
+    y_table = pose([0, 0, -10 * MM])
+    y_obj = pose([0, 0, zc])
+    c = np.array([0.0, 0.0, zc])
+    fl = -(s_neg + gap0 + pad_th + half)
+    fr = s_pos + gap0 + pad_th + half
+    y0 = np.stack([y_table, y_obj, pose(c + R @ np.array([fl, 0, 0]), R), pose(c + R @ np.array([fr, 0, 0]), R)])
+    close = 60
+    tk = []
+    for k in range(n_steps):
+        if k < close:
+            sq, ox = (gap0 + tau_d) * (k + 1) / close, 0.0
+        else:
+            sq, ox = gap0 + tau_d, A_x * math.sin(2 * math.pi * 2 * (k + 1 - close) / 140.0)
+        cc = c + R @ np.array([ox, 0.0, 0.0])
+        tk.append(np.stack([pose(cc + R @ np.array([fl + sq, 0, 0]), R), pose(cc + R @ np.array([fr - sq, 0, 0]), R)]))
+    return y0, np.stack(tk)
+
+
 def env_inputs(scene: Scene, env_ids, n_steps: Optional[int] = None) -> EnvInputs:
     """Initial states (zero velocities) and per-step kinematic targets for the given global
     env ids.  Deterministic per env id."""
@@ -452,6 +684,10 @@ def env_inputs(scene: Scene, env_ids, n_steps: Optional[int] = None) -> EnvInput
             y0, tk = y0, np.zeros((n_steps, 0, 12))
         elif scene.name.startswith("C1"):
             y0, tk = _c1_env(scene, int(e), n_steps)
+        elif scene.name.startswith("C4"):
+            y0, tk = _c4_env(scene, int(e), n_steps)
+        elif scene.name == "C5":
+            y0, tk = _c5_env(scene, int(e), n_steps)
         else:
             y0, tk = _c2_env(scene, int(e), n_steps)
         ys.append(y0)
