@@ -39,6 +39,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "peg-insertion env-steps/s and ×real-time, dual sensors, at 1/2/4/8 B200"
 WORKLOADS = {
+    "C4": "C4: parallel-gripper grasp, dual 40x40x4 mm pads (14x14x3 lattice, 588 nodes/1690 tets each), 8 procedural "
+          "star-shaped objects (perturbed level-3 icospheres, 642 v/1280 t; 256 envs per shape, one batch each), "
+          "2 kinematic fingers + static table, dt=0.02 s",
+    "C5": "C5: Allegro-like hand, four 24x24x3 mm fingertip pads (9x9x4 lattice, 324 nodes/960 tets each), palm + 16 "
+          "kinematic links driven by on-device forward kinematics of a 16-joint script, dynamic engraved tile "
+          "(16x30x22 mm, 8676 triangles), static table, dt=0.02 s",
     "C2": "C2: peg insertion, dual low-res sensors (2 pads x 8x6x3 lattice, 144 nodes/350 tets each), "
           "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s",
     "C3": "C3: peg insertion, dual high-res sensors (2 pads x 19x16x5 lattice, 1520 nodes/5400 tets each), "
@@ -47,6 +53,8 @@ WORKLOADS = {
 DEFAULTS = {  # config: (scaling, envs, default steps)
     "C3": ("strong", 4096, 10),
     "C2": ("weak", 1024, 20),
+    "C4": ("weak", 2048, 10),
+    "C5": ("strong", 1024, 10),
 }
 
 
@@ -287,11 +295,60 @@ def _pcts(v):
             "max": float(v.max())}
 
 
+class Part:
+    """One homogeneous batch of the workload (C4 has one per object shape) on its own CUDA stream."""
+
+    def __init__(self, sc, ids, W, K, dev, chain=False):
+        import torch
+        from paper_2504_12908_b200 import scenes as S
+        from paper_2504_12908_b200 import taccel as T
+        self.sc, self.ids, self.E = sc, ids, len(ids)
+        self.stream = torch.cuda.Stream(dev)
+        self.ei = S.env_inputs(sc, ids, n_steps=W + K)
+        self.batch = T.Batch(sc, self.E, device=dev.index, stream=self.stream)
+        st = self.batch.set_state(self.ei.x0, self.ei.y0)
+        assert (st == 0).all(), f"bad initial states: {np.unique(st)}"
+        self.ykin_dev = torch.tensor(self.ei.ykin, device=dev)
+        self.chain = chain
+        if chain:                                          # C5: targets compiled on the device from joint targets
+            self.batch.set_chain(S.hand_chain())
+            q = np.stack([S.hand_script(int(g), W + K).reshape(W + K, -1) for g in ids], 1)
+            self.q_dev = torch.tensor(q, device=dev)
+            self.base_dev = torch.tensor(np.repeat(S.hand_palm_pose()[None], self.E, 0), device=dev)
+        NC, NM = self.batch.n_coated, self.batch.n_markers
+        self.out_dev = [tuple(torch.empty((self.E, n, 3), dtype=torch.float64, device=dev) for n in (NC, NM, NM))
+                        for _ in range(K)]
+
+    def step(self, k, targets, outs, stats=None):
+        """One lockstep step: targets (tac_set_targets, or joint targets → tac_set_joint_targets), tac_step,
+        gel readout."""
+        import torch
+        with torch.cuda.stream(self.stream):
+            if self.chain:
+                self.batch.set_joint_targets(targets[k], base=self.base_dev)
+            else:
+                self.batch.set_targets(targets[k])
+            f = int((self.batch.step(1) != 0).sum())
+            self.batch.get_gel_deformation(out=outs)
+            if stats is not None:
+                stats.append(self.batch.stats())
+        return f
+
+
+def run_parts(parts, fn):
+    """Run fn(part) for every part concurrently (one host thread per batch: tac_step is host-blocking and
+    releases the GIL inside the C call); returns the results in part order."""
+    if len(parts) == 1:
+        return [fn(parts[0])]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(parts)) as ex:
+        return list(ex.map(fn, parts))
+
+
 def run_config(cfg_name, a, rank, world, dev, envs_total=None, envs_per_gpu=None, steps=None, primary=True):
     import torch
     import torch.distributed as dist
     from paper_2504_12908_b200 import scenes as S
-    from paper_2504_12908_b200 import taccel as T
     from paper_2504_12908_b200.shard import env_range, reduce_run_stats, split_range
 
     scaling = DEFAULTS[cfg_name][0]
@@ -305,102 +362,115 @@ def run_config(cfg_name, a, rank, world, dev, envs_total=None, envs_per_gpu=None
     else:
         per = envs_per_gpu or DEFAULTS[cfg_name][1]
         ids = np.asarray(list(env_range(rank, world, per)))
-    E = len(ids)
     W, K = a.warmup, (steps or a.steps)
-    sc = S.make_scene(cfg_name)
-    ei = S.env_inputs(sc, ids, n_steps=W + K)
-    stream = torch.cuda.current_stream(dev)
-    batch = T.Batch(sc, E, device=dev.index, stream=stream)
-    st = batch.set_state(ei.x0, ei.y0)
-    assert (st == 0).all(), f"bad initial states: {np.unique(st)}"
-    ykin_dev = torch.tensor(ei.ykin, device=dev)                     # (S, E, NK, 12) device-resident
-    NC, NM = batch.n_coated, batch.n_markers
-    out_dev = [(torch.empty((E, NC, 3), dtype=torch.float64, device=dev), torch.empty((E, NM, 3), dtype=torch.float64, device=dev),
-                torch.empty((E, NM, 3), dtype=torch.float64, device=dev)) for _ in range(K)]
+    if cfg_name == "C4":                   # 8 object shapes, one homogeneous batch each (env id → shape)
+        per_shape = max(1, (len(ids) + 7) // 8) if scaling == "strong" else max(1, (envs_per_gpu or DEFAULTS["C4"][1]) // 8)
+        groups = {}
+        for g in ids:
+            groups.setdefault(int((g % (8 * per_shape)) // per_shape), []).append(int(g))
+        parts = [Part(S.make_scene(f"C4:{sh}"), np.asarray(gl), W, K, dev) for sh, gl in sorted(groups.items())]
+    else:
+        parts = [Part(S.make_scene(cfg_name), ids, W, K, dev, chain=(cfg_name == "C5"))]
+    E = sum(p.E for p in parts)
+    sc = parts[0].sc
+    main = torch.cuda.current_stream(dev)
     fails = 0
 
-    def lockstep(k0, n, targets, outs, stats_out=None):
+    def lockstep(part, k0, n, targets, outs, stats_out=None):
         f = 0
         for k in range(n):
-            batch.set_targets(targets[k0 + k])
-            f += int((batch.step(1) != 0).sum())
-            batch.get_gel_deformation(out=outs[k])
-            if stats_out is not None:
-                stats_out.append(batch.stats())
+            f += part.step(k0 + k, targets, outs[k], stats_out)
         return f
 
+    tables = lambda p: p.q_dev if p.chain else p.ykin_dev
     # warm-up (untimed): W lockstep steps
-    fails += lockstep(0, W, ykin_dev, [out_dev[0]] * W)
-    saved = batch.get_state()
-    stats0 = batch.stats()
+    fails += sum(run_parts(parts, lambda p: lockstep(p, 0, W, tables(p), [p.out_dev[0]] * W)))
+    saved = [p.batch.get_state() for p in parts]
+    stats0 = [p.batch.stats() for p in parts]
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+
+    def timed(fn):
+        """CUDA-event time on the main stream with every part's stream joined in (device-side)."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        for p in parts:
+            p.stream.wait_event(e0)
+        res = run_parts(parts, fn)
+        for p in parts:
+            ej = torch.cuda.Event()
+            ej.record(p.stream)
+            main.wait_event(ej)
+        e1.record(main)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1), res
 
     # ---- timed: K lockstep steps, device-resident inputs/outputs ----
     clocks = Clocks(dev.index)
     clocks.start()
-    batch.profile(True)
-    batch.profile_read(reset=True)
-    per_step = []
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for p in parts:
+        p.batch.profile(True)
+        p.batch.profile_read(reset=True)
+    per_step = {id(p): [] for p in parts}
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    ev0.record(stream)
-    fails += lockstep(W, K, ykin_dev, out_dev, per_step)
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    prof = batch.profile_read(reset=True)
-    batch.profile(False)
+    ms, fl = timed(lambda p: lockstep(p, W, K, tables(p), p.out_dev, per_step[id(p)]))
+    fails += sum(fl)
+    profs = [p.batch.profile_read(reset=True) for p in parts]
+    for p in parts:
+        p.batch.profile(False)
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    stats1 = batch.stats()
-    pcg_local = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for s0, s1 in zip(stats0, stats1))
-    pcg_iters_local = sum(s1["pcg_iters_total"] - s0["pcg_iters_total"] for s0, s1 in zip(stats0, stats1))
-    newton = [s["newton_iters"] for ss in per_step for s in ss]
-    pcg_per_step = [s["pcg_iters"] for ss in per_step for s in ss]
-    n_active = [s["n_active"] for ss in per_step for s in ss]
-    n_res = [s["n_residual"] for ss in per_step for s in ss]
-    min_d = min((s["min_dist"] for ss in per_step for s in ss), default=float("inf"))
+    stats1 = [p.batch.stats() for p in parts]
+    pcg_local = sum(s1["pcg_alg_bytes_total"] - s0["pcg_alg_bytes_total"] for S0, S1 in zip(stats0, stats1) for s0, s1 in zip(S0, S1))
+    pcg_iters_local = sum(s1["pcg_iters_total"] - s0["pcg_iters_total"] for S0, S1 in zip(stats0, stats1) for s0, s1 in zip(S0, S1))
+    allst = [s for p in parts for ss in per_step[id(p)] for s in ss]
+    newton = [s["newton_iters"] for s in allst]
+    pcg_per_step = [s["pcg_iters"] for s in allst]
+    n_active = [s["n_active"] for s in allst]
+    n_res = [s["n_residual"] for s in allst]
+    n_fr = [s["n_friction"] for s in allst]
+    min_d = min((s["min_dist"] for s in allst), default=float("inf"))
 
     # ---- scheduled mode (context): the same K steps, envs advance independently ----
     ms_sched = 0.0
-    if not a.no_schedule:
-        x, xd, y, yd = saved
-        batch.set_state(x, y, xd, yd)
-        outs = tuple(torch.empty((K, E) + t.shape[1:], dtype=torch.float64, device=dev) for t in out_dev[0])
+    if not a.no_schedule and not parts[0].chain:
+        for p, sv in zip(parts, saved):
+            x, xd, y, yd = sv
+            p.batch.set_state(x, y, xd, yd)
+        outs = {id(p): tuple(torch.empty((K, p.E) + t.shape[1:], dtype=torch.float64, device=dev) for t in p.out_dev[0])
+                for p in parts}
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        batch.step_schedule(ykin_dev[W:W + K], out=outs)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms_sched = e0.elapsed_time(e1)
 
-    # ---- e2e: the same K lockstep steps through the C ABI with pinned HOST buffers (targets in,
-    #      per-step gel readout out, both copied inside the timed region) ----
+        def sched(p):
+            with torch.cuda.stream(p.stream):
+                p.batch.step_schedule(p.ykin_dev[W:W + K], out=outs[id(p)])
+        ms_sched, _ = timed(sched)
+
+    # ---- e2e: the same K lockstep steps through the C ABI with pinned HOST buffers (targets or joint
+    #      targets in, per-step gel readout out, both copied inside the timed region) ----
     ms_e2e, h2d, d2h = 0.0, 0, 0
     if not a.no_e2e:
-        x, xd, y, yd = saved
-        batch.set_state(x, y, xd, yd)
-        yk_host = torch.from_numpy(np.ascontiguousarray(ei.ykin[W:W + K])).pin_memory()
-        outs_h = [tuple(torch.empty(t.shape, dtype=torch.float64).pin_memory() for t in out_dev[0]) for _ in range(K)]
-        h2d = yk_host[0].numel() * 8
-        d2h = sum(t.numel() * 8 for t in outs_h[0])
+        for p, sv in zip(parts, saved):
+            x, xd, y, yd = sv
+            p.batch.set_state(x, y, xd, yd)
+        host = {}
+        for p in parts:
+            tab = (p.q_dev if p.chain else p.ykin_dev)[W:W + K].cpu().pin_memory()
+            outs_h = [tuple(torch.empty(t.shape, dtype=torch.float64).pin_memory() for t in p.out_dev[0]) for _ in range(K)]
+            host[id(p)] = (tab, outs_h)
+            h2d += tab[0].numel() * 8
+            d2h += sum(t.numel() * 8 for t in outs_h[0])
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
-        e0.record(stream)
-        lockstep(0, K, yk_host, outs_h)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+        ms_dev, _ = timed(lambda p: lockstep(p, 0, K, host[id(p)][0], host[id(p)][1]))
         wall = time.perf_counter() - t0
-        ms_e2e = max(e0.elapsed_time(e1), 1e3 * wall)
+        ms_e2e = max(ms_dev, 1e3 * wall)
 
     tot, cnt, mins = reduce_run_stats([ms, ms_e2e, ms_sched], [float(fails), float(pcg_iters_local), float(E)], world,
                                       device=dev, mins=[min_d])
@@ -409,24 +479,32 @@ def run_config(cfg_name, a, rank, world, dev, envs_total=None, envs_per_gpu=None
     n_env_total = int(n_env_total)
     dt = sc.config.dt
     value = n_env_total * K / (ms / 1e3)
+    prof = {}
+    for pr in profs:
+        for k, v in pr.items():
+            m0, n0 = prof.get(k, (0.0, 0))
+            prof[k] = (m0 + v[0], n0 + v[1])
     res = {"cfg": cfg_name, "E_local": E, "n_env_total": n_env_total, "scaling": scaling, "K": K, "W": W, "ms": ms,
-           "value": value, "dt": dt, "clocks": clk, "fails": fails, "min_dist": float(mins[0]),
-           "workspace_gb": batch.workspace.numel() / 1e9, "pcg_kernel": batch.pcg_kernel, "prof": prof}
+           "value": value, "dt": dt, "clocks": clk, "fails": fails, "min_dist": float(mins[0]), "n_batches": len(parts),
+           "workspace_gb": sum(p.batch.workspace.numel() for p in parts) / 1e9, "pcg_kernel": parts[0].batch.pcg_kernel,
+           "prof": prof}
     res["e2e"] = None if a.no_e2e else {"value": n_env_total * K / (ms_e2e / 1e3), "unit": "env-steps/s",
                                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                                        "path": "tac_set_targets (pinned host) + tac_step + tac_get_gel_deformation (pinned host) per step"}
-    res["schedule"] = None if a.no_schedule else {"value": n_env_total * K / (ms_sched / 1e3), "ms_per_step": ms_sched / K,
-                                                  "mode": "tac_step_schedule: envs advance independently through the same K steps"}
+                                        "path": ("tac_set_joint_targets" if parts[0].chain else "tac_set_targets") +
+                                                " (pinned host) + tac_step + tac_get_gel_deformation (pinned host) per step"}
+    res["schedule"] = None if (a.no_schedule or parts[0].chain) else {
+        "value": n_env_total * K / (ms_sched / 1e3), "ms_per_step": ms_sched / K,
+        "mode": "tac_step_schedule: envs advance independently through the same K steps"}
     res["solver"] = {"newton_iters_per_env_step": _pcts(newton), "pcg_iters_per_env_step": _pcts(pcg_per_step),
                      "pcg_iters_per_newton_iter": pcg_iters_all / max(sum(newton) * world, 1) if newton else None,
                      "active_pairs_per_env": _pcts(n_active), "residual_pairs_per_env": _pcts(n_res),
+                     "friction_pairs_per_env": _pcts(n_fr), "mu_friction": sc.config.mu_friction,
                      "failed_env_steps": fails, "min_dist_m": float(mins[0]),
                      "sample": "rank-0 per-env stats of every timed step" if world > 1 else "every env, every timed step"}
-    # roofline of the dominant kernel (PCG), from this rank's counters and CUDA events
     phases = {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items() if v[1] > 0}
     res["phases"] = phases
     res["launches"] = int(sum(v["launches"] for v in phases.values()))
-    res["roofline"] = roofline(cfg_name, res["pcg_kernel"], phases, pcg_local, ms, K)
+    res["roofline"] = roofline(cfg_name, res["pcg_kernel"], phases, pcg_local, ms * len(parts), K)
     return res
 
 

@@ -179,6 +179,32 @@ tac_status tac_set_state(tac_batch* b, int32_t env0, int32_t n, const double* x,
  * attached-vertex targets s^x follow from the mount links. */
 tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, const double* y_kin, void* stream);
 
+/* ---- on-device forward kinematics and action compilation ------
+ * A robot is a tree of links, each driving one kinematic affine body.  Link i (parents before
+ * children) has: parent (−1 = the env's base pose), origin[12] — the fixed transform (t, R row-major)
+ * from the parent's joint frame to its own joint frame at zero joint angle, axis[3] — the unit joint axis
+ * in its joint frame, joint — the index of its joint coordinate (revolute) or −1 (fixed), body[12] —
+ * the kinematic body's frame relative to the link's joint frame, kin_body — the affine body index it
+ * drives.  Joint frame of link i: J_i = J_parent · origin_i · Rot(axis_i, q_joint); target of its body:
+ * J_i · body_i (homogeneous products).  The chain is copied (host arrays borrowed for the call). */
+typedef struct {
+  int32_t n_links, n_joints;
+  const int32_t* parent;       /* [n_links] */
+  const double* origin;        /* [n_links][12] */
+  const double* axis;          /* [n_links][3] */
+  const int32_t* joint;        /* [n_links] joint index or −1 */
+  const double* body;          /* [n_links][12] */
+  const int32_t* kin_body;     /* [n_links] kinematic affine body index */
+} tac_chain_desc;
+tac_status tac_set_chain(tac_batch* b, const tac_chain_desc* chain);
+/* Action compilation on the device: joint targets q [n][n_joints] and base poses [n][12] (NULL = keep the
+ * previous base, identity at first) of envs [env0, env0+n) → the kinematic targets s^y of every chain
+ * link's body (the attached-vertex targets s^x follow from them at the next step).  Kinematic
+ * bodies outside the chain keep their targets.  Host or device buffers; enqueued on `stream`. */
+tac_status tac_set_joint_targets(tac_batch* b, int32_t env0, int32_t n, const double* base, const double* q, void* stream);
+/* Current kinematic targets y_kin [n][NK][12] (as set by tac_set_targets / tac_set_joint_targets). */
+tac_status tac_get_targets(tac_batch* b, int32_t env0, int32_t n, double* y_kin, void* stream);
+
 /* Advance every enabled env by n_steps time steps.  Host-blocking.  env_status [E] (may be NULL). */
 tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_status, void* stream);
 

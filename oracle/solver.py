@@ -231,6 +231,11 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
             if p_inf <= cfg.newton_tol_rel * L and mu_used == 0.0:
                 converged = True
                 break
+            # reading R14d: under an LM shift the step is no convergence measure; converged when the
+            # mass-scaled gradient step M⁻¹g is below τ_N·L_env (embedded ∞-norm)
+            if mu_used > 0.0 and embedded_inf_norm(model, spla.spsolve(Mreg.tocsc(), g)) <= cfg.newton_tol_rel * L:
+                converged = True
+                break
             if p_inf > cfg.max_step_rel * L:            # step cap (reading R17c)
                 p = p * (cfg.max_step_rel * L / p_inf)
             dx, dy = En.unpack(model, p, np.zeros_like(y))

@@ -64,7 +64,7 @@ struct HostT {
   std::vector<int> tri_blk, edge_blk;            // [NT][6], [NE][2] BSR index of (v_i, v_j) within a soft primitive (-1)
   int NNZ = 0;
   std::vector<int> body_kind, dof_slot, dof_body;
-  std::vector<double> My, bmass, bs1, bvol, bkappa;
+  std::vector<double> My, MyInv, bmass, bs1, bvol, bkappa;
   std::vector<int> vert_body, vert_aff;
   std::vector<double> vert_xbar;
   std::vector<int> sverts, tris, tri_body, edges, edge_body, body_sv_ptr;
@@ -332,6 +332,24 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
     for (auto& e : tri_edges(tg)) { all_edges.push_back(e); H.edge_body.push_back(ns + b); }
     o += A.n_verts;
   }
+  // (M^y)⁻¹ per body by Gauss-Jordan with partial pivoting (SPD 12×12)
+  H.MyInv.assign(144 * (size_t)na, 0.0);
+  for (int b = 0; b < na; ++b) {
+    double A[12][24];
+    for (int i = 0; i < 12; ++i)
+      for (int j = 0; j < 24; ++j) A[i][j] = j < 12 ? H.My[144 * (size_t)b + 12 * i + j] : (j - 12 == i ? 1.0 : 0.0);
+    for (int c = 0; c < 12; ++c) {
+      int piv = c;
+      for (int r = c + 1; r < 12; ++r) if (std::fabs(A[r][c]) > std::fabs(A[piv][c])) piv = r;
+      for (int j = 0; j < 24; ++j) std::swap(A[c][j], A[piv][j]);
+      const double d = A[c][c];
+      for (int j = 0; j < 24; ++j) A[c][j] /= d;
+      for (int r = 0; r < 12; ++r)
+        if (r != c) { const double f = A[r][c]; for (int j = 0; j < 24; ++j) A[r][j] -= f * A[c][j]; }
+    }
+    for (int i = 0; i < 12; ++i)
+      for (int j = 0; j < 12; ++j) H.MyInv[144 * (size_t)b + 12 * i + j] = A[i][12 + j];
+  }
   H.NT = (int)all_tris.size();
   H.NE = (int)all_edges.size();
   for (auto& t : all_tris) for (int k = 0; k < 3; ++k) H.tris.push_back(t[k]);
@@ -529,6 +547,7 @@ struct tac_batch {
   char* ws = nullptr;
   size_t ws_bytes = 0;
   int* h_flag = nullptr;  // pinned
+  void* chain_mem = nullptr;                 // forward-kinematics chain (tac_set_chain)
   std::vector<EnvCtl> hctl;
   // tracing
   bool prof = false;
@@ -586,7 +605,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.sedge = ti(H.sedge); D.vadj_ptr = ti(H.vadj_ptr); D.vadj = ti(H.vadj); D.vdiag_ptr = ti(H.vdiag_ptr);
   D.vdiag = ti(H.vdiag); D.eblk_ptr = ti(H.eblk_ptr); D.eblk = ti(H.eblk);
   D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rupx = ti(H.rupx); D.eup = ti(H.eup); D.tri_blk = ti(H.tri_blk); D.edge_blk = ti(H.edge_blk); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
-  D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My);
+  D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My); D.MyInv = td(H.MyInv);
   D.bmass = td(H.bmass); D.bs1 = td(H.bs1); D.bvol = td(H.bvol); D.bkappa = td(H.bkappa);
   D.vert_body = ti(H.vert_body); D.vert_aff = ti(H.vert_aff); D.vert_xbar = td(H.vert_xbar);
   D.sverts = ti(H.sverts); D.body_sv_ptr = ti(H.body_sv_ptr); D.tris = ti(H.tris); D.tri_body = ti(H.tri_body); D.edges = ti(H.edges);
@@ -669,6 +688,7 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.mu_f = cfg->mu_friction; D.eps_v = cfg->eps_v;
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
   D.elist = nullptr; D.elist_out = nullptr;
+  D.n_links = 0; D.n_joints = 0;
   D.cl.nc = H.cl_nc; D.cl.rpr = H.cl_rpr; D.cl.threads = H.cl_threads; D.cl.nvt = H.cl_nvt;
   D.cl.nle_max = H.cl_nle_max; D.cl.nlb_max = H.cl_nlb_max; D.cl.cplcap = H.cl_cplcap; D.cl.smem = H.cl_smem_bytes;
 }
@@ -741,7 +761,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, need, st);
 #define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
   UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
-  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(eup); UP(tri_blk); UP(edge_blk); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
+  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(eup); UP(tri_blk); UP(edge_blk); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(MyInv); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
   UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(body_sv_ptr); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
   UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
@@ -766,6 +786,7 @@ extern "C" tac_status tac_batch_destroy(tac_batch* b) {
   if (!b) return TAC_OK;
   DevGuard _dg(b->device);
   if (b->h_flag) cudaFreeHost(b->h_flag);
+  if (b->chain_mem) cudaFree(b->chain_mem);
   for (auto e : b->ev_pool) cudaEventDestroy(e);
   delete b;
   return TAC_OK;
@@ -830,6 +851,83 @@ extern "C" tac_status tac_set_state(tac_batch* b, int32_t env0, int32_t n, const
   s = pull_ctl(b, st);
   if (s) return s;
   return write_status(b, env0, n, env_status, st);
+}
+
+static bool is_device_ptr(const void* p);
+
+extern "C" tac_status tac_set_chain(tac_batch* b, const tac_chain_desc* ch) {
+  if (!b || !ch || ch->n_links <= 0 || ch->n_links > 64 || ch->n_joints < 0 || !ch->parent || !ch->origin || !ch->axis ||
+      !ch->joint || !ch->body || !ch->kin_body)
+    return fail(TAC_E_INVALID, "bad chain description");
+  ON_DEVICE(b);
+  Dev& D = b->D;
+  const HostT& H = b->H;
+  const int nl = ch->n_links;
+  std::vector<int> kin(nl);
+  for (int i = 0; i < nl; ++i) {
+    if (ch->parent[i] >= i || ch->parent[i] < -1) return fail(TAC_E_INVALID, "chain parents must precede their links");
+    if (ch->joint[i] >= ch->n_joints || ch->joint[i] < -1) return fail(TAC_E_INVALID, "joint index out of range");
+    const int kb = ch->kin_body[i];
+    if (kb < 0 || kb >= H.NA || H.kin_of_body[kb] < 0) return fail(TAC_E_INVALID, "chain link drives a non-kinematic body");
+    kin[i] = H.kin_of_body[kb];
+    const double* a = ch->axis + 3 * i;
+    if (ch->joint[i] >= 0 && std::fabs(a[0] * a[0] + a[1] * a[1] + a[2] * a[2] - 1.0) > 1e-12)
+      return fail(TAC_E_INVALID, "joint axis must be a unit vector");
+  }
+  const size_t bytes = sizeof(int) * 3 * nl + sizeof(double) * (27 * (size_t)nl + 12 * (size_t)D.E) + 256;
+  if (b->chain_mem) { cudaFree(b->chain_mem); b->chain_mem = nullptr; }
+  CUDA_TRY(cudaMalloc(&b->chain_mem, bytes));
+  char* m = (char*)b->chain_mem;
+  double* origin = (double*)m; double* axis = origin + 12 * nl; double* body = axis + 3 * nl; double* base = body + 12 * nl;
+  int* parent = (int*)(base + 12 * (size_t)D.E); int* joint = parent + nl; int* kinb = joint + nl;
+  CUDA_TRY(cudaMemcpy(origin, ch->origin, sizeof(double) * 12 * nl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(axis, ch->axis, sizeof(double) * 3 * nl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(body, ch->body, sizeof(double) * 12 * nl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(parent, ch->parent, sizeof(int) * nl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(joint, ch->joint, sizeof(int) * nl, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(kinb, kin.data(), sizeof(int) * nl, cudaMemcpyHostToDevice));
+  std::vector<double> ident((size_t)12 * D.E, 0.0);
+  for (int e = 0; e < D.E; ++e) { ident[12 * e + 3] = 1.0; ident[12 * e + 7] = 1.0; ident[12 * e + 11] = 1.0; }
+  CUDA_TRY(cudaMemcpy(base, ident.data(), sizeof(double) * 12 * D.E, cudaMemcpyHostToDevice));
+  D.n_links = nl; D.n_joints = ch->n_joints;
+  D.ch_parent = parent; D.ch_origin = origin; D.ch_axis = axis; D.ch_joint = joint; D.ch_body = body; D.ch_kin = kinb;
+  D.ch_base = base;
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_set_joint_targets(tac_batch* b, int32_t env0, int32_t n, const double* base, const double* q,
+                                           void* stream) {
+  tac_status s = check_range(b, env0, n);
+  if (s) return s;
+  if (!b->chain_mem) return fail(TAC_E_INVALID, "no chain: call tac_set_chain first");
+  if (!q && b->D.n_joints > 0) return fail(TAC_E_INVALID, "q is required");
+  ON_DEVICE(b);
+  Dev& D = b->D;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (base) CUDA_TRY(cudaMemcpyAsync(D.ch_base + (size_t)env0 * 12, base, sizeof(double) * 12 * n, cudaMemcpyDefault, st));
+  const double* dq = q;
+  void* tmp = nullptr;
+  if (q && !is_device_ptr(q)) {
+    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double) * (size_t)n * std::max(D.n_joints, 1), st));
+    CUDA_TRY(cudaMemcpyAsync(tmp, q, sizeof(double) * (size_t)n * D.n_joints, cudaMemcpyHostToDevice, st));
+    dq = (const double*)tmp;
+  }
+  launch_fk(D, env0, n, dq, st);
+  CUDA_TRY(cudaGetLastError());
+  if (tmp) CUDA_TRY(cudaFreeAsync(tmp, st));
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_get_targets(tac_batch* b, int32_t env0, int32_t n, double* y_kin, void* stream) {
+  tac_status s = check_range(b, env0, n);
+  if (s) return s;
+  if (!y_kin) return fail(TAC_E_INVALID, "y_kin is null");
+  ON_DEVICE(b);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (b->D.NK) CUDA_TRY(cudaMemcpyAsync(y_kin, b->D.ykin + (size_t)env0 * b->D.NK * 12, sizeof(double) * 12 * b->D.NK * n,
+                                        cudaMemcpyDefault, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TAC_OK;
 }
 
 extern "C" tac_status tac_set_targets(tac_batch* b, int32_t env0, int32_t n, const double* y_kin, void* stream) {
@@ -924,7 +1022,7 @@ extern "C" tac_status tac_step(tac_batch* b, int32_t n_steps, uint8_t* env_statu
   return any_failed ? fail(TAC_E_ENV_FAILED, "one or more envs failed (see env_status)") : TAC_OK;
 }
 
-static bool is_device_ptr(const void* p) {
+static bool is_device_ptr(const void* p) {  // (declared above)
   if (!p) return false;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }

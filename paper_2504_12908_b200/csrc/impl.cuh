@@ -127,6 +127,7 @@ struct Dev {
   const int* dof_slot;    // [NA] (-1 static)
   const int* dof_body;    // [ND]
   const double* My;       // [NA][144]
+  const double* MyInv;    // [NA][144] (M^y)⁻¹ (convergence test under an LM shift, reading R14d)
   const double* bmass;    // [NA]
   const double* bs1;      // [NA][3]
   const double* bvol;     // [NA]
@@ -226,6 +227,11 @@ struct Dev {
   int* fr_res;            // [E][act_cap]
   double* fr_xb;          // [E][act_cap][12]
   double* fr_dat;         // [E][act_cap][16] Δt²μλⁿ | n̂ 3 | Γ weights of slots 1..3 | yⁿ_j = x_j − x_0 (j = 1..3) 9
+  // forward kinematics chain (tac_set_chain; separate device allocation owned by the batch)
+  int n_links, n_joints;
+  const int* ch_parent; const double* ch_origin; const double* ch_axis; const int* ch_joint; const double* ch_body;
+  const int* ch_kin;      // kinematic index (0..NK-1) of each link's body
+  double* ch_base;        // [E][12] base pose per env
   int* any_active;        // [1] envs still active after k_control (count)
   int* act_list;          // [2][E] compacted active-env lists (double-buffered by Newton iteration parity)
   const int* elist;       // per launch: env list of this launch (nullptr = env0 + blockIdx)

@@ -2594,6 +2594,26 @@ __device__ void pcg_finish(const Dev& D, int e, double* p, double* red, double m
                            double gp) {
   EnvCtl& C = D.ctl[e];
   const int n = D.n;
+  // reading R14d: under an LM shift (μ > 0) the step no longer measures convergence; the env is
+  // converged when the mass-scaled gradient step M⁻¹g is below τ_N·L_env (embedded ∞-norm)
+  const double mu_used = D.hmode == 2 ? mu : 0.0;
+  double gm = 1.0 / 0.0;
+  if (mu_used > 0.0 && !bad) {
+    const double* g = D.g + (size_t)e * n;
+    double* mg = D.Ad + (size_t)e * n;                  // PCG scratch, free after the solve
+    for (int i = threadIdx.x; i < 3 * D.V; i += blockDim.x) mg[i] = g[i] / D.mass[i / 3];
+    for (int i = threadIdx.x; i < 12 * D.ND; i += blockDim.x) {
+      const int d = i / 12, row = i % 12;
+      const double* Mi = D.MyInv + (size_t)D.dof_body[d] * 144 + 12 * row;
+      const double* gb = g + 3 * D.V + 12 * d;
+      double t = 0.0;
+      for (int c = 0; c < 12; ++c) t += Mi[c] * gb[c];
+      mg[3 * D.V + i] = t;
+    }
+    __syncthreads();
+    gm = embedded_inf_norm(D, e, mg, red);
+    __syncthreads();
+  }
   double pm = embedded_inf_norm(D, e, p, red);
   // step cap (reading R17c): scale p to max_step·L_env if longer (direction unchanged)
   const double cap = D.max_step * C.L;
@@ -2619,11 +2639,10 @@ __device__ void pcg_finish(const Dev& D, int e, double* p, double* red, double m
       C.xfail = 1;                                        // retry projected next pass (not counted)
     } else {
       C.newton += 1;
-      const double mu_used = D.hmode == 2 ? mu : 0.0;
       C.mu_used = mu_used;
       if (D.hmode == 2) C.mu = (mu * 0.1 >= D.lm_mu0) ? mu * 0.1 : 0.0;
       if (bad || !(pm == pm) || !(gp < 0.0 || zero_g)) { C.phase = PHASE_FAILED; C.status = ENV_NONFINITE; }
-      else C.inner_conv = (pm <= D.tolN * C.L && mu_used == 0.0) ? 1 : 0;
+      else C.inner_conv = ((pm <= D.tolN * C.L && mu_used == 0.0) || gm <= D.tolN * C.L) ? 1 : 0;
     }
   }
 }
@@ -3236,6 +3255,58 @@ __global__ void __launch_bounds__(NTHREADS) k_advance(Dev D, int env0, const dou
 }
 
 // ------------------------------------------------------------------------------------------
+// forward kinematics / action compilation: one thread per (env, link); each thread
+// multiplies the homogeneous transforms from the root to its link (depth ≤ n_links) — no inter-thread
+// dependencies, deterministic
+// ------------------------------------------------------------------------------------------
+struct Xf { double t[3], R[9]; };
+__device__ __forceinline__ Xf xf_load(const double* y) {
+  Xf a;
+  for (int i = 0; i < 3; ++i) a.t[i] = y[i];
+  for (int i = 0; i < 9; ++i) a.R[i] = y[3 + i];
+  return a;
+}
+__device__ __forceinline__ Xf xf_mul(const Xf& a, const Xf& b) {   // a ∘ b: x ↦ a.t + a.R (b.t + b.R x)
+  Xf c;
+  for (int i = 0; i < 3; ++i) {
+    c.t[i] = a.t[i] + a.R[3 * i] * b.t[0] + a.R[3 * i + 1] * b.t[1] + a.R[3 * i + 2] * b.t[2];
+    for (int j = 0; j < 3; ++j) c.R[3 * i + j] = a.R[3 * i] * b.R[j] + a.R[3 * i + 1] * b.R[3 + j] + a.R[3 * i + 2] * b.R[6 + j];
+  }
+  return c;
+}
+__device__ __forceinline__ Xf xf_rot(const double* a, double th) {   // Rodrigues: cos θ I + sin θ [a]× + (1 − cos θ) a aᵀ
+  Xf r;
+  const double c = cos(th), s = sin(th), k = 1.0 - c;
+  r.t[0] = r.t[1] = r.t[2] = 0.0;
+  r.R[0] = c + k * a[0] * a[0]; r.R[1] = k * a[0] * a[1] - s * a[2]; r.R[2] = k * a[0] * a[2] + s * a[1];
+  r.R[3] = k * a[1] * a[0] + s * a[2]; r.R[4] = c + k * a[1] * a[1]; r.R[5] = k * a[1] * a[2] - s * a[0];
+  r.R[6] = k * a[2] * a[0] - s * a[1]; r.R[7] = k * a[2] * a[1] + s * a[0]; r.R[8] = c + k * a[2] * a[2];
+  return r;
+}
+// joint frame of link i of env e (walks the ancestors; chains are shallow)
+__device__ Xf fk_joint_frame(const Dev& D, int e, const double* q, int i) {
+  int path[32], depth = 0;
+  for (int l = i; l >= 0 && depth < 32; l = D.ch_parent[l]) path[depth++] = l;
+  Xf T = xf_load(D.ch_base + (size_t)e * 12);
+  for (int d = depth - 1; d >= 0; --d) {
+    const int l = path[d];
+    T = xf_mul(T, xf_load(D.ch_origin + 12 * (size_t)l));
+    const int j = D.ch_joint[l];
+    if (j >= 0) T = xf_mul(T, xf_rot(D.ch_axis + 3 * (size_t)l, q[j]));
+  }
+  return T;
+}
+__global__ void k_fk(Dev D, int env0, int ne, const double* q /*[ne][n_joints]*/) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= ne * D.n_links) return;
+  const int el = gid / D.n_links, i = gid % D.n_links, e = env0 + el;
+  const Xf T = xf_mul(fk_joint_frame(D, e, q + (size_t)el * D.n_joints, i), xf_load(D.ch_body + 12 * (size_t)i));
+  double* out = D.ykin + ((size_t)e * D.NK + D.ch_kin[i]) * 12;
+  for (int k = 0; k < 3; ++k) out[k] = T.t[k];
+  for (int k = 0; k < 9; ++k) out[3 + k] = T.R[k];
+}
+
+// ------------------------------------------------------------------------------------------
 // host launchers
 // ------------------------------------------------------------------------------------------
 // per-device state: the __constant__ tables and the dynamic-shared-memory attributes exist once per
@@ -3387,8 +3458,8 @@ static PcgPlan pcg_plan(const Dev& D) {
   const int thr = (thr_env >= 128 && thr_env <= PCG_R_THREADS && thr_env % 32 == 0) ? thr_env : pcg_r_threads(D.V);
   const size_t rb = pcg_r_bytes(D, thr);
   // preference: the single-CTA env-resident k_pcg_r (measured faster than k_pcg_cl with one CTA on C2:
-  // 229 vs 285 ms / 10 steps), then the cluster-resident k_pcg_cl for envs that do not fit one SM
-  // (TAC_PCG_CLUSTER=n forces the cluster kernel with n CTAs per env), then the streamed k_pcg
+  // 229 vs 285 ms / 10 steps), else the streamed k_pcg; TAC_PCG_CLUSTER=n forces the cluster-resident
+  // k_pcg_cl with n CTAs per env
   const bool force_cl = cluster_env > 0;
   if (resident && !force_cl) {
     const bool use512 = thr > 384 || lb512;
@@ -3400,7 +3471,9 @@ static PcgPlan pcg_plan(const Dev& D) {
       return PcgPlan{use512 ? PCG_RESIDENT512 : PCG_RESIDENT, thr, rb, lpr};
     cudaGetLastError();
   }
-  if (resident && cluster_env != 0 && D.cl.nc > 0 && cl_fits(D)) return PcgPlan{PCG_CLUSTER, D.cl.threads, D.cl.smem, 1};
+  // the cluster kernel only on request: on C3 (16-CTA clusters, ≤ 9 envs in flight) it measured 10.3 s
+  // of PCG per 4 steps against 5.7 s for the streamed kernel (profiles/r2_c3_pcg_ab.json)
+  if (resident && force_cl && D.cl.nc > 0 && cl_fits(D)) return PcgPlan{PCG_CLUSTER, D.cl.threads, D.cl.smem, 1};
   const size_t with_vec = spmv_smem(D) + (size_t)5 * D.n * sizeof(double);
   const int vsm = with_vec <= 200 * 1024 ? 1 : 0;
   return PcgPlan{vsm ? PCG_STREAM_VSM : PCG_STREAM, NTHREADS, vsm ? with_vec : spmv_smem(D), lpr};
@@ -3473,6 +3546,10 @@ void launch_gather_y(const Dev& D, int env0, int ne, int which, cudaStream_t s) 
 }
 void launch_validate(const Dev& D, int env0, int ne, cudaStream_t s) { k_validate<<<ne, NTHREADS, 0, s>>>(D, env0); }
 void launch_readout(const Dev& D, int env0, int ne, cudaStream_t s) { k_readout<<<ne, 128, 0, s>>>(D, env0); }
+void launch_fk(const Dev& D, int env0, int ne, const double* q, cudaStream_t s) {
+  const int n = ne * D.n_links;
+  if (n > 0) k_fk<<<(n + 127) / 128, 128, 0, s>>>(D, env0, ne, q);
+}
 void launch_begin_sched(const Dev& D, int env0, int ne, const double* sched, cudaStream_t s) {
   k_begin_sched<<<ne, NTHREADS, 0, s>>>(D, env0, sched);
 }

@@ -476,6 +476,27 @@ def fk_hand(y_palm, q):
     return np.stack(out)
 
 
+def hand_chain():
+    """The C5 hand as a kinematic tree (input description for tac_set_chain, include/taccel.h): link 0 the
+    palm (fixed to the base pose), then per finger proximal (abduction about z), two middle links and the
+    distal link (flexions about −y), each driving its kinematic body; same geometry as fk_hand."""
+    L = HAND_L
+    ident = pose([0, 0, 0])
+    parent, origin, axis, joint, body, kin = [-1], [ident], [np.array([0.0, 0.0, 1.0])], [-1], [ident], [2]
+    frames = hand_base_frames()
+    for fi, f in enumerate(HAND_FINGERS):
+        base, Rb = frames[f]
+        for j in range(4):
+            parent.append(0 if j == 0 else len(parent) - 1)
+            origin.append(pose(base, Rb) if j == 0 else pose([0, 0, -L[j - 1]]))
+            axis.append(np.array([0.0, 0.0, 1.0]) if j == 0 else np.array([0.0, -1.0, 0.0]))
+            joint.append(4 * fi + j)
+            body.append(pose([0, 0, -L[j] / 2]))
+            kin.append(3 + 4 * fi + j)
+    return {"parent": np.array(parent), "origin": np.stack(origin), "axis": np.stack(axis), "joint": np.array(joint),
+            "body": np.stack(body), "kin_body": np.array(kin), "n_joints": 16}
+
+
 def scene_C5():
     """C5: Allegro-like hand — palm (60x60x15 mm) and 4 fingers of 4 kinematic link boxes,
     four fingertip pads (24x24x3 mm, 9x9x4 lattice) on the distal links' inner faces, a dynamic engraved

@@ -71,6 +71,11 @@ class EnvStats(ctypes.Structure):
                 ("lm_mu", ctypes.c_double), ("n_friction", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
+class ChainDesc(ctypes.Structure):
+    _fields_ = [("n_links", ctypes.c_int32), ("n_joints", ctypes.c_int32), ("parent", c_int_p), ("origin", c_double_p),
+                ("axis", c_double_p), ("joint", c_int_p), ("body", c_double_p), ("kin_body", c_int_p)]
+
+
 def header_symbols():
     """Function names declared in include/taccel.h."""
     txt = open(HEADER).read()
@@ -107,6 +112,9 @@ def load():
             "tac_debug_accd": [vp, ctypes.c_int32, vp, vp, vp, c_double_p, vp],
             "tac_debug_pcg": [vp, ctypes.c_int32, vp, vp, ctypes.c_int32, ctypes.c_double, vp, c_int_p, c_double_p, vp],
             "tac_debug_inject_fault": [vp, ctypes.c_int32, ctypes.c_int32, vp],
+            "tac_set_chain": [vp, ctypes.POINTER(ChainDesc)],
+            "tac_set_joint_targets": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp],
+            "tac_get_targets": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp],
             "tac_profile_enable": [vp, ctypes.c_int32],
             "tac_profile_read": [vp, c_double_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32],
             "tac_profile_iterations": [vp, c_int_p, c_double_p, ctypes.c_int32, c_int_p],
@@ -262,6 +270,30 @@ class Batch:
     def set_targets(self, y_kin, env0: int = 0):
         y_kin = _f64(y_kin)
         _check(self.lib.tac_set_targets(self.handle, env0, y_kin.shape[0], _ptr(y_kin), self._s()))
+
+    def set_chain(self, chain: dict):
+        """Kinematic tree for on-device forward kinematics (keys: parent, origin, axis, joint, body,
+        kin_body, n_joints — see include/taccel.h tac_chain_desc)."""
+        keep = {k: (np.ascontiguousarray(chain[k], np.int32) if k in ("parent", "joint", "kin_body")
+                    else np.ascontiguousarray(chain[k], np.float64)) for k in ("parent", "origin", "axis", "joint", "body", "kin_body")}
+        d = ChainDesc()
+        d.n_links, d.n_joints = len(keep["parent"]), int(chain["n_joints"])
+        for k in ("parent", "joint", "kin_body"):
+            setattr(d, k, keep[k].ctypes.data_as(c_int_p))
+        for k in ("origin", "axis", "body"):
+            setattr(d, k, keep[k].ctypes.data_as(c_double_p))
+        _check(self.lib.tac_set_chain(self.handle, ctypes.byref(d)))
+
+    def set_joint_targets(self, q, base=None, env0: int = 0):
+        q = _f64(q)
+        _check(self.lib.tac_set_joint_targets(self.handle, env0, q.shape[0], _ptr(_f64(base)) if base is not None else None,
+                                              _ptr(q), self._s()))
+
+    def get_targets(self, env0: int = 0, n: Optional[int] = None):
+        n = self.n_envs - env0 if n is None else n
+        out = np.zeros((n, self.NK, 12))
+        _check(self.lib.tac_get_targets(self.handle, env0, n, _ptr(out), self._s()))
+        return out
 
     def step(self, n_steps: int = 1, raise_on_failure: bool = False):
         st = np.zeros(self.n_envs, np.uint8)

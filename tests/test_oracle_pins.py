@@ -870,3 +870,39 @@ def test_friction_incline_stick_and_slip(mu):
     eps_dt = 1e-3 * 0.01
     assert np.all(np.abs(out["stick"][4:]) < 10 * eps_dt), out["stick"]
     assert np.all(out["slip"][4:] > 0) and np.all(np.diff(out["slip"][4:]) > 0), out["slip"]
+
+
+# ------------------------------------------------------------------------------------ forward kinematics
+
+from oracle import kinematics as K
+
+
+def test_fk_planar_three_link_closed_form():
+    """3-joint planar arm: joint axes z, link lengths along x; the tip is at
+    Σ_i L_i (cos Σ_{j≤i} θ_j, sin Σ_{j≤i} θ_j) and its frame is rotated by Σθ — closed form to 1e-12."""
+    L = [0.3, 0.2, 0.1]
+    th = [0.4, -1.1, 0.7]
+    ident = np.r_[np.zeros(3), np.eye(3).ravel()]
+    chain = {"parent": [-1, 0, 1, 2], "joint": [0, 1, 2, -1], "axis": [[0, 0, 1]] * 4,
+             "origin": [ident, np.r_[L[0], 0, 0, np.eye(3).ravel()], np.r_[L[1], 0, 0, np.eye(3).ravel()],
+                        np.r_[L[2], 0, 0, np.eye(3).ravel()]],
+             "body": [ident] * 4}
+    out = K.forward(chain, ident, np.array(th))
+    c = np.cumsum(th)
+    tip = np.array([sum(L[i] * math.cos(c[i]) for i in range(3)), sum(L[i] * math.sin(c[i]) for i in range(3)), 0.0])
+    assert np.allclose(out[3, :3], tip, atol=1e-12)
+    assert np.allclose(out[3, 3:].reshape(3, 3), S.rot_z(c[-1]), atol=1e-12)
+
+
+def test_fk_hand_chain_matches_scene_generator():
+    """The C5 chain description (input to tac_set_chain) reproduces the scene generator's link targets
+    (12-vector compositions) through the oracle's 4×4 homogeneous products, to 1e-12."""
+    ch = S.hand_chain()
+    qs = S.hand_script(3, 120)
+    yp = S.hand_palm_pose()
+    for k in (0, 40, 79, 119):
+        ref = S.fk_hand(yp, qs[k])
+        q = qs[k].reshape(-1)
+        out = K.forward(ch, yp, q)
+        assert np.abs(out[1:] - ref).max() <= 1e-12
+        assert np.abs(out[0] - yp).max() <= 1e-15
