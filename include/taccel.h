@@ -229,6 +229,20 @@ tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_t n, double
 
 tac_status tac_get_stats(tac_batch* b, tac_env_stats* out /* [E] host */, void* stream);
 
+/* Depth and normal maps of the deformed coated surface ∂⁺G̃ of every pad ("extract the depth
+ * and normal maps d(u,v), n(u,v) ... from the deformed coated surface"; reading R22): an orthographic
+ * camera in each pad's sensor frame looks along −z at the coated face.  Pixel (i, j) of an H×W map
+ * (H, W ≥ 2) samples the sensor-frame point (x₀ + j·(x₁−x₀)/(W−1), y₀ + i·(y₁−y₀)/(H−1)), a
+ * corner-aligned grid over the rest extent [x₀,x₁]×[y₀,y₁] of the pad's coated vertices.  A coated
+ * triangle (surface triangle with three coated vertices) covers a pixel when the pixel's barycentric
+ * coordinates in the triangle's deformed xy projection are all ≥ −1e-9.  depth = z_ref − z, the largest
+ * over covering triangles of the linearly interpolated deformed height z below the rest height z_ref of
+ * the coated face (positive = indentation); normal = the normalised sum of the covering triangles'
+ * (deformed, sensor-frame) area vectors, oriented +z.  Uncovered pixels: depth NaN, normal 0.
+ * depth [n][npads][H][W], normal [n][npads][H][W][3] (either may be NULL), host or device memory. */
+tac_status tac_get_depth_maps(tac_batch* b, int32_t env0, int32_t n, int32_t H, int32_t W, double* depth, double* normal,
+                              void* stream);
+
 const char* tac_last_error(void);
 
 /* ---- tracing: CUDA-event phase timers on the launch stream ----------------------------------

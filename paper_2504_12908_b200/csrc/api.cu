@@ -74,6 +74,8 @@ struct HostT {
   std::vector<double> att_local;
   std::vector<int> coat_vert, coat_pad, mark_tri, mark_pad, pad_mount;
   std::vector<double> mark_bary, pad_T;
+  std::vector<int> ct_ptr, ct_tri, coat_ptr;     // depth maps: coated triangles per pad, coated-vertex ranges
+  std::vector<double> cam;                       // [npads][5]
   // cluster PCG plan (k_pcg_cl): soft rows split into cl_nc contiguous ranges of cl_rpr rows
   int cl_nc = 0, cl_rpr = 0, cl_threads = 0, cl_nvt = 0, cl_nle_max = 0, cl_nlb_max = 0, cl_cplcap = 0;
   size_t cl_smem_bytes = 0;
@@ -510,6 +512,31 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
   }
   H.NC = (int)H.att_vert.size();
   H.NCOAT = (int)H.coat_vert.size();
+  // coated triangles per pad (surface triangles with 3 coated vertices, canonical surface order) and
+  // each pad's camera box (rest extent of its coated vertices in the sensor frame, z_ref = max rest z)
+  {
+    std::vector<int> cidx(H.V, -1);
+    for (int i = 0; i < H.NCOAT; ++i) cidx[H.coat_vert[i]] = i;
+    H.ct_ptr.assign(1, 0);
+    H.coat_ptr.assign(1, 0);
+    for (int p = 0; p < ns; ++p) {
+      for (auto& t : soft_tris[p]) {
+        const int a = cidx[t[0]], b = cidx[t[1]], c = cidx[t[2]];
+        if (a >= 0 && b >= 0 && c >= 0) { H.ct_tri.push_back(a); H.ct_tri.push_back(b); H.ct_tri.push_back(c); }
+      }
+      H.ct_ptr.push_back((int)H.ct_tri.size() / 3);
+      int n_c = 0;
+      double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300, zr = -1e300;
+      for (int i = 0; i < H.NCOAT; ++i)
+        if (H.coat_pad[i] == p) {
+          ++n_c;
+          const double* X = &H.Xrest[3 * (size_t)H.coat_vert[i]];
+          x0 = std::min(x0, X[0]); x1 = std::max(x1, X[0]); y0 = std::min(y0, X[1]); y1 = std::max(y1, X[1]); zr = std::max(zr, X[2]);
+        }
+      H.coat_ptr.push_back(H.coat_ptr.back() + n_c);
+      for (double v : {x0, x1, y0, y1, zr}) H.cam.push_back(v);
+    }
+  }
   H.NMARK = (int)H.mark_pad.size();
   H.kin_of_body.assign(na, -1);
   for (int b = 0; b < na; ++b)
@@ -617,6 +644,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.coat_vert = ti(H.coat_vert); D.coat_pad = ti(H.coat_pad); D.mark_tri = ti(H.mark_tri);
   D.mark_bary = td(H.mark_bary); D.mark_pad = ti(H.mark_pad); D.pad_mount = ti(H.pad_mount);
   D.pad_T = td(H.pad_T); D.Xrest = td(H.Xrest);
+  D.ct_ptr = ti(H.ct_ptr); D.ct_tri = ti(H.ct_tri); D.coat_ptr = ti(H.coat_ptr); D.cam = td(H.cam);
   D.cl.eptr = ti(H.cl_eptr); D.cl.edge = ti(H.cl_edge); D.cl.bptr = ti(H.cl_bptr); D.cl.lrptr = ti(H.cl_lrptr);
   D.cl.blk = reinterpret_cast<const int2*>(ti(H.cl_blk));
   const size_t e = (size_t)E, n = H.n;
@@ -688,6 +716,11 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.mu_f = cfg->mu_friction; D.eps_v = cfg->eps_v;
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
   D.elist = nullptr; D.elist_out = nullptr;
+  D.NCT = (int)H.ct_tri.size() / 3; D.maxct = 0; D.maxcv = 0;
+  for (int p = 0; p + 1 < (int)H.ct_ptr.size(); ++p) {
+    D.maxct = std::max(D.maxct, H.ct_ptr[p + 1] - H.ct_ptr[p]);
+    D.maxcv = std::max(D.maxcv, H.coat_ptr[p + 1] - H.coat_ptr[p]);
+  }
   D.n_links = 0; D.n_joints = 0;
   D.cl.nc = H.cl_nc; D.cl.rpr = H.cl_rpr; D.cl.threads = H.cl_threads; D.cl.nvt = H.cl_nvt;
   D.cl.nle_max = H.cl_nle_max; D.cl.nlb_max = H.cl_nlb_max; D.cl.cplcap = H.cl_cplcap; D.cl.smem = H.cl_smem_bytes;
@@ -765,7 +798,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(body_sv_ptr); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
   UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
-  UP(mark_bary); UP(mark_pad); UP(pad_mount); UP(pad_T); UP(Xrest);
+  UP(mark_bary); UP(mark_pad); UP(pad_mount); UP(pad_T); UP(Xrest); UP(ct_ptr); UP(ct_tri); UP(coat_ptr); UP(cam);
 #undef UP
   if (e == cudaSuccess) e = up(D.cl.eptr, H.cl_eptr, st);
   if (e == cudaSuccess) e = up(D.cl.edge, H.cl_edge, st);
@@ -1123,6 +1156,36 @@ extern "C" tac_status tac_get_gel_deformation(tac_batch* b, int32_t env0, int32_
     CUDA_TRY(cudaMemcpyAsync(marker_pos, D.out_mpos + (size_t)env0 * D.NMARK * 3, (size_t)n * D.NMARK * 3 * 8, cudaMemcpyDefault, st));
   if (marker_flow && D.NMARK)
     CUDA_TRY(cudaMemcpyAsync(marker_flow, D.out_mflow + (size_t)env0 * D.NMARK * 3, (size_t)n * D.NMARK * 3 * 8, cudaMemcpyDefault, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (b->prof) prof_flush(b);
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_get_depth_maps(tac_batch* b, int32_t env0, int32_t n, int32_t H, int32_t W, double* depth,
+                                         double* normal, void* stream) {
+  tac_status s = check_range(b, env0, n);
+  if (s) return s;
+  if (H < 2 || W < 2 || (long long)H * W > (1LL << 24)) return fail(TAC_E_INVALID, "depth map size must be 2..16M pixels");
+  if (!depth && !normal) return TAC_OK;
+  ON_DEVICE(b);
+  Dev& D = b->D;
+  if (D.npads == 0 || D.NCT == 0) return fail(TAC_E_INVALID, "no coated triangles");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t npx = (size_t)n * D.npads * H * W;
+  double *dd = depth, *dn = normal;
+  void* tmp = nullptr;
+  const bool hd = depth && !is_device_ptr(depth), hn = normal && !is_device_ptr(normal);
+  if (hd || hn) {
+    CUDA_TRY(cudaMallocAsync(&tmp, npx * 8 * ((hd ? 1 : 0) + (hn ? 3 : 0)) + 64, st));
+    double* t = (double*)tmp;
+    if (hd) { dd = t; t += npx; }
+    if (hn) dn = t;
+  }
+  { PROF(PH_READOUT); launch_depth(D, env0, n, H, W, dd, dn, st); }
+  CUDA_TRY(cudaGetLastError());
+  if (hd) CUDA_TRY(cudaMemcpyAsync(depth, dd, npx * 8, cudaMemcpyDeviceToHost, st));
+  if (hn) CUDA_TRY(cudaMemcpyAsync(normal, dn, npx * 24, cudaMemcpyDeviceToHost, st));
+  if (tmp) CUDA_TRY(cudaFreeAsync(tmp, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (b->prof) prof_flush(b);
   return TAC_OK;

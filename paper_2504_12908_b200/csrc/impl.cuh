@@ -164,6 +164,12 @@ struct Dev {
   const int* pad_mount;   // [npads]
   const double* pad_T;    // [npads][12]
   const double* Xrest;    // [V][3] pad-frame rest positions
+  // depth maps (tac_get_depth_maps): coated triangles per pad (indices into the coat list), camera box
+  const int* ct_ptr;      // [npads+1]
+  const int* ct_tri;      // [NCT][3] indices into coat_vert
+  const int* coat_ptr;    // [npads+1] range of each pad's coated vertices in coat_vert
+  const double* cam;      // [npads][5] x0, x1, y0, y1, z_ref (sensor frame, rest)
+  int NCT, maxct, maxcv;
   // ---- per env ----
   EnvCtl* ctl;            // [E]
   double *q, *qn, *vel, *qt, *g, *p, *r, *z, *dd, *Ad;   // [E][n]

@@ -3255,6 +3255,127 @@ __global__ void __launch_bounds__(NTHREADS) k_advance(Dev D, int env0, const dou
 }
 
 // ------------------------------------------------------------------------------------------
+// depth and normal maps of the deformed coated surface (reading R22): one CTA per (env, pad);
+// the pad's coated vertices are brought to its sensor frame, the coated triangles binned into 16×16-pixel
+// cells (lists sorted by triangle → deterministic sums), then each pixel takes the max depth and the
+// summed area vector over the covering triangles of its cell
+// ------------------------------------------------------------------------------------------
+constexpr int DEPTH_THREADS = 256;
+constexpr int DEPTH_CELL = 16;
+__global__ void __launch_bounds__(DEPTH_THREADS) k_depth(Dev D, int env0, int H, int W, int ent_cap, double* depth,
+                                                          double* normal) {
+  const int el = blockIdx.x / D.npads, p = blockIdx.x % D.npads, e = env0 + el;
+  extern __shared__ double dsm_depth[];
+  const int c0 = D.coat_ptr[p], nc = D.coat_ptr[p + 1] - c0;
+  const int t0 = D.ct_ptr[p], nt = D.ct_ptr[p + 1] - t0;
+  const int ncx = (W + DEPTH_CELL - 1) / DEPTH_CELL, ncy = (H + DEPTH_CELL - 1) / DEPTH_CELL, ncell = ncx * ncy;
+  double* X = dsm_depth;                                    // [nc][3] sensor-frame deformed positions
+  int* cnt = reinterpret_cast<int*>(X + 3 * (size_t)nc);    // [ncell + 1]
+  int* cur = cnt + ncell + 1;                               // [ncell]
+  int* ent = cur + ncell;                                   // [ent_cap] triangle index (local)
+  __shared__ int sh[33], ovf;
+  const double* q = D.q + (size_t)e * D.n;
+  const double* T = D.pad_T + 12 * p;
+  const int mb = D.pad_mount[p];
+  double Ai[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  v3 tl = mk(0, 0, 0);
+  if (mb >= 0) {
+    const double* y = body_y(D, e, mb);
+    inv33(y + 3, Ai);
+    tl = mk(y[0], y[1], y[2]);
+  }
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const int v = D.coat_vert[c0 + i];
+    const v3 loc = mb >= 0 ? mul33(Ai, ld3(q + 3 * v) - tl) : ld3(q + 3 * v);
+    st3(X + 3 * i, mul33T(T + 3, loc - ld3(T)));
+  }
+  const double* cam = D.cam + 5 * p;
+  const double x0 = cam[0], y0 = cam[2], dx = (cam[1] - cam[0]) / (W - 1), dy = (cam[3] - cam[2]) / (H - 1), zref = cam[4];
+  for (int i = threadIdx.x; i <= ncell; i += blockDim.x) cnt[i] = 0;
+  if (threadIdx.x == 0) ovf = 0;
+  __syncthreads();
+  const int* tri = D.ct_tri + 3 * (size_t)t0;
+  // pixel-index range of a triangle's projected bounding box (pixels whose centre can be covered)
+  auto prange = [&](int t, int* j0, int* j1, int* i0, int* i1) {
+    const int a = tri[3 * t] - c0, b = tri[3 * t + 1] - c0, c = tri[3 * t + 2] - c0;
+    const double xl = fmin(X[3 * a], fmin(X[3 * b], X[3 * c])), xh = fmax(X[3 * a], fmax(X[3 * b], X[3 * c]));
+    const double yl = fmin(X[3 * a + 1], fmin(X[3 * b + 1], X[3 * c + 1])), yh = fmax(X[3 * a + 1], fmax(X[3 * b + 1], X[3 * c + 1]));
+    const double px = 1e-7 * (xh - xl + dx), py = 1e-7 * (yh - yl + dy);   // margin ≫ the coverage tolerance
+    *j0 = max(0, (int)ceil((xl - px - x0) / dx)); *j1 = min(W - 1, (int)floor((xh + px - x0) / dx));
+    *i0 = max(0, (int)ceil((yl - py - y0) / dy)); *i1 = min(H - 1, (int)floor((yh + py - y0) / dy));
+  };
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    int j0, j1, i0, i1;
+    prange(t, &j0, &j1, &i0, &i1);
+    if (j0 > j1 || i0 > i1) continue;
+    for (int cy = i0 / DEPTH_CELL; cy <= i1 / DEPTH_CELL; ++cy)
+      for (int cx = j0 / DEPTH_CELL; cx <= j1 / DEPTH_CELL; ++cx) atomicAdd(&cnt[cy * ncx + cx], 1);
+  }
+  __syncthreads();
+  {
+    const int per = (ncell + blockDim.x - 1) / blockDim.x, b0 = threadIdx.x * per;
+    int sum = 0;
+    for (int i = 0; i < per && b0 + i < ncell; ++i) sum += cnt[b0 + i];
+    int tot;
+    int run = block_excl_scan(sum, sh, &tot);
+    for (int i = 0; i < per && b0 + i < ncell; ++i) { const int c = cnt[b0 + i]; cnt[b0 + i] = run; cur[b0 + i] = run; run += c; }
+    __syncthreads();
+    if (threadIdx.x == 0) { cnt[ncell] = tot; if (tot > ent_cap) ovf = 1; }
+    __syncthreads();
+  }
+  const bool brute = ovf != 0;                             // too many entries: every pixel tests every triangle
+  if (!brute) {
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+      int j0, j1, i0, i1;
+      prange(t, &j0, &j1, &i0, &i1);
+      if (j0 > j1 || i0 > i1) continue;
+      for (int cy = i0 / DEPTH_CELL; cy <= i1 / DEPTH_CELL; ++cy)
+        for (int cx = j0 / DEPTH_CELL; cx <= j1 / DEPTH_CELL; ++cx) ent[atomicAdd(&cur[cy * ncx + cx], 1)] = t;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x)            // ascending triangle order per cell
+      for (int i = cnt[c] + 1; i < cnt[c + 1]; ++i) {
+        const int key = ent[i];
+        int j = i - 1;
+        while (j >= cnt[c] && ent[j] > key) { ent[j + 1] = ent[j]; --j; }
+        ent[j + 1] = key;
+      }
+    __syncthreads();
+  }
+  const size_t plane = (size_t)H * W, base = ((size_t)el * D.npads + p) * plane;
+  for (int px = threadIdx.x; px < H * W; px += blockDim.x) {
+    const int i = px / W, j = px % W;
+    const double cxp = x0 + j * dx, cyp = y0 + i * dy;
+    const int cell = (i / DEPTH_CELL) * ncx + (j / DEPTH_CELL);
+    const int k0 = brute ? 0 : cnt[cell], k1 = brute ? nt : cnt[cell + 1];
+    double best = -1.0 / 0.0;
+    v3 nsum = mk(0, 0, 0);
+    bool any = false;
+    for (int k = k0; k < k1; ++k) {
+      const int t = brute ? k : ent[k];
+      const int a = tri[3 * t] - c0, b = tri[3 * t + 1] - c0, c = tri[3 * t + 2] - c0;
+      const v3 A = ld3(X + 3 * a), B = ld3(X + 3 * b), Cc = ld3(X + 3 * c);
+      const double ar = (B.x - A.x) * (Cc.y - A.y) - (B.y - A.y) * (Cc.x - A.x);
+      if (ar == 0.0) continue;
+      const double wa = ((B.x - cxp) * (Cc.y - cyp) - (B.y - cyp) * (Cc.x - cxp)) / ar;
+      const double wb = ((Cc.x - cxp) * (A.y - cyp) - (Cc.y - cyp) * (A.x - cxp)) / ar;
+      const double wc = ((A.x - cxp) * (B.y - cyp) - (A.y - cyp) * (B.x - cxp)) / ar;
+      if (wa < -1e-9 || wb < -1e-9 || wc < -1e-9) continue;
+      any = true;
+      best = fmax(best, zref - (wa * A.z + wb * B.z + wc * Cc.z));
+      v3 av = cross(B - A, Cc - A);
+      if (av.z < 0.0) av = -av;
+      nsum += av;
+    }
+    if (depth) depth[base + px] = any ? best : 0.0 / 0.0;
+    if (normal) {
+      const double ln = sqrt(dot(nsum, nsum));
+      st3(normal + 3 * (base + px), any && ln > 0.0 ? (1.0 / ln) * nsum : mk(0, 0, 0));
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // forward kinematics / action compilation: one thread per (env, link); each thread
 // multiplies the homogeneous transforms from the root to its link (depth ≤ n_links) — no inter-thread
 // dependencies, deterministic
@@ -3546,6 +3667,15 @@ void launch_gather_y(const Dev& D, int env0, int ne, int which, cudaStream_t s) 
 }
 void launch_validate(const Dev& D, int env0, int ne, cudaStream_t s) { k_validate<<<ne, NTHREADS, 0, s>>>(D, env0); }
 void launch_readout(const Dev& D, int env0, int ne, cudaStream_t s) { k_readout<<<ne, 128, 0, s>>>(D, env0); }
+void launch_depth(const Dev& D, int env0, int ne, int H, int W, double* depth, double* normal, cudaStream_t s) {
+  const int ncell = ((W + DEPTH_CELL - 1) / DEPTH_CELL) * ((H + DEPTH_CELL - 1) / DEPTH_CELL);
+  static size_t attr[MAX_DEVICES] = {};
+  const size_t fixed = (size_t)24 * D.maxcv + (size_t)4 * (2 * ncell + 1) + 64;
+  const int ent_cap = (int)std::max<size_t>(64, ((size_t)200 * 1024 - std::min<size_t>(fixed, (size_t)200 * 1024)) / 4);
+  const size_t bytes = fixed + (size_t)4 * ent_cap;
+  ensure_smem(k_depth, attr, bytes);
+  k_depth<<<ne * D.npads, DEPTH_THREADS, bytes, s>>>(D, env0, H, W, ent_cap, depth, normal);
+}
 void launch_fk(const Dev& D, int env0, int ne, const double* q, cudaStream_t s) {
   const int n = ne * D.n_links;
   if (n > 0) k_fk<<<(n + 127) / 128, 128, 0, s>>>(D, env0, ne, q);

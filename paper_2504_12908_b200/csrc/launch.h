@@ -26,6 +26,7 @@ void launch_scatter_y(const Dev& D, int env0, int ne, int which, cudaStream_t s)
 void launch_gather_y(const Dev& D, int env0, int ne, int which, cudaStream_t s);
 void launch_validate(const Dev& D, int env0, int ne, cudaStream_t s);
 void launch_readout(const Dev& D, int env0, int ne, cudaStream_t s);
+void launch_depth(const Dev& D, int env0, int ne, int H, int W, double* depth, double* normal, cudaStream_t s);
 void launch_fk(const Dev& D, int env0, int ne, const double* q, cudaStream_t s);
 void launch_begin_sched(const Dev& D, int env0, int ne, const double* sched, cudaStream_t s);
 void launch_advance(const Dev& D, int env0, int ne, const double* sched, int nsteps, double* oc, double* om,

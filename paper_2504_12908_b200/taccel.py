@@ -115,6 +115,7 @@ def load():
             "tac_set_chain": [vp, ctypes.POINTER(ChainDesc)],
             "tac_set_joint_targets": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp],
             "tac_get_targets": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp],
+            "tac_get_depth_maps": [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp, vp],
             "tac_profile_enable": [vp, ctypes.c_int32],
             "tac_profile_read": [vp, c_double_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32],
             "tac_profile_iterations": [vp, c_int_p, c_double_p, ctypes.c_int32, c_int_p],
@@ -335,6 +336,16 @@ class Batch:
         c, mp, mf = out
         _check(self.lib.tac_get_gel_deformation(self.handle, env0, n, _ptr(c), _ptr(mp), _ptr(mf), self._s()))
         return out
+
+    def get_depth_maps(self, H: int, W: int, env0: int = 0, n: Optional[int] = None, device=None, normals: bool = True):
+        """Depth [n, pads, H, W] and normal [n, pads, H, W, 3] maps of the coated surfaces (tac_get_depth_maps)."""
+        n = self.n_envs - env0 if n is None else n
+        dev = self.device if device is None else device
+        npads = len(self.scene.soft)
+        d = torch.empty((n, npads, H, W), dtype=torch.float64, device=dev)
+        nm = torch.empty((n, npads, H, W, 3), dtype=torch.float64, device=dev) if normals else None
+        _check(self.lib.tac_get_depth_maps(self.handle, env0, n, H, W, _ptr(d), _ptr(nm), self._s()))
+        return d, nm
 
     def stats(self):
         arr = (EnvStats * self.n_envs)()

@@ -420,3 +420,33 @@ def test_friction_incline_stick_slip_matches_oracle(mu):
             assert np.all(np.abs(dx) < 10 * eps_dt), dx
         else:
             assert np.all(dx > 0) and np.all(np.diff(dx) > 0), dx
+
+
+# ------------------------------------------------------------------------------------------ depth maps
+
+@pytest.mark.parametrize("name,E,steps", [("C1", 2, 6), ("C2", 3, 12)])
+def test_depth_normal_maps_match_oracle(name, E, steps):
+    """tac_get_depth_maps (reading R22) after `steps` lockstep steps (pads pressed): depth
+    and normal maps of every pad of every env match the oracle rasteriser within 1e-12 (NaN pattern
+    identical), at a non-square resolution."""
+    from oracle import tactile as Tc
+    sc = S.make_scene(name)
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, range(E), n_steps=steps)
+    b = T.Batch(sc, E)
+    assert (b.set_state(ei.x0, ei.y0) == 0).all()
+    for k in range(steps):
+        b.set_targets(ei.ykin[k])
+        assert (b.step(1) == 0).all()
+    H, W = 17, 23
+    d, nm = (t.cpu().numpy() for t in b.get_depth_maps(H, W))
+    x_all, _, y_all, _ = (t.cpu().numpy() for t in b.get_state())
+    deepest = 0.0
+    for e in range(E):
+        Do, No = Tc.depth_maps(mod, x_all[e], y_all[e], H, W)
+        assert np.array_equal(np.isnan(d[e]), np.isnan(Do))
+        ok = ~np.isnan(Do)
+        assert np.abs(d[e][ok] - Do[ok]).max() <= 1e-12
+        assert np.abs(nm[e] - No).max() <= 1e-12
+        deepest = max(deepest, np.nanmax(Do))
+    assert deepest > 1e-5                                 # some pad is indented

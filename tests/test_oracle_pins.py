@@ -906,3 +906,59 @@ def test_fk_hand_chain_matches_scene_generator():
         out = K.forward(ch, yp, q)
         assert np.abs(out[1:] - ref).max() <= 1e-12
         assert np.abs(out[0] - yp).max() <= 1e-15
+
+
+# ------------------------------------------------------------------------------------ depth maps
+
+from oracle import tactile as Tc
+
+
+def _c1_pad_state():
+    sc = S.make_scene("C1")
+    mod = M.prepare(sc)
+    ei = S.env_inputs(sc, [0], n_steps=1)
+    return sc, mod, ei.x0[0].copy(), ei.y0[0].copy()
+
+
+def test_depth_map_undeformed_and_rigid_motion():
+    """Undeformed pad → depth 0 and normal +z at every pixel (S:L532 'zero depth without contact');
+    moving the pad rigidly with its mount link leaves the maps unchanged (sensor frame)."""
+    sc, mod, x, y = _c1_pad_state()
+    D0, N0 = Tc.depth_maps(mod, x, y, 9, 11)
+    assert np.all(np.abs(D0) <= 1e-15) and np.allclose(N0, [0, 0, 1], atol=1e-15)
+    R = S.rot_z(0.7) @ S.rot_y(0.2)
+    t = np.array([0.01, -0.02, 0.03])
+    y2 = y.copy()
+    y2[0] = np.r_[t + R @ y[0, :3], (R @ y[0, 3:].reshape(3, 3)).ravel()]
+    x2 = x @ R.T + t
+    D1, N1 = Tc.depth_maps(mod, x2, y2, 9, 11)
+    assert np.all(np.abs(D1) <= 1e-12) and np.allclose(N1, [0, 0, 1], atol=1e-12)
+
+
+def test_depth_map_sphere_cap_closed_form():
+    """A sphere of radius R pressed h into the coated face (constructed state: every coated vertex
+    lowered to the cap): pixels on lattice vertices read the analytic cap depth
+    d(r) = h − (R − √(R² − r²)) and pixels on lattice edges the average of the edge's vertex depths
+    (the surface is piecewise linear), to 1e-12; flat regions keep normal +z."""
+    sc, mod, x, y = _c1_pad_state()
+    pad = sc.soft[0]
+    Rs, h = 10e-3, 0.6e-3
+    off = 0
+    cap = lambda r: np.maximum(0.0, h - (Rs - np.sqrt(np.maximum(Rs * Rs - r * r, 0.0))))
+    xs = x.copy()
+    X = pad.rest_pos
+    for v in pad.coated:
+        xs[off + v, 2] -= cap(np.hypot(X[v, 0], X[v, 1]))
+    H = W = 15                                           # 8x8 vertex lattice → vertices at even pixels
+    D, N = Tc.depth_maps(mod, xs, y, H, W)
+    xv = np.linspace(X[pad.coated, 0].min(), X[pad.coated, 0].max(), W)
+    yv = np.linspace(X[pad.coated, 1].min(), X[pad.coated, 1].max(), H)
+    for i in range(0, H, 2):
+        for j in range(0, W, 2):
+            assert D[0, i, j] == pytest.approx(cap(np.hypot(xv[j], yv[i])), abs=1e-12)
+    for i in range(0, H, 2):                             # midpoints of lattice edges along x
+        for j in range(1, W, 2):
+            expect = 0.5 * (cap(np.hypot(xv[j - 1], yv[i])) + cap(np.hypot(xv[j + 1], yv[i])))
+            assert D[0, i, j] == pytest.approx(expect, abs=1e-12)
+    assert np.allclose(N[0, 0, 0], [0, 0, 1], atol=1e-12)
+    assert np.nanmax(D) <= h                              # the interpolant never exceeds the cap depth
