@@ -148,7 +148,8 @@ typedef struct {
   int32_t n_couplings;           /* last Newton iteration: condensed 3×12 soft–body coupling blocks */
   double lm_mu;                  /* LM shift μ of the last solve (hessian_mode 2; 0 = pure Newton) */
   int32_t n_friction;            /* lagged friction pairs of the last step (the active set at its start xⁿ) */
-  int32_t pad_;
+  int32_t capacity_flags;        /* capacity overflows since tac_batch_create (TAC_ENV_CAPACITY): 1 candidates,
+                                    2 large-primitive list of the broad phase, 4 hash entries, 8 active pairs */
 } tac_env_stats;
 
 struct tac_batch;

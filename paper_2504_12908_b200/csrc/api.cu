@@ -678,7 +678,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.cpl_v = C.take<int>(e * D.cpl_cap + 1); D.cpl_d = C.take<int>(e * D.cpl_cap + 1);
   D.cpl_val = C.take<double>(e * 36 * D.cpl_cap + 1); D.cpl_out = C.take<double>(e * 3 * D.cpl_cap + 1);
   D.srec = C.take<double>(e * 4 * D.act_cap * SREC); D.snb = C.take<int>(e * 4 * D.act_cap * 2);
-  D.sbody = C.take<int>(e * 4 * D.act_cap); D.brec = C.take<double>(e * D.act_cap * 2 * BREC);
+  D.sbody = C.take<int>(e * 4 * D.act_cap); D.brec = C.take<double>((size_t)D.brec_envs * D.act_cap * 2 * BREC);
   D.bpart = C.take<double>(e * (size_t)((D.act_cap + 31) / 32) * std::max(H.ND, 1) * BPART);
   D.qcnt = C.take<int>(e * (size_t)(H.NSV + H.NE) + 1);
   D.qtmp = C.take<int>(e * (size_t)(H.NSV + H.NE) * 2 * 32 + 1);
@@ -714,6 +714,7 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
   D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.bp_margin = cfg->bp_margin; D.K = (double)std::max(cfg->ls_expand, 1);
   D.mu_f = cfg->mu_friction; D.eps_v = cfg->eps_v;
+  D.brec_envs = cfg->hessian_mode == 2 ? 1 : E;
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
   D.elist = nullptr; D.elist_out = nullptr;
   D.NCT = (int)H.ct_tri.size() / 3; D.maxct = 0; D.maxcv = 0;
@@ -1206,7 +1207,7 @@ extern "C" tac_status tac_get_stats(tac_batch* b, tac_env_stats* out, void* stre
     out[e].min_dist = c.min_d2 < b->D.dhat * b->D.dhat ? std::sqrt(c.min_d2) : HUGE_VAL;
     out[e].n_residual = c.n_res; out[e].n_couplings = c.n_cpl;
     out[e].lm_mu = c.mu_used;
-    out[e].n_friction = c.n_fr; out[e].pad_ = 0;
+    out[e].n_friction = c.n_fr; out[e].capacity_flags = c.cap_seen;
   }
   return TAC_OK;
 }

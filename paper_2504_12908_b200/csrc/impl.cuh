@@ -45,6 +45,8 @@ struct EnvCtl {
   double mu_used;         // LM shift of the last solve (hessian_mode 2)
   int fault, pad3_;       // test-only fault injection (tac_debug_inject_fault): env status forced at k_control
   int n_fr, fr_frozen;    // lagged friction pairs of this step (appended after the barrier pairs), frozen at xⁿ
+  int cap_seen, cap_need; // capacity overflows seen since batch creation (bits: 1 candidates, 2 big-target list,
+                          // 4 hash entries, 8 active pairs) and the largest candidate count requested
 };
 
 // ---- env-resident cluster PCG (pcg_cluster.cuh): plan built on the host from the soft BSR pattern ----
@@ -215,7 +217,9 @@ struct Dev {
   double* srec;           // [E][4*act_cap][SREC] per soft slot, vertex-sorted position (k_pairs)
   int* snb;               // [E][4*act_cap][2] BSR block of each soft neighbour record (-1 none)
   int* sbody;             // [E][4*act_cap] DoF body of the coupling record (-1 none / residual)
-  double* brec;           // [E][act_cap][2][BREC] per (pair, DoF body) records (k_pairs, projected envs)
+  double* brec;           // [brec_envs][act_cap][2][BREC] per (pair, DoF body) records (k_pairs, projected envs)
+  int brec_envs;          // E for hessian modes 0/1; 1 for mode 2, where only the one-env debug evaluations
+                          // of the projected Hessian use these records
   double* bpart;          // [E][ceil(act_cap/32)][ND][BPART] per 32-pair chunk body partial sums
   int* cptr;              // [E][V+1] soft contribution lists
   int* clist;             // [E][4*act_cap]

@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     long nc = (long)(h[0] - l[0] + 1) * (h[1] - l[1] + 1) * (h[2] - l[2] + 1);
     if (nc > MAXCELLS) {
       int k = atomicAdd(&nbig_s, 1);
-      if (k < BIG_CAP) big[k] = code; else ovf_s = 1;
+      if (k < BIG_CAP) big[k] = code; else ovf_s |= 2;
       continue;
     }
     for (int x = l[0]; x <= h[0]; ++x)
@@ -407,11 +407,11 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
     }
     __syncthreads();
     if (threadIdx.x == 0) cnt[NBUCKET] = tot;
-    if (tot > D.ent_cap && threadIdx.x == 0) ovf_s = 1;
+    if (tot > D.ent_cap && threadIdx.x == 0) ovf_s |= 4;
     __syncthreads();
   }
   if (ovf_s) {
-    if (threadIdx.x == 0) { C.overflow = 1; C.ncand = 0; }
+    if (threadIdx.x == 0) { C.overflow |= ovf_s; C.cap_seen = ovf_s; C.ncand = 0; }
     return;
   }
   // pass 2: fill entries
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(BROAD_THREADS) k_broad(Dev D, int env0, int sw
   }
   if (threadIdx.x == 0) {
     C.ncand = min(total, D.cand_cap);
-    if (total > D.cand_cap) C.overflow = 1;
+    if (total > D.cand_cap) { C.overflow |= 1; C.cap_seen |= 1; C.cap_need = max(C.cap_need, total); }
   }
 }
 
@@ -608,7 +608,7 @@ __device__ int friction_pairs(const Dev& D, int e, int nbar) {
     for (int i = 0; i < 12; ++i) axb[12 * pos + i] = D.fr_xb[(ea + k) * 12 + i];
   }
   __syncthreads();
-  if (threadIdx.x == 0) { C.n_act = n; if (nbar + nfr > D.act_cap) C.overflow = 1; }
+  if (threadIdx.x == 0) { C.n_act = n; if (nbar + nfr > D.act_cap) { C.overflow |= 8; C.cap_seen |= 8; } }
   __syncthreads();
   return n;
 }
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
     __shared__ double redm[32];
     mind2 = block_min(mind2, redm);
   }
-  if (threadIdx.x == 0) { C.n_act = nact; C.min_d2 = mind2; if (total > D.act_cap) C.overflow = 1; }
+  if (threadIdx.x == 0) { C.n_act = nact; C.min_d2 = mind2; if (total > D.act_cap) { C.overflow |= 8; C.cap_seen |= 8; } }
   __syncthreads();
   if (D.mu_f > 0.0) nact = friction_pairs(D, e, nact);
   // residual pairs (kept matrix-free in the SpMV), ascending
@@ -1096,7 +1096,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
     for (int rb = 0; rb < 2; ++rb) {
       const int bd = rb == 0 ? bd0 : bd1;
       if (bd < 0) break;
-      double* out = D.brec + (((size_t)e * D.act_cap + k) * 2 + rb) * BREC;
+      double* out = D.brec + (((size_t)(e % D.brec_envs) * D.act_cap + k) * 2 + rb) * BREC;
       for (int i = lane; i < BREC; i += 32) {
         double v = 0.0;
         if (i < PH) {
@@ -1150,7 +1150,7 @@ __global__ void k_bpart_proj(Dev D, int env0, int force) {
       if (bd1 >= 0 && bd1 < bd0) { const int tmp = bd0; bd0 = bd1; bd1 = tmp; }
       const int rb = bd0 == d ? 0 : (bd1 == d ? 1 : -1);
       if (rb < 0) continue;
-      const double* rec = D.brec + (((size_t)e * D.act_cap + k) * 2 + rb) * BREC;
+      const double* rec = D.brec + (((size_t)(e % D.brec_envs) * D.act_cap + k) * 2 + rb) * BREC;
       const bool res = ares[k] != 0;
       if (i < 12) sum += rec[PH + i];
       else if (i < 12 + PH) { if (!res) sum += rec[i - 12]; }

@@ -68,7 +68,7 @@ class EnvStats(ctypes.Structure):
                 ("constraint_residual", ctypes.c_double), ("pcg_iters_total", ctypes.c_int64),
                 ("pcg_alg_bytes_total", ctypes.c_double), ("diag", ctypes.c_double * 4),
                 ("min_dist", ctypes.c_double), ("n_residual", ctypes.c_int32), ("n_couplings", ctypes.c_int32),
-                ("lm_mu", ctypes.c_double), ("n_friction", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("lm_mu", ctypes.c_double), ("n_friction", ctypes.c_int32), ("capacity_flags", ctypes.c_int32)]
 
 
 class ChainDesc(ctypes.Structure):

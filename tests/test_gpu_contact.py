@@ -354,7 +354,7 @@ def test_friction_energy_gradient_hvp_parity(name, slide):
     # noise on both sides: they are compared relative to 1e-12 of the total energy instead
     floor = 1e-12 * sum(abs(t) for t in terms.values())
     for i, k in enumerate(En.TERMS):
-        assert abs(et[i] - terms[k]) <= REL * max(abs(terms[k]), floor), (k, et[i], terms[k])
+        assert abs(et[i] - terms[k]) <= max(REL * abs(terms[k]), floor), (k, et[i], terms[k])
     go, H = En.assemble(mod, ctx, x, y, pairs, project=False)
     assert rel_inf(g, go) <= REL
     assert rel_inf(hv, H @ v) <= REL

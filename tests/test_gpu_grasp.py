@@ -71,7 +71,7 @@ def _single_step(sc, mod, ei, b, ykin_dev, k, envs):
         terms = En.energy_terms(mod, ctx, x, y, pairs)
         floor = 1e-12 * sum(abs(t) for t in terms.values())
         for i, name in enumerate(En.TERMS):
-            assert abs(et[i] - terms[name]) <= 1e-9 * max(abs(terms[name]), floor), (k, e, name)
+            assert abs(et[i] - terms[name]) <= max(1e-9 * abs(terms[name]), floor), (k, e, name)
         go, H = En.assemble(mod, ctx, x, y, pairs, project=False)
         rel = lambda a, c: np.abs(a - c).max() / max(np.abs(a).max(), np.abs(c).max())
         assert rel(g, go) <= 1e-9 and rel(hv, H @ vv) <= 1e-9, (k, e)

@@ -93,6 +93,73 @@ def sched(E=8, K=12):
     print("schedule", b.step_schedule(yk[K // 2:]), flush=True)
 
 
+def grasp(name="C4:0", E=256, k_end=30):
+    """Lockstep a grasp workload; on a failure print the env's stats (capacity flags)."""
+    sc = S.make_scene(name)
+    ei = S.env_inputs(sc, np.arange(E), n_steps=k_end)
+    b = T.Batch(sc, E)
+    print("set_state", np.unique(b.set_state(ei.x0, ei.y0), return_counts=True), flush=True)
+    chain = name == "C5"
+    if chain:
+        b.set_chain(S.hand_chain())
+        q = torch.tensor(np.stack([S.hand_script(e, k_end).reshape(k_end, -1) for e in range(E)], 1), device="cuda")
+        yp = np.repeat(S.hand_palm_pose()[None], E, 0)
+    yk = torch.tensor(ei.ykin, device="cuda")
+    for k in range(k_end):
+        if chain:
+            b.set_joint_targets(q[k], base=yp)
+        else:
+            b.set_targets(yk[k])
+        st = b.step(1)
+        ss = b.stats()
+        bad = np.nonzero(st)[0]
+        nc = np.array([s["n_candidates"] for s in ss]); na = np.array([s["n_active"] for s in ss])
+        print(k, "cand max", nc.max(), "active max", na.max(), "newton max", max(s["newton_iters"] for s in ss), "failed", bad[:6], flush=True)
+        for e in bad[:2]:
+            print("   ", e, ss[e], flush=True)
+        if len(bad):
+            break
+
+
+def tail(name="C2", E=1024, k_end=12):
+    """Lockstep steps 0..k_end of `name`; per step the slowest envs' stats; then the oracle traces the
+    slowest env's step from the shared GPU state (per Newton iteration: α, ‖p‖, μ, energies)."""
+    from oracle import mesh as M, solver as SO
+    sc = S.make_scene(name)
+    ei = S.env_inputs(sc, np.arange(E), n_steps=k_end + 1)
+    b = T.Batch(sc, E)
+    b.set_state(ei.x0, ei.y0)
+    yk = torch.tensor(ei.ykin, device="cuda")
+    worst = None
+    for k in range(k_end + 1):
+        x, xd, y, yd = (t.cpu().numpy() for t in b.get_state())
+        b.set_targets(yk[k])
+        st = b.step(1)
+        ss = b.stats()
+        nw = np.array([s["newton_iters"] for s in ss])
+        order = np.argsort(-nw)[:3]
+        print(k, "newton p50 %d max %d" % (np.median(nw), nw.max()), "failed", np.nonzero(st)[0][:5], flush=True)
+        for e in order:
+            s = ss[e]
+            print("   env", e, {kk: s[kk] for kk in ("newton_iters", "pcg_iters", "ls_backtracks", "al_rounds", "alpha_min", "lm_mu", "n_active")}, flush=True)
+        if worst is None or nw.max() > worst[0]:
+            worst = (nw.max(), k, int(order[0]), (x[order[0]], xd[order[0]], y[order[0]], yd[order[0]]))
+    n, k, e, (x, xd, y, yd) = worst
+    print("oracle trace: step", k, "env", e, "GPU newton", n, flush=True)
+    mod = M.prepare(sc)
+    L = M.env_scale(mod, ei.x0[e], ei.y0[e])
+    trace = []
+    ost, ostats = SO.step(mod, SO.State(x.copy(), xd.copy(), y.copy(), yd.copy()), ei.ykin[k, e], L_env=L, trace=trace)
+    print("oracle stats", ostats, flush=True)
+    for t in trace:
+        print("  ", {kk: (round(v, 6) if isinstance(v, float) and abs(v) > 1e-3 else v) for kk, v in t.items()}, flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "capacity"
-    {"capacity": capacity, "c3": c3_fail, "pcg": pcg, "sched": sched}[which]()
+    if which == "tail":
+        tail(*(sys.argv[2:3] or ["C2"]))
+    elif which == "grasp":
+        grasp(*(sys.argv[2:3] or ["C4:0"]))
+    else:
+        {"capacity": capacity, "c3": c3_fail, "pcg": pcg, "sched": sched}[which]()
