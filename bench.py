@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--no-schedule", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phases", action="store_true", help="add the per-phase breakdown to the JSON line")
+    ap.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
+                    help="override a solver constant of the scene config (experiments; recorded in the line)")
     a = ap.parse_args()
     if a.steps is None:
         a.steps = DEFAULTS[a.config][2]
@@ -298,10 +300,13 @@ def _pcts(v):
 class Part:
     """One homogeneous batch of the workload (C4 has one per object shape) on its own CUDA stream."""
 
-    def __init__(self, sc, ids, W, K, dev, chain=False):
+    def __init__(self, sc, ids, W, K, dev, chain=False, overrides=None):
+        import dataclasses
         import torch
         from paper_2504_12908_b200 import scenes as S
         from paper_2504_12908_b200 import taccel as T
+        if overrides:
+            sc.config = dataclasses.replace(sc.config, **overrides)
         self.sc, self.ids, self.E = sc, ids, len(ids)
         self.stream = torch.cuda.Stream(dev)
         self.ei = S.env_inputs(sc, ids, n_steps=W + K)
@@ -363,14 +368,18 @@ def run_config(cfg_name, a, rank, world, dev, envs_total=None, envs_per_gpu=None
         per = envs_per_gpu or DEFAULTS[cfg_name][1]
         ids = np.asarray(list(env_range(rank, world, per)))
     W, K = a.warmup, (steps or a.steps)
+    ov = {}
+    for kv in a.set:
+        k, v = kv.split("=", 1)
+        ov[k] = type(getattr(S.Config(), k))(v)
     if cfg_name == "C4":                   # 8 object shapes, one homogeneous batch each (env id → shape)
         per_shape = max(1, (len(ids) + 7) // 8) if scaling == "strong" else max(1, (envs_per_gpu or DEFAULTS["C4"][1]) // 8)
         groups = {}
         for g in ids:
             groups.setdefault(int((g % (8 * per_shape)) // per_shape), []).append(int(g))
-        parts = [Part(S.make_scene(f"C4:{sh}"), np.asarray(gl), W, K, dev) for sh, gl in sorted(groups.items())]
+        parts = [Part(S.make_scene(f"C4:{sh}"), np.asarray(gl), W, K, dev, overrides=ov) for sh, gl in sorted(groups.items())]
     else:
-        parts = [Part(S.make_scene(cfg_name), ids, W, K, dev, chain=(cfg_name == "C5"))]
+        parts = [Part(S.make_scene(cfg_name), ids, W, K, dev, chain=(cfg_name == "C5"), overrides=ov)]
     E = sum(p.E for p in parts)
     sc = parts[0].sc
     main = torch.cuda.current_stream(dev)
@@ -484,7 +493,7 @@ def run_config(cfg_name, a, rank, world, dev, envs_total=None, envs_per_gpu=None
         for k, v in pr.items():
             m0, n0 = prof.get(k, (0.0, 0))
             prof[k] = (m0 + v[0], n0 + v[1])
-    res = {"cfg": cfg_name, "E_local": E, "n_env_total": n_env_total, "scaling": scaling, "K": K, "W": W, "ms": ms,
+    res = {"cfg": cfg_name, "overrides": ov, "E_local": E, "n_env_total": n_env_total, "scaling": scaling, "K": K, "W": W, "ms": ms,
            "value": value, "dt": dt, "clocks": clk, "fails": fails, "min_dist": float(mins[0]), "n_batches": len(parts),
            "workspace_gb": sum(p.batch.workspace.numel() for p in parts) / 1e9, "pcg_kernel": parts[0].batch.pcg_kernel,
            "prof": prof}
@@ -584,6 +593,7 @@ def main():
         "ms_per_step": r["ms"] / r["K"], "higher_is_better": True, "scaling": r["scaling"], "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[r["cfg"]], "envs_total": r["n_env_total"], "envs_per_gpu": r["E_local"],
+                   "solver_overrides": r["overrides"] or None,
                    "envs": E_note, "dt": r["dt"],
                    "stepping": "lockstep: per step tac_set_targets (device target table) + tac_step + tac_get_gel_deformation "
                                "(device buffers) for every env",

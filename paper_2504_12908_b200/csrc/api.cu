@@ -80,6 +80,10 @@ struct HostT {
   int cl_nc = 0, cl_rpr = 0, cl_threads = 0, cl_nvt = 0, cl_nle_max = 0, cl_nlb_max = 0, cl_cplcap = 0;
   size_t cl_smem_bytes = 0;
   std::vector<int> cl_eptr, cl_edge, cl_bptr, cl_lrptr, cl_blk;   // cl_blk: 2 ints per block
+  // sliced-ELL layout of the row-ordered soft blocks (streamed PCG)
+  std::vector<int> ell_len, ell_cb, ell_col, ell_row;
+  std::vector<long long> ell_vb, ell_pos;
+  size_t ell_total = 0;
 };
 
 // Cluster PCG plan for nc CTAs per env (pcg_cluster.cuh): rows [r·rpr, (r+1)·rpr) on rank r; each rank
@@ -549,6 +553,41 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
   }
   if (H.NT + H.NE >= (1 << 29)) return fail(TAC_E_CAPACITY, "too many primitives");
   choose_cluster(H);
+  // sliced ELL (SELL-32-σ): rows sorted by length (descending, stable), groups of 32 consecutive sorted
+  // rows padded to the group's longest row; ell_row maps a slot to its vertex
+  {
+    const int G = (H.V + 31) / 32;
+    std::vector<int> order(H.V);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return H.rptr[a + 1] - H.rptr[a] > H.rptr[b + 1] - H.rptr[b];
+    });
+    H.ell_row.assign((size_t)32 * G, -1);
+    for (int i = 0; i < H.V; ++i) H.ell_row[i] = order[i];
+    H.ell_pos.assign(H.NNZ, 0);
+    long long vb = 0;
+    int cb = 0;
+    for (int g = 0; g < G; ++g) {
+      int len = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int v = H.ell_row[32 * g + l];
+        if (v >= 0) len = std::max(len, H.rptr[v + 1] - H.rptr[v]);
+      }
+      H.ell_len.push_back(len);
+      H.ell_vb.push_back(vb);
+      H.ell_cb.push_back(cb);
+      for (int j = 0; j < len; ++j)
+        for (int l = 0; l < 32; ++l) {
+          const int v = H.ell_row[32 * g + l];
+          const bool real = v >= 0 && H.rptr[v] + j < H.rptr[v + 1];
+          H.ell_col.push_back(real ? H.rcol[H.rptr[v] + j] : (v >= 0 ? v : 0));
+          if (real) H.ell_pos[H.rptr[v] + j] = vb + (long long)9 * 32 * j + l;
+        }
+      vb += (long long)9 * 32 * len;
+      cb += 32 * len;
+    }
+    H.ell_total = (size_t)vb;
+  }
   return TAC_OK;
 }
 
@@ -645,6 +684,11 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.mark_bary = td(H.mark_bary); D.mark_pad = ti(H.mark_pad); D.pad_mount = ti(H.pad_mount);
   D.pad_T = td(H.pad_T); D.Xrest = td(H.Xrest);
   D.ct_ptr = ti(H.ct_ptr); D.ct_tri = ti(H.ct_tri); D.coat_ptr = ti(H.coat_ptr); D.cam = td(H.cam);
+  {
+    auto tl = [&](const std::vector<long long>& v) { return C.take<long long>(std::max<size_t>(v.size(), 1)); };
+    D.ell_row = ti(H.ell_row); D.ell_len = ti(H.ell_len); D.ell_vb = tl(H.ell_vb); D.ell_cb = ti(H.ell_cb); D.ell_col = ti(H.ell_col);
+    D.ell_pos = tl(H.ell_pos);
+  }
   D.cl.eptr = ti(H.cl_eptr); D.cl.edge = ti(H.cl_edge); D.cl.bptr = ti(H.cl_bptr); D.cl.lrptr = ti(H.cl_lrptr);
   D.cl.blk = reinterpret_cast<const int2*>(ti(H.cl_blk));
   const size_t e = (size_t)E, n = H.n;
@@ -691,6 +735,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
     D.fr_info = C.take<int>(e * fc * 4); D.fr_vid = C.take<int>(e * fc * 4); D.fr_slot = C.take<int>(e * fc * 4);
     D.fr_res = C.take<int>(e * fc); D.fr_xb = C.take<double>(e * fc * 12); D.fr_dat = C.take<double>(e * fc * 16);
   }
+  D.Hell = C.take<double>(D.ell_groups ? e * D.ell_total : 1);
   D.any_active = C.take<int>(1);
   D.act_list = C.take<int>(2 * e);
   return C.off + 256;
@@ -723,6 +768,14 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
     D.maxcv = std::max(D.maxcv, H.coat_ptr[p + 1] - H.coat_ptr[p]);
   }
   D.n_links = 0; D.n_joints = 0;
+  D.ell_total = H.ell_total;
+  // the streamed PCG (envs that do not fit one SM, or TAC_PCG_RESIDENT=0) reads the soft blocks in the
+  // sliced-ELL copy
+  {
+    const char* res = getenv("TAC_PCG_RESIDENT");
+    const bool streamed = (res && atoi(res) == 0) || pcg_r_bytes(D, pcg_r_threads(D.V)) > (size_t)(227 - 4) * 1024;
+    D.ell_groups = streamed ? (int)H.ell_len.size() : 0;
+  }
   D.cl.nc = H.cl_nc; D.cl.rpr = H.cl_rpr; D.cl.threads = H.cl_threads; D.cl.nvt = H.cl_nvt;
   D.cl.nle_max = H.cl_nle_max; D.cl.nlb_max = H.cl_nlb_max; D.cl.cplcap = H.cl_cplcap; D.cl.smem = H.cl_smem_bytes;
 }
@@ -801,6 +854,12 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
   UP(mark_bary); UP(mark_pad); UP(pad_mount); UP(pad_T); UP(Xrest); UP(ct_ptr); UP(ct_tri); UP(coat_ptr); UP(cam);
 #undef UP
+  if (e == cudaSuccess) e = up(D.ell_row, H.ell_row, st);
+  if (e == cudaSuccess) e = up(D.ell_len, H.ell_len, st);
+  if (e == cudaSuccess) e = up(D.ell_vb, H.ell_vb, st);
+  if (e == cudaSuccess) e = up(D.ell_cb, H.ell_cb, st);
+  if (e == cudaSuccess) e = up(D.ell_col, H.ell_col, st);
+  if (e == cudaSuccess) e = up(D.ell_pos, H.ell_pos, st);
   if (e == cudaSuccess) e = up(D.cl.eptr, H.cl_eptr, st);
   if (e == cudaSuccess) e = up(D.cl.edge, H.cl_edge, st);
   if (e == cudaSuccess) e = up(D.cl.bptr, H.cl_bptr, st);

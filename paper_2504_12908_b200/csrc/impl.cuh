@@ -247,6 +247,41 @@ struct Dev {
   const int* elist;       // per launch: env list of this launch (nullptr = env0 + blockIdx)
   int* elist_out;         // per launch: list k_control / k_advance append the next iteration's active envs to
   ClPlan cl;              // cluster PCG plan (cl.nc = 0: not available for this template)
+  // warp-interleaved (sliced ELL) copy of the row-ordered soft blocks for the streamed PCG: rows in groups
+  // of 32 (one warp), group g padded to its longest row; value (slot j, component c, lane l) of group g at
+  // ell_vb[g] + (9j + c)·32 + l, its column at ell_cb[g] + 32j + l — every warp load is 256 contiguous bytes
+  int ell_groups;         // ⌈V/32⌉ (0: no ELL copy)
+  size_t ell_total;       // doubles per env
+  const int* ell_row;     // [32·groups] vertex of each slot (rows sorted by length, −1 padding)
+  const int* ell_len;     // [groups] slots of the group
+  const long long* ell_vb;// [groups] value base (doubles)
+  const int* ell_cb;      // [groups] column base
+  const int* ell_col;     // [Σ 32·len] column vertex (padding: the row itself, value 0)
+  const long long* ell_pos;// [NNZ] value base of row-ordered block q (component c at + 32c)
+  double* Hell;           // [E][ell_total]
 };
+
+// shared-memory bytes of the env-resident k_pcg_r (kernels.cu) for a batch: the host sizes the
+// streamed path's ELL copy by it, the launcher decides which PCG kernel runs
+constexpr int PCG_R_THREADS = 512;   // upper bound; the launch picks pcg_r_threads(V)
+// threads of k_pcg_r: 4 lanes per soft row, as few row passes as fit in 512 threads with the rows
+// split evenly over the passes (C2: V = 288 → 3 passes × 96 rows = 384 threads)
+__host__ __device__ inline int pcg_r_threads(int V) {
+  for (int passes = 1;; ++passes) {
+    const int rows = (V + passes - 1) / passes;
+    const int t = ((4 * rows + 31) / 32) * 32;
+    if (t <= PCG_R_THREADS) return t < 128 ? 128 : t;
+  }
+}
+__host__ __device__ inline size_t pcg_r_ncpl(const Dev& D) {          // coupling bound: ≤ 1 per (v, d)
+  const size_t a = (size_t)D.V * D.ND, b = (size_t)D.cpl_cap;
+  return a < b ? a : b;
+}
+__host__ __device__ inline size_t pcg_r_bytes(const Dev& D, int threads) {
+  const size_t nd = (size_t)(threads / 32) * D.ND * 12 + 1 + 5 * (size_t)D.n + 9 * (size_t)D.NEs +
+                    18 * (size_t)D.V + 288 * (size_t)D.ND + 3 * pcg_r_ncpl(D);
+  const size_t ni = 3 * ((size_t)D.V + 1) + (size_t)D.V + 2 * (size_t)D.NNZ;
+  return nd * sizeof(double) + ni * sizeof(int);
+}
 
 }  // namespace tac

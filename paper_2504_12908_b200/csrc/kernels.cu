@@ -2098,7 +2098,7 @@ struct SmemMat {
 // Returns this thread's partial Σ x_i y_i over the rows it wrote (for fused PCG dot products).
 constexpr int SPMV_ALL = 15;
 __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
-                       double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL, int stream_lpr = 4) {
+                       double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL, int stream_lpr = 4, bool ell = false) {
   const EnvCtl& C = D.ctl[e];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
@@ -2234,6 +2234,38 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
   const double* Hd = R ? R->Hd : D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
   const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
   const int* rptr = R ? R->rptr : D.rptr;
+  // soft rows, streamed operator in sliced-ELL layout (k_pcg after its per-launch conversion): slot s of
+  // the sorted row order, warp = 32 consecutive slots, every block component load is 256 contiguous bytes
+  if (ell && !R) {
+    const double* He = D.Hell + (size_t)e * D.ell_total;
+    const int nslot = 32 * D.ell_groups;
+    for (int s0 = 0; s0 < nslot; s0 += blockDim.x) {
+      const int slot = s0 + threadIdx.x;
+      const int v = slot < nslot ? D.ell_row[slot] : -1;
+      if (v < 0) continue;
+      const int g = slot >> 5, l = slot & 31, len = D.ell_len[g];
+      const double* hb = He + D.ell_vb[g] + l;
+      const int* cb = D.ell_col + D.ell_cb[g] + l;
+      v3 acc = mk(0, 0, 0);
+#pragma unroll 2
+      for (int j = 0; j < len; ++j) {
+        const v3 xu = ld3(x + 3 * cb[32 * j]);
+        const double* B = hb + 288 * j;
+        acc += mk(B[0] * xu.x + B[32] * xu.y + B[64] * xu.z, B[96] * xu.x + B[128] * xu.y + B[160] * xu.z,
+                  B[192] * xu.x + B[224] * xu.y + B[256] * xu.z);
+      }
+      const v3 xv = ld3(x + 3 * v);
+      const size_t V = D.V;
+      acc += mk(Hd[v] * xv.x + Hd[V + v] * xv.y + Hd[2 * V + v] * xv.z,
+                Hd[3 * V + v] * xv.x + Hd[4 * V + v] * xv.y + Hd[5 * V + v] * xv.z,
+                Hd[6 * V + v] * xv.x + Hd[7 * V + v] * xv.y + Hd[8 * V + v] * xv.z);
+      for (int j = cptr[v], j1r = cptr[v] + rcnt[v]; j < j1r; ++j) acc += ld3(sout + 3 * j);
+      for (int j = cpp[v]; j < cpp[v + 1]; ++j) acc += ld3(cout + 3 * j);
+      if (mu != 0.0) acc += (mu * D.mass[v]) * xv;
+      st3(y + 3 * v, acc);
+      xy += xv.x * acc.x + xv.y * acc.y + xv.z * acc.z;
+    }
+  } else
   // soft rows: lpr lanes per row (streamed operator: 4; resident: 1, measured best); lane q of the
   // group takes blocks j = rptr[v]+q, +lpr, ... (adjacent lanes read adjacent 72-byte blocks), then a
   // shuffle reduction; lane q==0 adds the diagonal block and the contiguous pair outputs and stores
@@ -2367,27 +2399,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force,
 }
 
 // shared-memory bytes of k_pcg_r for this batch (0 if the env does not fit one CTA)
-constexpr int PCG_R_THREADS = 512;   // upper bound; the launch picks pcg_r_threads(V)
-// threads of k_pcg_r: 4 lanes per soft row, as few row passes as fit in 512 threads with the rows
-// split evenly over the passes (C2: V = 288 → 3 passes × 96 rows = 384 threads)
-__host__ __device__ inline int pcg_r_threads(int V) {
-  for (int passes = 1;; ++passes) {
-    const int rows = (V + passes - 1) / passes;
-    const int t = ((4 * rows + 31) / 32) * 32;
-    if (t <= PCG_R_THREADS) return t < 128 ? 128 : t;
-  }
-}
-__host__ __device__ inline size_t pcg_r_ncpl(const Dev& D) {          // coupling bound: ≤ 1 per (v, d)
-  const size_t a = (size_t)D.V * D.ND, b = (size_t)D.cpl_cap;
-  return a < b ? a : b;
-}
-__host__ __device__ inline size_t pcg_r_bytes(const Dev& D, int threads) {
-  const size_t nd = (size_t)(threads / 32) * D.ND * 12 + 1 + 5 * (size_t)D.n + 9 * (size_t)D.NEs +
-                    18 * (size_t)D.V + 288 * (size_t)D.ND + 3 * pcg_r_ncpl(D);
-  const size_t ni = 3 * ((size_t)D.V + 1) + (size_t)D.V + 2 * (size_t)D.NNZ;
-  return nd * sizeof(double) + ni * sizeof(int);
-}
-
 // env-resident PCG: one CTA (512 threads) per env with the condensed soft matrix, diagonal and body
 // blocks, preconditioner and index arrays staged once into shared memory; only the (few) residual
 // pairs and the soft–body couplings are read from global memory per iteration
@@ -2462,6 +2473,18 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
   double gp = 0.0;
   bool zero_g = false;
   __shared__ double chol_scratch[144], chol_T[144];
+  // streamed operator: the soft blocks of this env in sliced-ELL layout, once per launch
+  const bool ell = !R && D.ell_groups > 0;
+  if (ell) {
+    double* He = D.Hell + (size_t)e * D.ell_total;
+    const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
+    for (int q = threadIdx.x; q < D.NNZ; q += blockDim.x) {
+      const long long b = D.ell_pos[q];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) He[b + 32 * c] = Ho[9 * (size_t)q + c];
+    }
+    __syncthreads();
+  }
   for (int attempt = 0;; ++attempt) {
     if (attempt > 0) {
       if (R) reinvert_precond(D, e, mu, Rw_Ps, Rw_Pb, chol_scratch, chol_T);      // resident copies
@@ -2487,7 +2510,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
       __syncthreads();
       while (!bad && it < D.max_pcg && rz > stop) {
         CLK_INIT
-        double loc = spmv(D, e, d, Ad, bpart, mu, R, 2 | 4, stream_lpr);
+        double loc = spmv(D, e, d, Ad, bpart, mu, R, 2 | 4, stream_lpr, ell);
         loc = warp_sum(loc);
         if (lane == 0) red[wi] = loc;
         CLK(5)
@@ -2547,7 +2570,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
       }
     }
     while (!R && !fused && !bad && it < D.max_pcg && rz > stop) {
-      spmv(D, e, d, Ad, bpart, mu, R);
+      spmv(D, e, d, Ad, bpart, mu, R, SPMV_ALL, 4, ell);
       CLK_INIT
       part = 0.0;
       for (int i = threadIdx.x; i < n; i += blockDim.x) part += d[i] * Ad[i];
