@@ -386,14 +386,20 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
         H.A_e[eid[{std::min(u, w), std::max(u, w)}]] += a / 3.0;
       }
     }
-    std::vector<double> len;
-    for (auto& e : all_edges) {
+    // hash cell = the median surface edge of the soft pads (the primitives every contact involves), or of
+    // all bodies without pads — a finely tessellated rigid body (the C5 tile) must not shrink the cells
+    // until every link and table face lands in the broad phase's large-primitive list
+    std::vector<double> len, len_soft;
+    for (size_t i = 0; i < all_edges.size(); ++i) {
+      const auto& e = all_edges[i];
       auto d = sub3(&H.vert_xbar[3 * e[1]], &H.vert_xbar[3 * e[0]]);
       H.elen2.push_back(dot3(d, d));
       len.push_back(std::sqrt(dot3(d, d)));
+      if (H.edge_body[i] < ns) len_soft.push_back(len.back());
     }
-    std::sort(len.begin(), len.end());
-    double med = len.empty() ? 1.0 : len[len.size() / 2];
+    std::vector<double>& lsel = len_soft.empty() ? len : len_soft;
+    std::sort(lsel.begin(), lsel.end());
+    double med = lsel.empty() ? 1.0 : lsel[lsel.size() / 2];
     H.cell = std::max(2.0 * cfg->dhat, med);
   }
   // body-pair mask (reading R8)

@@ -17,7 +17,7 @@ namespace tac {
 constexpr int NTHREADS = 256;
 constexpr int NBUCKET = 4096;      // spatial-hash buckets per env (shared memory)
 constexpr int MAXCELLS = 32;       // targets spanning more cells go to the per-env "big" list
-constexpr int BIG_CAP = 2048;
+constexpr int BIG_CAP = 8192;
 constexpr int TETBUF = 90;         // 12 gradient + 78 packed Hessian
 constexpr int PH = 78;
 constexpr int SREC = 66;          // per soft slot record: g 3 | H_ss 9 | coupling 36 | soft neighbours 18
