@@ -121,6 +121,29 @@ def grasp(name="C4:0", E=256, k_end=30):
             break
 
 
+def iters(name="C2", E=1024, k_end=12):
+    """Per Newton iteration of lockstep step k_end: envs still active and host wall ms; phase split of
+    that step (CUDA events)."""
+    sc = S.make_scene(name)
+    ei = S.env_inputs(sc, np.arange(E), n_steps=k_end + 1)
+    b = T.Batch(sc, E)
+    b.set_state(ei.x0, ei.y0)
+    yk = torch.tensor(ei.ykin, device="cuda")
+    for k in range(k_end):
+        b.set_targets(yk[k])
+        b.step(1)
+    b.set_targets(yk[k_end])
+    b.profile(True)
+    b.profile_read(reset=True)
+    b.step(1)
+    prof = b.profile_read(reset=True)
+    act, ms = b.profile_iterations()
+    print("step", k_end, "iterations", len(act), "total ms %.1f" % sum(ms))
+    for i, (a, m) in enumerate(zip(act, ms)):
+        print("  it %3d active %5d  %.3f ms" % (i, a, m))
+    print({k: (round(v[0], 2), v[1]) for k, v in prof.items() if v[1]})
+
+
 def tail(name="C2", E=1024, k_end=12):
     """Lockstep steps 0..k_end of `name`; per step the slowest envs' stats; then the oracle traces the
     slowest env's step from the shared GPU state (per Newton iteration: α, ‖p‖, μ, energies)."""
@@ -159,6 +182,8 @@ if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "capacity"
     if which == "tail":
         tail(*(sys.argv[2:3] or ["C2"]))
+    elif which == "iters":
+        iters(*(sys.argv[2:3] or ["C2"]))
     elif which == "grasp":
         grasp(*(sys.argv[2:3] or ["C4:0"]))
     else:
