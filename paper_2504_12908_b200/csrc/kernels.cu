@@ -2459,11 +2459,12 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
   const double* g = D.g + (size_t)e * n;
   double* const p_out = D.p + (size_t)e * n;
   double *p, *r, *z, *d, *Ad;
-  if (vsm) {
+  if (vsm == 1) {
     double* base = dsmem + ((blockDim.x / 32) * D.ND * 12 + 1);
     p = base; r = base + n; z = base + 2 * n; d = base + 3 * n; Ad = base + 4 * n;
   } else {
     p = p_out; r = D.r + (size_t)e * n; z = D.z + (size_t)e * n; d = D.dd + (size_t)e * n; Ad = D.Ad + (size_t)e * n;
+    if (vsm == 2) d = dsmem + ((blockDim.x / 32) * D.ND * 12 + 1);   // the SpMV's gathered vector on chip
   }
   // hessian_mode 2 (reading R14c): solve (H + μM) p = −g; on negative curvature or a non-descent
   // direction raise μ ← max(μ₀, 10μ), re-invert the block-Jacobi blocks and restart (same launch)
@@ -2603,7 +2604,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     if (D.hmode != 2 || (!bad && (gp < 0.0 || zero_g)) || mu > 1e12) break;
     mu = fmax(D.lm_mu0, 10.0 * mu);
   }
-  if (vsm) {
+  if (vsm == 1) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) p_out[i] = p[i];
     __syncthreads();
     p = p_out;
@@ -3619,8 +3620,10 @@ static PcgPlan pcg_plan(const Dev& D) {
   // of PCG per 4 steps against 5.7 s for the streamed kernel (profiles/r2_c3_pcg_ab.json)
   if (resident && force_cl && D.cl.nc > 0 && cl_fits(D)) return PcgPlan{PCG_CLUSTER, D.cl.threads, D.cl.smem, 1};
   const size_t with_vec = spmv_smem(D) + (size_t)5 * D.n * sizeof(double);
-  const int vsm = with_vec <= 200 * 1024 ? 1 : 0;
-  return PcgPlan{vsm ? PCG_STREAM_VSM : PCG_STREAM, NTHREADS, vsm ? with_vec : spmv_smem(D), lpr};
+  const size_t with_d = spmv_smem(D) + (size_t)D.n * sizeof(double);
+  if (with_vec <= 200 * 1024) return PcgPlan{PCG_STREAM_VSM, NTHREADS, with_vec, lpr};
+  if (with_d <= 110 * 1024) return PcgPlan{PCG_STREAM_D, NTHREADS, with_d, lpr};   // 2 CTAs per SM
+  return PcgPlan{PCG_STREAM, NTHREADS, spmv_smem(D), lpr};
 }
 
 int pcg_path(const Dev& D) { return pcg_plan(D).path; }
@@ -3630,6 +3633,7 @@ const char* pcg_path_name(int path) {
     case PCG_RESIDENT512: return "k_pcg_r512";
     case PCG_STREAM_VSM: return "k_pcg (streamed operator, vectors in shared memory)";
     case PCG_STREAM: return "k_pcg (streamed operator)";
+    case PCG_STREAM_D: return "k_pcg (streamed operator, search direction in shared memory)";
     case PCG_CLUSTER: return "k_pcg_cl";
     default: return "";
   }
@@ -3662,7 +3666,7 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   ensure_smem(k_pcg, cst, pl.bytes);
   static const int sfused = getenv("TAC_PCG_STREAM_FUSED") ? atoi(getenv("TAC_PCG_STREAM_FUSED")) : 1;
   static const int slpr = getenv("TAC_PCG_STREAM_LPR") ? atoi(getenv("TAC_PCG_STREAM_LPR")) : 1;
-  k_pcg<<<ne, NTHREADS, pl.bytes, s>>>(D, env0, force, pl.path == PCG_STREAM_VSM ? 1 : 0, sfused,
+  k_pcg<<<ne, NTHREADS, pl.bytes, s>>>(D, env0, force, pl.path == PCG_STREAM_VSM ? 1 : (pl.path == PCG_STREAM_D ? 2 : 0), sfused,
                                         slpr == 2 || slpr == 4 ? slpr : 1);
 }
 void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s) {

@@ -5,7 +5,7 @@
 
 namespace tac {
 cudaError_t init_tables();
-enum { PCG_RESIDENT = 0, PCG_RESIDENT512 = 1, PCG_STREAM_VSM = 2, PCG_STREAM = 3, PCG_CLUSTER = 4 };
+enum { PCG_RESIDENT = 0, PCG_RESIDENT512 = 1, PCG_STREAM_VSM = 2, PCG_STREAM = 3, PCG_CLUSTER = 4, PCG_STREAM_D = 5 };
 int pcg_path(const Dev& D);                 // which PCG kernel launch_pcg uses for this batch
 const char* pcg_path_name(int path);
 void launch_positions(const Dev& D, int env0, int ne, int with_p, int force, cudaStream_t s);
