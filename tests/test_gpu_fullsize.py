@@ -244,3 +244,21 @@ def test_c3_env_split_bitwise_equal():
     halves = [run(0, 2048), run(2048, E)]
     for j in range(4):
         assert np.array_equal(full[j], np.concatenate([halves[0][j], halves[1][j]]))
+
+
+def test_c2_with_friction_single_steps_from_shared_states():
+    """C2 with lagged friction (μ = 0.5, reading R20; NEXT 1) × 256 envs, lockstep to step 25 (pads
+    squeezing the peg: friction pairs on every pad–peg contact); envs 0 and 255 take step 25 on the GPU and
+    in the oracle from the shared state (friction frozen at that state on both sides)."""
+    import dataclasses
+    sc = S.make_scene("C2")
+    sc.config = dataclasses.replace(sc.config, mu_friction=0.5, eps_v=1e-3)
+    E = 256
+    ei = S.env_inputs(sc, np.arange(E), n_steps=26)
+    b = T.Batch(sc, E)
+    assert (b.set_state(ei.x0, ei.y0) == 0).all()
+    ykin = torch.tensor(ei.ykin, device=torch.device("cuda", 0))
+    mod = M.prepare(sc)
+    _lockstep(b, ykin, 0, 25)
+    assert max(s["n_friction"] for s in b.stats()) > 0
+    _shared_state_step(sc, mod, ei, b, ykin, 25, (0, 255))
