@@ -81,6 +81,38 @@ def pcg():
         print("  argmax", d.argmax(), p_gpu[d.argmax()], p_ref[d.argmax()])
 
 
+def sanity():
+    """Small runs through every kernel family, for compute-sanitizer: C2 lockstep + schedule (resident PCG),
+    C3 one step (streamed PCG with the ELL copy), C1 with friction + depth maps, C5 with device FK."""
+    import dataclasses
+    sched(E=4, K=6)
+    sc = S.make_scene("C3")
+    ei = S.env_inputs(sc, np.arange(2), n_steps=1)
+    b = T.Batch(sc, 2)
+    b.set_state(ei.x0, ei.y0)
+    b.set_targets(ei.ykin[0])
+    print("C3", b.pcg_kernel, b.step(1), flush=True)
+    sc = S.make_scene("C1")
+    sc.config = dataclasses.replace(sc.config, mu_friction=0.5)
+    ei = S.env_inputs(sc, np.arange(2), n_steps=3)
+    b = T.Batch(sc, 2)
+    b.set_state(ei.x0, ei.y0)
+    for k in range(3):
+        b.set_targets(ei.ykin[k])
+        print("C1 friction", b.step(1), flush=True)
+    d, n = b.get_depth_maps(12, 16)
+    print("depth max", float(torch.nan_to_num(d).max()), flush=True)
+    sc = S.make_scene("C5")
+    ei = S.env_inputs(sc, np.arange(2), n_steps=2)
+    b = T.Batch(sc, 2)
+    b.set_state(ei.x0, ei.y0)
+    b.set_chain(S.hand_chain())
+    for k in range(2):
+        q = np.stack([S.hand_script(e, 2)[k].reshape(-1) for e in range(2)])
+        b.set_joint_targets(q, base=np.repeat(S.hand_palm_pose()[None], 2, 0))
+        print("C5", b.step(1), flush=True)
+
+
 def sched(E=8, K=12):
     sc = S.make_scene("C2")
     ei = S.env_inputs(sc, np.arange(E), n_steps=K)
@@ -187,4 +219,4 @@ if __name__ == "__main__":
     elif which == "grasp":
         grasp(*(sys.argv[2:3] or ["C4:0"]))
     else:
-        {"capacity": capacity, "c3": c3_fail, "pcg": pcg, "sched": sched}[which]()
+        {"capacity": capacity, "c3": c3_fail, "pcg": pcg, "sched": sched, "sanity": sanity}[which]()
