@@ -145,8 +145,12 @@ static void choose_cluster(HostT& H) {
   static const int force_nc = getenv("TAC_PCG_CLUSTER") ? atoi(getenv("TAC_PCG_CLUSTER")) : -1;
   H.cl_nc = 0;
   if (force_nc == 0) return;
+  // with the tail split (TAC_PCG_TAIL_NEWTON > 0) the cluster kernel serves single slow envs, so it
+  // should spread an env over several SMs: at least 4 CTAs
+  static const int tail = getenv("TAC_PCG_TAIL_NEWTON") ? atoi(getenv("TAC_PCG_TAIL_NEWTON")) : 0;
   for (int nc : {1, 2, 4, 8, 16}) {
     if (force_nc > 0 && nc != force_nc) continue;
+    if (force_nc <= 0 && tail > 0 && nc < 4) continue;
     if (plan_cluster(H, nc, budget)) {
       if (getenv("TAC_DEBUG_PLAN"))
         fprintf(stderr, "cluster plan: nc=%d rpr=%d threads=%d nle_max=%d nlb_max=%d cplcap=%d smem=%zu\n", H.cl_nc, H.cl_rpr,
@@ -618,7 +622,7 @@ struct tac_batch {
   int device = 0;
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  int* h_flag = nullptr;  // pinned
+  int* h_flag = nullptr;  // pinned [3]
   void* chain_mem = nullptr;                 // forward-kinematics chain (tac_set_chain)
   std::vector<EnvCtl> hctl;
   // tracing
@@ -742,8 +746,8 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
     D.fr_res = C.take<int>(e * fc); D.fr_xb = C.take<double>(e * fc * 12); D.fr_dat = C.take<double>(e * fc * 16);
   }
   D.Hell = C.take<double>(D.ell_groups ? e * D.ell_total : 1);
-  D.any_active = C.take<int>(1);
-  D.act_list = C.take<int>(2 * e);
+  D.any_active = C.take<int>(3);
+  D.act_list = C.take<int>(6 * e);
   return C.off + 256;
 }
 
@@ -774,6 +778,10 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
     D.maxcv = std::max(D.maxcv, H.coat_ptr[p + 1] - H.coat_ptr[p]);
   }
   D.n_links = 0; D.n_joints = 0;
+  {
+    static const int tn = getenv("TAC_PCG_TAIL_NEWTON") ? atoi(getenv("TAC_PCG_TAIL_NEWTON")) : 0;
+    D.tail_newton = tn;
+  }
   D.ell_total = H.ell_total;
   // the streamed PCG (envs that do not fit one SM, or TAC_PCG_RESIDENT=0) reads the soft blocks in the
   // sliced-ELL copy
@@ -874,7 +882,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   b->hctl.assign(n_envs, EnvCtl{});
   for (auto& c : b->hctl) { c.phase = PHASE_IDLE; c.disabled = 1; c.status = ENV_DISABLED; c.L = 1.0; c.rho = cfg->al_rho0; c.Keff = 1.0; }
   if (e == cudaSuccess) e = cudaMemcpyAsync(D.ctl, b->hctl.data(), sizeof(EnvCtl) * n_envs, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMallocHost(&b->h_flag, sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&b->h_flag, 3 * sizeof(int));
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) { delete b; return fail(TAC_E_CUDA, std::string("create: ") + cudaGetErrorString(e)); }
   *out = b;
@@ -1064,23 +1072,36 @@ static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st, c
   { PROF(PH_BROAD_STATIC); launch_broad(D, env0, ne, 0, 0, st); }
   const long max_it = (long)(D.max_newton + 2) * (sc ? sc->nsteps : 1);
   Dev L = D;                              // per-iteration launch copy (active-env list)
-  int n_run = ne, e0 = env0;
+  int n_run = ne, e0 = env0, n_tail = 0, n_bulk = ne;
+  const bool split = compact && D.tail_newton > 0 && tail_pcg_available(D);
+  if (!split) L.tail_newton = 0;
   for (long it = 0; it < max_it; ++it) {
-    L.elist_out = compact ? D.act_list + (size_t)((it + 1) & 1) * D.E : nullptr;
+    const size_t nb = (size_t)((it + 1) & 1) * 3 * D.E;
+    L.elist_out = compact ? D.act_list + nb : nullptr;
     { PROF(PH_POSITIONS); launch_positions(L, e0, n_run, 0, 0, st); }
     { PROF(PH_NARROW); launch_narrow(L, e0, n_run, 0, st); }
     { PROF(PH_TETS); launch_tets(L, e0, n_run, 0, st); }
     { PROF(PH_PAIRS); launch_pairs(L, e0, n_run, 0, st); }
     { PROF(PH_ASSEMBLE); launch_assemble(L, e0, n_run, 0, st); }
-    { PROF(PH_PCG); launch_pcg(L, e0, n_run, 0, st); }
+    if (split && it > 0) {                   // per env: tail envs on the cluster kernel, the rest default
+      const int* cur = L.elist;
+      Dev Lt = L, Lb = L;
+      Lt.elist = cur + D.E;
+      Lb.elist = cur + 2 * (size_t)D.E;
+      if (n_bulk) { PROF(PH_PCG); launch_pcg(Lb, 0, n_bulk, 0, st); }
+      if (n_tail) { PROF(PH_PCG); launch_cluster_pcg(Lt, 0, n_tail, 0, st); }
+    } else {
+      PROF(PH_PCG);
+      launch_pcg(L, e0, n_run, 0, st);
+    }
     { PROF(PH_POSITIONS); launch_positions(L, e0, n_run, 1, 0, st); }
     { PROF(PH_BROAD_SWEPT); launch_broad(L, e0, n_run, 1, 0, st); }
     { PROF(PH_CCD); launch_ccd(L, e0, n_run, 0, st); }
     { PROF(PH_LINESEARCH); launch_linesearch(L, e0, n_run, st); }
-    CUDA_TRY(cudaMemsetAsync(D.any_active, 0, sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(D.any_active, 0, 3 * sizeof(int), st));
     { PROF(PH_CONTROL); launch_control(L, e0, n_run, st); }
     if (sc) { PROF(PH_END); launch_advance(L, e0, n_run, sc->sched, sc->nsteps, sc->oc, sc->om, sc->of, st); }
-    CUDA_TRY(cudaMemcpyAsync(b->h_flag, D.any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(b->h_flag, D.any_active, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
     if (b->prof) prof_flush(b);
@@ -1090,8 +1111,10 @@ static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st, c
     t0 = t1;
     if (!*b->h_flag) break;
     if (compact) {
-      L.elist = D.act_list + (size_t)((it + 1) & 1) * D.E;
-      n_run = *b->h_flag;
+      L.elist = D.act_list + nb;
+      n_run = b->h_flag[0];
+      n_tail = b->h_flag[1];
+      n_bulk = b->h_flag[2];
       e0 = 0;
     }
   }

@@ -242,8 +242,10 @@ struct Dev {
   const int* ch_parent; const double* ch_origin; const double* ch_axis; const int* ch_joint; const double* ch_body;
   const int* ch_kin;      // kinematic index (0..NK-1) of each link's body
   double* ch_base;        // [E][12] base pose per env
-  int* any_active;        // [1] envs still active after k_control (count)
-  int* act_list;          // [2][E] compacted active-env lists (double-buffered by Newton iteration parity)
+  int* any_active;        // [3] envs still active after k_control: total, tail (≥ tail_newton), bulk
+  int tail_newton;        // > 0: envs with at least this many Newton iterations in the step solve with the
+                          // cluster-resident PCG (k_pcg_cl), the others with the default kernel
+  int* act_list;          // [2][3][E] compacted active-env lists (all, tail, bulk), double-buffered by iteration parity
   const int* elist;       // per launch: env list of this launch (nullptr = env0 + blockIdx)
   int* elist_out;         // per launch: list k_control / k_advance append the next iteration's active envs to
   ClPlan cl;              // cluster PCG plan (cl.nc = 0: not available for this template)

@@ -28,7 +28,16 @@ __device__ __forceinline__ int env_at(const Dev& D, int env0, int b) { return D.
 // result depends only on the env) and count it
 __device__ __forceinline__ void mark_active(const Dev& D, int e) {
   const int slot = atomicAdd(D.any_active, 1);
-  if (D.elist_out) D.elist_out[slot] = e;
+  if (D.elist_out) {
+    D.elist_out[slot] = e;
+    // PCG split (per env, from its own history only → batch-independent): envs in the long tail of a
+    // step (≥ tail_newton Newton iterations) solve with the cluster-resident kernel, the rest streamed
+    if (D.tail_newton > 0) {
+      const bool tail = D.ctl[e].newton >= D.tail_newton;
+      const int s2 = atomicAdd(D.any_active + (tail ? 1 : 2), 1);
+      D.elist_out[(size_t)D.E * (tail ? 1 : 2) + s2] = e;
+    }
+  }
 }
 
 // f-factor of the affine Jacobian: column α of J_v is e_{i(α)} scaled by f(α) (1 for t, x̄_j for A_ij)
@@ -3638,6 +3647,17 @@ const char* pcg_path_name(int path) {
     default: return "";
   }
 }
+
+void launch_cluster_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
+  switch (D.cl.nc) {
+    case 1: launch_cl<1>(D, env0, ne, force, s); return;
+    case 2: launch_cl<2>(D, env0, ne, force, s); return;
+    case 4: launch_cl<4>(D, env0, ne, force, s); return;
+    case 8: launch_cl<8>(D, env0, ne, force, s); return;
+    case 16: launch_cl<16>(D, env0, ne, force, s); return;
+  }
+}
+bool tail_pcg_available(const Dev& D) { return D.cl.nc > 1 && cl_fits(D); }
 
 void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   PcgPlan pl = pcg_plan(D);

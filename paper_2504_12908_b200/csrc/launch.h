@@ -15,6 +15,8 @@ void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s);
 void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s);
 void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s);
 void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+void launch_cluster_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s);
+bool tail_pcg_available(const Dev& D);
 void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s);
 void launch_ccd(const Dev& D, int env0, int ne, int force, cudaStream_t s);
 void launch_energy(const Dev& D, int env0, int ne, double alpha, cudaStream_t s);
