@@ -295,6 +295,12 @@ tac_status tac_debug_pcg(tac_batch* b, int32_t env, const double* x, const doubl
  * that step and DISABLED, exactly like a detected failure; other envs are unaffected. */
 tac_status tac_debug_inject_fault(tac_batch* b, int32_t env, int32_t status, void* stream);
 
+/* Newton-iteration trace of one env (diagnostic): rows = NULL, cap > 0 starts tracing env `env` into a
+ * fresh device buffer of cap rows; env < 0 stops; rows != NULL copies min(n, cap) rows and the count n.
+ * Row: [Newton iteration, PCG iterations, μ used, ‖p‖_emb,∞, ‖M⁻¹g‖_emb,∞ (under a shift), gᵀp,
+ *       α (negative = line search failed), E(q), E(q+αp), backtracks]. */
+tac_status tac_debug_trace(tac_batch* b, int32_t env, int32_t cap, double* rows, int32_t* n);
+
 /* Name of the PCG kernel tac_step launches for this batch (env-resident "k_pcg_r"/"k_pcg_r512" when the
  * condensed operator fits one SM's shared memory, else the streamed-operator "k_pcg"). */
 const char* tac_pcg_kernel_name(const tac_batch* b);

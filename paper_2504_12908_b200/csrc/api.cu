@@ -624,6 +624,7 @@ struct tac_batch {
   size_t ws_bytes = 0;
   int* h_flag = nullptr;  // pinned [3]
   void* chain_mem = nullptr;                 // forward-kinematics chain (tac_set_chain)
+  void* trace_mem = nullptr;                 // Newton-iteration trace (tac_debug_trace)
   std::vector<EnvCtl> hctl;
   // tracing
   bool prof = false;
@@ -778,6 +779,7 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
     D.maxcv = std::max(D.maxcv, H.coat_ptr[p + 1] - H.coat_ptr[p]);
   }
   D.n_links = 0; D.n_joints = 0;
+  D.trace = nullptr; D.trace_env = -1; D.trace_cap = 0; D.trace_n = nullptr;
   {
     static const int tn = getenv("TAC_PCG_TAIL_NEWTON") ? atoi(getenv("TAC_PCG_TAIL_NEWTON")) : 0;
     D.tail_newton = tn;
@@ -894,6 +896,7 @@ extern "C" tac_status tac_batch_destroy(tac_batch* b) {
   DevGuard _dg(b->device);
   if (b->h_flag) cudaFreeHost(b->h_flag);
   if (b->chain_mem) cudaFree(b->chain_mem);
+  if (b->trace_mem) cudaFree(b->trace_mem);
   for (auto e : b->ev_pool) cudaEventDestroy(e);
   delete b;
   return TAC_OK;
@@ -1555,6 +1558,30 @@ extern "C" tac_status tac_debug_inject_fault(tac_batch* b, int32_t env, int32_t 
   int v = status;
   CUDA_TRY(cudaMemcpyAsync(&b->D.ctl[env].fault, &v, sizeof(int), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return TAC_OK;
+}
+
+extern "C" tac_status tac_debug_trace(tac_batch* b, int32_t env, int32_t cap, double* rows, int32_t* n) {
+  if (!b || env >= b->D.E || cap < 0) return fail(TAC_E_INVALID, "bad arguments");
+  ON_DEVICE(b);
+  Dev& D = b->D;
+  if (env >= 0 && cap > 0 && !rows) {                    // start tracing env: (re)allocate and reset
+    if (b->trace_mem) { cudaFree(b->trace_mem); b->trace_mem = nullptr; }
+    CUDA_TRY(cudaMalloc(&b->trace_mem, sizeof(double) * 10 * (size_t)cap + 16));
+    D.trace = (double*)b->trace_mem;
+    D.trace_n = (int*)(D.trace + 10 * (size_t)cap);
+    D.trace_cap = cap;
+    D.trace_env = env;
+    CUDA_TRY(cudaMemset(D.trace_n, 0, sizeof(int)));
+    return TAC_OK;
+  }
+  if (env < 0) { D.trace_env = -1; return TAC_OK; }       // stop tracing
+  if (!D.trace) return fail(TAC_E_INVALID, "no trace");
+  int m = 0;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(&m, D.trace_n, sizeof(int), cudaMemcpyDeviceToHost));
+  if (n) *n = m;
+  if (rows) CUDA_TRY(cudaMemcpy(rows, D.trace, sizeof(double) * 10 * std::min(m, cap), cudaMemcpyDeviceToHost));
   return TAC_OK;
 }
 

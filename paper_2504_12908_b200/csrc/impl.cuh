@@ -242,6 +242,11 @@ struct Dev {
   const int* ch_parent; const double* ch_origin; const double* ch_axis; const int* ch_joint; const double* ch_body;
   const int* ch_kin;      // kinematic index (0..NK-1) of each link's body
   double* ch_base;        // [E][12] base pose per env
+  // Newton-iteration trace of one env (tac_debug_trace; test/diagnostic only): rows of
+  // [newton, pcg iterations, μ used, ‖p‖_emb,∞, ‖M⁻¹g‖_emb,∞, gᵀp, α, E(q), E(q+αp), line-search backtracks]
+  double* trace;          // [trace_cap][10]
+  int trace_env, trace_cap;
+  int* trace_n;
   int* any_active;        // [3] envs still active after k_control: total, tail (≥ tail_newton), bulk
   int tail_newton;        // > 0: envs with at least this many Newton iterations in the step solve with the
                           // cluster-resident PCG (k_pcg_cl), the others with the default kernel

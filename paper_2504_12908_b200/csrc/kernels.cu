@@ -2668,6 +2668,14 @@ __device__ void pcg_finish(const Dev& D, int e, double* p, double* red, double m
     C.pcg_bytes += bpi * it_total;
     C.gp = gp;
     C.pnorm = pm;
+    if (e == D.trace_env && D.trace) {                   // diagnostic trace (tac_debug_trace)
+      const int r = *D.trace_n;
+      if (r < D.trace_cap) {
+        double* t = D.trace + 10 * (size_t)r;
+        t[0] = C.newton; t[1] = it_total; t[2] = D.hmode == 2 ? mu : 0.0; t[3] = pm; t[4] = gm; t[5] = gp;
+        t[6] = 0.0; t[7] = 0.0; t[8] = 0.0; t[9] = 0.0;
+      }
+    }
     if (exact_failed) {
       C.xfail = 1;                                        // retry projected next pass (not counted)
     } else {
@@ -2989,6 +2997,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
     C.ls_bt += bt;
     if (!ok) { C.phase = PHASE_FAILED; C.status = ENV_NEWTON_STALL; }
     else { C.alpha_min = fmin(C.alpha_min, alpha); C.alpha = alpha; C.energy = E1; }
+    if (e == D.trace_env && D.trace) {
+      const int r = *D.trace_n;
+      if (r < D.trace_cap) {
+        double* t = D.trace + 10 * (size_t)r;
+        t[6] = ok ? alpha : -alpha; t[7] = E0; t[8] = E1; t[9] = bt;
+        *D.trace_n = r + 1;
+      }
+    }
     C.ls_E0 = E0; C.ls_E1 = E1;
   }
 }

@@ -115,6 +115,7 @@ def load():
             "tac_set_chain": [vp, ctypes.POINTER(ChainDesc)],
             "tac_set_joint_targets": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp],
             "tac_get_targets": [vp, ctypes.c_int32, ctypes.c_int32, vp, vp],
+            "tac_debug_trace": [vp, ctypes.c_int32, ctypes.c_int32, vp, c_int_p],
             "tac_get_depth_maps": [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp, vp],
             "tac_profile_enable": [vp, ctypes.c_int32],
             "tac_profile_read": [vp, c_double_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32],
@@ -412,6 +413,15 @@ class Batch:
         _check(self.lib.tac_debug_pcg(self.handle, env, _ptr(_f64(x)), _ptr(_f64(y)), 1 if exact else 0, float(mu), _ptr(p),
                                       ctypes.byref(it), ctypes.byref(mu_used), self._s()))
         return (p, it.value, mu_used.value) if with_mu else (p, it.value)
+
+    def debug_trace_start(self, env, cap=4096):
+        _check(self.lib.tac_debug_trace(self.handle, env, cap, None, None))
+
+    def debug_trace_read(self, cap=4096):
+        rows = np.zeros((cap, 10))
+        n = ctypes.c_int32()
+        _check(self.lib.tac_debug_trace(self.handle, 0, cap, _ptr(rows), ctypes.byref(n)))
+        return rows[:min(n.value, cap)]
 
     def debug_inject_fault(self, env, status):
         _check(self.lib.tac_debug_inject_fault(self.handle, env, int(status), self._s()))

@@ -81,6 +81,33 @@ def pcg():
         print("  argmax", d.argmax(), p_gpu[d.argmax()], p_ref[d.argmax()])
 
 
+def trace(name="C3", k_end=37, E=4096):
+    """Lockstep to step k_end; run step k_end once to find the slowest env, restore the state, trace that
+    env's Newton iterations while re-running the step."""
+    sc = S.make_scene(name)
+    ei = S.env_inputs(sc, np.arange(E), n_steps=k_end + 1)
+    b = T.Batch(sc, E)
+    b.set_state(ei.x0, ei.y0)
+    yk = torch.tensor(ei.ykin, device="cuda")
+    for k in range(k_end):
+        b.set_targets(yk[k])
+        b.step(1)
+    x, xd, y, yd = b.get_state()
+    b.set_targets(yk[k_end])
+    b.step(1)
+    nw = np.array([s["newton_iters"] for s in b.stats()])
+    e = int(nw.argmax())
+    print("step", k_end, "slowest env", e, "newton", nw[e], "p50", np.median(nw), flush=True)
+    b.set_state(x[e:e + 1], y[e:e + 1], xd[e:e + 1], yd[e:e + 1], env0=e)
+    b.set_targets(yk[k_end][e:e + 1], env0=e)
+    b.debug_trace_start(e, 4096)
+    b.step(1)
+    rows = b.debug_trace_read(4096)
+    print("newton pcg mu p_inf gm gp alpha E0 E1 bt")
+    for r in rows:
+        print(" ".join("%.4g" % v for v in r), flush=True)
+
+
 def sanity():
     """Small runs through every kernel family, for compute-sanitizer: C2 lockstep + schedule (resident PCG),
     C3 one step (streamed PCG with the ELL copy), C1 with friction + depth maps, C5 with device FK."""
@@ -214,6 +241,8 @@ if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "capacity"
     if which == "tail":
         tail(*(sys.argv[2:3] or ["C2"]))
+    elif which == "trace":
+        trace(*(sys.argv[2:3] or ["C3"]), *(int(a) for a in sys.argv[3:4]))
     elif which == "iters":
         iters(*(sys.argv[2:3] or ["C2"]))
     elif which == "grasp":
