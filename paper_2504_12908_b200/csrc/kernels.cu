@@ -3063,6 +3063,15 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
     __syncthreads();
     const bool done = res <= D.tolAL * C.L;
     const int rounds = C.al_rounds + 1;
+    if (threadIdx.x == 0 && e == D.trace_env && D.trace) {   // diagnostic trace row of the AL round end
+      const int r = *D.trace_n;
+      if (r < D.trace_cap) {
+        double* t = D.trace + 10 * (size_t)r;
+        t[0] = -1.0; t[1] = rounds; t[2] = C.rho; t[3] = res; t[4] = D.tolAL * C.L; t[5] = C.newton;
+        t[6] = 0.0; t[7] = 0.0; t[8] = 0.0; t[9] = 0.0;
+        *D.trace_n = r + 1;
+      }
+    }
     __syncthreads();
     if (done) {
       if (threadIdx.x == 0) { C.residual = res; C.al_rounds = rounds; C.phase = PHASE_DONE; C.inner_conv = 0; }
