@@ -41,14 +41,14 @@ METRIC = "peg-insertion env-steps/s and ×real-time, dual sensors, at 1/2/4/8 B2
 WORKLOADS = {
     "C4": "C4: parallel-gripper grasp, dual 40x40x4 mm pads (14x14x3 lattice, 588 nodes/1690 tets each), 8 procedural "
           "star-shaped objects (perturbed level-3 icospheres, 642 v/1280 t; 256 envs per shape, one batch each), "
-          "2 kinematic fingers + static table, dt=0.02 s",
+          "2 kinematic fingers + static table, frictional contact mu=0.5 (lagged D_k), dt=0.02 s",
     "C5": "C5: Allegro-like hand, four 24x24x3 mm fingertip pads (9x9x4 lattice, 324 nodes/960 tets each), palm + 16 "
           "kinematic links driven by on-device forward kinematics of a 16-joint script, dynamic engraved tile "
-          "(16x30x22 mm, 8676 triangles), static table, dt=0.02 s",
+          "(16x30x22 mm, 8676 triangles), static table, frictional contact mu=0.5 (lagged D_k), dt=0.02 s",
     "C2": "C2: peg insertion, dual low-res sensors (2 pads x 8x6x3 lattice, 144 nodes/350 tets each), "
-          "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s",
+          "1 dynamic peg + 2 kinematic fingers + static blind hole, frictional contact mu=0.5 (lagged D_k), dt=0.02 s",
     "C3": "C3: peg insertion, dual high-res sensors (2 pads x 19x16x5 lattice, 1520 nodes/5400 tets each), "
-          "1 dynamic peg + 2 kinematic fingers + static blind hole, dt=0.02 s",
+          "1 dynamic peg + 2 kinematic fingers + static blind hole, frictional contact mu=0.5 (lagged D_k), dt=0.02 s",
 }
 DEFAULTS = {  # config: (scaling, envs, default steps)
     "C3": ("strong", 4096, 10),

@@ -89,10 +89,26 @@ def any_inverted(model: Model, x):
     return bool((np.linalg.det(F) <= 0).any())
 
 
-def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
+def forcing_eta(cfg, rz0, hist):
+    """Relaxed PCG tolerance of one Newton iteration (reading R22; "carefully relaxing convergence
+    tolerances"), Eisenstat–Walker choice 2 with γ = 0.9, α = 2 in the preconditioned gradient norm
+    ‖g‖² = r₀ᵀz₀ of the solve:  η_k = γ·r₀ᵀz₀(k) / r₀ᵀz₀(k−1),  safeguard η_k ≥ γ η_{k−1}² when γ η_{k−1}² > 0.1,
+    clamped to [pcg_eta, pcg_eta_max];  the first solve of a time step uses pcg_eta_max.  hist holds
+    (r₀ᵀz₀, η) of the previous accepted solve of this step, or None."""
+    if hist is None:
+        return cfg.pcg_eta_max
+    rz_prev, eta_prev = hist
+    eta = 0.9 * rz0 / rz_prev
+    if 0.9 * eta_prev * eta_prev > 0.1:
+        eta = max(eta, 0.9 * eta_prev * eta_prev)
+    return min(max(eta, cfg.pcg_eta), cfg.pcg_eta_max)
+
+
+def block_jacobi_pcg(model: Model, H, g, eta, max_iter, info=None):
     """Block-Jacobi PCG for H p = −g from p₀ = 0 (3×3 per soft vertex, 12×12 per body); stop
     at rᵀz ≤ η² r₀ᵀz₀ or max_iter (reading R15; P:L325 names PCG).  Returns (None, it) if a
-    search direction with dᵀHd ≤ 0 is met (H not SPD)."""
+    search direction with dᵀHd ≤ 0 is met (H not SPD).  eta may be a function of r₀ᵀz₀ (the relaxed
+    tolerance of reading R22); info (a dict) receives the r₀ᵀz₀ and η used."""
     n = len(g)
     V = model.V
     blocks = [(3 * v, 3) for v in range(V)] + [(3 * V + 12 * s, 12) for s in range(model.n_dof_bodies)]
@@ -114,6 +130,10 @@ def block_jacobi_pcg(model: Model, H, g, eta, max_iter):
     d = z.copy()
     rz = r @ z
     rz0 = rz
+    if callable(eta):
+        eta = eta(rz0)
+    if info is not None:
+        info["rz0"], info["eta"] = rz0, eta
     it = 0
     while it < max_iter and rz > eta * eta * rz0:
         q = H @ d
@@ -154,7 +174,14 @@ def sweep_factor(cfg, p_inf):
     return K
 
 
-def _solve_spd(model, H, g, solver, cfg, stats):
+def _pcg_eta(cfg, ew):
+    """the PCG tolerance: fixed η (R15), or the relaxed forcing of R22 when pcg_eta_max > 0"""
+    if getattr(cfg, "pcg_eta_max", 0.0) > 0.0:
+        return lambda rz0: forcing_eta(cfg, rz0, ew.get("hist"))
+    return cfg.pcg_eta
+
+
+def _solve_spd(model, H, g, solver, cfg, stats, ew=None):
     """Newton direction from the EXACT Hessian if it is SPD (Cholesky succeeds / CG meets no
     negative curvature) and the direction is a descent direction; None otherwise (reading R14b)."""
     if solver == "direct":
@@ -166,10 +193,13 @@ def _solve_spd(model, H, g, solver, cfg, stats):
         import scipy.linalg as sla
         p = sla.cho_solve((Lc, True), -g)
     else:
-        p, it = block_jacobi_pcg(model, H, g, cfg.pcg_eta, cfg.max_pcg)
+        ew = {} if ew is None else ew
+        info = {}
+        p, it = block_jacobi_pcg(model, H, g, _pcg_eta(cfg, ew), cfg.max_pcg, info)
         stats.pcg_iters += it
         if p is None:
             return None
+        ew["last"] = (info["rz0"], info["eta"])
     if not (g @ p < 0) and np.any(g):
         return None
     return p
@@ -189,6 +219,7 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
     nfail = 0         # consecutive failed exact attempts (back-off 2, 4, ... 64)
     mode = cfg.hessian_mode
     mu = 0.0          # mass-scaled Levenberg-Marquardt shift (hessian_mode 2, reading R14c)
+    ew = {}           # relaxed-tolerance history of this step (reading R22): (r₀ᵀz₀, η) of the last accepted solve
     Mreg = mass_matrix(model) if mode == 2 else None
     for al_round in range(cfg.max_al_rounds):
         stats.al_rounds = al_round + 1
@@ -201,7 +232,7 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
             if mode == 2:
                 g, H = En.assemble(model, ctx, x, y, pairs, project=False)
                 while True:
-                    p = _solve_spd(model, H + mu * Mreg if mu > 0 else H, g, solver, cfg, stats)
+                    p = _solve_spd(model, H + mu * Mreg if mu > 0 else H, g, solver, cfg, stats, ew)
                     if p is not None or mu > 1e12:
                         break
                     mu = max(cfg.lm_mu0, 10.0 * mu)
@@ -209,7 +240,7 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
                 mu = mu * 0.1 if mu * 0.1 >= cfg.lm_mu0 else 0.0
             if mode == 1 and hold == 0:
                 g, H = En.assemble(model, ctx, x, y, pairs, project=False)
-                p = _solve_spd(model, H, g, solver, cfg, stats)
+                p = _solve_spd(model, H, g, solver, cfg, stats, ew)
                 if p is None:
                     nfail += 1
                     hold = min(2 ** nfail, cfg.hold_cap)
@@ -220,10 +251,14 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
                 if solver == "direct":
                     p = spla.spsolve(sp.csc_matrix(H), -g)
                 else:
-                    p, it = block_jacobi_pcg(model, H, g, cfg.pcg_eta, cfg.max_pcg)
+                    info = {}
+                    p, it = block_jacobi_pcg(model, H, g, _pcg_eta(cfg, ew), cfg.max_pcg, info)
                     stats.pcg_iters += it
+                    ew["last"] = (info["rz0"], info["eta"])
                 hold = max(hold - 1, 0)
             stats.newton_iters += 1
+            if "last" in ew:
+                ew["hist"] = ew.pop("last")
             if p is None or not np.all(np.isfinite(p)):
                 stats.status = NONFINITE
                 break

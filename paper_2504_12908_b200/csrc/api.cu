@@ -716,7 +716,8 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.Hb = C.take<double>(e * H.ND * 144 + 1); D.Pinv_s = C.take<double>(e * H.V * 9 + 1);
   D.Pinv_b = C.take<double>(e * H.ND * 144 + 1);
   D.Dg_s = C.take<double>(e * H.V * 9 + 1); D.Dg_b = C.take<double>(e * H.ND * 144 + 1);
-  D.tetbuf = C.take<double>(e * TETBUF * H.T + 1);
+  const size_t ea = (size_t)D.asm_envs;   // assembly scratch (tets → pairs → assemble) for one chunk of envs
+  D.tetbuf = C.take<double>(ea * TETBUF * H.T + 1);
   D.cand_a = C.take<int>(e * D.cand_cap); D.cand_b = C.take<int>(e * D.cand_cap);
   D.ent = C.take<int>(e * D.ent_cap * 2); D.big = C.take<int>(e * BIG_CAP);
   D.tbox = C.take<double>(e * (H.NT + H.NE) * 6);
@@ -732,9 +733,9 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.rcnt = C.take<int>(e * H.V + 1); D.cpl_ptr = C.take<int>(e * (H.V + 1));
   D.cpl_v = C.take<int>(e * D.cpl_cap + 1); D.cpl_d = C.take<int>(e * D.cpl_cap + 1);
   D.cpl_val = C.take<double>(e * 36 * D.cpl_cap + 1); D.cpl_out = C.take<double>(e * 3 * D.cpl_cap + 1);
-  D.srec = C.take<double>(e * 4 * D.act_cap * SREC); D.snb = C.take<int>(e * 4 * D.act_cap * 2);
-  D.sbody = C.take<int>(e * 4 * D.act_cap); D.brec = C.take<double>((size_t)D.brec_envs * D.act_cap * 2 * BREC);
-  D.bpart = C.take<double>(e * (size_t)((D.act_cap + 31) / 32) * std::max(H.ND, 1) * BPART);
+  D.srec = C.take<double>(ea * 4 * D.act_cap * SREC); D.snb = C.take<int>(ea * 4 * D.act_cap * 2);
+  D.sbody = C.take<int>(ea * 4 * D.act_cap); D.brec = C.take<double>((size_t)D.brec_envs * D.act_cap * 2 * BREC);
+  D.bpart = C.take<double>(ea * (size_t)((D.act_cap + 31) / 32) * std::max(H.ND, 1) * BPART);
   D.qcnt = C.take<int>(e * (size_t)(H.NSV + H.NE) + 1);
   D.qtmp = C.take<int>(e * (size_t)(H.NSV + H.NE) * 2 * 32 + 1);
   D.lsl = C.take<int>(e * (size_t)D.cand_cap);
@@ -770,7 +771,14 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
   D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.bp_margin = cfg->bp_margin; D.K = (double)std::max(cfg->ls_expand, 1);
   D.mu_f = cfg->mu_friction; D.eps_v = cfg->eps_v;
-  D.brec_envs = cfg->hessian_mode == 2 ? 1 : E;
+  // assembly scratch in chunks of asm_envs envs (TAC_ASM_CHUNK, default 1024): the per-tet and per-pair
+  // records live only from k_tets / k_pairs* to k_assemble_*, so the Newton loop runs those three phases
+  // chunk by chunk over the envs of the iteration and the scratch is sized for one chunk
+  {
+    static const int chunk = getenv("TAC_ASM_CHUNK") ? std::max(1, atoi(getenv("TAC_ASM_CHUNK"))) : 1024;
+    D.asm_envs = std::max(1, std::min(E, chunk));
+  }
+  D.brec_envs = cfg->hessian_mode == 2 ? 1 : D.asm_envs;
   for (int i = 0; i < 3; ++i) D.grav[i] = sc->gravity[i];
   D.elist = nullptr; D.elist_out = nullptr;
   D.NCT = (int)H.ct_tri.size() / 3; D.maxct = 0; D.maxcv = 0;
@@ -1083,9 +1091,14 @@ static tac_status newton_loop(tac_batch* b, int env0, int ne, cudaStream_t st, c
     L.elist_out = compact ? D.act_list + nb : nullptr;
     { PROF(PH_POSITIONS); launch_positions(L, e0, n_run, 0, 0, st); }
     { PROF(PH_NARROW); launch_narrow(L, e0, n_run, 0, st); }
-    { PROF(PH_TETS); launch_tets(L, e0, n_run, 0, st); }
-    { PROF(PH_PAIRS); launch_pairs(L, e0, n_run, 0, st); }
-    { PROF(PH_ASSEMBLE); launch_assemble(L, e0, n_run, 0, st); }
+    for (int c0 = 0; c0 < n_run; c0 += D.asm_envs) {   // assembly scratch chunks (see fill_dims)
+      Dev Lc = L;
+      if (Lc.elist) Lc.elist += c0;
+      const int m = std::min(D.asm_envs, n_run - c0);
+      { PROF(PH_TETS); launch_tets(Lc, e0 + c0, m, 0, st); }
+      { PROF(PH_PAIRS); launch_pairs(Lc, e0 + c0, m, 0, st); }
+      { PROF(PH_ASSEMBLE); launch_assemble(Lc, e0 + c0, m, 0, st); }
+    }
     if (split && it > 0) {                   // per env: tail envs on the cluster kernel, the rest default
       const int* cur = L.elist;
       Dev Lt = L, Lb = L;

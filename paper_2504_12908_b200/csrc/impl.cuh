@@ -218,6 +218,7 @@ struct Dev {
   int* snb;               // [E][4*act_cap][2] BSR block of each soft neighbour record (-1 none)
   int* sbody;             // [E][4*act_cap] DoF body of the coupling record (-1 none / residual)
   double* brec;           // [brec_envs][act_cap][2][BREC] per (pair, DoF body) records (k_pairs, projected envs)
+  int asm_envs;           // env slots of the assembly scratch (tetbuf, srec/snb/sbody, bpart, brec): one chunk
   int brec_envs;          // E for hessian modes 0/1; 1 for mode 2, where only the one-env debug evaluations
                           // of the projected Hessian use these records
   double* bpart;          // [E][ceil(act_cap/32)][ND][BPART] per 32-pair chunk body partial sums

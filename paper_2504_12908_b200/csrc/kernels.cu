@@ -820,6 +820,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.y);
+  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= D.T) return;
@@ -830,7 +831,7 @@ __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
 #pragma unroll
   for (int i = 0; i < 9; ++i) Dmi[i] = D.Dmi[9 * t + i];
   const double scale = D.dt * D.dt * D.vol[t];
-  double* out = D.tetbuf + (size_t)e * TETBUF * D.T + t;     // SoA [90][T], stored as computed
+  double* out = D.tetbuf + (size_t)sl * TETBUF * D.T + t;     // SoA [90][T], stored as computed
   const size_t T = D.T;
   auto gst = [&](int i, double v) { out[(size_t)i * T] = v; };
   auto hst = [&](int i, double v) { out[(size_t)(12 + i) * T] = v; };
@@ -889,6 +890,7 @@ __device__ __forceinline__ double tri_u2_fast(const double* w, const double* e1,
 // spread over the whole GPU; CTAs past the env's active count exit at once.
 __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.y);
+  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
   if (C.exact) return;                                    // exact Hessians: k_pairs_x (thread per pair)
@@ -1072,7 +1074,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
       int nbt[2] = {-1, -1}, nn = 0;
       for (int t = 0; t < 4; ++t)
         if (t != s && codes[t] >= 0 && nn < 2) nbt[nn++] = t;
-      double* rec = D.srec + ((size_t)e * 4 * D.act_cap + j) * SREC;
+      double* rec = D.srec + ((size_t)sl * 4 * D.act_cap + j) * SREC;
       for (int i = lane; i < SREC; i += 32) {
         double v = 0.0;
         if (i < 3) v = S.gf[3 * s + i];
@@ -1097,15 +1099,15 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
           for (int q = D.rptr[v]; q < D.rptr[v + 1]; ++q)
             if (D.rcol[q] == wv) { jb = q; break; }
         }
-        D.snb[((size_t)e * 4 * D.act_cap + j) * 2 + lane] = jb;
+        D.snb[((size_t)sl * 4 * D.act_cap + j) * 2 + lane] = jb;
       }
-      if (lane == 0) D.sbody[(size_t)e * 4 * D.act_cap + j] = res ? -1 : bd0;
+      if (lane == 0) D.sbody[(size_t)sl * 4 * D.act_cap + j] = res ? -1 : bd0;
     }
     // per DoF body of the pair (ascending, ≤2): packed Σ_{s,t on body} J_sᵀ H_st J_t (78) and Σ_s J_sᵀ g_s (12)
     for (int rb = 0; rb < 2; ++rb) {
       const int bd = rb == 0 ? bd0 : bd1;
       if (bd < 0) break;
-      double* out = D.brec + (((size_t)(e % D.brec_envs) * D.act_cap + k) * 2 + rb) * BREC;
+      double* out = D.brec + (((size_t)(sl % D.brec_envs) * D.act_cap + k) * 2 + rb) * BREC;
       for (int i = lane; i < BREC; i += 32) {
         double v = 0.0;
         if (i < PH) {
@@ -1134,6 +1136,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
 // partial[chunk][d] = Σ over the chunk's 32 pairs in pair order (same layout as k_pairs_x)
 __global__ void k_bpart_proj(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.y);
+  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
   if (C.exact) return;
@@ -1159,13 +1162,13 @@ __global__ void k_bpart_proj(Dev D, int env0, int force) {
       if (bd1 >= 0 && bd1 < bd0) { const int tmp = bd0; bd0 = bd1; bd1 = tmp; }
       const int rb = bd0 == d ? 0 : (bd1 == d ? 1 : -1);
       if (rb < 0) continue;
-      const double* rec = D.brec + (((size_t)(e % D.brec_envs) * D.act_cap + k) * 2 + rb) * BREC;
+      const double* rec = D.brec + (((size_t)(sl % D.brec_envs) * D.act_cap + k) * 2 + rb) * BREC;
       const bool res = ares[k] != 0;
       if (i < 12) sum += rec[PH + i];
       else if (i < 12 + PH) { if (!res) sum += rec[i - 12]; }
       else if (res) sum += rec[i - 12 - PH];
     }
-    D.bpart[(((size_t)e * nchunk + blockIdx.x) * D.ND + d) * BPART + i] = sum;
+    D.bpart[(((size_t)sl * nchunk + blockIdx.x) * D.ND + d) * BPART + i] = sum;
   }
 }
 
@@ -1292,6 +1295,7 @@ __constant__ unsigned char c_colpk[PH];    // column-order position be(be+1)/2+a
 
 __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.y);
+  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
   const EnvCtl& C = D.ctl[e];
   if (!C.exact) return;                                   // projected Hessians: k_pairs (warp Jacobi)
@@ -1529,7 +1533,7 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
           for (int jj = 0; jj < 3; ++jj) q += sg[jj] * HYS(3 * jj + r, lb);
           Q[3 * lb + r] = q;
         }
-      double* rec = D.srec + ((size_t)e * 4 * D.act_cap + j) * SREC;
+      double* rec = D.srec + ((size_t)sl * 4 * D.act_cap + j) * SREC;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         double gg = 0.0;
@@ -1582,13 +1586,13 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
             jb = D.edge_blk[2 * (size_t)(s < 2 ? inf.z : inf.w) + (s & 1)];
           }
         }
-        D.snb[((size_t)e * 4 * D.act_cap + j) * 2 + nb] = jb;
+        D.snb[((size_t)sl * 4 * D.act_cap + j) * 2 + nb] = jb;
       }
       for (int nb = nn; nb < 2; ++nb) {
         for (int i = 0; i < 9; ++i) rec[48 + 9 * nb + i] = 0.0;
-        D.snb[((size_t)e * 4 * D.act_cap + j) * 2 + nb] = -1;
+        D.snb[((size_t)sl * 4 * D.act_cap + j) * 2 + nb] = -1;
       }
-      D.sbody[(size_t)e * 4 * D.act_cap + j] = res ? -1 : bd0;
+      D.sbody[(size_t)sl * 4 * D.act_cap + j] = res ? -1 : bd0;
     }
     }  // live
     // per (32-pair chunk, DoF body) partial sums of the body records, deterministic warp trees:
@@ -1597,7 +1601,7 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
     const size_t chunk = (size_t)kb >> 5;
     for (int d = 0; d < D.ND; ++d) {
       const bool mine = bd0 == d || bd1 == d;
-      double* out = D.bpart + (((size_t)e * nchunk + chunk) * D.ND + d) * BPART;
+      double* out = D.bpart + (((size_t)sl * nchunk + chunk) * D.ND + d) * BPART;
       if (__ballot_sync(0xffffffffu, mine) == 0u) {
         for (int i = lane; i < BPART; i += 32) out[i] = 0.0;
         continue;
@@ -1770,6 +1774,7 @@ __device__ void chol_inverse12_warp(const double* A, double* Ainv, double* L /*1
 constexpr int ASM_SOFT_MAX = 320;
 __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.x);
+  const int sl = blockIdx.x;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
   __shared__ int shs[33];
   __shared__ int next_cv;
@@ -1778,7 +1783,7 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
   const double* q = D.q + (size_t)e * D.n;
   const double* qt = D.qt + (size_t)e * D.n;
   double* g = D.g + (size_t)e * D.n;
-  const double* tb = D.tetbuf + (size_t)e * TETBUF * D.T;
+  const double* tb = D.tetbuf + (size_t)sl * TETBUF * D.T;
   const int* cptr = D.cptr + (size_t)e * (D.V + 1);
   const double dt2 = D.dt * D.dt, rho = C.rho;
   const double* s_att = D.s_att + (size_t)e * D.NC * 3;
@@ -1804,9 +1809,9 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
   double* cval = D.cpl_val + (size_t)e * 36 * D.cpl_cap;
   double* Hoe = D.Ho + (size_t)e * D.NNZ * 9;
   const int* rcnt = D.rcnt + (size_t)e * D.V;
-  const double* srec = D.srec + (size_t)e * 4 * D.act_cap * SREC;
-  const int* snb = D.snb + (size_t)e * 4 * D.act_cap * 2;
-  const int* sbody = D.sbody + (size_t)e * 4 * D.act_cap;
+  const double* srec = D.srec + (size_t)sl * 4 * D.act_cap * SREC;
+  const int* snb = D.snb + (size_t)sl * 4 * D.act_cap * 2;
+  const int* sbody = D.sbody + (size_t)sl * 4 * D.act_cap;
   int* cvl = reinterpret_cast<int*>(dsm_asm);        // [V] soft vertices with contact records
   double* accs = dsm_asm + (D.V + 3) / 2;             // [ngrp][maxrl][9] soft–soft block sums
   int cpl_run = 0, nct = 0;
@@ -1978,6 +1983,7 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
 // pairs' body blocks (k_pairs_x partials) and the 12×12 block-Jacobi inverses
 __global__ void __launch_bounds__(NTHREADS, 2) k_assemble_body(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.x);
+  const int sl = blockIdx.x;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
   __shared__ JacobiScratch JS[NTHREADS / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -2044,7 +2050,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_assemble_body(Dev D, int env0, 
   {
     const int nch = (C.n_act + 31) >> 5;
     const size_t nchunk = (size_t)(D.act_cap + 31) >> 5;
-    const double* bp = D.bpart + (size_t)e * nchunk * D.ND * BPART;
+    const double* bp = D.bpart + (size_t)sl * nchunk * D.ND * BPART;
     for (int t = threadIdx.x; t < D.ND * 156; t += blockDim.x) {
       const int d = t / 156, i = t % 156;
       if (i < 144) {
@@ -3063,14 +3069,33 @@ __global__ void __launch_bounds__(NTHREADS) k_control(Dev D, int env0) {
     __syncthreads();
     const bool done = res <= D.tolAL * C.L;
     const int rounds = C.al_rounds + 1;
-    if (threadIdx.x == 0 && e == D.trace_env && D.trace) {   // diagnostic trace row of the AL round end
+    if (e == D.trace_env && D.trace) {                       // diagnostic trace row of the AL round end
+      __shared__ int arg;                                    // which constraint attains the max residual
+      if (threadIdx.x == 0) arg = -1;
+      __syncthreads();
+      for (int c = threadIdx.x; c < D.NC; c += blockDim.x) {
+        v3 r = ld3(q + 3 * D.att_vert[c]) - ld3(s_att + 3 * c);
+        if (sqrt(dot(r, r)) == res) atomicMax(&arg, c);
+      }
+      for (int i = threadIdx.x; i < D.NKV; i += blockDim.x) {
+        int gv = D.kin_vlist[i], b = D.vert_aff[gv], ki = D.kin_of_body[b], d = D.dof_slot[b];
+        const double* y = q + 3 * D.V + 12 * d;
+        const double* sk = D.s_kin + ((size_t)e * D.NK + ki) * 12;
+        double dy[12];
+        for (int j = 0; j < 12; ++j) dy[j] = y[j] - sk[j];
+        v3 u = embed(dy, ld3(D.vert_xbar + 3 * gv));
+        if (sqrt(dot(u, u)) == res) atomicMax(&arg, (1 << 24) + gv);
+      }
+      __syncthreads();
       const int r = *D.trace_n;
-      if (r < D.trace_cap) {
+      if (threadIdx.x == 0 && r < D.trace_cap) {
         double* t = D.trace + 10 * (size_t)r;
         t[0] = -1.0; t[1] = rounds; t[2] = C.rho; t[3] = res; t[4] = D.tolAL * C.L; t[5] = C.newton;
-        t[6] = 0.0; t[7] = 0.0; t[8] = 0.0; t[9] = 0.0;
+        t[6] = arg >> 24; t[7] = arg & 0xffffff;
+        t[8] = (arg >> 24) ? D.vert_aff[arg & 0xffffff] : (arg >= 0 ? D.att_vert[arg] : -1); t[9] = 0.0;
         *D.trace_n = r + 1;
       }
+      __syncthreads();
     }
     __syncthreads();
     if (done) {

@@ -92,6 +92,7 @@ class Config:
     bp_margin: float = 1.0e-4      # δ of the reusable candidate list (R11b); 0 = rebuild every iteration
     cand_capacity_per_env: int = 65536
     active_capacity_per_env: int = 4096
+    pcg_eta_max: float = 0.0       # relaxed PCG tolerance (reading R22): 0 = fixed η; > 0 = Eisenstat–Walker forcing in [η, η_max]
     mu_friction: float = 0.0       # Coulomb coefficient μ of the lagged friction D_k; 0 = frictionless
     eps_v: float = 1.0e-3          # ε_v (m/s): static/dynamic friction transition of f1 (S:L244 default)
 
@@ -281,11 +282,21 @@ def scene_C1(variant="C1"):
     return Scene(variant, [pad], [base, cube], np.array([0, 0, -9.81]), cfg, n_steps=10)
 
 
+# Coulomb coefficient of the manipulation workloads C2-C5 (reading R23): the paper's E_IPC carries the lagged
+# friction D_k and its peg insertion and grasps rely on it; μ itself is not given
+# (P:L216 calibrates it per object), 0.5 is a typical gel-on-object value.  Without friction a squeezed peg or
+# object has no tangential hold and slides out of the grasp within a step (measured: Newton tails of 100-400
+# iterations on C2/C3).  C1 stays frictionless (its pins are the frictionless closed forms).
+MU_MANIP = 0.5
+
+
 def scene_C2(high_res=False):
     """C2/C3: two pads on two kinematic finger boxes (25x22x6 mm) squeezing a
     dynamic 12x12x60 mm square peg (~3 mm tessellation) that rests on the floor of a static blind
-    hole (40x40x20 mm block, 12.6 mm square hole 15 mm deep, 0.3 mm clearance).  dt = 0.02 s."""
-    cfg = Config(dt=0.02)
+    hole (40x40x20 mm block, 12.6 mm square hole 15 mm deep, 0.3 mm clearance).  dt = 0.02 s, μ = MU_MANIP.
+    Active-pair capacity (barrier + frozen friction pairs): C2 4096, C3 8192 (measured C3 maxima ≈ 2,800
+    barrier pairs, about as many friction pairs)."""
+    cfg = Config(dt=0.02, mu_friction=MU_MANIP, active_capacity_per_env=8192 if high_res else 4096)
     # static block with the hole; top face at z=0
     hw = 6.3 * MM
     xl = _axis_lines([-20 * MM, -hw, hw, 20 * MM], 3.5 * MM)
@@ -389,8 +400,8 @@ def star_object(shape: int):
 def scene_C4(shape: int = 0):
     """C4: parallel gripper — two 40x40x4 mm pads (14x14x3 lattice) on kinematic finger
     boxes (6x44x44 mm) squeeze star object `shape` (dynamic) standing on a static 200x200x20 mm table
-    (top face at z = 0).  dt = 0.02 s."""
-    cfg = Config(dt=0.02)
+    (top face at z = 0).  dt = 0.02 s, μ = MU_MANIP, active-pair capacity 8192."""
+    cfg = Config(dt=0.02, mu_friction=MU_MANIP, active_capacity_per_env=8192)
     tV, tT = box_surface((200 * MM, 200 * MM, 20 * MM), spacing=25 * MM)
     table = AffineBody(tV, tT, kind=STATIC)
     oV, oT = star_object(shape)
@@ -410,6 +421,8 @@ HAND_L = (20 * MM, 25 * MM, 20 * MM, 24 * MM)          # link lengths: proximal,
 HAND_FINGERS = ("thumb", "index", "middle", "ring")
 HAND_APPROACH = {"thumb": (1.0, 0.0), "index": (-1.0, 0.0), "middle": (0.0, -1.0), "ring": (0.0, 1.0)}
 TILE = (16 * MM, 30 * MM, 22 * MM)                     # x (between the engraved faces), y, z
+HAND_PALM_HALF = 7.5 * MM                               # half the palm thickness (finger bases on its bottom face)
+HAND_PAD_LIFT = 2.0 * MM                                # distal-link centre above the tile centre
 
 
 def engraved_tile(seed_shape: int = 0):
@@ -452,8 +465,8 @@ def hand_base_frames():
         R = np.array([[ax, -ay, 0.0], [ay, ax, 0.0], [0.0, 0.0, 1.0]])      # columns: x_l = a, y_l, z_l = up
         face = TILE[0] / 2 if ay == 0 else TILE[1] / 2
         dist = face + 0.2 * MM + 3 * MM + 4 * MM        # tile face, gap, pad thickness, half the distal link
-        c_distal = -dist * np.array([ax, ay, 0.0])      # palm frame origin above the tile centre
-        base = c_distal + np.array([0, 0, L0 + L1 + L2 + L3 / 2])
+        c_distal = -dist * np.array([ax, ay, 0.0])      # horizontal offset from the palm centre
+        base = c_distal + np.array([0, 0, -HAND_PALM_HALF])   # on the palm's bottom face
         out[f] = (base, R)
     return out
 
@@ -501,9 +514,8 @@ def scene_C5():
     """C5: Allegro-like hand — palm (60x60x15 mm) and 4 fingers of 4 kinematic link boxes,
     four fingertip pads (24x24x3 mm, 9x9x4 lattice) on the distal links' inner faces, a dynamic engraved
     tile (16x30x22 mm) standing on a static table.  Bodies: table, tile, palm, 16 links.  dt = 0.02 s."""
-    # the light link boxes (≈2 g) hold the pads against the tile through the AL: a stiffer first penalty
-    # and more rounds than the peg scenes (measured AL_INFEASIBLE at ρ₀ = 1e8 / 8 rounds, step 32)
-    cfg = Config(dt=0.02, al_rho0=1e9, max_al_rounds=12)
+    # μ = MU_MANIP; the engraved faces under four pads need more than 4096 active pairs (measured overflow)
+    cfg = Config(dt=0.02, mu_friction=MU_MANIP, active_capacity_per_env=12288)
     tV, tT = box_surface((200 * MM, 200 * MM, 20 * MM), spacing=25 * MM)
     tileV, tileT = engraved_tile()
     pV, pT = box_surface((60 * MM, 60 * MM, 15 * MM))
@@ -522,8 +534,10 @@ def scene_C5():
 
 
 def hand_palm_pose():
+    """Palm pose: with zero joint angles the distal links (and their pads) are centred HAND_PAD_LIFT above
+    the tile centre, so the 24 mm pads clear the table top and overhang the 22 mm tile at its top."""
     L0, L1, L2, L3 = HAND_L
-    return pose([0, 0, TILE[2] / 2 + 0.08 * MM + L3 / 2 + L2 + L1 + L0 + 7.5 * MM])
+    return pose([0, 0, TILE[2] / 2 + 0.08 * MM + HAND_PAD_LIFT + L3 / 2 + L2 + L1 + L0 + HAND_PALM_HALF])
 
 
 def hand_script(env_id: int, n_steps: int):

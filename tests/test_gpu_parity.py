@@ -3,6 +3,8 @@
 Bars (BASELINE.json north_star): contact-pair sets bit-exact; energies, gradients and
 Hessian-vector products within 1e-9 relative (fp64); positions after each converged step within
 1e-6·L_env."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -34,7 +36,10 @@ def _built():
 
 
 def _perturbed(name, seed, amp=2e-5, press=None):
+    # frictionless operator: these cases check the projected and exact barrier/elastic Hessians and the
+    # PCG on them (friction batches use the exact Hessian only; friction parity: test_gpu_contact.py)
     sc = S.make_scene(name)
+    sc.config = dataclasses.replace(sc.config, mu_friction=0.0)
     mod = M.prepare(sc)
     ei = S.env_inputs(sc, [0], n_steps=1)
     rng = np.random.default_rng(seed)
@@ -304,3 +309,30 @@ def test_streamed_pcg_path_parity():
                         os.path.join(here, "test_gpu_parity.py")], env=env, capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+def test_chunked_assembly_scratch_bitwise():
+    """The assembly scratch (per-tet and per-pair records) is sized for one chunk of envs and the Newton loop
+    runs tets → pairs → assemble chunk by chunk (TAC_ASM_CHUNK).  C2 with 7 envs, 4 lockstep steps: chunks of
+    3 envs (3 launches per phase, compacted env lists split across chunks) must give bitwise the states of
+    the default single chunk."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys, hashlib, numpy as np, torch; sys.path.insert(0, %r)\n"
+            "from paper_2504_12908_b200 import scenes as S, taccel as T\n"
+            "sc = S.make_scene('C2'); ei = S.env_inputs(sc, np.arange(7), n_steps=4)\n"
+            "b = T.Batch(sc, 7); b.set_state(ei.x0, ei.y0)\n"
+            "for k in range(4):\n"
+            "    b.set_targets(ei.ykin[k]); assert (b.step(1) == 0).all()\n"
+            "h = hashlib.sha256(b''.join(t.cpu().numpy().tobytes() for t in b.get_state())).hexdigest()\n"
+            "print(h, sum(s['n_friction'] for s in b.stats()))\n" % os.path.dirname(here))
+    out = []
+    for chunk in ("1024", "3"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, TAC_ASM_CHUNK=chunk),
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr[-3000:]
+        out.append(r.stdout.split())
+    assert out[0][0] == out[1][0], out
+    assert int(out[0][1]) > 0            # the default C2 workload carries frozen friction pairs

@@ -14,6 +14,7 @@ from paper_2504_12908_b200 import taccel as T
 
 
 def run(E=128, k_end=80, al_rounds=None, rho0=None):
+    E, k_end = int(E), int(k_end)
     sc = S.make_scene("C5")
     over = {}
     if al_rounds:

@@ -152,7 +152,11 @@ def study(path, env=0, steps=None):
                 for rot in (False, True):
                     Pc = coarse_basis(mod, agg, nag, rot, x if rot else None)
                     Ac = (Pc.T @ A @ Pc).toarray()
-                    cf = sla.cho_factor(Ac)
+                    try:
+                        cf = sla.cho_factor(Ac)
+                    except np.linalg.LinAlgError:
+                        res[f"{'RB' if rot else 'T'}agg{a}"] = (0, float('nan'))
+                        continue
                     nm = f"{'RB' if rot else 'T'}agg{a}({Pc.shape[1]})"
                     run(nm + "+", lambda r, Pc=Pc, cf=cf: Binv @ r + Pc @ sla.cho_solve(cf, Pc.T @ r))
 
