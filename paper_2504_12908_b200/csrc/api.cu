@@ -61,6 +61,7 @@ struct HostT {
   std::vector<int> rptr, rcol, rblk_ptr, rblk;   // row-ordered symmetric BSR (off-diagonal)
   std::vector<int> rupx;                         // [NNZ] 2·(edge id) + (block stored transposed)
   std::vector<int> eup;                          // [NEs] row-ordered index of the edge's upper block
+  std::vector<int> elo;                          // [NEs] row-ordered index of the edge's lower (transposed) block
   std::vector<int> tri_blk, edge_blk;            // [NT][6], [NE][2] BSR index of (v_i, v_j) within a soft primitive (-1)
   int NNZ = 0;
   std::vector<int> body_kind, dof_slot, dof_body;
@@ -81,8 +82,8 @@ struct HostT {
   size_t cl_smem_bytes = 0;
   std::vector<int> cl_eptr, cl_edge, cl_bptr, cl_lrptr, cl_blk;   // cl_blk: 2 ints per block
   // sliced-ELL layout of the row-ordered soft blocks (streamed PCG)
-  std::vector<int> ell_len, ell_cb, ell_col, ell_row;
-  std::vector<long long> ell_vb, ell_pos;
+  std::vector<int> ell_len, ell_cb, ell_col, ell_row, ell_llen, ell_lcb, ell_lcol;
+  std::vector<long long> ell_vb, ell_pos, ell_lpos;
   size_t ell_total = 0;
 };
 
@@ -464,6 +465,7 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
         H.rcol.push_back(u);
         H.rupx.push_back(2 * sid[{std::min(u, v), std::max(u, v)}] + (u < v ? 1 : 0));
         if (u > v) { H.eup.resize(H.NEs); H.eup[sid[{v, u}]] = (int)H.rcol.size() - 1; }
+        else { H.elo.resize(H.NEs); H.elo[sid[{u, v}]] = (int)H.rcol.size() - 1; }
       }
       H.rptr.push_back((int)H.rcol.size());
     }
@@ -563,38 +565,85 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
   }
   if (H.NT + H.NE >= (1 << 29)) return fail(TAC_E_CAPACITY, "too many primitives");
   choose_cluster(H);
-  // sliced ELL (SELL-32-σ): rows sorted by length (descending, stable), groups of 32 consecutive sorted
-  // rows padded to the group's longest row; ell_row maps a slot to its vertex
+  // symmetric sliced ELL for the streamed PCG (SELL-32, natural row order): only the UPPER off-diagonal
+  // block of each soft edge is stored (value of slot (g, l), entry j, component c at ell_vb[g] + 288j + 32c
+  // + l, its column at ell_cb[g] + 32j + l); row v's lower entries (u < v) read the transposed upper block
+  // of row u through ell_lpos (template).  Natural order keeps the lattice's translation invariance, so the
+  // transposed reads of a warp's 32 consecutive rows hit a few consecutive lanes of one or two groups.
   {
     const int G = (H.V + 31) / 32;
-    std::vector<int> order(H.V);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      return H.rptr[a + 1] - H.rptr[a] > H.rptr[b + 1] - H.rptr[b];
-    });
     H.ell_row.assign((size_t)32 * G, -1);
-    for (int i = 0; i < H.V; ++i) H.ell_row[i] = order[i];
-    H.ell_pos.assign(H.NNZ, 0);
+    for (int i = 0; i < H.V; ++i) H.ell_row[i] = i;
+    H.ell_pos.assign(H.NNZ, -1);
+    auto upper = [&](int v, int j) { return H.rcol[H.rptr[v] + j] > v; };
     long long vb = 0;
     int cb = 0;
-    for (int g = 0; g < G; ++g) {
+    for (int g = 0; g < G; ++g) {                    // upper entries: value layout
       int len = 0;
       for (int l = 0; l < 32; ++l) {
-        const int v = H.ell_row[32 * g + l];
-        if (v >= 0) len = std::max(len, H.rptr[v + 1] - H.rptr[v]);
+        const int v = 32 * g + l;
+        if (v >= H.V) continue;
+        int nu = 0;
+        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j) nu += upper(v, j);
+        len = std::max(len, nu);
       }
       H.ell_len.push_back(len);
       H.ell_vb.push_back(vb);
       H.ell_cb.push_back(cb);
+      std::vector<int> k(32, 0);
+      std::vector<std::vector<int>> cols(32, std::vector<int>(len, -1));
+      for (int l = 0; l < 32; ++l) {
+        const int v = 32 * g + l;
+        if (v >= H.V) continue;
+        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j)
+          if (upper(v, j)) {
+            H.ell_pos[H.rptr[v] + j] = vb + (long long)288 * k[l] + l;
+            cols[l][k[l]++] = H.rcol[H.rptr[v] + j];
+          }
+      }
       for (int j = 0; j < len; ++j)
         for (int l = 0; l < 32; ++l) {
-          const int v = H.ell_row[32 * g + l];
-          const bool real = v >= 0 && H.rptr[v] + j < H.rptr[v + 1];
-          H.ell_col.push_back(real ? H.rcol[H.rptr[v] + j] : (v >= 0 ? v : 0));
-          if (real) H.ell_pos[H.rptr[v] + j] = vb + (long long)9 * 32 * j + l;
+          const int v = 32 * g + l;
+          H.ell_col.push_back(cols[l][j] >= 0 ? cols[l][j] : (v < H.V ? v : 0));
         }
-      vb += (long long)9 * 32 * len;
+      vb += (long long)288 * len;
       cb += 32 * len;
+    }
+    const long long zero = vb;                       // one all-zero block for the lower padding
+    vb += 288;
+    int lcb = 0;
+    for (int g = 0; g < G; ++g) {                    // lower entries: transposed reads of upper blocks
+      int len = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int v = 32 * g + l;
+        if (v >= H.V) continue;
+        int nl = 0;
+        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j) nl += !upper(v, j);
+        len = std::max(len, nl);
+      }
+      H.ell_llen.push_back(len);
+      H.ell_lcb.push_back(lcb);
+      std::vector<std::vector<std::pair<int, long long>>> ent(32);
+      for (int l = 0; l < 32; ++l) {
+        const int v = 32 * g + l;
+        if (v >= H.V) continue;
+        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j)
+          if (!upper(v, j)) {
+            const int u = H.rcol[H.rptr[v] + j];
+            long long pu = -1;                       // the upper block (u, v) in row u
+            for (int q = H.rptr[u]; q < H.rptr[u + 1]; ++q)
+              if (H.rcol[q] == v) pu = H.ell_pos[q];
+            ent[l].push_back({u, pu});
+          }
+      }
+      for (int j = 0; j < len; ++j)
+        for (int l = 0; l < 32; ++l) {
+          const int v = 32 * g + l;
+          const bool real = j < (int)ent[l].size();
+          H.ell_lcol.push_back(real ? ent[l][j].first : (v < H.V ? v : 0));
+          H.ell_lpos.push_back(real ? ent[l][j].second : zero);
+        }
+      lcb += 32 * len;
     }
     H.ell_total = (size_t)vb;
   }
@@ -681,7 +730,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.tets = ti(H.tets); D.Dmi = td(H.Dmi); D.vol = td(H.vol); D.mu = td(H.mu); D.lam = td(H.lam); D.mass = td(H.mass);
   D.sedge = ti(H.sedge); D.vadj_ptr = ti(H.vadj_ptr); D.vadj = ti(H.vadj); D.vdiag_ptr = ti(H.vdiag_ptr);
   D.vdiag = ti(H.vdiag); D.eblk_ptr = ti(H.eblk_ptr); D.eblk = ti(H.eblk);
-  D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rupx = ti(H.rupx); D.eup = ti(H.eup); D.tri_blk = ti(H.tri_blk); D.edge_blk = ti(H.edge_blk); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
+  D.rptr = ti(H.rptr); D.rcol = ti(H.rcol); D.rupx = ti(H.rupx); D.eup = ti(H.eup); D.elo = ti(H.elo); D.tri_blk = ti(H.tri_blk); D.edge_blk = ti(H.edge_blk); D.rblk_ptr = ti(H.rblk_ptr); D.rblk = ti(H.rblk);
   D.body_kind = ti(H.body_kind); D.dof_slot = ti(H.dof_slot); D.dof_body = ti(H.dof_body); D.My = td(H.My); D.MyInv = td(H.MyInv);
   D.bmass = td(H.bmass); D.bs1 = td(H.bs1); D.bvol = td(H.bvol); D.bkappa = td(H.bkappa);
   D.vert_body = ti(H.vert_body); D.vert_aff = ti(H.vert_aff); D.vert_xbar = td(H.vert_xbar);
@@ -699,6 +748,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
     auto tl = [&](const std::vector<long long>& v) { return C.take<long long>(std::max<size_t>(v.size(), 1)); };
     D.ell_row = ti(H.ell_row); D.ell_len = ti(H.ell_len); D.ell_vb = tl(H.ell_vb); D.ell_cb = ti(H.ell_cb); D.ell_col = ti(H.ell_col);
     D.ell_pos = tl(H.ell_pos);
+    D.ell_llen = ti(H.ell_llen); D.ell_lcb = ti(H.ell_lcb); D.ell_lcol = ti(H.ell_lcol); D.ell_lpos = tl(H.ell_lpos);
   }
   D.cl.eptr = ti(H.cl_eptr); D.cl.edge = ti(H.cl_edge); D.cl.bptr = ti(H.cl_bptr); D.cl.lrptr = ti(H.cl_lrptr);
   D.cl.blk = reinterpret_cast<const int2*>(ti(H.cl_blk));
@@ -712,7 +762,8 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.s_kin = C.take<double>(e * H.NK * 12 + 1); D.lam_kin = C.take<double>(e * H.NK * 12 + 1);
   D.ykin = C.take<double>(e * H.NK * 12 + 1);
   D.P = C.take<double>(e * H.NVall * 3); D.Pd = C.take<double>(e * H.NVall * 3);
-  D.Hd = C.take<double>(e * H.V * 9 + 1); D.Ho = C.take<double>(e * H.NNZ * 9 + 1);
+  D.Hd = C.take<double>(e * H.V * 9 + 1);
+  D.Ho = C.take<double>(D.asm_ell ? 1 : e * H.NNZ * 9 + 1);   // row-ordered soft blocks (not kept when asm_ell)
   D.Hb = C.take<double>(e * H.ND * 144 + 1); D.Pinv_s = C.take<double>(e * H.V * 9 + 1);
   D.Pinv_b = C.take<double>(e * H.ND * 144 + 1);
   D.Dg_s = C.take<double>(e * H.V * 9 + 1); D.Dg_b = C.take<double>(e * H.ND * 144 + 1);
@@ -799,6 +850,10 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
     const char* res = getenv("TAC_PCG_RESIDENT");
     const bool streamed = (res && atoi(res) == 0) || pcg_r_bytes(D, pcg_r_threads(D.V)) > (size_t)(227 - 4) * 1024;
     D.ell_groups = streamed ? (int)H.ell_len.size() : 0;
+    // the assembly writes the soft blocks straight into the sliced-ELL layout (no row-ordered copy, no
+    // per-launch conversion in k_pcg) unless a cluster PCG (which reads the row-ordered blocks) may run
+    const char* cl = getenv("TAC_PCG_CLUSTER");
+    D.asm_ell = D.ell_groups > 0 && !(cl && atoi(cl) > 0) && D.tail_newton == 0 ? 1 : 0;
   }
   D.cl.nc = H.cl_nc; D.cl.rpr = H.cl_rpr; D.cl.threads = H.cl_threads; D.cl.nvt = H.cl_nvt;
   D.cl.nle_max = H.cl_nle_max; D.cl.nlb_max = H.cl_nlb_max; D.cl.cplcap = H.cl_cplcap; D.cl.smem = H.cl_smem_bytes;
@@ -872,7 +927,7 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, need, st);
 #define UP(f) if (e == cudaSuccess) e = up(D.f, H.f, st)
   UP(tets); UP(Dmi); UP(vol); UP(mu); UP(lam); UP(mass); UP(sedge); UP(vadj_ptr); UP(vadj); UP(vdiag_ptr); UP(vdiag);
-  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(eup); UP(tri_blk); UP(edge_blk); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(MyInv); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
+  UP(eblk_ptr); UP(eblk); UP(rptr); UP(rcol); UP(rupx); UP(eup); UP(elo); UP(tri_blk); UP(edge_blk); UP(rblk_ptr); UP(rblk); UP(body_kind); UP(dof_slot); UP(dof_body); UP(My); UP(MyInv); UP(bmass); UP(bs1); UP(bvol); UP(bkappa);
   UP(vert_body); UP(vert_aff); UP(vert_xbar); UP(sverts); UP(body_sv_ptr); UP(tris); UP(tri_body); UP(edges); UP(edge_body);
   UP(A_v); UP(A_e); UP(elen2); UP(allowed); UP(att_vert); UP(att_body); UP(att_local); UP(att_of_vert);
   UP(kin_body); UP(kin_of_body); UP(affv_list); UP(kin_vlist); UP(coat_vert); UP(coat_pad); UP(mark_tri);
@@ -884,6 +939,10 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (e == cudaSuccess) e = up(D.ell_cb, H.ell_cb, st);
   if (e == cudaSuccess) e = up(D.ell_col, H.ell_col, st);
   if (e == cudaSuccess) e = up(D.ell_pos, H.ell_pos, st);
+  if (e == cudaSuccess) e = up(D.ell_llen, H.ell_llen, st);
+  if (e == cudaSuccess) e = up(D.ell_lcb, H.ell_lcb, st);
+  if (e == cudaSuccess) e = up(D.ell_lcol, H.ell_lcol, st);
+  if (e == cudaSuccess) e = up(D.ell_lpos, H.ell_lpos, st);
   if (e == cudaSuccess) e = up(D.cl.eptr, H.cl_eptr, st);
   if (e == cudaSuccess) e = up(D.cl.edge, H.cl_edge, st);
   if (e == cudaSuccess) e = up(D.cl.bptr, H.cl_bptr, st);

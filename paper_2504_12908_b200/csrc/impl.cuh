@@ -122,6 +122,7 @@ struct Dev {
   const int* tri_blk;     // [NT][6] BSR index of (v_i, v_j) of a soft triangle, ordered pairs (0,1),(0,2),(1,0),(1,2),(2,0),(2,1)
   const int* edge_blk;    // [NE][2] BSR index of (v0, v1), (v1, v0) of a soft edge
   const int* eup;         // [NEs] row-ordered index of each soft edge's upper block (i < j, row i)
+  const int* elo;         // [NEs] row-ordered index of each soft edge's lower block (row j, the transpose)
   const int* rupx;        // [NNZ] 2·(soft edge id) + 1 if the block is the transpose of the edge's upper block
   const int* rblk_ptr;    // [NNZ+1]
   const int* rblk;        // entries 16*tet + 4*a + b (a ↔ row, b ↔ column)
@@ -218,6 +219,7 @@ struct Dev {
   int* snb;               // [E][4*act_cap][2] BSR block of each soft neighbour record (-1 none)
   int* sbody;             // [E][4*act_cap] DoF body of the coupling record (-1 none / residual)
   double* brec;           // [brec_envs][act_cap][2][BREC] per (pair, DoF body) records (k_pairs, projected envs)
+  int asm_ell;            // 1: the assembly writes the soft off-diagonal blocks into Hell (sliced ELL) only
   int asm_envs;           // env slots of the assembly scratch (tetbuf, srec/snb/sbody, bpart, brec): one chunk
   int brec_envs;          // E for hessian modes 0/1; 1 for mode 2, where only the one-env debug evaluations
                           // of the projected Hessian use these records
@@ -260,12 +262,16 @@ struct Dev {
   // ell_vb[g] + (9j + c)·32 + l, its column at ell_cb[g] + 32j + l — every warp load is 256 contiguous bytes
   int ell_groups;         // ⌈V/32⌉ (0: no ELL copy)
   size_t ell_total;       // doubles per env
-  const int* ell_row;     // [32·groups] vertex of each slot (rows sorted by length, −1 padding)
+  const int* ell_row;     // [32·groups] vertex of each slot (natural order, −1 padding)
   const int* ell_len;     // [groups] slots of the group
   const long long* ell_vb;// [groups] value base (doubles)
   const int* ell_cb;      // [groups] column base
   const int* ell_col;     // [Σ 32·len] column vertex (padding: the row itself, value 0)
-  const long long* ell_pos;// [NNZ] value base of row-ordered block q (component c at + 32c)
+  const long long* ell_pos;// [NNZ] value base of row-ordered block q if it is an upper block (u > v), else −1
+  const int* ell_llen;    // [groups] lower entries of the group (rows' neighbours u < v)
+  const int* ell_lcb;     // [groups] base of the group's lower columns / positions
+  const int* ell_lcol;    // [Σ 32·llen] column u of lower entry j of slot l (padding: the row itself)
+  const long long* ell_lpos;// [Σ 32·llen] value base of the upper block (u, v) read transposed (padding: a zero block)
   double* Hell;           // [E][ell_total]
 };
 

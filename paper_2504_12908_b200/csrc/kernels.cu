@@ -1789,16 +1789,32 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
   const double* s_att = D.s_att + (size_t)e * D.NC * 3;
   const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
   CLK_INIT
-  // ---- soft edge blocks (elastic) ----
-  for (int ei = threadIdx.x; ei < D.NNZ; ei += blockDim.x) {
+  // ---- soft edge blocks (elastic): one thread per edge {i < j} sums the tets' (i, j) blocks once and
+  // stores the upper block (row i) and its transpose (row j) — into the sliced-ELL copy the streamed PCG
+  // reads (asm_ell) or the row-ordered blocks ----
+  double* const He = D.asm_ell ? D.Hell + (size_t)e * D.ell_total : nullptr;
+  for (int ei = threadIdx.x; ei < D.NEs; ei += blockDim.x) {
     double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = D.rblk_ptr[ei]; j < D.rblk_ptr[ei + 1]; ++j) {
-      int ent = D.rblk[j], t = ent >> 4, a = (ent >> 2) & 3, b = ent & 3;
+    for (int j = D.eblk_ptr[ei]; j < D.eblk_ptr[ei + 1]; ++j) {
+      int ent = D.eblk[j], t = ent >> 4, a = (ent >> 2) & 3, b = ent & 3;
+#pragma unroll
       for (int r = 0; r < 3; ++r)
+#pragma unroll
         for (int c = 0; c < 3; ++c) B[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * b + c, 12)) * D.T + t];
     }
-    double* ho = D.Ho + ((size_t)e * D.NNZ + ei) * 9;
-    for (int i = 0; i < 9; ++i) ho[i] = B[i];
+    const int qu = D.eup[ei], ql = D.elo[ei];
+    if (He) {                                           // symmetric sliced ELL: the upper block only
+      double* hu = He + D.ell_pos[qu];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) hu[32 * i] = B[i];
+    } else {
+      double* hu = D.Ho + ((size_t)e * D.NNZ + qu) * 9;
+      double* hl = D.Ho + ((size_t)e * D.NNZ + ql) * 9;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { hu[3 * r + c] = B[3 * r + c]; hl[3 * c + r] = B[3 * r + c]; }
+    }
   }
   __syncthreads();
   CLK(10)
@@ -1944,19 +1960,22 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
           }
         for (unsigned m = touched; m; m &= m - 1u) {
           const int sl = __ffs(m) - 1;
-          double* hb = Hoe + (size_t)(r0 + sl) * 9;
-          hb[l8] += acc[9 * sl + l8];
-          if (l8 == 0) hb[8] += acc[9 * sl + 8];
+          if (He && D.ell_pos[r0 + sl] < 0) continue;     // lower block: its transpose is summed by row u
+          const int hs = He ? 32 : 1;                     // element stride of the block's storage
+          double* hb = He ? He + D.ell_pos[r0 + sl] : Hoe + (size_t)(r0 + sl) * 9;
+          hb[hs * l8] += acc[9 * sl + l8];
+          if (l8 == 0) hb[hs * 8] += acc[9 * sl + 8];
         }
       } else {
         for (int j = jr; j < j1; ++j)
           for (int nb = 0; nb < 2; ++nb) {
             const int jb = snb[2 * j + nb];
-            if (jb < 0) continue;
-            double* hb = Hoe + (size_t)jb * 9;
+            if (jb < 0 || (He && D.ell_pos[jb] < 0)) continue;
+            const int hs = He ? 32 : 1;
+            double* hb = He ? He + D.ell_pos[jb] : Hoe + (size_t)jb * 9;
             const double* rec = srec + (size_t)j * SREC + 48 + 9 * nb;
-            hb[l8] += rec[l8];
-            if (l8 == 0) hb[8] += rec[8];
+            hb[hs * l8] += rec[l8];
+            if (l8 == 0) hb[hs * 8] += rec[8];
           }
       }
     }
@@ -2249,8 +2268,9 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
   const double* Hd = R ? R->Hd : D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
   const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
   const int* rptr = R ? R->rptr : D.rptr;
-  // soft rows, streamed operator in sliced-ELL layout (k_pcg after its per-launch conversion): slot s of
-  // the sorted row order, warp = 32 consecutive slots, every block component load is 256 contiguous bytes
+  // soft rows, streamed operator in the symmetric sliced-ELL layout (written by the assembly, or converted
+  // once per k_pcg launch): warp = 32 consecutive rows, every upper-block component load is 256 contiguous
+  // bytes; the lower entries read the transposed upper blocks of the neighbouring rows
   if (ell && !R) {
     const double* He = D.Hell + (size_t)e * D.ell_total;
     const int nslot = 32 * D.ell_groups;
@@ -2268,6 +2288,17 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
         const double* B = hb + 288 * j;
         acc += mk(B[0] * xu.x + B[32] * xu.y + B[64] * xu.z, B[96] * xu.x + B[128] * xu.y + B[160] * xu.z,
                   B[192] * xu.x + B[224] * xu.y + B[256] * xu.z);
+      }
+      // lower neighbours u < v: the upper block (u, v) of row u, transposed
+      const int llen = D.ell_llen[g];
+      const int* lc = D.ell_lcol + D.ell_lcb[g] + l;
+      const long long* lp = D.ell_lpos + D.ell_lcb[g] + l;
+#pragma unroll 2
+      for (int j = 0; j < llen; ++j) {
+        const v3 xu = ld3(x + 3 * lc[32 * j]);
+        const double* B = He + lp[32 * j];
+        acc += mk(B[0] * xu.x + B[96] * xu.y + B[192] * xu.z, B[32] * xu.x + B[128] * xu.y + B[224] * xu.z,
+                  B[64] * xu.x + B[160] * xu.y + B[256] * xu.z);
       }
       const v3 xv = ld3(x + 3 * v);
       const size_t V = D.V;
@@ -2491,11 +2522,12 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
   __shared__ double chol_scratch[144], chol_T[144];
   // streamed operator: the soft blocks of this env in sliced-ELL layout, once per launch
   const bool ell = !R && D.ell_groups > 0;
-  if (ell) {
+  if (ell && !D.asm_ell) {                    // row-ordered blocks → sliced ELL (when the assembly did not)
     double* He = D.Hell + (size_t)e * D.ell_total;
     const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
     for (int q = threadIdx.x; q < D.NNZ; q += blockDim.x) {
       const long long b = D.ell_pos[q];
+      if (b < 0) continue;                         // lower block: read transposed from the upper copy
 #pragma unroll
       for (int c = 0; c < 9; ++c) He[b + 32 * c] = Ho[9 * (size_t)q + c];
     }
@@ -2705,7 +2737,7 @@ namespace tac {
 __global__ void __launch_bounds__(NTHREADS) k_spmv(Dev D, int env0, const double* x, double* y) {
   const int e = env_at(D, env0, blockIdx.x);
   extern __shared__ double part[];
-  spmv(D, e, x, y, part);
+  spmv(D, e, x, y, part, 0.0, nullptr, SPMV_ALL, 4, D.asm_ell != 0);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -3733,11 +3765,11 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
                  with_vec <= 200 * 1024 ? with_vec : spmv_smem(D), pl.lpr};
   }
   static size_t cst[MAX_DEVICES] = {};
-  ensure_smem(k_pcg, cst, pl.bytes);
   static const int sfused = getenv("TAC_PCG_STREAM_FUSED") ? atoi(getenv("TAC_PCG_STREAM_FUSED")) : 1;
   static const int slpr = getenv("TAC_PCG_STREAM_LPR") ? atoi(getenv("TAC_PCG_STREAM_LPR")) : 1;
-  k_pcg<<<ne, NTHREADS, pl.bytes, s>>>(D, env0, force, pl.path == PCG_STREAM_VSM ? 1 : (pl.path == PCG_STREAM_D ? 2 : 0), sfused,
-                                        slpr == 2 || slpr == 4 ? slpr : 1);
+  const int vsm = pl.path == PCG_STREAM_VSM ? 1 : (pl.path == PCG_STREAM_D ? 2 : 0), lpr = slpr == 2 || slpr == 4 ? slpr : 1;
+  ensure_smem(k_pcg, cst, pl.bytes);
+  k_pcg<<<ne, NTHREADS, pl.bytes, s>>>(D, env0, force, vsm, sfused, lpr);
 }
 void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s) {
   k_spmv<<<1, NTHREADS, spmv_smem(D), s>>>(D, env0, x, y);

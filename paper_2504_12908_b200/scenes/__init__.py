@@ -514,8 +514,9 @@ def scene_C5():
     """C5: Allegro-like hand — palm (60x60x15 mm) and 4 fingers of 4 kinematic link boxes,
     four fingertip pads (24x24x3 mm, 9x9x4 lattice) on the distal links' inner faces, a dynamic engraved
     tile (16x30x22 mm) standing on a static table.  Bodies: table, tile, palm, 16 links.  dt = 0.02 s."""
-    # μ = MU_MANIP; the engraved faces under four pads need more than 4096 active pairs (measured overflow)
-    cfg = Config(dt=0.02, mu_friction=MU_MANIP, active_capacity_per_env=12288)
+    # μ = MU_MANIP; the engraved faces under four pads: measured 8,505 barrier + 3,783 friction pairs in one
+    # env at step 5 (the pads' 2.7 mm edges against the tile's 0.6 mm engraving cells) -> capacity 24576
+    cfg = Config(dt=0.02, mu_friction=MU_MANIP, active_capacity_per_env=24576)
     tV, tT = box_surface((200 * MM, 200 * MM, 20 * MM), spacing=25 * MM)
     tileV, tileT = engraved_tile()
     pV, pT = box_surface((60 * MM, 60 * MM, 15 * MM))
