@@ -82,8 +82,8 @@ struct HostT {
   size_t cl_smem_bytes = 0;
   std::vector<int> cl_eptr, cl_edge, cl_bptr, cl_lrptr, cl_blk;   // cl_blk: 2 ints per block
   // sliced-ELL layout of the row-ordered soft blocks (streamed PCG)
-  std::vector<int> ell_len, ell_cb, ell_col, ell_row, ell_llen, ell_lcb, ell_lcol;
-  std::vector<long long> ell_vb, ell_pos, ell_lpos;
+  std::vector<int> ell_len, ell_cb, ell_col, ell_row;
+  std::vector<long long> ell_vb, ell_pos;
   size_t ell_total = 0;
 };
 
@@ -565,85 +565,41 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
   }
   if (H.NT + H.NE >= (1 << 29)) return fail(TAC_E_CAPACITY, "too many primitives");
   choose_cluster(H);
-  // symmetric sliced ELL for the streamed PCG (SELL-32, natural row order): only the UPPER off-diagonal
-  // block of each soft edge is stored (value of slot (g, l), entry j, component c at ell_vb[g] + 288j + 32c
-  // + l, its column at ell_cb[g] + 32j + l); row v's lower entries (u < v) read the transposed upper block
-  // of row u through ell_lpos (template).  Natural order keeps the lattice's translation invariance, so the
-  // transposed reads of a warp's 32 consecutive rows hit a few consecutive lanes of one or two groups.
+  // sliced ELL (SELL-32-σ) for the streamed PCG: rows sorted by length (descending, stable), groups of 32
+  // consecutive sorted rows padded to the group's longest row; ell_row maps a slot to its vertex; both
+  // blocks of a soft edge are stored (a symmetric upper-only variant with transposed reads of the lower
+  // neighbours was measured slower: the dependent position loads and transposed gathers cost more than the
+  // halved operator bytes, C3 PCG 7.2 -> 7.6 s per 10 steps)
   {
     const int G = (H.V + 31) / 32;
+    std::vector<int> order(H.V);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return H.rptr[a + 1] - H.rptr[a] > H.rptr[b + 1] - H.rptr[b];
+    });
     H.ell_row.assign((size_t)32 * G, -1);
-    for (int i = 0; i < H.V; ++i) H.ell_row[i] = i;
-    H.ell_pos.assign(H.NNZ, -1);
-    auto upper = [&](int v, int j) { return H.rcol[H.rptr[v] + j] > v; };
+    for (int i = 0; i < H.V; ++i) H.ell_row[i] = order[i];
+    H.ell_pos.assign(H.NNZ, 0);
     long long vb = 0;
     int cb = 0;
-    for (int g = 0; g < G; ++g) {                    // upper entries: value layout
+    for (int g = 0; g < G; ++g) {
       int len = 0;
       for (int l = 0; l < 32; ++l) {
-        const int v = 32 * g + l;
-        if (v >= H.V) continue;
-        int nu = 0;
-        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j) nu += upper(v, j);
-        len = std::max(len, nu);
+        const int v = H.ell_row[32 * g + l];
+        if (v >= 0) len = std::max(len, H.rptr[v + 1] - H.rptr[v]);
       }
       H.ell_len.push_back(len);
       H.ell_vb.push_back(vb);
       H.ell_cb.push_back(cb);
-      std::vector<int> k(32, 0);
-      std::vector<std::vector<int>> cols(32, std::vector<int>(len, -1));
-      for (int l = 0; l < 32; ++l) {
-        const int v = 32 * g + l;
-        if (v >= H.V) continue;
-        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j)
-          if (upper(v, j)) {
-            H.ell_pos[H.rptr[v] + j] = vb + (long long)288 * k[l] + l;
-            cols[l][k[l]++] = H.rcol[H.rptr[v] + j];
-          }
-      }
       for (int j = 0; j < len; ++j)
         for (int l = 0; l < 32; ++l) {
-          const int v = 32 * g + l;
-          H.ell_col.push_back(cols[l][j] >= 0 ? cols[l][j] : (v < H.V ? v : 0));
+          const int v = H.ell_row[32 * g + l];
+          const bool real = v >= 0 && H.rptr[v] + j < H.rptr[v + 1];
+          H.ell_col.push_back(real ? H.rcol[H.rptr[v] + j] : (v >= 0 ? v : 0));
+          if (real) H.ell_pos[H.rptr[v] + j] = vb + (long long)9 * 32 * j + l;
         }
-      vb += (long long)288 * len;
+      vb += (long long)9 * 32 * len;
       cb += 32 * len;
-    }
-    const long long zero = vb;                       // one all-zero block for the lower padding
-    vb += 288;
-    int lcb = 0;
-    for (int g = 0; g < G; ++g) {                    // lower entries: transposed reads of upper blocks
-      int len = 0;
-      for (int l = 0; l < 32; ++l) {
-        const int v = 32 * g + l;
-        if (v >= H.V) continue;
-        int nl = 0;
-        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j) nl += !upper(v, j);
-        len = std::max(len, nl);
-      }
-      H.ell_llen.push_back(len);
-      H.ell_lcb.push_back(lcb);
-      std::vector<std::vector<std::pair<int, long long>>> ent(32);
-      for (int l = 0; l < 32; ++l) {
-        const int v = 32 * g + l;
-        if (v >= H.V) continue;
-        for (int j = 0; j < H.rptr[v + 1] - H.rptr[v]; ++j)
-          if (!upper(v, j)) {
-            const int u = H.rcol[H.rptr[v] + j];
-            long long pu = -1;                       // the upper block (u, v) in row u
-            for (int q = H.rptr[u]; q < H.rptr[u + 1]; ++q)
-              if (H.rcol[q] == v) pu = H.ell_pos[q];
-            ent[l].push_back({u, pu});
-          }
-      }
-      for (int j = 0; j < len; ++j)
-        for (int l = 0; l < 32; ++l) {
-          const int v = 32 * g + l;
-          const bool real = j < (int)ent[l].size();
-          H.ell_lcol.push_back(real ? ent[l][j].first : (v < H.V ? v : 0));
-          H.ell_lpos.push_back(real ? ent[l][j].second : zero);
-        }
-      lcb += 32 * len;
     }
     H.ell_total = (size_t)vb;
   }
@@ -748,7 +704,6 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
     auto tl = [&](const std::vector<long long>& v) { return C.take<long long>(std::max<size_t>(v.size(), 1)); };
     D.ell_row = ti(H.ell_row); D.ell_len = ti(H.ell_len); D.ell_vb = tl(H.ell_vb); D.ell_cb = ti(H.ell_cb); D.ell_col = ti(H.ell_col);
     D.ell_pos = tl(H.ell_pos);
-    D.ell_llen = ti(H.ell_llen); D.ell_lcb = ti(H.ell_lcb); D.ell_lcol = ti(H.ell_lcol); D.ell_lpos = tl(H.ell_lpos);
   }
   D.cl.eptr = ti(H.cl_eptr); D.cl.edge = ti(H.cl_edge); D.cl.bptr = ti(H.cl_bptr); D.cl.lrptr = ti(H.cl_lrptr);
   D.cl.blk = reinterpret_cast<const int2*>(ti(H.cl_blk));
@@ -821,7 +776,7 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.max_newton = cfg->max_newton; D.max_al = cfg->max_al_rounds; D.max_pcg = cfg->max_pcg;
   D.max_accd = cfg->max_accd_iters; D.mollify = cfg->ee_mollifier; D.hmode = cfg->hessian_mode;
   D.hold_cap = std::max(cfg->hold_cap, 1); D.lm_mu0 = cfg->lm_mu0; D.bp_margin = cfg->bp_margin; D.K = (double)std::max(cfg->ls_expand, 1);
-  D.mu_f = cfg->mu_friction; D.eps_v = cfg->eps_v;
+  D.mu_f = cfg->mu_friction; D.eps_v = cfg->eps_v; D.eta_max = cfg->pcg_eta_max;
   // assembly scratch in chunks of asm_envs envs (TAC_ASM_CHUNK, default 1024): the per-tet and per-pair
   // records live only from k_tets / k_pairs* to k_assemble_*, so the Newton loop runs those three phases
   // chunk by chunk over the envs of the iteration and the scratch is sized for one chunk
@@ -863,7 +818,8 @@ static tac_status check_cfg(const tac_config* c) {
   if (!(c->max_step_rel > 0) || !(c->dt > 0) || !(c->dhat > 0) || !(c->kappa >= 0) || c->max_newton <= 0 || c->max_al_rounds <= 0 ||
       c->max_pcg <= 0 || !(c->pcg_eta > 0) || !(c->accd_s > 0 && c->accd_s < 1) || c->hessian_mode < 0 ||
       c->hessian_mode > 2 || !(c->lm_mu0 > 0) || !(c->bp_margin >= 0) || c->ls_expand < 1 || (c->ls_expand & (c->ls_expand - 1)) != 0 ||
-      !(c->mu_friction >= 0) || !(c->eps_v > 0))
+      !(c->mu_friction >= 0) || !(c->eps_v > 0) ||
+      !(c->pcg_eta_max == 0.0 || (c->pcg_eta_max >= c->pcg_eta && c->pcg_eta_max < 1.0)))
     return fail(TAC_E_INVALID, "invalid tac_config");
   if (c->mu_friction > 0 && c->hessian_mode != 2)
     return fail(TAC_E_INVALID, "friction (mu_friction > 0) requires hessian_mode 2");
@@ -939,10 +895,6 @@ extern "C" tac_status tac_batch_create(const tac_scene_desc* scene, int32_t n_en
   if (e == cudaSuccess) e = up(D.ell_cb, H.ell_cb, st);
   if (e == cudaSuccess) e = up(D.ell_col, H.ell_col, st);
   if (e == cudaSuccess) e = up(D.ell_pos, H.ell_pos, st);
-  if (e == cudaSuccess) e = up(D.ell_llen, H.ell_llen, st);
-  if (e == cudaSuccess) e = up(D.ell_lcb, H.ell_lcb, st);
-  if (e == cudaSuccess) e = up(D.ell_lcol, H.ell_lcol, st);
-  if (e == cudaSuccess) e = up(D.ell_lpos, H.ell_lpos, st);
   if (e == cudaSuccess) e = up(D.cl.eptr, H.cl_eptr, st);
   if (e == cudaSuccess) e = up(D.cl.edge, H.cl_edge, st);
   if (e == cudaSuccess) e = up(D.cl.bptr, H.cl_bptr, st);

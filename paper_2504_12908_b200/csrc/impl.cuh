@@ -47,6 +47,8 @@ struct EnvCtl {
   int n_fr, fr_frozen;    // lagged friction pairs of this step (appended after the barrier pairs), frozen at xⁿ
   int cap_seen, cap_need; // capacity overflows seen since batch creation (bits: 1 candidates, 2 big-target list,
                           // 4 hash entries, 8 active pairs) and the largest candidate count requested
+  double ew_rz0, ew_eta;  // relaxed PCG tolerance (R22): r₀ᵀz₀ and η of the last accepted solve of this step
+  int ew_has, pad4_;      // 1 once this step has an accepted solve
 };
 
 // ---- env-resident cluster PCG (pcg_cluster.cuh): plan built on the host from the soft BSR pattern ----
@@ -102,6 +104,7 @@ struct Dev {
   double lm_mu0;
   double bp_margin;         // δ of the reusable candidate list (0 = rebuild every iteration)
   double mu_f, eps_v;       // lagged friction: μ (0 = off) and ε_v
+  double eta_max;           // relaxed PCG tolerance (R22): 0 = fixed η
   double grav[3];
   // ---- template ----
   const int* tets;        // [T][4]
@@ -262,16 +265,12 @@ struct Dev {
   // ell_vb[g] + (9j + c)·32 + l, its column at ell_cb[g] + 32j + l — every warp load is 256 contiguous bytes
   int ell_groups;         // ⌈V/32⌉ (0: no ELL copy)
   size_t ell_total;       // doubles per env
-  const int* ell_row;     // [32·groups] vertex of each slot (natural order, −1 padding)
+  const int* ell_row;     // [32·groups] vertex of each slot (rows sorted by length, −1 padding)
   const int* ell_len;     // [groups] slots of the group
   const long long* ell_vb;// [groups] value base (doubles)
   const int* ell_cb;      // [groups] column base
   const int* ell_col;     // [Σ 32·len] column vertex (padding: the row itself, value 0)
-  const long long* ell_pos;// [NNZ] value base of row-ordered block q if it is an upper block (u > v), else −1
-  const int* ell_llen;    // [groups] lower entries of the group (rows' neighbours u < v)
-  const int* ell_lcb;     // [groups] base of the group's lower columns / positions
-  const int* ell_lcol;    // [Σ 32·llen] column u of lower entry j of slot l (padding: the row itself)
-  const long long* ell_lpos;// [Σ 32·llen] value base of the upper block (u, v) read transposed (padding: a zero block)
+  const long long* ell_pos;// [NNZ] value base of row-ordered block q (component c at + 32c)
   double* Hell;           // [E][ell_total]
 };
 

@@ -1803,10 +1803,13 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
         for (int c = 0; c < 3; ++c) B[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * b + c, 12)) * D.T + t];
     }
     const int qu = D.eup[ei], ql = D.elo[ei];
-    if (He) {                                           // symmetric sliced ELL: the upper block only
+    if (He) {
       double* hu = He + D.ell_pos[qu];
+      double* hl = He + D.ell_pos[ql];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) hu[32 * i] = B[i];
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { hu[32 * (3 * r + c)] = B[3 * r + c]; hl[32 * (3 * c + r)] = B[3 * r + c]; }
     } else {
       double* hu = D.Ho + ((size_t)e * D.NNZ + qu) * 9;
       double* hl = D.Ho + ((size_t)e * D.NNZ + ql) * 9;
@@ -1960,7 +1963,6 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
           }
         for (unsigned m = touched; m; m &= m - 1u) {
           const int sl = __ffs(m) - 1;
-          if (He && D.ell_pos[r0 + sl] < 0) continue;     // lower block: its transpose is summed by row u
           const int hs = He ? 32 : 1;                     // element stride of the block's storage
           double* hb = He ? He + D.ell_pos[r0 + sl] : Hoe + (size_t)(r0 + sl) * 9;
           hb[hs * l8] += acc[9 * sl + l8];
@@ -1970,7 +1972,7 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
         for (int j = jr; j < j1; ++j)
           for (int nb = 0; nb < 2; ++nb) {
             const int jb = snb[2 * j + nb];
-            if (jb < 0 || (He && D.ell_pos[jb] < 0)) continue;
+            if (jb < 0) continue;
             const int hs = He ? 32 : 1;
             double* hb = He ? He + D.ell_pos[jb] : Hoe + (size_t)jb * 9;
             const double* rec = srec + (size_t)j * SREC + 48 + 9 * nb;
@@ -2268,9 +2270,9 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
   const double* Hd = R ? R->Hd : D.Hd + (size_t)e * D.V * 9;       // SoA [9][V]
   const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
   const int* rptr = R ? R->rptr : D.rptr;
-  // soft rows, streamed operator in the symmetric sliced-ELL layout (written by the assembly, or converted
-  // once per k_pcg launch): warp = 32 consecutive rows, every upper-block component load is 256 contiguous
-  // bytes; the lower entries read the transposed upper blocks of the neighbouring rows
+  // soft rows, streamed operator in sliced-ELL layout (written by the assembly, or converted once per k_pcg
+  // launch): slot s of the sorted row order, warp = 32 consecutive slots, every block component load is 256
+  // contiguous bytes
   if (ell && !R) {
     const double* He = D.Hell + (size_t)e * D.ell_total;
     const int nslot = 32 * D.ell_groups;
@@ -2288,17 +2290,6 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
         const double* B = hb + 288 * j;
         acc += mk(B[0] * xu.x + B[32] * xu.y + B[64] * xu.z, B[96] * xu.x + B[128] * xu.y + B[160] * xu.z,
                   B[192] * xu.x + B[224] * xu.y + B[256] * xu.z);
-      }
-      // lower neighbours u < v: the upper block (u, v) of row u, transposed
-      const int llen = D.ell_llen[g];
-      const int* lc = D.ell_lcol + D.ell_lcb[g] + l;
-      const long long* lp = D.ell_lpos + D.ell_lcb[g] + l;
-#pragma unroll 2
-      for (int j = 0; j < llen; ++j) {
-        const v3 xu = ld3(x + 3 * lc[32 * j]);
-        const double* B = He + lp[32 * j];
-        acc += mk(B[0] * xu.x + B[96] * xu.y + B[192] * xu.z, B[32] * xu.x + B[128] * xu.y + B[224] * xu.z,
-                  B[64] * xu.x + B[160] * xu.y + B[256] * xu.z);
       }
       const v3 xv = ld3(x + 3 * v);
       const size_t V = D.V;
@@ -2432,6 +2423,17 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z, const S
 // ------------------------------------------------------------------------------------------
 __device__ void pcg_finish(const Dev& D, int e, double* p, double* red, double mu, bool bad, bool zero_g, int it_total,
                            double gp);
+// PCG tolerance of this solve (reading R22): fixed η, or the Eisenstat–Walker forcing from the
+// env's last accepted solve of the step: η = 0.9·r₀ᵀz₀ / (r₀ᵀz₀)_prev, ≥ 0.9·η_prev² when that exceeds 0.1,
+// clamped to [η, η_max]; η_max for the first solve of a step.  Uniform across the block (rz0 is).
+__device__ __forceinline__ double pcg_forcing(const Dev& D, const EnvCtl& C, double rz0) {
+  if (!(D.eta_max > 0.0)) return D.eta;
+  if (!C.ew_has) return D.eta_max;
+  double eta = 0.9 * rz0 / C.ew_rz0;
+  const double sg = 0.9 * C.ew_eta * C.ew_eta;
+  if (sg > 0.1) eta = fmax(eta, sg);
+  return fmin(fmax(eta, D.eta), D.eta_max);
+}
 // vsm = 1: the five PCG vectors live in shared memory (n small enough), p is copied out at the end
 __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb,
                          int fused = 0, int stream_lpr = 4);
@@ -2519,6 +2521,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
   int it_total = 0;
   double gp = 0.0;
   bool zero_g = false;
+  double rz0_used = 0.0, eta_used = 0.0;
   __shared__ double chol_scratch[144], chol_T[144];
   // streamed operator: the soft blocks of this env in sliced-ELL layout, once per launch
   const bool ell = !R && D.ell_groups > 0;
@@ -2527,7 +2530,6 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     const double* Ho = D.Ho + (size_t)e * D.NNZ * 9;
     for (int q = threadIdx.x; q < D.NNZ; q += blockDim.x) {
       const long long b = D.ell_pos[q];
-      if (b < 0) continue;                         // lower block: read transposed from the upper copy
 #pragma unroll
       for (int c = 0; c < 9; ++c) He[b + 32 * c] = Ho[9 * (size_t)q + c];
     }
@@ -2544,7 +2546,8 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     double part = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) { d[i] = z[i]; part += r[i] * z[i]; }
     double rz = block_sum(part, red);
-    const double rz0 = rz, stop = D.eta * D.eta * rz0;
+    const double rz0 = rz, eta_k = pcg_forcing(D, C, rz0), stop = eta_k * eta_k * rz0;
+    rz0_used = rz0; eta_used = eta_k;
     zero_g = rz0 == 0.0;                                 // g = 0: p = 0 is the (converged) answer
     int it = 0;
     bad = !(rz0 == rz0);
@@ -2656,6 +2659,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     __syncthreads();
     p = p_out;
   }
+  if (threadIdx.x == 0 && !bad && rz0_used > 0.0) { C.ew_rz0 = rz0_used; C.ew_eta = eta_used; C.ew_has = 1; }
   pcg_finish(D, e, p, red, mu, bad, zero_g, it_total, gp);
 }
 
@@ -3188,6 +3192,7 @@ __device__ void begin_env(const Dev& D, int e, const double* yk) {
     C.al_rounds = 0; C.n_act = 0; C.overflow = 0; C.alpha_ccd = 1.0; C.alpha_min = 1.0;  // (ncand: reusable list)
     C.rho = D.rho0; C.r_prev = 1.0 / 0.0; C.energy = 0.0; C.residual = 0.0; C.gp = 0.0; C.pnorm = 0.0; C.alpha = 1.0;
     C.exact = D.hmode >= 1 ? 1 : 0; C.hold = 0; C.nfail = 0; C.xfail = 0; C.Keff = 1.0; C.mu = 0.0;
+    C.ew_has = 0; C.ew_rz0 = 0.0; C.ew_eta = 0.0;
     C.n_fr = 0; C.fr_frozen = 0;
   }
   __syncthreads();

@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
   bool bad = false, zero_g = false;
   int it_total = 0;
   double gp = 0.0;
+  double rz0_used = 0.0, eta_used = 0.0;
   auto uv_at = [&](int colpk) -> v3 {                  // u of a soft vertex (local or remote rank)
     const int rk = colpk >> 16, lr = colpk & 0xffff;
     if constexpr (NC == 1) return ld3(usm + 3 * lr);
@@ -339,7 +340,8 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       cl_sum2<NC>(a0, b0, red, rred, 0);
       rz = a0;
     }
-    const double stop = D.eta * D.eta * rz;
+    const double eta_k = pcg_forcing(D, C, rz), stop = eta_k * eta_k * rz;   // R22 (fixed η by default)
+    rz0_used = rz; eta_used = eta_k;
     zero_g = rz == 0.0;
     bad = !(rz == rz);
     if constexpr (NC > 1) {
@@ -514,6 +516,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
   __threadfence();
   cl_barrier<NC>();
   if (rank != 0) return;
+  if (threadIdx.x == 0 && !bad && rz0_used > 0.0) { C.ew_rz0 = rz0_used; C.ew_eta = eta_used; C.ew_has = 1; }
   pcg_finish_noinline(D, e, p_out, red, mu, bad, zero_g, it_total, gp);
 }
 

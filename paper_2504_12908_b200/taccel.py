@@ -58,7 +58,8 @@ class Config(ctypes.Structure):
                 ("hessian_mode", ctypes.c_int32), ("ls_expand", ctypes.c_int32),
                 ("hold_cap", ctypes.c_int32), ("lm_mu0", ctypes.c_double), ("bp_margin", ctypes.c_double),
                 ("cand_capacity_per_env", ctypes.c_int32), ("active_capacity_per_env", ctypes.c_int32),
-                ("mu_friction", ctypes.c_double), ("eps_v", ctypes.c_double)]
+                ("mu_friction", ctypes.c_double), ("eps_v", ctypes.c_double),
+                ("pcg_eta_max", ctypes.c_double)]
 
 
 class EnvStats(ctypes.Structure):

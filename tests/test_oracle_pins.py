@@ -962,3 +962,32 @@ def test_depth_map_sphere_cap_closed_form():
             assert D[0, i, j] == pytest.approx(expect, abs=1e-12)
     assert np.allclose(N[0, 0, 0], [0, 0, 1], atol=1e-12)
     assert np.nanmax(D) <= h                              # the interpolant never exceeds the cap depth
+
+
+def test_relaxed_pcg_tolerance_reaches_the_same_step():
+    """Reading R22 ("carefully relaxing convergence tolerances"): the Eisenstat–Walker forcing only
+    changes how accurately each Newton direction is solved, not the minimiser — a C1 press step with the PCG
+    solver at η ∈ [1e-4, 0.1] lands on the direct-solve step within 1e-7·L_env (the Newton tolerance), the
+    forcing is live (a different PCG iteration count from the fixed η), and the first solve of a step uses
+    η_max."""
+    import dataclasses
+    sc0 = S.make_scene("C1")
+    ei = S.env_inputs(sc0, [0], n_steps=3)
+    out = {}
+    for key, (solver, em) in {"direct": ("direct", 0.0), "fixed": ("pcg", 0.0), "relaxed": ("pcg", 0.1)}.items():
+        sc = S.make_scene("C1")
+        sc.config = dataclasses.replace(sc.config, pcg_eta_max=em)
+        mod = M.prepare(sc)
+        L = M.env_scale(mod, ei.x0[0], ei.y0[0])
+        st = SO.State(ei.x0[0].copy(), np.zeros_like(ei.x0[0]), ei.y0[0].copy(), np.zeros_like(ei.y0[0]))
+        pcg = 0
+        for k in range(3):
+            st, stats = SO.step(mod, st, ei.ykin[k, 0], solver=solver, L_env=L)
+            assert stats.status == SO.ENV_OK
+            pcg += stats.pcg_iters
+        out[key] = (M.all_positions(mod, st.x, st.y), pcg, L)
+    P0, _, L = out["direct"]
+    for key in ("fixed", "relaxed"):
+        assert np.abs(out[key][0] - P0).max() <= 1e-7 * L, key
+    assert out["relaxed"][1] != out["fixed"][1], (out["relaxed"][1], out["fixed"][1])
+    assert SO.forcing_eta(dataclasses.replace(sc0.config, pcg_eta_max=0.1), 1.0, None) == 0.1
