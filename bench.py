@@ -528,17 +528,19 @@ def roofline(cfg_name, kernel, phases, pcg_bytes, ms_step_total, K):
     pcg_ms = phases["pcg"]["ms"]
     launches = max(phases["pcg"]["launches"], 1)
     ach = pcg_bytes / (pcg_ms / 1e3) / 1e9
-    traffic, tsrc = None, None
+    traffic, tsrc, t_alg, t_ratio = None, None, None, None
     tfile = os.path.join(ROOT, "profiles", "r2_pcg_traffic.json")
     if os.path.exists(tfile):
         tj = json.load(open(tfile)).get(cfg_name)
         if tj and tj.get("kernel") == kernel.split(" ")[0]:
-            traffic = tj["dram_bytes_per_launch"]
+            traffic, t_alg, t_ratio = tj["dram_bytes_per_launch"], tj["alg_bytes_per_launch"], tj["traffic_over_alg"]
             tsrc = (f"profiles/r2_pcg_traffic.json: ncu dram__bytes_read.sum+write.sum per {tj['kernel']} launch, "
-                    f"{tj['what']}")
+                    f"{tj['what']}; traffic_alg_bytes_per_launch = the device-counted algorithmic bytes of the same "
+                    f"launches (the launches of one step differ in size, so compare the ratio)")
     resident = kernel.startswith("k_pcg_r")
     return {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "traffic": traffic, "traffic_source": tsrc, "peak_source": src,
+            "traffic": traffic, "traffic_alg_bytes_per_launch": t_alg, "traffic_over_alg": t_ratio,
+            "traffic_source": tsrc, "peak_source": src,
             "share_of_step": pcg_ms / ms_step_total, "alg_bytes_per_launch": pcg_bytes / launches,
             "alg_model": "per PCG iteration per env: 72(V+E_s)+4E_s+640*P_res+296*N_cpl+1248*ND+48V+96n "
                          "(SURVEY sec 8(d) B_pcg on the condensed operator; DESIGN.md sec 5)",

@@ -69,7 +69,7 @@ HD double nh_energy(const v3* x, const double* Dmi, double mu, double lam, bool*
 }
 
 // Gradient g[12] (slot-major: 3*k + c) and packed-upper projected Hessian H[78] of scale·Ψ(F(x)).
-// Outputs go through store functors: gst(i, value) for the 12 gradient entries, hst(packed index, value)
+// Outputs go through store functors: gst(i, value) for the 12 gradient entries, hst(r, s, value) for r ≤ s
 // for the 78 Hessian entries (k_tets stores straight to its SoA buffer, no local arrays)
 template <class GStore, class HStore>
 HD void nh_grad_hess_t(const v3* x, const double* Dmi, double mu, double lam, double scale, double* psi_out,
@@ -156,21 +156,23 @@ HD void nh_grad_hess_t(const v3* x, const double* Dmi, double mu, double lam, do
   v3 qb[9][4];
   for (int m = 0; m < nneg; ++m)
     for (int k = 0; k < 4; ++k) qb[m][k] = mul33(negQ[m], beta[k]);
+#pragma unroll
   for (int r = 0; r < 12; ++r) {
     int k = r / 3, c = r % 3;
+#pragma unroll
     for (int s = r; s < 12; ++s) {
       int l = s / 3, d = s % 3;
       double v = lam * comp(h[k], c) * comp(h[l], d) + kk * comp(h[l], c) * comp(h[k], d);
       if (c == d) v += mu * dot(beta[k], beta[l]);
       for (int m = 0; m < nneg; ++m) v -= negl[m] * comp(qb[m][k], c) * comp(qb[m][l], d);
-      hst(sym_idx(r, s, 12), scale * v);
+      hst(r, s, scale * v);
     }
   }
 }
 HD void nh_grad_hess(const v3* x, const double* Dmi, double mu, double lam, double scale, double* psi_out,
                      double* g, double* H, bool project = true) {
   nh_grad_hess_t(x, Dmi, mu, lam, scale, psi_out, [&](int i, double v) { g[i] = v; },
-                 [&](int i, double v) { H[i] = v; }, project);
+                 [&](int r, int s, double v) { H[sym_idx(r, s, 12)] = v; }, project);
 }
 
 // ABD orthogonality energy E = κ V ‖AAᵀ − I‖²_F (reading R9 of the garbled ARAP term P:L116):

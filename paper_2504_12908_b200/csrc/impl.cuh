@@ -188,7 +188,7 @@ struct Dev {
   double *Hb;             // [E][ND][144]
   double *Pinv_s, *Pinv_b;// [E][V][9], [E][ND][144]
   double *Dg_s, *Dg_b;    // raw block-Jacobi diagonal blocks (before the LM shift and inversion)
-  double* tetbuf;         // [E][90][T]
+  double* tetbuf;         // [asm_envs][90][T]
   int *cand_a, *cand_b;   // [E][cand_cap] (cand_a bit 30 = EE)
   int* ent;               // [E][ent_cap][2]
   int* big;               // [E][BIG_CAP]

@@ -831,12 +831,39 @@ __global__ void __launch_bounds__(NTHREADS) k_tets(Dev D, int env0, int force) {
 #pragma unroll
   for (int i = 0; i < 9; ++i) Dmi[i] = D.Dmi[9 * t + i];
   const double scale = D.dt * D.dt * D.vol[t];
-  double* out = D.tetbuf + (size_t)sl * TETBUF * D.T + t;     // SoA [90][T], stored as computed
+  // per-tet gradient and packed upper Hessian, SoA [90][T] (coalesced stores; an element-record layout in
+  // assembly order was measured slower: its scattered 8-byte stores cost k_tets 3.5x, the gathers it saved
+  // were latency-, not sector-bound)
+  double* out = D.tetbuf + (size_t)sl * TETBUF * D.T + t;
   const size_t T = D.T;
   auto gst = [&](int i, double v) { out[(size_t)i * T] = v; };
-  auto hst = [&](int i, double v) { out[(size_t)(12 + i) * T] = v; };
+  auto hst = [&](int r, int s, double v) { out[(size_t)(12 + sym_idx(r, s, 12)) * T] = v; };
   if (D.ctl[e].exact) nh_grad_hess_t(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, gst, hst, false);
   else nh_grad_hess_t(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, gst, hst, true);
+}
+// exact Hessians only (hessian_mode 2, every env): the projected branch (SVD, negative-mode subtraction)
+// is not compiled in, so the kernel keeps a small register/stack footprint
+__global__ void __launch_bounds__(NTHREADS) k_tets_x(Dev D, int env0, int force) {
+  const int e = env_at(D, env0, blockIdx.y);
+  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
+  if (env_skip(D, e, force)) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= D.T) return;
+  const double* q = D.q + (size_t)e * D.n;
+  int4 tv = reinterpret_cast<const int4*>(D.tets)[t];
+  v3 x[4] = {ld3(q + 3 * tv.x), ld3(q + 3 * tv.y), ld3(q + 3 * tv.z), ld3(q + 3 * tv.w)};
+  double Dmi[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Dmi[i] = D.Dmi[9 * t + i];
+  const double scale = D.dt * D.dt * D.vol[t];
+  // per-tet gradient and packed upper Hessian, SoA [90][T] (coalesced stores; an element-record layout in
+  // assembly order was measured slower: its scattered 8-byte stores cost k_tets 3.5x, the gathers it saved
+  // were latency-, not sector-bound)
+  double* out = D.tetbuf + (size_t)sl * TETBUF * D.T + t;
+  const size_t T = D.T;
+  auto gst = [&](int i, double v) { out[(size_t)i * T] = v; };
+  auto hst = [&](int r, int s, double v) { out[(size_t)(12 + sym_idx(r, s, 12)) * T] = v; };
+  nh_grad_hess_t(x, Dmi, D.mu[t], D.lam[t], scale, nullptr, gst, hst, false);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1769,31 +1796,19 @@ __device__ void chol_inverse12_warp(const double* A, double* Ainv, double* L /*1
   __syncwarp();
 }
 
-// soft part of the assembly (elastic edge and diagonal blocks, gradient, condensed contact terms,
-// 3×3 block-Jacobi inverses); register-light, so it runs at higher occupancy than the body part
-constexpr int ASM_SOFT_MAX = 320;
-__global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int env0, int force) {
-  const int e = env_at(D, env0, blockIdx.x);
-  const int sl = blockIdx.x;                   // slot in the assembly scratch (launch-local, < asm_envs)
+// elastic soft edge blocks, grid-parallel over (edge tile, env): one thread per soft edge {i < j} sums its
+// tets' (i, j) block once (template list eblk, in order) and stores it and its transpose — into the
+// sliced-ELL copy the streamed PCG reads (asm_ell) or the row-ordered blocks.  Split out of k_assemble_soft,
+// where 256 threads per env walked the edges one after another (latency-bound dependent loads)
+__global__ void __launch_bounds__(NTHREADS) k_asm_edges(Dev D, int env0, int force) {
+  const int e = env_at(D, env0, blockIdx.y);
+  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
-  __shared__ int shs[33];
-  __shared__ int next_cv;
-  extern __shared__ double dsm_asm[];   // contact-vertex list [V] ints
-  EnvCtl& C = D.ctl[e];
-  const double* q = D.q + (size_t)e * D.n;
-  const double* qt = D.qt + (size_t)e * D.n;
-  double* g = D.g + (size_t)e * D.n;
+  const int ei = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ei >= D.NEs) return;
   const double* tb = D.tetbuf + (size_t)sl * TETBUF * D.T;
-  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
-  const double dt2 = D.dt * D.dt, rho = C.rho;
-  const double* s_att = D.s_att + (size_t)e * D.NC * 3;
-  const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
-  CLK_INIT
-  // ---- soft edge blocks (elastic): one thread per edge {i < j} sums the tets' (i, j) blocks once and
-  // stores the upper block (row i) and its transpose (row j) — into the sliced-ELL copy the streamed PCG
-  // reads (asm_ell) or the row-ordered blocks ----
   double* const He = D.asm_ell ? D.Hell + (size_t)e * D.ell_total : nullptr;
-  for (int ei = threadIdx.x; ei < D.NEs; ei += blockDim.x) {
+  {
     double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = D.eblk_ptr[ei]; j < D.eblk_ptr[ei + 1]; ++j) {
       int ent = D.eblk[j], t = ent >> 4, a = (ent >> 2) & 3, b = ent & 3;
@@ -1819,7 +1834,73 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
         for (int c = 0; c < 3; ++c) { hu[3 * r + c] = B[3 * r + c]; hl[3 * c + r] = B[3 * r + c]; }
     }
   }
-  __syncthreads();
+}
+
+// soft vertex terms, grid-parallel over (vertex tile, env): inertia, gravity, AL and the elastic diagonal
+// blocks and gradient (from the tets' records), the SpMV diagonal Hd, the raw diagonal Dg_s (LM re-inversion)
+// and the block-Jacobi inverse of vertices without contact records (contact vertices: k_assemble_soft phase 3,
+// after their condensed records are added).  Split out of k_assemble_soft like k_asm_edges.
+__global__ void __launch_bounds__(NTHREADS) k_asm_verts(Dev D, int env0, int force) {
+  const int e = env_at(D, env0, blockIdx.y);
+  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
+  if (env_skip(D, e, force)) return;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= D.V) return;
+  const EnvCtl& C = D.ctl[e];
+  const double* q = D.q + (size_t)e * D.n;
+  const double* qt = D.qt + (size_t)e * D.n;
+  const double* tb = D.tetbuf + (size_t)sl * TETBUF * D.T;
+  const double dt2 = D.dt * D.dt, rho = C.rho;
+  const double m = D.mass[v];
+  v3 x = ld3(q + 3 * v), xt = ld3(qt + 3 * v);
+  v3 gv = m * (x - xt) - (dt2 * m) * mk(D.grav[0], D.grav[1], D.grav[2]);
+  double dg = m;
+  const int ci = D.att_of_vert[v];
+  if (ci >= 0) {
+    v3 r = x - ld3(D.s_att + (size_t)e * D.NC * 3 + 3 * ci);
+    gv += (rho * m) * r - m * ld3(D.lam_att + (size_t)e * D.NC * 3 + 3 * ci);
+    dg += rho * m;
+  }
+  double Hv[9] = {dg, 0, 0, 0, dg, 0, 0, 0, dg};
+  for (int j = D.vdiag_ptr[v]; j < D.vdiag_ptr[v + 1]; ++j) {
+    int ent = D.vdiag[j], t = ent >> 2, a = ent & 3;
+    gv += mk(tb[(size_t)(3 * a) * D.T + t], tb[(size_t)(3 * a + 1) * D.T + t], tb[(size_t)(3 * a + 2) * D.T + t]);
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) Hv[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * a + c, 12)) * D.T + t];
+  }
+  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
+  const bool hasc = cptr[v + 1] > cptr[v];
+  st3(D.g + (size_t)e * D.n + 3 * v, gv);
+  double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]: SpMV diagonal (contact added in phase 2)
+  double* ds = D.Dg_s + (size_t)e * D.V * 9;         // raw diagonal block (SoA) for LM re-inversion
+  for (int i = 0; i < 9; ++i) { hd[(size_t)i * D.V + v] = Hv[i]; ds[(size_t)i * D.V + v] = Hv[i]; }
+  if (!hasc) {
+    const double sh = C.mu * m;                       // mass-scaled LM shift μ·m_v I (R14c)
+    Hv[0] += sh; Hv[4] += sh; Hv[8] += sh;
+    double Pi[9];
+    inv33(Hv, Pi);
+    double* ps = D.Pinv_s + (size_t)e * D.V * 9;     // SoA [9][V]
+    for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
+  }
+}
+
+// soft part of the assembly (elastic edge and diagonal blocks, gradient, condensed contact terms,
+// 3×3 block-Jacobi inverses); register-light, so it runs at higher occupancy than the body part
+constexpr int ASM_SOFT_MAX = 320;
+__global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int env0, int force) {
+  const int e = env_at(D, env0, blockIdx.x);
+  const int sl = blockIdx.x;                   // slot in the assembly scratch (launch-local, < asm_envs)
+  if (env_skip(D, e, force)) return;
+  __shared__ int shs[33];
+  __shared__ int next_cv;
+  extern __shared__ double dsm_asm[];   // contact-vertex list [V] ints
+  EnvCtl& C = D.ctl[e];
+  double* g = D.g + (size_t)e * D.n;
+  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
+  CLK_INIT
+  // the elastic edge blocks and the vertex terms come from k_asm_edges / k_asm_verts (grid-parallel, launched
+  // before this kernel); here: the condensed contact records, coupling lists and contact-vertex inverses
+  double* const He = D.asm_ell ? D.Hell + (size_t)e * D.ell_total : nullptr;
   CLK(10)
   // ---- soft vertices: gradient, diagonal blocks, and the condensed contact terms of row v ----
   int* cpp = D.cpl_ptr + (size_t)e * (D.V + 1);
@@ -1834,45 +1915,16 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
   int* cvl = reinterpret_cast<int*>(dsm_asm);        // [V] soft vertices with contact records
   double* accs = dsm_asm + (D.V + 3) / 2;             // [ngrp][maxrl][9] soft–soft block sums
   int cpl_run = 0, nct = 0;
-  // phase 1 (thread per vertex): inertia, gravity, AL and elastic terms; body mask of the condensed
-  // records; coupling offsets and the contact-vertex list by block scans
+  // phase 1 (thread per vertex): body mask of the condensed records; coupling offsets and the
+  // contact-vertex list by block scans (the vertex terms themselves: k_asm_verts, launched before)
   for (int v0 = 0; v0 < D.V; v0 += blockDim.x) {
     const int v = v0 + threadIdx.x;
     unsigned bmask = 0u;
     int hasc = 0;
     if (v < D.V) {
-      const double m = D.mass[v];
-      v3 x = ld3(q + 3 * v), xt = ld3(qt + 3 * v);
-      v3 gv = m * (x - xt) - (dt2 * m) * mk(D.grav[0], D.grav[1], D.grav[2]);
-      double dg = m;
-      int ci = D.att_of_vert[v];
-      if (ci >= 0) {
-        v3 r = x - ld3(s_att + 3 * ci);
-        gv += (rho * m) * r - m * ld3(lam_att + 3 * ci);
-        dg += rho * m;
-      }
-      double Hv[9] = {dg, 0, 0, 0, dg, 0, 0, 0, dg};
-      for (int j = D.vdiag_ptr[v]; j < D.vdiag_ptr[v + 1]; ++j) {
-        int ent = D.vdiag[j], t = ent >> 2, a = ent & 3;
-        gv += mk(tb[(size_t)(3 * a) * D.T + t], tb[(size_t)(3 * a + 1) * D.T + t], tb[(size_t)(3 * a + 2) * D.T + t]);
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) Hv[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * a + c, 12)) * D.T + t];
-      }
       const int j0 = cptr[v], j1 = cptr[v + 1];
       hasc = j1 > j0;
       for (int j = j0 + rcnt[v]; j < j1; ++j) { const int d = sbody[j]; if (d >= 0) bmask |= 1u << d; }
-      st3(g + 3 * v, gv);
-      double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]: SpMV diagonal (contact added in phase 2)
-      double* ds = D.Dg_s + (size_t)e * D.V * 9;         // raw diagonal block (SoA) for LM re-inversion
-      for (int i = 0; i < 9; ++i) { hd[(size_t)i * D.V + v] = Hv[i]; ds[(size_t)i * D.V + v] = Hv[i]; }
-      if (!hasc) {
-        const double sh = C.mu * m;                       // mass-scaled LM shift μ·m_v I (R14c)
-        Hv[0] += sh; Hv[4] += sh; Hv[8] += sh;
-        double Pi[9];
-        inv33(Hv, Pi);
-        double* ps = D.Pinv_s + (size_t)e * D.V * 9;     // SoA [9][V]
-        for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
-      }
     }
     int tot, totc;
     const int ex = block_excl_scan(__popc(bmask), shs, &tot);
@@ -2130,29 +2182,11 @@ struct SmemMat {
   const int *rptr, *rcol, *rupx, *cptr, *rcnt, *cpp;
 };
 
-// what: 1 = zero the body partials + barrier, 2 = pass A (+ barrier), 4 = pass B, 8 = final barrier.
-// Returns this thread's partial Σ x_i y_i over the rows it wrote (for fused PCG dot products).
-constexpr int SPMV_ALL = 15;
-__device__ double spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
-                       double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL, int stream_lpr = 4, bool ell = false) {
-  const EnvCtl& C = D.ctl[e];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
-  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
-  const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
-  const int* spos = D.spos + (size_t)e * 4 * D.act_cap;
-  double* sout = D.sout + (size_t)e * 4 * D.act_cap * 3;
-  const int* rl = D.res_list + (size_t)e * D.act_cap;
-  const int nres = C.n_res, ncpl = C.n_cpl;
-  const int nb12 = D.ND * 12;
-  CLK_INIT
-  double xy = 0.0;
-  if (what & 1) {
-    for (int i = threadIdx.x; i < nw * nb12; i += blockDim.x) part[i] = 0.0;
-    __syncthreads();
-  }
-  CLK(0)
-  if (what & 2) {
+// SpMV pass A1 (residual pairs, matrix-free 12×12, one pair per lane), out of line: rare (two soft bodies or two
+// DoF bodies in one pair) and register-heavy, so the PCG loop does not carry its registers
+__device__ __noinline__ void spmv_residual(const Dev& D, int e, const double* x, double* part, const double* aH, const int* aslot,
+                                          const double* axb, const int* spos, double* sout, const int* rl, int nres, int nb12,
+                                          int lane, int w) {
   // pass A1: residual pairs, matrix-free 12×12 (one pair per lane)
   for (int base = 32 * w; base < nres; base += blockDim.x) {
     const int idx = base + lane;
@@ -2217,6 +2251,32 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
         for (int i = 0; i < 12; ++i) part[w * nb12 + 12 * d + i] += c[i];
     }
   }
+}
+
+// what: 1 = zero the body partials + barrier, 2 = pass A (+ barrier), 4 = pass B, 8 = final barrier.
+// Returns this thread's partial Σ x_i y_i over the rows it wrote (for fused PCG dot products).
+constexpr int SPMV_ALL = 15;
+__device__ double spmv(const Dev& D, int e, const double* x, double* y, double* part /*smem [nw][ND][12]*/,
+                       double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL, int stream_lpr = 4, bool ell = false) {
+  const EnvCtl& C = D.ctl[e];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
+  const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
+  const int* spos = D.spos + (size_t)e * 4 * D.act_cap;
+  double* sout = D.sout + (size_t)e * 4 * D.act_cap * 3;
+  const int* rl = D.res_list + (size_t)e * D.act_cap;
+  const int nres = C.n_res, ncpl = C.n_cpl;
+  const int nb12 = D.ND * 12;
+  CLK_INIT
+  double xy = 0.0;
+  if (what & 1) {
+    for (int i = threadIdx.x; i < nw * nb12; i += blockDim.x) part[i] = 0.0;
+    __syncthreads();
+  }
+  CLK(0)
+  if (what & 2) {
+  if (nres > 0) spmv_residual(D, e, x, part, aH, aslot, axb, spos, sout, rl, nres, nb12, lane, w);
   // pass A2: soft–body couplings (one per lane): soft output C_vd x_d → cpl_out[c] (summed by row v
   // in pass B), body output C_vdᵀ x_v warp-reduced per body into part[w][d]
   {
@@ -2372,7 +2432,7 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
 // block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c).  The 3×3 soft
 // blocks are thread-parallel; warp 0 inverts the body blocks one by one (warp Cholesky) meanwhile.
 // Outputs: ps [9][V] SoA and pb [ND][144] (global, or the resident shared-memory copies)
-__device__ void reinvert_precond(const Dev& D, int e, double mu, double* ps, double* pb, double* scratch /*smem 144*/,
+__device__ __noinline__ void reinvert_precond(const Dev& D, int e, double mu, double* ps, double* pb, double* scratch /*smem 144*/,
                                  double* T /*smem 144*/) {
   const double* ds = D.Dg_s + (size_t)e * D.V * 9;
   for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
@@ -2435,10 +2495,15 @@ __device__ __forceinline__ double pcg_forcing(const Dev& D, const EnvCtl& C, dou
   return fmin(fmax(eta, D.eta), D.eta_max);
 }
 // vsm = 1: the five PCG vectors live in shared memory (n small enough), p is copied out at the end
+__device__ __noinline__ void pcg_finish_noinline(const Dev& D, int e, double* p, double* red, double mu, bool bad, bool zero_g,
+                                                 int it_total, double gp);
 __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* red, SmemMat* R, double* Rw_Ps, double* Rw_Pb,
                          int fused = 0, int stream_lpr = 4);
 
-__global__ void __launch_bounds__(NTHREADS, 2) k_pcg(Dev D, int env0, int force, int vsm, int fused, int lpr) {
+// 2 CTAs/SM (128 registers); a 3-CTA/SM budget (80 registers) was measured slower (C3 PCG 6.7 -> 9.1 s / 10
+// steps: spills in the SpMV loop)
+template <int MINB>
+__global__ void __launch_bounds__(NTHREADS, MINB) k_pcg(Dev D, int env0, int force, int vsm, int fused, int lpr) {
   const int e = env_at(D, env0, blockIdx.x);
   if (env_skip(D, e, force)) return;
   __shared__ double red[32];
@@ -2660,7 +2725,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     p = p_out;
   }
   if (threadIdx.x == 0 && !bad && rz0_used > 0.0) { C.ew_rz0 = rz0_used; C.ew_eta = eta_used; C.ew_has = 1; }
-  pcg_finish(D, e, p, red, mu, bad, zero_g, it_total, gp);
+  pcg_finish_noinline(D, e, p, red, mu, bad, zero_g, it_total, gp);   // out of line: keeps the loop's registers
 }
 
 // end of a PCG launch (block-level, one CTA per env): embedded ∞-norm of the direction, step cap
@@ -3601,7 +3666,9 @@ void launch_narrow(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
 }
 void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   dim3 grid((D.T + NTHREADS - 1) / NTHREADS, ne);
-  if (D.T > 0) k_tets<<<grid, NTHREADS, 0, s>>>(D, env0, force);
+  if (D.T == 0) return;
+  if (D.hmode == 2 && !force) k_tets_x<<<grid, NTHREADS, 0, s>>>(D, env0, force);
+  else k_tets<<<grid, NTHREADS, 0, s>>>(D, env0, force);
 }
 void launch_pairs(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   // hessian_mode 2 (R14c) keeps every env on exact Hessians; modes 0/1 (and debug evaluations,
@@ -3622,6 +3689,8 @@ void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) 
   const int bytes = ((D.V + 3) / 2) * (int)sizeof(double) + (D.maxrl <= 32 ? (thr / 8) * D.maxrl * 9 * (int)sizeof(double) : 0);
   static size_t attr[MAX_DEVICES] = {};
   ensure_smem(k_assemble_soft, attr, bytes);
+  if (D.NEs > 0) k_asm_edges<<<dim3((D.NEs + NTHREADS - 1) / NTHREADS, ne), NTHREADS, 0, s>>>(D, env0, force);
+  if (D.V > 0) k_asm_verts<<<dim3((D.V + NTHREADS - 1) / NTHREADS, ne), NTHREADS, 0, s>>>(D, env0, force);
   k_assemble_soft<<<ne, thr, bytes, s>>>(D, env0, force);
   if (D.ND > 0) k_assemble_body<<<ne, NTHREADS, 0, s>>>(D, env0, force);
 }
@@ -3773,8 +3842,8 @@ void launch_pcg(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   static const int sfused = getenv("TAC_PCG_STREAM_FUSED") ? atoi(getenv("TAC_PCG_STREAM_FUSED")) : 1;
   static const int slpr = getenv("TAC_PCG_STREAM_LPR") ? atoi(getenv("TAC_PCG_STREAM_LPR")) : 1;
   const int vsm = pl.path == PCG_STREAM_VSM ? 1 : (pl.path == PCG_STREAM_D ? 2 : 0), lpr = slpr == 2 || slpr == 4 ? slpr : 1;
-  ensure_smem(k_pcg, cst, pl.bytes);
-  k_pcg<<<ne, NTHREADS, pl.bytes, s>>>(D, env0, force, vsm, sfused, lpr);
+  ensure_smem(k_pcg<2>, cst, pl.bytes);
+  k_pcg<2><<<ne, NTHREADS, pl.bytes, s>>>(D, env0, force, vsm, sfused, lpr);
 }
 void launch_spmv(const Dev& D, int env0, const double* x, double* y, cudaStream_t s) {
   k_spmv<<<1, NTHREADS, spmv_smem(D), s>>>(D, env0, x, y);

@@ -133,7 +133,8 @@ def test_c5_device_fk_matches_homogeneous_products():
 def test_c5_hand_grasp_single_steps():
     """C5 (4 pads, 17 kinematic links, engraved tile), 128 envs (the per-GPU share of 1024 on 8 GPUs):
     targets compiled on the device from the joint script each step; lockstep to step 60 (pads pressing the
-    tile faces) and 85 (oscillation), env 0 and 127 step once on the GPU and in the oracle."""
+    tile faces, env 0) and 85 (oscillation, env 127) one env steps once on the GPU and in the oracle (the
+    oracle step of an engraved-tile env takes minutes: ~12k active pairs through autograd)."""
     sc = S.make_scene("C5")
     E = 128
     ei = S.env_inputs(sc, np.arange(E), n_steps=86)
@@ -148,9 +149,9 @@ def test_c5_hand_grasp_single_steps():
     for k in range(60):
         b.set_joint_targets(qdev[k], base=yp)
         assert (b.step(1) == 0).all(), k
-    n = [c[2] for c in _single_step(sc, mod, ei, b, ykin, 60, (0, 127))]
+    n = [c[2] for c in _single_step(sc, mod, ei, b, ykin, 60, (0,))]
     assert max(n) > 0
     for k in range(61, 85):
         b.set_joint_targets(qdev[k], base=yp)
         assert (b.step(1) == 0).all(), k
-    _single_step(sc, mod, ei, b, ykin, 85, (0,))
+    _single_step(sc, mod, ei, b, ykin, 85, (127,))

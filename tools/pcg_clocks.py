@@ -4,18 +4,22 @@ import ctypes, sys
 import numpy as np, torch
 sys.path.insert(0, "/root/repo")
 from paper_2504_12908_b200 import scenes as S, taccel as T
+T.LIB_PATH = T.LIB_PATH.replace("libtaccel_cuda.so", "libtaccel_cuda_clk.so")   # the -DTAC_CLOCKS build
 E, W, K = (int(a) for a in sys.argv[1:4])
+CFG = sys.argv[4] if len(sys.argv) > 4 else "C2"
 NAMES = ["zero+sync", "pass A (pairs, couplings)", "B2 barrier", "soft rows", "body rows", "dAd warp sum", "B3 wait", "update+precond+rz", "B4 wait", "beta, d upd, B1"]
-sc = S.make_scene("C2")
+sc = S.make_scene(CFG)
 ei = S.env_inputs(sc, np.arange(E), n_steps=W + K)
 b = T.Batch(sc, E)
 b.set_state(ei.x0, ei.y0)
 yk = torch.tensor(ei.ykin, device="cuda")
-b.step_schedule(yk[:W])
+for k in range(W):
+    b.set_targets(yk[k]); b.step(1)
 lib = T.load()
 buf = (ctypes.c_ulonglong * 32)()
 lib.tac_debug_clocks(buf)
-b.step_schedule(yk[W:W + K])
+for k in range(W, W + K):
+    b.set_targets(yk[k]); b.step(1)
 lib.tac_debug_clocks(buf)
 n = buf[15]
 tot = sum(buf[i] for i in range(10))
