@@ -1836,54 +1836,6 @@ __global__ void __launch_bounds__(NTHREADS) k_asm_edges(Dev D, int env0, int for
   }
 }
 
-// soft vertex terms, grid-parallel over (vertex tile, env): inertia, gravity, AL and the elastic diagonal
-// blocks and gradient (from the tets' records), the SpMV diagonal Hd, the raw diagonal Dg_s (LM re-inversion)
-// and the block-Jacobi inverse of vertices without contact records (contact vertices: k_assemble_soft phase 3,
-// after their condensed records are added).  Split out of k_assemble_soft like k_asm_edges.
-__global__ void __launch_bounds__(NTHREADS) k_asm_verts(Dev D, int env0, int force) {
-  const int e = env_at(D, env0, blockIdx.y);
-  const int sl = blockIdx.y;                   // slot in the assembly scratch (launch-local, < asm_envs)
-  if (env_skip(D, e, force)) return;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= D.V) return;
-  const EnvCtl& C = D.ctl[e];
-  const double* q = D.q + (size_t)e * D.n;
-  const double* qt = D.qt + (size_t)e * D.n;
-  const double* tb = D.tetbuf + (size_t)sl * TETBUF * D.T;
-  const double dt2 = D.dt * D.dt, rho = C.rho;
-  const double m = D.mass[v];
-  v3 x = ld3(q + 3 * v), xt = ld3(qt + 3 * v);
-  v3 gv = m * (x - xt) - (dt2 * m) * mk(D.grav[0], D.grav[1], D.grav[2]);
-  double dg = m;
-  const int ci = D.att_of_vert[v];
-  if (ci >= 0) {
-    v3 r = x - ld3(D.s_att + (size_t)e * D.NC * 3 + 3 * ci);
-    gv += (rho * m) * r - m * ld3(D.lam_att + (size_t)e * D.NC * 3 + 3 * ci);
-    dg += rho * m;
-  }
-  double Hv[9] = {dg, 0, 0, 0, dg, 0, 0, 0, dg};
-  for (int j = D.vdiag_ptr[v]; j < D.vdiag_ptr[v + 1]; ++j) {
-    int ent = D.vdiag[j], t = ent >> 2, a = ent & 3;
-    gv += mk(tb[(size_t)(3 * a) * D.T + t], tb[(size_t)(3 * a + 1) * D.T + t], tb[(size_t)(3 * a + 2) * D.T + t]);
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) Hv[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * a + c, 12)) * D.T + t];
-  }
-  const int* cptr = D.cptr + (size_t)e * (D.V + 1);
-  const bool hasc = cptr[v + 1] > cptr[v];
-  st3(D.g + (size_t)e * D.n + 3 * v, gv);
-  double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]: SpMV diagonal (contact added in phase 2)
-  double* ds = D.Dg_s + (size_t)e * D.V * 9;         // raw diagonal block (SoA) for LM re-inversion
-  for (int i = 0; i < 9; ++i) { hd[(size_t)i * D.V + v] = Hv[i]; ds[(size_t)i * D.V + v] = Hv[i]; }
-  if (!hasc) {
-    const double sh = C.mu * m;                       // mass-scaled LM shift μ·m_v I (R14c)
-    Hv[0] += sh; Hv[4] += sh; Hv[8] += sh;
-    double Pi[9];
-    inv33(Hv, Pi);
-    double* ps = D.Pinv_s + (size_t)e * D.V * 9;     // SoA [9][V]
-    for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
-  }
-}
-
 // soft part of the assembly (elastic edge and diagonal blocks, gradient, condensed contact terms,
 // 3×3 block-Jacobi inverses); register-light, so it runs at higher occupancy than the body part
 constexpr int ASM_SOFT_MAX = 320;
@@ -1898,8 +1850,7 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
   double* g = D.g + (size_t)e * D.n;
   const int* cptr = D.cptr + (size_t)e * (D.V + 1);
   CLK_INIT
-  // the elastic edge blocks and the vertex terms come from k_asm_edges / k_asm_verts (grid-parallel, launched
-  // before this kernel); here: the condensed contact records, coupling lists and contact-vertex inverses
+  // the elastic edge blocks come from k_asm_edges (grid-parallel, launched before this kernel)
   double* const He = D.asm_ell ? D.Hell + (size_t)e * D.ell_total : nullptr;
   CLK(10)
   // ---- soft vertices: gradient, diagonal blocks, and the condensed contact terms of row v ----
@@ -1915,16 +1866,52 @@ __global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int en
   int* cvl = reinterpret_cast<int*>(dsm_asm);        // [V] soft vertices with contact records
   double* accs = dsm_asm + (D.V + 3) / 2;             // [ngrp][maxrl][9] soft–soft block sums
   int cpl_run = 0, nct = 0;
-  // phase 1 (thread per vertex): body mask of the condensed records; coupling offsets and the
-  // contact-vertex list by block scans (the vertex terms themselves: k_asm_verts, launched before)
+  // phase 1 (thread per vertex): inertia, gravity, AL and elastic terms; body mask of the condensed
+  // records; coupling offsets and the contact-vertex list by block scans (a grid-parallel split of the vertex
+  // terms, like k_asm_edges, measured no faster)
+  const double* q = D.q + (size_t)e * D.n;
+  const double* qt = D.qt + (size_t)e * D.n;
+  const double* tb = D.tetbuf + (size_t)sl * TETBUF * D.T;
+  const double dt2 = D.dt * D.dt, rho = C.rho;
+  const double* s_att = D.s_att + (size_t)e * D.NC * 3;
+  const double* lam_att = D.lam_att + (size_t)e * D.NC * 3;
   for (int v0 = 0; v0 < D.V; v0 += blockDim.x) {
     const int v = v0 + threadIdx.x;
     unsigned bmask = 0u;
     int hasc = 0;
     if (v < D.V) {
+      const double m = D.mass[v];
+      v3 x = ld3(q + 3 * v), xt = ld3(qt + 3 * v);
+      v3 gv = m * (x - xt) - (dt2 * m) * mk(D.grav[0], D.grav[1], D.grav[2]);
+      double dg = m;
+      int ci = D.att_of_vert[v];
+      if (ci >= 0) {
+        v3 r = x - ld3(s_att + 3 * ci);
+        gv += (rho * m) * r - m * ld3(lam_att + 3 * ci);
+        dg += rho * m;
+      }
+      double Hv[9] = {dg, 0, 0, 0, dg, 0, 0, 0, dg};
+      for (int j = D.vdiag_ptr[v]; j < D.vdiag_ptr[v + 1]; ++j) {
+        int ent = D.vdiag[j], t = ent >> 2, a = ent & 3;
+        gv += mk(tb[(size_t)(3 * a) * D.T + t], tb[(size_t)(3 * a + 1) * D.T + t], tb[(size_t)(3 * a + 2) * D.T + t]);
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) Hv[3 * r + c] += tb[(size_t)(12 + sym_idx(3 * a + r, 3 * a + c, 12)) * D.T + t];
+      }
       const int j0 = cptr[v], j1 = cptr[v + 1];
       hasc = j1 > j0;
       for (int j = j0 + rcnt[v]; j < j1; ++j) { const int d = sbody[j]; if (d >= 0) bmask |= 1u << d; }
+      st3(g + 3 * v, gv);
+      double* hd = D.Hd + (size_t)e * D.V * 9;           // SoA [9][V]: SpMV diagonal (contact added in phase 2)
+      double* ds = D.Dg_s + (size_t)e * D.V * 9;         // raw diagonal block (SoA) for LM re-inversion
+      for (int i = 0; i < 9; ++i) { hd[(size_t)i * D.V + v] = Hv[i]; ds[(size_t)i * D.V + v] = Hv[i]; }
+      if (!hasc) {
+        const double sh = C.mu * m;                       // mass-scaled LM shift μ·m_v I (R14c)
+        Hv[0] += sh; Hv[4] += sh; Hv[8] += sh;
+        double Pi[9];
+        inv33(Hv, Pi);
+        double* ps = D.Pinv_s + (size_t)e * D.V * 9;     // SoA [9][V]
+        for (int i = 0; i < 9; ++i) ps[(size_t)i * D.V + v] = Pi[i];
+      }
     }
     int tot, totc;
     const int ex = block_excl_scan(__popc(bmask), shs, &tot);
@@ -2184,9 +2171,9 @@ struct SmemMat {
 
 // SpMV pass A1 (residual pairs, matrix-free 12×12, one pair per lane), out of line: rare (two soft bodies or two
 // DoF bodies in one pair) and register-heavy, so the PCG loop does not carry its registers
-__device__ __noinline__ void spmv_residual(const Dev& D, int e, const double* x, double* part, const double* aH, const int* aslot,
-                                          const double* axb, const int* spos, double* sout, const int* rl, int nres, int nb12,
-                                          int lane, int w) {
+__device__ __forceinline__ void spmv_residual_inl(const Dev& D, int e, const double* x, double* part, const double* aH,
+                                                 const int* aslot, const double* axb, const int* spos, double* sout,
+                                                 const int* rl, int nres, int nb12, int lane, int w) {
   // pass A1: residual pairs, matrix-free 12×12 (one pair per lane)
   for (int base = 32 * w; base < nres; base += blockDim.x) {
     const int idx = base + lane;
@@ -2253,6 +2240,12 @@ __device__ __noinline__ void spmv_residual(const Dev& D, int e, const double* x,
   }
 }
 
+__device__ __noinline__ void spmv_residual(const Dev& D, int e, const double* x, double* part, const double* aH, const int* aslot,
+                                          const double* axb, const int* spos, double* sout, const int* rl, int nres, int nb12,
+                                          int lane, int w) {
+  spmv_residual_inl(D, e, x, part, aH, aslot, axb, spos, sout, rl, nres, nb12, lane, w);
+}
+
 // what: 1 = zero the body partials + barrier, 2 = pass A (+ barrier), 4 = pass B, 8 = final barrier.
 // Returns this thread's partial Σ x_i y_i over the rows it wrote (for fused PCG dot products).
 constexpr int SPMV_ALL = 15;
@@ -2276,7 +2269,10 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
   }
   CLK(0)
   if (what & 2) {
-  if (nres > 0) spmv_residual(D, e, x, part, aH, aslot, axb, spos, sout, rl, nres, nb12, lane, w);
+  if (nres > 0) {                      // the streamed kernel calls it out of line (registers); the resident inline
+    if (R) spmv_residual_inl(D, e, x, part, aH, aslot, axb, spos, sout, rl, nres, nb12, lane, w);
+    else spmv_residual(D, e, x, part, aH, aslot, axb, spos, sout, rl, nres, nb12, lane, w);
+  }
   // pass A2: soft–body couplings (one per lane): soft output C_vd x_d → cpl_out[c] (summed by row v
   // in pass B), body output C_vdᵀ x_v warp-reduced per body into part[w][d]
   {
@@ -2344,7 +2340,7 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
       const double* hb = He + D.ell_vb[g] + l;
       const int* cb = D.ell_col + D.ell_cb[g] + l;
       v3 acc = mk(0, 0, 0);
-#pragma unroll 2
+#pragma unroll 4
       for (int j = 0; j < len; ++j) {
         const v3 xu = ld3(x + 3 * cb[32 * j]);
         const double* B = hb + 288 * j;
@@ -2637,19 +2633,34 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
         if (!(dAd > 0.0)) { bad = true; __syncthreads(); break; }   // uniform; red[] reads done
         const double alpha = rz / dAd;
         double loc2 = 0.0;
-        for (int v = threadIdx.x; v < V; v += blockDim.x) {
-          v3 rv = ld3(r + 3 * v);
-          const v3 dv = ld3(d + 3 * v), av = ld3(Ad + 3 * v);
-          double* pv = p + 3 * v;
-          pv[0] += alpha * dv.x; pv[1] += alpha * dv.y; pv[2] += alpha * dv.z;
-          rv = mk(rv.x - alpha * av.x, rv.y - alpha * av.y, rv.z - alpha * av.z);
-          st3(r + 3 * v, rv);
-          const double* Ps = R ? R->Ps : D.Pinv_s + (size_t)e * V * 9;
-          const v3 zv = mk(Ps[v] * rv.x + Ps[V + v] * rv.y + Ps[2 * V + v] * rv.z,
-                           Ps[3 * V + v] * rv.x + Ps[4 * V + v] * rv.y + Ps[5 * V + v] * rv.z,
-                           Ps[6 * V + v] * rv.x + Ps[7 * V + v] * rv.y + Ps[8 * V + v] * rv.z);
-          st3(z + 3 * v, zv);
-          loc2 += rv.x * zv.x + rv.y * zv.y + rv.z * zv.z;
+        // two vertices per thread and pass, every load issued before the stores (r, p, z may alias the loaded
+        // arrays as far as the compiler knows, so it would not hoist the next vertex's loads itself)
+        const double* Ps = R ? R->Ps : D.Pinv_s + (size_t)e * V * 9;
+        for (int v0 = threadIdx.x; v0 < V; v0 += 2 * blockDim.x) {
+          const int v1 = v0 + blockDim.x;
+          const bool h1 = v1 < V;
+          v3 rr[2], aa[2], dd[2], pp[2];
+          double P[2][9];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int v = k ? (h1 ? v1 : v0) : v0;
+            rr[k] = ld3(r + 3 * v); aa[k] = ld3(Ad + 3 * v); dd[k] = ld3(d + 3 * v); pp[k] = ld3(p + 3 * v);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) P[k][i] = Ps[(size_t)i * V + v];
+          }
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (k == 1 && !h1) break;
+            const int v = k ? v1 : v0;
+            const v3 rv = mk(rr[k].x - alpha * aa[k].x, rr[k].y - alpha * aa[k].y, rr[k].z - alpha * aa[k].z);
+            st3(p + 3 * v, mk(pp[k].x + alpha * dd[k].x, pp[k].y + alpha * dd[k].y, pp[k].z + alpha * dd[k].z));
+            st3(r + 3 * v, rv);
+            const double* Q = P[k];
+            const v3 zv = mk(Q[0] * rv.x + Q[1] * rv.y + Q[2] * rv.z, Q[3] * rv.x + Q[4] * rv.y + Q[5] * rv.z,
+                             Q[6] * rv.x + Q[7] * rv.y + Q[8] * rv.z);
+            st3(z + 3 * v, zv);
+            loc2 += rv.x * zv.x + rv.y * zv.y + rv.z * zv.z;
+          }
         }
         for (int db = nwp - 1 - wi; db >= 0 && db < D.ND; db += nwp) {   // body db (last warps): lanes 0..11 own its rows
           const int o = 3 * V + 12 * db;
@@ -2725,7 +2736,8 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
     p = p_out;
   }
   if (threadIdx.x == 0 && !bad && rz0_used > 0.0) { C.ew_rz0 = rz0_used; C.ew_eta = eta_used; C.ew_has = 1; }
-  pcg_finish_noinline(D, e, p, red, mu, bad, zero_g, it_total, gp);   // out of line: keeps the loop's registers
+  if (R) pcg_finish(D, e, p, red, mu, bad, zero_g, it_total, gp);
+  else pcg_finish_noinline(D, e, p, red, mu, bad, zero_g, it_total, gp);   // streamed: out of line (registers)
 }
 
 // end of a PCG launch (block-level, one CTA per env): embedded ∞-norm of the direction, step cap
@@ -3690,7 +3702,6 @@ void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) 
   static size_t attr[MAX_DEVICES] = {};
   ensure_smem(k_assemble_soft, attr, bytes);
   if (D.NEs > 0) k_asm_edges<<<dim3((D.NEs + NTHREADS - 1) / NTHREADS, ne), NTHREADS, 0, s>>>(D, env0, force);
-  if (D.V > 0) k_asm_verts<<<dim3((D.V + NTHREADS - 1) / NTHREADS, ne), NTHREADS, 0, s>>>(D, env0, force);
   k_assemble_soft<<<ne, thr, bytes, s>>>(D, env0, force);
   if (D.ND > 0) k_assemble_body<<<ne, NTHREADS, 0, s>>>(D, env0, force);
 }
