@@ -154,7 +154,8 @@ typedef struct {
   double lm_mu;                  /* LM shift μ of the last solve (hessian_mode 2; 0 = pure Newton) */
   int32_t n_friction;            /* lagged friction pairs of the last step (the active set at its start xⁿ) */
   int32_t capacity_flags;        /* capacity overflows since tac_batch_create (TAC_ENV_CAPACITY): 1 candidates,
-                                    2 large-primitive list of the broad phase, 4 hash entries, 8 active pairs */
+                                    2 large-primitive list of the broad phase, 4 hash entries, 8 active pairs,
+                                    16 residual (matrix-free) pairs, capacity max(64, active_capacity_per_env/4) */
 } tac_env_stats;
 
 struct tac_batch;

@@ -729,7 +729,7 @@ static size_t layout(Carver& C, Dev& D, const HostT& H, int E) {
   D.tbox = C.take<double>(e * (H.NT + H.NE) * 6);
   D.vref = C.take<double>(e * H.NSV * 6 + 1);
   D.act_info = C.take<int>(e * D.act_cap * 4); D.act_vid = C.take<int>(e * D.act_cap * 4);
-  D.act_g = C.take<double>(e * D.act_cap * 12); D.act_H = C.take<double>(e * D.act_cap * PH);
+  D.act_H = C.take<double>(e * D.res_cap * PH);   // residual pairs' 12×12 only (by residual index)
   D.act_out = C.take<double>(1);
   D.spos = C.take<int>(e * 4 * D.act_cap); D.sout = C.take<double>(e * 4 * D.act_cap * 3);
   D.act_slot = C.take<int>(e * 4 * D.act_cap); D.act_xb = C.take<double>(e * 12 * D.act_cap);
@@ -767,6 +767,7 @@ static void fill_dims(Dev& D, const HostT& H, const tac_config* cfg, int E, cons
   D.NCOAT = H.NCOAT; D.NMARK = H.NMARK; D.NAV = (int)H.affv_list.size(); D.NKV = (int)H.kin_vlist.size();
   D.cand_cap = std::max(cfg->cand_capacity_per_env, 64);
   D.act_cap = std::max(cfg->active_capacity_per_env, 16);
+  D.res_cap = std::max(64, D.act_cap / 4);      // residual (matrix-free) pairs: two soft bodies or two DoF bodies
   D.ent_cap = 16 * (H.NT + H.NE) + 4096;
   // every coupling (v, d) owns at least one soft slot of an active pair, and each (v, d) occurs once
   D.cpl_cap = (int)std::max<long long>(1, std::min<long long>((long long)H.V * H.ND, 4LL * D.act_cap));

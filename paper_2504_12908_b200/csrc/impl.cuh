@@ -95,7 +95,7 @@ struct Dev {
   int NNZ;                // off-diagonal soft blocks in row order (2·NEs)
   int maxrl;              // longest soft BSR row (blocks)
   int E, V, T, NA, ND, NVall, NSV, NT, NE, NEs, NC, NK, NB, n, npads, NCOAT, NMARK;
-  int cand_cap, act_cap, ent_cap, cpl_cap;
+  int cand_cap, act_cap, ent_cap, cpl_cap, res_cap;
   // ---- config ----
   double max_step;     // relative step cap (reading R17c)
   double dt, dhat, kappa, tolN, tolAL, eta, armijo, accd_s, rho0, cell;
@@ -199,8 +199,7 @@ struct Dev {
   double* vref;           // [E][NSV][6] reference boxes of surface vertices at the last build
   int* act_info;          // [E][act_cap][4] (kind, type, a, b)
   int* act_vid;           // [E][act_cap][4]
-  double* act_g;          // [E][act_cap][12]
-  double* act_H;          // [E][act_cap][78]
+  double* act_H;          // [E][res_cap][78] packed 12×12 of the residual (matrix-free) pairs, by residual index
   double* act_out;        // [E][act_cap][12] (unused)
   int* act_slot;          // [E][4*act_cap] slot code: soft vertex ≥ 0, DoF body d → −1−d, static → INT_MIN
   double* act_xb;         // [E][4*act_cap][3] rest position x̄ of affine slots

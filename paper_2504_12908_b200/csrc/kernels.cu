@@ -729,16 +729,24 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
   {
     const int* ares = D.act_res + (size_t)e * D.act_cap;
     int* rl = D.res_list + (size_t)e * D.act_cap;
+    int* aresw = D.act_res + (size_t)e * D.act_cap;
     int run = 0;
     for (int t0 = 0; t0 < nact; t0 += blockDim.x) {
       const int k = t0 + threadIdx.x;
-      const int f = k < nact ? ares[k] : 0;
+      const int f = k < nact ? (ares[k] != 0) : 0;
       int tot;
       const int ex = block_excl_scan(f, sh, &tot);
-      if (f) rl[run + ex] = k;
+      __syncthreads();
+      if (f) {
+        rl[run + ex] = k;
+        aresw[k] = run + ex + 1;                  // residual index + 1: the slot of its 12×12 in act_H
+      }
       run += tot;
     }
-    if (threadIdx.x == 0) C.n_res = run;
+    if (threadIdx.x == 0) {
+      C.n_res = run;
+      if (run > D.res_cap) { C.overflow |= 16; C.cap_seen |= 16; }   // residual Hessians (act_H) capacity
+    }
   }
   // soft-vertex contribution lists: count, scan, fill, per-vertex sort (deterministic)
   for (int v = threadIdx.x; v <= D.V; v += blockDim.x) vcnt[v] = 0;
@@ -928,8 +936,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
   const double* P = D.P + (size_t)e * D.NVall * 3;
   const int* info = D.act_info + (size_t)e * D.act_cap * 4;
   const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
-  double* ag = D.act_g + (size_t)e * D.act_cap * 12;
-  double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  double* aH = D.act_H + (size_t)e * D.res_cap * PH;
   PairScratch& S = PS[w];
   const bool project = !C.exact;
   // CTA b takes the pair chunks b, b + gridDim.x, ... (a fixed small grid: empty CTAs cost launch time)
@@ -1037,7 +1044,6 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
     __syncwarp();
     if (lane < 12) {
       const double gfin = scale * (m * B1 * S.gs[lane] + B * m1 * S.gc[lane]);
-      ag[12 * k + lane] = gfin;
       S.gf[lane] = gfin;
     }
     // 3) 12×12 (upper) from the variable blocks
@@ -1070,9 +1076,10 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 3) k_pairs(Dev D, int env0, i
       __syncwarp();
       jacobi12_psd(S.J, lane, 32);
     }
-    const bool res = D.act_res[(size_t)e * D.act_cap + k] != 0;
-    if (res)      // residual pairs stay matrix-free in the SpMV: packed upper 12×12, AoS (coalesced)
-      for (int i = lane; i < PH; i += 32) aH[(size_t)k * PH + i] = S.J.A[12 * c_unpack_r[i] + c_unpack_c[i]];
+    const int ridx = D.act_res[(size_t)e * D.act_cap + k];
+    const bool res = ridx != 0;
+    if (res && ridx <= D.res_cap)   // residual pairs stay matrix-free in the SpMV: packed upper 12×12, AoS
+      for (int i = lane; i < PH; i += 32) aH[(size_t)(ridx - 1) * PH + i] = S.J.A[12 * c_unpack_r[i] + c_unpack_c[i]];
     // 4) condensed records (contact condensation, impl.cuh), read by k_assemble without touching H
     for (int i = lane; i < 144; i += 32) {
       const int r = i / 12, c = i % 12;
@@ -1330,7 +1337,7 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
   const double* P = D.P + (size_t)e * D.NVall * 3;
   const int* info = D.act_info + (size_t)e * D.act_cap * 4;
   const int* avid = D.act_vid + (size_t)e * D.act_cap * 4;
-  double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  double* aH = D.act_H + (size_t)e * D.res_cap * PH;
   const size_t e4 = (size_t)e * 4 * D.act_cap;
   __shared__ double sHy[45][128];                         // H_y of this thread's pair (records phase)
   const int tx = threadIdx.x;
@@ -1505,7 +1512,8 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
     // ---- records (H_y from shared memory) ----
     const int4 c4 = reinterpret_cast<const int4*>(D.act_slot + e4)[k];
     codes[0] = c4.x; codes[1] = c4.y; codes[2] = c4.z; codes[3] = c4.w;
-    res = D.act_res[(size_t)e * D.act_cap + k] != 0;
+    const int ridx = D.act_res[(size_t)e * D.act_cap + k];
+    res = ridx != 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int cd = codes[t];
@@ -1517,8 +1525,8 @@ __global__ void __launch_bounds__(128) k_pairs_x(Dev D, int env0, int force) {
     }
     if (bd1 >= 0 && bd1 < bd0) { const int tmp = bd0; bd0 = bd1; bd1 = tmp; }
     // residual pairs: packed upper slot-space 12×12 for the matrix-free SpMV pass
-    if (res) {
-      double* Hk = aH + (size_t)k * PH;
+    if (res && ridx <= D.res_cap) {
+      double* Hk = aH + (size_t)(ridx - 1) * PH;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
 #pragma unroll
@@ -2197,7 +2205,7 @@ __device__ __forceinline__ void spmv_residual_inl(const Dev& D, int e, const dou
         }
         xl[3 * s] = u.x; xl[3 * s + 1] = u.y; xl[3 * s + 2] = u.z;
       }
-      const double* H = aH + (size_t)k * PH;            // packed upper 12×12 (AoS)
+      const double* H = aH + (size_t)idx * PH;          // packed upper 12×12 (AoS), by residual index
 #pragma unroll
       for (int r = 0; r < 12; ++r) out[r] = 0.0;
 #pragma unroll
@@ -2253,7 +2261,7 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
                        double mu = 0.0, const SmemMat* R = nullptr, int what = SPMV_ALL, int stream_lpr = 4, bool ell = false) {
   const EnvCtl& C = D.ctl[e];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  const double* aH = D.act_H + (size_t)e * D.res_cap * PH;
   const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
   const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
   const int* spos = D.spos + (size_t)e * 4 * D.act_cap;
@@ -2296,7 +2304,9 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
 #pragma unroll
         for (int b = 0; b < 12; ++b) {
           const double xbb = xb[b];
-          const double c0 = cval[(size_t)b * ccap + c], c1 = cval[(size_t)(12 + b) * ccap + c], c2 = cval[(size_t)(24 + b) * ccap + c];
+          const double* cv = cval + (size_t)b * ccap + c;     // coupling blocks: streamed like the soft blocks
+          const double c0 = R ? cv[0] : __ldcs(cv), c1 = R ? cv[12 * ccap] : __ldcs(cv + 12 * ccap),
+                       c2 = R ? cv[24 * ccap] : __ldcs(cv + 24 * ccap);
           so[0] += c0 * xbb; so[1] += c1 * xbb; so[2] += c2 * xbb;
           ob[b] = c0 * xv.x + c1 * xv.y + c2 * xv.z;
         }
@@ -2340,18 +2350,21 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
       const double* hb = He + D.ell_vb[g] + l;
       const int* cb = D.ell_col + D.ell_cb[g] + l;
       v3 acc = mk(0, 0, 0);
+      // the operator is read once per iteration: streaming loads (evict-first), so the per-env vectors, which
+      // every iteration re-reads, keep their L2 lines
 #pragma unroll 4
       for (int j = 0; j < len; ++j) {
         const v3 xu = ld3(x + 3 * cb[32 * j]);
         const double* B = hb + 288 * j;
-        acc += mk(B[0] * xu.x + B[32] * xu.y + B[64] * xu.z, B[96] * xu.x + B[128] * xu.y + B[160] * xu.z,
-                  B[192] * xu.x + B[224] * xu.y + B[256] * xu.z);
+        acc += mk(__ldcs(B) * xu.x + __ldcs(B + 32) * xu.y + __ldcs(B + 64) * xu.z,
+                  __ldcs(B + 96) * xu.x + __ldcs(B + 128) * xu.y + __ldcs(B + 160) * xu.z,
+                  __ldcs(B + 192) * xu.x + __ldcs(B + 224) * xu.y + __ldcs(B + 256) * xu.z);
       }
       const v3 xv = ld3(x + 3 * v);
       const size_t V = D.V;
-      acc += mk(Hd[v] * xv.x + Hd[V + v] * xv.y + Hd[2 * V + v] * xv.z,
-                Hd[3 * V + v] * xv.x + Hd[4 * V + v] * xv.y + Hd[5 * V + v] * xv.z,
-                Hd[6 * V + v] * xv.x + Hd[7 * V + v] * xv.y + Hd[8 * V + v] * xv.z);
+      acc += mk(__ldcs(Hd + v) * xv.x + __ldcs(Hd + V + v) * xv.y + __ldcs(Hd + 2 * V + v) * xv.z,
+                __ldcs(Hd + 3 * V + v) * xv.x + __ldcs(Hd + 4 * V + v) * xv.y + __ldcs(Hd + 5 * V + v) * xv.z,
+                __ldcs(Hd + 6 * V + v) * xv.x + __ldcs(Hd + 7 * V + v) * xv.y + __ldcs(Hd + 8 * V + v) * xv.z);
       for (int j = cptr[v], j1r = cptr[v] + rcnt[v]; j < j1r; ++j) acc += ld3(sout + 3 * j);
       for (int j = cpp[v]; j < cpp[v + 1]; ++j) acc += ld3(cout + 3 * j);
       if (mu != 0.0) acc += (mu * D.mass[v]) * xv;
@@ -2646,7 +2659,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
             const int v = k ? (h1 ? v1 : v0) : v0;
             rr[k] = ld3(r + 3 * v); aa[k] = ld3(Ad + 3 * v); dd[k] = ld3(d + 3 * v); pp[k] = ld3(p + 3 * v);
 #pragma unroll
-            for (int i = 0; i < 9; ++i) P[k][i] = Ps[(size_t)i * V + v];
+            for (int i = 0; i < 9; ++i) P[k][i] = R ? Ps[(size_t)i * V + v] : __ldcs(Ps + (size_t)i * V + v);
           }
 #pragma unroll
           for (int k = 0; k < 2; ++k) {

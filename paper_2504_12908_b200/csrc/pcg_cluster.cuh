@@ -77,7 +77,7 @@ template <int NC>
 __device__ __noinline__ double cl_residual_pairs(const Dev& D, int e, int nres, int rpr, const double* usm, const double* ub,
                                                  double* wpart, double* const* ru) {
   const int lane = threadIdx.x & 31, tid = threadIdx.x, ND = D.ND;
-  const double* aH = D.act_H + (size_t)e * D.act_cap * PH;
+  const double* aH = D.act_H + (size_t)e * D.res_cap * PH;
   const int* aslot = D.act_slot + (size_t)e * 4 * D.act_cap;
   const double* axb = D.act_xb + (size_t)e * 12 * D.act_cap;
   const int* spos = D.spos + (size_t)e * 4 * D.act_cap;
@@ -112,7 +112,7 @@ __device__ __noinline__ double cl_residual_pairs(const Dev& D, int e, int nres, 
         }
         xl[3 * s] = q.x; xl[3 * s + 1] = q.y; xl[3 * s + 2] = q.z;
       }
-      const double* Hk = aH + (size_t)k * PH;
+      const double* Hk = aH + (size_t)idx * PH;
 #pragma unroll
       for (int a = 0; a < 12; ++a)
 #pragma unroll

@@ -11,8 +11,13 @@ iK, iN, iV, iID = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metri
 alg = json.loads(re.search(r"ALG (\{.*\})", open(logf).read()).group(1))
 kname = alg["kernel"].split(" ")[0]
 per = {}
+import re as _re
+def _base(n):    # "void k_pcg<2>(Dev, ...)" -> "k_pcg"
+    n = n.split("(")[0].strip()
+    n = n.split(" ")[-1]
+    return _re.sub(r"<.*>$", "", n)
 for r in rows:
-    if r[iK].split("(")[0].strip() != kname:
+    if _base(r[iK]) != kname:
         continue
     per.setdefault(r[iID], {})[r[iN]] = float(r[iV].replace(",", ""))
 n = len(per)
