@@ -567,9 +567,10 @@ static tac_status build_template(const tac_scene_desc* sc, const tac_config* cfg
   choose_cluster(H);
   // sliced ELL (SELL-32-σ) for the streamed PCG: rows sorted by length (descending, stable), groups of 32
   // consecutive sorted rows padded to the group's longest row; ell_row maps a slot to its vertex; both
-  // blocks of a soft edge are stored (a symmetric upper-only variant with transposed reads of the lower
-  // neighbours was measured slower: the dependent position loads and transposed gathers cost more than the
-  // halved operator bytes, C3 PCG 7.2 -> 7.6 s per 10 steps)
+  // blocks of a soft edge are stored.  Symmetric upper-only variants with transposed reads of the lower
+  // neighbours were measured slower twice: natural row order (C3 PCG 7.2 -> 7.6 s per 10 steps) and a reverse
+  // Cuthill-McKee slot order with window-sorted groups (6.1 -> 12.4 s: the extra loop's registers spill in the
+  // SpMV, and even the two-sided path compiled beside it slowed to 9.9 s)
   {
     const int G = (H.V + 31) / 32;
     std::vector<int> order(H.V);

@@ -209,7 +209,7 @@ struct Dev {
   // BSR pattern and at most one DoF body is folded at assembly into the soft BSR blocks (soft–soft),
   // the body's 12×12 (J_sᵀH_stJ_t), and one 3×12 coupling block C_vd = Σ H_st J_t per (soft vertex v,
   // body d); the remaining "residual" pairs stay matrix-free (12×12 through J) in the SpMV
-  int* act_res;           // [E][act_cap] 1 = residual pair
+  int* act_res;           // [E][act_cap] 0 = condensed pair, else residual index + 1 (its act_H slot)
   int* res_list;          // [E][act_cap] residual pair indices (ascending)
   int* rcnt;              // [E][V] residual slots of v = first rcnt[v] entries of its clist range
   int* cpl_ptr;           // [E][V+1] coupling blocks of soft vertex v (ascending body)

@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
         const int c = b1 - b0;
         for (int i = 0; i < c; ++i) {
           const int key = clist[b0 + i];
-          const int res = ares[key >> 2];
+          const int res = ares[key >> 2] != 0;         // ares holds the residual index + 1 (0: condensed)
           nr += res;
           kk[i] = key | ((res ? 0 : 1) << 30);
         }
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int for
         }
       } else {
         for (int i = b0; i < b1; ++i) {
-          const int res = ares[clist[i] >> 2];
+          const int res = ares[clist[i] >> 2] != 0;
           nr += res;
           clist[i] |= (res ? 0 : 1) << 30;
         }
