@@ -18,11 +18,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 M="--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"
 timeout 900 ncu --profile-from-start off -k regex:"^k_pcg" $M --csv --log-file gpurun_out/f_traffic_c3.csv python tools/pcg_traffic.py C3 4096 5 > gpurun_out/f_traffic_c3.log 2>&1
 timeout 600 ncu --profile-from-start off -k regex:"^k_pcg" $M --csv --log-file gpurun_out/f_traffic_c2.csv python tools/pcg_traffic.py C2 1024 12 > gpurun_out/f_traffic_c2.log 2>&1
+# full-set captures at 1024 envs (C3 x 4096 makes ncu back the device memory up in host memory and fail)
 for K in "^k_pcg:k_pcg:C3" "^k_pcg_r$:k_pcg_r:C2" "^k_assemble_soft$:k_assemble_soft:C3" "^k_asm_edges$:k_asm_edges:C3"; do
   RX=$(echo $K | cut -d: -f1); TAG=$(echo $K | cut -d: -f2); CF=$(echo $K | cut -d: -f3)
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${RX}" --launch-skip 0 --launch-count 1 -o /tmp/f_${TAG}_${CF} -f python bench.py --config $CF --steps 1 --warmup 3 $L > gpurun_out/f_ncu_${TAG}_${CF}.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${RX}" --launch-skip 0 --launch-count 1 -o /tmp/f_${TAG}_${CF} -f python bench.py --config $CF --envs-total 1024 --steps 1 --warmup 3 $L > gpurun_out/f_ncu_${TAG}_${CF}.log 2>&1
   ncu -i /tmp/f_${TAG}_${CF}.ncu-rep --page raw --csv > gpurun_out/f_${TAG}_${CF}_raw.csv 2>/dev/null
 done
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/dbg_r2.py sanity > gpurun_out/f_sanitizer_$tool.log 2>&1
-done
+# compute-sanitizer is closed on this GPU pool (its runs left GPUs needing a reset)
