@@ -2441,7 +2441,7 @@ __device__ double spmv(const Dev& D, int e, const double* x, double* y, double* 
 // block-Jacobi inverses of (diag blocks + μM) — LM retry inside k_pcg (R14c).  The 3×3 soft
 // blocks are thread-parallel; warp 0 inverts the body blocks one by one (warp Cholesky) meanwhile.
 // Outputs: ps [9][V] SoA and pb [ND][144] (global, or the resident shared-memory copies)
-__device__ __noinline__ void reinvert_precond(const Dev& D, int e, double mu, double* ps, double* pb, double* scratch /*smem 144*/,
+__device__ __forceinline__ void reinvert_precond_inl(const Dev& D, int e, double mu, double* ps, double* pb, double* scratch /*smem 144*/,
                                  double* T /*smem 144*/) {
   const double* ds = D.Dg_s + (size_t)e * D.V * 9;
   for (int v = threadIdx.x; v < D.V; v += blockDim.x) {
@@ -2464,6 +2464,10 @@ __device__ __noinline__ void reinvert_precond(const Dev& D, int e, double mu, do
     }
   }
   __syncthreads();
+}
+__device__ __noinline__ void reinvert_precond(const Dev& D, int e, double mu, double* ps, double* pb, double* scratch,
+                                             double* T) {
+  reinvert_precond_inl(D, e, mu, ps, pb, scratch, T);
 }
 
 __device__ void precond(const Dev& D, int e, const double* r, double* z, const SmemMat* R = nullptr) {
@@ -2611,7 +2615,7 @@ __device__ void pcg_body(const Dev& D, int e, int vsm, double* dsmem, double* re
   }
   for (int attempt = 0;; ++attempt) {
     if (attempt > 0) {
-      if (R) reinvert_precond(D, e, mu, Rw_Ps, Rw_Pb, chol_scratch, chol_T);      // resident copies
+      if (R) reinvert_precond_inl(D, e, mu, Rw_Ps, Rw_Pb, chol_scratch, chol_T);  // resident copies (inline)
       else reinvert_precond(D, e, mu, D.Pinv_s + (size_t)e * D.V * 9, D.Pinv_b + (size_t)e * D.ND * 144, chol_scratch, chol_T);
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.0; r[i] = -g[i]; }
