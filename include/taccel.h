@@ -133,7 +133,7 @@ typedef struct {
                                     μ > 0 requires hessian_mode 2 (the friction Hessian is PSD and is not projected) */
   double eps_v;                  /* ε_v (m/s) of the friction transition f1 */
   double pcg_eta_max;            /* relaxed PCG tolerance ("carefully relaxing convergence tolerances";
-                                    DESIGN R22): 0 = the fixed η above; > 0 = per Newton iteration the
+                                    DESIGN R24): 0 = the fixed η above; > 0 = per Newton iteration the
                                     Eisenstat–Walker forcing η_k = 0.9·(r₀ᵀz₀)_k/(r₀ᵀz₀)_{k−1}, safeguarded by
                                     0.9·η_{k−1}² when that exceeds 0.1, clamped to [pcg_eta, pcg_eta_max]; the first
                                     solve of a time step uses pcg_eta_max.  Must be 0 or in [pcg_eta, 1).      */

@@ -90,7 +90,7 @@ def any_inverted(model: Model, x):
 
 
 def forcing_eta(cfg, rz0, hist):
-    """Relaxed PCG tolerance of one Newton iteration (reading R22; "carefully relaxing convergence
+    """Relaxed PCG tolerance of one Newton iteration (reading R24; "carefully relaxing convergence
     tolerances"), Eisenstat–Walker choice 2 with γ = 0.9, α = 2 in the preconditioned gradient norm
     ‖g‖² = r₀ᵀz₀ of the solve:  η_k = γ·r₀ᵀz₀(k) / r₀ᵀz₀(k−1),  safeguard η_k ≥ γ η_{k−1}² when γ η_{k−1}² > 0.1,
     clamped to [pcg_eta, pcg_eta_max];  the first solve of a time step uses pcg_eta_max.  hist holds
@@ -108,7 +108,7 @@ def block_jacobi_pcg(model: Model, H, g, eta, max_iter, info=None):
     """Block-Jacobi PCG for H p = −g from p₀ = 0 (3×3 per soft vertex, 12×12 per body); stop
     at rᵀz ≤ η² r₀ᵀz₀ or max_iter (reading R15; P:L325 names PCG).  Returns (None, it) if a
     search direction with dᵀHd ≤ 0 is met (H not SPD).  eta may be a function of r₀ᵀz₀ (the relaxed
-    tolerance of reading R22); info (a dict) receives the r₀ᵀz₀ and η used."""
+    tolerance of reading R24); info (a dict) receives the r₀ᵀz₀ and η used."""
     n = len(g)
     V = model.V
     blocks = [(3 * v, 3) for v in range(V)] + [(3 * V + 12 * s, 12) for s in range(model.n_dof_bodies)]
@@ -175,7 +175,7 @@ def sweep_factor(cfg, p_inf):
 
 
 def _pcg_eta(cfg, ew):
-    """the PCG tolerance: fixed η (R15), or the relaxed forcing of R22 when pcg_eta_max > 0"""
+    """the PCG tolerance: fixed η (R15), or the relaxed forcing of R24 when pcg_eta_max > 0"""
     if getattr(cfg, "pcg_eta_max", 0.0) > 0.0:
         return lambda rz0: forcing_eta(cfg, rz0, ew.get("hist"))
     return cfg.pcg_eta
@@ -219,7 +219,7 @@ def step(model: Model, st: State, y_kin_target, solver="direct", L_env=None, tra
     nfail = 0         # consecutive failed exact attempts (back-off 2, 4, ... 64)
     mode = cfg.hessian_mode
     mu = 0.0          # mass-scaled Levenberg-Marquardt shift (hessian_mode 2, reading R14c)
-    ew = {}           # relaxed-tolerance history of this step (reading R22): (r₀ᵀz₀, η) of the last accepted solve
+    ew = {}           # relaxed-tolerance history of this step (reading R24): (r₀ᵀz₀, η) of the last accepted solve
     Mreg = mass_matrix(model) if mode == 2 else None
     for al_round in range(cfg.max_al_rounds):
         stats.al_rounds = al_round + 1

@@ -47,7 +47,7 @@ struct EnvCtl {
   int n_fr, fr_frozen;    // lagged friction pairs of this step (appended after the barrier pairs), frozen at xⁿ
   int cap_seen, cap_need; // capacity overflows seen since batch creation (bits: 1 candidates, 2 big-target list,
                           // 4 hash entries, 8 active pairs) and the largest candidate count requested
-  double ew_rz0, ew_eta;  // relaxed PCG tolerance (R22): r₀ᵀz₀ and η of the last accepted solve of this step
+  double ew_rz0, ew_eta;  // relaxed PCG tolerance (R24): r₀ᵀz₀ and η of the last accepted solve of this step
   int ew_has, pad4_;      // 1 once this step has an accepted solve
 };
 
@@ -104,7 +104,7 @@ struct Dev {
   double lm_mu0;
   double bp_margin;         // δ of the reusable candidate list (0 = rebuild every iteration)
   double mu_f, eps_v;       // lagged friction: μ (0 = off) and ε_v
-  double eta_max;           // relaxed PCG tolerance (R22): 0 = fixed η
+  double eta_max;           // relaxed PCG tolerance (R24): 0 = fixed η
   double grav[3];
   // ---- template ----
   const int* tets;        // [T][4]

@@ -2496,7 +2496,7 @@ __device__ void precond(const Dev& D, int e, const double* r, double* z, const S
 // ------------------------------------------------------------------------------------------
 __device__ void pcg_finish(const Dev& D, int e, double* p, double* red, double mu, bool bad, bool zero_g, int it_total,
                            double gp);
-// PCG tolerance of this solve (reading R22): fixed η, or the Eisenstat–Walker forcing from the
+// PCG tolerance of this solve (reading R24): fixed η, or the Eisenstat–Walker forcing from the
 // env's last accepted solve of the step: η = 0.9·r₀ᵀz₀ / (r₀ᵀz₀)_prev, ≥ 0.9·η_prev² when that exceeds 0.1,
 // clamped to [η, η_max]; η_max for the first solve of a step.  Uniform across the block (rz0 is).
 __device__ __forceinline__ double pcg_forcing(const Dev& D, const EnvCtl& C, double rz0) {

@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(CL_MAX_THREADS, 1) k_pcg_cl(const __grid_const
       cl_sum2<NC>(a0, b0, red, rred, 0);
       rz = a0;
     }
-    const double eta_k = pcg_forcing(D, C, rz), stop = eta_k * eta_k * rz;   // R22 (fixed η by default)
+    const double eta_k = pcg_forcing(D, C, rz), stop = eta_k * eta_k * rz;   // R24 (fixed η by default)
     rz0_used = rz; eta_used = eta_k;
     zero_g = rz == 0.0;
     bad = !(rz == rz);

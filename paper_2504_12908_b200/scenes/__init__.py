@@ -92,7 +92,7 @@ class Config:
     bp_margin: float = 1.0e-4      # δ of the reusable candidate list (R11b); 0 = rebuild every iteration
     cand_capacity_per_env: int = 65536
     active_capacity_per_env: int = 4096
-    pcg_eta_max: float = 0.0       # relaxed PCG tolerance (reading R22): 0 = fixed η; > 0 = Eisenstat–Walker forcing in [η, η_max]
+    pcg_eta_max: float = 0.0       # relaxed PCG tolerance (reading R24): 0 = fixed η; > 0 = Eisenstat–Walker forcing in [η, η_max]
     mu_friction: float = 0.0       # Coulomb coefficient μ of the lagged friction D_k; 0 = frictionless
     eps_v: float = 1.0e-3          # ε_v (m/s): static/dynamic friction transition of f1 (S:L244 default)
 

@@ -265,7 +265,7 @@ def test_c2_with_friction_single_steps_from_shared_states():
 
 
 def test_c2_relaxed_pcg_tolerance_single_steps():
-    """Relaxed PCG tolerance (reading R22, "carefully relaxing convergence tolerances"; NEXT 4): C2 ×
+    """Relaxed PCG tolerance (reading R24, "carefully relaxing convergence tolerances"; NEXT 4): C2 ×
     64 envs with the Eisenstat–Walker forcing in [η, 0.1]; the converged steps still agree with the oracle's
     exact Newton solves from shared states at steps 12 and 30 (positions within 1e-6·L_env, active sets
     bit-exact, derivatives 1e-9), and the forcing is live (a different PCG iteration count from the fixed η)."""

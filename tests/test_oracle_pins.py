@@ -965,7 +965,7 @@ def test_depth_map_sphere_cap_closed_form():
 
 
 def test_relaxed_pcg_tolerance_reaches_the_same_step():
-    """Reading R22 ("carefully relaxing convergence tolerances"): the Eisenstat–Walker forcing only
+    """Reading R24 ("carefully relaxing convergence tolerances"): the Eisenstat–Walker forcing only
     changes how accurately each Newton direction is solved, not the minimiser — a C1 press step with the PCG
     solver at η ∈ [1e-4, 0.1] lands on the direct-solve step within 1e-7·L_env (the Newton tolerance), the
     forcing is live (a different PCG iteration count from the fixed η), and the first solve of a step uses

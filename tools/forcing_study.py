@@ -1,4 +1,4 @@
-"""Relaxed PCG tolerance study (reading R22, NEXT 4): oracle steps (PCG solver) from dumped GPU states with
+"""Relaxed PCG tolerance study (reading R24, NEXT 4): oracle steps (PCG solver) from dumped GPU states with
 fixed η and with the Eisenstat–Walker forcing at several η_max; prints Newton / PCG counts and the position
 difference against the fixed-η result (in L_env).
 
