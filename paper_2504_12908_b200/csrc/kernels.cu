@@ -662,7 +662,8 @@ __device__ bool pair_is_residual(const Dev& D, const int* vid) {
   return false;
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2) k_narrow(Dev D, int env0, int force) {
+template <int MINB>
+__global__ void __launch_bounds__(NTHREADS, MINB) k_narrow(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (env_skip(D, e, force)) return;
@@ -3084,7 +3085,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_energy(Dev D, int env0, double 
 }
 
 // backtracking line search from α = min(1, α_ccd); Armijo c
-__global__ void __launch_bounds__(NTHREADS, 2) k_linesearch(Dev D, int env0) {
+template <int MINB>
+__global__ void __launch_bounds__(NTHREADS, MINB) k_linesearch(Dev D, int env0) {
   const int e = env_at(D, env0, blockIdx.x);
   EnvCtl& C = D.ctl[e];
   if (C.phase != PHASE_ACTIVE || C.inner_conv || C.xfail) return;
@@ -3691,7 +3693,10 @@ void launch_broad(const Dev& D, int env0, int ne, int swept, int force, cudaStre
 }
 void launch_narrow(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   size_t smem = (size_t)(2 * D.V + 1) * sizeof(int);
-  k_narrow<<<ne, NTHREADS, smem, s>>>(D, env0, force);
+  // 3 CTAs/SM measured faster than 2 (C3 narrow 280 -> 240 ms / 10 steps); TAC_NARROW_MINB=2 restores 128 registers
+  static const int minb = getenv("TAC_NARROW_MINB") ? atoi(getenv("TAC_NARROW_MINB")) : 3;
+  if (minb == 3) k_narrow<3><<<ne, NTHREADS, smem, s>>>(D, env0, force);
+  else k_narrow<2><<<ne, NTHREADS, smem, s>>>(D, env0, force);
 }
 void launch_tets(const Dev& D, int env0, int ne, int force, cudaStream_t s) {
   dim3 grid((D.T + NTHREADS - 1) / NTHREADS, ne);
@@ -3883,7 +3888,11 @@ void launch_energy(const Dev& D, int env0, int ne, double alpha, cudaStream_t s)
   k_energy<<<ne, NTHREADS, 0, s>>>(D, env0, alpha);
 }
 void launch_linesearch(const Dev& D, int env0, int ne, cudaStream_t s) {
-  k_linesearch<<<ne, NTHREADS, 0, s>>>(D, env0);
+  // 3 CTAs/SM (80 registers, some spills) measured faster than 2 (C3 line search 374 -> 344 ms / 10 steps);
+  // TAC_LS_MINB=2 restores the 128-register budget
+  static const int minb = getenv("TAC_LS_MINB") ? atoi(getenv("TAC_LS_MINB")) : 3;
+  if (minb == 3) k_linesearch<3><<<ne, NTHREADS, 0, s>>>(D, env0);
+  else k_linesearch<2><<<ne, NTHREADS, 0, s>>>(D, env0);
 }
 void launch_control(const Dev& D, int env0, int ne, cudaStream_t s) {
   k_control<<<ne, NTHREADS, 0, s>>>(D, env0);
