@@ -1848,7 +1848,10 @@ __global__ void __launch_bounds__(NTHREADS) k_asm_edges(Dev D, int env0, int for
 // soft part of the assembly (elastic edge and diagonal blocks, gradient, condensed contact terms,
 // 3×3 block-Jacobi inverses); register-light, so it runs at higher occupancy than the body part
 constexpr int ASM_SOFT_MAX = 320;
-__global__ void __launch_bounds__(ASM_SOFT_MAX, 2) k_assemble_soft(Dev D, int env0, int force) {
+// MINB: 3 CTAs/SM (64 registers) for envs that fit one pass of ≤ 320 threads (C2: assemble 135 -> 123 ms / 20
+// steps), 2 otherwise (C3 measured 1.63 -> 2.27 s / 10 steps at 3)
+template <int MINB>
+__global__ void __launch_bounds__(ASM_SOFT_MAX, MINB) k_assemble_soft(Dev D, int env0, int force) {
   const int e = env_at(D, env0, blockIdx.x);
   const int sl = blockIdx.x;                   // slot in the assembly scratch (launch-local, < asm_envs)
   if (env_skip(D, e, force)) return;
@@ -3721,10 +3724,13 @@ void launch_assemble(const Dev& D, int env0, int ne, int force, cudaStream_t s) 
   // threads: one per soft vertex in a single pass when V ≤ 320 (rounded to warps), else 256
   const int thr = D.V <= ASM_SOFT_MAX ? std::max(128, (D.V + 31) / 32 * 32) : NTHREADS;
   const int bytes = ((D.V + 3) / 2) * (int)sizeof(double) + (D.maxrl <= 32 ? (thr / 8) * D.maxrl * 9 * (int)sizeof(double) : 0);
-  static size_t attr[MAX_DEVICES] = {};
-  ensure_smem(k_assemble_soft, attr, bytes);
+  static size_t attr[MAX_DEVICES] = {}, attr3[MAX_DEVICES] = {};
+  const bool small = D.V <= ASM_SOFT_MAX;
+  if (small) ensure_smem(k_assemble_soft<3>, attr3, bytes);
+  else ensure_smem(k_assemble_soft<2>, attr, bytes);
   if (D.NEs > 0) k_asm_edges<<<dim3((D.NEs + NTHREADS - 1) / NTHREADS, ne), NTHREADS, 0, s>>>(D, env0, force);
-  k_assemble_soft<<<ne, thr, bytes, s>>>(D, env0, force);
+  if (small) k_assemble_soft<3><<<ne, thr, bytes, s>>>(D, env0, force);
+  else k_assemble_soft<2><<<ne, thr, bytes, s>>>(D, env0, force);
   if (D.ND > 0) k_assemble_body<<<ne, NTHREADS, 0, s>>>(D, env0, force);
 }
 static size_t spmv_smem(const Dev& D) { return (size_t)(NTHREADS / 32) * D.ND * 12 * sizeof(double) + 8; }
